@@ -1,0 +1,113 @@
+/*
+ * smes.h -- C ABI of the B200-native SMES layer (arXiv 2602.09386) hot path.
+ *
+ * The reference (taskmoe 0.1.0) exposes this path as NumPy functions, not an
+ * FFI; each entry point below replaces one reference function (file:line in
+ * /root/reference/pkg/src/taskmoe) and is what a ctypes / cffi binding of the
+ * reference's module API binds to.
+ *
+ * Conventions
+ *   - plain device pointers + sizes; no torch types; `stream` is a cudaStream_t.
+ *   - functions never allocate; the caller passes outputs and workspaces.
+ *   - every launch is stream-ordered and host-sync free (CUDA-graph capturable);
+ *     data-dependent sizes (N_act, segment offsets) stay on the device.
+ *   - return 0 on success, else an SMES_ERR_* code; smes_last_error() gives the
+ *     message.  Codes map 1:1 to taskmoe.errors (errors.py:4-49).
+ *   - bf16 = __nv_bfloat16 storage, fp32 accumulation.  Deterministic: no
+ *     floating-point atomics, fixed reduction orders.
+ */
+#ifndef SMES_H_
+#define SMES_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMES_ABI_VERSION 1
+
+#define SMES_OK 0
+#define SMES_ERR_SHAPE 1    /* taskmoe.errors.ShapeError    */
+#define SMES_ERR_CONFIG 2   /* taskmoe.errors.ConfigError   */
+#define SMES_ERR_NUMERICS 3 /* taskmoe.errors.NumericsError */
+#define SMES_ERR_STATE 4    /* taskmoe.errors.StateError    */
+#define SMES_ERR_CUDA 5     /* CUDA runtime / driver failure */
+
+const char* smes_last_error(void);
+int smes_abi_version(void);
+
+/* ---- K1 progressive router: replaces route_batch (routing.py:235-281) incl.
+ *      softmax (linalg.py:74-83), _top_k_rows (routing.py:184-187) and
+ *      _renormalized_weights_batch (routing.py:203-211); fuses the per-chunk
+ *      histograms of build_execution_plan (execution.py:109) and
+ *      compute_load_stats (balance.py:65-68).  Stage I in fp64.
+ *      z element (t,b,e) at z[t*stride_t + b*stride_b + e]. */
+int smes_route_rows_per_warp(int B);
+int smes_route_num_chunks(int B, int rows_per_warp);
+int smes_route_batch(const float* z, long stride_t, long stride_b, const double* probs_in,
+                     const double* task_weights, int T, int B, int E, int k_shared, int k_adaptive,
+                     int rows_per_warp, int32_t* shared, int32_t* adaptive, int32_t* active, float* wsel,
+                     uint32_t* umask, int32_t* usize, int32_t* chunk_union, int32_t* chunk_active,
+                     double* chunk_mass, double* chunk_dmass, double* probs_out, int32_t* flag, void* stream);
+
+/* ---- K2 execution plan: replaces build_execution_plan (execution.py:85-123)
+ *      and the gather hidden[plan.gather_instances] (model.py:301).
+ *      Segments are padded to 128 rows (seg_pad); seg_log are the reference's
+ *      segment_offsets.  totals = {N_act, padded rows}. */
+int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
+                     const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
+                     double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
+                     unsigned int* ticket, void* stream);
+int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,
+                      const int32_t* seg_pad, const int32_t* loads, const void* h_bf16, long ldh, void* X_bf16,
+                      long ldx, int32_t* row_of, int umax, int32_t* gather_inst, int32_t* gather_exp,
+                      void* zero_rows2_bf16, long ldz2, int d2, void* stream);
+
+/* ---- K3 grouped GEMM (tcgen05 + TMEM + TMA): replaces grouped_gemm
+ *      (execution.py:126-158) and the expert part of backward (training.py:180-191).
+ *      ragged-M: C[m,n] = act(sum_k A[m,k] W_g[n,k] + bias_g[n])   (b_mn = 0, fwd)
+ *                C[m,n] = mask(sum_k A[m,k] W_g[k,n])              (b_mn = 1, dgrad)
+ *      ragged-K: C_g[i,j] = sum_{m in g} P[m,i] Q[m,j]           (wgrad, fp32 out)
+ *      seg = padded group offsets (device). */
+int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, int G, int N, int K, int b_mn,
+                       const int* seg, const float* bias, int act, uint32_t* relu_bits_out,
+                       const uint32_t* relu_bits_in, long bits_ld, void* C, long ldc, int out_fp32,
+                       long m_limit, void* stream);
+int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
+                       const int* seg, float* C, void* stream);
+
+/* ---- K4 combine + heads + BCE: replaces reconstruct_task_reps (execution.py:161-191),
+ *      _heads (model.py:202-208) and _weighted_bce (training.py:54-57). */
+int smes_combine_grid(int B);
+int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
+                     const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
+                     const float* head_w, const float* head_b, void* reps, float* logits, float* preds,
+                     const float* labels, const float* lam, double* loss_part, int grid, void* stream);
+
+/* ---- K6+K7 heads/combine backward + LB gradient: replaces backward
+ *      (training.py:146-179) and lb_loss_gradient (balance.py:83-99). */
+int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
+                     const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
+                     const float* head_w, const float* preds, const float* labels, const float* lam, float inv_b,
+                     int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, int dense_probs,
+                     const float* z, float* part_dw, float* part_db, int grid, void* stream);
+
+/* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
+int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
+                        float* freq_f32, void* stream);
+int smes_loss_finalize(int nparts, const double* part, double inv_b, double beta, const double* stats_value,
+                       double* out, void* stream);
+
+/* ---- reductions: bias grads (training.py:190), un-permute (training.py:192 + :212),
+ *      per-CTA partials (training.py:151-152). */
+int smes_seg_colsum(const void* M, long ld, long rows_cap, int N, const int32_t* seg, int G, float* part, float* out,
+                    void* stream);
+int smes_unpermute(int B, int d, const int32_t* usize, const int32_t* row_of, int umax, const void* dX, long ldx,
+                   const float* dh_router, float* dh, void* stream);
+int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMES_H_ */

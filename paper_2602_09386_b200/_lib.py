@@ -1,0 +1,89 @@
+"""ctypes binding of the in-tree C-ABI library ``_smes.so`` (include/smes.h).
+
+There is no fallback: if the library or a CUDA device is missing, the product
+path raises.  Status codes map to the reference's exception classes
+(taskmoe/errors.py:4-49).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_smes.so")
+
+P = C.c_void_p
+I = C.c_int
+L = C.c_long
+F = C.c_float
+D = C.c_double
+
+# name -> argtypes (restype is int status unless listed in _RESTYPE)
+SIGNATURES = {
+    "smes_last_error": [],
+    "smes_abi_version": [],
+    "smes_route_rows_per_warp": [I],
+    "smes_route_num_chunks": [I, I],
+    "smes_route_batch": [P, L, L, P, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
+    "smes_plan_reduce": [I, I, P, P, P, P, P, P, P, P, P, P, P, P],
+    "smes_plan_scatter": [I, I, I, I, P, P, P, P, P, L, P, L, P, I, P, P, P, L, I, P],
+    "smes_gemm_ragged_m": [P, L, L, P, I, I, I, I, P, P, I, P, P, L, P, L, I, L, P],
+    "smes_gemm_ragged_k": [P, L, P, L, L, I, I, I, P, P, P],
+    "smes_combine_grid": [I],
+    "smes_combine_fwd": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, P, P, P, P, P, I, P],
+    "smes_combine_bwd": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, P, F, I, P, P, P, F, I, P, P, P, I, P],
+    "smes_stats_finalize": [I, I, D, I, P, P, P, P],
+    "smes_loss_finalize": [I, P, D, D, P, P, P],
+    "smes_seg_colsum": [P, L, L, I, P, I, P, P, P],
+    "smes_unpermute": [I, I, P, P, I, P, L, P, P, P],
+    "smes_part_reduce": [P, I, I, P, P],
+}
+_RESTYPE = {"smes_last_error": C.c_char_p}
+# entry points that return a value rather than a status
+_VALUE_FNS = {"smes_abi_version", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
+              "smes_last_error"}
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    """Load (once) and type the library; raises ImportError if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise ImportError(f"SMES CUDA library not built: {path} (run paper_2602_09386_b200/build.py)")
+        lib = C.CDLL(path)
+        for name, argt in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.argtypes = argt
+            fn.restype = _RESTYPE.get(name, C.c_int)
+        _lib = lib
+    return _lib
+
+
+_CODE_TO_EXC = {
+    1: errors.ShapeError,
+    2: errors.ConfigError,
+    3: errors.NumericsError,
+    4: errors.StateError,
+    5: errors.CudaError,
+}
+
+
+def call(name: str, *args):
+    """Invoke an entry point; raise the mapped exception on a non-zero status."""
+    lib = load()
+    rc = getattr(lib, name)(*args)
+    if name in _VALUE_FNS:
+        return rc
+    if rc != 0:
+        msg = lib.smes_last_error().decode(errors="replace")
+        raise _CODE_TO_EXC.get(rc, errors.TaskMoeError)(msg)
+    return rc
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()

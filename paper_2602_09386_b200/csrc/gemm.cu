@@ -1,0 +1,466 @@
+// Grouped expert GEMM on sm_100a: TMA -> smem (SW128) -> tcgen05.mma (TMEM
+// fp32 accumulators, double-buffered) -> tcgen05.ld epilogue -> smem -> TMA store.
+//
+// Replaces the reference's per-expert segment loop `grouped_gemm`
+// (taskmoe/execution.py:126-158) and the expert part of `backward`
+// (taskmoe/training.py:180-191).  One persistent, warp-specialised kernel
+// template covers the three contractions of the SMES expert stack:
+//
+//   RAGGED_M, B K-major  (fwd):   C[m, n]  = act(sum_k A[m, k] W_g[n, k] + b_g[n])   rows m in group g
+//   RAGGED_M, B MN-major (dgrad): C[m, n]  = mask(sum_k A[m, k] W_g[k, n])
+//   RAGGED_K            (wgrad): C_g[i, j] = sum_{m in g} P[m, i] Q[m, j]            (fp32 out)
+//
+// Packed rows are grouped expert-major and every group is padded to a multiple
+// of 128 rows (pad rows are zero in the operands), so an M-tile never straddles
+// two experts and the wgrad reduction runs in whole 64-row K-blocks.  Group
+// offsets live on the device: no host sync, CUDA-graph capturable.
+//
+// Warp roles (256 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer,
+// w2 TMEM allocator, w4..w7 epilogue (warp q%4 owns TMEM lanes 32q..32q+31).
+#include "ptx.cuh"
+#include "smes_capi.h"
+
+namespace smes {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+enum { MODE_RAGGED_M = 0, MODE_RAGGED_K = 1 };
+
+struct GemmArgs {
+  const int* seg;             // (G+1) padded group offsets in rows (multiples of BM)
+  int G;                      // groups
+  int N;                      // ragged-M: output cols;   ragged-K: J
+  int K;                      // ragged-M: reduction dim; ragged-K: unused
+  int I;                      // ragged-K: output rows per group
+  const float* bias;          // ragged-M fwd: (G, N) or null
+  int act;                    // 0 identity, 1 relu
+  uint32_t* bits_out;         // relu bitmask out: [(N/32)][bits_ld] words, or null
+  const uint32_t* bits_in;    // relu bitmask applied to the output (dgrad), or null
+  int bits_ld;
+  int out_fp32;
+};
+
+template <int BN>
+struct Smem {
+  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kA = BM * BK * 2;        // 16 KB
+  static constexpr int kB = BN * BK * 2;        // 32 / 16 KB
+  static constexpr int kStg = 32 * 128;         // 4 KB per staging buffer
+  static constexpr int kOffB = kStages * kA;
+  static constexpr int kOffStg = kOffB + kStages * kB;
+  static constexpr int kOffBar = kOffStg + 4 * 2 * kStg;
+  static constexpr int kOffSeg = kOffBar + 256;
+  static constexpr int kBytes = kOffSeg + 257 * 4 + 12 + 1024;   // + barriers + group table + alignment slack
+  static constexpr int kTmemCols = 2 * BN;
+};
+
+__device__ __forceinline__ int find_group(const int* seg_s, int G, int row) {
+  // largest g with seg[g] <= row  (segments are padded, so row lies inside a non-empty one)
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (seg_s[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+template <int BN, int MODE, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  using S = Smem<BN>;
+  constexpr int kStages = S::kStages;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::kOffB;
+  uint8_t* sStg = smem + S::kOffStg;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  for (int i = threadIdx.x; i <= args.G; i += blockDim.x) seg_s[i] = args.seg[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmC);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, S::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  // ---- tile space
+  int num_tiles, n_tiles = 0, i_tiles = 0, j_tiles = 0;
+  if (MODE == MODE_RAGGED_M) {
+    n_tiles = (args.N + BN - 1) / BN;
+    num_tiles = (seg_s[args.G] / BM) * n_tiles;
+  } else {
+    i_tiles = (args.I + BM - 1) / BM;
+    j_tiles = (args.N + BN - 1) / BN;
+    num_tiles = args.G * i_tiles * j_tiles;
+  }
+  // decode: (group, row0 of A / i0, n0 / j0, k-block range)
+  auto decode = [&](int tile, int& g, int& r0, int& c0, int& kb0, int& nkb) {
+    if (MODE == MODE_RAGGED_M) {
+      int mt = tile / n_tiles;
+      r0 = mt * BM;
+      c0 = (tile - mt * n_tiles) * BN;
+      g = find_group(seg_s, args.G, r0);
+      kb0 = 0;
+      nkb = (args.K + BK - 1) / BK;
+    } else {
+      int per = i_tiles * j_tiles;
+      g = tile / per;
+      int r = tile - g * per;
+      r0 = (r / j_tiles) * BM;
+      c0 = (r % j_tiles) * BN;
+      kb0 = seg_s[g] / BK;
+      nkb = (seg_s[g + 1] - seg_s[g]) / BK;
+    }
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int g, r0, c0, kb0, nkb;
+        decode(tile, g, r0, c0, kb0, nkb);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], S::kA + S::kB);
+          uint8_t* a = sA + stage * S::kA;
+          uint8_t* b = sB + stage * S::kB;
+          const int k0 = (kb0 + kb) * BK;
+          if (MODE == MODE_RAGGED_M) {
+            tma_load_2d(a, &tmA, &full[stage], k0, r0);                       // box {64 k, 128 rows}
+            if (!B_MN) {
+              tma_load_3d(b, &tmB, &full[stage], k0, c0, g);                  // box {64 k, BN n, 1}
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)                               // box {64 n, 64 k, 1}
+                tma_load_3d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0, g);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, k0);
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer (single thread)
+      constexpr bool A_MN = (MODE == MODE_RAGGED_K);
+      constexpr bool BMN = (MODE == MODE_RAGGED_K) || B_MN;
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        int g, r0, c0, kb0, nkb;
+        decode(tile, g, r0, c0, kb0, nkb);
+        const int acc = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * S::kA);
+          const uint32_t b_addr = smem_u32(sB + stage * S::kB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            uint64_t ad = A_MN ? umma_desc_sw128(a_addr + k * 2048, 8192, 1024)
+                               : umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            uint64_t bd = BMN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                              : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            tc_mma_f16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);        // smem slot free once these MMAs have read it
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[acc]);            // accumulator ready (also fires for nkb == 0)
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue: TMEM -> regs -> (bias, act, mask) -> smem (SW128) -> TMA store
+    const int q = warp & 3;
+    uint8_t* stg0 = sStg + q * 2 * S::kStg;
+    int it = 0, nst = 0;
+    constexpr int kColsPerChunkBf = 64, kColsPerChunkF = 32;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      int g, r0, c0, kb0, nkb;
+      decode(tile, g, r0, c0, kb0, nkb);
+      const int acc = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], aphase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
+      const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
+      const int ncols = MODE == MODE_RAGGED_M ? args.N : args.N;
+      const bool fp32out = args.out_fp32 != 0;
+      const int cpc = fp32out ? kColsPerChunkF : kColsPerChunkBf;
+      for (int cc = 0; cc < BN / cpc; ++cc) {
+        const int n = c0 + cc * cpc;
+        if (n >= ncols) break;
+        uint32_t v[64];
+        {
+          uint32_t t0[32];
+          tmem_ld32(tbase + cc * cpc, t0);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = t0[j];
+          if (!fp32out) {
+            uint32_t t1[32];
+            tmem_ld32(tbase + cc * cpc + 32, t1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[32 + j] = t1[j];
+          } else {
+            tmem_ld_wait();
+          }
+        }
+        float f[64];
+        const int nv = fp32out ? 32 : 64;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) f[j] = (j < nv && nkb > 0) ? __uint_as_float(v[j]) : 0.f;
+        if (MODE == MODE_RAGGED_M) {
+          if (args.bias != nullptr) {
+            const float* bp = args.bias + (size_t)g * args.N + n;
+#pragma unroll
+            for (int j = 0; j < 64; j += 4) {
+              if (j < nv && n + j < ncols) {
+                float4 bb = __ldg(reinterpret_cast<const float4*>(bp + j));
+                f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+              }
+            }
+          }
+          if (args.act == 1) {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) f[j] = fmaxf(f[j], 0.f);
+          }
+          if (args.bits_out != nullptr) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (h * 32 < nv && n + h * 32 < ncols) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
+                args.bits_out[(size_t)((n >> 5) + h) * args.bits_ld + row] = w;
+              }
+            }
+          }
+          if (args.bits_in != nullptr) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (h * 32 < nv && n + h * 32 < ncols) {
+                uint32_t w = __ldg(&args.bits_in[(size_t)((n >> 5) + h) * args.bits_ld + row]);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) f[h * 32 + j] = ((w >> j) & 1u) ? f[h * 32 + j] : 0.f;
+              }
+            }
+          }
+        }
+        // stage into smem (128 B per row, 128B swizzle) and TMA-store a {cpc x 32} box
+        uint8_t* stg = stg0 + (nst & 1) * S::kStg;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 pk;
+          if (fp32out) {
+            pk = make_uint4(__float_as_uint(f[4 * c]), __float_as_uint(f[4 * c + 1]), __float_as_uint(f[4 * c + 2]),
+                            __float_as_uint(f[4 * c + 3]));
+          } else {
+            pk = make_uint4(pack_bf16(f[8 * c], f[8 * c + 1]), pack_bf16(f[8 * c + 2], f[8 * c + 3]),
+                            pack_bf16(f[8 * c + 4], f[8 * c + 5]), pack_bf16(f[8 * c + 6], f[8 * c + 7]));
+          }
+          rowp[c ^ (lane & 7)] = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (MODE == MODE_RAGGED_M) tma_store_2d(&tmC, stg, n, r0 + 32 * q);
+          else tma_store_3d(&tmC, stg, n, r0 + 32 * q, g);
+          bulk_commit();
+        }
+        ++nst;
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, S::kTmemCols);
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// rank-2/3 tensor map; dims innermost first; strides (bytes) for dims 1..rank-1
+static int make_map(CUtensorMap* m, CUtensorMapDataType dt, int rank, const void* ptr, const uint64_t* dims,
+                    const uint64_t* strides_bytes, const uint32_t* box) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return set_error(SMES_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], e[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = enc(m, dt, rank, const_cast<void*>(ptr), d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SMES_ERR_CUDA, "cuTensorMapEncodeTiled failed (code %d)", (int)r);
+  return SMES_OK;
+}
+
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <int BN, int MODE, bool B_MN>
+static int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& args,
+                  cudaStream_t st) {
+  auto kern = grouped_gemm_kernel<BN, MODE, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::kBytes);
+    if (ea != cudaSuccess)
+      return set_error(SMES_ERR_CUDA, "grouped_gemm smem attribute (%d B): %s", Smem<BN>::kBytes, cudaGetErrorString(ea));
+    attr = true;
+  }
+  kern<<<num_sms(), kThreads, Smem<BN>::kBytes, st>>>(a, b, c, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "grouped_gemm launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+}  // namespace smes
+
+using namespace smes;
+
+extern "C" {
+
+int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, int G, int N, int K, int b_mn,
+                       const int* seg, const float* bias, int act, uint32_t* bits_out, const uint32_t* bits_in,
+                       long bits_ld, void* C, long ldc, int out_fp32, long m_limit, void* stream) {
+  if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
+  if (N <= 0 || K <= 0 || rows_cap <= 0) return set_error(SMES_ERR_SHAPE, "empty GEMM N=%d K=%d", N, K);
+  if ((lda * 2) % 16 || (ldc * (out_fp32 ? 4 : 2)) % 16 || (K * 2) % 16 || (N * 2) % 16)
+    return set_error(SMES_ERR_SHAPE, "GEMM strides must be 16-byte aligned (lda=%ld ldc=%ld K=%d N=%d)", lda, ldc,
+                     K, N);
+  if ((bits_out || bits_in) && (N % 32))
+    return set_error(SMES_ERR_SHAPE, "relu bitmask needs N %% 32 == 0 (N=%d)", N);
+  CUtensorMap ta, tb, tc;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows_cap}, str[1] = {(uint64_t)lda * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, A, dims, str, box))) return rc;
+  }
+  if (!b_mn) {  // W (G, N, K) K-major
+    uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)G};
+    uint64_t str[2] = {(uint64_t)K * 2, (uint64_t)N * K * 2};
+    uint32_t box[3] = {64, (uint32_t)(N >= 256 ? 256 : 128), 1};
+    if (N >= 256) box[1] = 256;
+    if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, W, dims, str, box))) return rc;
+  } else {      // W (G, K, N): element (n, k) at W[g][k][n]
+    uint64_t dims[3] = {(uint64_t)N, (uint64_t)K, (uint64_t)G};
+    uint64_t str[2] = {(uint64_t)N * 2, (uint64_t)N * K * 2};
+    uint32_t box[3] = {64, 64, 1};
+    if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, W, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)N, (uint64_t)m_limit}, str[1] = {(uint64_t)ldc * (out_fp32 ? 4 : 2)};
+    uint32_t box[2] = {(uint32_t)(out_fp32 ? 32 : 64), 32};
+    if ((rc = make_map(&tc, out_fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, C, dims,
+                       str, box)))
+      return rc;
+  }
+  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, out_fp32};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool wide = N >= 256;
+  if (wide) {
+    // K-major B box is {64, 256}: requires BN == 256
+    return b_mn ? launch<256, MODE_RAGGED_M, true>(ta, tb, tc, args, st)
+                : launch<256, MODE_RAGGED_M, false>(ta, tb, tc, args, st);
+  }
+  return b_mn ? launch<128, MODE_RAGGED_M, true>(ta, tb, tc, args, st)
+              : launch<128, MODE_RAGGED_M, false>(ta, tb, tc, args, st);
+}
+
+int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
+                       const int* seg, float* C, void* stream) {
+  if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
+  if (I <= 0 || J <= 0) return set_error(SMES_ERR_SHAPE, "empty wgrad I=%d J=%d", I, J);
+  if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16 || (I * 2) % 16 || (J * 2) % 16)
+    return set_error(SMES_ERR_SHAPE, "wgrad strides must be 16-byte aligned");
+  CUtensorMap ta, tb, tc;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)I, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldp * 2};
+    uint32_t box[2] = {64, 64};
+    if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, P, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)J, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
+    uint32_t box[2] = {64, 64};
+    if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Q, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)J, (uint64_t)I, (uint64_t)G};
+    uint64_t str[2] = {(uint64_t)J * 4, (uint64_t)I * J * 4};
+    uint32_t box[3] = {32, 32, 1};
+    if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, str, box))) return rc;
+  }
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, 1};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (J >= 256) return launch<256, MODE_RAGGED_K, true>(ta, tb, tc, args, st);
+  return launch<128, MODE_RAGGED_K, true>(ta, tb, tc, args, st);
+}
+
+}  // extern "C"

@@ -1,0 +1,255 @@
+// K2 -- execution plan: per-expert loads + stable counting sort + gather.
+//
+// Restates `build_execution_plan` (taskmoe/execution.py:85-123) and the gather
+// `hidden[plan.gather_instances]` (taskmoe/model.py:301) on the device:
+//   loads[e]  = #instances whose union holds e           (execution.py:109, bincount)
+//   order     = expert-major, instance-ascending          (execution.py:110, lexsort((b, e)))
+//   offsets   = exclusive prefix of loads                 (execution.py:113)
+// The router already produced per-chunk union histograms, so the sort is a
+// two-level counting sort: chunk_reduce scans each expert's column of chunk
+// counts (chunk base), scatter then ranks rows inside a chunk with per-warp
+// counts + in-order walks.  The result is bit-identical to lexsort.
+// Physical layout: each expert segment is padded to a multiple of 128 rows
+// (zero rows) so GEMM tiles never straddle experts; logical offsets are kept
+// alongside for the reference-facing ExecutionPlan view.
+#include "ptx.cuh"
+#include "smes_capi.h"
+
+namespace smes {
+
+constexpr int PL_WARPS = 4;       // must match the router's RT_WARPS
+constexpr int SEG_ALIGN = 128;
+
+// grid = E blocks: column scans of the (C, E) chunk tables.  The last block to
+// finish derives the padded / logical segment offsets (ticket counter, reset
+// in-kernel so the kernel is CUDA-graph replayable).
+__global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ chunk_union,
+                                    const int32_t* __restrict__ chunk_active, const double* __restrict__ chunk_mass,
+                                    const double* __restrict__ chunk_dmass, int32_t* __restrict__ chunk_base,
+                                    int32_t* __restrict__ loads, double* __restrict__ stats_raw,
+                                    int32_t* __restrict__ seg_pad, int32_t* __restrict__ seg_log,
+                                    int32_t* __restrict__ totals, unsigned int* __restrict__ ticket) {
+  const int e = blockIdx.x;
+  __shared__ int32_t warp_tot[32];
+  __shared__ double red[3][32];
+  __shared__ bool is_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int32_t carry = 0;
+  double s_act = 0.0, s_m = 0.0, s_dm = 0.0;
+  // stats sums in fixed per-thread strided order, then fixed tree
+  for (int c = tid; c < C; c += blockDim.x) {
+    s_act += (double)chunk_active[(long)c * E + e];
+    s_m += chunk_mass[(long)c * E + e];
+    s_dm += chunk_dmass[(long)c * E + e];
+  }
+  // exclusive scan of chunk_union[:, e] in tiles of blockDim
+  for (int c0 = 0; c0 < C; c0 += blockDim.x) {
+    int c = c0 + tid;
+    int v = c < C ? chunk_union[(long)c * E + e] : 0;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      int w = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      warp_tot[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    int excl = x - v + (warp > 0 ? warp_tot[warp - 1] : 0) + carry;
+    if (c < C) chunk_base[(long)c * E + e] = excl;
+    carry += warp_tot[nw - 1];
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s_act += __shfl_xor_sync(0xffffffffu, s_act, o);
+    s_m += __shfl_xor_sync(0xffffffffu, s_m, o);
+    s_dm += __shfl_xor_sync(0xffffffffu, s_dm, o);
+  }
+  if (lane == 0) { red[0][warp] = s_act; red[1][warp] = s_m; red[2][warp] = s_dm; }
+  __syncthreads();
+  if (tid == 0) {
+    double a = 0, m = 0, dm = 0;
+    for (int w = 0; w < nw; ++w) { a += red[0][w]; m += red[1][w]; dm += red[2][w]; }
+    loads[e] = carry;
+    stats_raw[e] = a;            // active counts (as fp64, all-reduce friendly)
+    stats_raw[E + e] = m;        // sparse mass sum
+    stats_raw[2 * E + e] = dm;   // dense mass sum
+    __threadfence();
+    unsigned int t = atomicAdd(ticket, 1u);
+    is_last = (t == (unsigned)(gridDim.x - 1));
+  }
+  __syncthreads();
+  if (is_last && tid == 0) {
+    __threadfence();
+    int p = 0, l = 0;
+    for (int i = 0; i < E; ++i) {
+      int ld = ((volatile int32_t*)loads)[i];
+      seg_pad[i] = p;
+      seg_log[i] = l;
+      p += (ld + SEG_ALIGN - 1) / SEG_ALIGN * SEG_ALIGN;
+      l += ld;
+    }
+    seg_pad[E] = p;
+    seg_log[E] = l;
+    totals[0] = l;   // N_act (logical rows)
+    totals[1] = p;   // physical rows incl. padding
+    *ticket = 0u;
+  }
+}
+
+// grid = C + E blocks.  Blocks < C: stable scatter of chunk c's (instance, expert)
+// pairs + vectorised gather of hidden rows.  Blocks >= C: zero the pad rows of
+// expert (blockIdx - C) in X (and optionally in the d_packed buffer).
+template <int EPL, int VEC>
+__global__ void __launch_bounds__(PL_WARPS * 32)
+    scatter_kernel(int B, int E, int d, int rows_per_warp, const uint32_t* __restrict__ umask,
+                   const int32_t* __restrict__ chunk_base, const int32_t* __restrict__ seg_pad,
+                   const int32_t* __restrict__ loads, const __nv_bfloat16* __restrict__ h, long ldh,
+                   __nv_bfloat16* __restrict__ X, long ldx, int32_t* __restrict__ row_of, int umax,
+                   int32_t* __restrict__ gather_inst, int32_t* __restrict__ gather_exp,
+                   __nv_bfloat16* __restrict__ zero_rows2, long ldz2, int d2) {
+  const int C = (B + PL_WARPS * rows_per_warp - 1) / (PL_WARPS * rows_per_warp);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int EW = (E + 31) >> 5;
+  if ((int)blockIdx.x >= C) {
+    // ---- pad fill for expert e
+    const int e = blockIdx.x - C;
+    const int lo = seg_pad[e] + loads[e], hi = seg_pad[e + 1];
+    const uint4 z4 = make_uint4(0, 0, 0, 0);
+    for (int r = lo + warp; r < hi; r += PL_WARPS) {
+      for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(X + (long)r * ldx + c) = z4;
+      if (zero_rows2 != nullptr)
+        for (int c = lane * 8; c < d2; c += 256) *reinterpret_cast<uint4*>(zero_rows2 + (long)r * ldz2 + c) = z4;
+      if (lane == 0) { gather_inst[r] = -1; gather_exp[r] = e; }
+    }
+    return;
+  }
+  __shared__ int32_t s_cnt[PL_WARPS][1024];
+  const int c = blockIdx.x;
+  const int row0 = c * PL_WARPS * rows_per_warp + warp * rows_per_warp;
+  const int rend = min(row0 + rows_per_warp, B);
+  // phase 1: per-warp counts of union membership (lane owns experts lane + 32 j)
+  int cnt[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) cnt[j] = 0;
+  for (int b = row0; b < rend; ++b) {
+#pragma unroll
+    for (int j = 0; j < EPL; ++j)
+      if (j < EW) cnt[j] += (__ldg(&umask[(long)b * EW + j]) >> lane) & 1u;
+  }
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    int e = lane + 32 * j;
+    if (e < E) s_cnt[warp][e] = cnt[j];
+  }
+  __syncthreads();
+  // phase 2: running row index per owned expert = seg_pad + chunk_base + earlier warps
+  int run[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    int e = lane + 32 * j;
+    if (e < E) {
+      int base = __ldg(&seg_pad[e]) + __ldg(&chunk_base[(long)c * E + e]);
+      for (int w = 0; w < warp; ++w) base += s_cnt[w][e];
+      run[j] = base;
+    } else {
+      run[j] = 0;
+    }
+  }
+  // phase 3: in-order walk; each row's copies land at consecutive positions per expert
+  for (int b = row0; b < rend; ++b) {
+    uint4 hv[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      int col = (v * 32 + lane) * 8;
+      hv[v] = col < d ? __ldg(reinterpret_cast<const uint4*>(h + (long)b * ldh + col)) : make_uint4(0, 0, 0, 0);
+    }
+    int u = 0;
+    for (int j = 0; j < EW; ++j) {
+      uint32_t word = __ldg(&umask[(long)b * EW + j]);
+      int my_r = 0;
+#pragma unroll
+      for (int jj = 0; jj < EPL; ++jj)
+        if (jj == j) my_r = run[jj];
+      if ((word >> lane) & 1u) {
+#pragma unroll
+        for (int jj = 0; jj < EPL; ++jj)
+          if (jj == j) run[jj]++;
+      }
+      while (word) {
+        int bit = __ffs(word) - 1;
+        word &= word - 1;
+        int r = __shfl_sync(0xffffffffu, my_r, bit);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          int col = (v * 32 + lane) * 8;
+          if (col < d) *reinterpret_cast<uint4*>(X + (long)r * ldx + col) = hv[v];
+        }
+        if (lane == 0) {
+          row_of[(long)b * umax + u] = r;
+          gather_inst[r] = b;
+          gather_exp[r] = j * 32 + bit;
+        }
+        ++u;
+      }
+    }
+  }
+}
+
+}  // namespace smes
+
+using namespace smes;
+
+extern "C" {
+
+int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active, const double* chunk_mass,
+                     const double* chunk_dmass, int32_t* chunk_base, int32_t* loads, double* stats_raw,
+                     int32_t* seg_pad, int32_t* seg_log, int32_t* totals, unsigned int* ticket, void* stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
+                                         stats_raw, seg_pad, seg_log, totals, ticket);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,
+                      const int32_t* seg_pad, const int32_t* loads, const void* h, long ldh, void* X, long ldx,
+                      int32_t* row_of, int umax, int32_t* gather_inst, int32_t* gather_exp, void* zero_rows2,
+                      long ldz2, int d2, void* stream) {
+  if (E > 1024) return set_error(SMES_ERR_SHAPE, "plan: E=%d exceeds 1024", E);
+  if (d % 8 || d > 2048 || (zero_rows2 && d2 % 8))
+    return set_error(SMES_ERR_SHAPE, "plan: d=%d must be a multiple of 8 and <= 2048", d);
+  const int C = (B + PL_WARPS * rows_per_warp - 1) / (PL_WARPS * rows_per_warp);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int epl = (E + 31) / 32;
+  const int vec = (d + 255) / 256;
+  dim3 grid(C + E);
+  auto* hh = reinterpret_cast<const __nv_bfloat16*>(h);
+  auto* xx = reinterpret_cast<__nv_bfloat16*>(X);
+  auto* zz = reinterpret_cast<__nv_bfloat16*>(zero_rows2);
+#define PL_CASE(EP, VV)                                                                                       \
+  if (epl <= EP && vec <= VV) {                                                                               \
+    scatter_kernel<EP, VV><<<grid, PL_WARPS * 32, 0, st>>>(B, E, d, rows_per_warp, umask, chunk_base, seg_pad, \
+                                                           loads, hh, ldh, xx, ldx, row_of, umax, gather_inst, \
+                                                           gather_exp, zz, ldz2, d2);                          \
+  } else
+  PL_CASE(1, 1) PL_CASE(1, 2) PL_CASE(1, 4) PL_CASE(1, 8) PL_CASE(2, 1) PL_CASE(2, 2) PL_CASE(2, 4) PL_CASE(2, 8)
+  PL_CASE(8, 1) PL_CASE(8, 2) PL_CASE(8, 4) PL_CASE(8, 8) PL_CASE(32, 2) PL_CASE(32, 4) PL_CASE(32, 8) {}
+#undef PL_CASE
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_scatter launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,202 @@
+// K5 / K9 / bias grads -- deterministic reductions (fixed order, no float atomics).
+//
+//   stats_finalize : LoadStats from the (possibly all-reduced) per-expert sums
+//                    (taskmoe/balance.py:62-70): f = counts/(B T), p = mass/(B T),
+//                    L_lb = (E/K) <f, p>
+//   loss_finalize  : task loss (training.py:57) and total (training.py:90-94)
+//   seg_colsum     : per-expert bias gradients db_e = sum_{rows in e} d_pre (training.py:190)
+//   unpermute      : d_hidden[b] = d_router[b] + sum_u dX[row(b,u)] (training.py:192, :212)
+//   part_reduce    : per-CTA partials -> one vector (head grads, training.py:151-152)
+#include "ptx.cuh"
+#include "smes_capi.h"
+
+namespace smes {
+
+__global__ void stats_finalize_kernel(int E, int K, double bt, int dense, const double* __restrict__ raw,
+                                      double* __restrict__ out, float* __restrict__ freq_f32) {
+  // out: [freq E][mass E][counts E][value]
+  __shared__ double red[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double part = 0.0;
+  for (int e = tid; e < E; e += blockDim.x) {
+    const double f = raw[e] / bt;
+    const double m = (dense ? raw[2 * E + e] : raw[E + e]) / bt;
+    out[e] = f;
+    out[E + e] = m;
+    out[2 * E + e] = raw[e];
+    freq_f32[e] = (float)f;
+    part += f * m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[warp] = part;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    out[3 * E] = ((double)E / (double)K) * s;
+  }
+}
+
+__global__ void loss_finalize_kernel(int n, const double* __restrict__ part, double inv_b, double beta,
+                                     const double* __restrict__ stats_value, double* __restrict__ out) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    const double task = s * inv_b;
+    const double lb = stats_value ? *stats_value : 0.0;
+    out[0] = task;
+    out[1] = lb;
+    out[2] = task + beta * lb;
+  }
+}
+
+// stage 1: one block per 128-row tile (tiles never straddle groups); thread = 8 columns
+__global__ void seg_colsum_tiles_kernel(const __nv_bfloat16* __restrict__ M, long ld, int N,
+                                        const int32_t* __restrict__ seg, int G, float* __restrict__ part) {
+  const int tile = blockIdx.x;
+  if (tile * 128 >= seg[G]) return;
+  for (int c = threadIdx.x * 8; c < N; c += blockDim.x * 8) {
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const __nv_bfloat16* p = M + (long)tile * 128 * ld + c;
+    for (int r = 0; r < 128; ++r) {
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(p + (long)r * ld));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { float2 f = __bfloat1622float2(h[i]); s[2 * i] += f.x; s[2 * i + 1] += f.y; }
+    }
+    float* o = part + (long)tile * N + c;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = s[i];
+  }
+}
+
+// stage 2: out[g][n] = sum of the group's tile partials in tile order
+__global__ void seg_colsum_groups_kernel(const float* __restrict__ part, int N, const int32_t* __restrict__ seg,
+                                         float* __restrict__ out) {
+  const int g = blockIdx.y;
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const int t0 = seg[g] / 128, t1 = seg[g + 1] / 128;
+  float s = 0.f;
+  for (int t = t0; t < t1; ++t) s += part[(long)t * N + n];
+  out[(long)g * N + n] = s;
+}
+
+template <int VEC>
+__global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize, const int32_t* __restrict__ row_of,
+                                 int umax, const __nv_bfloat16* __restrict__ dX, long ldx,
+                                 const float* __restrict__ dh_router, float* __restrict__ dh) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const int b = warp;
+  float acc[VEC][8];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    const int c = (v * 32 + lane) * 8;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[v][i] = 0.f;
+    if (dh_router && c < d) {
+      float4 x0 = __ldg(reinterpret_cast<const float4*>(dh_router + (long)b * d + c));
+      float4 x1 = __ldg(reinterpret_cast<const float4*>(dh_router + (long)b * d + c + 4));
+      acc[v][0] = x0.x; acc[v][1] = x0.y; acc[v][2] = x0.z; acc[v][3] = x0.w;
+      acc[v][4] = x1.x; acc[v][5] = x1.y; acc[v][6] = x1.z; acc[v][7] = x1.w;
+    }
+  }
+  const int U = usize[b];
+  for (int u = 0; u < U; ++u) {
+    const long r = row_of[(long)b * umax + u];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+      const int c = (v * 32 + lane) * 8;
+      if (c < d) {
+        uint4 q = __ldg(reinterpret_cast<const uint4*>(dX + r * ldx + c));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          float2 f = __bfloat1622float2(h[i]);
+          acc[v][2 * i] += f.x;
+          acc[v][2 * i + 1] += f.y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    const int c = (v * 32 + lane) * 8;
+    if (c < d) {
+      *reinterpret_cast<float4*>(dh + (long)b * d + c) = make_float4(acc[v][0], acc[v][1], acc[v][2], acc[v][3]);
+      *reinterpret_cast<float4*>(dh + (long)b * d + c + 4) = make_float4(acc[v][4], acc[v][5], acc[v][6], acc[v][7]);
+    }
+  }
+}
+
+__global__ void part_reduce_kernel(const float* __restrict__ part, int nparts, int n, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float s = 0.f;
+  for (int p = 0; p < nparts; ++p) s += part[(long)p * n + i];
+  out[i] = s;
+}
+
+}  // namespace smes
+
+using namespace smes;
+
+static int launch_check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+extern "C" {
+
+int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
+                        float* freq_f32, void* stream) {
+  stats_finalize_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, K, batch_times_tasks, dense, raw,
+                                                                               out, freq_f32);
+  return launch_check("stats_finalize");
+}
+
+int smes_loss_finalize(int nparts, const double* part, double inv_b, double beta, const double* stats_value,
+                       double* out, void* stream) {
+  loss_finalize_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(nparts, part, inv_b, beta, stats_value,
+                                                                            out);
+  return launch_check("loss_finalize");
+}
+
+int smes_seg_colsum(const void* M, long ld, long rows_cap, int N, const int32_t* seg, int G, float* part, float* out,
+                    void* stream) {
+  if (N % 8 || ld % 8) return set_error(SMES_ERR_SHAPE, "seg_colsum: N=%d and ld must be multiples of 8", N);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int tiles = (int)(rows_cap / 128);
+  int th = N / 8 < 256 ? N / 8 : 256;
+  th = (th + 31) / 32 * 32;
+  seg_colsum_tiles_kernel<<<tiles, th, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(M), ld, N, seg, G, part);
+  int rc = launch_check("seg_colsum_tiles");
+  if (rc) return rc;
+  dim3 g2((N + 127) / 128, G);
+  seg_colsum_groups_kernel<<<g2, 128, 0, st>>>(part, N, seg, out);
+  return launch_check("seg_colsum_groups");
+}
+
+int smes_unpermute(int B, int d, const int32_t* usize, const int32_t* row_of, int umax, const void* dX, long ldx,
+                   const float* dh_router, float* dh, void* stream) {
+  if (d % 8 || d > 2048) return set_error(SMES_ERR_SHAPE, "unpermute: d=%d", d);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int vec = (d + 255) / 256;
+  const int blocks = (B * 32 + 255) / 256;
+  auto* x = reinterpret_cast<const __nv_bfloat16*>(dX);
+  if (vec <= 1) unpermute_kernel<1><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  else if (vec <= 2) unpermute_kernel<2><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  else if (vec <= 4) unpermute_kernel<4><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  else unpermute_kernel<8><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  return launch_check("unpermute");
+}
+
+int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream) {
+  part_reduce_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, nparts, n, out);
+  return launch_check("part_reduce");
+}
+
+}  // extern "C"

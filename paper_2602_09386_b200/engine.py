@@ -1,0 +1,349 @@
+"""SMES layer engine: device workspaces + the kernel sequence of one step.
+
+One :class:`SMESEngine` owns every buffer of the hot path for a fixed shape
+(B, T, E, budget, expert stack).  ``forward`` / ``backward`` issue only
+``_smes.so`` kernels on the current CUDA stream -- no host syncs, no torch
+compute -- so a whole fwd+bwd step can be captured in one CUDA graph
+(``capture_step``).
+
+Kernel sequence (reference functions in taskmoe/ they replace):
+  fwd: router GEMM (routing.py:101-103) -> route (routing.py:235-281)
+       -> plan reduce + scatter/gather (execution.py:85-123, model.py:301)
+       -> expert GEMMs (execution.py:126-158) -> stats finalize (balance.py:54-80)
+       -> combine + heads + BCE (execution.py:161-191, model.py:202-208,
+          training.py:54-57) -> loss finalize (training.py:90-94)
+  bwd: combine/heads/LB backward (training.py:146-179, balance.py:83-99)
+       -> expert dgrad/wgrad/bias (training.py:180-191) -> router dgrad/wgrad
+          (training.py:209-212) -> un-permute (training.py:192) -> head grads
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _lib
+from ._lib import call, ptr
+from .errors import ConfigError, CudaError, ShapeError
+
+ACT = {"identity": 0, "relu": 1}
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise CudaError("SMES kernels need a CUDA device (sm_100a); there is no CPU fallback")
+    _lib.load()
+
+
+@dataclass
+class ExpertLayer:
+    """One expert pool (experts.py:17-73): W (E, d_out, d_in), b (E, d_out), act."""
+    weight: torch.Tensor
+    bias: torch.Tensor
+    act: str = "relu"
+
+    @property
+    def d_in(self):
+        return self.weight.shape[2]
+
+    @property
+    def d_out(self):
+        return self.weight.shape[1]
+
+
+@dataclass
+class SMESParams:
+    """Parameters of the SMES layer in the reference layouts (model.py:36-111), fp32 masters."""
+    router_w: torch.Tensor          # (T, E, d)
+    router_b: torch.Tensor          # (T, E)
+    layers: list                    # [ExpertLayer]
+    head_w: torch.Tensor            # (T, d_out)
+    head_b: torch.Tensor            # (T,)
+    task_weights: torch.Tensor | None = None   # (T,) Stage-I pooling weights (routing.py:79-87)
+    task_loss_weights: torch.Tensor | None = None  # (T,) lambda_t (training.py:138)
+    lb_strength: float = 0.0        # beta (model.py:158)
+
+    @property
+    def num_tasks(self):
+        return self.router_w.shape[0]
+
+    @property
+    def num_experts(self):
+        return self.router_w.shape[1]
+
+    @property
+    def d_in(self):
+        return self.router_w.shape[2]
+
+    @property
+    def d_out(self):
+        return self.layers[-1].d_out
+
+
+def _round(x, m):
+    return (x + m - 1) // m * m
+
+
+class SMESEngine:
+    """Fixed-shape executor of the SMES hot path on one GPU."""
+
+    def __init__(self, params: SMESParams, batch_size: int, k_shared: int, k_adaptive: int,
+                 dense_probs_in_stats: bool = False, keep_reps: bool = True,
+                 device: torch.device | str | None = None):
+        _require_cuda()
+        self.dev = torch.device(device or "cuda")
+        p = params
+        self.p = p
+        T, E, d = p.num_tasks, p.num_experts, p.d_in
+        B = int(batch_size)
+        ks, ka = int(k_shared), int(k_adaptive)
+        K = ks + ka
+        if ks < 0 or ka < 0:
+            raise ConfigError("budget counts must be non-negative")
+        if K < 1:
+            raise ConfigError("budget must activate at least one expert per task")
+        if K > E:
+            raise ConfigError(f"budget k={K} exceeds expert count {E}: stage-II would have only "
+                              f"{E - ks} candidates for {ka} adaptive picks")
+        if B < 1:
+            raise ShapeError("empty batch")
+        if (T * E) % 8 or d % 32:
+            raise ShapeError(f"kernel layout needs T*E % 8 == 0 and d % 32 == 0 (T*E={T * E}, d={d})")
+        dims = [d] + [l.d_out for l in p.layers]
+        if any(x % 32 for x in dims):
+            raise ShapeError(f"expert widths must be multiples of 32, got {dims}")
+        for i, l in enumerate(p.layers):
+            if l.d_in != dims[i] or l.weight.shape[0] != E:
+                raise ShapeError(f"expert layer {i} has shape {tuple(l.weight.shape)}")
+            if l.act not in ACT:
+                raise ConfigError(f"unknown nonlinearity '{l.act}', expected one of {tuple(ACT)}")
+        self.T, self.E, self.d, self.B, self.ks, self.ka, self.K = T, E, d, B, ks, ka, K
+        self.dims = dims
+        self.d_out = dims[-1]
+        self.dense = bool(dense_probs_in_stats)
+        self.keep_reps = keep_reps
+        self.umax = min(E, ks + T * ka)
+        self.rows_cap = _round(B * self.umax + E * 127, 128)
+        self.B_pad = _round(B, 128)
+        self.rpw = call("smes_route_rows_per_warp", B)
+        self.C = call("smes_route_num_chunks", B, self.rpw)
+        self.grid = call("smes_combine_grid", B)
+        self._alloc()
+        self.refresh_weights()
+
+    # ------------------------------------------------------------------ buffers
+    def _alloc(self):
+        dev, T, E, B, K, d = self.dev, self.T, self.E, self.B, self.K, self.d
+        i32, f32, f64, bf = torch.int32, torch.float32, torch.float64, torch.bfloat16
+        z = lambda *s, dt=f32: torch.zeros(*s, dtype=dt, device=dev)
+        EW = (E + 31) // 32
+        R = self.rows_cap
+        self.z = z(B, T * E)
+        self.shared = z(B, self.ks, dt=i32)
+        self.adaptive = z(T, B, self.ka, dt=i32)
+        self.active = z(T, B, K, dt=i32)
+        self.wsel = z(T, B, K)
+        self.umask = z(B, EW, dt=torch.int32)
+        self.usize = z(B, dt=i32)
+        self.chunk_union = z(self.C, E, dt=i32)
+        self.chunk_active = z(self.C, E, dt=i32)
+        self.chunk_mass = z(self.C, E, dt=f64)
+        self.chunk_dmass = z(self.C, E, dt=f64)
+        self.chunk_base = z(self.C, E, dt=i32)
+        self.loads = z(E, dt=i32)
+        self.stats_raw = z(3 * E, dt=f64)
+        self.seg_pad = z(E + 1, dt=i32)
+        self.seg_log = z(E + 1, dt=i32)
+        self.totals = z(2, dt=i32)
+        self.ticket = z(1, dt=i32)
+        self.flag = z(1, dt=i32)
+        self.row_of = z(B, self.umax, dt=i32)
+        self.gather_inst = z(R, dt=i32)
+        self.gather_exp = z(R, dt=i32)
+        self.X = z(R, d, dt=bf)
+        self.outs = [z(R, w, dt=bf) for w in self.dims[1:]]
+        self.bits = [z(w // 32, R, dt=torch.int32) if (l.act == "relu" and i < len(self.p.layers) - 1) else None
+                     for i, (w, l) in enumerate(zip(self.dims[1:], self.p.layers))]
+        self.reps = z(T, B, self.d_out, dt=bf) if self.keep_reps else None
+        self.logits = z(T, B)
+        self.preds = z(T, B)
+        self.labels = z(T, B)
+        self.loss_part = z(self.grid, dt=f64)
+        self.loss_out = z(3, dt=f64)
+        self.stats_out = z(3 * E + 1, dt=f64)
+        self.freq32 = z(E)
+        self.seg_router = torch.tensor([0, self.B_pad], dtype=i32, device=dev)
+        # backward
+        self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
+        self.dX = z(R, d, dt=bf)
+        self.dz = z(self.B_pad, T * E, dt=bf)
+        self.g_layers = [(z(E, l.d_out, l.d_in), z(E, l.d_out)) for l in self.p.layers]
+        self.colsum_part = z(R // 128, max(max(self.dims), T * E))
+        self.g_router_w = z(T * E, d)
+        self.g_router_b = z(T * E)
+        self.dh_router = z(B, d)
+        self.d_hidden = z(B, d)
+        self.part_dw = z(self.grid, T, self.d_out)
+        self.part_db = z(self.grid, T)
+        self.g_head_w = z(T, self.d_out)
+        self.g_head_b = z(T)
+        self.h = z(B, d, dt=bf)
+
+    def refresh_weights(self):
+        """Copy fp32 master parameters into the bf16 / fp32 kernel operands."""
+        p, T, E, d = self.p, self.T, self.E, self.d
+        dev = self.dev
+        self.wr_bf = p.router_w.detach().reshape(T * E, d).to(dev, torch.bfloat16).contiguous()
+        self.br = p.router_b.detach().reshape(T * E).to(dev, torch.float32).contiguous()
+        self.w_bf = [l.weight.detach().to(dev, torch.bfloat16).contiguous() for l in p.layers]
+        self.b32 = [l.bias.detach().to(dev, torch.float32).contiguous() for l in p.layers]
+        self.head_w = p.head_w.detach().to(dev, torch.float32).contiguous()
+        self.head_b = p.head_b.detach().to(dev, torch.float32).contiguous()
+        tw = p.task_weights if p.task_weights is not None else torch.ones(T)
+        self.tw = tw.detach().to(dev, torch.float64).contiguous()
+        lam = p.task_loss_weights if p.task_loss_weights is not None else torch.ones(T)
+        self.lam = lam.detach().to(dev, torch.float32).contiguous()
+        self.beta = float(p.lb_strength)
+
+    # ------------------------------------------------------------------ steps
+    def _stream(self):
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def set_inputs(self, h: torch.Tensor, labels: torch.Tensor | None = None):
+        """Stage the layer input (and labels) into the engine's device buffers."""
+        if h.shape != (self.B, self.d):
+            raise ShapeError(f"hidden has shape {tuple(h.shape)}, engine expects ({self.B}, {self.d})")
+        self.h.copy_(h, non_blocking=True)
+        if labels is not None:
+            if labels.shape != (self.T, self.B):
+                raise ShapeError(f"labels shape {tuple(labels.shape)} does not match ({self.T}, {self.B})")
+            self.labels.copy_(labels, non_blocking=True)
+
+    def forward(self, with_loss: bool = True):
+        s = self._stream()
+        T, E, B, d = self.T, self.E, self.B, self.d
+        # router logits z = h W_r^T + b_r  (B, T*E) fp32
+        call("smes_gemm_ragged_m", ptr(self.h), d, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
+             ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
+        self.route(s)
+        call("smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
+             ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
+             ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), s)
+        call("smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
+             ptr(self.loads), ptr(self.h), d, ptr(self.X), d, ptr(self.row_of), self.umax, ptr(self.gather_inst),
+             ptr(self.gather_exp), ptr(self.d_outs[-1]), self.d_out, self.d_out, s)
+        self.experts_forward(s)
+        self.stats_finalize(s)
+        call("smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
+             ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
+             ptr(self.head_b), ptr(self.reps), ptr(self.logits), ptr(self.preds),
+             ptr(self.labels) if with_loss else None, ptr(self.lam), ptr(self.loss_part) if with_loss else None,
+             self.grid, s)
+        if with_loss:
+            call("smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
+                 self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
+
+    def route(self, s, probs_in=None, probs_out=None):
+        T, E, B = self.T, self.E, self.B
+        call("smes_route_batch", ptr(self.z), E, T * E, ptr(probs_in), ptr(self.tw), T, B, E, self.ks, self.ka,
+             self.rpw, ptr(self.shared), ptr(self.adaptive), ptr(self.active), ptr(self.wsel), ptr(self.umask),
+             ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
+             ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), s)
+
+    def experts_forward(self, s):
+        R = self.rows_cap
+        inp = self.X
+        for i, l in enumerate(self.p.layers):
+            call("smes_gemm_ragged_m", ptr(inp), self.dims[i], R, ptr(self.w_bf[i]), self.E, self.dims[i + 1],
+                 self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act], ptr(self.bits[i]), None, R,
+                 ptr(self.outs[i]), self.dims[i + 1], 0, R, s)
+            inp = self.outs[i]
+
+    def stats_finalize(self, s, batch_times_tasks: float | None = None):
+        bt = float(self.B * self.T) if batch_times_tasks is None else batch_times_tasks
+        call("smes_stats_finalize", self.E, self.K, bt, int(self.dense), ptr(self.stats_raw), ptr(self.stats_out),
+             ptr(self.freq32), s)
+
+    def backward(self, batch_scale: int | None = None, lb_batch: int | None = None):
+        """Reverse pass.  ``batch_scale`` is the B of lambda/B (training.py:148);
+        ``lb_batch`` the B of the LB coefficient E/(K B T) (balance.py:97)."""
+        s = self._stream()
+        T, E, B, d, K = self.T, self.E, self.B, self.d, self.K
+        R = self.rows_cap
+        bs = B if batch_scale is None else batch_scale
+        lbb = B if lb_batch is None else lb_batch
+        lb_coef = self.beta * E / (K * lbb * T)
+        relu_last = int(self.p.layers[-1].act == "relu")
+        call("smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
+             ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
+             ptr(self.preds), ptr(self.labels), ptr(self.lam), 1.0 / bs, relu_last, ptr(self.d_outs[-1]),
+             ptr(self.dz), ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw),
+             ptr(self.part_db), self.grid, s)
+        n_layers = len(self.p.layers)
+        for i in range(n_layers - 1, -1, -1):
+            dout = self.d_outs[i]
+            inp = self.X if i == 0 else self.outs[i - 1]
+            gw, gb = self.g_layers[i]
+            di, do = self.dims[i], self.dims[i + 1]
+            if i > 0:   # dgrad into the previous layer's output, masked by its relu
+                call("smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
+                     None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
+            call("smes_gemm_ragged_k", ptr(dout), do, ptr(inp), di, R, E, do, di, ptr(self.seg_pad), ptr(gw), s)
+            call("smes_seg_colsum", ptr(dout), do, R, do, ptr(self.seg_pad), E, ptr(self.colsum_part), ptr(gb), s)
+        # dX = d_out0 W_0
+        call("smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
+             ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
+        # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
+        call("smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
+             ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
+        call("smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), d, B, 1, T * E, d, ptr(self.seg_router),
+             ptr(self.g_router_w), s)
+        call("smes_seg_colsum", ptr(self.dz), T * E, self.B_pad, T * E, ptr(self.seg_router), 1,
+             ptr(self.colsum_part), ptr(self.g_router_b), s)
+        call("smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
+             ptr(self.dh_router), ptr(self.d_hidden), s)
+        call("smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out, ptr(self.g_head_w), s)
+        call("smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
+
+    def step(self):
+        self.forward(with_loss=True)
+        self.backward()
+
+    # ------------------------------------------------------------------ graphs
+    def capture_step(self, warmup: int = 1) -> torch.cuda.CUDAGraph:
+        """Capture one fwd+bwd step (inputs read from ``self.h`` / ``self.labels``)."""
+        st = torch.cuda.Stream(self.dev)
+        st.wait_stream(torch.cuda.current_stream(self.dev))
+        with torch.cuda.stream(st):
+            for _ in range(warmup):
+                self.step()
+        torch.cuda.current_stream(self.dev).wait_stream(st)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.step()
+        return g
+
+    # ------------------------------------------------------------------ views
+    def n_act(self) -> int:
+        """Logical packed rows (reads the device counter: a host sync)."""
+        return int(self.totals[0].item())
+
+    def gradients(self) -> dict:
+        """Gradient blocks with the reference's names (model.py:94-111), single-pool
+        stacks use ``expert_{e}``; deeper stacks ``expert{l}_{e}``."""
+        T, E = self.T, self.E
+        g = {}
+        single = len(self.p.layers) == 1
+        for li, (gw, gb) in enumerate(self.g_layers):
+            for e in range(E):
+                pre = f"expert_{e}" if single else f"expert{li}_{e}"
+                g[pre + ".weight"] = gw[e]
+                g[pre + ".bias"] = gb[e]
+        rw = self.g_router_w.view(T, E, self.d)
+        rb = self.g_router_b.view(T, E)
+        for t in range(T):
+            g[f"router_{t}.weight"] = rw[t]
+            g[f"router_{t}.bias"] = rb[t]
+            g[f"head_{t}.weight"] = self.g_head_w[t:t + 1]
+            g[f"head_{t}.bias"] = self.g_head_b[t:t + 1]
+        return g

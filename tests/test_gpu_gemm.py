@@ -1,0 +1,132 @@
+"""tcgen05 grouped GEMM (csrc/gemm.cu) vs a plain PyTorch fp32 reference of the same op."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_09386_b200 import _lib
+from paper_2602_09386_b200._lib import call, ptr
+
+
+def _segments(loads, align=128):
+    seg = [0]
+    for n in loads:
+        seg.append(seg[-1] + (n + align - 1) // align * align)
+    return seg
+
+
+def _packed(loads, d, gen, dev):
+    seg = _segments(loads)
+    x = torch.zeros(seg[-1] + 128, d, device=dev)
+    for g, n in enumerate(loads):
+        x[seg[g]:seg[g] + n] = torch.randn(n, d, generator=gen, device=dev)
+    return seg, x
+
+
+@pytest.mark.parametrize("N,K", [(256, 128), (128, 256), (512, 256), (96, 64), (64, 512)])
+@pytest.mark.parametrize("act", [0, 1])
+def test_ragged_m_forward(N, K, act):
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(N * 7 + K + act)
+    loads = [300, 0, 129, 1, 128, 517]
+    E = len(loads)
+    seg, x = _packed(loads, K, g, dev)
+    R = x.shape[0]
+    xb = x.to(torch.bfloat16).contiguous()
+    w = (torch.randn(E, N, K, generator=g, device=dev) / K ** 0.5).to(torch.bfloat16).contiguous()
+    b = torch.randn(E, N, generator=g, device=dev).contiguous()
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.full((R, N), float("nan"), device=dev).to(torch.bfloat16)
+    bits = torch.zeros((N + 31) // 32, R, dtype=torch.int32, device=dev) if N % 32 == 0 and act else None
+    call("smes_gemm_ragged_m", ptr(xb), K, R, ptr(w), E, N, K, 0, ptr(seg_t), ptr(b), act, ptr(bits), None, R,
+         ptr(out), N, 0, R, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, n = seg[e], loads[e]
+        if n == 0:
+            continue
+        ref = xb[lo:lo + n].float() @ w[e].float().T + b[e]
+        if act:
+            ref = ref.clamp_min(0)
+        got = out[lo:lo + n].float()
+        err = (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
+        assert err < 1e-2, (e, err)
+        if bits is not None:
+            word = bits[:, lo:lo + n].T.contiguous()   # (n, N/32)
+            expect = (ref.to(torch.bfloat16).float() > 0)
+            for j in range(N // 32):
+                m = ((word[:, j:j + 1].long() >> torch.arange(32, device=dev)) & 1).bool()
+                assert torch.equal(m, expect[:, 32 * j:32 * j + 32])
+
+
+def test_ragged_m_fp32_out_unaligned_rows():
+    """Plain GEMM (router logits): 1 group, M not a multiple of 128, fp32 out, clipped store."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(3)
+    M, N, K = 1000, 256, 256
+    a = torch.randn(M, K, generator=g, device=dev).to(torch.bfloat16)
+    w = (torch.randn(1, N, K, generator=g, device=dev) * 1e-3).to(torch.bfloat16)
+    b = torch.randn(1, N, generator=g, device=dev)
+    seg = torch.tensor([0, 1024], dtype=torch.int32, device=dev)
+    out = torch.full((M + 24, N), 7.0, device=dev)
+    call("smes_gemm_ragged_m", ptr(a), K, M, ptr(w), 1, N, K, 0, ptr(seg), ptr(b), 0, None, None, 0, ptr(out), N, 1,
+         M, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = a.float() @ w[0].float().T + b[0]
+    assert (out[:M] - ref).abs().max().item() <= 1e-5 * ref.abs().max().item() + 1e-6
+    assert torch.all(out[M:] == 7.0)   # rows >= m_limit untouched
+
+
+@pytest.mark.parametrize("N,K", [(256, 512), (128, 256)])
+def test_ragged_m_dgrad_masked(N, K):
+    """dgrad: C[m, n] = mask(sum_k A[m, k] W_g[k, n]) with W stored (G, K, N)."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(11 + N)
+    loads = [200, 77, 0, 384]
+    E = len(loads)
+    seg, a = _packed(loads, K, g, dev)
+    R = a.shape[0]
+    ab = a.to(torch.bfloat16)
+    w = (torch.randn(E, K, N, generator=g, device=dev) / K ** 0.5).to(torch.bfloat16)
+    bits = torch.randint(-2 ** 31, 2 ** 31 - 1, (N // 32, R), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    call("smes_gemm_ragged_m", ptr(ab), K, R, ptr(w), E, N, K, 1, ptr(seg_t), None, 0, None, ptr(bits), R, ptr(out),
+         N, 0, R, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, n = seg[e], loads[e]
+        if n == 0:
+            continue
+        ref = ab[lo:lo + n].float() @ w[e].float()
+        word = bits[:, lo:lo + n].T.long()
+        mask = torch.cat([((word[:, j:j + 1] >> torch.arange(32, device=dev)) & 1) for j in range(N // 32)], 1).bool()
+        ref = torch.where(mask, ref, torch.zeros_like(ref))
+        got = out[lo:lo + n].float()
+        assert (got - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("I,J", [(256, 512), (512, 256), (128, 128), (64, 256)])
+def test_ragged_k_wgrad(I, J):
+    """wgrad: C_g[i, j] = sum_{m in g} P[m, i] Q[m, j] (fp32), empty groups -> exact zeros."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(I + 3 * J)
+    loads = [300, 0, 129, 640]
+    E = len(loads)
+    seg, pm = _packed(loads, I, g, dev)
+    _, qm = _packed(loads, J, g, dev)
+    R = pm.shape[0]
+    pb, qb = pm.to(torch.bfloat16), qm.to(torch.bfloat16)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.full((E, I, J), float("nan"), device=dev)
+    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J, R, E, I, J, ptr(seg_t), ptr(out),
+         torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, hi = seg[e], seg[e + 1]
+        ref = pb[lo:hi].float().T @ qb[lo:hi].float()
+        if loads[e] == 0:
+            assert torch.all(out[e] == 0)
+            continue
+        err = (out[e] - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 1e-5, (e, err)
