@@ -45,6 +45,13 @@ _RESTYPE = {"smes_last_error": C.c_char_p}
 _VALUE_FNS = {"smes_abi_version", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_last_error"}
 
+# kernels launched per successful call (for the bench's gpu_launches count)
+KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_scatter": 1, "smes_gemm_ragged_m": 1,
+                    "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
+                    "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1}
+launch_count = 0
+_timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
+
 _lib = None
 
 
@@ -72,15 +79,24 @@ _CODE_TO_EXC = {
 }
 
 
+tag = None   # label of the current launch site (set by the engine for per-kernel timing)
+
+
 def call(name: str, *args):
     """Invoke an entry point; raise the mapped exception on a non-zero status."""
+    global launch_count
     lib = load()
-    rc = getattr(lib, name)(*args)
     if name in _VALUE_FNS:
-        return rc
+        return getattr(lib, name)(*args)
+    if _timer is not None:
+        with _timer(tag or name):
+            rc = getattr(lib, name)(*args)
+    else:
+        rc = getattr(lib, name)(*args)
     if rc != 0:
         msg = lib.smes_last_error().decode(errors="replace")
         raise _CODE_TO_EXC.get(rc, errors.TaskMoeError)(msg)
+    launch_count += KERNELS_PER_CALL.get(name, 0)
     return rc
 
 

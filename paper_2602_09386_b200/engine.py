@@ -80,6 +80,14 @@ class SMESParams:
         return self.layers[-1].d_out
 
 
+def _tagged(tag, name, *args):
+    _lib.tag = tag
+    try:
+        return call(name, *args)
+    finally:
+        _lib.tag = None
+
+
 def _round(x, m):
     return (x + m - 1) // m * m
 
@@ -177,16 +185,23 @@ class SMESEngine:
         self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
         self.dX = z(R, d, dt=bf)
         self.dz = z(self.B_pad, T * E, dt=bf)
-        self.g_layers = [(z(E, l.d_out, l.d_in), z(E, l.d_out)) for l in self.p.layers]
+        # all parameter gradients live in ONE flat fp32 buffer (a single data-parallel all-reduce)
+        shapes = [(E, l.d_out, l.d_in) for l in self.p.layers] + [(E, l.d_out) for l in self.p.layers]
+        shapes += [(T * E, d), (T * E,), (T, self.d_out), (T,)]
+        sizes = [int(torch.Size(sh).numel()) for sh in shapes]
+        self.grad_flat = z(sum(sizes))
+        views, off = [], 0
+        for sh, n in zip(shapes, sizes):
+            views.append(self.grad_flat[off:off + n].view(sh))
+            off += n
+        nl = len(self.p.layers)
+        self.g_layers = [(views[i], views[nl + i]) for i in range(nl)]
+        self.g_router_w, self.g_router_b, self.g_head_w, self.g_head_b = views[2 * nl:]
         self.colsum_part = z(R // 128, max(max(self.dims), T * E))
-        self.g_router_w = z(T * E, d)
-        self.g_router_b = z(T * E)
         self.dh_router = z(B, d)
         self.d_hidden = z(B, d)
         self.part_dw = z(self.grid, T, self.d_out)
         self.part_db = z(self.grid, T)
-        self.g_head_w = z(T, self.d_out)
-        self.g_head_b = z(T)
         self.h = z(B, d, dt=bf)
 
     def refresh_weights(self):
@@ -220,32 +235,43 @@ class SMESEngine:
             self.labels.copy_(labels, non_blocking=True)
 
     def forward(self, with_loss: bool = True):
+        self.forward_a()
+        self.forward_b(with_loss=with_loss)
+
+    def forward_a(self):
+        """Router GEMM -> routing -> plan -> expert GEMMs.  Ends with the per-expert
+        LoadStats sums in ``stats_raw`` (the data-parallel exchange point)."""
         s = self._stream()
         T, E, B, d = self.T, self.E, self.B, self.d
         # router logits z = h W_r^T + b_r  (B, T*E) fp32
-        call("smes_gemm_ragged_m", ptr(self.h), d, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
+        _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), d, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
              ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
         self.route(s)
-        call("smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
+        _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
              ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), s)
-        call("smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
+        _tagged("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
              ptr(self.loads), ptr(self.h), d, ptr(self.X), d, ptr(self.row_of), self.umax, ptr(self.gather_inst),
              ptr(self.gather_exp), ptr(self.d_outs[-1]), self.d_out, self.d_out, s)
         self.experts_forward(s)
-        self.stats_finalize(s)
-        call("smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
+
+    def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None):
+        """LoadStats finalize (global B*T under data parallelism) -> combine + heads + loss."""
+        s = self._stream()
+        T, E, B = self.T, self.E, self.B
+        self.stats_finalize(s, batch_times_tasks)
+        _tagged("combine_fwd", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
              ptr(self.head_b), ptr(self.reps), ptr(self.logits), ptr(self.preds),
              ptr(self.labels) if with_loss else None, ptr(self.lam), ptr(self.loss_part) if with_loss else None,
              self.grid, s)
         if with_loss:
-            call("smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
+            _tagged("loss_finalize", "smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
                  self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
 
     def route(self, s, probs_in=None, probs_out=None):
         T, E, B = self.T, self.E, self.B
-        call("smes_route_batch", ptr(self.z), E, T * E, ptr(probs_in), ptr(self.tw), T, B, E, self.ks, self.ka,
+        _tagged("route", "smes_route_batch", ptr(self.z), E, T * E, ptr(probs_in), ptr(self.tw), T, B, E, self.ks, self.ka,
              self.rpw, ptr(self.shared), ptr(self.adaptive), ptr(self.active), ptr(self.wsel), ptr(self.umask),
              ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), s)
@@ -254,14 +280,14 @@ class SMESEngine:
         R = self.rows_cap
         inp = self.X
         for i, l in enumerate(self.p.layers):
-            call("smes_gemm_ragged_m", ptr(inp), self.dims[i], R, ptr(self.w_bf[i]), self.E, self.dims[i + 1],
+            _tagged(f"fc{i + 1}_fwd", "smes_gemm_ragged_m", ptr(inp), self.dims[i], R, ptr(self.w_bf[i]), self.E, self.dims[i + 1],
                  self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act], ptr(self.bits[i]), None, R,
                  ptr(self.outs[i]), self.dims[i + 1], 0, R, s)
             inp = self.outs[i]
 
     def stats_finalize(self, s, batch_times_tasks: float | None = None):
         bt = float(self.B * self.T) if batch_times_tasks is None else batch_times_tasks
-        call("smes_stats_finalize", self.E, self.K, bt, int(self.dense), ptr(self.stats_raw), ptr(self.stats_out),
+        _tagged("stats_finalize", "smes_stats_finalize", self.E, self.K, bt, int(self.dense), ptr(self.stats_raw), ptr(self.stats_out),
              ptr(self.freq32), s)
 
     def backward(self, batch_scale: int | None = None, lb_batch: int | None = None):
@@ -274,7 +300,7 @@ class SMESEngine:
         lbb = B if lb_batch is None else lb_batch
         lb_coef = self.beta * E / (K * lbb * T)
         relu_last = int(self.p.layers[-1].act == "relu")
-        call("smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
+        _tagged("combine_bwd", "smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
              ptr(self.preds), ptr(self.labels), ptr(self.lam), 1.0 / bs, relu_last, ptr(self.d_outs[-1]),
              ptr(self.dz), ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw),
@@ -286,28 +312,50 @@ class SMESEngine:
             gw, gb = self.g_layers[i]
             di, do = self.dims[i], self.dims[i + 1]
             if i > 0:   # dgrad into the previous layer's output, masked by its relu
-                call("smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
+                _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
-            call("smes_gemm_ragged_k", ptr(dout), do, ptr(inp), di, R, E, do, di, ptr(self.seg_pad), ptr(gw), s)
-            call("smes_seg_colsum", ptr(dout), do, R, do, ptr(self.seg_pad), E, ptr(self.colsum_part), ptr(gb), s)
+            _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), di, R, E, do, di, ptr(self.seg_pad), ptr(gw), s)
+            _tagged(f"fc{i + 1}_bias", "smes_seg_colsum", ptr(dout), do, R, do, ptr(self.seg_pad), E, ptr(self.colsum_part), ptr(gb), s)
         # dX = d_out0 W_0
-        call("smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
+        _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
              ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
         # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
-        call("smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
+        _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
              ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
-        call("smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), d, B, 1, T * E, d, ptr(self.seg_router),
+        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), d, B, 1, T * E, d, ptr(self.seg_router),
              ptr(self.g_router_w), s)
-        call("smes_seg_colsum", ptr(self.dz), T * E, self.B_pad, T * E, ptr(self.seg_router), 1,
+        _tagged("router_bias", "smes_seg_colsum", ptr(self.dz), T * E, self.B_pad, T * E, ptr(self.seg_router), 1,
              ptr(self.colsum_part), ptr(self.g_router_b), s)
-        call("smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
+        _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
              ptr(self.dh_router), ptr(self.d_hidden), s)
-        call("smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out, ptr(self.g_head_w), s)
-        call("smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
+        _tagged("head_reduce", "smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out, ptr(self.g_head_w), s)
+        _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
     def step(self):
         self.forward(with_loss=True)
         self.backward()
+
+    # ------------------------------------------------------------------ accounting
+    def work_model(self, n_act: int) -> dict:
+        """Algorithmic work per launch tag: (flops, bytes, bound).  SURVEY 8(d)."""
+        T, E, B, K, d, do = self.T, self.E, self.B, self.K, self.d, self.d_out
+        U = n_act / B
+        w = {"router_fwd": (2.0 * B * d * T * E, B * (d * 2 + T * E * 4), "tensor"),
+             "router_dgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 4), "tensor"),
+             "router_wgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 2), "tensor"),
+             "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4), "hbm"),
+             "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8, "hbm"),
+             "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12), "hbm"),
+             "combine_bwd": (0.0, B * (U * do * 2 * 2 + T * K * 8 + T * 8 + T * E * 2), "hbm"),
+             "unpermute": (0.0, B * (U * d * 2 + d * 8), "hbm")}
+        for i in range(len(self.dims) - 1):
+            di, dn = self.dims[i], self.dims[i + 1]
+            f = 2.0 * n_act * di * dn
+            w[f"fc{i + 1}_fwd"] = (f, n_act * (di + dn) * 2, "tensor")
+            w[f"fc{i + 1}_wgrad"] = (f, n_act * (di + dn) * 2, "tensor")
+            w[f"fc{i + 1}_dgrad"] = (f, n_act * (di + dn) * 2, "tensor")
+            w[f"fc{i + 1}_bias"] = (0.0, n_act * dn * 2, "hbm")
+        return w
 
     # ------------------------------------------------------------------ graphs
     def capture_step(self, warmup: int = 1) -> torch.cuda.CUDAGraph:
