@@ -42,23 +42,27 @@ int smes_abi_version(void);
  *      _renormalized_weights_batch (routing.py:203-211); fuses the per-chunk
  *      histograms of build_execution_plan (execution.py:109) and
  *      compute_load_stats (balance.py:65-68).  Stage I in fp64.
- *      z element (t,b,e) at z[t*stride_t + b*stride_b + e]. */
+ *      z element (t,b,e) at z[t*stride_t + b*stride_b + e].  frozen = 1 reuses the selections in
+ *      shared/adaptive and recomputes weights + statistics (model.py:284-300). */
 int smes_route_rows_per_warp(int B);
 int smes_route_num_chunks(int B, int rows_per_warp);
 int smes_route_batch(const float* z, long stride_t, long stride_b, const double* probs_in,
                      const double* task_weights, int T, int B, int E, int k_shared, int k_adaptive,
                      int rows_per_warp, int32_t* shared, int32_t* adaptive, int32_t* active, float* wsel,
                      uint32_t* umask, int32_t* usize, int32_t* chunk_union, int32_t* chunk_active,
-                     double* chunk_mass, double* chunk_dmass, double* probs_out, int32_t* flag, void* stream);
+                     double* chunk_mass, double* chunk_dmass, double* probs_out, int32_t* flag, int frozen,
+                     void* stream);
 
 /* ---- K2 execution plan: replaces build_execution_plan (execution.py:85-123)
  *      and the gather hidden[plan.gather_instances] (model.py:301).
  *      Segments are padded to 128 rows (seg_pad); seg_log are the reference's
- *      segment_offsets.  totals = {N_act, padded rows}. */
+ *      segment_offsets.  totals = {0, padded rows, N_act}. */
 int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
                      const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
                      double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
                      unsigned int* ticket, void* stream);
+int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
+                     void* stream);
 int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,
                       const int32_t* seg_pad, const int32_t* loads, const void* h_bf16, long ldh, void* X_bf16,
                       long ldx, int32_t* row_of, int umax, int32_t* gather_inst, int32_t* gather_exp,
@@ -79,19 +83,20 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
 
 /* ---- K4 combine + heads + BCE: replaces reconstruct_task_reps (execution.py:161-191),
  *      _heads (model.py:202-208) and _weighted_bce (training.py:54-57). */
-int smes_combine_grid(int B);
+int smes_combine_grid(int B, int T, int d_out);
 int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
                      const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
-                     const float* head_w, const float* head_b, void* reps, float* logits, float* preds,
+                     const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits, float* preds,
                      const float* labels, const float* lam, double* loss_part, int grid, void* stream);
 
 /* ---- K6+K7 heads/combine backward + LB gradient: replaces backward
  *      (training.py:146-179) and lb_loss_gradient (balance.py:83-99). */
 int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
                      const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
-                     const float* head_w, const float* preds, const float* labels, const float* lam, float inv_b,
-                     int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, int dense_probs,
-                     const float* z, float* part_dw, float* part_db, int grid, void* stream);
+                     const float* head_w, const float* P, long ldp, const void* reps, const float* preds,
+                     const float* labels, const float* lam, float inv_b, int relu_last, void* dpacked, void* dz,
+                     const float* freq, float lb_coef, int dense_probs, const float* z, float* part_dw,
+                     float* part_db, int grid, void* stream);
 
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
@@ -106,6 +111,14 @@ int smes_seg_colsum(const void* M, long ld, long rows_cap, int N, const int32_t*
 int smes_unpermute(int B, int d, const int32_t* usize, const int32_t* row_of, int umax, const void* dX, long ldx,
                    const float* dh_router, float* dh, void* stream);
 int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream);
+
+/* ---- standalone reference entry points: lb_loss_gradient (balance.py:83-99) as a dense
+ *      (T,B,E) tensor; task_loss (training.py:60-87) partial sums + validity flags
+ *      (bit 1: prediction outside [0,1], bit 2: label not in {0,1}). */
+int smes_lb_grad(int T, int B, int E, int K, const int32_t* active, const float* wsel, const float* z, long zst,
+                 long zsb, const float* freq, float coef, int dense, float* out, void* stream);
+int smes_bce_loss(int T, int B, const float* pred, const float* labels, const float* lam, double* part, int nparts,
+                  int32_t* bad, void* stream);
 
 #ifdef __cplusplus
 }

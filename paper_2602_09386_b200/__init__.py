@@ -1,6 +1,32 @@
-"""B200-native SMES layer (arXiv 2602.09386): sm_100a CUDA kernels behind the
-reference package's (taskmoe) Python module API."""
+"""B200-native SMES layer (arXiv 2602.09386).
+
+sm_100a CUDA kernels (csrc/, C ABI in include/smes.h) behind the reference
+package's (taskmoe 0.1.0) Python module API: the same function names,
+argument orders, result types and exception classes, on CUDA tensors.
+There is no CPU fallback: every entry point raises CudaError without a GPU.
+"""
 from .errors import ConfigError, CudaError, NumericsError, ShapeError, StateError, TaskMoeError
 from .engine import ExpertLayer, SMESEngine, SMESParams
+from .routing import (BatchRouting, RoutingBudget, RoutingDecision, naive_route_batch, progressive_route,
+                      renormalized_weights, route_batch)
+from .execution import (ExecutionPlan, ExpertPool, FlopCounter, build_execution_plan, grouped_gemm,
+                        init_expert_pool, reconstruct_task_reps)
+from .balance import LoadStats, SkewDiagnostics, compute_load_stats, lb_loss_gradient, skew_diagnostics
+from .linalg import Affine, init_affine
+from .model import ForwardResult, MoeModel, RouterBank, forward_sparse, init_model
+from .training import BackwardResult, backward, task_loss, total_loss
 
 __version__ = "0.1.0"
+
+__all__ = [
+    "TaskMoeError", "ShapeError", "ConfigError", "NumericsError", "StateError", "CudaError",
+    "SMESEngine", "SMESParams", "ExpertLayer",
+    "RoutingBudget", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route", "naive_route_batch",
+    "renormalized_weights",
+    "ExecutionPlan", "ExpertPool", "FlopCounter", "build_execution_plan", "grouped_gemm", "init_expert_pool",
+    "reconstruct_task_reps",
+    "LoadStats", "SkewDiagnostics", "compute_load_stats", "lb_loss_gradient", "skew_diagnostics",
+    "Affine", "init_affine",
+    "ForwardResult", "MoeModel", "RouterBank", "forward_sparse", "init_model",
+    "BackwardResult", "backward", "task_loss", "total_loss",
+]

@@ -2,19 +2,21 @@
 //
 // Forward restates `reconstruct_task_reps` (taskmoe/execution.py:161-191) fused
 // with `_heads` (taskmoe/model.py:202-208) and the clamped BCE
-// (taskmoe/training.py:54-57): every packed row of an instance is loaded ONCE
-// and accumulated into all T task representations with the renormalised
-// weights; the head dot products, sigmoid and per-instance loss follow in
-// registers.
+// (taskmoe/training.py:54-57).  Each packed row O[u] of an instance is loaded
+// ONCE; it is accumulated into all T task representations and projected onto
+// all T heads:  P[u, t] = <head_w_t, O[u]>  (so logit_t = sum_u w[u,t] P[u,t] + b_t).
+// P is kept (rows x T fp32) for the backward.
 //
 // Backward restates training.py:146-179 (+ the LB term of :155-157 and
-// balance.py:83-99):
-//   dlogit    = lambda_t / B * (yhat - y) * [clamp inactive]                   (:147-148)
-//   d_packed  = sum_t w[t,e] dlogit_t head_w_t  (x relu mask if last act relu) (:172-176, :180-181)
-//   g[t,k]    = dlogit_t <head_w_t, O[row]>,  dz = w (g - <g,w>) + beta dLB/dz  (:171, :178-179)
-//   dW_head_t = sum_b dlogit_t reps_t = sum_rows (w dlogit_t) O[row]            (:151)
-// One CTA of S warps owns one instance at a time (persistent grid); head-grad
-// partials stay in registers across instances and are reduced in fixed order.
+// balance.py:83-99) without touching O (identity last pool):
+//   dlogit_t  = lambda_t / B (yhat - y) [clamp inactive]                       (:147-148)
+//   d_packed[u] = sum_t w[u,t] dlogit_t head_w_t  (x [O>0] if last act relu)   (:172-176, :180-181)
+//   g[t,k]    = dlogit_t P[u(t,k), t]                                           (:171)
+//   dz[t,e_k] = w_k (g_k - sum_j g_j w_j) + beta * coef * w_k (f[e_k] - <w, f>) (:178-179, balance.py:97-99)
+//   dW_head_t = sum_b dlogit_t reps_t                                           (:151)
+// A CTA of 8 warps owns 8/S instances at a time (S warps per instance, each
+// thread 4..16 columns); head-grad partials stay in registers across instances
+// and are combined in a fixed order (deterministic).
 #include "ptx.cuh"
 #include "smes_capi.h"
 
@@ -22,6 +24,9 @@ namespace smes {
 
 constexpr int CB_MAX_U = 128;
 constexpr int CB_MAX_T = 32;
+constexpr int CB_THREADS = 256;
+constexpr int CB_WARPS = CB_THREADS / 32;
+constexpr int CB_MAX_TK = 1024;
 
 __device__ __forceinline__ int union_rank(const uint32_t* um, int e) {
   int r = 0;
@@ -30,27 +35,32 @@ __device__ __forceinline__ int union_rank(const uint32_t* um, int e) {
 }
 
 template <int VPL>
-__device__ __forceinline__ void load_row(const __nv_bfloat16* p, float (&x)[VPL]) {
-  if constexpr (VPL == 8) {
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+__device__ __forceinline__ void load_bf(const __nv_bfloat16* p, float (&x)[VPL]) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { float2 f = __bfloat1622float2(h[i]); x[2 * i] = f.x; x[2 * i + 1] = f.y; }
-  } else {
+  for (int i = 0; i < VPL; i += 8) {
+    if constexpr (VPL >= 8) {
+      uint4 v = __ldg(reinterpret_cast<const uint4*>(p + i));
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { float2 f = __bfloat1622float2(h[j]); x[i + 2 * j] = f.x; x[i + 2 * j + 1] = f.y; }
+    }
+  }
+  if constexpr (VPL == 4) {
     uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-    for (int i = 0; i < 2; ++i) { float2 f = __bfloat1622float2(h[i]); x[2 * i] = f.x; x[2 * i + 1] = f.y; }
+    for (int j = 0; j < 2; ++j) { float2 f = __bfloat1622float2(h[j]); x[2 * j] = f.x; x[2 * j + 1] = f.y; }
   }
 }
 template <int VPL>
-__device__ __forceinline__ void store_row(__nv_bfloat16* p, const float (&x)[VPL]) {
-  if constexpr (VPL == 8) {
-    uint4 v = make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-    *reinterpret_cast<uint4*>(p) = v;
+__device__ __forceinline__ void store_bf(__nv_bfloat16* p, const float (&x)[VPL]) {
+  if constexpr (VPL == 4) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
   } else {
-    uint2 v = make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
-    *reinterpret_cast<uint2*>(p) = v;
+#pragma unroll
+    for (int i = 0; i < VPL; i += 8)
+      *reinterpret_cast<uint4*>(p + i) = make_uint4(pack_bf16(x[i], x[i + 1]), pack_bf16(x[i + 2], x[i + 3]),
+                                                    pack_bf16(x[i + 4], x[i + 5]), pack_bf16(x[i + 6], x[i + 7]));
   }
 }
 template <int VPL>
@@ -60,6 +70,33 @@ __device__ __forceinline__ void load_f32(const float* p, float (&x)[VPL]) {
     float4 v = __ldg(reinterpret_cast<const float4*>(p + i));
     x[i] = v.x; x[i + 1] = v.y; x[i + 2] = v.z; x[i + 3] = v.w;
   }
+}
+
+// Butterfly reduce-scatter of N (power of two <= 32) per-lane values over a warp.
+// Returns the warp total of index t = (lane >> (5 - log2 N)) & (N - 1).
+template <int N>
+__device__ __forceinline__ float warp_reduce_scatter(float (&v)[N], int lane) {
+  constexpr int lg = N == 1 ? 0 : N == 2 ? 1 : N == 4 ? 2 : N == 8 ? 3 : N == 16 ? 4 : 5;
+#pragma unroll
+  for (int s = 0; s < lg; ++s) {
+    const int half = N >> (s + 1);
+    const int o = 16 >> s;
+    const bool upper = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = upper ? v[i] : v[i + half];
+      const float keep = upper ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> lg; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+  return v[0];
+}
+template <int N>
+__device__ __forceinline__ int rs_index(int lane) {
+  constexpr int lg = N == 1 ? 0 : N == 2 ? 1 : N == 4 ? 2 : N == 8 ? 3 : N == 16 ? 4 : 5;
+  return (lane >> (5 - lg)) & (N - 1);
 }
 
 struct CombineArgs {
@@ -73,270 +110,336 @@ struct CombineArgs {
   long ldo;
   const float* head_w;     // (T, d_out)
   const float* head_b;     // (T,)
-  // forward outputs
-  __nv_bfloat16* reps;     // optional (T, B, d_out)
+  float* P;                // (rows, ldp) head projections of every packed row
+  int ldp;
+  __nv_bfloat16* reps;     // (T, B, d_out)
   float* logits;           // (T, B)
   float* preds;            // (T, B)
   const float* labels;     // optional (T, B)
   const float* lam;        // (T,)
   double* loss_part;       // (grid,) per-CTA sum of lambda-weighted BCE
   // backward
-  float inv_b;             // 1 / B used in dlogit (training.py:148)
-  int relu_last;           // last expert pool is relu: mask d_packed by O > 0 (training.py:180-181)
+  float inv_b;
+  int relu_last;
   __nv_bfloat16* dpacked;  // (rows, ldo)
   __nv_bfloat16* dz;       // (B, T*E) dense
-  const float* freq;       // (E,) global selection frequency (balance.py:66)
-  float lb_coef;           // beta * E / (K * B * T)  (balance.py:97, training.py:157)
-  int dense_probs;         // LB gradient through full_probs (balance.py:96)
+  const float* freq;       // (E,)
+  float lb_coef;           // beta * E / (K * B * T)
+  int dense_probs;
   const float* z;          // logits (B, T*E) (dense mode only)
   float* part_dw;          // (grid, T, d_out)
   float* part_db;          // (grid, T)
 };
 
+// shared-memory layout per instance group
+template <int MAXT>
+struct GroupSmem {
+  uint32_t um[32];
+  int32_t rows[CB_MAX_U];
+  float wt[CB_MAX_U * MAXT];
+  float dl[MAXT];
+};
+
 template <int VPL, int MAXT>
-__global__ void __launch_bounds__(256) combine_fwd_kernel(const CombineArgs a) {
-  const int S = blockDim.x >> 5;
+__global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.d_out / (32 * VPL);        // warps per instance
+  const int G = CB_WARPS / S;                 // instances per CTA iteration
+  const int gi = warp / S, ws = warp % S;
+  const int col = (ws * 32 + lane) * VPL;
   const int T = a.T, K = a.K, EW = (a.E + 31) >> 5;
-  const int col = threadIdx.x * VPL;
-  __shared__ uint32_t s_um[32];
-  __shared__ int32_t s_rows[CB_MAX_U];
-  __shared__ float s_wt[CB_MAX_U * CB_MAX_T];
-  __shared__ float s_red[8][CB_MAX_T];
+  const int ldp = a.ldp;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  GroupSmem<MAXT>* gs = reinterpret_cast<GroupSmem<MAXT>*>(smraw) + gi;
+  const int gthreads = S * 32, gtid = ws * 32 + lane;
+  // logits: lane -> (task t, u-residue ug); MAXT <= 32
+  const int lt = lane & (MAXT - 1), ug = lane / MAXT;
+  constexpr int NG = 32 / MAXT;
   double my_loss = 0.0;
-  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    const int U = a.usize[b];
-    for (int j = threadIdx.x; j < EW; j += blockDim.x) s_um[j] = a.umask[(long)b * EW + j];
-    for (int u = threadIdx.x; u < U; u += blockDim.x) s_rows[u] = a.row_of[(long)b * a.umax + u];
-    for (int i = threadIdx.x; i < U * T; i += blockDim.x) s_wt[i] = 0.f;
-    __syncthreads();
-    for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
-      const int t = i / K;
-      const long o = ((long)t * a.B + b) * K + (i - t * K);
-      const int u = union_rank(s_um, a.active[o]);
-      s_wt[u * T + t] = a.wsel[o];
+  const int iters = (a.B + (long)gridDim.x * G - 1) / ((long)gridDim.x * G);
+  for (int it = 0; it < iters; ++it) {
+    const int b = (it * gridDim.x + blockIdx.x) * G + gi;
+    const bool valid = b < a.B;
+    const int U = valid ? a.usize[b] : 0;
+    if (valid) {
+      for (int j = gtid; j < EW; j += gthreads) gs->um[j] = a.umask[(long)b * EW + j];
+      for (int u = gtid; u < U; u += gthreads) gs->rows[u] = a.row_of[(long)b * a.umax + u];
+      for (int i = gtid; i < U * MAXT; i += gthreads) gs->wt[i] = 0.f;
     }
     __syncthreads();
-    float acc[MAXT][VPL];
+    if (valid) {
+      for (int i = gtid; i < T * K; i += gthreads) {
+        const int t = i / K;
+        const long o = ((long)t * a.B + b) * K + (i - t * K);
+        gs->wt[union_rank(gs->um, a.active[o]) * MAXT + t] = a.wsel[o];
+      }
+    }
+    __syncthreads();
+    if (valid) {
+      // reps_t = sum_u w[u,t] O[u]   (every packed row read once)
+      float acc[MAXT][VPL];
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t)
+      for (int t = 0; t < MAXT; ++t)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) acc[t][v] = 0.f;
-    for (int u = 0; u < U; ++u) {
-      float x[VPL];
-      load_row<VPL>(a.O + (long)s_rows[u] * a.ldo + col, x);
+        for (int v = 0; v < VPL; ++v) acc[t][v] = 0.f;
+      for (int u = 0; u < U; ++u) {
+        float x[VPL];
+        load_bf<VPL>(a.O + (long)gs->rows[u] * a.ldo + col, x);
 #pragma unroll
-      for (int t = 0; t < MAXT; ++t) {
-        if (t < T) {
-          const float w = s_wt[u * T + t];
+        for (int t = 0; t < MAXT; ++t) {
+          const float w = gs->wt[u * MAXT + t];
 #pragma unroll
           for (int v = 0; v < VPL; ++v) acc[t][v] = fmaf(w, x[v], acc[t][v]);
         }
       }
-    }
-    // heads: logit_t = <head_w_t, reps_t> + head_b_t
 #pragma unroll
-    for (int t = 0; t < MAXT; ++t) {
-      if (t < T) {
-        if (a.reps) store_row<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, acc[t]);
-        float hw[VPL];
-        load_f32<VPL>(a.head_w + (long)t * a.d_out + col, hw);
-        float p = 0.f;
+      for (int t = 0; t < MAXT; ++t)
+        if (t < T) store_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, acc[t]);
+      // logit_t = b_t + sum_u w[u,t] P[u,t]   (P = O head_W^T from the tensor-core GEMM)
+      if (ws == 0 && a.P != nullptr) {
+        float sacc = 0.f;
+        if (lt < T)
+          for (int u = ug; u < U; u += NG) sacc = fmaf(gs->wt[u * MAXT + lt], __ldg(a.P + (long)gs->rows[u] * ldp + lt), sacc);
 #pragma unroll
-        for (int v = 0; v < VPL; ++v) p = fmaf(hw[v], acc[t][v], p);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-        if (lane == 0) s_red[warp][t] = p;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < T) {
-      const int t = threadIdx.x;
-      float lg = a.head_b[t];
-      for (int w = 0; w < S; ++w) lg += s_red[w][t];
-      // stable sigmoid (linalg.py:108-113)
-      const float ez = expf(-fabsf(lg));
-      const float pos = 1.f / (1.f + ez);
-      const float pr = lg >= 0.f ? pos : 1.f - pos;
-      a.logits[(long)t * a.B + b] = lg;
-      a.preds[(long)t * a.B + b] = pr;
-      if (a.labels) {
-        // clamped BCE (training.py:54-57), accumulated in fp64
-        const double y = a.labels[(long)t * a.B + b];
-        double pc = (double)pr;
-        pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
-        my_loss += (double)a.lam[t] * -(y * log(pc) + (1.0 - y) * log1p(-pc));
+        for (int o = 16; o >= MAXT; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (ug == 0 && lt < T) {
+          const int t = lt;
+          const float lg = sacc + a.head_b[t];
+          const float ez = expf(-fabsf(lg));               // stable sigmoid (linalg.py:108-113)
+          const float pos = 1.f / (1.f + ez);
+          const float pr = lg >= 0.f ? pos : 1.f - pos;
+          a.logits[(long)t * a.B + b] = lg;
+          a.preds[(long)t * a.B + b] = pr;
+          if (a.labels) {
+            const double y = a.labels[(long)t * a.B + b];
+            double pc = (double)pr;
+            pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
+            my_loss += (double)a.lam[t] * -(y * log(pc) + (1.0 - y) * log1p(-pc));
+          }
+        }
       }
     }
     __syncthreads();
   }
   if (a.loss_part) {
-    // fixed-order CTA reduction of the per-task-thread sums
-    __shared__ double s_l[CB_MAX_T];
-    if (threadIdx.x < CB_MAX_T) s_l[threadIdx.x] = 0.0;
-    __syncthreads();
-    if (threadIdx.x < T) s_l[threadIdx.x] = my_loss;
+    double* s_l = reinterpret_cast<double*>(smraw);
+    s_l[threadIdx.x] = my_loss;
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0.0;
-      for (int t = 0; t < T; ++t) s += s_l[t];
+      for (int i = 0; i < CB_THREADS; ++i) s += s_l[i];
       a.loss_part[blockIdx.x] = s;
     }
   }
 }
 
 template <int VPL, int MAXT>
-__global__ void __launch_bounds__(256) combine_bwd_kernel(const CombineArgs a) {
-  const int S = blockDim.x >> 5;
+__global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E;
-  const int col = threadIdx.x * VPL;
-  __shared__ uint32_t s_um[32];
-  __shared__ int32_t s_rows[CB_MAX_U];
-  __shared__ float s_wt[CB_MAX_U * CB_MAX_T];
-  __shared__ float s_proj[CB_MAX_U * CB_MAX_T];
-  __shared__ float s_dl[CB_MAX_T];
-  __shared__ float s_red[8][CB_MAX_T];
-  float acc_dw[MAXT][VPL];
+  const int S = a.d_out / (32 * VPL);
+  const int G = CB_WARPS / S;
+  const int gi = warp / S, ws = warp % S;
+  const int col = (ws * 32 + lane) * VPL;
+  const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E, TK = T * K;
+  const int ldp = a.ldp;
+  const int n = T * a.d_out;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  GroupSmem<MAXT>* gs = reinterpret_cast<GroupSmem<MAXT>*>(smraw) + gi;
+  float* s_dw = reinterpret_cast<float*>(reinterpret_cast<GroupSmem<MAXT>*>(smraw) + G);   // [G][T*d_out]
+  float* s_pair = s_dw + (long)G * n;                                                     // [G][2][T*K]
+  float* my_dw = s_dw + (long)gi * n;
+  float* gw_s = s_pair + (long)gi * 2 * TK;
+  float* wf_s = gw_s + TK;
+  for (int i = threadIdx.x; i < G * n; i += CB_THREADS) s_dw[i] = 0.f;
+  float hw[MAXT][VPL];
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t)
+  for (int t = 0; t < MAXT; ++t) {
+    if (t < T) load_f32<VPL>(a.head_w + (long)t * a.d_out + col, hw[t]);
+    else {
 #pragma unroll
-    for (int v = 0; v < VPL; ++v) acc_dw[t][v] = 0.f;
+      for (int v = 0; v < VPL; ++v) hw[t][v] = 0.f;
+    }
+  }
   float my_db = 0.f;
-  for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
-    const int U = a.usize[b];
-    for (int j = threadIdx.x; j < EW; j += blockDim.x) s_um[j] = a.umask[(long)b * EW + j];
-    for (int u = threadIdx.x; u < U; u += blockDim.x) s_rows[u] = a.row_of[(long)b * a.umax + u];
-    for (int i = threadIdx.x; i < U * T; i += blockDim.x) s_wt[i] = 0.f;
-    if (threadIdx.x < T) {
-      const int t = threadIdx.x;
-      const float p = a.preds[(long)t * a.B + b], y = a.labels[(long)t * a.B + b];
-      const bool inside = p > 1e-7f && p < 1.f - 1e-7f;
-      const float dl = inside ? a.lam[t] * a.inv_b * (p - y) : 0.f;
-      s_dl[t] = dl;
-      my_db += dl;
-    }
-    // zero this instance's dz row (dense (B, T*E) operand of the router GEMMs)
-    for (int i = threadIdx.x * 8; i < TE; i += blockDim.x * 8)
-      *reinterpret_cast<uint4*>(a.dz + (long)b * TE + i) = make_uint4(0, 0, 0, 0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < T * K; i += blockDim.x) {
-      const int t = i / K;
-      const long o = ((long)t * a.B + b) * K + (i - t * K);
-      const int u = union_rank(s_um, a.active[o]);
-      s_wt[u * T + t] = a.wsel[o];
+  const int gthreads = S * 32, gtid = ws * 32 + lane;
+  const int iters = (a.B + (long)gridDim.x * G - 1) / ((long)gridDim.x * G);
+  for (int it = 0; it < iters; ++it) {
+    const int b = (it * gridDim.x + blockIdx.x) * G + gi;
+    const bool valid = b < a.B;
+    const int U = valid ? a.usize[b] : 0;
+    if (valid) {
+      for (int j = gtid; j < EW; j += gthreads) gs->um[j] = a.umask[(long)b * EW + j];
+      for (int u = gtid; u < U; u += gthreads) gs->rows[u] = a.row_of[(long)b * a.umax + u];
+      for (int i = gtid; i < U * MAXT; i += gthreads) gs->wt[i] = 0.f;
+      if (gtid < T) {
+        const int t = gtid;
+        const float p = a.preds[(long)t * a.B + b], y = a.labels[(long)t * a.B + b];
+        const bool inside = p > 1e-7f && p < 1.f - 1e-7f;
+        const float dl = inside ? a.lam[t] * a.inv_b * (p - y) : 0.f;
+        gs->dl[t] = dl;
+        my_db += dl;
+      }
     }
     __syncthreads();
-    for (int u = 0; u < U; ++u) {
-      const long r = s_rows[u];
-      float x[VPL], dp[VPL];
-      load_row<VPL>(a.O + r * a.ldo + col, x);
+    if (valid) {
+      for (int i = gtid; i < TK; i += gthreads) {
+        const int t = i / K;
+        const long o = ((long)t * a.B + b) * K + (i - t * K);
+        gs->wt[union_rank(gs->um, a.active[o]) * MAXT + t] = a.wsel[o];
+      }
+    }
+    __syncthreads();
+    if (valid) {
+      float dl[MAXT];
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) dp[v] = 0.f;
+      for (int t = 0; t < MAXT; ++t) dl[t] = t < T ? gs->dl[t] : 0.f;
+      // d_packed[u] = sum_t w[u,t] dlogit_t head_w_t
+      for (int u = 0; u < U; ++u) {
+        const long r = gs->rows[u];
+        float dp[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) dp[v] = 0.f;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          const float c = gs->wt[u * MAXT + t] * dl[t];
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) dp[v] = fmaf(c, hw[t][v], dp[v]);
+        }
+        if (a.relu_last) {
+          float x[VPL];
+          load_bf<VPL>(a.O + r * a.ldo + col, x);
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) dp[v] = x[v] > 0.f ? dp[v] : 0.f;
+        }
+        store_bf<VPL>(a.dpacked + r * a.ldo + col, dp);
+      }
+      // dW_head_t += dlogit_t * reps_t  (group-private smem accumulator, lane-owned columns)
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
         if (t < T) {
-          float hw[VPL];
-          load_f32<VPL>(a.head_w + (long)t * a.d_out + col, hw);
-          const float c = s_wt[u * T + t] * s_dl[t];
-          float p = 0.f;
+          float x[VPL];
+          load_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, x);
+          float* dst = my_dw + (long)t * a.d_out + col;
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) {
-            dp[v] = fmaf(c, hw[v], dp[v]);
-            acc_dw[t][v] = fmaf(c, x[v], acc_dw[t][v]);
-            p = fmaf(hw[v], x[v], p);
+          for (int v = 0; v < VPL; ++v) dst[v] = fmaf(dl[t], x[v], dst[v]);
+        }
+      }
+      // router-logit gradient over the (task, pick) pairs (softmax over the active set only)
+      if (ws == 0) {
+        __nv_bfloat16* dzr = a.dz + (long)b * TE;
+        for (int i = lane * 8; i < TE; i += 256) *reinterpret_cast<uint4*>(dzr + i) = make_uint4(0, 0, 0, 0);
+        if (!a.dense_probs) {
+          for (int i = lane; i < TK; i += 32) {
+            const int t = i / K;
+            const long o = ((long)t * a.B + b) * K + (i - t * K);
+            const int e = a.active[o];
+            const float w = a.wsel[o];
+            const float p = __ldg(a.P + (long)gs->rows[union_rank(gs->um, e)] * ldp + t);
+            gw_s[i] = gs->dl[t] * p * w;          // g_k w_k
+            wf_s[i] = w * __ldg(a.freq + e);      // w_k f_k
           }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-          if (lane == 0) s_red[warp][t] = p;
+          __syncwarp();
+          for (int i = lane; i < TK; i += 32) {
+            const int t = i / K;
+            const long o = ((long)t * a.B + b) * K + (i - t * K);
+            float Gt = 0.f, Ft = 0.f;
+            for (int k = 0; k < K; ++k) { Gt += gw_s[t * K + k]; Ft += wf_s[t * K + k]; }
+            const int e = a.active[o];
+            const float w = a.wsel[o];
+            // w (g - G) + coef w (f - F)
+            dzr[t * E + e] = __float2bfloat16_rn((gw_s[i] - w * Gt) + a.lb_coef * (wf_s[i] - w * Ft));
+          }
+          __syncwarp();
+        } else if (lane < T) {
+          const int t = lane;
+          const long ob = ((long)t * a.B + b) * K;
+          float G2 = 0.f;
+          for (int k = 0; k < K; ++k) {
+            const int e = a.active[ob + k];
+            G2 += gs->dl[t] * a.P[(long)gs->rows[union_rank(gs->um, e)] * ldp + t] * a.wsel[ob + k];
+          }
+          const float* zr = a.z + (long)b * TE + (long)t * E;
+          float mx = -INFINITY;
+          for (int e = 0; e < E; ++e) mx = fmaxf(mx, zr[e]);
+          float s = 0.f, Fd = 0.f;
+          for (int e = 0; e < E; ++e) { float q = expf(zr[e] - mx); s += q; Fd += q * a.freq[e]; }
+          Fd /= s;
+          __nv_bfloat16* dzt = dzr + (long)t * E;
+          for (int e = 0; e < E; ++e) dzt[e] = __float2bfloat16_rn(a.lb_coef * (expf(zr[e] - mx) / s) * (a.freq[e] - Fd));
+          for (int k = 0; k < K; ++k) {
+            const int e = a.active[ob + k];
+            const float w = a.wsel[ob + k];
+            const float g = gs->dl[t] * a.P[(long)gs->rows[union_rank(gs->um, e)] * ldp + t];
+            dzt[e] = __float2bfloat16_rn(w * (g - G2) + __bfloat162float(dzt[e]));
+          }
         }
-      }
-      if (a.relu_last) {
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) dp[v] = x[v] > 0.f ? dp[v] : 0.f;
-      }
-      store_row<VPL>(a.dpacked + r * a.ldo + col, dp);
-      __syncthreads();
-      if (threadIdx.x < T) {
-        float p = 0.f;
-        for (int w = 0; w < S; ++w) p += s_red[w][threadIdx.x];
-        s_proj[u * T + threadIdx.x] = p;
-      }
-      __syncthreads();
-    }
-    // router-logit gradient, one thread per task (softmax over the active set only)
-    if (threadIdx.x < T) {
-      const int t = threadIdx.x;
-      const long ob = ((long)t * a.B + b) * K;
-      float G = 0.f, F = 0.f;
-      for (int k = 0; k < K; ++k) {
-        const int e = a.active[ob + k];
-        const float w = a.wsel[ob + k];
-        G += s_dl[t] * s_proj[union_rank(s_um, e) * T + t] * w;
-        F += w * a.freq[e];
-      }
-      __nv_bfloat16* dzr = a.dz + (long)b * TE + (long)t * E;
-      if (a.dense_probs) {
-        // balance.py:96-99 with full_probs: dense over all E
-        const float* zr = a.z + (long)b * TE + (long)t * E;
-        float mx = -INFINITY;
-        for (int e = 0; e < E; ++e) mx = fmaxf(mx, zr[e]);
-        float s = 0.f, Fd = 0.f;
-        for (int e = 0; e < E; ++e) { float q = expf(zr[e] - mx); s += q; Fd += q * a.freq[e]; }
-        Fd /= s;
-        for (int e = 0; e < E; ++e) {
-          const float q = expf(zr[e] - mx) / s;
-          dzr[e] = __float2bfloat16_rn(a.lb_coef * q * (a.freq[e] - Fd));
-        }
-      }
-      for (int k = 0; k < K; ++k) {
-        const int e = a.active[ob + k];
-        const float w = a.wsel[ob + k];
-        const float g = s_dl[t] * s_proj[union_rank(s_um, e) * T + t];
-        float v = w * (g - G);
-        if (a.dense_probs) v += __bfloat162float(dzr[e]);
-        else v += a.lb_coef * w * (a.freq[e] - F);
-        dzr[e] = __float2bfloat16_rn(v);
       }
     }
     __syncthreads();
   }
-  // per-CTA head-grad partials
-  float* pw = a.part_dw + (long)blockIdx.x * T * a.d_out;
-#pragma unroll
-  for (int t = 0; t < MAXT; ++t)
-    if (t < T)
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) pw[(long)t * a.d_out + col + v] = acc_dw[t][v];
-  if (threadIdx.x < T) a.part_db[(long)blockIdx.x * T + threadIdx.x] = my_db;
-}
-
-static int pick_vpl(int T, int d_out) {
-  // keep MAXT * VPL <= 128 accumulators per thread
-  int vpl = (T <= 8) ? 8 : 4;
-  if (d_out / vpl < 32) vpl = 4;
-  return vpl;
+  // per-CTA head-grad partials: sum the G groups in fixed order
+  float* s_db = s_pair;    // reuse (G * MAXT floats)
+  if (gtid < T) s_db[gi * MAXT + gtid] = my_db;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += CB_THREADS) {
+    float s = 0.f;
+    for (int g = 0; g < G; ++g) s += s_dw[(long)g * n + i];
+    a.part_dw[(long)blockIdx.x * n + i] = s;
+  }
+  if (threadIdx.x < T) {
+    float s = 0.f;
+    for (int g = 0; g < G; ++g) s += s_db[g * MAXT + threadIdx.x];
+    a.part_db[(long)blockIdx.x * T + threadIdx.x] = s;
+  }
 }
 
 }  // namespace smes
 
 using namespace smes;
 
+static int pick_vpl(int T, int d_out) {
+  // VPL columns per thread, S = d_out / (32 VPL) warps per instance (1, 2, 4 or 8)
+  int mt = T <= 4 ? 4 : T <= 8 ? 8 : T <= 16 ? 16 : 32;
+  int vpl = mt <= 8 ? 8 : 4;
+  while (vpl > 4 && d_out / (32 * vpl) < 1) vpl /= 2;
+  if (d_out % (32 * vpl)) return -1;
+  int s = d_out / (32 * vpl);
+  if (s != 1 && s != 2 && s != 4 && s != 8) return -1;
+  return vpl;
+}
+
+static size_t combine_smem(bool bwd, int T, int K, int d_out, int vpl, int mt) {
+  const int S = d_out / (32 * vpl), G = CB_WARPS / S;
+  size_t groups = 0;
+  switch (mt) {
+    case 4: groups = sizeof(GroupSmem<4>); break;
+    case 8: groups = sizeof(GroupSmem<8>); break;
+    case 16: groups = sizeof(GroupSmem<16>); break;
+    default: groups = sizeof(GroupSmem<32>); break;
+  }
+  size_t s = groups * G;
+  if (bwd) s += (size_t)G * T * d_out * 4 + (size_t)G * (2 * T * K > mt ? 2 * T * K : mt) * 4;
+  size_t tail = (size_t)CB_THREADS * 8;
+  return s > tail ? s : tail;
+}
+
 static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream) {
   if (a.T > CB_MAX_T) return set_error(SMES_ERR_SHAPE, "combine: T=%d exceeds %d", a.T, CB_MAX_T);
   if (a.umax > CB_MAX_U) return set_error(SMES_ERR_SHAPE, "combine: union bound %d exceeds %d", a.umax, CB_MAX_U);
   if (a.E > 1024) return set_error(SMES_ERR_SHAPE, "combine: E=%d exceeds 1024", a.E);
   const int vpl = pick_vpl(a.T, a.d_out);
-  if (a.d_out % (32 * vpl)) return set_error(SMES_ERR_SHAPE, "combine: d_out=%d must be a multiple of %d", a.d_out, 32 * vpl);
-  const int threads = a.d_out / vpl;
-  if (threads > 256) return set_error(SMES_ERR_SHAPE, "combine: d_out=%d too large", a.d_out);
+  if (vpl < 0) return set_error(SMES_ERR_SHAPE, "combine: unsupported d_out=%d for T=%d", a.d_out, a.T);
   if (bwd && ((a.T * a.E) % 8)) return set_error(SMES_ERR_SHAPE, "combine_bwd: T*E must be a multiple of 8");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (a.T * a.K > CB_MAX_TK) return set_error(SMES_ERR_SHAPE, "combine: T*K=%d exceeds %d", a.T * a.K, CB_MAX_TK);
   const int mt = a.T <= 4 ? 4 : a.T <= 8 ? 8 : a.T <= 16 ? 16 : 32;
-#define CB_CASE(V, M)                                                        \
-  if (vpl == V && mt == M) {                                                 \
-    if (bwd) combine_bwd_kernel<V, M><<<grid, threads, 0, st>>>(a);          \
-    else combine_fwd_kernel<V, M><<<grid, threads, 0, st>>>(a);              \
+  const size_t smem = combine_smem(bwd, a.T, a.K, a.d_out, vpl, mt);
+  if (smem > 227 * 1024) return set_error(SMES_ERR_SHAPE, "combine: shared memory %zu too large", smem);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+#define CB_CASE(V, M)                                                                                    \
+  if (vpl == V && mt == M) {                                                                             \
+    auto kf = bwd ? combine_bwd_kernel<V, M> : combine_fwd_kernel<V, M>;                                 \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    kf<<<grid, CB_THREADS, smem, st>>>(a);                                                               \
   } else
   CB_CASE(8, 4) CB_CASE(8, 8) CB_CASE(4, 4) CB_CASE(4, 8) CB_CASE(4, 16) CB_CASE(4, 32) {
     return set_error(SMES_ERR_SHAPE, "combine: unsupported T=%d d_out=%d", a.T, a.d_out);
@@ -349,33 +452,42 @@ static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream) {
 
 extern "C" {
 
-int smes_combine_grid(int B) {
-  int g = 148 * 16;
-  return B < g ? B : g;
+int smes_combine_grid(int B, int T, int d_out) {
+  const int vpl = pick_vpl(T, d_out);
+  const int S = vpl > 0 ? d_out / (32 * vpl) : 1;
+  const int G = CB_WARPS / (S > 0 ? S : 1);
+  int need = (B + G - 1) / G;
+  int g = 148 * 2;     // ~1-2 resident CTAs per SM (register / smem bound); fewer head-grad partials
+  return need < g ? need : g;
 }
 
 int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
                      const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
-                     const float* head_w, const float* head_b, void* reps, float* logits, float* preds,
+                     const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits, float* preds,
                      const float* labels, const float* lam, double* loss_part, int grid, void* stream) {
   CombineArgs a{};
   a.T = T; a.B = B; a.E = E; a.K = K; a.d_out = d_out; a.umax = umax;
   a.umask = umask; a.usize = usize; a.row_of = row_of; a.active = active; a.wsel = wsel;
   a.O = reinterpret_cast<const __nv_bfloat16*>(O); a.ldo = ldo; a.head_w = head_w; a.head_b = head_b;
+  a.P = const_cast<float*>(P); a.ldp = (int)ldp;
   a.reps = reinterpret_cast<__nv_bfloat16*>(reps); a.logits = logits; a.preds = preds; a.labels = labels;
   a.lam = lam; a.loss_part = loss_part;
+  if (!reps) return set_error(SMES_ERR_STATE, "combine_fwd: reps buffer is required");
   return combine_launch(false, a, grid, stream);
 }
 
 int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
                      const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
-                     const float* head_w, const float* preds, const float* labels, const float* lam, float inv_b,
-                     int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, int dense_probs,
-                     const float* z, float* part_dw, float* part_db, int grid, void* stream) {
+                     const float* head_w, const float* P, long ldp, const void* reps, const float* preds, const float* labels,
+                     const float* lam, float inv_b, int relu_last, void* dpacked, void* dz, const float* freq,
+                     float lb_coef, int dense_probs, const float* z, float* part_dw, float* part_db, int grid,
+                     void* stream) {
   CombineArgs a{};
   a.T = T; a.B = B; a.E = E; a.K = K; a.d_out = d_out; a.umax = umax;
   a.umask = umask; a.usize = usize; a.row_of = row_of; a.active = active; a.wsel = wsel;
-  a.O = reinterpret_cast<const __nv_bfloat16*>(O); a.ldo = ldo; a.head_w = head_w;
+  a.O = reinterpret_cast<const __nv_bfloat16*>(O); a.ldo = ldo; a.head_w = head_w; a.P = const_cast<float*>(P);
+  a.ldp = (int)ldp;
+  a.reps = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(reps));
   a.preds = const_cast<float*>(preds); a.labels = labels; a.lam = lam; a.inv_b = inv_b; a.relu_last = relu_last;
   a.dpacked = reinterpret_cast<__nv_bfloat16*>(dpacked); a.dz = reinterpret_cast<__nv_bfloat16*>(dz);
   a.freq = freq; a.lb_coef = lb_coef; a.dense_probs = dense_probs; a.z = z; a.part_dw = part_dw; a.part_db = part_db;

@@ -24,7 +24,8 @@ namespace smes {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;   // 4 non-epilogue warps + 8 epilogue warps (2 per TMEM lane quarter)
+constexpr int kEpiWarps = 8;
 
 enum { MODE_RAGGED_M = 0, MODE_RAGGED_K = 1 };
 
@@ -50,7 +51,7 @@ struct Smem {
   static constexpr int kStg = 32 * 128;         // 4 KB per staging buffer
   static constexpr int kOffB = kStages * kA;
   static constexpr int kOffStg = kOffB + kStages * kB;
-  static constexpr int kOffBar = kOffStg + 4 * 2 * kStg;
+  static constexpr int kOffBar = kOffStg + kEpiWarps * kStg;
   static constexpr int kOffSeg = kOffBar + 256;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 12 + 1024;   // + barriers + group table + alignment slack
   static constexpr int kTmemCols = 2 * BN;
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 128); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps * 32); }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, S::kTmemCols);
@@ -205,10 +206,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ================= epilogue: TMEM -> regs -> (bias, act, mask) -> smem (SW128) -> TMA store
+    // warp w owns TMEM lanes 32*(w%4).. and every other column chunk (parity (w-4)/4)
     const int q = warp & 3;
-    uint8_t* stg0 = sStg + q * 2 * S::kStg;
-    int it = 0, nst = 0;
-    constexpr int kColsPerChunkBf = 64, kColsPerChunkF = 32;
+    const int par = (warp - 4) >> 2;
+    uint8_t* stg = sStg + (warp - 4) * S::kStg;
+    const bool fp32out = args.out_fp32 != 0;
+    const int cpc = fp32out ? 32 : 64;
+    const int ncols = args.N;
+    int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       int g, r0, c0, kb0, nkb;
       decode(tile, g, r0, c0, kb0, nkb);
@@ -218,41 +223,43 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
       const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
-      const int ncols = MODE == MODE_RAGGED_M ? args.N : args.N;
-      const bool fp32out = args.out_fp32 != 0;
-      const int cpc = fp32out ? kColsPerChunkF : kColsPerChunkBf;
-      for (int cc = 0; cc < BN / cpc; ++cc) {
+      for (int cc = par; cc < BN / cpc; cc += 2) {
         const int n = c0 + cc * cpc;
         if (n >= ncols) break;
-        uint32_t v[64];
-        {
+        float f[64];
+        if (nkb > 0) {
           uint32_t t0[32];
           tmem_ld32(tbase + cc * cpc, t0);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = t0[j];
           if (!fp32out) {
             uint32_t t1[32];
             tmem_ld32(tbase + cc * cpc + 32, t1);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[32 + j] = t1[j];
+            for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = __uint_as_float(t1[j]); }
           } else {
             tmem_ld_wait();
-          }
-        }
-        float f[64];
-        const int nv = fp32out ? 32 : 64;
 #pragma unroll
-        for (int j = 0; j < 64; ++j) f[j] = (j < nv && nkb > 0) ? __uint_as_float(v[j]) : 0.f;
+            for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = 0.f; }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) f[j] = 0.f;
+        }
         if (MODE == MODE_RAGGED_M) {
           if (args.bias != nullptr) {
             const float* bp = args.bias + (size_t)g * args.N + n;
+            if (n + cpc <= ncols) {
 #pragma unroll
-            for (int j = 0; j < 64; j += 4) {
-              if (j < nv && n + j < ncols) {
-                float4 bb = __ldg(reinterpret_cast<const float4*>(bp + j));
-                f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+              for (int j = 0; j < 64; j += 4) {
+                if (j < cpc) {
+                  float4 bb = __ldg(reinterpret_cast<const float4*>(bp + j));
+                  f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+                }
               }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 64; ++j)
+                if (j < cpc && n + j < ncols) f[j] += __ldg(bp + j);
             }
           }
           if (args.act == 1) {
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (args.bits_out != nullptr) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (h * 32 < nv && n + h * 32 < ncols) {
+              if (h * 32 < cpc && n + h * 32 < ncols) {
                 uint32_t w = 0;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
@@ -273,8 +280,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (args.bits_in != nullptr) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (h * 32 < nv && n + h * 32 < ncols) {
-                uint32_t w = __ldg(&args.bits_in[(size_t)((n >> 5) + h) * args.bits_ld + row]);
+              if (h * 32 < cpc && n + h * 32 < ncols) {
+                const uint32_t w = __ldg(&args.bits_in[(size_t)((n >> 5) + h) * args.bits_ld + row]);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[h * 32 + j] = ((w >> j) & 1u) ? f[h * 32 + j] : 0.f;
               }
@@ -282,8 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         // stage into smem (128 B per row, 128B swizzle) and TMA-store a {cpc x 32} box
-        uint8_t* stg = stg0 + (nst & 1) * S::kStg;
-        if (lane == 0) bulk_wait_read<1>();
+        if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
         uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
 #pragma unroll
@@ -305,7 +311,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           else tma_store_3d(&tmC, stg, n, r0 + 32 * q, g);
           bulk_commit();
         }
-        ++nst;
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -390,7 +395,7 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                        long bits_ld, void* C, long ldc, int out_fp32, long m_limit, void* stream) {
   if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
   if (N <= 0 || K <= 0 || rows_cap <= 0) return set_error(SMES_ERR_SHAPE, "empty GEMM N=%d K=%d", N, K);
-  if ((lda * 2) % 16 || (ldc * (out_fp32 ? 4 : 2)) % 16 || (K * 2) % 16 || (N * 2) % 16)
+  if ((lda * 2) % 16 || (ldc * (out_fp32 ? 4 : 2)) % 16 || (K * 2) % 16)
     return set_error(SMES_ERR_SHAPE, "GEMM strides must be 16-byte aligned (lda=%ld ldc=%ld K=%d N=%d)", lda, ldc,
                      K, N);
   if ((bits_out || bits_in) && (N % 32))

@@ -101,8 +101,9 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     }
     seg_pad[E] = p;
     seg_log[E] = l;
-    totals[0] = l;   // N_act (logical rows)
+    totals[0] = 0;   // totals[0:2] doubles as the one-group segment table [0, padded rows]
     totals[1] = p;   // physical rows incl. padding
+    totals[2] = l;   // N_act (logical rows)
     *ticket = 0u;
   }
 }
@@ -127,7 +128,8 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
     const int lo = seg_pad[e] + loads[e], hi = seg_pad[e + 1];
     const uint4 z4 = make_uint4(0, 0, 0, 0);
     for (int r = lo + warp; r < hi; r += PL_WARPS) {
-      for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(X + (long)r * ldx + c) = z4;
+      if (X != nullptr)
+        for (int c = lane * 8; c < d; c += 256) *reinterpret_cast<uint4*>(X + (long)r * ldx + c) = z4;
       if (zero_rows2 != nullptr)
         for (int c = lane * 8; c < d2; c += 256) *reinterpret_cast<uint4*>(zero_rows2 + (long)r * ldz2 + c) = z4;
       if (lane == 0) { gather_inst[r] = -1; gather_exp[r] = e; }
@@ -172,7 +174,8 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       int col = (v * 32 + lane) * 8;
-      hv[v] = col < d ? __ldg(reinterpret_cast<const uint4*>(h + (long)b * ldh + col)) : make_uint4(0, 0, 0, 0);
+      hv[v] = (h != nullptr && col < d) ? __ldg(reinterpret_cast<const uint4*>(h + (long)b * ldh + col))
+                                        : make_uint4(0, 0, 0, 0);
     }
     int u = 0;
     for (int j = 0; j < EW; ++j) {
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           int col = (v * 32 + lane) * 8;
-          if (col < d) *reinterpret_cast<uint4*>(X + (long)r * ldx + col) = hv[v];
+          if (h != nullptr && col < d) *reinterpret_cast<uint4*>(X + (long)r * ldx + col) = hv[v];
         }
         if (lane == 0) {
           row_of[(long)b * umax + u] = r;
@@ -203,6 +206,36 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
         ++u;
       }
     }
+  }
+}
+
+// chunk histograms of union membership for an arbitrary union bitmask (the
+// build_execution_plan(unions, E) entry point, when no router ran before it)
+__global__ void __launch_bounds__(PL_WARPS * 32)
+    plan_counts_kernel(int B, int E, int rows_per_warp, const uint32_t* __restrict__ umask,
+                       int32_t* __restrict__ chunk_union, int32_t* __restrict__ usize) {
+  __shared__ int32_t s_cnt[PL_WARPS][1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int EW = (E + 31) >> 5;
+  const int row0 = blockIdx.x * PL_WARPS * rows_per_warp + warp * rows_per_warp;
+  const int rend = min(row0 + rows_per_warp, B);
+  for (int e = lane; e < E; e += 32) s_cnt[warp][e] = 0;
+  __syncwarp();
+  for (int b = row0; b < rend; ++b) {
+    int sz = 0;
+    for (int j = 0; j < EW; ++j) {
+      const uint32_t w = umask[(long)b * EW + j];
+      sz += __popc(w);
+      const int e = j * 32 + lane;
+      if (e < E && ((w >> lane) & 1u)) s_cnt[warp][e] += 1;
+    }
+    if (lane == 0) usize[b] = sz;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int c = 0;
+    for (int w = 0; w < PL_WARPS; ++w) c += s_cnt[w][e];
+    chunk_union[(long)blockIdx.x * E + e] = c;
   }
 }
 
@@ -220,6 +253,17 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
                                          stats_raw, seg_pad, seg_log, totals, ticket);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
+                     void* stream) {
+  if (E > 1024) return set_error(SMES_ERR_SHAPE, "plan: E=%d exceeds 1024", E);
+  const int C = (B + PL_WARPS * rows_per_warp - 1) / (PL_WARPS * rows_per_warp);
+  plan_counts_kernel<<<C, PL_WARPS * 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(B, E, rows_per_warp, umask,
+                                                                                     chunk_union, usize);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_counts launch: %s", cudaGetErrorString(e));
   return SMES_OK;
 }
 

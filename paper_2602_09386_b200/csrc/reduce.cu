@@ -40,9 +40,16 @@ __global__ void stats_finalize_kernel(int E, int K, double bt, int dense, const 
 
 __global__ void loss_finalize_kernel(int n, const double* __restrict__ part, double inv_b, double beta,
                                      const double* __restrict__ stats_value, double* __restrict__ out) {
+  __shared__ double red[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) s += part[i];
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     const double task = s * inv_b;
     const double lb = stats_value ? *stats_value : 0.0;
     out[0] = task;
@@ -51,23 +58,39 @@ __global__ void loss_finalize_kernel(int n, const double* __restrict__ part, dou
   }
 }
 
-// stage 1: one block per 128-row tile (tiles never straddle groups); thread = 8 columns
-__global__ void seg_colsum_tiles_kernel(const __nv_bfloat16* __restrict__ M, long ld, int N,
-                                        const int32_t* __restrict__ seg, int G, float* __restrict__ part) {
+// stage 1: one block per 128-row tile (tiles never straddle groups).  Thread = 8 columns x
+// a strided subset of the tile's rows; the row groups are combined in a fixed order.
+__global__ void __launch_bounds__(256) seg_colsum_tiles_kernel(const __nv_bfloat16* __restrict__ M, long ld, int N,
+                                                               const int32_t* __restrict__ seg, int G,
+                                                               float* __restrict__ part) {
+  __shared__ float red[2048 + 64];
   const int tile = blockIdx.x;
   if (tile * 128 >= seg[G]) return;
-  for (int c = threadIdx.x * 8; c < N; c += blockDim.x * 8) {
+  const int ct = N / 8;                       // column threads (<= 256)
+  const int rg = 256 / ct;                    // row groups
+  const int c = (threadIdx.x % ct) * 8, g = threadIdx.x / ct;
+  for (int n0 = 0; n0 < N; n0 += 2048) {
     float s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const __nv_bfloat16* p = M + (long)tile * 128 * ld + c;
-    for (int r = 0; r < 128; ++r) {
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(p + (long)r * ld));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+    if (g < rg && n0 + c < N) {
+      const __nv_bfloat16* p = M + (long)tile * 128 * ld + n0 + c;
+#pragma unroll 4
+      for (int r = g; r < 128; r += rg) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(p + (long)r * ld));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) { float2 f = __bfloat1622float2(h[i]); s[2 * i] += f.x; s[2 * i + 1] += f.y; }
+        for (int i = 0; i < 4; ++i) { float2 f = __bfloat1622float2(h[i]); s[2 * i] += f.x; s[2 * i + 1] += f.y; }
+      }
     }
-    float* o = part + (long)tile * N + c;
+    // fixed-order combine of the row groups: group 0 first, then 1, ...
+    for (int k = 0; k < rg; ++k) {
+      if (g == k && n0 + c < N) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = s[i];
+        for (int i = 0; i < 8; ++i) red[c + i] = (k == 0 ? 0.f : red[c + i]) + s[i];
+      }
+      __syncthreads();
+    }
+    for (int i = threadIdx.x; i < min(2048, N - n0); i += blockDim.x) part[(long)tile * N + n0 + i] = red[i];
+    __syncthreads();
   }
 }
 
@@ -78,9 +101,16 @@ __global__ void seg_colsum_groups_kernel(const float* __restrict__ part, int N, 
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
   const int t0 = seg[g] / 128, t1 = seg[g + 1] / 128;
-  float s = 0.f;
-  for (int t = t0; t < t1; ++t) s += part[(long)t * N + n];
-  out[(long)g * N + n] = s;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  int t = t0;
+  for (; t + 4 <= t1; t += 4) {
+    s0 += part[(long)t * N + n];
+    s1 += part[(long)(t + 1) * N + n];
+    s2 += part[(long)(t + 2) * N + n];
+    s3 += part[(long)(t + 3) * N + n];
+  }
+  for (; t < t1; ++t) s0 += part[(long)t * N + n];
+  out[(long)g * N + n] = (s0 + s1) + (s2 + s3);
 }
 
 template <int VEC>
@@ -132,11 +162,96 @@ __global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize
 }
 
 __global__ void part_reduce_kernel(const float* __restrict__ part, int nparts, int n, float* __restrict__ out) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  float s = 0.f;
-  for (int p = 0; p < nparts; ++p) s += part[(long)p * n + i];
-  out[i] = s;
+  __shared__ float red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + lane;
+  const int per = (nparts + 7) / 8;
+  const int p0 = warp * per, p1 = min(nparts, p0 + per);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (i < n) {
+    int p = p0;
+    for (; p + 4 <= p1; p += 4) {
+      s0 += part[(long)p * n + i];
+      s1 += part[(long)(p + 1) * n + i];
+      s2 += part[(long)(p + 2) * n + i];
+      s3 += part[(long)(p + 3) * n + i];
+    }
+    for (; p < p1; ++p) s0 += part[(long)p * n + i];
+  }
+  red[warp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (warp == 0 && i < n) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    out[i] = t;
+  }
+}
+
+// dL_lb/dz (balance.py:83-99): one warp per (t, b) row; sparse reading uses the
+// renormalised weights on the active set, dense reading the full softmax of z.
+__global__ void lb_grad_kernel(int T, int B, int E, int K, const int32_t* __restrict__ active,
+                               const float* __restrict__ wsel, const float* __restrict__ z, long zst, long zsb,
+                               const float* __restrict__ freq, float coef, int dense, float* __restrict__ out) {
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (row >= T * B) return;
+  const int t = row / B, b = row - t * B;
+  float* o = out + (long)row * E;
+  if (!dense) {
+    for (int e = lane; e < E; e += 32) o[e] = 0.f;
+    __syncwarp();
+    float wf = 0.f, w = 0.f;
+    int e = 0;
+    if (lane < K) {
+      e = active[(long)row * K + lane];
+      w = wsel[(long)row * K + lane];
+      wf = w * freq[e];
+    }
+    float F = wf;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) F += __shfl_xor_sync(0xffffffffu, F, s);
+    if (lane < K) o[e] = coef * w * (freq[e] - F);
+  } else {
+    const float* zr = z + (long)t * zst + (long)b * zsb;
+    float mx = -INFINITY;
+    for (int e = lane; e < E; e += 32) mx = fmaxf(mx, zr[e]);
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    float sum = 0.f, F = 0.f;
+    for (int e = lane; e < E; e += 32) { const float q = expf(zr[e] - mx); sum += q; F += q * freq[e]; }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, s);
+      F += __shfl_xor_sync(0xffffffffu, F, s);
+    }
+    F /= sum;
+    for (int e = lane; e < E; e += 32) o[e] = coef * (expf(zr[e] - mx) / sum) * (freq[e] - F);
+  }
+}
+
+// weighted clamped BCE (training.py:54-57) -> per-block fp64 partials
+__global__ void bce_kernel(int T, int B, const float* __restrict__ pred, const float* __restrict__ y,
+                           const float* __restrict__ lam, double* __restrict__ part, int32_t* __restrict__ bad) {
+  __shared__ double red[32];
+  double v = 0.0;
+  int badv = 0;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < (long)T * B; i += (long)gridDim.x * blockDim.x) {
+    const int t = (int)(i / B);
+    const double p = pred[i], yy = y[i];
+    if (!(p >= 0.0 && p <= 1.0)) badv |= 1;
+    if (!(yy == 0.0 || yy == 1.0)) badv |= 2;
+    const double c = p < 1e-7 ? 1e-7 : (p > 1.0 - 1e-7 ? 1.0 - 1e-7 : p);
+    v += (double)lam[t] * -(yy * log(c) + (1.0 - yy) * log1p(-c));
+  }
+  if (badv) atomicOr(bad, badv);
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    part[blockIdx.x] = s;
+  }
 }
 
 }  // namespace smes
@@ -160,7 +275,7 @@ int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const
 
 int smes_loss_finalize(int nparts, const double* part, double inv_b, double beta, const double* stats_value,
                        double* out, void* stream) {
-  loss_finalize_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(nparts, part, inv_b, beta, stats_value,
+  loss_finalize_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(nparts, part, inv_b, beta, stats_value,
                                                                             out);
   return launch_check("loss_finalize");
 }
@@ -169,14 +284,13 @@ int smes_seg_colsum(const void* M, long ld, long rows_cap, int N, const int32_t*
                     void* stream) {
   if (N % 8 || ld % 8) return set_error(SMES_ERR_SHAPE, "seg_colsum: N=%d and ld must be multiples of 8", N);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (N / 8 > 256 || N % 8) return set_error(SMES_ERR_SHAPE, "seg_colsum: N=%d must be <= 2048", N);
   const int tiles = (int)(rows_cap / 128);
-  int th = N / 8 < 256 ? N / 8 : 256;
-  th = (th + 31) / 32 * 32;
-  seg_colsum_tiles_kernel<<<tiles, th, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(M), ld, N, seg, G, part);
+  seg_colsum_tiles_kernel<<<tiles, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(M), ld, N, seg, G, part);
   int rc = launch_check("seg_colsum_tiles");
   if (rc) return rc;
-  dim3 g2((N + 127) / 128, G);
-  seg_colsum_groups_kernel<<<g2, 128, 0, st>>>(part, N, seg, out);
+  dim3 g2((N + 63) / 64, G);
+  seg_colsum_groups_kernel<<<g2, 64, 0, st>>>(part, N, seg, out);
   return launch_check("seg_colsum_groups");
 }
 
@@ -194,8 +308,23 @@ int smes_unpermute(int B, int d, const int32_t* usize, const int32_t* row_of, in
   return launch_check("unpermute");
 }
 
+int smes_lb_grad(int T, int B, int E, int K, const int32_t* active, const float* wsel, const float* z, long zst,
+                 long zsb, const float* freq, float coef, int dense, float* out, void* stream) {
+  if (K > 32) return set_error(SMES_ERR_CONFIG, "lb_grad: K=%d exceeds 32", K);
+  const long rows = (long)T * B;
+  lb_grad_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      T, B, E, K, active, wsel, z, zst, zsb, freq, coef, dense, out);
+  return launch_check("lb_grad");
+}
+
+int smes_bce_loss(int T, int B, const float* pred, const float* labels, const float* lam, double* part, int nparts,
+                  int32_t* bad, void* stream) {
+  bce_kernel<<<nparts, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(T, B, pred, labels, lam, part, bad);
+  return launch_check("bce_loss");
+}
+
 int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream) {
-  part_reduce_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, nparts, n, out);
+  part_reduce_kernel<<<(n + 31) / 32, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, nparts, n, out);
   return launch_check("part_reduce");
 }
 

@@ -40,6 +40,7 @@ struct RouteArgs {
   double* chunk_dmass;     // (C, E) dense mass
   double* probs_out;       // optional (T,B,E) fp64 dense softmax
   int32_t* flag;           // non-finite logits seen (sticky)
+  int frozen;              // 1: shared/adaptive are inputs (model.py:284-300), weights/stats recomputed
 };
 
 template <int EPL>
@@ -84,7 +85,7 @@ __device__ __forceinline__ void warp_argmax_f32(const float (&v)[EPL], const uin
   }
 }
 
-template <int EPL>
+template <int EPL, int TP>
 __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = a.T, E = a.E, ks = a.ks, ka = a.ka, K = ks + ka;
@@ -110,19 +111,35 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
   for (int r = 0; r < a.rows_per_warp; ++r) {
     const int b = row0 + r;
     if (b >= a.B) break;
+    // ---------------- load the row's logits (all tasks when T*EPL fits in registers)
+    float zpre[TP > 0 ? TP : 1][EPL];
+    if (TP > 0) {
+#pragma unroll
+      for (int t = 0; t < TP; ++t) {
+        const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          int e = lane + 32 * j;
+          zpre[t][j] = (t < T && e < E) ? __ldg(zr + e) : -INFINITY;
+        }
+      }
+    }
     // ---------------- Stage I (fp64)
     double pooled[EPL];
     double dsum[EPL];
 #pragma unroll
     for (int j = 0; j < EPL; ++j) { pooled[j] = 0.0; dsum[j] = 0.0; }
-    for (int t = 0; t < T; ++t) {
+#pragma unroll
+    for (int t = 0; t < (TP > 0 ? TP : 1024); ++t) {
+      if (t >= T) break;
       const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
       float zv[EPL];
       float mx = -INFINITY;
 #pragma unroll
       for (int j = 0; j < EPL; ++j) {
         int e = lane + 32 * j;
-        zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
+        if (TP > 0) zv[j] = zpre[TP > 0 ? t : 0][j];
+        else zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
         if (e < E && !isfinite(zv[j])) bad = 1;
         mx = fmaxf(mx, zv[j]);
       }
@@ -140,8 +157,10 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double inv = 1.0 / s;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) p[j] = p[j] / s;
+        (void)inv;
       } else {
         const double* pr = a.probs_in + ((long)t * a.B + b) * E;
 #pragma unroll
@@ -167,12 +186,21 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     // shared set: K_s rounds of warp argmax on (pooled desc, index asc)
     uint32_t taken = 0;  // bit j: expert lane+32j is shared
     int my_shared = -1;  // lane i < ks holds the i-th pick
-    for (int i = 0; i < ks; ++i) {
-      double bv;
-      int bi;
-      warp_argmax_f64<EPL>(pooled, taken, lane, E, bv, bi);
-      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-      if (lane == i) my_shared = bi;
+    if (a.frozen) {
+      const int v = lane < ks ? a.shared[(long)b * ks + lane] : -1;
+      for (int i = 0; i < ks; ++i) {
+        const int bi = __shfl_sync(0xffffffffu, v, i);
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      }
+      my_shared = v;
+    } else {
+      for (int i = 0; i < ks; ++i) {
+        double bv;
+        int bi;
+        warp_argmax_f64<EPL>(pooled, taken, lane, E, bv, bi);
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == i) my_shared = bi;
+      }
     }
     // sort the shared picks ascending (rank among the ks lanes)
     int srank = 0;
@@ -180,27 +208,40 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
       int o = __shfl_sync(0xffffffffu, my_shared, j);
       if (lane < ks && o < my_shared) ++srank;
     }
+    __syncwarp();
     if (lane < ks) a.shared[(long)b * ks + srank] = my_shared;
 
     // ---------------- Stage II, per task
     uint32_t in_union = taken;  // union bits owned by this lane
-    for (int t = 0; t < T; ++t) {
+#pragma unroll
+    for (int t = 0; t < (TP > 0 ? TP : 1024); ++t) {
+      if (t >= T) break;
       const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
       float zv[EPL];
 #pragma unroll
       for (int j = 0; j < EPL; ++j) {
         int e = lane + 32 * j;
-        zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
+        if (TP > 0) zv[j] = zpre[TP > 0 ? t : 0][j];
+        else zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
         if ((taken >> j) & 1u) zv[j] = -INFINITY;
       }
       uint32_t picked = 0;
       int my_pick = -1;  // lane i < ka holds the i-th adaptive pick
-      for (int i = 0; i < ka; ++i) {
-        float bv;
-        int bi;
-        warp_argmax_f32<EPL>(zv, taken | picked, lane, E, bv, bi);
-        if ((bi & 31) == lane) picked |= 1u << (bi >> 5);
-        if (lane == i) my_pick = bi;
+      if (a.frozen) {
+        const int v = lane < ka ? a.adaptive[((long)t * a.B + b) * ka + lane] : -1;
+        for (int i = 0; i < ka; ++i) {
+          const int bi = __shfl_sync(0xffffffffu, v, i);
+          if ((bi & 31) == lane) picked |= 1u << (bi >> 5);
+        }
+        my_pick = v;
+      } else {
+        for (int i = 0; i < ka; ++i) {
+          float bv;
+          int bi;
+          warp_argmax_f32<EPL>(zv, taken | picked, lane, E, bv, bi);
+          if ((bi & 31) == lane) picked |= 1u << (bi >> 5);
+          if (lane == i) my_pick = bi;
+        }
       }
       in_union |= picked;
       int arank = 0;
@@ -208,6 +249,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         int o = __shfl_sync(0xffffffffu, my_pick, j);
         if (lane < ka && o < my_pick) ++arank;
       }
+      __syncwarp();
       if (lane < ka) a.adaptive[((long)t * a.B + b) * ka + arank] = my_pick;
       // active = sorted(shared U adaptive): lanes 0..K-1 each hold one member
       int val = -1;
@@ -221,7 +263,20 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         int o = __shfl_sync(0xffffffffu, val, j);
         if (o < val) ++pos;
       }
-      float zsel = lane < K ? __ldg(zr + val) : -INFINITY;
+      float zsel;
+      if (TP > 0) {
+        // owner lane of expert val holds it in zpre[t][val / 32]
+        float mine = 0.f;
+        const int src = lane < K ? (val & 31) : 0, jj = lane < K ? (val >> 5) : 0;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          float cand = __shfl_sync(0xffffffffu, zpre[TP > 0 ? t : 0][j], src);
+          if (j == jj) mine = cand;
+        }
+        zsel = lane < K ? mine : -INFINITY;
+      } else {
+        zsel = lane < K ? __ldg(zr + val) : -INFINITY;
+      }
       float mx = zsel;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -259,6 +314,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     }
     __syncwarp();
   }
+  bad = __any_sync(0xffffffffu, bad);
   if (bad && lane == 0) atomicOr(a.flag, 1);
   __syncthreads();
   // chunk partials in fixed warp order
@@ -301,7 +357,7 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
                      int T, int B, int E, int k_shared, int k_adaptive, int rows_per_warp, int32_t* shared,
                      int32_t* adaptive, int32_t* active, float* wsel, uint32_t* umask, int32_t* usize,
                      int32_t* chunk_union, int32_t* chunk_active, double* chunk_mass, double* chunk_dmass,
-                     double* probs_out, int32_t* flag, void* stream) {
+                     double* probs_out, int32_t* flag, int frozen, void* stream) {
   if (T < 1 || B < 1 || E < 1) return set_error(SMES_ERR_SHAPE, "route_batch: empty logits T=%d B=%d E=%d", T, B, E);
   if (E > RT_MAX_E) return set_error(SMES_ERR_SHAPE, "route_batch: E=%d exceeds %d", E, RT_MAX_E);
   if (k_shared < 0 || k_adaptive < 0) return set_error(SMES_ERR_CONFIG, "budget counts must be non-negative");
@@ -313,19 +369,26 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
   if (k_shared + k_adaptive > 32) return set_error(SMES_ERR_CONFIG, "budget k=%d exceeds 32", k_shared + k_adaptive);
   RouteArgs a{z, stride_t, stride_b, probs_in, task_weights, T, B, E, k_shared, k_adaptive, rows_per_warp,
               shared, adaptive, active, wsel, umask, usize, chunk_union, chunk_active, chunk_mass, chunk_dmass,
-              probs_out, flag};
+              probs_out, flag, frozen};
   const int C = smes_route_num_chunks(B, rows_per_warp);
   const size_t smem = (size_t)RT_WARPS * (E + 1) * 24 + 64;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int epl = (E + 31) / 32;
-#define RT_LAUNCH(N)                                                                            \
-  if (epl <= N) {                                                                               \
-    if (smem > 48 * 1024)                                                                       \
-      cudaFuncSetAttribute(route_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    route_kernel<N><<<C, RT_WARPS * 32, smem, st>>>(a);                                        \
+#define RT_LAUNCH_T(N, TPV)                                                                       \
+  {                                                                                               \
+    if (smem > 48 * 1024)                                                                         \
+      cudaFuncSetAttribute(route_kernel<N, TPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    route_kernel<N, TPV><<<C, RT_WARPS * 32, smem, st>>>(a);                                     \
+  }
+#define RT_LAUNCH(N)                                                                              \
+  if (epl <= N) {                                                                                 \
+    if (T * N <= 8 && T <= 8 / N) RT_LAUNCH_T(N, (8 / N > 0 ? 8 / N : 1))                         \
+    else if (T * N <= 32 && T <= 32 / N) RT_LAUNCH_T(N, (32 / N > 0 ? 32 / N : 1))               \
+    else RT_LAUNCH_T(N, 0)                                                                        \
   } else
   RT_LAUNCH(1) RT_LAUNCH(2) RT_LAUNCH(4) RT_LAUNCH(8) RT_LAUNCH(16) RT_LAUNCH(32) {}
 #undef RT_LAUNCH
+#undef RT_LAUNCH_T
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "route_batch launch: %s", cudaGetErrorString(e));
   return SMES_OK;

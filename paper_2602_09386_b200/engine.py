@@ -128,6 +128,7 @@ class SMESEngine:
         self.T, self.E, self.d, self.B, self.ks, self.ka, self.K = T, E, d, B, ks, ka, K
         self.dims = dims
         self.d_out = dims[-1]
+        self.grid = call("smes_combine_grid", B, T, self.d_out)
         self.dense = bool(dense_probs_in_stats)
         self.keep_reps = keep_reps
         self.umax = min(E, ks + T * ka)
@@ -135,7 +136,6 @@ class SMESEngine:
         self.B_pad = _round(B, 128)
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
-        self.grid = call("smes_combine_grid", B)
         self._alloc()
         self.refresh_weights()
 
@@ -162,7 +162,7 @@ class SMESEngine:
         self.stats_raw = z(3 * E, dt=f64)
         self.seg_pad = z(E + 1, dt=i32)
         self.seg_log = z(E + 1, dt=i32)
-        self.totals = z(2, dt=i32)
+        self.totals = z(3, dt=i32)     # {0, padded rows, N_act}; [0:2] is the one-group segment table
         self.ticket = z(1, dt=i32)
         self.flag = z(1, dt=i32)
         self.row_of = z(B, self.umax, dt=i32)
@@ -172,7 +172,9 @@ class SMESEngine:
         self.outs = [z(R, w, dt=bf) for w in self.dims[1:]]
         self.bits = [z(w // 32, R, dt=torch.int32) if (l.act == "relu" and i < len(self.p.layers) - 1) else None
                      for i, (w, l) in enumerate(zip(self.dims[1:], self.p.layers))]
-        self.reps = z(T, B, self.d_out, dt=bf) if self.keep_reps else None
+        self.reps = z(T, B, self.d_out, dt=bf)     # required by the backward (head grads)
+        self.ldp = _round(T, 4)
+        self.P = z(R, self.ldp)                     # head projections P = O head_W^T of every packed row
         self.logits = z(T, B)
         self.preds = z(T, B)
         self.labels = z(T, B)
@@ -181,6 +183,11 @@ class SMESEngine:
         self.stats_out = z(3 * E + 1, dt=f64)
         self.freq32 = z(E)
         self.seg_router = torch.tensor([0, self.B_pad], dtype=i32, device=dev)
+        # router wgrad reduces over B: split the batch into 256-row groups (split-K), reduce after
+        self.rw_splits = max(1, min(64, self.B_pad // 256))
+        edges = [min(self.B_pad, (self.B_pad // self.rw_splits) // 128 * 128 * i) for i in range(self.rw_splits)]
+        self.seg_router_split = torch.tensor(edges + [self.B_pad], dtype=i32, device=dev)
+        self.rw_part = z(self.rw_splits, T * E, d)
         # backward
         self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
         self.dX = z(R, d, dt=bf)
@@ -213,6 +220,7 @@ class SMESEngine:
         self.w_bf = [l.weight.detach().to(dev, torch.bfloat16).contiguous() for l in p.layers]
         self.b32 = [l.bias.detach().to(dev, torch.float32).contiguous() for l in p.layers]
         self.head_w = p.head_w.detach().to(dev, torch.float32).contiguous()
+        self.head_w_bf = self.head_w.to(torch.bfloat16).reshape(1, T, -1).contiguous()
         self.head_b = p.head_b.detach().to(dev, torch.float32).contiguous()
         tw = p.task_weights if p.task_weights is not None else torch.ones(T)
         self.tw = tw.detach().to(dev, torch.float64).contiguous()
@@ -238,7 +246,7 @@ class SMESEngine:
         self.forward_a()
         self.forward_b(with_loss=with_loss)
 
-    def forward_a(self):
+    def forward_a(self, frozen: bool = False):
         """Router GEMM -> routing -> plan -> expert GEMMs.  Ends with the per-expert
         LoadStats sums in ``stats_raw`` (the data-parallel exchange point)."""
         s = self._stream()
@@ -246,7 +254,7 @@ class SMESEngine:
         # router logits z = h W_r^T + b_r  (B, T*E) fp32
         _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), d, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
              ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
-        self.route(s)
+        self.route(s, frozen=frozen)
         _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
              ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), s)
@@ -262,19 +270,19 @@ class SMESEngine:
         self.stats_finalize(s, batch_times_tasks)
         _tagged("combine_fwd", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
-             ptr(self.head_b), ptr(self.reps), ptr(self.logits), ptr(self.preds),
+             ptr(self.head_b), ptr(self.P), self.ldp, ptr(self.reps), ptr(self.logits), ptr(self.preds),
              ptr(self.labels) if with_loss else None, ptr(self.lam), ptr(self.loss_part) if with_loss else None,
              self.grid, s)
         if with_loss:
             _tagged("loss_finalize", "smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
                  self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
 
-    def route(self, s, probs_in=None, probs_out=None):
+    def route(self, s, probs_in=None, probs_out=None, frozen=False):
         T, E, B = self.T, self.E, self.B
         _tagged("route", "smes_route_batch", ptr(self.z), E, T * E, ptr(probs_in), ptr(self.tw), T, B, E, self.ks, self.ka,
              self.rpw, ptr(self.shared), ptr(self.adaptive), ptr(self.active), ptr(self.wsel), ptr(self.umask),
              ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
-             ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), s)
+             ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), int(frozen), s)
 
     def experts_forward(self, s):
         R = self.rows_cap
@@ -284,6 +292,9 @@ class SMESEngine:
                  self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act], ptr(self.bits[i]), None, R,
                  ptr(self.outs[i]), self.dims[i + 1], 0, R, s)
             inp = self.outs[i]
+        # head projections of every packed row: P = O head_W^T (tcgen05 GEMM, N = T)
+        _tagged("head_proj", "smes_gemm_ragged_m", ptr(self.outs[-1]), self.d_out, R, ptr(self.head_w_bf), 1, self.T,
+                self.d_out, 0, ptr(self.totals), None, 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
 
     def stats_finalize(self, s, batch_times_tasks: float | None = None):
         bt = float(self.B * self.T) if batch_times_tasks is None else batch_times_tasks
@@ -302,7 +313,9 @@ class SMESEngine:
         relu_last = int(self.p.layers[-1].act == "relu")
         _tagged("combine_bwd", "smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
-             ptr(self.preds), ptr(self.labels), ptr(self.lam), 1.0 / bs, relu_last, ptr(self.d_outs[-1]),
+             ptr(self.P), self.ldp, ptr(self.reps), ptr(self.preds), ptr(self.labels), ptr(self.lam), 1.0 / bs,
+             relu_last,
+             ptr(self.d_outs[-1]),
              ptr(self.dz), ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw),
              ptr(self.part_db), self.grid, s)
         n_layers = len(self.p.layers)
@@ -322,8 +335,10 @@ class SMESEngine:
         # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
         _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
              ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
-        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), d, B, 1, T * E, d, ptr(self.seg_router),
-             ptr(self.g_router_w), s)
+        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), d, B, self.rw_splits, T * E, d,
+                ptr(self.seg_router_split), ptr(self.rw_part), s)
+        _tagged("router_wgrad", "smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d,
+                ptr(self.g_router_w), s)
         _tagged("router_bias", "smes_seg_colsum", ptr(self.dz), T * E, self.B_pad, T * E, ptr(self.seg_router), 1,
              ptr(self.colsum_part), ptr(self.g_router_b), s)
         _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
@@ -343,6 +358,7 @@ class SMESEngine:
         w = {"router_fwd": (2.0 * B * d * T * E, B * (d * 2 + T * E * 4), "tensor"),
              "router_dgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 4), "tensor"),
              "router_wgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 2), "tensor"),
+             "head_proj": (2.0 * n_act * do * T, n_act * (do * 2 + T * 4), "hbm"),
              "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4), "hbm"),
              "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8, "hbm"),
              "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12), "hbm"),
@@ -374,7 +390,7 @@ class SMESEngine:
     # ------------------------------------------------------------------ views
     def n_act(self) -> int:
         """Logical packed rows (reads the device counter: a host sync)."""
-        return int(self.totals[0].item())
+        return int(self.totals[2].item())
 
     def gradients(self) -> dict:
         """Gradient blocks with the reference's names (model.py:94-111), single-pool
