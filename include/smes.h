@@ -73,13 +73,15 @@ int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* um
  *      ragged-M: C[m,n] = act(sum_k A[m,k] W_g[n,k] + bias_g[n])   (b_mn = 0, fwd)
  *                C[m,n] = mask(sum_k A[m,k] W_g[k,n])              (b_mn = 1, dgrad)
  *      ragged-K: C_g[i,j] = sum_{m in g} P[m,i] Q[m,j]           (wgrad, fp32 out)
+ *                db_g[i]  = sum_{m in g} P[m,i]   when db_out != NULL: Q must carry a column of
+ *                ones at index J (ldq >= J+64); one extra N=64 tile computes the bias grad.
  *      seg = padded group offsets (device). */
 int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, int G, int N, int K, int b_mn,
                        const int* seg, const float* bias, int act, uint32_t* relu_bits_out,
                        const uint32_t* relu_bits_in, long bits_ld, void* C, long ldc, int out_fp32,
                        long m_limit, void* stream);
 int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
-                       const int* seg, float* C, void* stream);
+                       const int* seg, float* C, float* db_out, void* stream);
 
 /* ---- K4 combine + heads + BCE: replaces reconstruct_task_reps (execution.py:161-191),
  *      _heads (model.py:202-208) and _weighted_bce (training.py:54-57). */
@@ -97,6 +99,15 @@ int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint
                      const float* labels, const float* lam, float inv_b, int relu_last, void* dpacked, void* dz,
                      const float* freq, float lb_coef, int dense_probs, const float* z, float* part_dw,
                      float* part_db, int grid, void* stream);
+
+/* ---- K4+K6+K7 fused for a training step (sparse LB reading): the forward combine + heads + BCE
+ *      also emits dlogit, d_packed, dz and the head-grad partials while the rows are on chip. */
+int smes_combine_train(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
+                       const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
+                       const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits,
+                       float* preds, const float* labels, const float* lam, double* loss_part, float inv_b,
+                       int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, float* part_dw,
+                       float* part_db, int grid, void* stream);
 
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,

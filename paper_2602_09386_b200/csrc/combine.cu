@@ -34,22 +34,22 @@ __device__ __forceinline__ int union_rank(const uint32_t* um, int e) {
   return r + __popc(um[e >> 5] & ((1u << (e & 31)) - 1u));
 }
 
+// bf16 row slice -> fp32 registers (generic load: used on the shared-memory row stages)
 template <int VPL>
 __device__ __forceinline__ void load_bf(const __nv_bfloat16* p, float (&x)[VPL]) {
+  if constexpr (VPL == 4) {
+    const uint2 v = *reinterpret_cast<const uint2*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
-  for (int i = 0; i < VPL; i += 8) {
-    if constexpr (VPL >= 8) {
-      uint4 v = __ldg(reinterpret_cast<const uint4*>(p + i));
+    for (int j = 0; j < 2; ++j) { float2 f = __bfloat1622float2(h[j]); x[2 * j] = f.x; x[2 * j + 1] = f.y; }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VPL; i += 8) {
+      const uint4 v = *reinterpret_cast<const uint4*>(p + i);
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
       for (int j = 0; j < 4; ++j) { float2 f = __bfloat1622float2(h[j]); x[i + 2 * j] = f.x; x[i + 2 * j + 1] = f.y; }
     }
-  }
-  if constexpr (VPL == 4) {
-    uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-    for (int j = 0; j < 2; ++j) { float2 f = __bfloat1622float2(h[j]); x[2 * j] = f.x; x[2 * j + 1] = f.y; }
   }
 }
 template <int VPL>
@@ -131,13 +131,26 @@ struct CombineArgs {
   float* part_db;          // (grid, T)
 };
 
-// shared-memory layout per instance group
-template <int MAXT>
-struct GroupSmem {
-  uint32_t um[32];
-  int32_t rows[CB_MAX_U];
-  float wt[CB_MAX_U * MAXT];
-  float dl[MAXT];
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+}
+
+// Per-instance-group shared memory (sized at run time by umax):
+//   um[32] | rows[umax] | wt[umax][MAXT] | dl[MAXT] | P stage [umax][ldp] | row stage [nrow][d_out] bf16
+struct GroupLayout {
+  int off_rows, off_wt, off_dl, off_p, off_stage, bytes;
+  __host__ __device__ GroupLayout(int umax, int maxt, int ldp, int stage_rows, int d_out) {
+    auto al = [](int x) { return (x + 15) & ~15; };
+    off_rows = 128;
+    off_wt = al(off_rows + umax * 4);
+    off_dl = al(off_wt + umax * maxt * 4);
+    off_p = al(off_dl + maxt * 4);
+    off_stage = al(off_p + umax * ldp * 4);
+    bytes = al(off_stage + stage_rows * d_out * 2);
+  }
 };
 
 template <int VPL, int MAXT>
@@ -147,14 +160,22 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
   const int G = CB_WARPS / S;                 // instances per CTA iteration
   const int gi = warp / S, ws = warp % S;
   const int col = (ws * 32 + lane) * VPL;
-  const int T = a.T, K = a.K, EW = (a.E + 31) >> 5;
+  const int T = a.T, K = a.K, EW = (a.E + 31) >> 5, umax = a.umax;
   const int ldp = a.ldp;
+  const bool has_p = a.P != nullptr;
   extern __shared__ __align__(16) uint8_t smraw[];
-  GroupSmem<MAXT>* gs = reinterpret_cast<GroupSmem<MAXT>*>(smraw) + gi;
+  const GroupLayout L(umax, MAXT, ldp, umax, a.d_out);
+  uint8_t* g0 = smraw + (size_t)gi * L.bytes;
+  uint32_t* s_um = reinterpret_cast<uint32_t*>(g0);
+  int32_t* s_rows = reinterpret_cast<int32_t*>(g0 + L.off_rows);
+  float* s_wt = reinterpret_cast<float*>(g0 + L.off_wt);
+  float* s_p = reinterpret_cast<float*>(g0 + L.off_p);
+  __nv_bfloat16* s_o = reinterpret_cast<__nv_bfloat16*>(g0 + L.off_stage);
   const int gthreads = S * 32, gtid = ws * 32 + lane;
-  // logits: lane -> (task t, u-residue ug); MAXT <= 32
   const int lt = lane & (MAXT - 1), ug = lane / MAXT;
   constexpr int NG = 32 / MAXT;
+  const int cpr = a.d_out / 8;                 // 16-byte chunks per O row
+  const int pcr = ldp / 4;                     // 16-byte chunks per P row
   double my_loss = 0.0;
   const int iters = (a.B + (long)gridDim.x * G - 1) / ((long)gridDim.x * G);
   for (int it = 0; it < iters; ++it) {
@@ -162,17 +183,28 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
     const bool valid = b < a.B;
     const int U = valid ? a.usize[b] : 0;
     if (valid) {
-      for (int j = gtid; j < EW; j += gthreads) gs->um[j] = a.umask[(long)b * EW + j];
-      for (int u = gtid; u < U; u += gthreads) gs->rows[u] = a.row_of[(long)b * a.umax + u];
-      for (int i = gtid; i < U * MAXT; i += gthreads) gs->wt[i] = 0.f;
+      for (int j = gtid; j < EW; j += gthreads) s_um[j] = a.umask[(long)b * EW + j];
+      for (int u = gtid; u < U; u += gthreads) s_rows[u] = a.row_of[(long)b * a.umax + u];
+      for (int i = gtid; i < U * MAXT; i += gthreads) s_wt[i] = 0.f;
     }
     __syncthreads();
     if (valid) {
+      // gather every packed row of the instance (and its head projections) into smem at once
+      for (int i = gtid; i < U * cpr; i += gthreads) {
+        const int u = i / cpr, c = i - u * cpr;
+        cp_async16(s_o + (long)u * a.d_out + c * 8, a.O + (long)s_rows[u] * a.ldo + c * 8);
+      }
+      if (has_p)
+        for (int i = gtid; i < U * pcr; i += gthreads) {
+          const int u = i / pcr, c = i - u * pcr;
+          cp_async16(s_p + (long)u * ldp + c * 4, a.P + (long)s_rows[u] * ldp + c * 4);
+        }
       for (int i = gtid; i < T * K; i += gthreads) {
         const int t = i / K;
         const long o = ((long)t * a.B + b) * K + (i - t * K);
-        gs->wt[union_rank(gs->um, a.active[o]) * MAXT + t] = a.wsel[o];
+        s_wt[union_rank(s_um, a.active[o]) * MAXT + t] = a.wsel[o];
       }
+      cp_async_wait_all();
     }
     __syncthreads();
     if (valid) {
@@ -184,10 +216,10 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
         for (int v = 0; v < VPL; ++v) acc[t][v] = 0.f;
       for (int u = 0; u < U; ++u) {
         float x[VPL];
-        load_bf<VPL>(a.O + (long)gs->rows[u] * a.ldo + col, x);
+        load_bf<VPL>(s_o + (long)u * a.d_out + col, x);
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
-          const float w = gs->wt[u * MAXT + t];
+          const float w = s_wt[u * MAXT + t];
 #pragma unroll
           for (int v = 0; v < VPL; ++v) acc[t][v] = fmaf(w, x[v], acc[t][v]);
         }
@@ -196,10 +228,10 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
       for (int t = 0; t < MAXT; ++t)
         if (t < T) store_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, acc[t]);
       // logit_t = b_t + sum_u w[u,t] P[u,t]   (P = O head_W^T from the tensor-core GEMM)
-      if (ws == 0 && a.P != nullptr) {
+      if (ws == 0 && has_p) {
         float sacc = 0.f;
         if (lt < T)
-          for (int u = ug; u < U; u += NG) sacc = fmaf(gs->wt[u * MAXT + lt], __ldg(a.P + (long)gs->rows[u] * ldp + lt), sacc);
+          for (int u = ug; u < U; u += NG) sacc = fmaf(s_wt[u * MAXT + lt], s_p[u * ldp + lt], sacc);
 #pragma unroll
         for (int o = 16; o >= MAXT; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
         if (ug == 0 && lt < T) {
@@ -233,6 +265,219 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
   }
 }
 
+// Training-step combine: forward (reps, logits, preds, loss) AND the backward terms of
+// training.py:146-179 + balance.py:83-99 (sparse reading) in one pass -- labels and the
+// global selection frequency are known when the forward combine runs, so dlogit,
+// d_packed, dz and the head-grad partials are produced while reps are still in
+// registers and the packed rows / head projections are still staged in smem.
+template <int VPL, int MAXT>
+__global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const CombineArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.d_out / (32 * VPL);
+  const int G = CB_WARPS / S;
+  const int gi = warp / S, ws = warp % S;
+  const int col = (ws * 32 + lane) * VPL;
+  const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E, TK = T * K, umax = a.umax;
+  const int ldp = a.ldp;
+  const int n = T * a.d_out;
+  extern __shared__ __align__(16) uint8_t smraw[];
+  const GroupLayout L(umax, MAXT, ldp, umax, a.d_out);
+  float* s_hw = reinterpret_cast<float*>(smraw);                       // [T][d_out]
+  int32_t* s_act_all = reinterpret_cast<int32_t*>(s_hw + n);           // [G][T*K]
+  float* s_w_all = reinterpret_cast<float*>(s_act_all + (size_t)G * TK);
+  float* s_gw_all = s_w_all + (size_t)G * TK;
+  float* s_wf_all = s_gw_all + (size_t)G * TK;
+  uint8_t* g0 = reinterpret_cast<uint8_t*>(s_wf_all + (size_t)G * TK);
+  g0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g0) + 15) & ~uintptr_t(15)) + (size_t)gi * L.bytes;
+  int32_t* s_act = s_act_all + (size_t)gi * TK;
+  float* s_w = s_w_all + (size_t)gi * TK;
+  float* s_gw = s_gw_all + (size_t)gi * TK;
+  float* s_wf = s_wf_all + (size_t)gi * TK;
+  uint32_t* s_um = reinterpret_cast<uint32_t*>(g0);
+  int32_t* s_rows = reinterpret_cast<int32_t*>(g0 + L.off_rows);
+  float* s_wt = reinterpret_cast<float*>(g0 + L.off_wt);
+  float* s_dl = reinterpret_cast<float*>(g0 + L.off_dl);
+  float* s_p = reinterpret_cast<float*>(g0 + L.off_p);
+  __nv_bfloat16* s_o = reinterpret_cast<__nv_bfloat16*>(g0 + L.off_stage);
+  for (int i = threadIdx.x; i < n; i += CB_THREADS) s_hw[i] = a.head_w[i];
+  const int gthreads = S * 32, gtid = ws * 32 + lane;
+  const int lt = lane & (MAXT - 1), ug = lane / MAXT;
+  constexpr int NG = 32 / MAXT;
+  const int cpr = a.d_out / 8, pcr = ldp / 4;
+  float acc_dw[MAXT][VPL];
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) acc_dw[t][v] = 0.f;
+  float my_db = 0.f;
+  double my_loss = 0.0;
+  const int iters = (a.B + (long)gridDim.x * G - 1) / ((long)gridDim.x * G);
+  for (int it = 0; it < iters; ++it) {
+    const int b = (it * gridDim.x + blockIdx.x) * G + gi;
+    const bool valid = b < a.B;
+    const int U = valid ? a.usize[b] : 0;
+    // P1: instance tables
+    if (valid) {
+      for (int j = gtid; j < EW; j += gthreads) s_um[j] = a.umask[(long)b * EW + j];
+      for (int u = gtid; u < U; u += gthreads) s_rows[u] = a.row_of[(long)b * a.umax + u];
+      for (int i = gtid; i < U * MAXT; i += gthreads) s_wt[i] = 0.f;
+      for (int i = gtid; i < TK; i += gthreads) {
+        const int t = i / K;
+        const long o = ((long)t * a.B + b) * K + (i - t * K);
+        s_act[i] = a.active[o];
+        s_w[i] = a.wsel[o];
+      }
+    }
+    __syncthreads();
+    // P2: gather rows + projections, build the (union row x task) weight table
+    if (valid) {
+      for (int i = gtid; i < U * cpr; i += gthreads) {
+        const int u = i / cpr, c = i - u * cpr;
+        cp_async16(s_o + (long)u * a.d_out + c * 8, a.O + (long)s_rows[u] * a.ldo + c * 8);
+      }
+      for (int i = gtid; i < U * pcr; i += gthreads) {
+        const int u = i / pcr, c = i - u * pcr;
+        cp_async16(s_p + (long)u * ldp + c * 4, a.P + (long)s_rows[u] * ldp + c * 4);
+      }
+      for (int i = gtid; i < TK; i += gthreads) s_wt[union_rank(s_um, s_act[i]) * MAXT + i / K] = s_w[i];
+      cp_async_wait_all();
+    }
+    __syncthreads();
+    // P3: reps, logits, preds, loss, dlogit
+    float acc[MAXT][VPL];
+#pragma unroll
+    for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) acc[t][v] = 0.f;
+    if (valid) {
+      for (int u = 0; u < U; ++u) {
+        float x[VPL];
+        load_bf<VPL>(s_o + (long)u * a.d_out + col, x);
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          const float w = s_wt[u * MAXT + t];
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) acc[t][v] = fmaf(w, x[v], acc[t][v]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t)
+        if (t < T) store_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, acc[t]);
+      if (ws == 0) {
+        float sacc = 0.f;
+        if (lt < T)
+          for (int u = ug; u < U; u += NG) sacc = fmaf(s_wt[u * MAXT + lt], s_p[u * ldp + lt], sacc);
+#pragma unroll
+        for (int o = 16; o >= MAXT; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
+        if (ug == 0 && lt < T) {
+          const int t = lt;
+          const float lg = sacc + a.head_b[t];
+          const float ez = expf(-fabsf(lg));               // stable sigmoid (linalg.py:108-113)
+          const float pos = 1.f / (1.f + ez);
+          const float pr = lg >= 0.f ? pos : 1.f - pos;
+          a.logits[(long)t * a.B + b] = lg;
+          a.preds[(long)t * a.B + b] = pr;
+          const float y = a.labels[(long)t * a.B + b];
+          double pc = (double)pr;
+          pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
+          my_loss += (double)a.lam[t] * -((double)y * log(pc) + (1.0 - (double)y) * log1p(-pc));
+          const bool inside = pr > 1e-7f && pr < 1.f - 1e-7f;          // training.py:147-148
+          const float dl = inside ? a.lam[t] * a.inv_b * (pr - y) : 0.f;
+          s_dl[t] = dl;
+          my_db += dl;
+        }
+      }
+    }
+    __syncthreads();
+    // P4: d_packed rows, head-grad accumulation, (task, pick) pair terms
+    if (valid) {
+      float dl[MAXT];
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) dl[t] = t < T ? s_dl[t] : 0.f;
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t)
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) acc_dw[t][v] = fmaf(dl[t], acc[t][v], acc_dw[t][v]);
+      for (int u = 0; u < U; ++u) {
+        asm volatile("" ::: "memory");
+        float dp[VPL];
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) dp[v] = 0.f;
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          if (t < T) {
+            const float c = s_wt[u * MAXT + t] * dl[t];
+#pragma unroll
+            for (int v = 0; v < VPL; v += 4) {
+              const float4 h4 = *reinterpret_cast<const float4*>(s_hw + (long)t * a.d_out + col + v);
+              dp[v] = fmaf(c, h4.x, dp[v]);
+              dp[v + 1] = fmaf(c, h4.y, dp[v + 1]);
+              dp[v + 2] = fmaf(c, h4.z, dp[v + 2]);
+              dp[v + 3] = fmaf(c, h4.w, dp[v + 3]);
+            }
+          }
+        }
+        if (a.relu_last) {
+          float x[VPL];
+          load_bf<VPL>(s_o + (long)u * a.d_out + col, x);
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) dp[v] = x[v] > 0.f ? dp[v] : 0.f;
+        }
+        store_bf<VPL>(a.dpacked + (long)s_rows[u] * a.ldo + col, dp);
+      }
+      __nv_bfloat16* dzr = a.dz + (long)b * TE;
+      for (int i = gtid * 8; i < TE; i += gthreads * 8) *reinterpret_cast<uint4*>(dzr + i) = make_uint4(0, 0, 0, 0);
+      for (int i = gtid; i < TK; i += gthreads) {
+        const int t = i / K, e = s_act[i];
+        const float w = s_w[i];
+        s_gw[i] = s_dl[t] * s_p[union_rank(s_um, e) * ldp + t] * w;   // g_k w_k
+        s_wf[i] = w * __ldg(a.freq + e);                                // w_k f_k
+      }
+    }
+    __syncthreads();
+    // P5: dz = w (g - sum_j g_j w_j) + beta coef w (f - sum_j w_j f_j)   (sparse reading)
+    if (valid) {
+      __nv_bfloat16* dzr = a.dz + (long)b * TE;
+      for (int i = gtid; i < TK; i += gthreads) {
+        const int t = i / K;
+        float Gt = 0.f, Ft = 0.f;
+        for (int k = 0; k < K; ++k) { Gt += s_gw[t * K + k]; Ft += s_wf[t * K + k]; }
+        const float w = s_w[i];
+        dzr[t * E + s_act[i]] = __float2bfloat16_rn((s_gw[i] - w * Gt) + a.lb_coef * (s_wf[i] - w * Ft));
+      }
+    }
+    __syncthreads();
+  }
+  // per-CTA partials: head grads (groups summed in fixed order) and the loss
+  float* s_red = reinterpret_cast<float*>(smraw);
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+    if (t < T)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) s_red[(long)gi * n + (long)t * a.d_out + col + v] = acc_dw[t][v];
+  float* s_db = s_red + (long)G * n;
+  if (ws == 0 && ug == 0 && lt < T) s_db[gi * MAXT + lt] = my_db;
+  double* s_l = reinterpret_cast<double*>(s_db + G * MAXT + 2);
+  s_l = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_l) + 7) & ~uintptr_t(7));
+  s_l[threadIdx.x] = my_loss;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += CB_THREADS) {
+    float sum = 0.f;
+    for (int g = 0; g < G; ++g) sum += s_red[(long)g * n + i];
+    a.part_dw[(long)blockIdx.x * n + i] = sum;
+  }
+  if (threadIdx.x < T) {
+    float sum = 0.f;
+    for (int g = 0; g < G; ++g) sum += s_db[g * MAXT + threadIdx.x];
+    a.part_db[(long)blockIdx.x * T + threadIdx.x] = sum;
+  }
+  if (threadIdx.x == 0 && a.loss_part) {
+    double sum = 0.0;
+    for (int i = 0; i < CB_THREADS; ++i) sum += s_l[i];
+    a.loss_part[blockIdx.x] = sum;
+  }
+}
+
 template <int VPL, int MAXT>
 __global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -240,103 +485,132 @@ __global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineAr
   const int G = CB_WARPS / S;
   const int gi = warp / S, ws = warp % S;
   const int col = (ws * 32 + lane) * VPL;
-  const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E, TK = T * K;
+  const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E, TK = T * K, umax = a.umax;
   const int ldp = a.ldp;
   const int n = T * a.d_out;
   extern __shared__ __align__(16) uint8_t smraw[];
-  GroupSmem<MAXT>* gs = reinterpret_cast<GroupSmem<MAXT>*>(smraw) + gi;
-  float* s_dw = reinterpret_cast<float*>(reinterpret_cast<GroupSmem<MAXT>*>(smraw) + G);   // [G][T*d_out]
-  float* s_pair = s_dw + (long)G * n;                                                     // [G][2][T*K]
-  float* my_dw = s_dw + (long)gi * n;
+  const int stage_rows = T + (a.relu_last ? umax : 0);
+  const GroupLayout L(umax, MAXT, ldp, stage_rows, a.d_out);
+  float* s_hw = reinterpret_cast<float*>(smraw);                                   // [T][d_out]
+  float* s_pair = s_hw + n;                                                        // [G][2][T*K]
+  uint8_t* g0 = reinterpret_cast<uint8_t*>(s_pair + (size_t)G * 2 * TK) + 0;
+  g0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g0) + 15) & ~uintptr_t(15)) + (size_t)gi * L.bytes;
+  uint32_t* s_um = reinterpret_cast<uint32_t*>(g0);
+  int32_t* s_rows = reinterpret_cast<int32_t*>(g0 + L.off_rows);
+  float* s_wt = reinterpret_cast<float*>(g0 + L.off_wt);
+  float* s_dl = reinterpret_cast<float*>(g0 + L.off_dl);
+  float* s_p = reinterpret_cast<float*>(g0 + L.off_p);
+  __nv_bfloat16* s_reps = reinterpret_cast<__nv_bfloat16*>(g0 + L.off_stage);      // [T][d_out]
+  __nv_bfloat16* s_o = s_reps + (size_t)T * a.d_out;                                // [umax][d_out] (relu_last)
   float* gw_s = s_pair + (long)gi * 2 * TK;
   float* wf_s = gw_s + TK;
-  for (int i = threadIdx.x; i < G * n; i += CB_THREADS) s_dw[i] = 0.f;
-  float hw[MAXT][VPL];
+  for (int i = threadIdx.x; i < n; i += CB_THREADS) s_hw[i] = a.head_w[i];
+  float acc_dw[MAXT][VPL];
 #pragma unroll
-  for (int t = 0; t < MAXT; ++t) {
-    if (t < T) load_f32<VPL>(a.head_w + (long)t * a.d_out + col, hw[t]);
-    else {
+  for (int t = 0; t < MAXT; ++t)
 #pragma unroll
-      for (int v = 0; v < VPL; ++v) hw[t][v] = 0.f;
-    }
-  }
+    for (int v = 0; v < VPL; ++v) acc_dw[t][v] = 0.f;
   float my_db = 0.f;
   const int gthreads = S * 32, gtid = ws * 32 + lane;
+  const int cpr = a.d_out / 8, pcr = ldp / 4;
   const int iters = (a.B + (long)gridDim.x * G - 1) / ((long)gridDim.x * G);
   for (int it = 0; it < iters; ++it) {
     const int b = (it * gridDim.x + blockIdx.x) * G + gi;
     const bool valid = b < a.B;
     const int U = valid ? a.usize[b] : 0;
     if (valid) {
-      for (int j = gtid; j < EW; j += gthreads) gs->um[j] = a.umask[(long)b * EW + j];
-      for (int u = gtid; u < U; u += gthreads) gs->rows[u] = a.row_of[(long)b * a.umax + u];
-      for (int i = gtid; i < U * MAXT; i += gthreads) gs->wt[i] = 0.f;
+      for (int j = gtid; j < EW; j += gthreads) s_um[j] = a.umask[(long)b * EW + j];
+      for (int u = gtid; u < U; u += gthreads) s_rows[u] = a.row_of[(long)b * a.umax + u];
+      for (int i = gtid; i < U * MAXT; i += gthreads) s_wt[i] = 0.f;
       if (gtid < T) {
         const int t = gtid;
         const float p = a.preds[(long)t * a.B + b], y = a.labels[(long)t * a.B + b];
         const bool inside = p > 1e-7f && p < 1.f - 1e-7f;
         const float dl = inside ? a.lam[t] * a.inv_b * (p - y) : 0.f;
-        gs->dl[t] = dl;
+        s_dl[t] = dl;
         my_db += dl;
+      }
+      for (int i = gtid; i < T * cpr; i += gthreads) {
+        const int t = i / cpr, c = i - t * cpr;
+        cp_async16(s_reps + (long)t * a.d_out + c * 8, a.reps + ((long)t * a.B + b) * a.d_out + c * 8);
       }
     }
     __syncthreads();
     if (valid) {
+      for (int i = gtid; i < U * pcr; i += gthreads) {
+        const int u = i / pcr, c = i - u * pcr;
+        cp_async16(s_p + (long)u * ldp + c * 4, a.P + (long)s_rows[u] * ldp + c * 4);
+      }
+      if (a.relu_last)
+        for (int i = gtid; i < U * cpr; i += gthreads) {
+          const int u = i / cpr, c = i - u * cpr;
+          cp_async16(s_o + (long)u * a.d_out + c * 8, a.O + (long)s_rows[u] * a.ldo + c * 8);
+        }
       for (int i = gtid; i < TK; i += gthreads) {
         const int t = i / K;
         const long o = ((long)t * a.B + b) * K + (i - t * K);
-        gs->wt[union_rank(gs->um, a.active[o]) * MAXT + t] = a.wsel[o];
+        s_wt[union_rank(s_um, a.active[o]) * MAXT + t] = a.wsel[o];
       }
+      cp_async_wait_all();
     }
     __syncthreads();
     if (valid) {
       float dl[MAXT];
 #pragma unroll
-      for (int t = 0; t < MAXT; ++t) dl[t] = t < T ? gs->dl[t] : 0.f;
-      // d_packed[u] = sum_t w[u,t] dlogit_t head_w_t
+      for (int t = 0; t < MAXT; ++t) dl[t] = t < T ? s_dl[t] : 0.f;
+      // d_packed[u] = sum_t w[u,t] dlogit_t head_w_t   (x relu mask of O if the last pool is relu)
       for (int u = 0; u < U; ++u) {
-        const long r = gs->rows[u];
+        asm volatile("" ::: "memory");   // keep head_w in smem (do not hoist T*VPL values into registers)
+        const long r = s_rows[u];
         float dp[VPL];
 #pragma unroll
         for (int v = 0; v < VPL; ++v) dp[v] = 0.f;
 #pragma unroll
         for (int t = 0; t < MAXT; ++t) {
-          const float c = gs->wt[u * MAXT + t] * dl[t];
+          if (t < T) {
+            const float c = s_wt[u * MAXT + t] * dl[t];
+            float hw[VPL];
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) dp[v] = fmaf(c, hw[t][v], dp[v]);
+            for (int v = 0; v < VPL; v += 4) {
+              const float4 h4 = *reinterpret_cast<const float4*>(s_hw + (long)t * a.d_out + col + v);
+              hw[v] = h4.x; hw[v + 1] = h4.y; hw[v + 2] = h4.z; hw[v + 3] = h4.w;
+            }
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) dp[v] = fmaf(c, hw[v], dp[v]);
+          }
         }
         if (a.relu_last) {
           float x[VPL];
-          load_bf<VPL>(a.O + r * a.ldo + col, x);
+          load_bf<VPL>(s_o + (long)u * a.d_out + col, x);
 #pragma unroll
           for (int v = 0; v < VPL; ++v) dp[v] = x[v] > 0.f ? dp[v] : 0.f;
         }
         store_bf<VPL>(a.dpacked + r * a.ldo + col, dp);
       }
-      // dW_head_t += dlogit_t * reps_t  (group-private smem accumulator, lane-owned columns)
+      // dW_head_t += dlogit_t * reps_t
 #pragma unroll
       for (int t = 0; t < MAXT; ++t) {
         if (t < T) {
           float x[VPL];
-          load_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, x);
-          float* dst = my_dw + (long)t * a.d_out + col;
+          load_bf<VPL>(s_reps + (long)t * a.d_out + col, x);
 #pragma unroll
-          for (int v = 0; v < VPL; ++v) dst[v] = fmaf(dl[t], x[v], dst[v]);
+          for (int v = 0; v < VPL; ++v) acc_dw[t][v] = fmaf(dl[t], x[v], acc_dw[t][v]);
         }
       }
       // router-logit gradient over the (task, pick) pairs (softmax over the active set only)
       if (ws == 0) {
         __nv_bfloat16* dzr = a.dz + (long)b * TE;
         for (int i = lane * 8; i < TE; i += 256) *reinterpret_cast<uint4*>(dzr + i) = make_uint4(0, 0, 0, 0);
+        __syncwarp();
         if (!a.dense_probs) {
           for (int i = lane; i < TK; i += 32) {
             const int t = i / K;
             const long o = ((long)t * a.B + b) * K + (i - t * K);
             const int e = a.active[o];
             const float w = a.wsel[o];
-            const float p = __ldg(a.P + (long)gs->rows[union_rank(gs->um, e)] * ldp + t);
-            gw_s[i] = gs->dl[t] * p * w;          // g_k w_k
-            wf_s[i] = w * __ldg(a.freq + e);      // w_k f_k
+            const float p = s_p[union_rank(s_um, e) * ldp + t];
+            gw_s[i] = s_dl[t] * p * w;             // g_k w_k
+            wf_s[i] = w * __ldg(a.freq + e);       // w_k f_k
           }
           __syncwarp();
           for (int i = lane; i < TK; i += 32) {
@@ -356,7 +630,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineAr
           float G2 = 0.f;
           for (int k = 0; k < K; ++k) {
             const int e = a.active[ob + k];
-            G2 += gs->dl[t] * a.P[(long)gs->rows[union_rank(gs->um, e)] * ldp + t] * a.wsel[ob + k];
+            G2 += s_dl[t] * s_p[union_rank(s_um, e) * ldp + t] * a.wsel[ob + k];
           }
           const float* zr = a.z + (long)b * TE + (long)t * E;
           float mx = -INFINITY;
@@ -369,7 +643,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineAr
           for (int k = 0; k < K; ++k) {
             const int e = a.active[ob + k];
             const float w = a.wsel[ob + k];
-            const float g = gs->dl[t] * a.P[(long)gs->rows[union_rank(gs->um, e)] * ldp + t];
+            const float g = s_dl[t] * s_p[union_rank(s_um, e) * ldp + t];
             dzt[e] = __float2bfloat16_rn(w * (g - G2) + __bfloat162float(dzt[e]));
           }
         }
@@ -377,13 +651,20 @@ __global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineAr
     }
     __syncthreads();
   }
-  // per-CTA head-grad partials: sum the G groups in fixed order
-  float* s_db = s_pair;    // reuse (G * MAXT floats)
+  // per-CTA head-grad partials: the G groups summed in fixed order through smem
+  float* s_red = reinterpret_cast<float*>(smraw);          // reuse: [G][T*d_out] (fits, see combine_smem)
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < MAXT; ++t)
+    if (t < T)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) s_red[(long)gi * n + (long)t * a.d_out + col + v] = acc_dw[t][v];
+  float* s_db = s_red + (long)G * n;
   if (gtid < T) s_db[gi * MAXT + gtid] = my_db;
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += CB_THREADS) {
     float s = 0.f;
-    for (int g = 0; g < G; ++g) s += s_dw[(long)g * n + i];
+    for (int g = 0; g < G; ++g) s += s_red[(long)g * n + i];
     a.part_dw[(long)blockIdx.x * n + i] = s;
   }
   if (threadIdx.x < T) {
@@ -400,7 +681,7 @@ using namespace smes;
 static int pick_vpl(int T, int d_out) {
   // VPL columns per thread, S = d_out / (32 VPL) warps per instance (1, 2, 4 or 8)
   int mt = T <= 4 ? 4 : T <= 8 ? 8 : T <= 16 ? 16 : 32;
-  int vpl = mt <= 8 ? 8 : 4;
+  int vpl = mt <= 4 ? 8 : 4;      // keep MAXT*VPL <= 32 accumulators per thread (occupancy)
   while (vpl > 4 && d_out / (32 * vpl) < 1) vpl /= 2;
   if (d_out % (32 * vpl)) return -1;
   int s = d_out / (32 * vpl);
@@ -408,36 +689,46 @@ static int pick_vpl(int T, int d_out) {
   return vpl;
 }
 
-static size_t combine_smem(bool bwd, int T, int K, int d_out, int vpl, int mt) {
+static size_t combine_smem(bool bwd, int T, int K, int d_out, int vpl, int mt, int umax, int ldp, int relu_last) {
   const int S = d_out / (32 * vpl), G = CB_WARPS / S;
-  size_t groups = 0;
-  switch (mt) {
-    case 4: groups = sizeof(GroupSmem<4>); break;
-    case 8: groups = sizeof(GroupSmem<8>); break;
-    case 16: groups = sizeof(GroupSmem<16>); break;
-    default: groups = sizeof(GroupSmem<32>); break;
+  size_t s;
+  if (!bwd) {
+    GroupLayout L(umax, mt, ldp, umax, d_out);
+    s = (size_t)G * L.bytes;
+    size_t tail = (size_t)CB_THREADS * 8;
+    return s > tail ? s : tail;
   }
-  size_t s = groups * G;
-  if (bwd) s += (size_t)G * T * d_out * 4 + (size_t)G * (2 * T * K > mt ? 2 * T * K : mt) * 4;
-  size_t tail = (size_t)CB_THREADS * 8;
+  GroupLayout L(umax, mt, ldp, T + (relu_last ? umax : 0), d_out);
+  s = (size_t)T * d_out * 4 + (size_t)G * 2 * T * K * 4 + 16 + (size_t)G * L.bytes;
+  size_t tail = (size_t)G * T * d_out * 4 + (size_t)G * mt * 4;
   return s > tail ? s : tail;
 }
 
-static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream) {
+static size_t combine_train_smem(int T, int K, int d_out, int vpl, int mt, int umax, int ldp) {
+  const int S = d_out / (32 * vpl), G = CB_WARPS / S;
+  GroupLayout L(umax, mt, ldp, umax, d_out);
+  size_t s = (size_t)T * d_out * 4 + (size_t)G * 4 * T * K * 4 + 16 + (size_t)G * L.bytes;
+  size_t tail = (size_t)G * T * d_out * 4 + (size_t)G * mt * 4 + 16 + (size_t)CB_THREADS * 8;
+  return s > tail ? s : tail;
+}
+
+static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream, bool train = false) {
   if (a.T > CB_MAX_T) return set_error(SMES_ERR_SHAPE, "combine: T=%d exceeds %d", a.T, CB_MAX_T);
   if (a.umax > CB_MAX_U) return set_error(SMES_ERR_SHAPE, "combine: union bound %d exceeds %d", a.umax, CB_MAX_U);
   if (a.E > 1024) return set_error(SMES_ERR_SHAPE, "combine: E=%d exceeds 1024", a.E);
   const int vpl = pick_vpl(a.T, a.d_out);
   if (vpl < 0) return set_error(SMES_ERR_SHAPE, "combine: unsupported d_out=%d for T=%d", a.d_out, a.T);
   if (bwd && ((a.T * a.E) % 8)) return set_error(SMES_ERR_SHAPE, "combine_bwd: T*E must be a multiple of 8");
+  if (a.ldp % 4) return set_error(SMES_ERR_SHAPE, "combine: P row stride %d must be a multiple of 4", a.ldp);
   if (a.T * a.K > CB_MAX_TK) return set_error(SMES_ERR_SHAPE, "combine: T*K=%d exceeds %d", a.T * a.K, CB_MAX_TK);
   const int mt = a.T <= 4 ? 4 : a.T <= 8 ? 8 : a.T <= 16 ? 16 : 32;
-  const size_t smem = combine_smem(bwd, a.T, a.K, a.d_out, vpl, mt);
+  const size_t smem = train ? combine_train_smem(a.T, a.K, a.d_out, vpl, mt, a.umax, a.ldp)
+                            : combine_smem(bwd, a.T, a.K, a.d_out, vpl, mt, a.umax, a.ldp > 0 ? a.ldp : 4, a.relu_last);
   if (smem > 227 * 1024) return set_error(SMES_ERR_SHAPE, "combine: shared memory %zu too large", smem);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 #define CB_CASE(V, M)                                                                                    \
   if (vpl == V && mt == M) {                                                                             \
-    auto kf = bwd ? combine_bwd_kernel<V, M> : combine_fwd_kernel<V, M>;                                 \
+    auto kf = train ? combine_train_kernel<V, M> : bwd ? combine_bwd_kernel<V, M> : combine_fwd_kernel<V, M>; \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     kf<<<grid, CB_THREADS, smem, st>>>(a);                                                               \
   } else
@@ -474,6 +765,26 @@ int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint
   a.lam = lam; a.loss_part = loss_part;
   if (!reps) return set_error(SMES_ERR_STATE, "combine_fwd: reps buffer is required");
   return combine_launch(false, a, grid, stream);
+}
+
+int smes_combine_train(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
+                       const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
+                       const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits,
+                       float* preds, const float* labels, const float* lam, double* loss_part, float inv_b,
+                       int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, float* part_dw,
+                       float* part_db, int grid, void* stream) {
+  if (!P || !labels || !reps || !dpacked || !dz)
+    return set_error(SMES_ERR_STATE, "combine_train: P, labels, reps, dpacked and dz are required");
+  CombineArgs a{};
+  a.T = T; a.B = B; a.E = E; a.K = K; a.d_out = d_out; a.umax = umax;
+  a.umask = umask; a.usize = usize; a.row_of = row_of; a.active = active; a.wsel = wsel;
+  a.O = reinterpret_cast<const __nv_bfloat16*>(O); a.ldo = ldo; a.head_w = head_w; a.head_b = head_b;
+  a.P = const_cast<float*>(P); a.ldp = (int)ldp;
+  a.reps = reinterpret_cast<__nv_bfloat16*>(reps); a.logits = logits; a.preds = preds; a.labels = labels;
+  a.lam = lam; a.loss_part = loss_part; a.inv_b = inv_b; a.relu_last = relu_last;
+  a.dpacked = reinterpret_cast<__nv_bfloat16*>(dpacked); a.dz = reinterpret_cast<__nv_bfloat16*>(dz);
+  a.freq = freq; a.lb_coef = lb_coef; a.part_dw = part_dw; a.part_db = part_db;
+  return combine_launch(false, a, grid, stream, true);
 }
 
 int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,

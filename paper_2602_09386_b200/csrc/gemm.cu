@@ -41,6 +41,7 @@ struct GemmArgs {
   const uint32_t* bits_in;    // relu bitmask applied to the output (dgrad), or null
   int bits_ld;
   int out_fp32;
+  float* db_out;              // ragged-K: per-group column sums of P via Q's ones column (G, I), or null
 };
 
 template <int BN>
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     num_tiles = (seg_s[args.G] / BM) * n_tiles;
   } else {
     i_tiles = (args.I + BM - 1) / BM;
-    j_tiles = (args.N + BN - 1) / BN;
+    j_tiles = (args.N + BN - 1) / BN + (args.db_out != nullptr ? 1 : 0);
     num_tiles = args.G * i_tiles * j_tiles;
   }
   // decode: (group, row0 of A / i0, n0 / j0, k-block range)
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int r = tile - g * per;
       r0 = (r / j_tiles) * BM;
       c0 = (r % j_tiles) * BN;
+      if (args.db_out != nullptr && (r % j_tiles) == j_tiles - 1) c0 = args.N;   // bias tile: Q's ones column
       kb0 = seg_s[g] / BK;
       nkb = (seg_s[g + 1] - seg_s[g]) / BK;
     }
@@ -145,7 +147,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode(tile, g, r0, c0, kb0, nkb);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], S::kA + S::kB);
+          const bool tail = (MODE == MODE_RAGGED_K) && args.db_out != nullptr && c0 == args.N;
+          mbar_expect_tx(&full[stage], S::kA + (tail ? 8192 : S::kB));
           uint8_t* a = sA + stage * S::kA;
           uint8_t* b = sB + stage * S::kB;
           const int k0 = (kb0 + kb) * BK;
@@ -162,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, k0);
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
+            for (int j = 0; j < (tail ? 1 : BN / 64); ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -173,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= MMA issuer (single thread)
       constexpr bool A_MN = (MODE == MODE_RAGGED_K);
       constexpr bool BMN = (MODE == MODE_RAGGED_K) || B_MN;
-      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
+      constexpr uint32_t idesc_main = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
+      constexpr uint32_t idesc_tail = umma_idesc_bf16(BM, 64, A_MN ? 1 : 0, BMN ? 1 : 0);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -185,6 +189,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
+        const uint32_t idesc = (MODE == MODE_RAGGED_K && args.db_out != nullptr && c0 == args.N) ? idesc_tail
+                                                                                                : idesc_main;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -223,6 +229,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
       const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
+      if (MODE == MODE_RAGGED_K && args.db_out != nullptr && c0 == args.N) {
+        // bias tile: column 0 of the accumulator is sum_m P[m, i] * 1 = db_g[i]
+        if (par == 0) {
+          uint32_t t0[32];
+          tmem_ld32(tbase, t0);
+          tmem_ld_wait();
+          const int i = r0 + 32 * q + lane;
+          if (i < args.I) args.db_out[(size_t)g * args.I + i] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        continue;
+      }
       for (int cc = par; cc < BN / cpc; cc += 2) {
         const int n = c0 + cc * cpc;
         if (n >= ncols) break;
@@ -426,7 +445,7 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                        str, box)))
       return rc;
   }
-  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, out_fp32};
+  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, out_fp32, nullptr};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool wide = N >= 256;
   if (wide) {
@@ -439,7 +458,7 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
 }
 
 int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
-                       const int* seg, float* C, void* stream) {
+                       const int* seg, float* C, float* db_out, void* stream) {
   if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
   if (I <= 0 || J <= 0) return set_error(SMES_ERR_SHAPE, "empty wgrad I=%d J=%d", I, J);
   if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16 || (I * 2) % 16 || (J * 2) % 16)
@@ -451,8 +470,10 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
     uint32_t box[2] = {64, 64};
     if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, P, dims, str, box))) return rc;
   }
+  if (db_out && ldq < J + 64)
+    return set_error(SMES_ERR_SHAPE, "wgrad bias fusion needs ldq >= J + 64 (ones column at J), ldq=%ld J=%d", ldq, J);
   {
-    uint64_t dims[2] = {(uint64_t)J, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
+    uint64_t dims[2] = {(uint64_t)(db_out ? J + 64 : J), (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
     uint32_t box[2] = {64, 64};
     if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Q, dims, str, box))) return rc;
   }
@@ -462,7 +483,7 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
     uint32_t box[3] = {32, 32, 1};
     if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, str, box))) return rc;
   }
-  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, 1};
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, 1, db_out};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (J >= 256) return launch<256, MODE_RAGGED_K, true>(ta, tb, tc, args, st);
   return launch<128, MODE_RAGGED_K, true>(ta, tb, tc, args, st);

@@ -134,6 +134,7 @@ __global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize
     }
   }
   const int U = usize[b];
+#pragma unroll 4
   for (int u = 0; u < U; ++u) {
     const long r = row_of[(long)b * umax + u];
 #pragma unroll
@@ -161,11 +162,12 @@ __global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize
   }
 }
 
-__global__ void part_reduce_kernel(const float* __restrict__ part, int nparts, int n, float* __restrict__ out) {
-  __shared__ float red[8][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__global__ void __launch_bounds__(1024) part_reduce_kernel(const float* __restrict__ part, int nparts, int n,
+                                                            float* __restrict__ out) {
+  __shared__ float red[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int i = blockIdx.x * 32 + lane;
-  const int per = (nparts + 7) / 8;
+  const int per = (nparts + nw - 1) / nw;
   const int p0 = warp * per, p1 = min(nparts, p0 + per);
   float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   if (i < n) {
@@ -182,7 +184,7 @@ __global__ void part_reduce_kernel(const float* __restrict__ part, int nparts, i
   __syncthreads();
   if (warp == 0 && i < n) {
     float t = 0.f;
-    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    for (int w = 0; w < nw; ++w) t += red[w][lane];
     out[i] = t;
   }
 }
@@ -324,7 +326,7 @@ int smes_bce_loss(int T, int B, const float* pred, const float* labels, const fl
 }
 
 int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream) {
-  part_reduce_kernel<<<(n + 31) / 32, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, nparts, n, out);
+  part_reduce_kernel<<<(n + 31) / 32, nparts >= 256 ? 1024 : 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, nparts, n, out);
   return launch_check("part_reduce");
 }
 

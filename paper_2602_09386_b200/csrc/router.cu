@@ -43,45 +43,58 @@ struct RouteArgs {
   int frozen;              // 1: shared/adaptive are inputs (model.py:284-300), weights/stats recomputed
 };
 
-template <int EPL>
-__device__ __forceinline__ void warp_argmax_f64(const double (&v)[EPL], const uint32_t taken, int lane, int E,
-                                                double& best_v, int& best_i) {
-  best_v = -INFINITY;
-  best_i = 0x7fffffff;
-#pragma unroll
-  for (int j = 0; j < EPL; ++j) {
-    int e = lane + 32 * j;
-    if (e < E && !((taken >> j) & 1u)) {
-      if (v[j] > best_v || (v[j] == best_v && e < best_i)) { best_v = v[j]; best_i = e; }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double ov = __shfl_xor_sync(0xffffffffu, best_v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-    if (ov > best_v || (ov == best_v && oi < best_i)) { best_v = ov; best_i = oi; }
-  }
+// ---- order-preserving keys so warp arg-max runs on the REDUX unit (__reduce_max_sync)
+__device__ __forceinline__ uint32_t fkey(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fkey_inv(uint32_t k) {
+  return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+__device__ __forceinline__ uint64_t dkey(double d) {
+  const uint64_t u = (uint64_t)__double_as_longlong(d);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
 }
 
+// arg-max over the warp of (value desc, expert index asc); lane owns experts lane + 32 j.
+// Candidates with a set bit in `excl` (bit j) or e >= E are ignored.  Returns the expert.
 template <int EPL>
-__device__ __forceinline__ void warp_argmax_f32(const float (&v)[EPL], const uint32_t excl, int lane, int E,
-                                                float& best_v, int& best_i) {
-  best_v = -INFINITY;
-  best_i = 0x7fffffff;
+__device__ __forceinline__ int warp_argmax_key32(const uint32_t (&k)[EPL], uint32_t excl, int lane, int E) {
+  uint32_t bk = 0;
+  int bi = 0x7fffffff;
 #pragma unroll
   for (int j = 0; j < EPL; ++j) {
-    int e = lane + 32 * j;
-    if (e < E && !((excl >> j) & 1u)) {
-      // -inf (masked shared) entries can still be chosen last, like argsort of +inf (routing.py:265)
-      if (best_i == 0x7fffffff || v[j] > best_v || (v[j] == best_v && e < best_i)) { best_v = v[j]; best_i = e; }
-    }
+    const int e = lane + 32 * j;
+    if (e < E && !((excl >> j) & 1u) && k[j] > bk) { bk = k[j]; bi = e; }   // j ascending: ties keep lower e
   }
+  const uint32_t m = __reduce_max_sync(0xffffffffu, bk);
+  return __reduce_min_sync(0xffffffffu, (bk == m) ? bi : 0x7fffffff);
+}
+template <int EPL>
+__device__ __forceinline__ int warp_argmax_key64(const uint64_t (&k)[EPL], uint32_t excl, int lane, int E) {
+  uint64_t bk = 0;
+  int bi = 0x7fffffff;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    float ov = __shfl_xor_sync(0xffffffffu, best_v, o);
-    int oi = __shfl_xor_sync(0xffffffffu, best_i, o);
-    bool ovalid = oi != 0x7fffffff, svalid = best_i != 0x7fffffff;
-    if (ovalid && (!svalid || ov > best_v || (ov == best_v && oi < best_i))) { best_v = ov; best_i = oi; }
+  for (int j = 0; j < EPL; ++j) {
+    const int e = lane + 32 * j;
+    if (e < E && !((excl >> j) & 1u) && k[j] > bk) { bk = k[j]; bi = e; }
+  }
+  const uint32_t hi = (uint32_t)(bk >> 32), lo = (uint32_t)bk;
+  const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+  return __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bi : 0x7fffffff);
+}
+
+// position of each owned expert inside a sorted set given as per-lane bits (bit j: expert lane+32j)
+template <int EPL>
+__device__ __forceinline__ void sorted_positions(uint32_t bits, int lane, int (&pos)[EPL]) {
+  int base = 0;
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    const uint32_t w = __ballot_sync(0xffffffffu, (bits >> j) & 1u);
+    pos[j] = base + __popc(w & lt);
+    base += __popc(w);
   }
 }
 
@@ -91,19 +104,16 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
   const int T = a.T, E = a.E, ks = a.ks, ka = a.ka, K = ks + ka;
   const int EW = (E + 31) >> 5;
   extern __shared__ __align__(16) uint8_t sm[];
-  // per-warp private accumulators [warp][E]
+  // per-warp partials [warp][E]: union count, active count, sparse mass, dense mass
   int32_t* s_union = reinterpret_cast<int32_t*>(sm);
   int32_t* s_act = s_union + RT_WARPS * E;
   double* s_mass = reinterpret_cast<double*>(s_act + RT_WARPS * E + (E & 1) * RT_WARPS);
   double* s_dmass = s_mass + RT_WARPS * E;
-  for (int i = threadIdx.x; i < RT_WARPS * E; i += blockDim.x) {
-    s_union[i] = 0; s_act[i] = 0; s_mass[i] = 0.0; s_dmass[i] = 0.0;
-  }
-  __syncthreads();
-  int32_t* w_union = s_union + warp * E;
-  int32_t* w_act = s_act + warp * E;
-  double* w_mass = s_mass + warp * E;
-  double* w_dmass = s_dmass + warp * E;
+  // lane-owned accumulators over this warp's rows
+  int c_union[EPL], c_act[EPL];
+  double c_mass[EPL], c_dmass[EPL];
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) { c_union[j] = 0; c_act[j] = 0; c_mass[j] = 0.0; c_dmass[j] = 0.0; }
 
   const int chunk_rows = RT_WARPS * a.rows_per_warp;
   const int row0 = blockIdx.x * chunk_rows + warp * a.rows_per_warp;
@@ -111,7 +121,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
   for (int r = 0; r < a.rows_per_warp; ++r) {
     const int b = row0 + r;
     if (b >= a.B) break;
-    // ---------------- load the row's logits (all tasks when T*EPL fits in registers)
+    // ---------------- the row's logits (registers when T * EPL is small)
     float zpre[TP > 0 ? TP : 1][EPL];
     if (TP > 0) {
 #pragma unroll
@@ -119,203 +129,192 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
-          int e = lane + 32 * j;
+          const int e = lane + 32 * j;
           zpre[t][j] = (t < T && e < E) ? __ldg(zr + e) : -INFINITY;
         }
       }
     }
-    // ---------------- Stage I (fp64)
-    double pooled[EPL];
-    double dsum[EPL];
+    auto load_task = [&](int t, float (&zv)[EPL]) {
+      if (TP > 0) {
 #pragma unroll
-    for (int j = 0; j < EPL; ++j) { pooled[j] = 0.0; dsum[j] = 0.0; }
+        for (int tt = 0; tt < (TP > 0 ? TP : 1); ++tt)
+          if (tt == t) {
 #pragma unroll
-    for (int t = 0; t < (TP > 0 ? TP : 1024); ++t) {
-      if (t >= T) break;
-      const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
-      float zv[EPL];
-      float mx = -INFINITY;
-#pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        int e = lane + 32 * j;
-        if (TP > 0) zv[j] = zpre[TP > 0 ? t : 0][j];
-        else zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
-        if (e < E && !isfinite(zv[j])) bad = 1;
-        mx = fmaxf(mx, zv[j]);
-      }
-      const double wt = a.tw[t];
-      double p[EPL];
-      if (a.probs_in == nullptr) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        double s = 0.0;
+            for (int j = 0; j < EPL; ++j) zv[j] = zpre[tt][j];
+          }
+      } else {
+        const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
-          int e = lane + 32 * j;
-          p[j] = e < E ? exp((double)zv[j] - (double)mx) : 0.0;
-          s += p[j];
+          const int e = lane + 32 * j;
+          zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
+        }
+      }
+    };
+    // ---------------- Stage I (fp64): pooled = sum_t w_t softmax(z_t)   (routing.py:256-260)
+    double pooled[EPL];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) pooled[j] = 0.0;
+    for (int t = 0; t < T; ++t) {
+      float zv[EPL];
+      load_task(t, zv);
+      double p[EPL];
+      if (a.probs_in == nullptr) {
+        uint32_t mk = 0;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          const int e = lane + 32 * j;
+          if (e < E) {
+            if (!isfinite(zv[j])) bad = 1;
+            mk = max(mk, fkey(zv[j]));
+          }
+        }
+        const double mx = (double)fkey_inv(__reduce_max_sync(0xffffffffu, mk));
+        double sum = 0.0;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          const int e = lane + 32 * j;
+          p[j] = e < E ? exp((double)zv[j] - mx) : 0.0;
+          sum += p[j];
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const double inv = 1.0 / s;
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
 #pragma unroll
-        for (int j = 0; j < EPL; ++j) p[j] = p[j] / s;
-        (void)inv;
+        for (int j = 0; j < EPL; ++j) p[j] = p[j] / sum;
       } else {
         const double* pr = a.probs_in + ((long)t * a.B + b) * E;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
-          int e = lane + 32 * j;
+          const int e = lane + 32 * j;
           p[j] = e < E ? pr[e] : 0.0;
+          if (e < E && !isfinite(zv[j])) bad = 1;
         }
       }
+      const double wt = a.tw[t];
 #pragma unroll
       for (int j = 0; j < EPL; ++j) {
         pooled[j] += wt * p[j];
-        dsum[j] += p[j];
+        c_dmass[j] += p[j];
       }
       if (a.probs_out != nullptr) {
         double* po = a.probs_out + ((long)t * a.B + b) * E;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
-          int e = lane + 32 * j;
+          const int e = lane + 32 * j;
           if (e < E) po[e] = p[j];
         }
       }
     }
-    // shared set: K_s rounds of warp argmax on (pooled desc, index asc)
-    uint32_t taken = 0;  // bit j: expert lane+32j is shared
-    int my_shared = -1;  // lane i < ks holds the i-th pick
+    // shared set S: top-K_s of pooled, (score desc, index asc)   (routing.py:261, :184-187)
+    uint32_t taken = 0;  // bit j: expert lane + 32 j is shared
     if (a.frozen) {
       const int v = lane < ks ? a.shared[(long)b * ks + lane] : -1;
       for (int i = 0; i < ks; ++i) {
         const int bi = __shfl_sync(0xffffffffu, v, i);
         if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
       }
-      my_shared = v;
-    } else {
+    } else if (ks > 0) {
+      uint64_t pk[EPL];
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) pk[j] = dkey(pooled[j]);
       for (int i = 0; i < ks; ++i) {
-        double bv;
-        int bi;
-        warp_argmax_f64<EPL>(pooled, taken, lane, E, bv, bi);
+        const int bi = warp_argmax_key64<EPL>(pk, taken, lane, E);
         if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-        if (lane == i) my_shared = bi;
       }
     }
-    // sort the shared picks ascending (rank among the ks lanes)
-    int srank = 0;
-    for (int j = 0; j < ks; ++j) {
-      int o = __shfl_sync(0xffffffffu, my_shared, j);
-      if (lane < ks && o < my_shared) ++srank;
+    {
+      int pos[EPL];
+      sorted_positions<EPL>(taken, lane, pos);
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < EPL; ++j)
+        if ((taken >> j) & 1u) a.shared[(long)b * ks + pos[j]] = lane + 32 * j;
     }
-    __syncwarp();
-    if (lane < ks) a.shared[(long)b * ks + srank] = my_shared;
 
-    // ---------------- Stage II, per task
-    uint32_t in_union = taken;  // union bits owned by this lane
-#pragma unroll
-    for (int t = 0; t < (TP > 0 ? TP : 1024); ++t) {
-      if (t >= T) break;
-      const float* zr = a.z + (long)t * a.st + (long)b * a.sb;
+    // ---------------- Stage II per task: top-K_a of z_t with S excluded (routing.py:263-268)
+    uint32_t in_union = taken;
+    for (int t = 0; t < T; ++t) {
       float zv[EPL];
-#pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        int e = lane + 32 * j;
-        if (TP > 0) zv[j] = zpre[TP > 0 ? t : 0][j];
-        else zv[j] = e < E ? __ldg(zr + e) : -INFINITY;
-        if ((taken >> j) & 1u) zv[j] = -INFINITY;
-      }
+      load_task(t, zv);
       uint32_t picked = 0;
-      int my_pick = -1;  // lane i < ka holds the i-th adaptive pick
+      const long ot = ((long)t * a.B + b);
       if (a.frozen) {
-        const int v = lane < ka ? a.adaptive[((long)t * a.B + b) * ka + lane] : -1;
+        const int v = lane < ka ? a.adaptive[ot * ka + lane] : -1;
         for (int i = 0; i < ka; ++i) {
           const int bi = __shfl_sync(0xffffffffu, v, i);
           if ((bi & 31) == lane) picked |= 1u << (bi >> 5);
         }
-        my_pick = v;
-      } else {
+      } else if (ka > 0) {
+        uint32_t zk[EPL];
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) zk[j] = fkey(zv[j]);
         for (int i = 0; i < ka; ++i) {
-          float bv;
-          int bi;
-          warp_argmax_f32<EPL>(zv, taken | picked, lane, E, bv, bi);
+          const int bi = warp_argmax_key32<EPL>(zk, taken | picked, lane, E);
           if ((bi & 31) == lane) picked |= 1u << (bi >> 5);
-          if (lane == i) my_pick = bi;
         }
       }
       in_union |= picked;
-      int arank = 0;
-      for (int j = 0; j < ka; ++j) {
-        int o = __shfl_sync(0xffffffffu, my_pick, j);
-        if (lane < ka && o < my_pick) ++arank;
-      }
-      __syncwarp();
-      if (lane < ka) a.adaptive[((long)t * a.B + b) * ka + arank] = my_pick;
-      // active = sorted(shared U adaptive): lanes 0..K-1 each hold one member
-      int val = -1;
-      {
-        int sv = __shfl_sync(0xffffffffu, my_shared, lane < ks ? lane : 0);
-        int av = __shfl_sync(0xffffffffu, my_pick, (lane >= ks && lane < K) ? lane - ks : 0);
-        val = lane < ks ? sv : (lane < K ? av : 0x7fffffff);
-      }
-      int pos = 0;
-      for (int j = 0; j < K; ++j) {
-        int o = __shfl_sync(0xffffffffu, val, j);
-        if (o < val) ++pos;
-      }
-      float zsel;
-      if (TP > 0) {
-        // owner lane of expert val holds it in zpre[t][val / 32]
-        float mine = 0.f;
-        const int src = lane < K ? (val & 31) : 0, jj = lane < K ? (val >> 5) : 0;
+      const uint32_t act = taken | picked;
+      int apos[EPL], kpos[EPL];
+      sorted_positions<EPL>(picked, lane, apos);
+      sorted_positions<EPL>(act, lane, kpos);
+      // renormalised weights: softmax of z over the active set (routing.py:203-211)
+      uint32_t mk = 0;
 #pragma unroll
-        for (int j = 0; j < EPL; ++j) {
-          float cand = __shfl_sync(0xffffffffu, zpre[TP > 0 ? t : 0][j], src);
-          if (j == jj) mine = cand;
+      for (int j = 0; j < EPL; ++j)
+        if ((act >> j) & 1u) mk = max(mk, fkey(zv[j]));
+      const float mx = fkey_inv(__reduce_max_sync(0xffffffffu, mk));
+      float ex[EPL], sum = 0.f;
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        ex[j] = ((act >> j) & 1u) ? expf(zv[j] - mx) : 0.f;
+        sum += ex[j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      const float inv = 1.f / sum;
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+        if ((picked >> j) & 1u) a.adaptive[ot * ka + apos[j]] = e;
+        if ((act >> j) & 1u) {
+          const float w = ex[j] / sum;
+          a.active[ot * K + kpos[j]] = e;
+          a.wsel[ot * K + kpos[j]] = w;
+          c_act[j] += 1;
+          c_mass[j] += (double)w;
         }
-        zsel = lane < K ? mine : -INFINITY;
-      } else {
-        zsel = lane < K ? __ldg(zr + val) : -INFINITY;
       }
-      float mx = zsel;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      float ex = lane < K ? expf(zsel - mx) : 0.f;
-      float s = ex;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      float w = ex / s;
-      if (lane < K) {
-        long o = ((long)t * a.B + b) * K + pos;
-        a.active[o] = val;
-        a.wsel[o] = w;
-        w_act[val] += 1;       // distinct vals within a task: no intra-warp race
-        w_mass[val] += w;
-      }
-      __syncwarp();
+      (void)inv;
     }
-    // union bitmask words and size; per-expert union / dense-mass accumulation
+    // union bitmask words and size (routing.py:272)
     int usz = 0;
     for (int j = 0; j < EW; ++j) {
       uint32_t bit = 0;
-      if (j < EPL) bit = (in_union >> j) & 1u;
-      uint32_t word = __ballot_sync(0xffffffffu, bit != 0);
+#pragma unroll
+      for (int jj = 0; jj < EPL; ++jj)
+        if (jj == j) bit = (in_union >> jj) & 1u;
+      const uint32_t word = __ballot_sync(0xffffffffu, bit != 0);
       usz += __popc(word);
       if (lane == 0) a.umask[(long)b * EW + j] = word;
     }
     if (lane == 0) a.usize[b] = usz;
 #pragma unroll
-    for (int j = 0; j < EPL; ++j) {
-      int e = lane + 32 * j;
-      if (e < E) {
-        w_union[e] += (in_union >> j) & 1u;
-        w_dmass[e] += dsum[j];
-      }
-    }
-    __syncwarp();
+    for (int j = 0; j < EPL; ++j) c_union[j] += (in_union >> j) & 1u;
   }
   bad = __any_sync(0xffffffffu, bad);
   if (bad && lane == 0) atomicOr(a.flag, 1);
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    const int e = lane + 32 * j;
+    if (e < E) {
+      s_union[warp * E + e] = c_union[j];
+      s_act[warp * E + e] = c_act[j];
+      s_mass[warp * E + e] = c_mass[j];
+      s_dmass[warp * E + e] = c_dmass[j];
+    }
+  }
   __syncthreads();
   // chunk partials in fixed warp order
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -327,7 +326,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
       m += s_mass[w * E + e];
       dm += s_dmass[w * E + e];
     }
-    long o = (long)blockIdx.x * E + e;
+    const long o = (long)blockIdx.x * E + e;
     a.chunk_union[o] = cu;
     a.chunk_active[o] = ca;
     a.chunk_mass[o] = m;

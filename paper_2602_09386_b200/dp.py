@@ -40,7 +40,8 @@ class DataParallelStep:
         self.eng.forward_a()
 
     def _part_b(self):
-        self.eng.forward_b(with_loss=True, batch_times_tasks=float(self.b_global * self.eng.T))
+        self.eng.forward_b(with_loss=True, batch_times_tasks=float(self.b_global * self.eng.T), train=True,
+                           batch_scale=self.b_local, lb_batch=self.b_local)
         self.eng.backward(batch_scale=self.b_local, lb_batch=self.b_local)
 
     def capture(self, warmup: int = 1):

@@ -168,8 +168,19 @@ class SMESEngine:
         self.row_of = z(B, self.umax, dt=i32)
         self.gather_inst = z(R, dt=i32)
         self.gather_exp = z(R, dt=i32)
-        self.X = z(R, d, dt=bf)
-        self.outs = [z(R, w, dt=bf) for w in self.dims[1:]]
+        # every wgrad Q operand (each layer's input and h) carries 64 extra columns whose first one
+        # is 1.0: the wgrad GEMM's extra N=64 tile then yields the bias gradient (sum over rows)
+        self.ld_in = [w + 64 for w in self.dims[:-1]]           # leading dims of layer inputs
+        self.X = z(R, self.ld_in[0], dt=bf)
+        self.X[:, d] = 1.0
+        self.outs = []
+        for i, w in enumerate(self.dims[1:]):
+            last = i == len(self.dims) - 2
+            o = z(R, w if last else self.ld_in[i + 1], dt=bf)
+            if not last:
+                o[:, w] = 1.0
+            self.outs.append(o)
+        self.ld_out = [o.shape[1] for o in self.outs]
         self.bits = [z(w // 32, R, dt=torch.int32) if (l.act == "relu" and i < len(self.p.layers) - 1) else None
                      for i, (w, l) in enumerate(zip(self.dims[1:], self.p.layers))]
         self.reps = z(T, B, self.d_out, dt=bf)     # required by the backward (head grads)
@@ -188,6 +199,7 @@ class SMESEngine:
         edges = [min(self.B_pad, (self.B_pad // self.rw_splits) // 128 * 128 * i) for i in range(self.rw_splits)]
         self.seg_router_split = torch.tensor(edges + [self.B_pad], dtype=i32, device=dev)
         self.rw_part = z(self.rw_splits, T * E, d)
+        self.rb_part = z(self.rw_splits, T * E)
         # backward
         self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
         self.dX = z(R, d, dt=bf)
@@ -209,7 +221,10 @@ class SMESEngine:
         self.d_hidden = z(B, d)
         self.part_dw = z(self.grid, T, self.d_out)
         self.part_db = z(self.grid, T)
-        self.h = z(B, d, dt=bf)
+        self.ldh = d + 64
+        self.h_full = z(B, self.ldh, dt=bf)
+        self.h_full[:, d] = 1.0
+        self.h = self.h_full[:, :d]                 # strided view; kernels get ptr + ldh
 
     def refresh_weights(self):
         """Copy fp32 master parameters into the bf16 / fp32 kernel operands."""
@@ -252,22 +267,39 @@ class SMESEngine:
         s = self._stream()
         T, E, B, d = self.T, self.E, self.B, self.d
         # router logits z = h W_r^T + b_r  (B, T*E) fp32
-        _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), d, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
+        _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
              ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
         self.route(s, frozen=frozen)
         _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
              ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), s)
         _tagged("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
-             ptr(self.loads), ptr(self.h), d, ptr(self.X), d, ptr(self.row_of), self.umax, ptr(self.gather_inst),
+             ptr(self.loads), ptr(self.h), self.ldh, ptr(self.X), self.ld_in[0], ptr(self.row_of), self.umax,
+             ptr(self.gather_inst),
              ptr(self.gather_exp), ptr(self.d_outs[-1]), self.d_out, self.d_out, s)
         self.experts_forward(s)
 
-    def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None):
-        """LoadStats finalize (global B*T under data parallelism) -> combine + heads + loss."""
+    def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
+                  batch_scale: int | None = None, lb_batch: int | None = None):
+        """LoadStats finalize (global B*T under data parallelism) -> combine + heads + loss.
+        ``train`` (sparse LB reading) fuses the combine backward into the same pass."""
         s = self._stream()
         T, E, B = self.T, self.E, self.B
         self.stats_finalize(s, batch_times_tasks)
+        self._fused_bwd = bool(train and not self.dense)
+        if self._fused_bwd:
+            bs = B if batch_scale is None else batch_scale
+            lbb = B if lb_batch is None else lb_batch
+            lb_coef = self.beta * E / (self.K * lbb * T)
+            _tagged("combine_train", "smes_combine_train", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask),
+                    ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
+                    self.d_out, ptr(self.head_w), ptr(self.head_b), ptr(self.P), self.ldp, ptr(self.reps),
+                    ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam), ptr(self.loss_part),
+                    1.0 / bs, int(self.p.layers[-1].act == "relu"), ptr(self.d_outs[-1]), ptr(self.dz),
+                    ptr(self.freq32), lb_coef, ptr(self.part_dw), ptr(self.part_db), self.grid, s)
+            _tagged("loss_finalize", "smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
+                    self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
+            return
         _tagged("combine_fwd", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
              ptr(self.head_b), ptr(self.P), self.ldp, ptr(self.reps), ptr(self.logits), ptr(self.preds),
@@ -288,9 +320,9 @@ class SMESEngine:
         R = self.rows_cap
         inp = self.X
         for i, l in enumerate(self.p.layers):
-            _tagged(f"fc{i + 1}_fwd", "smes_gemm_ragged_m", ptr(inp), self.dims[i], R, ptr(self.w_bf[i]), self.E, self.dims[i + 1],
-                 self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act], ptr(self.bits[i]), None, R,
-                 ptr(self.outs[i]), self.dims[i + 1], 0, R, s)
+            _tagged(f"fc{i + 1}_fwd", "smes_gemm_ragged_m", ptr(inp), self.ld_in[i], R, ptr(self.w_bf[i]), self.E,
+                    self.dims[i + 1], self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act],
+                    ptr(self.bits[i]), None, R, ptr(self.outs[i]), self.ld_out[i], 0, R, s)
             inp = self.outs[i]
         # head projections of every packed row: P = O head_W^T (tcgen05 GEMM, N = T)
         _tagged("head_proj", "smes_gemm_ragged_m", ptr(self.outs[-1]), self.d_out, R, ptr(self.head_w_bf), 1, self.T,
@@ -311,13 +343,13 @@ class SMESEngine:
         lbb = B if lb_batch is None else lb_batch
         lb_coef = self.beta * E / (K * lbb * T)
         relu_last = int(self.p.layers[-1].act == "relu")
-        _tagged("combine_bwd", "smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
-             ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
-             ptr(self.P), self.ldp, ptr(self.reps), ptr(self.preds), ptr(self.labels), ptr(self.lam), 1.0 / bs,
-             relu_last,
-             ptr(self.d_outs[-1]),
-             ptr(self.dz), ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw),
-             ptr(self.part_db), self.grid, s)
+        if not getattr(self, "_fused_bwd", False):
+            _tagged("combine_bwd", "smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask),
+                    ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
+                    self.d_out, ptr(self.head_w), ptr(self.P), self.ldp, ptr(self.reps), ptr(self.preds),
+                    ptr(self.labels), ptr(self.lam), 1.0 / bs, relu_last, ptr(self.d_outs[-1]), ptr(self.dz),
+                    ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw), ptr(self.part_db),
+                    self.grid, s)
         n_layers = len(self.p.layers)
         for i in range(n_layers - 1, -1, -1):
             dout = self.d_outs[i]
@@ -327,27 +359,29 @@ class SMESEngine:
             if i > 0:   # dgrad into the previous layer's output, masked by its relu
                 _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
-            _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), di, R, E, do, di, ptr(self.seg_pad), ptr(gw), s)
-            _tagged(f"fc{i + 1}_bias", "smes_seg_colsum", ptr(dout), do, R, do, ptr(self.seg_pad), E, ptr(self.colsum_part), ptr(gb), s)
+            # wgrad + bias grad in one launch (ones column of the layer input, see _alloc)
+            _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do, di,
+                    ptr(self.seg_pad), ptr(gw), ptr(gb), s)
         # dX = d_out0 W_0
         _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
              ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
         # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
         _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
              ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
-        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), d, B, self.rw_splits, T * E, d,
-                ptr(self.seg_router_split), ptr(self.rw_part), s)
+        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits,
+                T * E, d, ptr(self.seg_router_split), ptr(self.rw_part), ptr(self.rb_part), s)
         _tagged("router_wgrad", "smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d,
                 ptr(self.g_router_w), s)
-        _tagged("router_bias", "smes_seg_colsum", ptr(self.dz), T * E, self.B_pad, T * E, ptr(self.seg_router), 1,
-             ptr(self.colsum_part), ptr(self.g_router_b), s)
+        _tagged("router_wgrad", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
+                ptr(self.g_router_b), s)
         _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
              ptr(self.dh_router), ptr(self.d_hidden), s)
         _tagged("head_reduce", "smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out, ptr(self.g_head_w), s)
         _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
     def step(self):
-        self.forward(with_loss=True)
+        self.forward_a()
+        self.forward_b(with_loss=True, train=True)
         self.backward()
 
     # ------------------------------------------------------------------ accounting

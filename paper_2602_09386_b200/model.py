@@ -210,7 +210,7 @@ def _encode(x: torch.Tensor, model: MoeModel, eng) -> dict:
     _gemm(xb, Fp, B, w1.reshape(1, dh, Fp).contiguous(), dh, Fp, model.encoder1.bias.float().contiguous(),
           1 if relu else 0, mid, dh, 0, B, bits_out=bits, bits_ld=_round(B, 128))
     w2 = model.encoder2.weight.to(torch.bfloat16).reshape(1, model.d_in, dh).contiguous()
-    _gemm(mid, dh, B, w2, model.d_in, dh, model.encoder2.bias.float().contiguous(), 0, eng.h, model.d_in, 0, B)
+    _gemm(mid, dh, B, w2, model.d_in, dh, model.encoder2.bias.float().contiguous(), 0, eng.h, eng.ldh, 0, B)
     return dict(xb=xb, Fp=Fp, F=F, mid=mid, bits=bits, w1=w1, w2=w2)
 
 

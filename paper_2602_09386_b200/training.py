@@ -88,7 +88,7 @@ def backward(result: ForwardResult, model: MoeModel, labels, dense_probs_in_stat
         raise NumericsError("labels must be 0 or 1")
     eng.labels.copy_(y)
     eng.dense = bool(dense_probs_in_stats)
-    eng.forward_b(with_loss=True)          # loss + LoadStats under this reading (training.py:140-142)
+    eng.forward_b(with_loss=True, train=True)   # loss + LoadStats (training.py:140-142) + fused combine bwd
     eng.backward()
     E, K = eng.E, eng.K
     lo = eng.loss_out.cpu()
@@ -113,7 +113,7 @@ def _encoder_backward(enc: dict, model: MoeModel, eng) -> dict:
     dhid[:B] = eng.d_hidden
     # encoder2: dW = d_hidden^T mid, db = sum d_hidden, d_mid = d_hidden W2 (x relu mask)
     dw2 = torch.zeros(1, d, dh, device=dev)
-    call("smes_gemm_ragged_k", ptr(dhid), d, ptr(enc["mid"]), dh, B, 1, d, dh, ptr(seg1), ptr(dw2), s)
+    call("smes_gemm_ragged_k", ptr(dhid), d, ptr(enc["mid"]), dh, B, 1, d, dh, ptr(seg1), ptr(dw2), None, s)
     part = torch.zeros(Bp // 128, max(d, dh), device=dev)
     db2 = torch.zeros(1, d, device=dev)
     call("smes_seg_colsum", ptr(dhid), d, Bp, d, ptr(seg1), 1, ptr(part), ptr(db2), s)
@@ -121,7 +121,7 @@ def _encoder_backward(enc: dict, model: MoeModel, eng) -> dict:
     _gemm(dhid, d, Bp, enc["w2"], dh, d, None, 0, dmid, dh, 0, B, b_mn=1, bits_in=enc["bits"], bits_ld=Bp)
     # encoder1: dW = d_pre^T x, db = sum d_pre
     dw1 = torch.zeros(1, dh, Fp, device=dev)
-    call("smes_gemm_ragged_k", ptr(dmid), dh, ptr(enc["xb"]), Fp, B, 1, dh, Fp, ptr(seg1), ptr(dw1), s)
+    call("smes_gemm_ragged_k", ptr(dmid), dh, ptr(enc["xb"]), Fp, B, 1, dh, Fp, ptr(seg1), ptr(dw1), None, s)
     db1 = torch.zeros(1, dh, device=dev)
     call("smes_seg_colsum", ptr(dmid), dh, Bp, dh, ptr(seg1), 1, ptr(part), ptr(db1), s)
     g["encoder1.weight"] = dw1[0, :, :F].contiguous()

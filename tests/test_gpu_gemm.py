@@ -119,7 +119,7 @@ def test_ragged_k_wgrad(I, J):
     pb, qb = pm.to(torch.bfloat16), qm.to(torch.bfloat16)
     seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
     out = torch.full((E, I, J), float("nan"), device=dev)
-    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J, R, E, I, J, ptr(seg_t), ptr(out),
+    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J, R, E, I, J, ptr(seg_t), ptr(out), None,
          torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     for e in range(E):
@@ -130,3 +130,34 @@ def test_ragged_k_wgrad(I, J):
             continue
         err = (out[e] - ref).abs().max().item() / ref.abs().max().item()
         assert err < 1e-5, (e, err)
+
+
+@pytest.mark.parametrize("I,J", [(256, 512), (512, 256), (128, 128)])
+def test_ragged_k_wgrad_with_fused_bias(I, J):
+    """db_g[i] = sum_m P[m, i] via the ones column at Q[:, J] (one extra N=64 tile)."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(7 * I + J)
+    loads = [200, 0, 77, 640]
+    E = len(loads)
+    seg, pm = _packed(loads, I, g, dev)
+    _, qm = _packed(loads, J, g, dev)
+    R = pm.shape[0]
+    pb = pm.to(torch.bfloat16)
+    qb = torch.zeros(R, J + 64, dtype=torch.bfloat16, device=dev)
+    qb[:, :J] = qm.to(torch.bfloat16)
+    qb[:, J] = 1.0
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.full((E, I, J), float("nan"), device=dev)
+    db = torch.full((E, I), float("nan"), device=dev)
+    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J + 64, R, E, I, J, ptr(seg_t), ptr(out), ptr(db),
+         torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, hi = seg[e], seg[e + 1]
+        ref = pb[lo:hi].float().T @ qb[lo:hi, :J].float()
+        refb = pb[lo:hi].float().sum(0)
+        if loads[e] == 0:
+            assert torch.all(out[e] == 0) and torch.all(db[e] == 0)
+            continue
+        assert (out[e] - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+        assert (db[e] - refb).abs().max().item() / refb.abs().max().item() < 1e-5
