@@ -56,11 +56,12 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
 /* ---- K2 execution plan: replaces build_execution_plan (execution.py:85-123)
  *      and the gather hidden[plan.gather_instances] (model.py:301).
  *      Segments are padded to 128 rows (seg_pad); seg_log are the reference's
- *      segment_offsets.  totals = {0, padded rows, N_act}. */
+ *      segment_offsets.  totals = {0, padded rows, N_act}.  seg_half (optional, 2E+1) splits
+ *      every padded segment into two 64-row-aligned halves (split-K tables). */
 int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
                      const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
                      double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
-                     unsigned int* ticket, void* stream);
+                     unsigned int* ticket, int32_t* seg_half, void* stream);
 int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
                      void* stream);
 int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,
@@ -74,7 +75,8 @@ int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* um
  *                C[m,n] = mask(sum_k A[m,k] W_g[k,n])              (b_mn = 1, dgrad)
  *      ragged-K: C_g[i,j] = sum_{m in g} P[m,i] Q[m,j]           (wgrad, fp32 out)
  *                db_g[i]  = sum_{m in g} P[m,i]   when db_out != NULL: Q must carry a column of
- *                ones at index J (ldq >= J+64); one extra N=64 tile computes the bias grad.
+ *                ones at index J (ldq >= J+64); extra N=64 tiles compute the bias grad as 4 K-slices
+ *                db_out[s][g][i] (s < 4) whose sum is db (fixed order, see smes_part_reduce).
  *      seg = padded group offsets (device). */
 int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, int G, int N, int K, int b_mn,
                        const int* seg, const float* bias, int act, uint32_t* relu_bits_out,
@@ -100,14 +102,19 @@ int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint
                      const float* freq, float lb_coef, int dense_probs, const float* z, float* part_dw,
                      float* part_db, int grid, void* stream);
 
-/* ---- K4+K6+K7 fused for a training step (sparse LB reading): the forward combine + heads + BCE
- *      also emits dlogit, d_packed, dz and the head-grad partials while the rows are on chip. */
-int smes_combine_train(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
-                       const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
-                       const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits,
-                       float* preds, const float* labels, const float* lam, double* loss_part, float inv_b,
-                       int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, float* part_dw,
-                       float* part_db, int grid, void* stream);
+/* ---- K4+K6+K7 for a training step (sparse LB reading): logits/preds/loss from the head
+ *      projections P, dlogit, the (row, task) coefficient matrix C = w * dlogit (bf16) and the
+ *      router-logit gradient dz (training.py:146-179, balance.py:83-99).  The dense parts,
+ *      d_packed = C head_W and dW_head = C^T O, are tcgen05 GEMMs (smes_gemm_*). */
+int smes_combine_train(int T, int B, int E, int K, int umax, const uint32_t* umask, const int32_t* usize,
+                       const int32_t* row_of, const int32_t* active, const float* wsel, const float* head_b,
+                       const float* P, long ldp, float* logits, float* preds, const float* labels, const float* lam,
+                       double* loss_part, float inv_b, void* cmat, long ldc, void* dz, const float* freq,
+                       float lb_coef, float* part_db, float* part_csum, float* part_rb, int grid, void* stream);
+/* last-pool bias grad when the last pool is identity: db[e] = (sum_rows_of_e C) head_W. part_csum
+ * (grid, E, T) and part_rb (grid, T*E: router bias grad = column sums of dz) are per-CTA partials
+ * from smes_combine_train (optional, may be NULL). */
+int smes_bias_from_csum(int E, int T, int d_out, const float* csum, const float* head_w, float* out, void* stream);
 
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,

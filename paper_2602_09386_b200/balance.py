@@ -48,7 +48,7 @@ def _raw_sums(routing: BatchRouting) -> torch.Tensor:
     call("smes_plan_reduce", C, E, ptr(routing.chunk_union), ptr(routing.chunk_active), ptr(routing.chunk_mass),
          ptr(routing.chunk_dmass), ptr(torch.zeros(C, E, dtype=i32, device=dev)), ptr(torch.zeros(E, dtype=i32, device=dev)),
          ptr(raw), ptr(torch.zeros(E + 1, dtype=i32, device=dev)), ptr(torch.zeros(E + 1, dtype=i32, device=dev)),
-         ptr(torch.zeros(3, dtype=i32, device=dev)), ptr(torch.zeros(1, dtype=i32, device=dev)), _stream())
+         ptr(torch.zeros(3, dtype=i32, device=dev)), ptr(torch.zeros(1, dtype=i32, device=dev)), None, _stream())
     return raw
 
 

@@ -265,210 +265,118 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
   }
 }
 
-// Training-step combine: forward (reps, logits, preds, loss) AND the backward terms of
-// training.py:146-179 + balance.py:83-99 (sparse reading) in one pass -- labels and the
-// global selection frequency are known when the forward combine runs, so dlogit,
-// d_packed, dz and the head-grad partials are produced while reps are still in
-// registers and the packed rows / head projections are still staged in smem.
-template <int VPL, int MAXT>
-__global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const CombineArgs a) {
+// Training-step combine (sparse LB reading).  Labels and the global selection frequency
+// are known when the forward combine runs, so one pass produces the forward outputs
+// (logits, preds, loss) and every backward term that is not a dense contraction:
+//   dlogit_t = lambda_t / B (yhat - y) [clamp inactive]                      (training.py:147-148)
+//   C[row, t] = w[row, t] dlogit_t            (bf16, one (rows, ldc) matrix)
+//   dz[t, e_k] = w_k (g_k - sum_j g_j w_j) + beta coef w_k (f_k - sum_j w_j f_j),
+//                g_k = dlogit_t P[row_k, t]                                   (training.py:171-179, balance.py:97-99)
+// The two dense contractions run on the tcgen05 GEMM afterwards:
+//   d_packed = C head_W   (K = T)         and      dW_head = C^T O   (split-K over expert halves).
+// Nothing per-column is computed here, so the kernel only touches T*K pairs per instance.
+template <int MAXT>
+__global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const CombineArgs a, __nv_bfloat16* cmat, int ldc,
+                                                                 float* part_csum, float* part_rb) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int S = a.d_out / (32 * VPL);
-  const int G = CB_WARPS / S;
-  const int gi = warp / S, ws = warp % S;
-  const int col = (ws * 32 + lane) * VPL;
   const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E, TK = T * K, umax = a.umax;
   const int ldp = a.ldp;
-  const int n = T * a.d_out;
   extern __shared__ __align__(16) uint8_t smraw[];
-  const GroupLayout L(umax, MAXT, ldp, umax, a.d_out);
-  float* s_hw = reinterpret_cast<float*>(smraw);                       // [T][d_out]
-  int32_t* s_act_all = reinterpret_cast<int32_t*>(s_hw + n);           // [G][T*K]
-  float* s_w_all = reinterpret_cast<float*>(s_act_all + (size_t)G * TK);
-  float* s_gw_all = s_w_all + (size_t)G * TK;
-  float* s_wf_all = s_gw_all + (size_t)G * TK;
-  uint8_t* g0 = reinterpret_cast<uint8_t*>(s_wf_all + (size_t)G * TK);
-  g0 = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(g0) + 15) & ~uintptr_t(15)) + (size_t)gi * L.bytes;
-  int32_t* s_act = s_act_all + (size_t)gi * TK;
-  float* s_w = s_w_all + (size_t)gi * TK;
-  float* s_gw = s_gw_all + (size_t)gi * TK;
-  float* s_wf = s_wf_all + (size_t)gi * TK;
-  uint32_t* s_um = reinterpret_cast<uint32_t*>(g0);
-  int32_t* s_rows = reinterpret_cast<int32_t*>(g0 + L.off_rows);
-  float* s_wt = reinterpret_cast<float*>(g0 + L.off_wt);
-  float* s_dl = reinterpret_cast<float*>(g0 + L.off_dl);
-  float* s_p = reinterpret_cast<float*>(g0 + L.off_p);
-  __nv_bfloat16* s_o = reinterpret_cast<__nv_bfloat16*>(g0 + L.off_stage);
-  for (int i = threadIdx.x; i < n; i += CB_THREADS) s_hw[i] = a.head_w[i];
-  const int gthreads = S * 32, gtid = ws * 32 + lane;
-  const int lt = lane & (MAXT - 1), ug = lane / MAXT;
-  constexpr int NG = 32 / MAXT;
-  const int cpr = a.d_out / 8, pcr = ldp / 4;
-  float acc_dw[MAXT][VPL];
-#pragma unroll
-  for (int t = 0; t < MAXT; ++t)
-#pragma unroll
-    for (int v = 0; v < VPL; ++v) acc_dw[t][v] = 0.f;
+  // per-warp (one instance per warp) tables
+  const int per_warp = 128 + umax * 4 + TK * 4 * 4 + MAXT * 4 + 64;
+  uint8_t* w0 = smraw + (size_t)warp * ((per_warp + 15) & ~15);
+  uint32_t* s_um = reinterpret_cast<uint32_t*>(w0);
+  int32_t* s_rows = reinterpret_cast<int32_t*>(w0 + 128);
+  int32_t* s_act = s_rows + umax;
+  float* s_w = reinterpret_cast<float*>(s_act + TK);
+  float* s_gw = s_w + TK;
+  float* s_wf = s_gw + TK;
+  float* s_dl = s_wf + TK;
+  // per-warp accumulators (conflict-free: within one instance every (task, expert) pair is distinct)
+  const size_t acc_base = (size_t)CB_WARPS * ((per_warp + 15) & ~15);
+  float* s_cs = part_csum ? reinterpret_cast<float*>(smraw + acc_base) + (size_t)warp * E * T : nullptr;  // [E][T]
+  float* s_rb = part_rb ? reinterpret_cast<float*>(smraw + acc_base) + (size_t)CB_WARPS * E * T * (part_csum ? 1 : 0) +
+                              (size_t)warp * TE : nullptr;                                                     // [T][E]
+  if (s_cs) for (int i = lane; i < E * T; i += 32) s_cs[i] = 0.f;
+  if (s_rb) for (int i = lane; i < TE; i += 32) s_rb[i] = 0.f;
   float my_db = 0.f;
   double my_loss = 0.0;
-  const int iters = (a.B + (long)gridDim.x * G - 1) / ((long)gridDim.x * G);
-  for (int it = 0; it < iters; ++it) {
-    const int b = (it * gridDim.x + blockIdx.x) * G + gi;
-    const bool valid = b < a.B;
-    const int U = valid ? a.usize[b] : 0;
-    // P1: instance tables
-    if (valid) {
-      for (int j = gtid; j < EW; j += gthreads) s_um[j] = a.umask[(long)b * EW + j];
-      for (int u = gtid; u < U; u += gthreads) s_rows[u] = a.row_of[(long)b * a.umax + u];
-      for (int i = gtid; i < U * MAXT; i += gthreads) s_wt[i] = 0.f;
-      for (int i = gtid; i < TK; i += gthreads) {
-        const int t = i / K;
-        const long o = ((long)t * a.B + b) * K + (i - t * K);
-        s_act[i] = a.active[o];
-        s_w[i] = a.wsel[o];
-      }
+  for (int b = blockIdx.x * CB_WARPS + warp; b < a.B; b += gridDim.x * CB_WARPS) {
+    const int U = a.usize[b];
+    for (int j = lane; j < EW; j += 32) s_um[j] = a.umask[(long)b * EW + j];
+    for (int u = lane; u < U; u += 32) s_rows[u] = a.row_of[(long)b * a.umax + u];
+    for (int i = lane; i < TK; i += 32) {
+      const int t = i / K;
+      const long o = ((long)t * a.B + b) * K + (i - t * K);
+      s_act[i] = a.active[o];
+      s_w[i] = a.wsel[o];
     }
-    __syncthreads();
-    // P2: gather rows + projections, build the (union row x task) weight table
-    if (valid) {
-      for (int i = gtid; i < U * cpr; i += gthreads) {
-        const int u = i / cpr, c = i - u * cpr;
-        cp_async16(s_o + (long)u * a.d_out + c * 8, a.O + (long)s_rows[u] * a.ldo + c * 8);
-      }
-      for (int i = gtid; i < U * pcr; i += gthreads) {
-        const int u = i / pcr, c = i - u * pcr;
-        cp_async16(s_p + (long)u * ldp + c * 4, a.P + (long)s_rows[u] * ldp + c * 4);
-      }
-      for (int i = gtid; i < TK; i += gthreads) s_wt[union_rank(s_um, s_act[i]) * MAXT + i / K] = s_w[i];
-      cp_async_wait_all();
+    __syncwarp();
+    // logits from the head projections: logit_t = b_t + sum_k w_k P[row_k, t]
+    float g_raw = 0.f, wf = 0.f;
+    int row_i = 0, t_i = 0;
+    for (int i = lane; i < TK; i += 32) {
+      t_i = i / K;
+      row_i = s_rows[union_rank(s_um, s_act[i])];
+      const float w = s_w[i];
+      g_raw = __ldg(a.P + (long)row_i * ldp + t_i);
+      s_gw[i] = w * g_raw;                      // w_k P_k  (scaled by dlogit below)
+      wf = w * __ldg(a.freq + s_act[i]);
+      s_wf[i] = wf;
     }
-    __syncthreads();
-    // P3: reps, logits, preds, loss, dlogit
-    float acc[MAXT][VPL];
-#pragma unroll
-    for (int t = 0; t < MAXT; ++t)
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) acc[t][v] = 0.f;
-    if (valid) {
-      for (int u = 0; u < U; ++u) {
-        float x[VPL];
-        load_bf<VPL>(s_o + (long)u * a.d_out + col, x);
-#pragma unroll
-        for (int t = 0; t < MAXT; ++t) {
-          const float w = s_wt[u * MAXT + t];
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) acc[t][v] = fmaf(w, x[v], acc[t][v]);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < MAXT; ++t)
-        if (t < T) store_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, acc[t]);
-      if (ws == 0) {
-        float sacc = 0.f;
-        if (lt < T)
-          for (int u = ug; u < U; u += NG) sacc = fmaf(s_wt[u * MAXT + lt], s_p[u * ldp + lt], sacc);
-#pragma unroll
-        for (int o = 16; o >= MAXT; o >>= 1) sacc += __shfl_xor_sync(0xffffffffu, sacc, o);
-        if (ug == 0 && lt < T) {
-          const int t = lt;
-          const float lg = sacc + a.head_b[t];
-          const float ez = expf(-fabsf(lg));               // stable sigmoid (linalg.py:108-113)
-          const float pos = 1.f / (1.f + ez);
-          const float pr = lg >= 0.f ? pos : 1.f - pos;
-          a.logits[(long)t * a.B + b] = lg;
-          a.preds[(long)t * a.B + b] = pr;
-          const float y = a.labels[(long)t * a.B + b];
-          double pc = (double)pr;
-          pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
-          my_loss += (double)a.lam[t] * -((double)y * log(pc) + (1.0 - (double)y) * log1p(-pc));
-          const bool inside = pr > 1e-7f && pr < 1.f - 1e-7f;          // training.py:147-148
-          const float dl = inside ? a.lam[t] * a.inv_b * (pr - y) : 0.f;
-          s_dl[t] = dl;
-          my_db += dl;
-        }
-      }
+    __syncwarp();
+    if (lane < T) {
+      const int t = lane;
+      float lg = a.head_b[t];
+      for (int k = 0; k < K; ++k) lg += s_gw[t * K + k];
+      const float ez = expf(-fabsf(lg));                 // stable sigmoid (linalg.py:108-113)
+      const float pos = 1.f / (1.f + ez);
+      const float pr = lg >= 0.f ? pos : 1.f - pos;
+      a.logits[(long)t * a.B + b] = lg;
+      a.preds[(long)t * a.B + b] = pr;
+      const float y = a.labels[(long)t * a.B + b];
+      double pc = (double)pr;
+      pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
+      my_loss += (double)a.lam[t] * -((double)y * log(pc) + (1.0 - (double)y) * log1p(-pc));
+      const bool inside = pr > 1e-7f && pr < 1.f - 1e-7f;
+      const float dl = inside ? a.lam[t] * a.inv_b * (pr - y) : 0.f;
+      s_dl[t] = dl;
+      my_db += dl;
     }
-    __syncthreads();
-    // P4: d_packed rows, head-grad accumulation, (task, pick) pair terms
-    if (valid) {
-      float dl[MAXT];
-#pragma unroll
-      for (int t = 0; t < MAXT; ++t) dl[t] = t < T ? s_dl[t] : 0.f;
-#pragma unroll
-      for (int t = 0; t < MAXT; ++t)
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) acc_dw[t][v] = fmaf(dl[t], acc[t][v], acc_dw[t][v]);
-      for (int u = 0; u < U; ++u) {
-        asm volatile("" ::: "memory");
-        float dp[VPL];
-#pragma unroll
-        for (int v = 0; v < VPL; ++v) dp[v] = 0.f;
-#pragma unroll
-        for (int t = 0; t < MAXT; ++t) {
-          if (t < T) {
-            const float c = s_wt[u * MAXT + t] * dl[t];
-#pragma unroll
-            for (int v = 0; v < VPL; v += 4) {
-              const float4 h4 = *reinterpret_cast<const float4*>(s_hw + (long)t * a.d_out + col + v);
-              dp[v] = fmaf(c, h4.x, dp[v]);
-              dp[v + 1] = fmaf(c, h4.y, dp[v + 1]);
-              dp[v + 2] = fmaf(c, h4.z, dp[v + 2]);
-              dp[v + 3] = fmaf(c, h4.w, dp[v + 3]);
-            }
-          }
-        }
-        if (a.relu_last) {
-          float x[VPL];
-          load_bf<VPL>(s_o + (long)u * a.d_out + col, x);
-#pragma unroll
-          for (int v = 0; v < VPL; ++v) dp[v] = x[v] > 0.f ? dp[v] : 0.f;
-        }
-        store_bf<VPL>(a.dpacked + (long)s_rows[u] * a.ldo + col, dp);
-      }
-      __nv_bfloat16* dzr = a.dz + (long)b * TE;
-      for (int i = gtid * 8; i < TE; i += gthreads * 8) *reinterpret_cast<uint4*>(dzr + i) = make_uint4(0, 0, 0, 0);
-      for (int i = gtid; i < TK; i += gthreads) {
-        const int t = i / K, e = s_act[i];
-        const float w = s_w[i];
-        s_gw[i] = s_dl[t] * s_p[union_rank(s_um, e) * ldp + t] * w;   // g_k w_k
-        s_wf[i] = w * __ldg(a.freq + e);                                // w_k f_k
-      }
+    __syncwarp();
+    // C rows: every (row, task) coefficient; rows of an instance are zeroed first (tasks that
+    // do not select the row's expert contribute 0)
+    for (int i = lane; i < U * (ldc / 8); i += 32) {
+      const int u = i / (ldc / 8), c = i - u * (ldc / 8);
+      *reinterpret_cast<uint4*>(cmat + (long)s_rows[u] * ldc + c * 8) = make_uint4(0, 0, 0, 0);
     }
-    __syncthreads();
-    // P5: dz = w (g - sum_j g_j w_j) + beta coef w (f - sum_j w_j f_j)   (sparse reading)
-    if (valid) {
-      __nv_bfloat16* dzr = a.dz + (long)b * TE;
-      for (int i = gtid; i < TK; i += gthreads) {
-        const int t = i / K;
-        float Gt = 0.f, Ft = 0.f;
-        for (int k = 0; k < K; ++k) { Gt += s_gw[t * K + k]; Ft += s_wf[t * K + k]; }
-        const float w = s_w[i];
-        dzr[t * E + s_act[i]] = __float2bfloat16_rn((s_gw[i] - w * Gt) + a.lb_coef * (s_wf[i] - w * Ft));
-      }
+    __nv_bfloat16* dzr = a.dz + (long)b * TE;
+    for (int i = lane * 8; i < TE; i += 256) *reinterpret_cast<uint4*>(dzr + i) = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    for (int i = lane; i < TK; i += 32) {
+      const int t = i / K;
+      const int row = s_rows[union_rank(s_um, s_act[i])];
+      const float w = s_w[i], dl = s_dl[t];
+      cmat[(long)row * ldc + t] = __float2bfloat16_rn(w * dl);
+      float Gt = 0.f, Ft = 0.f;
+      for (int k = 0; k < K; ++k) { Gt += s_gw[t * K + k]; Ft += s_wf[t * K + k]; }
+      // w (g - G) with g = dl P, G = dl sum_j w_j P_j ;  coef w (f - F)
+      const float dzv = dl * (s_gw[i] - w * Gt) + a.lb_coef * (s_wf[i] - w * Ft);
+      dzr[t * E + s_act[i]] = __float2bfloat16_rn(dzv);
+      if (s_cs) s_cs[s_act[i] * T + t] += w * dl;     // per-(expert, task) sum of C   -> last-pool bias grad
+      if (s_rb) s_rb[t * E + s_act[i]] += dzv;        // column sum of dz              -> router bias grad
     }
-    __syncthreads();
+    __syncwarp();
   }
-  // per-CTA partials: head grads (groups summed in fixed order) and the loss
-  float* s_red = reinterpret_cast<float*>(smraw);
-#pragma unroll
-  for (int t = 0; t < MAXT; ++t)
-    if (t < T)
-#pragma unroll
-      for (int v = 0; v < VPL; ++v) s_red[(long)gi * n + (long)t * a.d_out + col + v] = acc_dw[t][v];
-  float* s_db = s_red + (long)G * n;
-  if (ws == 0 && ug == 0 && lt < T) s_db[gi * MAXT + lt] = my_db;
-  double* s_l = reinterpret_cast<double*>(s_db + G * MAXT + 2);
-  s_l = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(s_l) + 7) & ~uintptr_t(7));
+  // per-CTA partials (fixed order)
+  __shared__ float s_db[CB_WARPS][CB_MAX_T];
+  __shared__ double s_l[CB_THREADS];
+  if (lane < T) s_db[warp][lane] = my_db;
   s_l[threadIdx.x] = my_loss;
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += CB_THREADS) {
-    float sum = 0.f;
-    for (int g = 0; g < G; ++g) sum += s_red[(long)g * n + i];
-    a.part_dw[(long)blockIdx.x * n + i] = sum;
-  }
   if (threadIdx.x < T) {
     float sum = 0.f;
-    for (int g = 0; g < G; ++g) sum += s_db[g * MAXT + threadIdx.x];
+    for (int w = 0; w < CB_WARPS; ++w) sum += s_db[w][threadIdx.x];
     a.part_db[(long)blockIdx.x * T + threadIdx.x] = sum;
   }
   if (threadIdx.x == 0 && a.loss_part) {
@@ -476,6 +384,33 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
     for (int i = 0; i < CB_THREADS; ++i) sum += s_l[i];
     a.loss_part[blockIdx.x] = sum;
   }
+  if (part_csum) {
+    const float* base = reinterpret_cast<const float*>(smraw + acc_base);
+    for (int i = threadIdx.x; i < E * T; i += CB_THREADS) {
+      float sum = 0.f;
+      for (int w = 0; w < CB_WARPS; ++w) sum += base[(size_t)w * E * T + i];
+      part_csum[(size_t)blockIdx.x * E * T + i] = sum;
+    }
+  }
+  if (part_rb) {
+    const float* base = reinterpret_cast<const float*>(smraw + acc_base) + (size_t)CB_WARPS * E * T * (part_csum ? 1 : 0);
+    for (int i = threadIdx.x; i < TE; i += CB_THREADS) {
+      float sum = 0.f;
+      for (int w = 0; w < CB_WARPS; ++w) sum += base[(size_t)w * TE + i];
+      part_rb[(size_t)blockIdx.x * TE + i] = sum;
+    }
+  }
+}
+
+// db[e][n] = sum_t csum[e][t] head_w[t][n]   (bias grad of an identity last pool: dO = C head_W)
+__global__ void bias_from_csum_kernel(int E, int T, int d_out, const float* __restrict__ csum,
+                                      const float* __restrict__ head_w, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E * d_out) return;
+  const int e = i / d_out, n = i - e * d_out;
+  float s = 0.f;
+  for (int t = 0; t < T; ++t) s = fmaf(csum[e * T + t], head_w[(long)t * d_out + n], s);
+  out[i] = s;
 }
 
 template <int VPL, int MAXT>
@@ -704,15 +639,7 @@ static size_t combine_smem(bool bwd, int T, int K, int d_out, int vpl, int mt, i
   return s > tail ? s : tail;
 }
 
-static size_t combine_train_smem(int T, int K, int d_out, int vpl, int mt, int umax, int ldp) {
-  const int S = d_out / (32 * vpl), G = CB_WARPS / S;
-  GroupLayout L(umax, mt, ldp, umax, d_out);
-  size_t s = (size_t)T * d_out * 4 + (size_t)G * 4 * T * K * 4 + 16 + (size_t)G * L.bytes;
-  size_t tail = (size_t)G * T * d_out * 4 + (size_t)G * mt * 4 + 16 + (size_t)CB_THREADS * 8;
-  return s > tail ? s : tail;
-}
-
-static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream, bool train = false) {
+static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream) {
   if (a.T > CB_MAX_T) return set_error(SMES_ERR_SHAPE, "combine: T=%d exceeds %d", a.T, CB_MAX_T);
   if (a.umax > CB_MAX_U) return set_error(SMES_ERR_SHAPE, "combine: union bound %d exceeds %d", a.umax, CB_MAX_U);
   if (a.E > 1024) return set_error(SMES_ERR_SHAPE, "combine: E=%d exceeds 1024", a.E);
@@ -722,13 +649,12 @@ static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream, bool
   if (a.ldp % 4) return set_error(SMES_ERR_SHAPE, "combine: P row stride %d must be a multiple of 4", a.ldp);
   if (a.T * a.K > CB_MAX_TK) return set_error(SMES_ERR_SHAPE, "combine: T*K=%d exceeds %d", a.T * a.K, CB_MAX_TK);
   const int mt = a.T <= 4 ? 4 : a.T <= 8 ? 8 : a.T <= 16 ? 16 : 32;
-  const size_t smem = train ? combine_train_smem(a.T, a.K, a.d_out, vpl, mt, a.umax, a.ldp)
-                            : combine_smem(bwd, a.T, a.K, a.d_out, vpl, mt, a.umax, a.ldp > 0 ? a.ldp : 4, a.relu_last);
+  const size_t smem = combine_smem(bwd, a.T, a.K, a.d_out, vpl, mt, a.umax, a.ldp > 0 ? a.ldp : 4, a.relu_last);
   if (smem > 227 * 1024) return set_error(SMES_ERR_SHAPE, "combine: shared memory %zu too large", smem);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
 #define CB_CASE(V, M)                                                                                    \
   if (vpl == V && mt == M) {                                                                             \
-    auto kf = train ? combine_train_kernel<V, M> : bwd ? combine_bwd_kernel<V, M> : combine_fwd_kernel<V, M>; \
+    auto kf = bwd ? combine_bwd_kernel<V, M> : combine_fwd_kernel<V, M>;                                 \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     kf<<<grid, CB_THREADS, smem, st>>>(a);                                                               \
   } else
@@ -767,24 +693,48 @@ int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint
   return combine_launch(false, a, grid, stream);
 }
 
-int smes_combine_train(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
-                       const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
-                       const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits,
-                       float* preds, const float* labels, const float* lam, double* loss_part, float inv_b,
-                       int relu_last, void* dpacked, void* dz, const float* freq, float lb_coef, float* part_dw,
-                       float* part_db, int grid, void* stream) {
-  if (!P || !labels || !reps || !dpacked || !dz)
-    return set_error(SMES_ERR_STATE, "combine_train: P, labels, reps, dpacked and dz are required");
+int smes_combine_train(int T, int B, int E, int K, int umax, const uint32_t* umask, const int32_t* usize,
+                       const int32_t* row_of, const int32_t* active, const float* wsel, const float* head_b,
+                       const float* P, long ldp, float* logits, float* preds, const float* labels, const float* lam,
+                       double* loss_part, float inv_b, void* cmat, long ldc, void* dz, const float* freq,
+                       float lb_coef, float* part_db, float* part_csum, float* part_rb, int grid, void* stream) {
+  if (!P || !labels || !cmat || !dz) return set_error(SMES_ERR_STATE, "combine_train: P, labels, C and dz are required");
+  if (T > CB_MAX_T) return set_error(SMES_ERR_SHAPE, "combine_train: T=%d exceeds %d", T, CB_MAX_T);
+  if (ldc % 8 || ldc < T) return set_error(SMES_ERR_SHAPE, "combine_train: ldc=%ld must be >= T and a multiple of 8", ldc);
+  if ((T * E) % 8) return set_error(SMES_ERR_SHAPE, "combine_train: T*E must be a multiple of 8");
+  if (umax > CB_MAX_U || T * K > CB_MAX_TK) return set_error(SMES_ERR_SHAPE, "combine_train: union/budget too large");
   CombineArgs a{};
-  a.T = T; a.B = B; a.E = E; a.K = K; a.d_out = d_out; a.umax = umax;
-  a.umask = umask; a.usize = usize; a.row_of = row_of; a.active = active; a.wsel = wsel;
-  a.O = reinterpret_cast<const __nv_bfloat16*>(O); a.ldo = ldo; a.head_w = head_w; a.head_b = head_b;
-  a.P = const_cast<float*>(P); a.ldp = (int)ldp;
-  a.reps = reinterpret_cast<__nv_bfloat16*>(reps); a.logits = logits; a.preds = preds; a.labels = labels;
-  a.lam = lam; a.loss_part = loss_part; a.inv_b = inv_b; a.relu_last = relu_last;
-  a.dpacked = reinterpret_cast<__nv_bfloat16*>(dpacked); a.dz = reinterpret_cast<__nv_bfloat16*>(dz);
-  a.freq = freq; a.lb_coef = lb_coef; a.part_dw = part_dw; a.part_db = part_db;
-  return combine_launch(false, a, grid, stream, true);
+  a.T = T; a.B = B; a.E = E; a.K = K; a.umax = umax;
+  a.umask = umask; a.usize = usize; a.row_of = row_of; a.active = active; a.wsel = wsel; a.head_b = head_b;
+  a.P = const_cast<float*>(P); a.ldp = (int)ldp; a.logits = logits; a.preds = preds; a.labels = labels; a.lam = lam;
+  a.loss_part = loss_part; a.inv_b = inv_b; a.dz = reinterpret_cast<__nv_bfloat16*>(dz); a.freq = freq;
+  a.lb_coef = lb_coef; a.part_db = part_db;
+  const int mt = T <= 4 ? 4 : T <= 8 ? 8 : T <= 16 ? 16 : 32;
+  const int per_warp = 128 + umax * 4 + T * K * 16 + mt * 4 + 64;
+  const size_t smem = (size_t)CB_WARPS * ((per_warp + 15) & ~15) +
+                      (size_t)CB_WARPS * ((part_csum ? E * T : 0) + (part_rb ? T * E : 0)) * 4;
+  if (smem > 200 * 1024) return set_error(SMES_ERR_SHAPE, "combine_train: E*T too large for the fused bias sums");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  auto* cm = reinterpret_cast<__nv_bfloat16*>(cmat);
+#define CT_CASE(M)                                                                                      \
+  if (mt == M) {                                                                                        \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(combine_train_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    combine_train_kernel<M><<<grid, CB_THREADS, smem, st>>>(a, cm, (int)ldc, part_csum, part_rb);      \
+  } else
+  CT_CASE(4) CT_CASE(8) CT_CASE(16) CT_CASE(32) {}
+#undef CT_CASE
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "combine_train launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_bias_from_csum(int E, int T, int d_out, const float* csum, const float* head_w, float* out, void* stream) {
+  const int n = E * d_out;
+  bias_from_csum_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, T, d_out, csum, head_w,
+                                                                                           out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "bias_from_csum launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
 }
 
 int smes_combine_bwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,

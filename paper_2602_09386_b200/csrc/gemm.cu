@@ -26,6 +26,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 384;   // 4 non-epilogue warps + 8 epilogue warps (2 per TMEM lane quarter)
 constexpr int kEpiWarps = 8;
+constexpr int kBiasSplit = 4;   // bias tiles are split 4-way along K (db_out holds 4 slices)
 
 enum { MODE_RAGGED_M = 0, MODE_RAGGED_K = 1 };
 
@@ -113,10 +114,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     num_tiles = (seg_s[args.G] / BM) * n_tiles;
   } else {
     i_tiles = (args.I + BM - 1) / BM;
-    j_tiles = (args.N + BN - 1) / BN + (args.db_out != nullptr ? 1 : 0);
-    num_tiles = args.G * i_tiles * j_tiles;
+    j_tiles = (args.N + BN - 1) / BN;          // main column tiles; bias tiles (if any) come after all of them
+    num_tiles = args.G * i_tiles * j_tiles + (args.db_out != nullptr ? args.G * i_tiles * kBiasSplit : 0);
   }
   // decode: (group, row0 of A / i0, n0 / j0, k-block range)
+  int part = 0;
   auto decode = [&](int tile, int& g, int& r0, int& c0, int& kb0, int& nkb) {
     if (MODE == MODE_RAGGED_M) {
       int mt = tile / n_tiles;
@@ -126,14 +128,26 @@ __global__ void __launch_bounds__(kThreads, 1)
       kb0 = 0;
       nkb = (args.K + BK - 1) / BK;
     } else {
-      int per = i_tiles * j_tiles;
-      g = tile / per;
-      int r = tile - g * per;
-      r0 = (r / j_tiles) * BM;
-      c0 = (r % j_tiles) * BN;
-      if (args.db_out != nullptr && (r % j_tiles) == j_tiles - 1) c0 = args.N;   // bias tile: Q's ones column
-      kb0 = seg_s[g] / BK;
-      nkb = (seg_s[g + 1] - seg_s[g]) / BK;
+      const int per = i_tiles * j_tiles, n_main = args.G * per;
+      if (tile < n_main) {
+        g = tile / per;
+        const int r = tile - g * per;
+        r0 = (r / j_tiles) * BM;
+        c0 = (r % j_tiles) * BN;
+        kb0 = seg_s[g] / BK;
+        nkb = (seg_s[g + 1] - seg_s[g]) / BK;
+      } else {                                   // narrow bias tiles last, split along K: they fill the tail wave
+        const int t2 = tile - n_main;
+        g = t2 / (i_tiles * kBiasSplit);
+        const int r = t2 - g * i_tiles * kBiasSplit;
+        r0 = (r / kBiasSplit) * BM;
+        part = r % kBiasSplit;
+        c0 = args.N;                             // Q's ones column
+        const int all = (seg_s[g + 1] - seg_s[g]) / BK;
+        const int lo = all * part / kBiasSplit, hi = all * (part + 1) / kBiasSplit;
+        kb0 = seg_s[g] / BK + lo;
+        nkb = hi - lo;
+      }
     }
   };
 
@@ -236,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(tbase, t0);
           tmem_ld_wait();
           const int i = r0 + 32 * q + lane;
-          if (i < args.I) args.db_out[(size_t)g * args.I + i] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
+          if (i < args.I)
+            args.db_out[((size_t)part * args.G + g) * args.I + i] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
@@ -461,7 +476,7 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
                        const int* seg, float* C, float* db_out, void* stream) {
   if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
   if (I <= 0 || J <= 0) return set_error(SMES_ERR_SHAPE, "empty wgrad I=%d J=%d", I, J);
-  if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16 || (I * 2) % 16 || (J * 2) % 16)
+  if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16)
     return set_error(SMES_ERR_SHAPE, "wgrad strides must be 16-byte aligned");
   CUtensorMap ta, tb, tc;
   int rc;

@@ -28,7 +28,8 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
                                     const double* __restrict__ chunk_dmass, int32_t* __restrict__ chunk_base,
                                     int32_t* __restrict__ loads, double* __restrict__ stats_raw,
                                     int32_t* __restrict__ seg_pad, int32_t* __restrict__ seg_log,
-                                    int32_t* __restrict__ totals, unsigned int* __restrict__ ticket) {
+                                    int32_t* __restrict__ totals, unsigned int* __restrict__ ticket,
+                                    int32_t* __restrict__ seg_half) {
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[32];
   __shared__ double red[3][32];
@@ -94,11 +95,14 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     int p = 0, l = 0;
     for (int i = 0; i < E; ++i) {
       int ld = ((volatile int32_t*)loads)[i];
+      const int len = (ld + SEG_ALIGN - 1) / SEG_ALIGN * SEG_ALIGN;
       seg_pad[i] = p;
       seg_log[i] = l;
-      p += (ld + SEG_ALIGN - 1) / SEG_ALIGN * SEG_ALIGN;
+      if (seg_half) { seg_half[2 * i] = p; seg_half[2 * i + 1] = p + len / 2; }   // 64-row aligned halves
+      p += len;
       l += ld;
     }
+    if (seg_half) seg_half[2 * E] = p;
     seg_pad[E] = p;
     seg_log[E] = l;
     totals[0] = 0;   // totals[0:2] doubles as the one-group segment table [0, padded rows]
@@ -247,10 +251,11 @@ extern "C" {
 
 int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active, const double* chunk_mass,
                      const double* chunk_dmass, int32_t* chunk_base, int32_t* loads, double* stats_raw,
-                     int32_t* seg_pad, int32_t* seg_log, int32_t* totals, unsigned int* ticket, void* stream) {
+                     int32_t* seg_pad, int32_t* seg_log, int32_t* totals, unsigned int* ticket, int32_t* seg_half,
+                     void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
-                                         stats_raw, seg_pad, seg_log, totals, ticket);
+                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
   return SMES_OK;

@@ -181,11 +181,23 @@ class SMESEngine:
                 o[:, w] = 1.0
             self.outs.append(o)
         self.ld_out = [o.shape[1] for o in self.outs]
-        self.bits = [z(w // 32, R, dt=torch.int32) if (l.act == "relu" and i < len(self.p.layers) - 1) else None
+        self.bits = [z(w // 32, R, dt=torch.int32) if l.act == "relu" else None
                      for i, (w, l) in enumerate(zip(self.dims[1:], self.p.layers))]
         self.reps = z(T, B, self.d_out, dt=bf)     # required by the backward (head grads)
         self.ldp = _round(T, 4)
         self.P = z(R, self.ldp)                     # head projections P = O head_W^T of every packed row
+        self.ldc = _round(T, 16)
+        self.Cm = z(R, self.ldc, dt=bf)             # C[row, t] = w[row, t] * dlogit_t (training step)
+        self.hw_part = z(2 * E, T, self.d_out)      # dW_head split-K partials (expert halves)
+        # bias grads folded into the training combine: last (identity) pool via per-(expert, task)
+        # sums of C, router via column sums of dz (per-warp smem accumulators, fixed-order reduce)
+        fits = 8 * 4 * (E * T + T * E) <= 150 * 1024
+        self.fuse_rb = fits
+        self.fuse_b_last = fits and self.p.layers[-1].act == "identity"
+        self.part_csum = z(self.grid, E, T) if self.fuse_b_last else None
+        self.part_rb = z(self.grid, T * E) if self.fuse_rb else None
+        self.csum = z(E, T)
+        self.seg_half = z(2 * E + 1, dt=i32)
         self.logits = z(T, B)
         self.preds = z(T, B)
         self.labels = z(T, B)
@@ -199,7 +211,7 @@ class SMESEngine:
         edges = [min(self.B_pad, (self.B_pad // self.rw_splits) // 128 * 128 * i) for i in range(self.rw_splits)]
         self.seg_router_split = torch.tensor(edges + [self.B_pad], dtype=i32, device=dev)
         self.rw_part = z(self.rw_splits, T * E, d)
-        self.rb_part = z(self.rw_splits, T * E)
+        self.rb_part = z(4, self.rw_splits, T * E)
         # backward
         self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
         self.dX = z(R, d, dt=bf)
@@ -215,6 +227,7 @@ class SMESEngine:
             off += n
         nl = len(self.p.layers)
         self.g_layers = [(views[i], views[nl + i]) for i in range(nl)]
+        self.db_slices = [z(4, E, l.d_out) for l in self.p.layers]   # wgrad bias K-slices
         self.g_router_w, self.g_router_b, self.g_head_w, self.g_head_b = views[2 * nl:]
         self.colsum_part = z(R // 128, max(max(self.dims), T * E))
         self.dh_router = z(B, d)
@@ -236,6 +249,10 @@ class SMESEngine:
         self.b32 = [l.bias.detach().to(dev, torch.float32).contiguous() for l in p.layers]
         self.head_w = p.head_w.detach().to(dev, torch.float32).contiguous()
         self.head_w_bf = self.head_w.to(torch.bfloat16).reshape(1, T, -1).contiguous()
+        ldc = _round(T, 16)
+        hwt = torch.zeros(1, self.head_w.shape[1], ldc, dtype=torch.bfloat16, device=dev)
+        hwt[0, :, :T] = self.head_w.t().to(torch.bfloat16)
+        self.head_wT_bf = hwt
         self.head_b = p.head_b.detach().to(dev, torch.float32).contiguous()
         tw = p.task_weights if p.task_weights is not None else torch.ones(T)
         self.tw = tw.detach().to(dev, torch.float64).contiguous()
@@ -272,11 +289,11 @@ class SMESEngine:
         self.route(s, frozen=frozen)
         _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
-             ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), s)
+             ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), ptr(self.seg_half), s)
         _tagged("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
              ptr(self.loads), ptr(self.h), self.ldh, ptr(self.X), self.ld_in[0], ptr(self.row_of), self.umax,
              ptr(self.gather_inst),
-             ptr(self.gather_exp), ptr(self.d_outs[-1]), self.d_out, self.d_out, s)
+             ptr(self.gather_exp), ptr(self.Cm), self.ldc, self.ldc, s)
         self.experts_forward(s)
 
     def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
@@ -291,12 +308,11 @@ class SMESEngine:
             bs = B if batch_scale is None else batch_scale
             lbb = B if lb_batch is None else lb_batch
             lb_coef = self.beta * E / (self.K * lbb * T)
-            _tagged("combine_train", "smes_combine_train", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask),
-                    ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
-                    self.d_out, ptr(self.head_w), ptr(self.head_b), ptr(self.P), self.ldp, ptr(self.reps),
-                    ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam), ptr(self.loss_part),
-                    1.0 / bs, int(self.p.layers[-1].act == "relu"), ptr(self.d_outs[-1]), ptr(self.dz),
-                    ptr(self.freq32), lb_coef, ptr(self.part_dw), ptr(self.part_db), self.grid, s)
+            _tagged("combine_train", "smes_combine_train", T, B, E, self.K, self.umax, ptr(self.umask),
+                    ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.head_b),
+                    ptr(self.P), self.ldp, ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam),
+                    ptr(self.loss_part), 1.0 / bs, ptr(self.Cm), self.ldc, ptr(self.dz), ptr(self.freq32), lb_coef,
+                    ptr(self.part_db), ptr(self.part_csum), ptr(self.part_rb), self.grid, s)
             _tagged("loss_finalize", "smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
                     self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
             return
@@ -343,7 +359,19 @@ class SMESEngine:
         lbb = B if lb_batch is None else lb_batch
         lb_coef = self.beta * E / (K * lbb * T)
         relu_last = int(self.p.layers[-1].act == "relu")
-        if not getattr(self, "_fused_bwd", False):
+        R = self.rows_cap
+        if getattr(self, "_fused_bwd", False):
+            # d_packed = C head_W (K = T padded to 16), relu mask of O if the last pool is relu
+            last = len(self.p.layers) - 1
+            _tagged("dpacked_gemm", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.head_wT_bf), 1,
+                    self.d_out, self.ldc, 0, ptr(self.totals), None, 0, None, ptr(self.bits[last]), R,
+                    ptr(self.d_outs[-1]), self.d_out, 0, R, s)
+            # dW_head = C^T O, split-K over expert halves, fixed-order reduce
+            _tagged("head_wgrad", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(self.outs[-1]), self.d_out, R,
+                    2 * E, T, self.d_out, ptr(self.seg_half), ptr(self.hw_part), None, s)
+            _tagged("head_wgrad", "smes_part_reduce", ptr(self.hw_part), 2 * E, T * self.d_out, ptr(self.g_head_w), s)
+        else:
+            self.d_outs[-1].zero_()      # dense-reading path (API only): pad rows must be zero
             _tagged("combine_bwd", "smes_combine_bwd", T, B, E, K, self.d_out, self.umax, ptr(self.umask),
                     ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
                     self.d_out, ptr(self.head_w), ptr(self.P), self.ldp, ptr(self.reps), ptr(self.preds),
@@ -359,24 +387,40 @@ class SMESEngine:
             if i > 0:   # dgrad into the previous layer's output, masked by its relu
                 _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
-            # wgrad + bias grad in one launch (ones column of the layer input, see _alloc)
-            _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do, di,
-                    ptr(self.seg_pad), ptr(gw), ptr(gb), s)
+            fused_last = i == n_layers - 1 and self.fuse_b_last and getattr(self, "_fused_bwd", False)
+            if fused_last:
+                # db = (per-expert sums of C) head_W: no bias tiles needed
+                _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
+                        di, ptr(self.seg_pad), ptr(gw), None, s)
+                _tagged(f"fc{i + 1}_bias", "smes_part_reduce", ptr(self.part_csum), self.grid, E * T, ptr(self.csum), s)
+                _tagged(f"fc{i + 1}_bias", "smes_bias_from_csum", E, T, do, ptr(self.csum), ptr(self.head_w), ptr(gb),
+                        s)
+            else:
+                # wgrad + bias grad in one launch (ones column of the layer input, see _alloc)
+                _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
+                        di, ptr(self.seg_pad), ptr(gw), ptr(self.db_slices[i]), s)
+                _tagged(f"fc{i + 1}_wgrad", "smes_part_reduce", ptr(self.db_slices[i]), 4, E * do, ptr(gb), s)
         # dX = d_out0 W_0
         _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
              ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
         # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
         _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
              ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
+        rb_fused = self.fuse_rb and getattr(self, "_fused_bwd", False)
         _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits,
-                T * E, d, ptr(self.seg_router_split), ptr(self.rw_part), ptr(self.rb_part), s)
+                T * E, d, ptr(self.seg_router_split), ptr(self.rw_part), None if rb_fused else ptr(self.rb_part), s)
         _tagged("router_wgrad", "smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d,
                 ptr(self.g_router_w), s)
-        _tagged("router_wgrad", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
-                ptr(self.g_router_b), s)
+        if rb_fused:
+            _tagged("router_bias", "smes_part_reduce", ptr(self.part_rb), self.grid, T * E, ptr(self.g_router_b), s)
+        else:
+            _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), 4 * self.rw_splits, T * E,
+                    ptr(self.g_router_b), s)
         _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
              ptr(self.dh_router), ptr(self.d_hidden), s)
-        _tagged("head_reduce", "smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out, ptr(self.g_head_w), s)
+        if not getattr(self, "_fused_bwd", False):
+            _tagged("head_reduce", "smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out,
+                    ptr(self.g_head_w), s)
         _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
     def step(self):
@@ -393,6 +437,9 @@ class SMESEngine:
              "router_dgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 4), "tensor"),
              "router_wgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 2), "tensor"),
              "head_proj": (2.0 * n_act * do * T, n_act * (do * 2 + T * 4), "hbm"),
+             "combine_train": (0.0, B * (U * T * 4 + T * K * 8 + T * 16 + T * E * 2) + n_act * self.ldc * 2, "hbm"),
+             "dpacked_gemm": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2), "hbm"),
+             "head_wgrad": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2), "hbm"),
              "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4), "hbm"),
              "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8, "hbm"),
              "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12), "hbm"),

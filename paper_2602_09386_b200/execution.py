@@ -210,7 +210,7 @@ def build_execution_plan(unions, num_experts: int, device=None) -> ExecutionPlan
     if B:
         s = _stream()
         call("smes_plan_reduce", C, E, ptr(chunk_union), ptr(chunk_active), ptr(chunk_mass), ptr(chunk_dmass),
-             ptr(chunk_base), ptr(loads), ptr(stats_raw), ptr(seg_pad), ptr(seg_log), ptr(totals), ptr(ticket), s)
+             ptr(chunk_base), ptr(loads), ptr(stats_raw), ptr(seg_pad), ptr(seg_log), ptr(totals), ptr(ticket), None, s)
         call("smes_plan_scatter", B, E, 8, rpw, ptr(umask), ptr(chunk_base), ptr(seg_pad), ptr(loads), None, 8,
              None, 8, ptr(row_of), umax, ptr(gather_inst), ptr(gather_exp), None, 8, 8, s)
     return ExecutionPlan(E, B, umax, rows_cap, seg_pad, seg_log, loads, totals, row_of, gather_inst, gather_exp,

@@ -148,10 +148,11 @@ def test_ragged_k_wgrad_with_fused_bias(I, J):
     qb[:, J] = 1.0
     seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
     out = torch.full((E, I, J), float("nan"), device=dev)
-    db = torch.full((E, I), float("nan"), device=dev)
-    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J + 64, R, E, I, J, ptr(seg_t), ptr(out), ptr(db),
+    db4 = torch.full((4, E, I), float("nan"), device=dev)
+    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J + 64, R, E, I, J, ptr(seg_t), ptr(out), ptr(db4),
          torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
+    db = db4.sum(0)
     for e in range(E):
         lo, hi = seg[e], seg[e + 1]
         ref = pb[lo:hi].float().T @ qb[lo:hi, :J].float()

@@ -31,7 +31,10 @@ def run_case(name):
     p, h, y, lam, beta = make_case(seed, B, T, E, d, d_out, ks, ka, d_ff=d_ff, router_scale=rs, **extra)
     eng = SMESEngine(to_engine_params(p, lam, beta), B, ks, ka, dense_probs_in_stats=dense)
     eng.set_inputs(torch.tensor(h, device="cuda"), torch.tensor(y, device="cuda", dtype=torch.float32))
-    eng.step()
+    eng.forward(with_loss=True)          # inference-style forward: materialises task reps
+    torch.cuda.synchronize()
+    eng.reps_fwd = eng.reps.clone()
+    eng.step()                           # training step (fused combine backward when sparse)
     torch.cuda.synchronize()
     return p, h, y, lam, beta, dense, eng
 
@@ -70,7 +73,7 @@ def test_layer_parity(name):
     for li in range(len(p.layers)):
         got = eng.outs[li][:, :eng.dims[li + 1]].float().cpu().numpy()[rows]
         assert rel(got, f.layer_outs[li]) < BF16_TOL, li
-    assert rel(eng.reps.float().cpu().numpy(), f.task_reps) < BF16_TOL
+    assert rel(eng.reps_fwd.float().cpu().numpy(), f.task_reps) < BF16_TOL
     assert rel(eng.logits.cpu().numpy(), f.head_logits) < BF16_TOL
     assert rel(eng.preds.cpu().numpy(), f.predictions) < BF16_TOL
 
