@@ -74,9 +74,8 @@ int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* um
  *      ragged-M: C[m,n] = act(sum_k A[m,k] W_g[n,k] + bias_g[n])   (b_mn = 0, fwd)
  *                C[m,n] = mask(sum_k A[m,k] W_g[k,n])              (b_mn = 1, dgrad)
  *      ragged-K: C_g[i,j] = sum_{m in g} P[m,i] Q[m,j]           (wgrad, fp32 out)
- *                db_g[i]  = sum_{m in g} P[m,i]   when db_out != NULL: Q must carry a column of
- *                ones at index J (ldq >= J+64); extra N=64 tiles compute the bias grad as 4 K-slices
- *                db_out[s][g][i] (s < 4) whose sum is db (fixed order, see smes_part_reduce).
+ *                db_g[i]  = sum_{m in g} P[m,i]   when db_out != NULL (G, I): an extra N=16 MMA per
+ *                K-step against a constant ones tile in smem, inside the j0 = 0 output tiles.
  *      seg = padded group offsets (device). */
 int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, int G, int N, int K, int b_mn,
                        const int* seg, const float* bias, int act, uint32_t* relu_bits_out,

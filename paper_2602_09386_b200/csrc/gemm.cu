@@ -26,7 +26,6 @@ constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int kThreads = 384;   // 4 non-epilogue warps + 8 epilogue warps (2 per TMEM lane quarter)
 constexpr int kEpiWarps = 8;
-constexpr int kBiasSplit = 4;   // bias tiles are split 4-way along K (db_out holds 4 slices)
 
 enum { MODE_RAGGED_M = 0, MODE_RAGGED_K = 1 };
 
@@ -45,14 +44,17 @@ struct GemmArgs {
   float* db_out;              // ragged-K: per-group column sums of P via Q's ones column (G, I), or null
 };
 
-template <int BN>
+template <int BN, int MODE>
 struct Smem {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  // ragged-K (wgrad) runs long K loops: one TMEM accumulator + 3 stages leave room for the ones tile
+  static constexpr int kStages = MODE == MODE_RAGGED_K ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6);
+  static constexpr int kAccStages = MODE == MODE_RAGGED_K ? 1 : 2;
   static constexpr int kA = BM * BK * 2;        // 16 KB
   static constexpr int kB = BN * BK * 2;        // 32 / 16 KB
   static constexpr int kStg = 32 * 128;         // 4 KB per staging buffer
   static constexpr int kOffB = kStages * kA;
-  static constexpr int kOffStg = kOffB + kStages * kB;
+  static constexpr int kOffOnes = kOffB + kStages * kB;                       // ragged-K: 64x64 bf16 ones tile
+  static constexpr int kOffStg = kOffOnes + (MODE == MODE_RAGGED_K ? 8192 : 0);
   static constexpr int kOffBar = kOffStg + kEpiWarps * kStg;
   static constexpr int kOffSeg = kOffBar + 256;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 12 + 1024;   // + barriers + group table + alignment slack
@@ -73,12 +75,14 @@ template <int BN, int MODE, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
-  using S = Smem<BN>;
+  using S = Smem<BN, MODE>;
   constexpr int kStages = S::kStages;
+  constexpr int kAcc = S::kAccStages;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::kOffB;
+  uint8_t* sOnes = smem + S::kOffOnes;
   uint8_t* sStg = smem + S::kOffStg;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* empty = full + kStages;
@@ -89,8 +93,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const bool fused_bias = MODE == MODE_RAGGED_K && args.db_out != nullptr;
 
   for (int i = threadIdx.x; i <= args.G; i += blockDim.x) seg_s[i] = args.seg[i];
+  if (MODE == MODE_RAGGED_K) {
+    // ones tile as an MN-major SW128 B operand: B'[k][n] = (n == 0) for 64 k-rows x 64 n-cols
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(sOnes);
+    for (int i = threadIdx.x; i < 8192 / 4; i += blockDim.x) o32[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int k = threadIdx.x;   // element n = 0 of row k sits in 16B chunk (0 ^ (k & 7))
+      reinterpret_cast<__nv_bfloat16*>(sOnes + k * 128 + (k & 7) * 16)[0] = __float2bfloat16_rn(1.f);
+    }
+    fence_proxy_async_smem();
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
@@ -114,11 +130,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     num_tiles = (seg_s[args.G] / BM) * n_tiles;
   } else {
     i_tiles = (args.I + BM - 1) / BM;
-    j_tiles = (args.N + BN - 1) / BN;          // main column tiles; bias tiles (if any) come after all of them
-    num_tiles = args.G * i_tiles * j_tiles + (args.db_out != nullptr ? args.G * i_tiles * kBiasSplit : 0);
+    j_tiles = (args.N + BN - 1) / BN;
+    num_tiles = args.G * i_tiles * j_tiles;
   }
   // decode: (group, row0 of A / i0, n0 / j0, k-block range)
-  int part = 0;
   auto decode = [&](int tile, int& g, int& r0, int& c0, int& kb0, int& nkb) {
     if (MODE == MODE_RAGGED_M) {
       int mt = tile / n_tiles;
@@ -128,26 +143,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       kb0 = 0;
       nkb = (args.K + BK - 1) / BK;
     } else {
-      const int per = i_tiles * j_tiles, n_main = args.G * per;
-      if (tile < n_main) {
-        g = tile / per;
-        const int r = tile - g * per;
-        r0 = (r / j_tiles) * BM;
-        c0 = (r % j_tiles) * BN;
-        kb0 = seg_s[g] / BK;
-        nkb = (seg_s[g + 1] - seg_s[g]) / BK;
-      } else {                                   // narrow bias tiles last, split along K: they fill the tail wave
-        const int t2 = tile - n_main;
-        g = t2 / (i_tiles * kBiasSplit);
-        const int r = t2 - g * i_tiles * kBiasSplit;
-        r0 = (r / kBiasSplit) * BM;
-        part = r % kBiasSplit;
-        c0 = args.N;                             // Q's ones column
-        const int all = (seg_s[g + 1] - seg_s[g]) / BK;
-        const int lo = all * part / kBiasSplit, hi = all * (part + 1) / kBiasSplit;
-        kb0 = seg_s[g] / BK + lo;
-        nkb = hi - lo;
-      }
+      const int per = i_tiles * j_tiles;
+      g = tile / per;
+      const int r = tile - g * per;
+      r0 = (r / j_tiles) * BM;
+      c0 = (r % j_tiles) * BN;
+      kb0 = seg_s[g] / BK;
+      nkb = (seg_s[g + 1] - seg_s[g]) / BK;
     }
   };
 
@@ -161,8 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         decode(tile, g, r0, c0, kb0, nkb);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          const bool tail = (MODE == MODE_RAGGED_K) && args.db_out != nullptr && c0 == args.N;
-          mbar_expect_tx(&full[stage], S::kA + (tail ? 8192 : S::kB));
+          mbar_expect_tx(&full[stage], S::kA + S::kB);
           uint8_t* a = sA + stage * S::kA;
           uint8_t* b = sB + stage * S::kB;
           const int k0 = (kb0 + kb) * BK;
@@ -179,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, k0);
 #pragma unroll
-            for (int j = 0; j < (tail ? 1 : BN / 64); ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -190,21 +191,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= MMA issuer (single thread)
       constexpr bool A_MN = (MODE == MODE_RAGGED_K);
       constexpr bool BMN = (MODE == MODE_RAGGED_K) || B_MN;
-      constexpr uint32_t idesc_main = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
-      constexpr uint32_t idesc_tail = umma_idesc_bf16(BM, 64, A_MN ? 1 : 0, BMN ? 1 : 0);
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN, A_MN ? 1 : 0, BMN ? 1 : 0);
+      constexpr uint32_t idesc_bias = umma_idesc_bf16(BM, 16, 1, 1);     // D[:, 0:16] += A * ones-tile
+      const uint32_t ones_addr = smem_u32(sOnes);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         int g, r0, c0, kb0, nkb;
         decode(tile, g, r0, c0, kb0, nkb);
-        const int acc = it & 1;
-        const uint32_t aphase = (it >> 1) & 1;
+        const int acc = it % kAcc;
+        const uint32_t aphase = (it / kAcc) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        const uint32_t idesc = (MODE == MODE_RAGGED_K && args.db_out != nullptr && c0 == args.N) ? idesc_tail
-                                                                                                : idesc_main;
+        const bool with_bias = fused_bias && c0 == 0;    // once per (group, i-tile)
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -217,6 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint64_t bd = BMN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
                               : umma_desc_sw128(b_addr + k * 32, 16, 1024);
             tc_mma_f16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+            if (with_bias)   // bias grad db[i] = sum_m P[m, i]: same A, constant ones B (cols BN..BN+15)
+              tc_mma_f16(tmem_base + BN, ad, umma_desc_sw128(ones_addr + k * 2048, 8192, 1024), idesc_bias,
+                         (kb | k) != 0);
           }
           tc_commit(&empty[stage]);        // smem slot free once these MMAs have read it
           if (++stage == kStages) { stage = 0; phase ^= 1; }
@@ -237,25 +241,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       int g, r0, c0, kb0, nkb;
       decode(tile, g, r0, c0, kb0, nkb);
-      const int acc = it & 1;
-      const uint32_t aphase = (it >> 1) & 1;
+      const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
+      // prefetch the relu bit-mask words of this warp's chunks before waiting for the MMA
+      uint32_t mword[BN / 32];
+      if (MODE == MODE_RAGGED_M && args.bits_in != nullptr) {
+#pragma unroll
+        for (int w = 0; w < BN / 32; ++w) {
+          const int n = c0 + 32 * w;
+          const bool mine = ((w * 32) / cpc) % 2 == par;
+          mword[w] = (mine && n < ncols) ? __ldg(&args.bits_in[(size_t)(n >> 5) * args.bits_ld + row]) : 0u;
+        }
+      }
+      const int acc = it % kAcc;
+      const uint32_t aphase = (it / kAcc) & 1;
       mbar_wait(&tfull[acc], aphase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
-      const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
-      if (MODE == MODE_RAGGED_K && args.db_out != nullptr && c0 == args.N) {
-        // bias tile: column 0 of the accumulator is sum_m P[m, i] * 1 = db_g[i]
-        if (par == 0) {
-          uint32_t t0[32];
-          tmem_ld32(tbase, t0);
-          tmem_ld_wait();
-          const int i = r0 + 32 * q + lane;
-          if (i < args.I)
-            args.db_out[((size_t)part * args.G + g) * args.I + i] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        continue;
+      if (fused_bias && c0 == 0 && par == 0) {
+        // bias grad: column 0 of the ones-product accumulator at TMEM column BN
+        uint32_t t0[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + BN, t0);
+        tmem_ld_wait();
+        if (row < args.I) args.db_out[(size_t)g * args.I + row] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
       }
       for (int cc = par; cc < BN / cpc; cc += 2) {
         const int n = c0 + cc * cpc;
@@ -298,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (args.act == 1) {
 #pragma unroll
-            for (int j = 0; j < 64; ++j) f[j] = fmaxf(f[j], 0.f);
+            for (int j = 0; j < 64; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
           }
           if (args.bits_out != nullptr) {
 #pragma unroll
@@ -314,8 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (args.bits_in != nullptr) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              if (h * 32 < cpc && n + h * 32 < ncols) {
-                const uint32_t w = __ldg(&args.bits_in[(size_t)((n >> 5) + h) * args.bits_ld + row]);
+              if (h * 32 < cpc) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int ww = 0; ww < BN / 32; ++ww)
+                  if (ww == (cc * cpc) / 32 + h) w = mword[ww];
 #pragma unroll
                 for (int j = 0; j < 32; ++j) f[h * 32 + j] = ((w >> j) & 1u) ? f[h * 32 + j] : 0.f;
               }
@@ -405,14 +415,15 @@ template <int BN, int MODE, bool B_MN>
 static int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& args,
                   cudaStream_t st) {
   auto kern = grouped_gemm_kernel<BN, MODE, B_MN>;
+  using SM = Smem<BN, MODE>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::kBytes);
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kBytes);
     if (ea != cudaSuccess)
-      return set_error(SMES_ERR_CUDA, "grouped_gemm smem attribute (%d B): %s", Smem<BN>::kBytes, cudaGetErrorString(ea));
+      return set_error(SMES_ERR_CUDA, "grouped_gemm smem attribute (%d B): %s", SM::kBytes, cudaGetErrorString(ea));
     attr = true;
   }
-  kern<<<num_sms(), kThreads, Smem<BN>::kBytes, st>>>(a, b, c, args);
+  kern<<<num_sms(), kThreads, SM::kBytes, st>>>(a, b, c, args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "grouped_gemm launch: %s", cudaGetErrorString(e));
   return SMES_OK;
@@ -485,10 +496,8 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
     uint32_t box[2] = {64, 64};
     if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, P, dims, str, box))) return rc;
   }
-  if (db_out && ldq < J + 64)
-    return set_error(SMES_ERR_SHAPE, "wgrad bias fusion needs ldq >= J + 64 (ones column at J), ldq=%ld J=%d", ldq, J);
   {
-    uint64_t dims[2] = {(uint64_t)(db_out ? J + 64 : J), (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
+    uint64_t dims[2] = {(uint64_t)J, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
     uint32_t box[2] = {64, 64};
     if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Q, dims, str, box))) return rc;
   }

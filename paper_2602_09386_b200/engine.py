@@ -211,7 +211,7 @@ class SMESEngine:
         edges = [min(self.B_pad, (self.B_pad // self.rw_splits) // 128 * 128 * i) for i in range(self.rw_splits)]
         self.seg_router_split = torch.tensor(edges + [self.B_pad], dtype=i32, device=dev)
         self.rw_part = z(self.rw_splits, T * E, d)
-        self.rb_part = z(4, self.rw_splits, T * E)
+        self.rb_part = z(self.rw_splits, T * E)
         # backward
         self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
         self.dX = z(R, d, dt=bf)
@@ -227,7 +227,6 @@ class SMESEngine:
             off += n
         nl = len(self.p.layers)
         self.g_layers = [(views[i], views[nl + i]) for i in range(nl)]
-        self.db_slices = [z(4, E, l.d_out) for l in self.p.layers]   # wgrad bias K-slices
         self.g_router_w, self.g_router_b, self.g_head_w, self.g_head_b = views[2 * nl:]
         self.colsum_part = z(R // 128, max(max(self.dims), T * E))
         self.dh_router = z(B, d)
@@ -398,8 +397,7 @@ class SMESEngine:
             else:
                 # wgrad + bias grad in one launch (ones column of the layer input, see _alloc)
                 _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
-                        di, ptr(self.seg_pad), ptr(gw), ptr(self.db_slices[i]), s)
-                _tagged(f"fc{i + 1}_wgrad", "smes_part_reduce", ptr(self.db_slices[i]), 4, E * do, ptr(gb), s)
+                        di, ptr(self.seg_pad), ptr(gw), ptr(gb), s)
         # dX = d_out0 W_0
         _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
              ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
@@ -414,7 +412,7 @@ class SMESEngine:
         if rb_fused:
             _tagged("router_bias", "smes_part_reduce", ptr(self.part_rb), self.grid, T * E, ptr(self.g_router_b), s)
         else:
-            _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), 4 * self.rw_splits, T * E,
+            _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
                     ptr(self.g_router_b), s)
         _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
              ptr(self.dh_router), ptr(self.d_hidden), s)

@@ -134,7 +134,7 @@ def test_ragged_k_wgrad(I, J):
 
 @pytest.mark.parametrize("I,J", [(256, 512), (512, 256), (128, 128)])
 def test_ragged_k_wgrad_with_fused_bias(I, J):
-    """db_g[i] = sum_m P[m, i] via the ones column at Q[:, J] (one extra N=64 tile)."""
+    """db_g[i] = sum_m P[m, i] via the in-tile ones-tile MMA (Q's extra columns are ignored)."""
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(7 * I + J)
     loads = [200, 0, 77, 640]
@@ -148,11 +148,10 @@ def test_ragged_k_wgrad_with_fused_bias(I, J):
     qb[:, J] = 1.0
     seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
     out = torch.full((E, I, J), float("nan"), device=dev)
-    db4 = torch.full((4, E, I), float("nan"), device=dev)
-    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J + 64, R, E, I, J, ptr(seg_t), ptr(out), ptr(db4),
+    db = torch.full((E, I), float("nan"), device=dev)
+    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J + 64, R, E, I, J, ptr(seg_t), ptr(out), ptr(db),
          torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
-    db = db4.sum(0)
     for e in range(E):
         lo, hi = seg[e], seg[e + 1]
         ref = pb[lo:hi].float().T @ qb[lo:hi, :J].float()
