@@ -115,6 +115,20 @@ int smes_combine_train(int T, int B, int E, int K, int umax, const uint32_t* uma
  * from smes_combine_train (optional, may be NULL). */
 int smes_bias_from_csum(int E, int T, int d_out, const float* csum, const float* head_w, float* out, void* stream);
 
+/* ---- head folding for the training step when the last expert pool is the identity
+ *      (model.py:202-208 composed with execution.py:126-158; backward training.py:146-191):
+ *      G (E, ldg, d_in) bf16 = head_w W_e (rows >= T zero), c (E, ldg) = head_w b_e, so the head
+ *      projections are P = H G_e^T + c_e (an N = ldg GEMM) and d_packed never materialises.
+ *      smes_unfold_grads expands Qt (E, d_in, ldg) = per-expert H^T C into dW = head_w^T Q_e,
+ *      db = head_w^T csum_e and dW_head = sum_e (Q_e W_e^T + csum_e b_e^T).
+ *      work: fp32 scratch of smes_fold_work_floats(E, T, d_out, d_in) floats (split-K partials). */
+int smes_fold_work_floats(int E, int T, int d_out, int d_in);
+int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* head_w, const void* W_bf16,
+                    const float* b, void* G_bf16, float* c, float* work, void* stream);
+int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Qt, long q_expert_stride,
+                      const float* csum, long csum_expert_stride, const float* head_w, const void* W_bf16,
+                      const float* b, float* dW, float* db, float* work, float* d_head_w, void* stream);
+
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
                         float* freq_f32, void* stream);

@@ -37,6 +37,9 @@ SIGNATURES = {
     "smes_combine_bwd": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, L, P, P, P, P, F, I, P, P, P, F, I, P, P, P, I, P],
     "smes_combine_train": [I, I, I, I, I, P, P, P, P, P, P, P, L, P, P, P, P, P, F, P, L, P, P, F, P, P, P, I, P],
     "smes_bias_from_csum": [I, I, I, P, P, P, P],
+    "smes_fold_work_floats": [I, I, I, I],
+    "smes_fold_heads": [I, I, I, I, I, P, P, P, P, P, P, P],
+    "smes_unfold_grads": [I, I, I, I, I, P, L, P, L, P, P, P, P, P, P, P, P],
     "smes_stats_finalize": [I, I, D, I, P, P, P, P],
     "smes_loss_finalize": [I, P, D, D, P, P, P],
     "smes_seg_colsum": [P, L, L, I, P, I, P, P, P],
@@ -47,14 +50,15 @@ SIGNATURES = {
 }
 _RESTYPE = {"smes_last_error": C.c_char_p}
 # entry points that return a value rather than a status
-_VALUE_FNS = {"smes_abi_version", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
+_VALUE_FNS = {"smes_abi_version", "smes_fold_work_floats", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_last_error"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_scatter": 1, "smes_gemm_ragged_m": 1,
                     "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
-                    "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1}
+                    "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,
+                    "smes_fold_heads": 2, "smes_unfold_grads": 3}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 

@@ -40,25 +40,30 @@ struct GemmArgs {
   uint32_t* bits_out;         // relu bitmask out: [(N/32)][bits_ld] words, or null
   const uint32_t* bits_in;    // relu bitmask applied to the output (dgrad), or null
   int bits_ld;
-  int out_fp32;
   float* db_out;              // ragged-K: per-group column sums of P via Q's ones column (G, I), or null
 };
 
+// Shared-memory plan.  ragged-M tiles are epilogue(store)-paced at the c2 shapes, so every
+// epilogue warp double-buffers its 4 KB TMA-store staging chunk (ncu r1: the single-buffer
+// bulk wait was the top stall); ragged-K (wgrad) runs long K loops and stores once per tile.
 template <int BN, int MODE>
 struct Smem {
-  // ragged-K (wgrad) runs long K loops: one TMEM accumulator + 3 stages leave room for the ones tile
-  static constexpr int kStages = MODE == MODE_RAGGED_K ? (BN == 256 ? 3 : 5) : (BN == 256 ? 4 : 6);
+  static constexpr int kStages = MODE == MODE_RAGGED_K ? (BN == 256 ? 3 : BN == 128 ? 5 : 6)
+                                                       : (BN == 256 ? 3 : BN == 128 ? 4 : 6);
   static constexpr int kAccStages = MODE == MODE_RAGGED_K ? 1 : 2;
-  static constexpr int kA = BM * BK * 2;        // 16 KB
-  static constexpr int kB = BN * BK * 2;        // 32 / 16 KB
-  static constexpr int kStg = 32 * 128;         // 4 KB per staging buffer
+  static constexpr int kStgBufs = MODE == MODE_RAGGED_K ? 1 : 2;
+  static constexpr int kA = BM * BK * 2;                         // 16 KB
+  static constexpr int kB = (BN < 64 && MODE == MODE_RAGGED_K ? 64 : BN) * BK * 2;   // MN-major boxes are 64 wide
+  static constexpr int kStg = 32 * 128;                          // 4 KB per staging buffer
   static constexpr int kOffB = kStages * kA;
   static constexpr int kOffOnes = kOffB + kStages * kB;                       // ragged-K: 64x64 bf16 ones tile
   static constexpr int kOffStg = kOffOnes + (MODE == MODE_RAGGED_K ? 8192 : 0);
-  static constexpr int kOffBar = kOffStg + kEpiWarps * kStg;
+  static constexpr int kOffBias = kOffStg + kEpiWarps * kStgBufs * kStg;      // 64 fp32 per epilogue warp
+  static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
   static constexpr int kOffSeg = kOffBar + 256;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 12 + 1024;   // + barriers + group table + alignment slack
   static constexpr int kTmemCols = 2 * BN;
+  static_assert(kBytes <= 232448, "shared memory plan exceeds 227 KB");
 };
 
 __device__ __forceinline__ int find_group(const int* seg_s, int G, int row) {
@@ -71,13 +76,17 @@ __device__ __forceinline__ int find_group(const int* seg_s, int G, int row) {
   return lo;
 }
 
-template <int BN, int MODE, bool B_MN>
+template <int BN, int MODE, bool B_MN, bool F32>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
   using S = Smem<BN, MODE>;
   constexpr int kStages = S::kStages;
   constexpr int kAcc = S::kAccStages;
+  constexpr int CPC = F32 ? 32 : 64;                 // output columns per 128-byte staged row chunk
+  constexpr int NCH = BN / CPC > 0 ? BN / CPC : 1;   // chunks per tile
+  constexpr int MYCH = (NCH + 1) / 2;                // chunks per epilogue warp (column parity split)
+  constexpr int NBBOX = BN / 64 > 0 ? BN / 64 : 1;   // 64-wide MN-major B boxes per stage
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, k0);
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
+            for (int j = 0; j < NBBOX; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
           }
           if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
@@ -230,26 +239,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     // ================= epilogue: TMEM -> regs -> (bias, act, mask) -> smem (SW128) -> TMA store
-    // warp w owns TMEM lanes 32*(w%4).. and every other column chunk (parity (w-4)/4)
+    // warp w owns TMEM lanes 32*(w%4).. and the column chunks of parity (w-4)/4
     const int q = warp & 3;
     const int par = (warp - 4) >> 2;
-    uint8_t* stg = sStg + (warp - 4) * S::kStg;
-    const bool fp32out = args.out_fp32 != 0;
-    const int cpc = fp32out ? 32 : 64;
+    uint8_t* stg0 = sStg + (warp - 4) * S::kStgBufs * S::kStg;
+    float* sbias = reinterpret_cast<float*>(smem + S::kOffBias) + (warp - 4) * 64;
     const int ncols = args.N;
-    int it = 0;
+    int it = 0, nstore = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       int g, r0, c0, kb0, nkb;
       decode(tile, g, r0, c0, kb0, nkb);
       const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
-      // prefetch the relu bit-mask words of this warp's chunks before waiting for the MMA
-      uint32_t mword[BN / 32];
-      if (MODE == MODE_RAGGED_M && args.bits_in != nullptr) {
+      // prefetch (before waiting for the MMA): relu bit-mask words and bias values of my chunks
+      uint32_t mw[MYCH][2];
+      float bv[MYCH][2];
 #pragma unroll
-        for (int w = 0; w < BN / 32; ++w) {
-          const int n = c0 + 32 * w;
-          const bool mine = ((w * 32) / cpc) % 2 == par;
-          mword[w] = (mine && n < ncols) ? __ldg(&args.bits_in[(size_t)(n >> 5) * args.bits_ld + row]) : 0u;
+      for (int i = 0; i < MYCH; ++i) {
+        const int n = c0 + (par + 2 * i) * CPC;
+        const bool ok = (par + 2 * i) < NCH && n < ncols;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mw[i][h] = 0u;
+          bv[i][h] = 0.f;
+          if (MODE == MODE_RAGGED_M && h * 32 < CPC && ok && n + 32 * h < ncols) {
+            if (args.bits_in != nullptr) mw[i][h] = __ldg(&args.bits_in[(size_t)((n >> 5) + h) * args.bits_ld + row]);
+            if (args.bias != nullptr && n + 32 * h + lane < ncols)
+              bv[i][h] = __ldg(args.bias + (size_t)g * args.N + n + 32 * h + lane);
+          }
         }
       }
       const int acc = it % kAcc;
@@ -264,53 +280,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         if (row < args.I) args.db_out[(size_t)g * args.I + row] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
       }
-      for (int cc = par; cc < BN / cpc; cc += 2) {
-        const int n = c0 + cc * cpc;
-        if (n >= ncols) break;
-        float f[64];
+#pragma unroll
+      for (int i = 0; i < MYCH; ++i) {
+        const int cc = par + 2 * i;
+        const int n = c0 + cc * CPC;
+        if (cc >= NCH || n >= ncols) break;
+        float f[CPC];
         if (nkb > 0) {
-          uint32_t t0[32];
-          tmem_ld32(tbase + cc * cpc, t0);
-          if (!fp32out) {
-            uint32_t t1[32];
-            tmem_ld32(tbase + cc * cpc + 32, t1);
+#pragma unroll
+          for (int h = 0; h < CPC / 32; ++h) {
+            uint32_t t[32];
+            tmem_ld32(tbase + cc * CPC + 32 * h, t);
             tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = __uint_as_float(t1[j]); }
-          } else {
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = 0.f; }
+            for (int j = 0; j < 32; ++j) f[32 * h + j] = __uint_as_float(t[j]);
           }
         } else {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) f[j] = 0.f;
+          for (int j = 0; j < CPC; ++j) f[j] = 0.f;
         }
         if (MODE == MODE_RAGGED_M) {
           if (args.bias != nullptr) {
-            const float* bp = args.bias + (size_t)g * args.N + n;
-            if (n + cpc <= ncols) {
+            // bias of these CPC columns, broadcast through a warp-private smem slot
+            __syncwarp();
 #pragma unroll
-              for (int j = 0; j < 64; j += 4) {
-                if (j < cpc) {
-                  float4 bb = __ldg(reinterpret_cast<const float4*>(bp + j));
-                  f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
-                }
-              }
-            } else {
+            for (int h = 0; h < CPC / 32; ++h) sbias[32 * h + lane] = bv[i][h];
+            __syncwarp();
 #pragma unroll
-              for (int j = 0; j < 64; ++j)
-                if (j < cpc && n + j < ncols) f[j] += __ldg(bp + j);
+            for (int j = 0; j < CPC; j += 4) {
+              const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
+              f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
             }
           }
           if (args.act == 1) {
 #pragma unroll
-            for (int j = 0; j < 64; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
+            for (int j = 0; j < CPC; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
           }
           if (args.bits_out != nullptr) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (h * 32 < cpc && n + h * 32 < ncols) {
+            for (int h = 0; h < CPC / 32; ++h) {
+              if (n + h * 32 < ncols) {
                 uint32_t w = 0;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
@@ -320,26 +329,26 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (args.bits_in != nullptr) {
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (h * 32 < cpc) {
-                uint32_t w = 0;
+            for (int h = 0; h < CPC / 32; ++h) {
+              const uint32_t w = mw[i][h];
 #pragma unroll
-                for (int ww = 0; ww < BN / 32; ++ww)
-                  if (ww == (cc * cpc) / 32 + h) w = mword[ww];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) f[h * 32 + j] = ((w >> j) & 1u) ? f[h * 32 + j] : 0.f;
-              }
+              for (int j = 0; j < 32; ++j) f[h * 32 + j] = ((w >> j) & 1u) ? f[h * 32 + j] : 0.f;
             }
           }
         }
-        // stage into smem (128 B per row, 128B swizzle) and TMA-store a {cpc x 32} box
-        if (lane == 0) bulk_wait_read<0>();
+        // stage into smem (128 B per row, 128B swizzle) and TMA-store a {CPC x 32} box; the
+        // staging buffers alternate so this chunk's STS overlaps the previous chunk's store
+        uint8_t* stg = stg0 + (nstore % S::kStgBufs) * S::kStg;
+        ++nstore;
+        if (lane == 0) {
+          if (S::kStgBufs == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+        }
         __syncwarp();
         uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           uint4 pk;
-          if (fp32out) {
+          if (F32) {
             pk = make_uint4(__float_as_uint(f[4 * c]), __float_as_uint(f[4 * c + 1]), __float_as_uint(f[4 * c + 2]),
                             __float_as_uint(f[4 * c + 3]));
           } else {
@@ -411,10 +420,10 @@ static int num_sms() {
   return g_num_sms;
 }
 
-template <int BN, int MODE, bool B_MN>
+template <int BN, int MODE, bool B_MN, bool F32>
 static int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& args,
                   cudaStream_t st) {
-  auto kern = grouped_gemm_kernel<BN, MODE, B_MN>;
+  auto kern = grouped_gemm_kernel<BN, MODE, B_MN, F32>;
   using SM = Smem<BN, MODE>;
   static bool attr = false;
   if (!attr) {
@@ -427,6 +436,15 @@ static int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "grouped_gemm launch: %s", cudaGetErrorString(e));
   return SMES_OK;
+}
+
+template <int BN>
+static int launch_m(bool b_mn, bool f32, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                    const GemmArgs& args, cudaStream_t st) {
+  if (b_mn) return f32 ? launch<BN, MODE_RAGGED_M, true, true>(a, b, c, args, st)
+                       : launch<BN, MODE_RAGGED_M, true, false>(a, b, c, args, st);
+  return f32 ? launch<BN, MODE_RAGGED_M, false, true>(a, b, c, args, st)
+             : launch<BN, MODE_RAGGED_M, false, false>(a, b, c, args, st);
 }
 
 }  // namespace smes
@@ -445,6 +463,8 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                      K, N);
   if ((bits_out || bits_in) && (N % 32))
     return set_error(SMES_ERR_SHAPE, "relu bitmask needs N %% 32 == 0 (N=%d)", N);
+  // N <= 32 with fp32 out (head projections, K = T outputs): a narrow BN = 32 tile
+  const bool narrow = N <= 32 && out_fp32 && !b_mn;
   CUtensorMap ta, tb, tc;
   int rc;
   {
@@ -455,8 +475,7 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
   if (!b_mn) {  // W (G, N, K) K-major
     uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)G};
     uint64_t str[2] = {(uint64_t)K * 2, (uint64_t)N * K * 2};
-    uint32_t box[3] = {64, (uint32_t)(N >= 256 ? 256 : 128), 1};
-    if (N >= 256) box[1] = 256;
+    uint32_t box[3] = {64, (uint32_t)(narrow ? 32 : N >= 256 ? 256 : 128), 1};
     if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, W, dims, str, box))) return rc;
   } else {      // W (G, K, N): element (n, k) at W[g][k][n]
     uint64_t dims[3] = {(uint64_t)N, (uint64_t)K, (uint64_t)G};
@@ -471,16 +490,12 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                        str, box)))
       return rc;
   }
-  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, out_fp32, nullptr};
+  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, nullptr};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const bool wide = N >= 256;
-  if (wide) {
-    // K-major B box is {64, 256}: requires BN == 256
-    return b_mn ? launch<256, MODE_RAGGED_M, true>(ta, tb, tc, args, st)
-                : launch<256, MODE_RAGGED_M, false>(ta, tb, tc, args, st);
-  }
-  return b_mn ? launch<128, MODE_RAGGED_M, true>(ta, tb, tc, args, st)
-              : launch<128, MODE_RAGGED_M, false>(ta, tb, tc, args, st);
+  if (narrow) return launch<32, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
+  // K-major B box is {64, 256} for N >= 256: requires BN == 256
+  if (N >= 256) return launch_m<256>(b_mn, out_fp32, ta, tb, tc, args, st);
+  return launch_m<128>(b_mn, out_fp32, ta, tb, tc, args, st);
 }
 
 int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
@@ -507,10 +522,11 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
     uint32_t box[3] = {32, 32, 1};
     if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, str, box))) return rc;
   }
-  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, 1, db_out};
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (J >= 256) return launch<256, MODE_RAGGED_K, true>(ta, tb, tc, args, st);
-  return launch<128, MODE_RAGGED_K, true>(ta, tb, tc, args, st);
+  if (J <= 16) return launch<16, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+  if (J >= 256) return launch<256, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+  return launch<128, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
 }
 
 }  // extern "C"

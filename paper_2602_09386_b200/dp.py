@@ -37,7 +37,10 @@ class DataParallelStep:
 
     # the three segments between the two collectives
     def _part_a(self):
-        self.eng.forward_a()
+        if getattr(self.eng, "can_fold", False):
+            self.eng.forward_a(fold=True)     # training step: heads folded into the last pool
+        else:
+            self.eng.forward_a()
 
     def _part_b(self):
         self.eng.forward_b(with_loss=True, batch_times_tasks=float(self.b_global * self.eng.T), train=True,

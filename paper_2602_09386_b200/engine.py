@@ -97,7 +97,7 @@ class SMESEngine:
 
     def __init__(self, params: SMESParams, batch_size: int, k_shared: int, k_adaptive: int,
                  dense_probs_in_stats: bool = False, keep_reps: bool = True,
-                 device: torch.device | str | None = None):
+                 device: torch.device | str | None = None, csum_from_gemm: bool = False):
         _require_cuda()
         self.dev = torch.device(device or "cuda")
         p = params
@@ -130,10 +130,15 @@ class SMESEngine:
         self.d_out = dims[-1]
         self.grid = call("smes_combine_grid", B, T, self.d_out)
         self.dense = bool(dense_probs_in_stats)
+        self._csum_from_gemm = bool(csum_from_gemm)
         self.keep_reps = keep_reps
         self.umax = min(E, ks + T * ka)
         self.rows_cap = _round(B * self.umax + E * 127, 128)
         self.B_pad = _round(B, 128)
+        # head folding (csrc/fold.cu) for training steps: needs an identity last pool and the
+        # sparse LB reading (the fused training combine produces the row coefficients C)
+        self.can_fold = p.layers[-1].act == "identity" and not self.dense and T <= 32
+        self._folded = False
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
         self._alloc()
@@ -184,7 +189,7 @@ class SMESEngine:
         self.bits = [z(w // 32, R, dt=torch.int32) if l.act == "relu" else None
                      for i, (w, l) in enumerate(zip(self.dims[1:], self.p.layers))]
         self.reps = z(T, B, self.d_out, dt=bf)     # required by the backward (head grads)
-        self.ldp = _round(T, 4)
+        self.ldp = _round(T, 8)
         self.P = z(R, self.ldp)                     # head projections P = O head_W^T of every packed row
         self.ldc = _round(T, 16)
         self.Cm = z(R, self.ldc, dt=bf)             # C[row, t] = w[row, t] * dlogit_t (training step)
@@ -193,10 +198,20 @@ class SMESEngine:
         # sums of C, router via column sums of dz (per-warp smem accumulators, fixed-order reduce)
         fits = 8 * 4 * (E * T + T * E) <= 150 * 1024
         self.fuse_rb = fits
-        self.fuse_b_last = fits and self.p.layers[-1].act == "identity"
+        # csum_from_gemm: take the per-(expert, task) sums of C from the folded wgrad's ones column
+        # instead of the combine's smem partials (automatic when those do not fit)
+        self.fuse_b_last = fits and self.p.layers[-1].act == "identity" and not self._csum_from_gemm
         self.part_csum = z(self.grid, E, T) if self.fuse_b_last else None
         self.part_rb = z(self.grid, T * E) if self.fuse_rb else None
         self.csum = z(E, T)
+        if self.can_fold:
+            di = self.dims[-2]
+            self.ldg = _round(T, 8)
+            self.G_fold = z(E, self.ldg, di, dt=bf)         # head_w W_last (per expert), rows >= T zero
+            self.c_fold = z(E, self.ldg)                    # head_w b_last
+            self.q_rows = di if self.fuse_b_last else di + 1   # + the ones column -> per-expert sums of C
+            self.Qt = z(E, self.q_rows, self.ldg)           # per-expert H^T C
+            self.fold_work = z(call("smes_fold_work_floats", E, T, self.d_out, di))
         self.seg_half = z(2 * E + 1, dt=i32)
         self.logits = z(T, B)
         self.preds = z(T, B)
@@ -277,9 +292,11 @@ class SMESEngine:
         self.forward_a()
         self.forward_b(with_loss=with_loss)
 
-    def forward_a(self, frozen: bool = False):
+    def forward_a(self, frozen: bool = False, fold: bool = False):
         """Router GEMM -> routing -> plan -> expert GEMMs.  Ends with the per-expert
-        LoadStats sums in ``stats_raw`` (the data-parallel exchange point)."""
+        LoadStats sums in ``stats_raw`` (the data-parallel exchange point).
+        ``fold`` (training steps only, see csrc/fold.cu): the last identity pool is folded into
+        the task heads, so its output O and the task reps are not materialised."""
         s = self._stream()
         T, E, B, d = self.T, self.E, self.B, self.d
         # router logits z = h W_r^T + b_r  (B, T*E) fp32
@@ -293,7 +310,9 @@ class SMESEngine:
              ptr(self.loads), ptr(self.h), self.ldh, ptr(self.X), self.ld_in[0], ptr(self.row_of), self.umax,
              ptr(self.gather_inst),
              ptr(self.gather_exp), ptr(self.Cm), self.ldc, self.ldc, s)
-        self.experts_forward(s)
+        if fold and not self.can_fold:
+            raise ConfigError("head folding needs an identity last expert pool and sparse LB statistics")
+        self.experts_forward(s, fold=fold)
 
     def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
                   batch_scale: int | None = None, lb_batch: int | None = None):
@@ -331,14 +350,25 @@ class SMESEngine:
              ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), int(frozen), s)
 
-    def experts_forward(self, s):
+    def experts_forward(self, s, fold: bool = False):
         R = self.rows_cap
         inp = self.X
-        for i, l in enumerate(self.p.layers):
+        L = len(self.p.layers)
+        for i, l in enumerate(self.p.layers[:L - 1] if fold else self.p.layers):
             _tagged(f"fc{i + 1}_fwd", "smes_gemm_ragged_m", ptr(inp), self.ld_in[i], R, ptr(self.w_bf[i]), self.E,
                     self.dims[i + 1], self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act],
                     ptr(self.bits[i]), None, R, ptr(self.outs[i]), self.ld_out[i], 0, R, s)
             inp = self.outs[i]
+        self._folded = fold
+        if fold:
+            # P = H G_e^T + c_e with G_e = head_W W_last,e: the last pool and the heads in one N = T GEMM
+            di = self.dims[L - 1]
+            _tagged("fold_heads", "smes_fold_heads", self.E, self.T, self.ldg, self.d_out, di, ptr(self.head_w),
+                    ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold), ptr(self.fold_work), s)
+            _tagged(f"fc{L}_fwd_folded", "smes_gemm_ragged_m", ptr(inp), self.ld_in[L - 1], R, ptr(self.G_fold),
+                    self.E, self.ldg, di, 0, ptr(self.seg_pad), ptr(self.c_fold), 0, None, None, 0, ptr(self.P),
+                    self.ldp, 1, R, s)
+            return
         # head projections of every packed row: P = O head_W^T (tcgen05 GEMM, N = T)
         _tagged("head_proj", "smes_gemm_ragged_m", ptr(self.outs[-1]), self.d_out, R, ptr(self.head_w_bf), 1, self.T,
                 self.d_out, 0, ptr(self.totals), None, 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
@@ -358,8 +388,33 @@ class SMESEngine:
         lbb = B if lb_batch is None else lb_batch
         lb_coef = self.beta * E / (K * lbb * T)
         relu_last = int(self.p.layers[-1].act == "relu")
-        R = self.rows_cap
-        if getattr(self, "_fused_bwd", False):
+        n_layers = len(self.p.layers)
+        fused = getattr(self, "_fused_bwd", False)
+        folded = fused and self._folded
+        top = n_layers - 1             # first pool handled by the generic dgrad/wgrad loop
+        if folded:
+            # the last (identity) pool through the folded heads (csrc/fold.cu):
+            #   d_in_last = (C G_e) * relu-mask,  Qt_e = H_e^T C,  dW/db/dW_head from Qt and csum
+            L = n_layers
+            di = self.dims[L - 1]
+            inp = self.X if L == 1 else self.outs[L - 2]
+            dst = self.dX if L == 1 else self.d_outs[L - 2]
+            mask = self.bits[L - 2] if L >= 2 else None
+            _tagged(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), E, di,
+                    self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
+            _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm), self.ldc,
+                    R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qt), None, s)
+            if self.fuse_b_last:
+                _tagged("csum", "smes_part_reduce", ptr(self.part_csum), self.grid, E * T, ptr(self.csum), s)
+                cs, cs_es = self.csum, T
+            else:
+                cs, cs_es = self.Qt[:, di, :], self.q_rows * self.ldg
+            gw, gb = self.g_layers[L - 1]
+            _tagged("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qt),
+                    self.q_rows * self.ldg, ptr(cs), cs_es, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]),
+                    ptr(gw), ptr(gb), ptr(self.fold_work), ptr(self.g_head_w), s)
+            top = n_layers - 2
+        elif fused:
             # d_packed = C head_W (K = T padded to 16), relu mask of O if the last pool is relu
             last = len(self.p.layers) - 1
             _tagged("dpacked_gemm", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.head_wT_bf), 1,
@@ -377,8 +432,7 @@ class SMESEngine:
                     ptr(self.labels), ptr(self.lam), 1.0 / bs, relu_last, ptr(self.d_outs[-1]), ptr(self.dz),
                     ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw), ptr(self.part_db),
                     self.grid, s)
-        n_layers = len(self.p.layers)
-        for i in range(n_layers - 1, -1, -1):
+        for i in range(top, -1, -1):
             dout = self.d_outs[i]
             inp = self.X if i == 0 else self.outs[i - 1]
             gw, gb = self.g_layers[i]
@@ -386,7 +440,7 @@ class SMESEngine:
             if i > 0:   # dgrad into the previous layer's output, masked by its relu
                 _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
-            fused_last = i == n_layers - 1 and self.fuse_b_last and getattr(self, "_fused_bwd", False)
+            fused_last = i == n_layers - 1 and self.fuse_b_last and fused
             if fused_last:
                 # db = (per-expert sums of C) head_W: no bias tiles needed
                 _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
@@ -399,8 +453,9 @@ class SMESEngine:
                 _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
                         di, ptr(self.seg_pad), ptr(gw), ptr(gb), s)
         # dX = d_out0 W_0
-        _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
-             ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
+        if not (folded and n_layers == 1):
+            _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
+                    ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
         # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
         _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
              ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
@@ -422,7 +477,7 @@ class SMESEngine:
         _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
     def step(self):
-        self.forward_a()
+        self.forward_a(fold=self.can_fold)
         self.forward_b(with_loss=True, train=True)
         self.backward()
 

@@ -161,3 +161,87 @@ def test_ragged_k_wgrad_with_fused_bias(I, J):
             continue
         assert (out[e] - ref).abs().max().item() / ref.abs().max().item() < 1e-5
         assert (db[e] - refb).abs().max().item() / refb.abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("N,K", [(8, 512), (16, 256), (32, 128)])
+def test_ragged_m_narrow_fp32(N, K):
+    """N <= 32 fp32-out tile (folded head projections P = H G_e^T + c_e)."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(5 * N + K)
+    loads = [300, 0, 129, 1, 517]
+    E = len(loads)
+    seg, x = _packed(loads, K, g, dev)
+    R = x.shape[0]
+    xb = x.to(torch.bfloat16).contiguous()
+    w = (torch.randn(E, N, K, generator=g, device=dev) / K ** 0.5).to(torch.bfloat16).contiguous()
+    b = torch.randn(E, N, generator=g, device=dev).contiguous()
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.full((R, N), float("nan"), device=dev)
+    call("smes_gemm_ragged_m", ptr(xb), K, R, ptr(w), E, N, K, 0, ptr(seg_t), ptr(b), 0, None, None, 0,
+         ptr(out), N, 1, R, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, n = seg[e], loads[e]
+        if n == 0:
+            continue
+        ref = xb[lo:lo + n].float() @ w[e].float().T + b[e]
+        err = (out[lo:lo + n] - ref).abs().max().item() / ref.abs().max().item()
+        assert err < 1e-5, (e, err)
+
+
+@pytest.mark.parametrize("K,N", [(8, 512), (16, 256), (8, 128)])
+def test_ragged_m_dgrad_small_k_masked(K, N):
+    """K = T dgrad of the folded heads: C[m, n] = mask(sum_t A[m, t] G_g[t, n]), A with a wider ld."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(K + N)
+    loads = [200, 0, 77, 384]
+    E = len(loads)
+    lda = 16
+    seg, a = _packed(loads, lda, g, dev)
+    a[:, K:] = 0
+    R = a.shape[0]
+    ab = a.to(torch.bfloat16).contiguous()
+    w = (torch.randn(E, K, N, generator=g, device=dev)).to(torch.bfloat16).contiguous()
+    bits = torch.randint(-2 ** 31, 2 ** 31 - 1, (N // 32, R), generator=g, device=dev, dtype=torch.int64).to(torch.int32)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.zeros(R, N, device=dev, dtype=torch.bfloat16)
+    call("smes_gemm_ragged_m", ptr(ab), lda, R, ptr(w), E, N, K, 1, ptr(seg_t), None, 0, None, ptr(bits), R,
+         ptr(out), N, 0, R, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, n = seg[e], loads[e]
+        if n == 0:
+            continue
+        ref = ab[lo:lo + n, :K].float() @ w[e].float()
+        word = bits[:, lo:lo + n].T.long()
+        mask = torch.cat([((word[:, j:j + 1] >> torch.arange(32, device=dev)) & 1) for j in range(N // 32)], 1).bool()
+        ref = torch.where(mask, ref, torch.zeros_like(ref))
+        assert (out[lo:lo + n].float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
+@pytest.mark.parametrize("I,J", [(512, 8), (256, 16), (513, 8)])
+def test_ragged_k_wgrad_narrow(I, J):
+    """Folded wgrad Qt_g[i, t] = sum_{m in g} H[m, i] C[m, t] with J = T <= 16 (BN = 16 tile);
+    I = d + 1 reads the ones column of H (per-expert sums of C)."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(I + J)
+    loads = [300, 0, 129, 640]
+    E = len(loads)
+    ldp = (I + 63) // 64 * 64
+    seg, pm = _packed(loads, ldp, g, dev)
+    _, qm = _packed(loads, 16, g, dev)
+    qm[:, J:] = 0
+    R = pm.shape[0]
+    pb, qb = pm.to(torch.bfloat16).contiguous(), qm.to(torch.bfloat16).contiguous()
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.full((E, I, J), float("nan"), device=dev)
+    call("smes_gemm_ragged_k", ptr(pb), ldp, ptr(qb), 16, R, E, I, J, ptr(seg_t), ptr(out), None,
+         torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, hi = seg[e], seg[e + 1]
+        ref = pb[lo:hi, :I].float().T @ qb[lo:hi, :J].float()
+        if loads[e] == 0:
+            assert torch.all(out[e] == 0)
+            continue
+        assert (out[e] - ref).abs().max().item() / ref.abs().max().item() < 1e-5

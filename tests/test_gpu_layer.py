@@ -23,25 +23,39 @@ CASES = {
     "c2_small_batch": (2, 2048, 8, 32, 256, 256, 4, 2, 512, 1e-3, False, {}),
     "dense_stats_taskw": (3, 700, 4, 16, 128, 128, 1, 2, 256, 1.0, True, dict(rand_task_w=True, rand_lam=True)),
     "no_shared": (4, 512, 4, 16, 128, 128, 0, 3, None, 1.0, False, {}),
+    "single_identity": (5, 1024, 4, 16, 128, 128, 2, 1, None, 1e-3, False, dict(last_act="identity")),
+    "c2_t5_csum_gemm": (6, 1536, 5, 32, 256, 256, 4, 2, 512, 1e-3, False, dict(rand_lam=True)),
 }
+# engine options per case (csum_from_gemm: per-expert sums of C from the folded wgrad's ones column)
+ENGINE_OPTS = {"c2_t5_csum_gemm": dict(csum_from_gemm=True)}
 
 
-def run_case(name):
+def run_case(name, fold=True):
     seed, B, T, E, d, d_out, ks, ka, d_ff, rs, dense, extra = CASES[name]
     p, h, y, lam, beta = make_case(seed, B, T, E, d, d_out, ks, ka, d_ff=d_ff, router_scale=rs, **extra)
-    eng = SMESEngine(to_engine_params(p, lam, beta), B, ks, ka, dense_probs_in_stats=dense)
+    eng = SMESEngine(to_engine_params(p, lam, beta), B, ks, ka, dense_probs_in_stats=dense,
+                     **ENGINE_OPTS.get(name, {}))
     eng.set_inputs(torch.tensor(h, device="cuda"), torch.tensor(y, device="cuda", dtype=torch.float32))
-    eng.forward(with_loss=True)          # inference-style forward: materialises task reps
+    eng.forward(with_loss=True)          # inference-style forward: materialises every pool output + task reps
     torch.cuda.synchronize()
     eng.reps_fwd = eng.reps.clone()
-    eng.step()                           # training step (fused combine backward when sparse)
+    eng.outs_fwd = [o.clone() for o in eng.outs]
+    # training step (fused combine backward when sparse; heads folded into an identity last pool)
+    eng.forward_a(fold=fold and eng.can_fold)
+    eng.forward_b(with_loss=True, train=True)
+    eng.backward()
     torch.cuda.synchronize()
     return p, h, y, lam, beta, dense, eng
 
 
-@pytest.mark.parametrize("name", list(CASES))
-def test_layer_parity(name):
-    p, h, y, lam, beta, dense, eng = run_case(name)
+PARAMS = [(n, True) for n in CASES] + [(n, False) for n in ("c1_mlp", "c2_small_batch", "single_identity")]
+
+
+@pytest.mark.parametrize("name,fold", PARAMS)
+def test_layer_parity(name, fold):
+    p, h, y, lam, beta, dense, eng = run_case(name, fold)
+    if fold and eng.can_fold:
+        assert eng._folded, "identity last pool + sparse stats must take the folded training path"
     T, E, B, ks, ka = eng.T, eng.E, eng.B, eng.ks, eng.ka
     z = eng.z.double().cpu().numpy().reshape(B, T, E).transpose(1, 0, 2)
 
@@ -71,7 +85,7 @@ def test_layer_parity(name):
     f = O.forward_sparse(h, p, ks, ka, logits=z, frozen=r, frozen_plan=plan)
     rows = np.nonzero(keep)[0]
     for li in range(len(p.layers)):
-        got = eng.outs[li][:, :eng.dims[li + 1]].float().cpu().numpy()[rows]
+        got = eng.outs_fwd[li][:, :eng.dims[li + 1]].float().cpu().numpy()[rows]
         assert rel(got, f.layer_outs[li]) < BF16_TOL, li
     assert rel(eng.reps_fwd.float().cpu().numpy(), f.task_reps) < BF16_TOL
     assert rel(eng.logits.cpu().numpy(), f.head_logits) < BF16_TOL
