@@ -129,6 +129,19 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
                       const float* csum, long csum_expert_stride, const float* head_w, const void* W_bf16,
                       const float* b, float* dW, float* db, float* work, float* d_head_w, void* stream);
 
+/* ---- fused expert MLP for training steps (csrc/mlp.cu): two chained tcgen05 MMAs per 128-row
+ *      tile with the d_ff-wide intermediate handed over in shared memory.
+ *      smes_mlp_fwd:   H = relu(X W1_e^T + b1_e) (+ relu bit-mask, H optional), P = H G_e^T + c_e
+ *                      (execution.py:126-158 for both pools + the folded heads model.py:202-208).
+ *      smes_mlp_dgrad: dH = (C G_e) * mask, dX = dH W1_e (training.py:180-192); dH optional.
+ *      d in {64, 128, 256, 512} (dgrad: <= 256), d_ff % 128 == 0, ldg <= 16. */
+int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
+                 const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* relu_bits,
+                 long bits_ld, void* H, long ldh, float* P, long ldp, void* stream);
+int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
+                   int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, void* dX, long lddx,
+                   void* dH, long lddh, void* stream);
+
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
                         float* freq_f32, void* stream);

@@ -1,0 +1,763 @@
+// Fused expert-MLP kernels for the training step (BASELINE expert MLP d -> d_ff -> d_out with
+// ReLU after fc1 and the identity last pool folded into the task heads, csrc/fold.cu).
+//
+// Both kernels chain two tcgen05 MMAs per 128-row tile through shared memory: the epilogue
+// warps turn the first accumulator (TMEM) into the bf16 A operand of the second MMA, chunk by
+// chunk (128 columns of d_ff), so the d_ff-wide intermediate never makes a round trip to HBM
+// between the two products.
+//
+//   mlp_fwd   (fc1 + folded fc2/heads, execution.py:126-158 twice + model.py:202-208):
+//       S_c = X W1[c]^T            (K = d, TMA-fed, N = 128)
+//       H_c = relu(S_c + b1[c])    -> relu bit-mask, H (kept for the weight gradients), smem
+//       P  += H_c G[c]^T           (K = 128, N = 16: the head projections, fp32)
+//   mlp_dgrad (training.py:180-192 for the two pools):
+//       S_c = C G[c]               (K = T: the rank-T d_packed through the folded heads)
+//       dH_c = S_c * mask[c]       -> smem
+//       dX += dH_c W1[c]           (K = 128, N = d)
+//
+// Rows are the padded expert-major packed rows of the execution plan (128-row aligned
+// segments, so a tile never straddles two experts); group offsets stay on the device.
+//
+// Warp roles (384 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4).. and the 64-column half (w-4)/4 of a chunk).
+#include "ptx.cuh"
+#include "smes_capi.h"
+
+namespace smes {
+namespace mlp {
+
+constexpr int BM = 128;          // rows per tile
+constexpr int CH = 128;          // d_ff columns per chunk
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;
+
+struct FwdArgs {
+  const int* seg;                // (E+1) padded segment offsets
+  int E, d, d_ff, ldp;
+  const float* b1;               // (E, d_ff)
+  const float* c;                // (E, ldg) folded head bias
+  int ldg;
+  uint32_t* bits;                // [(d_ff/32)][bits_ld] relu bit-mask of H
+  int bits_ld;
+  float* P;                      // (rows, ldp) fp32 head projections
+  int store_h;                   // write H through tmH
+};
+
+struct DgradArgs {
+  const int* seg;
+  int E, d, d_ff;
+  const uint32_t* bits;          // relu mask of H
+  int bits_ld;
+  int store_dh;                  // also write dH through tmDH (for the separate fc1 weight-gradient GEMM)
+};
+
+__device__ __forceinline__ int find_group(const int* seg_s, int G, int row) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (seg_s[mid] <= row) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Ring-buffer bookkeeping: slot and parity of the i-th use of an n-slot ring.
+__device__ __forceinline__ int slot_of(int i, int n) { return i % n; }
+__device__ __forceinline__ uint32_t par_of(int i, int n) { return (uint32_t)((i / n) & 1); }
+
+// Named barrier for the epilogue warps only (id 1, 256 threads).
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// 32 lanes x 16 columns TMEM load
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+// ============================================================================ forward
+template <int DK>     // d / 64
+struct FwdSmem {
+  static constexpr int kXS = DK <= 4 ? DK + 2 : DK;    // X k-block ring (16 KB slots): next tile prefetch
+  static constexpr int kWS = DK <= 4 ? 4 : 3;          // W1 k-block ring (16 KB: 128 n x 64 k)
+  static constexpr int kGS = DK <= 4 ? 4 : 2;          // G chunk ring (4 KB: 2 x {64 f, 16 t})
+  static constexpr int kOffX = 0;
+  static constexpr int kOffW = kOffX + kXS * 16384;
+  static constexpr int kOffG = kOffW + kWS * 16384;
+  static constexpr int kOffH = kOffG + kGS * 4096;      // 2 x 16 KB atoms (128 rows x 64 cols)
+  static constexpr int kOffBias = kOffH + 32768;        // 64 fp32 per epilogue warp
+  static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
+  static constexpr int kOffSeg = kOffBar + 512;
+  static constexpr int kBytes = kOffSeg + 257 * 4 + 1024;
+  static_assert(kBytes <= 232448, "mlp_fwd smem");
+};
+
+template <int DK>
+__global__ void __launch_bounds__(kThreads, 1)
+    mlp_fwd_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+                   const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmH,
+                   const FwdArgs a) {
+  using S = FwdSmem<DK>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sX = smem + S::kOffX;
+  uint8_t* sW = smem + S::kOffW;
+  uint8_t* sG = smem + S::kOffG;
+  uint8_t* sH = smem + S::kOffH;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* xfull = bar;                    // [kXS]
+  uint64_t* xempty = xfull + S::kXS;        // [kXS]
+  uint64_t* wfull = xempty + S::kXS;        // [kWS]
+  uint64_t* wempty = wfull + S::kWS;        // [kWS]
+  uint64_t* gfull = wempty + S::kWS;        // [kGS]
+  uint64_t* gempty = gfull + S::kGS;        // [kGS]
+  uint64_t* sfull = gempty + S::kGS;        // [2]
+  uint64_t* sempty = sfull + 2;             // [2]
+  uint64_t* hfull = sempty + 2;             // [1]
+  uint64_t* hempty = hfull + 1;             // [1]
+  uint64_t* pfull = hempty + 1;             // [2]
+  uint64_t* pempty = pfull + 2;             // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NC = a.d_ff / CH;
+  for (int i = threadIdx.x; i <= a.E; i += blockDim.x) seg_s[i] = a.seg[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX); tma_prefetch(&tmW1); tma_prefetch(&tmG); tma_prefetch(&tmH);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S::kXS; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 1); }
+    for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps);
+      mbar_init(&pfull[i], 1); mbar_init(&pempty[i], kEpiWarps / 2);
+    }
+    mbar_init(hfull, kEpiWarps);
+    mbar_init(hempty, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = seg_s[a.E] / BM;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer
+      int xi = 0, wi = 0, gi = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int r0 = tile * BM;
+        const int e = find_group(seg_s, a.E, r0);
+        for (int kb = 0; kb < DK; ++kb, ++xi) {
+          const int s = slot_of(xi, S::kXS);
+          mbar_wait(&xempty[s], par_of(xi, S::kXS) ^ 1);
+          mbar_expect_tx(&xfull[s], 16384);
+          tma_load_2d(sX + s * 16384, &tmX, &xfull[s], kb * 64, r0);          // box {64 k, 128 rows}
+        }
+        for (int c = 0; c < NC; ++c) {
+          {
+            const int s = slot_of(gi, S::kGS);
+            mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+            mbar_expect_tx(&gfull[s], 4096);
+            tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);          // box {64 f, 16 t, 1}
+            tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
+            ++gi;
+          }
+          for (int kb = 0; kb < DK; ++kb, ++wi) {
+            const int s = slot_of(wi, S::kWS);
+            mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
+            mbar_expect_tx(&wfull[s], 16384);
+            tma_load_3d(sW + s * 16384, &tmW1, &wfull[s], kb * 64, c * CH, e);  // box {64 k, 128 n, 1}
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ================= MMA issuer
+      constexpr uint32_t idS = umma_idesc_bf16(BM, CH, 0, 0);
+      constexpr uint32_t idP = umma_idesc_bf16(BM, 16, 0, 0);
+      int xi = 0, wi = 0, gi = 0, si = 0, hi = 0, it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int xbase = xi;
+        const int pb = it & 1;
+        const uint32_t tP = tmem_base + 256 + pb * 16;
+        // P-MMA of chunk cc (A = H smem, B = G slot), after the epilogue has written H
+        auto p_mma = [&](int cc) {
+          mbar_wait(hfull, (uint32_t)(hi & 1));
+          const int gs = slot_of(gi, S::kGS);
+          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
+          tc_fence_after();
+          if (cc == 0) { mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1)); tc_fence_after(); }
+          const uint32_t h_addr = smem_u32(sH), g_addr = smem_u32(sG + gs * 4096);
+#pragma unroll
+          for (int k = 0; k < CH / 16; ++k) {
+            const int atom = k >> 2, kk = k & 3;
+            tc_mma_f16(tP, umma_desc_sw128(h_addr + atom * 16384 + kk * 32, 16, 1024),
+                       umma_desc_sw128(g_addr + atom * 2048 + kk * 32, 16, 1024), idP, (cc | k) != 0);
+          }
+          tc_commit(hempty);
+          tc_commit(&gempty[gs]);
+          ++gi; ++hi;
+        };
+        for (int c = 0; c < NC; ++c, ++si) {
+          const int sb = si & 1;
+          mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t tS = tmem_base + sb * CH;
+          for (int kb = 0; kb < DK; ++kb, ++wi) {
+            const int xs = slot_of(xbase + kb, S::kXS);
+            if (c == 0) mbar_wait(&xfull[xs], par_of(xbase + kb, S::kXS));
+            const int ws = slot_of(wi, S::kWS);
+            mbar_wait(&wfull[ws], par_of(wi, S::kWS));
+            tc_fence_after();
+            const uint32_t x_addr = smem_u32(sX + xs * 16384), w_addr = smem_u32(sW + ws * 16384);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(tS, umma_desc_sw128(x_addr + k * 32, 16, 1024), umma_desc_sw128(w_addr + k * 32, 16, 1024),
+                         idS, (kb | k) != 0);
+            tc_commit(&wempty[ws]);
+            if (c == NC - 1) tc_commit(&xempty[xs]);     // X k-block no longer needed by this tile
+          }
+          tc_commit(&sfull[sb]);
+          if (c > 0) p_mma(c - 1);
+        }
+        p_mma(NC - 1);
+        tc_commit(&pfull[pb]);
+        xi = xbase + DK;
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;          // 64-column half of the chunk
+    float* sbias = reinterpret_cast<float*>(smem + S::kOffBias) + (warp - 4) * 64;
+    int si = 0, hi = 0, it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int r0 = tile * BM;
+      const int e = find_group(seg_s, a.E, r0);
+      const int row = r0 + 32 * q + lane;
+      for (int c = 0; c < NC; ++c, ++si) {
+        const int n0 = c * CH + par * 64;
+        const float bv0 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + lane);
+        const float bv1 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + 32 + lane);
+        const int sb = si & 1;
+        mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        tc_fence_after();
+        float f[64];
+        {
+          uint32_t t0[32], t1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + sb * CH + par * 64;
+          tmem_ld32(ta, t0);
+          tmem_ld32(ta + 32, t1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = __uint_as_float(t1[j]); }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sb]);       // accumulator drained into registers
+        sbias[lane] = bv0;
+        sbias[32 + lane] = bv1;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 64; j += 4) {
+          const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
+          f[j] = fmaxf(f[j] + bb.x, 0.f);
+          f[j + 1] = fmaxf(f[j + 1] + bb.y, 0.f);
+          f[j + 2] = fmaxf(f[j + 2] + bb.z, 0.f);
+          f[j + 3] = fmaxf(f[j + 3] + bb.w, 0.f);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
+          a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
+        }
+        // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
+        mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
+                                      pack_bf16(f[8 * cc + 4], f[8 * cc + 5]), pack_bf16(f[8 * cc + 6], f[8 * cc + 7]));
+          *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.store_h) {
+            tma_store_2d(&tmH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
+            bulk_commit();
+          }
+          mbar_arrive(hfull);
+        }
+        ++hi;
+      }
+      // head projections of this tile: P[row, t] = acc + c[e, t]
+      const int pb = it & 1;
+      mbar_wait(&pfull[pb], (uint32_t)((it >> 1) & 1));
+      tc_fence_after();
+      if (par == 0) {
+        uint32_t t0[16];
+        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + 256 + pb * 16, t0);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[pb]);
+        float* prow = a.P + (size_t)row * a.ldp;
+        const float* ce = a.c + (size_t)e * a.ldg;
+#pragma unroll
+        for (int t = 0; t < 16; t += 4) {
+          if (t < a.ldp) {
+            float4 v;
+            v.x = __uint_as_float(t0[t + 0]) + ce[t + 0];
+            v.y = __uint_as_float(t0[t + 1]) + ce[t + 1];
+            v.z = __uint_as_float(t0[t + 2]) + ce[t + 2];
+            v.w = __uint_as_float(t0[t + 3]) + ce[t + 3];
+            *reinterpret_cast<float4*>(prow + t) = v;
+          }
+        }
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+// ============================================================================ dgrad
+template <int DK>     // d / 64 (the output width of dX)
+struct DgSmem {
+  static constexpr int kCS = 2;                         // C tile ring (16 KB: {64 t, 128 rows}, K = 16 used)
+  static constexpr int kGS = 2;                         // G ring (chunk: 2 x {64 f, 16 t} = 4 KB, MN-major B)
+  static constexpr int kWS = DK <= 4 ? 3 : 2;           // W1 k-block ring: 64 f x d (DK x 8 KB boxes {64 j, 64 f})
+  static constexpr int kWB = DK * 8192;
+  static constexpr int kOffC = 0;
+  static constexpr int kOffG = kOffC + kCS * 16384;
+  static constexpr int kOffW = kOffG + kGS * 4096;
+  static constexpr int kOffH = kOffW + kWS * kWB;        // dH chunk: 2 x 16 KB atoms
+  static constexpr int kOffStg = kOffH + 32768;          // dX store staging: 8 warps x 4 KB
+  static constexpr int kOffBar = kOffStg + kEpiWarps * 4096;
+  static constexpr int kOffSeg = kOffBar + 512;
+  static constexpr int kBytes = kOffSeg + 257 * 4 + 1024;
+  static_assert(kBytes <= 232448, "mlp_dgrad smem");
+};
+
+template <int DK>
+__global__ void __launch_bounds__(kThreads, 1)
+    mlp_dgrad_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmG,
+                     const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmDX,
+                     const __grid_constant__ CUtensorMap tmDH, const DgradArgs a) {
+  using S = DgSmem<DK>;
+  constexpr int D = DK * 64;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sC = smem + S::kOffC;
+  uint8_t* sG = smem + S::kOffG;
+  uint8_t* sW = smem + S::kOffW;
+  uint8_t* sH = smem + S::kOffH;
+  uint8_t* sStg = smem + S::kOffStg;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* cfull = bar;                   // [kCS]
+  uint64_t* cempty = cfull + S::kCS;
+  uint64_t* gfull = cempty + S::kCS;       // [kGS]
+  uint64_t* gempty = gfull + S::kGS;
+  uint64_t* wfull = gempty + S::kGS;       // [kWS]
+  uint64_t* wempty = wfull + S::kWS;
+  uint64_t* sfull = wempty + S::kWS;       // [2]
+  uint64_t* sempty = sfull + 2;
+  uint64_t* hfull = sempty + 2;            // [1]
+  uint64_t* hempty = hfull + 1;
+  uint64_t* dfull = hempty + 1;            // [1] dX accumulator
+  uint64_t* dempty = dfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NC = a.d_ff / CH;
+  for (int i = threadIdx.x; i <= a.E; i += blockDim.x) seg_s[i] = a.seg[i];
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmC); tma_prefetch(&tmG); tma_prefetch(&tmW1); tma_prefetch(&tmDX); tma_prefetch(&tmDH);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S::kCS; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 1); }
+    for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps); }
+    mbar_init(hfull, kEpiWarps);
+    mbar_init(hempty, 1);
+    mbar_init(dfull, 1);
+    mbar_init(dempty, kEpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_tiles = seg_s[a.E] / BM;
+  // TMEM: S double buffer at [0, 256), dX accumulator at [256, 256 + D)
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int ci = 0, gi = 0, wi = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ci) {
+        const int r0 = tile * BM;
+        const int e = find_group(seg_s, a.E, r0);
+        {
+          const int s = slot_of(ci, S::kCS);
+          mbar_wait(&cempty[s], par_of(ci, S::kCS) ^ 1);
+          mbar_expect_tx(&cfull[s], 16384);
+          tma_load_2d(sC + s * 16384, &tmC, &cfull[s], 0, r0);                   // box {64 t, 128 rows}
+        }
+        for (int c = 0; c < NC; ++c) {
+          {
+            const int s = slot_of(gi, S::kGS);
+            mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+            mbar_expect_tx(&gfull[s], 4096);
+            tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);            // box {64 f, 16 t, 1}
+            tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
+            ++gi;
+          }
+          for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
+            const int s = slot_of(wi, S::kWS);
+            mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
+            mbar_expect_tx(&wfull[s], S::kWB);
+#pragma unroll
+            for (int j = 0; j < DK; ++j)                                          // box {64 j, 64 f, 1}
+              tma_load_3d(sW + s * S::kWB + j * 8192, &tmW1, &wfull[s], 64 * j, c * CH + kb * 64, e);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(BM, CH, 0, 1);     // A = C (K-major), B = G (MN-major)
+      constexpr uint32_t idD = umma_idesc_bf16(BM, D, 0, 1);      // A = dH (K-major), B = W1 (MN-major)
+      int ci = 0, gi = 0, wi = 0, si = 0, hi = 0, it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ci, ++it) {
+        const int cs = slot_of(ci, S::kCS);
+        mbar_wait(&cfull[cs], par_of(ci, S::kCS));
+        const uint32_t c_addr = smem_u32(sC + cs * 16384);
+        auto s_mma = [&](int c) {
+          const int sb = si & 1;
+          mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
+          const int gs = slot_of(gi, S::kGS);
+          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
+          tc_fence_after();
+          const uint32_t g_addr = smem_u32(sG + gs * 4096);
+          // K = 16 (tasks), one MMA; B MN-major: two 64-wide f atoms 2 KB apart
+          tc_mma_f16(tmem_base + sb * CH, umma_desc_sw128(c_addr, 16, 1024), umma_desc_sw128(g_addr, 2048, 1024),
+                     idS, 0u);
+          tc_commit(&sfull[sb]);
+          tc_commit(&gempty[gs]);
+          ++gi; ++si;
+        };
+        s_mma(0);
+        for (int c = 0; c < NC; ++c) {
+          if (c + 1 < NC) s_mma(c + 1);
+          if (c == NC - 1) tc_commit(&cempty[cs]);
+          mbar_wait(hfull, (uint32_t)(hi & 1));
+          // the dX accumulator must be drained by the previous tile's epilogue
+          if (c == 0) mbar_wait(dempty, (uint32_t)((it & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t h_addr = smem_u32(sH);
+          for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
+            const int ws = slot_of(wi, S::kWS);
+            mbar_wait(&wfull[ws], par_of(wi, S::kWS));
+            tc_fence_after();
+            const uint32_t w_addr = smem_u32(sW + ws * S::kWB);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(tmem_base + 256, umma_desc_sw128(h_addr + kb * 16384 + k * 32, 16, 1024),
+                         umma_desc_sw128(w_addr + k * 2048, 8192, 1024), idD, (c | kb | k) != 0);
+            tc_commit(&wempty[ws]);
+          }
+          tc_commit(hempty);
+          ++hi;
+        }
+        tc_commit(dfull);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;
+    uint8_t* stg = sStg + (warp - 4) * 4096;
+    int si = 0, hi = 0, it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int r0 = tile * BM;
+      const int row = r0 + 32 * q + lane;
+      for (int c = 0; c < NC; ++c, ++si) {
+        const int n0 = c * CH + par * 64;
+        const uint32_t m0 = __ldg(&a.bits[(size_t)(n0 >> 5) * a.bits_ld + row]);
+        const uint32_t m1 = __ldg(&a.bits[(size_t)((n0 >> 5) + 1) * a.bits_ld + row]);
+        const int sb = si & 1;
+        mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        tc_fence_after();
+        float f[64];
+        {
+          uint32_t t0[32], t1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + sb * CH + par * 64;
+          tmem_ld32(ta, t0);
+          tmem_ld32(ta + 32, t1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            f[j] = ((m0 >> j) & 1u) ? __uint_as_float(t0[j]) : 0.f;
+            f[32 + j] = ((m1 >> j) & 1u) ? __uint_as_float(t1[j]) : 0.f;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sempty[sb]);
+        mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
+        if (a.store_dh && lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
+                                      pack_bf16(f[8 * cc + 4], f[8 * cc + 5]), pack_bf16(f[8 * cc + 6], f[8 * cc + 7]));
+          *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.store_dh) {
+            tma_store_2d(&tmDH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
+            bulk_commit();
+          }
+          mbar_arrive(hfull);
+        }
+        ++hi;
+      }
+      // dX tile: TMEM [256, 256 + D) -> bf16 -> TMA store, 64-column chunks split by parity
+      mbar_wait(dfull, (uint32_t)(it & 1));
+      tc_fence_after();
+      for (int cc = par; cc < DK; cc += 2) {
+        uint32_t t0[32], t1[32];
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;
+        tmem_ld32(ta, t0);
+        tmem_ld32(ta + 32, t1);
+        tmem_ld_wait();
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t* src = k < 4 ? t0 : t1;
+          const int o = (k & 3) * 8;
+          rowp[k ^ (lane & 7)] = make_uint4(
+              pack_bf16(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
+              pack_bf16(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
+              pack_bf16(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
+              pack_bf16(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmDX, stg, cc * 64, r0 + 32 * q);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty);
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+}  // namespace mlp
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn2)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn2 encode_fn() {
+  static EncodeTiledFn2 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn2>(p);
+  }
+  return fn;
+}
+
+// bf16 tensor map, SW128; dims innermost first
+static int bf16_map(CUtensorMap* m, int rank, const void* ptr, const uint64_t* dims, const uint64_t* strides_bytes,
+                    const uint32_t* box) {
+  EncodeTiledFn2 enc = encode_fn();
+  if (!enc) return set_error(SMES_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (no CUDA driver?)");
+  cuuint64_t d[3], s[2];
+  cuuint32_t b[3], e[3] = {1, 1, 1};
+  for (int i = 0; i < rank; ++i) { d[i] = dims[i]; b[i] = box[i]; }
+  for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), d, s, b, e,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(SMES_ERR_CUDA, "cuTensorMapEncodeTiled failed (code %d)", (int)r);
+  return SMES_OK;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace smes
+
+using namespace smes;
+
+extern "C" {
+
+int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
+                 const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* bits, long bits_ld,
+                 void* H, long ldh, float* P, long ldp, void* stream) {
+  if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_fwd: expert count %d outside [1, 256]", E);
+  if (d % 64 || d < 64 || d > 512) return set_error(SMES_ERR_SHAPE, "mlp_fwd: d=%d must be a multiple of 64 in [64, 512]", d);
+  if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_fwd: d_ff=%d must be a multiple of 128", d_ff);
+  if (ldg < 1 || ldg > 16 || ldp > 16 || ldp % 4 || ldp > ldg)
+    return set_error(SMES_ERR_SHAPE, "mlp_fwd: ldg=%d ldp=%ld (need ldp <= ldg <= 16, ldp %% 4 == 0)", ldg, ldp);
+  if ((ldx * 2) % 16 || (ldh * 2) % 16) return set_error(SMES_ERR_SHAPE, "mlp_fwd: row strides must be 16-byte aligned");
+  CUtensorMap tx, tw, tg, th;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldx * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = bf16_map(&tx, 2, X, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d, (uint64_t)d_ff, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d * 2, (uint64_t)d_ff * d * 2};
+    uint32_t box[3] = {64, 128, 1};
+    if ((rc = bf16_map(&tw, 3, W1, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d_ff, (uint64_t)ldg, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d_ff * 2, (uint64_t)ldg * d_ff * 2};
+    uint32_t box[3] = {64, 16, 1};
+    if ((rc = bf16_map(&tg, 3, G, dims, str, box))) return rc;
+  }
+  {
+    const void* hp = H != nullptr ? H : X;     // map unused when H is not stored
+    uint64_t dims[2] = {(uint64_t)d_ff, (uint64_t)rows_cap}, str[1] = {(uint64_t)(H != nullptr ? ldh : ldx) * 2};
+    uint32_t box[2] = {64, 32};
+    if (H == nullptr) dims[0] = (uint64_t)d;
+    if ((rc = bf16_map(&th, 2, hp, dims, str, box))) return rc;
+  }
+  mlp::FwdArgs args{seg, E, d, d_ff, (int)ldp, b1, c, ldg, bits, (int)bits_ld, P, H != nullptr ? 1 : 0};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+#define SMES_FWD_CASE(DK)                                                                              \
+  case DK: {                                                                                           \
+    auto k = mlp::mlp_fwd_kernel<DK>;                                                                  \
+    const int sm = mlp::FwdSmem<DK>::kBytes;                                                           \
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd smem attribute: %s", cudaGetErrorString(e)); \
+    k<<<sm_count(), mlp::kThreads, sm, st>>>(tx, tw, tg, th, args);                                    \
+    break;                                                                                             \
+  }
+  switch (d / 64) {
+    SMES_FWD_CASE(1)
+    SMES_FWD_CASE(2)
+    SMES_FWD_CASE(4)
+    SMES_FWD_CASE(8)
+    default:
+      return set_error(SMES_ERR_SHAPE, "mlp_fwd: d=%d not instantiated (64, 128, 256, 512)", d);
+  }
+#undef SMES_FWD_CASE
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
+                   int d_ff, const int* seg, const uint32_t* bits, long bits_ld, void* dX, long lddx, void* dH,
+                   long lddh, void* stream) {
+  if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_dgrad: expert count %d outside [1, 256]", E);
+  if (d % 64 || d < 64 || d > 256) return set_error(SMES_ERR_SHAPE, "mlp_dgrad: d=%d must be a multiple of 64 in [64, 256]", d);
+  if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_dgrad: d_ff=%d must be a multiple of 128", d_ff);
+  if (ldg < 1 || ldg > 16 || ldc < ldg || (ldc * 2) % 16 || (lddx * 2) % 16)
+    return set_error(SMES_ERR_SHAPE, "mlp_dgrad: ldg=%d ldc=%ld lddx=%ld", ldg, ldc, lddx);
+  CUtensorMap tc, tg, tw, td, th;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)ldg, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldc * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = bf16_map(&tc, 2, C, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d_ff, (uint64_t)ldg, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d_ff * 2, (uint64_t)ldg * d_ff * 2};
+    uint32_t box[3] = {64, 16, 1};
+    if ((rc = bf16_map(&tg, 3, G, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d, (uint64_t)d_ff, (uint64_t)E};    // W1 (E, d_ff, d): element (j, f)
+    uint64_t str[2] = {(uint64_t)d * 2, (uint64_t)d_ff * d * 2};
+    uint32_t box[3] = {64, 64, 1};
+    if ((rc = bf16_map(&tw, 3, W1, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)rows_cap}, str[1] = {(uint64_t)lddx * 2};
+    uint32_t box[2] = {64, 32};
+    if ((rc = bf16_map(&td, 2, dX, dims, str, box))) return rc;
+  }
+  {
+    if (dH != nullptr && (lddh * 2) % 16) return set_error(SMES_ERR_SHAPE, "mlp_dgrad: dH stride must be 16-byte aligned");
+    uint64_t dims[2] = {(uint64_t)(dH ? d_ff : d), (uint64_t)rows_cap}, str[1] = {(uint64_t)(dH ? lddh : lddx) * 2};
+    uint32_t box[2] = {64, 32};
+    if ((rc = bf16_map(&th, 2, dH ? dH : dX, dims, str, box))) return rc;
+  }
+  mlp::DgradArgs args{seg, E, d, d_ff, bits, (int)bits_ld, dH != nullptr ? 1 : 0};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+#define SMES_DG_CASE(DK)                                                                               \
+  case DK: {                                                                                           \
+    auto k = mlp::mlp_dgrad_kernel<DK>;                                                                \
+    const int sm = mlp::DgSmem<DK>::kBytes;                                                            \
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad smem attribute: %s", cudaGetErrorString(e)); \
+    k<<<sm_count(), mlp::kThreads, sm, st>>>(tc, tg, tw, td, th, args);                                   \
+    break;                                                                                             \
+  }
+  switch (d / 64) {
+    SMES_DG_CASE(1)
+    SMES_DG_CASE(2)
+    SMES_DG_CASE(4)
+    default:
+      return set_error(SMES_ERR_SHAPE, "mlp_dgrad: d=%d not instantiated (64, 128, 256)", d);
+  }
+#undef SMES_DG_CASE
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+}  // extern "C"

@@ -97,7 +97,8 @@ class SMESEngine:
 
     def __init__(self, params: SMESParams, batch_size: int, k_shared: int, k_adaptive: int,
                  dense_probs_in_stats: bool = False, keep_reps: bool = True,
-                 device: torch.device | str | None = None, csum_from_gemm: bool = False):
+                 device: torch.device | str | None = None, csum_from_gemm: bool = False,
+                 fuse_mlp: bool = True):
         _require_cuda()
         self.dev = torch.device(device or "cuda")
         p = params
@@ -139,6 +140,10 @@ class SMESEngine:
         # sparse LB reading (the fused training combine produces the row coefficients C)
         self.can_fold = p.layers[-1].act == "identity" and not self.dense and T <= 32
         self._folded = False
+        # fused expert MLP (csrc/mlp.cu) for folded training steps: relu fc1 + identity fc2
+        lay = p.layers
+        self.fuse_mlp = bool(fuse_mlp and self.can_fold and len(lay) == 2 and lay[0].act == "relu"
+                             and d % 64 == 0 and d <= 256 and lay[0].d_out % 128 == 0 and T <= 16)
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
         self._alloc()
@@ -354,7 +359,8 @@ class SMESEngine:
         R = self.rows_cap
         inp = self.X
         L = len(self.p.layers)
-        for i, l in enumerate(self.p.layers[:L - 1] if fold else self.p.layers):
+        pre = [] if (fold and self.fuse_mlp) else (self.p.layers[:L - 1] if fold else self.p.layers)
+        for i, l in enumerate(pre):
             _tagged(f"fc{i + 1}_fwd", "smes_gemm_ragged_m", ptr(inp), self.ld_in[i], R, ptr(self.w_bf[i]), self.E,
                     self.dims[i + 1], self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act],
                     ptr(self.bits[i]), None, R, ptr(self.outs[i]), self.ld_out[i], 0, R, s)
@@ -365,6 +371,13 @@ class SMESEngine:
             di = self.dims[L - 1]
             _tagged("fold_heads", "smes_fold_heads", self.E, self.T, self.ldg, self.d_out, di, ptr(self.head_w),
                     ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold), ptr(self.fold_work), s)
+            if self.fuse_mlp:
+                # fc1 (+ relu mask, H kept for the weight gradients) and P in one chained kernel
+                _tagged("mlp_fwd", "smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]),
+                        ptr(self.b32[0]), ptr(self.G_fold), ptr(self.c_fold), self.ldg, self.E, self.d, di,
+                        ptr(self.seg_pad), ptr(self.bits[0]), R, ptr(self.outs[0]), self.ld_out[0], ptr(self.P),
+                        self.ldp, s)
+                return
             _tagged(f"fc{L}_fwd_folded", "smes_gemm_ragged_m", ptr(inp), self.ld_in[L - 1], R, ptr(self.G_fold),
                     self.E, self.ldg, di, 0, ptr(self.seg_pad), ptr(self.c_fold), 0, None, None, 0, ptr(self.P),
                     self.ldp, 1, R, s)
@@ -400,8 +413,14 @@ class SMESEngine:
             inp = self.X if L == 1 else self.outs[L - 2]
             dst = self.dX if L == 1 else self.d_outs[L - 2]
             mask = self.bits[L - 2] if L >= 2 else None
-            _tagged(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), E, di,
-                    self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
+            if self.fuse_mlp:
+                # dH = (C G_e) * mask and dX = dH W1 in one chained kernel (dH kept for the fc1 wgrad)
+                _tagged("mlp_dgrad", "smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), self.ldg,
+                        ptr(self.w_bf[0]), E, d, di, ptr(self.seg_pad), ptr(mask), R, ptr(self.dX), d,
+                        ptr(dst), di, s)
+            else:
+                _tagged(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G_fold),
+                        E, di, self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
             _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm), self.ldc,
                     R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qt), None, s)
             if self.fuse_b_last:
@@ -437,7 +456,7 @@ class SMESEngine:
             inp = self.X if i == 0 else self.outs[i - 1]
             gw, gb = self.g_layers[i]
             di, do = self.dims[i], self.dims[i + 1]
-            if i > 0:   # dgrad into the previous layer's output, masked by its relu
+            if i > 0 and not (folded and self.fuse_mlp):   # dgrad into the previous layer's output, masked by its relu
                 _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
             fused_last = i == n_layers - 1 and self.fuse_b_last and fused
@@ -453,7 +472,7 @@ class SMESEngine:
                 _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
                         di, ptr(self.seg_pad), ptr(gw), ptr(gb), s)
         # dX = d_out0 W_0
-        if not (folded and n_layers == 1):
+        if not (folded and (n_layers == 1 or self.fuse_mlp)):
             _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
                     ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
         # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)

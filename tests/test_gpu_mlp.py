@@ -1,0 +1,94 @@
+"""Fused expert-MLP kernels (csrc/mlp.cu) vs a plain PyTorch fp32 reference of the same ops,
+with skewed expert loads (empty experts, single-row experts, multi-tile experts)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_09386_b200._lib import call, ptr
+
+
+def _setup(E, d, d_ff, T, loads, seed):
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(seed)
+    seg = [0]
+    for n in loads:
+        seg.append(seg[-1] + (n + 127) // 128 * 128)
+    R = seg[-1] + 128
+    ldx = d + 64
+    X = torch.zeros(R, ldx, device=dev, dtype=torch.bfloat16)
+    for e, n in enumerate(loads):
+        X[seg[e]:seg[e] + n, :d] = torch.randn(n, d, generator=g, device=dev).to(torch.bfloat16)
+    W1 = (torch.randn(E, d_ff, d, generator=g, device=dev) / d ** 0.5).to(torch.bfloat16)
+    b1 = torch.randn(E, d_ff, generator=g, device=dev) * 0.1
+    ldg = (T + 7) // 8 * 8
+    G = torch.zeros(E, ldg, d_ff, device=dev, dtype=torch.bfloat16)
+    G[:, :T] = (torch.randn(E, T, d_ff, generator=g, device=dev) / d_ff ** 0.5).to(torch.bfloat16)
+    c = torch.zeros(E, ldg, device=dev)
+    c[:, :T] = torch.randn(E, T, generator=g, device=dev)
+    return dev, g, seg, R, ldx, X, W1, b1, ldg, G, c
+
+
+CASES = [(8, 256, 512, 8, [300, 0, 129, 1, 128, 517, 0, 1000]),
+         (4, 128, 256, 4, [700, 5, 0, 260]),
+         (3, 64, 384, 13, [129, 0, 250]),
+         (2, 512, 256, 8, [200, 300])]
+
+
+@pytest.mark.parametrize("E,d,d_ff,T,loads", CASES)
+def test_mlp_fwd(E, d, d_ff, T, loads):
+    dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, E + d + d_ff)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    ldh = d_ff + 64
+    H = torch.full((R, ldh), 3.0, device=dev).to(torch.bfloat16)
+    bits = torch.zeros(d_ff // 32, R, dtype=torch.int32, device=dev)
+    ldp = ldg
+    P = torch.full((R, ldp), float("nan"), device=dev)
+    call("smes_mlp_fwd", ptr(X), ldx, R, ptr(W1), ptr(b1), ptr(G), ptr(c), ldg, E, d, d_ff, ptr(seg_t), ptr(bits), R,
+         ptr(H), ldh, ptr(P), ldp, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.all(H[:, d_ff:] == 3.0)          # columns beyond d_ff untouched
+    for e, n in enumerate(loads):
+        if n == 0:
+            continue
+        lo = seg[e]
+        pre = X[lo:lo + n, :d].float() @ W1[e].float().T + b1[e]
+        h = pre.clamp_min(0)
+        got_h = H[lo:lo + n, :d_ff].float()
+        assert (got_h - h).abs().max().item() <= 1e-2 * h.abs().max().item()
+        word = bits[:, lo:lo + n].T.long()
+        m = torch.cat([((word[:, j:j + 1] >> torch.arange(32, device=dev)) & 1) for j in range(d_ff // 32)], 1).bool()
+        agree = (m == (h > 0)).float().mean().item()
+        assert agree > 0.999, agree                   # fp32 vs bf16-free accumulation order near 0
+        p_ref = got_h @ G[e, :T].float().T + c[e, :T]   # from the kernel's own bf16 H
+        got_p = P[lo:lo + n, :T]
+        assert (got_p - p_ref).abs().max().item() <= 2e-3 * p_ref.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("E,d,d_ff,T,loads", [c for c in CASES if c[1] <= 256])
+def test_mlp_dgrad(E, d, d_ff, T, loads):
+    dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, 3 * E + d + d_ff)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    ldc = 16
+    C = torch.zeros(R, ldc, device=dev, dtype=torch.bfloat16)
+    for e, n in enumerate(loads):
+        C[seg[e]:seg[e] + n, :T] = (torch.randn(n, T, generator=g, device=dev) * 1e-2).to(torch.bfloat16)
+    bits = torch.randint(-2 ** 31, 2 ** 31 - 1, (d_ff // 32, R), generator=g, device=dev,
+                         dtype=torch.int64).to(torch.int32)
+    dX = torch.full((R, d), float("nan"), device=dev).to(torch.bfloat16)
+    dH = torch.full((R, d_ff), float("nan"), device=dev).to(torch.bfloat16)
+    call("smes_mlp_dgrad", ptr(C), ldc, R, ptr(G), ldg, ptr(W1), E, d, d_ff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
+         ptr(dH), d_ff, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e, n in enumerate(loads):
+        lo, hi = seg[e], seg[e + 1]
+        if hi == lo:
+            continue
+        word = bits[:, lo:hi].T.long()
+        m = torch.cat([((word[:, j:j + 1] >> torch.arange(32, device=dev)) & 1) for j in range(d_ff // 32)], 1).bool()
+        dh = (C[lo:hi, :T].float() @ G[e, :T].float()) * m
+        assert (dH[lo:hi].float() - dh).abs().max().item() <= 1e-2 * dh.abs().max().item() + 1e-8
+        dx = dH[lo:hi].float() @ W1[e].float()        # from the kernel's own bf16 dH
+        assert (dX[lo:hi].float() - dx).abs().max().item() <= 1e-2 * dx.abs().max().item() + 1e-8
+        if n < hi - lo:
+            assert torch.all(dX[lo + n:hi] == 0)       # pad rows (C = 0)
