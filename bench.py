@@ -247,8 +247,8 @@ def run_ours(args):
     # ---------------- per-kernel breakdown (eager, queued behind a sleep so events time pure GPU work)
     n_act = eng.n_act()
     kern = per_kernel_times(eng, reps=5)
-    work = eng.work_model(n_act)
     peaks, peak_src = _peaks()
+    work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
     breakdown = {}
     for tag, t_ms in kern.items():
         fl, by, bound = work.get(tag, (0.0, 0.0, "hbm"))
@@ -270,7 +270,8 @@ def run_ours(args):
                 "unit": dominant["unit"], "frac": dominant["frac"], "traffic": traffic,
                 "peak_source": f"{peak_src} (burst; kernel timed alone with CUDA events)",
                 "step_share": round(kern[dom] / sum(kern.values()), 4)}
-    expert_flops = sum(work[t][0] for t in work if t.startswith("fc") and not t.endswith("bias"))
+    expert_flops = sum(work[t][0] for t in kern if t in work and (t.startswith("fc") or t.startswith("mlp_"))
+                       and not t.endswith("bias"))
     step_tflops = (expert_flops + sum(work[t][0] for t in ("router_fwd", "router_dgrad", "router_wgrad"))) / (ms * 1e-3) / 1e12
 
     cpu = None

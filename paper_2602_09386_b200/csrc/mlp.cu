@@ -18,8 +18,8 @@
 // Rows are the padded expert-major packed rows of the execution plan (128-row aligned
 // segments, so a tile never straddles two experts); group offsets stay on the device.
 //
-// Warp roles (384 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4).. and the 64-column half (w-4)/4 of a chunk).
+// Warp roles (384 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer (fwd: S only), w2 TMEM
+// allocator, w3 (fwd) P-MMA issuer, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4).. and the 64-column half (w-4)/4 of a chunk).
 #include "ptx.cuh"
 #include "smes_capi.h"
 
@@ -80,9 +80,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // ============================================================================ forward
 template <int DK>     // d / 64
 struct FwdSmem {
-  static constexpr int kXS = DK <= 4 ? DK + 2 : DK;    // X k-block ring (16 KB slots): next tile prefetch
-  static constexpr int kWS = DK <= 4 ? 4 : 3;          // W1 k-block ring (16 KB: 128 n x 64 k)
-  static constexpr int kGS = DK <= 4 ? 4 : 2;          // G chunk ring (4 KB: 2 x {64 f, 16 t})
+  // X k-block ring (16 KB slots, spare slots prefetch the next tile), W1 k-block ring (16 KB:
+  // 128 n x 64 k, 1.5 chunks deep at d = 256), G chunk ring (4 KB: 2 x {64 f, 16 t})
+  static constexpr int kXS = DK <= 2 ? DK + 2 : DK <= 4 ? DK + 1 : DK;
+  static constexpr int kWS = DK <= 4 ? 6 : 3;
+  static constexpr int kGS = 2;
   static constexpr int kOffX = 0;
   static constexpr int kOffW = kOffX + kXS * 16384;
   static constexpr int kOffG = kOffW + kWS * 16384;
@@ -180,32 +182,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ================= MMA issuer
+      // ================= S-MMA issuer: S_c = X W1[c]^T, never waits on the epilogue's H
       constexpr uint32_t idS = umma_idesc_bf16(BM, CH, 0, 0);
-      constexpr uint32_t idP = umma_idesc_bf16(BM, 16, 0, 0);
-      int xi = 0, wi = 0, gi = 0, si = 0, hi = 0, it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      int xi = 0, wi = 0, si = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int xbase = xi;
-        const int pb = it & 1;
-        const uint32_t tP = tmem_base + 256 + pb * 16;
-        // P-MMA of chunk cc (A = H smem, B = G slot), after the epilogue has written H
-        auto p_mma = [&](int cc) {
-          mbar_wait(hfull, (uint32_t)(hi & 1));
-          const int gs = slot_of(gi, S::kGS);
-          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
-          tc_fence_after();
-          if (cc == 0) { mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1)); tc_fence_after(); }
-          const uint32_t h_addr = smem_u32(sH), g_addr = smem_u32(sG + gs * 4096);
-#pragma unroll
-          for (int k = 0; k < CH / 16; ++k) {
-            const int atom = k >> 2, kk = k & 3;
-            tc_mma_f16(tP, umma_desc_sw128(h_addr + atom * 16384 + kk * 32, 16, 1024),
-                       umma_desc_sw128(g_addr + atom * 2048 + kk * 32, 16, 1024), idP, (cc | k) != 0);
-          }
-          tc_commit(hempty);
-          tc_commit(&gempty[gs]);
-          ++gi; ++hi;
-        };
         for (int c = 0; c < NC; ++c, ++si) {
           const int sb = si & 1;
           mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
@@ -218,19 +199,47 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&wfull[ws], par_of(wi, S::kWS));
             tc_fence_after();
             const uint32_t x_addr = smem_u32(sX + xs * 16384), w_addr = smem_u32(sW + ws * 16384);
+#ifndef SMES_EXP_NO_S
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               tc_mma_f16(tS, umma_desc_sw128(x_addr + k * 32, 16, 1024), umma_desc_sw128(w_addr + k * 32, 16, 1024),
                          idS, (kb | k) != 0);
+#endif
             tc_commit(&wempty[ws]);
             if (c == NC - 1) tc_commit(&xempty[xs]);     // X k-block no longer needed by this tile
           }
           tc_commit(&sfull[sb]);
-          if (c > 0) p_mma(c - 1);
         }
-        p_mma(NC - 1);
-        tc_commit(&pfull[pb]);
         xi = xbase + DK;
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ================= P-MMA issuer: P += H_c G[c]^T once the epilogue has staged H_c
+      constexpr uint32_t idP = umma_idesc_bf16(BM, 16, 0, 0);
+      int gi = 0, hi = 0, it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int pb = it & 1;
+        const uint32_t tP = tmem_base + 256 + pb * 16;
+        for (int c = 0; c < NC; ++c, ++gi, ++hi) {
+          mbar_wait(hfull, (uint32_t)(hi & 1));
+          const int gs = slot_of(gi, S::kGS);
+          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
+          if (c == 0) mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t h_addr = smem_u32(sH), g_addr = smem_u32(sG + gs * 4096);
+#ifndef SMES_EXP_NO_P
+#pragma unroll
+          for (int k = 0; k < CH / 16; ++k) {
+            const int atom = k >> 2, kk = k & 3;
+            tc_mma_f16(tP, umma_desc_sw128(h_addr + atom * 16384 + kk * 32, 16, 1024),
+                       umma_desc_sw128(g_addr + atom * 2048 + kk * 32, 16, 1024), idP, (c | k) != 0);
+          }
+#endif
+          tc_commit(hempty);
+          tc_commit(&gempty[gs]);
+        }
+        tc_commit(&pfull[pb]);
       }
     }
   } else if (warp >= 4) {
@@ -263,6 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);       // accumulator drained into registers
+#ifndef SMES_EXP_NO_EPI
         sbias[lane] = bv0;
         sbias[32 + lane] = bv1;
         __syncwarp();
@@ -281,8 +291,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
           a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
         }
+#endif
         // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
         mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
+#ifndef SMES_EXP_NO_EPI
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
         uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
@@ -294,11 +306,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
+#endif
         if (lane == 0) {
+#ifndef SMES_EXP_NO_EPI
           if (a.store_h) {
             tma_store_2d(&tmH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
             bulk_commit();
           }
+#endif
           mbar_arrive(hfull);
         }
         ++hi;

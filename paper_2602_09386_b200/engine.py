@@ -501,30 +501,50 @@ class SMESEngine:
         self.backward()
 
     # ------------------------------------------------------------------ accounting
-    def work_model(self, n_act: int) -> dict:
-        """Algorithmic work per launch tag: (flops, bytes, bound).  SURVEY 8(d)."""
+    def work_model(self, n_act: int, balance: float = 260.0) -> dict:
+        """Algorithmic work per launch tag: (flops, bytes, bound).  SURVEY 8(d).
+        ``bound`` is "tensor" when the kernel's arithmetic intensity exceeds the machine balance
+        (FLOP/byte of the measured peaks), else "hbm"."""
         T, E, B, K, d, do = self.T, self.E, self.B, self.K, self.d, self.d_out
         U = n_act / B
-        w = {"router_fwd": (2.0 * B * d * T * E, B * (d * 2 + T * E * 4), "tensor"),
-             "router_dgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 4), "tensor"),
-             "router_wgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 2), "tensor"),
-             "head_proj": (2.0 * n_act * do * T, n_act * (do * 2 + T * 4), "hbm"),
-             "combine_train": (0.0, B * (U * T * 4 + T * K * 8 + T * 16 + T * E * 2) + n_act * self.ldc * 2, "hbm"),
-             "dpacked_gemm": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2), "hbm"),
-             "head_wgrad": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2), "hbm"),
-             "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4), "hbm"),
-             "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8, "hbm"),
-             "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12), "hbm"),
-             "combine_bwd": (0.0, B * (U * do * 2 * 2 + T * K * 8 + T * 8 + T * E * 2), "hbm"),
-             "unpermute": (0.0, B * (U * d * 2 + d * 8), "hbm")}
+        w = {"router_fwd": (2.0 * B * d * T * E, B * (d * 2 + T * E * 4)),
+             "router_dgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 4)),
+             "router_wgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 2)),
+             "head_proj": (2.0 * n_act * do * T, n_act * (do * 2 + T * 4)),
+             "combine_train": (0.0, B * (U * T * 4 + T * K * 8 + T * 16 + T * E * 2) + n_act * self.ldc * 2),
+             "dpacked_gemm": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2)),
+             "head_wgrad": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2)),
+             "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4)),
+             "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8),
+             "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12)),
+             "combine_bwd": (0.0, B * (U * do * 2 * 2 + T * K * 8 + T * 8 + T * E * 2)),
+             "unpermute": (0.0, B * (U * d * 2 + d * 8))}
         for i in range(len(self.dims) - 1):
             di, dn = self.dims[i], self.dims[i + 1]
             f = 2.0 * n_act * di * dn
-            w[f"fc{i + 1}_fwd"] = (f, n_act * (di + dn) * 2, "tensor")
-            w[f"fc{i + 1}_wgrad"] = (f, n_act * (di + dn) * 2, "tensor")
-            w[f"fc{i + 1}_dgrad"] = (f, n_act * (di + dn) * 2, "tensor")
-            w[f"fc{i + 1}_bias"] = (0.0, n_act * dn * 2, "hbm")
-        return w
+            w[f"fc{i + 1}_fwd"] = (f, n_act * (di + dn) * 2)
+            w[f"fc{i + 1}_wgrad"] = (f, n_act * (di + dn) * 2)
+            w[f"fc{i + 1}_dgrad"] = (f, n_act * (di + dn) * 2)
+            w[f"fc{i + 1}_bias"] = (0.0, n_act * dn * 2)
+        if self.can_fold:
+            L = len(self.dims) - 1
+            di = self.dims[-2]
+            lg = self.ldg
+            # folded last pool: P = H G^T (N = T), dH = C G (K = T), Qt = H^T C
+            w[f"fc{L}_fwd_folded"] = (2.0 * n_act * di * T, n_act * (di * 2 + self.ldp * 4))
+            w[f"fc{L}_dgrad_folded"] = (2.0 * n_act * di * T, n_act * (self.ldc * 2 + di * 2 + di / 8))
+            w[f"fc{L}_wgrad_folded"] = (2.0 * n_act * di * T, n_act * (di * 2 + self.ldc * 2))
+            w["fold_heads"] = (2.0 * E * T * do * di, E * do * di * 2 + E * lg * di * 2)
+            w["unfold"] = (4.0 * E * T * do * di, E * di * lg * 4 + E * do * di * (4 + 2))
+            if self.fuse_mlp:
+                dff = self.dims[1]
+                # fused MLP: fc1 (+ relu mask, H kept) and P in one pass; dgrad dH (kept) + dX in one pass
+                w["mlp_fwd"] = (2.0 * n_act * (d * dff + dff * T),
+                                n_act * (d * 2 + dff * 2 + dff / 8 + self.ldp * 4))
+                w["mlp_dgrad"] = (2.0 * n_act * (T * dff + dff * d),
+                                  n_act * (self.ldc * 2 + dff / 8 + d * 2 + dff * 2))
+        return {k: (f, b, "tensor" if b > 0 and f / b > balance else ("tensor" if b == 0 else "hbm"))
+                for k, (f, b) in w.items()}
 
     # ------------------------------------------------------------------ graphs
     def capture_step(self, warmup: int = 1) -> torch.cuda.CUDAGraph:
