@@ -142,6 +142,34 @@ int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ld
                    int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, void* dX, long lddx,
                    void* dH, long lddh, void* stream);
 
+/* ---- expert parallelism (csrc/ep.cu; BASELINE config c5).  Rank r owns experts [r*El, (r+1)*El),
+ *      El % 32 == 0 (whole union-mask words).  Fixed-slot buffers: every count stays on the device.
+ *      smes_ep_pack:       per owner r, the instances whose union meets r's words (ascending b):
+ *                          idx (n, B), pos (n, B) (-1 if absent), cnt (n), mask words (n, B, wpr), h rows (n, B, d)
+ *      smes_ep_segments:   (packed row, slot row, rows) per (peer, local expert); mode 0 owner, 1 source
+ *      smes_ep_copy_rows:  dir 0 packed -> slots, dir 1 slots -> packed (16-byte rows)
+ *      smes_ep_combine_dh: d_hidden[b] = dh_router[b] + sum_r dh_recv[r][pos[r][b]] (fixed owner order)
+ *      smes_ep_capacity_guard: empty the owner plan and raise flag if its rows exceed the workspace
+ *      smes_ep_put_slots / smes_ep_signal_wait: peer-memory all-to-all (CUDA IPC pointers, flag epochs)
+ *      smes_ipc_handle / smes_ipc_open / smes_ipc_close: CUDA IPC plumbing (64-byte handles). */
+int smes_ep_pack(int B, int EW, const uint32_t* umask, int n, int wpr, const void* h_bf16, long ldh, int d,
+                 int32_t* idx, int32_t* pos, int32_t* cnt, uint32_t* mask_out, void* h_out_bf16, void* stream);
+int smes_ep_segments(int mode, int n, int El, const int32_t* cnt, const int32_t* seg_pad, long slot_rows,
+                     int32_t* tab, void* stream);
+int smes_ep_copy_rows(int nseg, const int32_t* tab, int dir, const void* src, long src_ld_bytes, void* dst,
+                      long dst_ld_bytes, int row_bytes, void* stream);
+int smes_ep_combine_dh(int B, int d, int n, long slot_rows, const int32_t* pos, const float* dh_recv,
+                       const float* dh_router, float* out, void* stream);
+int smes_ep_capacity_guard(int E, long cap, const int32_t* totals, int32_t* seg_pad, int32_t* loads,
+                           uint32_t* umask, long n_mask_words, int32_t* usize, long n_inst, int32_t* flag,
+                           void* stream);
+int smes_ep_put_slots(int n, int self, const void* send, long slot_bytes, long row_bytes, const int32_t* rows_used,
+                      void* const* peer_recv_dev, void* stream);
+int smes_ep_signal_wait(int n, int self, void* const* peer_flags_dev, int32_t* my_flags, int epoch, void* stream);
+int smes_ipc_handle(void* dev_ptr, void* handle_out);
+int smes_ipc_open(const void* handle, void** dev_ptr_out);
+int smes_ipc_close(void* dev_ptr);
+
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
                         float* freq_f32, void* stream);

@@ -38,6 +38,16 @@ SIGNATURES = {
     "smes_combine_train": [I, I, I, I, I, P, P, P, P, P, P, P, L, P, P, P, P, P, F, P, L, P, P, F, P, P, P, I, P],
     "smes_bias_from_csum": [I, I, I, P, P, P, P],
     "smes_fold_work_floats": [I, I, I, I],
+    "smes_ep_pack": [I, I, P, I, I, P, L, I, P, P, P, P, P, P],
+    "smes_ep_segments": [I, I, I, P, P, L, P, P],
+    "smes_ep_copy_rows": [I, P, I, P, L, P, L, I, P],
+    "smes_ep_combine_dh": [I, I, I, L, P, P, P, P, P],
+    "smes_ep_capacity_guard": [I, L, P, P, P, P, L, P, L, P, P],
+    "smes_ep_put_slots": [I, I, P, L, L, P, P, P],
+    "smes_ep_signal_wait": [I, I, P, P, I, P],
+    "smes_ipc_handle": [P, P],
+    "smes_ipc_open": [P, P],
+    "smes_ipc_close": [P],
     "smes_mlp_fwd": [P, L, L, P, P, P, P, I, I, I, I, P, P, L, P, L, P, L, P],
     "smes_mlp_dgrad": [P, L, L, P, I, P, I, I, I, P, P, L, P, L, P, L, P],
     "smes_fold_heads": [I, I, I, I, I, P, P, P, P, P, P, P],
@@ -61,7 +71,9 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_sca
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
                     "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,
                     "smes_fold_heads": 2, "smes_unfold_grads": 3,
-                    "smes_mlp_fwd": 1, "smes_mlp_dgrad": 1}
+                    "smes_mlp_fwd": 1, "smes_mlp_dgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
+                    "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
+                    "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 

@@ -1,0 +1,130 @@
+"""Expert shard: the expert stack of a training step over an externally built plan.
+
+Used by the expert-parallel step (:mod:`ep`): an owner rank runs its local experts
+(reference ``ExpertPool`` / ``grouped_gemm``, experts.py:17-73, execution.py:126-158, and the
+expert part of ``backward``, training.py:180-192) on the rows other ranks dispatched to it.
+The last (identity) pool is folded into the task heads (csrc/fold.cu), so the shard consumes
+the packed layer input X and produces the head projections P of every row; the backward
+consumes the row coefficients C (training.py:160-179 after folding) and produces the
+parameter gradients of the local experts, the local share of dW_head and the per-row dX.
+
+Buffers are sized by ``rows_cap`` (a multiple of 128); rows follow the plan's padded,
+expert-major layout (``seg_pad``), pad rows of X and C are zero.
+"""
+from __future__ import annotations
+
+import torch
+
+from ._lib import call, ptr
+from .errors import ConfigError, ShapeError
+
+
+def _round(x, m):
+    return (x + m - 1) // m * m
+
+
+class ExpertShard:
+    def __init__(self, layers, T: int, head_w: torch.Tensor, rows_cap: int, device, fuse_mlp: bool = True):
+        if layers[-1].act != "identity" or len(layers) not in (1, 2) or (len(layers) == 2 and layers[0].act != "relu"):
+            raise ConfigError("expert shard needs [relu ->] identity expert pools (the folded heads)")
+        self.dev = torch.device(device)
+        self.layers = layers
+        self.E = layers[0].weight.shape[0]
+        self.T = T
+        self.dims = [layers[0].d_in] + [l.d_out for l in layers]
+        if any(x % 32 for x in self.dims):
+            raise ShapeError(f"expert widths must be multiples of 32, got {self.dims}")
+        self.d, self.d_out = self.dims[0], self.dims[-1]
+        self.R = _round(rows_cap, 128)
+        self.ldg = _round(T, 8)
+        self.ldp = self.ldg
+        self.ldc = _round(T, 16)
+        d, R, E = self.d, self.R, self.E
+        L = len(layers)
+        self.fuse = bool(fuse_mlp and L == 2 and d % 64 == 0 and d <= 256 and self.dims[1] % 128 == 0
+                         and T <= 16)
+        dev, bf, f32 = self.dev, torch.bfloat16, torch.float32
+        z = lambda *s, dt=f32: torch.zeros(*s, dtype=dt, device=dev)
+        self.ld_in = [w + 64 for w in self.dims[:-1]]
+        self.X = z(R, self.ld_in[0], dt=bf)
+        self.X[:, d] = 1.0                                 # ones column: bias grads in the wgrad GEMM
+        self.H = None
+        if L == 2:
+            self.H = z(R, self.ld_in[1], dt=bf)
+            self.H[:, self.dims[1]] = 1.0
+            self.bits = z(self.dims[1] // 32, R, dt=torch.int32)
+            self.dH = z(R, self.dims[1], dt=bf)
+        self.P = z(R, self.ldp)
+        self.Cm = z(R, self.ldc, dt=bf)
+        self.dX = z(R, d, dt=bf)
+        di = self.dims[-2]
+        self.G = z(E, self.ldg, di, dt=bf)
+        self.c = z(E, self.ldg)
+        self.q_rows = di + 1                               # ones column -> per-expert sums of C
+        self.Qt = z(E, self.q_rows, self.ldg)
+        self.work = z(call("smes_fold_work_floats", E, T, self.d_out, di))
+        shapes = [(E, l.d_out, l.d_in) for l in layers] + [(E, l.d_out) for l in layers]
+        sizes = [int(torch.Size(s).numel()) for s in shapes]
+        self.grad_flat = z(sum(sizes))
+        views, off = [], 0
+        for s, n in zip(shapes, sizes):
+            views.append(self.grad_flat[off:off + n].view(s))
+            off += n
+        self.g_layers = [(views[i], views[L + i]) for i in range(L)]
+        self.g_head_w = z(T, self.d_out)                   # this shard's share of dW_head
+        self.head_w = head_w
+        self.refresh_weights()
+
+    def refresh_weights(self):
+        self.w_bf = [l.weight.detach().to(self.dev, torch.bfloat16).contiguous() for l in self.layers]
+        self.b32 = [l.bias.detach().to(self.dev, torch.float32).contiguous() for l in self.layers]
+
+    # ------------------------------------------------------------------ forward
+    def forward(self, s, seg_pad):
+        """P of every packed row (X already scattered; seg_pad = padded expert offsets)."""
+        E, R, T = self.E, self.R, self.T
+        di = self.dims[-2]
+        call("smes_fold_heads", E, T, self.ldg, self.d_out, di, ptr(self.head_w), ptr(self.w_bf[-1]),
+             ptr(self.b32[-1]), ptr(self.G), ptr(self.c), ptr(self.work), s)
+        if len(self.layers) == 1:
+            call("smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.G), E, self.ldg, di, 0, ptr(seg_pad),
+                 ptr(self.c), 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
+            return
+        if self.fuse:
+            call("smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), ptr(self.b32[0]), ptr(self.G),
+                 ptr(self.c), self.ldg, E, self.d, di, ptr(seg_pad), ptr(self.bits), R, ptr(self.H), self.ld_in[1],
+                 ptr(self.P), self.ldp, s)
+            return
+        call("smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), E, di, self.d, 0, ptr(seg_pad),
+             ptr(self.b32[0]), 1, ptr(self.bits), None, R, ptr(self.H), self.ld_in[1], 0, R, s)
+        call("smes_gemm_ragged_m", ptr(self.H), self.ld_in[1], R, ptr(self.G), E, self.ldg, di, 0, ptr(seg_pad),
+             ptr(self.c), 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
+
+    # ------------------------------------------------------------------ backward
+    def backward(self, s, seg_pad):
+        """From C (row coefficients, pad rows zero): expert grads, dW_head share, dX."""
+        E, R, T = self.E, self.R, self.T
+        L = len(self.layers)
+        di = self.dims[-2]
+        inp = self.X if L == 1 else self.H
+        if L == 2 and self.fuse:
+            call("smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G), self.ldg, ptr(self.w_bf[0]), E, self.d, di,
+                 ptr(seg_pad), ptr(self.bits), R, ptr(self.dX), self.d, ptr(self.dH), di, s)
+        else:
+            dst = self.dX if L == 1 else self.dH
+            call("smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G), E, di, self.ldg, 1, ptr(seg_pad), None,
+                 0, None, ptr(self.bits) if L == 2 else None, R, ptr(dst), di, 0, R, s)
+        call("smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm), self.ldc, R, E, self.q_rows, self.ldg,
+             ptr(seg_pad), ptr(self.Qt), None, s)
+        gw, gb = self.g_layers[L - 1]
+        csum = self.Qt[:, di, :]
+        call("smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qt), self.q_rows * self.ldg, ptr(csum),
+             self.q_rows * self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw), ptr(gb),
+             ptr(self.work), ptr(self.g_head_w), s)
+        if L == 2:
+            gw0, gb0 = self.g_layers[0]
+            call("smes_gemm_ragged_k", ptr(self.dH), di, ptr(self.X), self.ld_in[0], R, E, di, self.d, ptr(seg_pad),
+                 ptr(gw0), ptr(gb0), s)
+            if not self.fuse:
+                call("smes_gemm_ragged_m", ptr(self.dH), di, R, ptr(self.w_bf[0]), E, self.d, di, 1, ptr(seg_pad),
+                     None, 0, None, None, R, ptr(self.dX), self.d, 0, R, s)
