@@ -1,19 +1,23 @@
 #!/usr/bin/env python
-"""Benchmark: SMES fwd+bwd samples/s on B200 (BASELINE.json configs[1], c2).
+"""Benchmark: SMES fwd+bwd samples/s on B200 (BASELINE.json configs[1], c2, by default).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c3|c4|c5] [--transport nccl|peer]
 
 One step = one SMES-layer fwd+bwd over one batch of synthetic KuaiRand-shaped
 input: routers -> progressive routing -> dedup plan/permute -> expert MLP
-(256->512->256, grouped tcgen05 GEMMs) -> combine -> task heads -> BCE +
-beta*L_lb, and the full backward (all parameter grads + d_hidden).
-c2: T=8 tasks, E=32 experts, K_s=4 shared + K_a=2 private, d_model=256,
-batch 16384 per GPU, bf16 storage / fp32 accumulate (Stage-I routing fp64).
-Weights: reference init (model.py:117-156), seed 0.  Inputs: h ~ N(0,1).
+(grouped tcgen05 GEMMs; the identity fc2 folded into the task heads) -> combine ->
+task heads -> BCE + beta*L_lb, and the full backward (all parameter grads + d_hidden).
+c2 (default, the headline): T=8 tasks, E=32 experts, K_s=4 shared + K_a=2 private,
+d_model=256, expert MLP 256->512->256, batch 16384 per GPU, bf16 storage / fp32
+accumulate (Stage-I routing fp64).  Weights: reference init (model.py:117-156), seed 0.
+Inputs: h ~ N(0,1), Bernoulli labels at (0.3, 0.1, 0.05, 0.2) cycled.
 
-N>1 (torchrun, one rank per GPU): weak scaling, 16384 samples per rank,
-data-parallel with the LB-statistics all-reduce and the gradient all-reduce
-(NCCL).  Timing: CUDA events per step, L2 flushed between steps, max over ranks.
+N>1 (torchrun, one rank per GPU): c2 weak scaling (16384 per rank), c3 strong scaling
+(65536 global), both data-parallel with the LB-statistics all-reduce and the gradient
+all-reduce (NCCL); c5 expert-parallel (experts sharded E/N, dispatch / return all-to-all,
+NCCL or the peer-memory transport).  c4 is the single-GPU inference latency sweep.
+Timing: CUDA events per step, L2 flushed between steps, max over ranks.
 """
 from __future__ import annotations
 
@@ -30,9 +34,26 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = dict(T=8, E=32, ks=4, ka=2, d=256, d_ff=512, d_out=256, B=16384, beta=0.01)
-WORKLOAD = ("c2: SMES fwd+bwd, 8 tasks, 32 experts, shared top-4 + private top-2, d_model=256, "
-            "expert MLP 256->512->256, batch 16384 per GPU, bf16")
+CONFIGS = {
+    # BASELINE.json configs (Appendix A assumptions for the fields it leaves open)
+    "c2": dict(T=8, E=32, ks=4, ka=2, d=256, d_ff=512, d_out=256, B=16384, beta=0.01, mode="dp", scaling="weak",
+               workload="c2: SMES fwd+bwd, 8 tasks, 32 experts, shared top-4 + private top-2, d_model=256, "
+                        "expert MLP 256->512->256, batch 16384 per GPU, bf16"),
+    "c3": dict(T=16, E=64, ks=4, ka=2, d=512, d_ff=1024, d_out=512, B=65536, beta=0.01, mode="dp", scaling="strong",
+               workload="c3: SMES fwd+bwd with multi-gate LB regularizer, 16 tasks, 64 experts, shared top-4 + "
+                        "private top-2, d_model=512, expert MLP 512->1024->512, global batch 65536, data-parallel, bf16"),
+    "c4": dict(T=16, E=64, ks=4, ka=2, d=512, d_ff=1024, d_out=512, beta=0.0, mode="infer",
+               batches=[256, 512, 1024, 2048, 4096, 8192],
+               workload="c4: SMES inference scoring (fwd only, no regularizer), 16 tasks, 64 experts, d_model=512, "
+                        "expert MLP 512->1024->512, batch 256..8192 sweep, bf16"),
+    "c5": dict(T=32, E=256, ks=4, ka=2, d=1024, d_ff=2048, d_out=1024, B=32768, beta=0.01, mode="ep",
+               scaling="weak",
+               workload="c5: SMES expert-parallel fwd+bwd, 32 tasks, 256 experts, shared top-4 + private top-2, "
+                        "d_model=1024, expert MLP 1024->2048->1024, 32768 samples per GPU (the 8-GPU share of the "
+                        "256K global batch), experts sharded E/N, bf16"),
+}
+CFG = CONFIGS["c2"]
+WORKLOAD = CFG["workload"]
 METRIC = "SMES fwd+bwd samples/sec"
 UNIT = "samples/s"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -56,27 +77,34 @@ def _dist_env():
 
 # --------------------------------------------------------------------------- CPU legs
 
-def _cpu_sample(b_sample: int, steps: int, warm: int = 1):
-    """Time the oracle port (the reference's algorithm restated in NumPy f64) on a
-    bounded sub-batch of the c2 workload: forward_sparse + backward."""
+CPU_SAMPLE = {"c2": 2048, "c3": 512, "c4": 1024, "c5": 128}
+
+
+def _cpu_sample(cfg_name: str, steps: int, warm: int = 1):
+    """Time the oracle port (the reference's algorithm restated in NumPy f64) on a bounded
+    sub-batch of the configuration: forward_sparse + backward (forward only for c4)."""
     from oracle import smes_oracle as O
+    c = CONFIGS[cfg_name]
+    b_sample = CPU_SAMPLE[cfg_name]
     rng = np.random.default_rng(0)
-    c = CFG
     p = O.init_layer_params(rng, c["d"], c["d_out"], c["E"], c["T"], d_ff=c["d_ff"])
     h = rng.normal(size=(b_sample, c["d"]))
     y = (rng.uniform(size=(c["T"], b_sample)) < np.resize([0.3, 0.1, 0.05, 0.2], c["T"])[:, None]).astype(float)
+    fwd_only = c["mode"] == "infer"
     times = []
     for i in range(warm + steps):
         t0 = time.perf_counter()
         f = O.forward_sparse(h, p, c["ks"], c["ka"])
-        O.backward(f, p, y, None, c["beta"])
+        if not fwd_only:
+            O.backward(f, p, y, None, c["beta"])
         dt = time.perf_counter() - t0
         if i >= warm:
             times.append(dt)
     med = statistics.median(times)
     cores = len(os.sched_getaffinity(0))
+    what = "forward_sparse" if fwd_only else "forward_sparse+backward"
     return {"value": b_sample / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"c2 shape at B={b_sample} (sub-batch of 16384), oracle/smes_oracle.py forward_sparse+backward, "
+            "sample": f"{cfg_name} shape at B={b_sample} (sub-batch), oracle/smes_oracle.py {what}, "
                       f"median of {steps} steps after {warm} warm-up, numpy f64 with {cores} host threads"}
 
 
@@ -85,14 +113,18 @@ def run_reference(args):
     if rank != 0:
         return 0
     os.environ.setdefault("OPENBLAS_NUM_THREADS", str(len(os.sched_getaffinity(0))))
-    b_sample = 2048
+    c = CONFIGS[args.config]
     steps = max(1, min(args.steps, 5))
-    cb = _cpu_sample(b_sample, steps, warm=min(1, args.warmup))
-    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
+    cb = _cpu_sample(args.config, steps, warm=min(1, args.warmup))
+    b_sample = CPU_SAMPLE[args.config]
+    metric = METRIC if c["mode"] != "infer" else "SMES inference samples/sec"
+    line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": min(1, args.warmup), "ms_per_step": 1e3 * b_sample / cb["value"],
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": CFG["B"] * args.gpus,
-                       "parallelism": f"dp{args.gpus}", "reference_sample_batch": b_sample},
+            "higher_is_better": True, "scaling": c.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": c.get("B", b_sample) * (args.gpus if c.get(
+                "scaling") == "weak" else 1), "parallelism": f"{c['mode']}{args.gpus}",
+                       "reference_sample_batch": b_sample},
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -151,104 +183,37 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def run_ours(args):
+def _make_params(c, dev, expert_range=None):
+    """Reference init (model.py:117-156): experts/heads U(+-1/sqrt(fan_in)), routers
+    U(+-1e-3/sqrt(d)), biases 0; seed 0.  ``expert_range`` keeps only [lo, hi) of the experts
+    (expert parallelism); the full bank is drawn so every rank sees the same weights."""
     import torch
-    import torch.distributed as dist
-
-    from paper_2602_09386_b200 import ExpertLayer, SMESEngine, SMESParams, _lib
-    from paper_2602_09386_b200.dp import DataParallelStep
-
-    world, rank, local = _dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    c = CFG
-    # reference init (model.py:117-156): experts/heads U(+-1/sqrt(fan_in)), routers U(+-1e-3/sqrt(d)), bias 0
+    from paper_2602_09386_b200 import ExpertLayer, SMESParams
     g = torch.Generator(device="cpu").manual_seed(0)
-    u = lambda shape, s: ((torch.rand(*shape, generator=g, dtype=torch.float64) * 2 - 1) * s).float().to(dev)
+    u = lambda shape, s: ((torch.rand(*shape, generator=g, dtype=torch.float32) * 2 - 1) * s)
     T, E, d, dff, do = c["T"], c["E"], c["d"], c["d_ff"], c["d_out"]
-    params = SMESParams(
-        router_w=u((T, E, d), 1e-3 / d ** 0.5), router_b=torch.zeros(T, E, device=dev),
-        layers=[ExpertLayer(u((E, dff, d), d ** -0.5), torch.zeros(E, dff, device=dev), "relu"),
-                ExpertLayer(u((E, do, dff), dff ** -0.5), torch.zeros(E, do, device=dev), "identity")],
-        head_w=u((T, do), do ** -0.5), head_b=torch.zeros(T, device=dev), lb_strength=c["beta"])
-    B = c["B"]
-    eng = SMESEngine(params, B, c["ks"], c["ka"], device=dev)
+    rw = u((T, E, d), 1e-3 / d ** 0.5)
+    w1 = u((E, dff, d), d ** -0.5)
+    w2 = u((E, do, dff), dff ** -0.5)
+    hw = u((T, do), do ** -0.5)
+    lo, hi = expert_range or (0, E)
+    dv = lambda t: t.to(dev)
+    return SMESParams(router_w=dv(rw), router_b=torch.zeros(T, E, device=dev),
+                      layers=[ExpertLayer(dv(w1[lo:hi]), torch.zeros(hi - lo, dff, device=dev), "relu"),
+                              ExpertLayer(dv(w2[lo:hi]), torch.zeros(hi - lo, do, device=dev), "identity")],
+                      head_w=dv(hw), head_b=torch.zeros(T, device=dev), lb_strength=c["beta"])
+
+
+def _host_inputs(c, B, rank):
+    import torch
     gh = torch.Generator(device="cpu").manual_seed(1000 + rank)
-    h_host = torch.randn(B, d, generator=gh).to(torch.bfloat16).pin_memory()
-    rates = torch.tensor(np.resize([0.3, 0.1, 0.05, 0.2], T), dtype=torch.float32)[:, None]
-    y_host = (torch.rand(T, B, generator=gh) < rates).float().pin_memory()
-    loss_host = torch.zeros(3, dtype=torch.float64).pin_memory()
-    eng.set_inputs(h_host.to(dev), y_host.to(dev))
+    h_host = torch.randn(B, c["d"], generator=gh).to(torch.bfloat16).pin_memory()
+    rates = torch.tensor(np.resize([0.3, 0.1, 0.05, 0.2], c["T"]), dtype=torch.float32)[:, None]
+    y_host = (torch.rand(c["T"], B, generator=gh) < rates).float().pin_memory()
+    return h_host, y_host
 
-    dp = DataParallelStep(eng)
-    dp.capture(warmup=1)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        dp.step()
-    barrier()
-
-    # ---------------- device-resident timed region (value)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches0 = _lib.launch_count
-    per_step_launches = count_step_launches(eng)
-    with ClockSampler(local) as clk:
-        barrier()
-        for i in range(args.steps):
-            flush.zero_()
-            starts[i].record()
-            dp.step()
-            ends[i].record()
-        barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    ms = tot.item() / args.steps
-    value = world * B / (ms / 1e3)
-
-    # ---------------- end-to-end through the public API with host buffers (e2e): every step's
-    # inputs are copied H2D from pinned memory (double-buffered, step i+1's copy overlapping
-    # step i) and every step's loss is read back D2H.
-    from paper_2602_09386_b200.pipeline import HostStepPipeline
-    pipe = HostStepPipeline(eng, step_fn=dp.step)
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(2):                                   # warm the pipeline path
-        pipe.prefetch(h_host, y_host)
-        pipe.step()
-    barrier()
-    flush.zero_()
-    e_start.record()
-    pipe.prefetch(h_host, y_host)
-    for i in range(args.steps):
-        last = i == args.steps - 1
-        pipe.step(None if last else h_host, None if last else y_host)
-    e_end.record()
-    barrier()
-    e_tot = torch.tensor([e_start.elapsed_time(e_end)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
-    e_ms = e_tot.item() / args.steps
-    e2e = {"value": world * B / (e_ms / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": h_host.numel() * h_host.element_size() + y_host.numel() * y_host.element_size(),
-           "d2h_bytes_per_step": pipe.loss_host.numel() * pipe.loss_host.element_size(),
-           "ms_per_step": e_ms,
-           "api": "pipeline.HostStepPipeline.step (pinned H2D of each step's inputs, double-buffered on a copy "
-                  "stream and overlapped with the previous step; D2H of each step's loss)"}
-
-    # ---------------- per-kernel breakdown (eager, queued behind a sleep so events time pure GPU work)
-    n_act = eng.n_act()
-    kern = per_kernel_times(eng, reps=5)
-    peaks, peak_src = _peaks()
-    work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
+def _roofline(kern, work, peaks, peak_src):
     breakdown = {}
     for tag, t_ms in kern.items():
         fl, by, bound = work.get(tag, (0.0, 0.0, "hbm"))
@@ -270,24 +235,80 @@ def run_ours(args):
                 "unit": dominant["unit"], "frac": dominant["frac"], "traffic": traffic,
                 "peak_source": f"{peak_src} (burst; kernel timed alone with CUDA events)",
                 "step_share": round(kern[dom] / sum(kern.values()), 4)}
-    expert_flops = sum(work[t][0] for t in kern if t in work and (t.startswith("fc") or t.startswith("mlp_"))
-                       and not t.endswith("bias"))
-    step_tflops = (expert_flops + sum(work[t][0] for t in ("router_fwd", "router_dgrad", "router_wgrad"))) / (ms * 1e-3) / 1e12
+    return roofline, breakdown
 
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        cpu = _cpu_sample(2048, 2)
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "global_batch": world * B, "per_gpu_batch": B,
-                           "parallelism": f"dp{world}", "n_act_rows": n_act, "mean_union": n_act / B,
-                           "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)",
-                           "graph": "fwd+bwd captured as 2 CUDA graphs around the LB-stats all-reduce"},
-                "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
-                "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-                "step_tflops": round(step_tflops, 1), "kernels": breakdown}
+
+def _timed_steps(step_fn, steps, world, dev, flush, local):
+    import torch
+    import torch.distributed as dist
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(steps):
+            flush.zero_()
+            starts[i].record()
+            step_fn()
+            ends[i].record()
+        barrier()
+    step_ms = [s_.elapsed_time(e) for s_, e in zip(starts, ends)]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    return tot.item() / steps, clk.summary()
+
+
+def _timed_e2e(pipe, h_host, y_host, steps, world, dev, flush):
+    """End to end through the host-fed step API: each step's inputs copied H2D from pinned
+    memory (double-buffered, overlapped with the previous step) and its loss read back D2H."""
+    import torch
+    import torch.distributed as dist
+    for _ in range(2):
+        pipe.prefetch(h_host, y_host)
+        pipe.step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    flush.zero_()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    pipe.prefetch(h_host, y_host)
+    for i in range(steps):
+        last = i == steps - 1
+        pipe.step(None if last else h_host, None if last else y_host)
+    e_end.record()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e_tot = torch.tensor([e_start.elapsed_time(e_end)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_tot, op=dist.ReduceOp.MAX)
+    return e_tot.item() / steps
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS[args.config]
+    mode = c["mode"]
+    if mode == "dp":
+        line = run_dp(args, c, world, rank, local, dev)
+    elif mode == "ep":
+        line = run_ep(args, c, world, rank, local, dev)
+    else:
+        line = run_infer(args, c, world, rank, local, dev)
+    if rank == 0 and line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -295,16 +316,203 @@ def run_ours(args):
     return 0
 
 
-def count_step_launches(eng):
+def run_dp(args, c, world, rank, local, dev):
+    import torch
+    from paper_2602_09386_b200 import SMESEngine, _lib
+    from paper_2602_09386_b200.dp import DataParallelStep
+    from paper_2602_09386_b200.pipeline import HostStepPipeline
+
+    B = c["B"] if c["scaling"] == "weak" else c["B"] // world
+    eng = SMESEngine(_make_params(c, dev), B, c["ks"], c["ka"], device=dev)
+    h_host, y_host = _host_inputs(c, B, rank)
+    eng.set_inputs(h_host.to(dev), y_host.to(dev))
+    dp = DataParallelStep(eng)
+    dp.capture(warmup=1)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    for _ in range(args.warmup):
+        dp.step()
+    per_step_launches = count_step_launches(eng.step)
+    ms, clocks = _timed_steps(dp.step, args.steps, world, dev, flush, local)
+    value = world * B / (ms / 1e3)
+    pipe = HostStepPipeline(eng, step_fn=dp.step)
+    e_ms = _timed_e2e(pipe, h_host, y_host, args.steps, world, dev, flush)
+    e2e = {"value": world * B / (e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": h_host.numel() * h_host.element_size() + y_host.numel() * y_host.element_size(),
+           "d2h_bytes_per_step": pipe.loss_host.numel() * pipe.loss_host.element_size(), "ms_per_step": e_ms,
+           "api": "pipeline.HostStepPipeline.step (pinned H2D of each step's inputs, double-buffered on a copy "
+                  "stream and overlapped with the previous step; D2H of each step's loss)"}
+    n_act = eng.n_act()
+    kern = per_kernel_times(eng.step, reps=5)
+    peaks, peak_src = _peaks()
+    work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    expert_flops = sum(work[t][0] for t in kern if t in work and (t.startswith("fc") or t.startswith("mlp_"))
+                       and not t.endswith("bias"))
+    step_tflops = (expert_flops + sum(work[t][0] for t in ("router_fwd", "router_dgrad", "router_wgrad"))) / (
+        ms * 1e-3) / 1e12
+    cpu = _cpu_sample(args.config, 2) if (rank == 0 and not args.no_cpu) else None
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": c["scaling"],
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": world * B, "per_gpu_batch": B,
+                       "parallelism": f"dp{world}", "n_act_rows": n_act, "mean_union": n_act / B,
+                       "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)",
+                       "graph": "fwd+bwd captured as 2 CUDA graphs around the LB-stats all-reduce"},
+            "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "step_tflops": round(step_tflops, 1), "kernels": breakdown}
+
+
+def run_ep(args, c, world, rank, local, dev):
+    import torch
+    from paper_2602_09386_b200.ep import EPRank, ExpertParallelStep, LoopbackComm, NcclComm, PeerComm
+    from paper_2602_09386_b200.pipeline import HostStepPipeline
+
+    B = c["B"]
+    E = c["E"]
+    El = E // world
+    rk = EPRank(_make_params(c, dev, (rank * El, (rank + 1) * El)), E, rank, world, B, c["ks"], c["ka"],
+                device=dev, capacity_factor=1.25)
+    h_host, y_host = _host_inputs(c, B, rank)
+    rk.set_inputs(h_host.to(dev), y_host.to(dev))
+    if world == 1:
+        comm = LoopbackComm([rk])
+    elif args.transport == "peer":
+        comm = PeerComm(rk)
+    else:
+        comm = NcclComm(rk)
+    ep = ExpertParallelStep([rk], comm)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        ep.step()
+    torch.cuda.synchronize()
+    rk.check()
+    per_step_launches = count_step_launches(ep.step)
+    ms, clocks = _timed_steps(ep.step, args.steps, world, dev, flush, local)
+    value = world * B / (ms / 1e3)
+    pipe = HostStepPipeline(rk, step_fn=ep.step)
+    e_ms = _timed_e2e(pipe, h_host, y_host, args.steps, world, dev, flush)
+    e2e = {"value": world * B / (e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": h_host.numel() * h_host.element_size() + y_host.numel() * y_host.element_size(),
+           "d2h_bytes_per_step": pipe.loss_host.numel() * pipe.loss_host.element_size(), "ms_per_step": e_ms,
+           "api": "pipeline.HostStepPipeline.step over ep.ExpertParallelStep.step"}
+    rk.check()
+    n_own = int(rk.totals_o[2].item())
+    kern = per_kernel_times(ep.step, reps=2)
+    peaks, peak_src = _peaks()
+    sh = rk.shard
+    d, dff, T = c["d"], c["d_ff"], c["T"]
+    bal = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    fl = 2.0 * n_own * d * dff
+    work = {"fc1_fwd": (fl, n_own * (d + dff) * 2), "fc1_dgrad": (fl, n_own * (d + dff) * 2),
+            "fc1_wgrad": (fl, n_own * (d + dff) * 2),
+            "fc2_fwd_folded": (2.0 * n_own * dff * T, n_own * (dff * 2 + sh.ldp * 4)),
+            "fc2_dgrad_folded": (2.0 * n_own * dff * T, n_own * (sh.ldc * 2 + dff * 2 + dff / 8)),
+            "fc2_wgrad_folded": (2.0 * n_own * dff * T, n_own * (dff * 2 + sh.ldc * 2))}
+    work = {k: (f, b, "tensor" if f / b > bal else "hbm") for k, (f, b) in work.items()}
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    expert_flops = 3 * fl + 3 * 2.0 * n_own * dff * T
+    cpu = _cpu_sample(args.config, 1) if (rank == 0 and not args.no_cpu) else None
+    if rank != 0:
+        return None
+    return {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": c["scaling"],
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": world * B, "per_gpu_batch": B,
+                       "parallelism": f"ep{world}", "experts_per_gpu": El,
+                       "transport": "loopback (1 rank)" if world == 1 else args.transport,
+                       "expert_rows_on_rank0": n_own,
+                       "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)"},
+            "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "step_tflops": round(expert_flops / (ms * 1e-3) / 1e12, 1), "kernels": breakdown}
+
+
+def run_infer(args, c, world, rank, local, dev):
+    """c4: fwd-only scoring through the reference-shaped forward (routers, routing, plan, experts,
+    combine, heads; task reps materialised), one CUDA graph per batch size, p50/p99 over
+    >= 1000 replays each.  Ranks > 0 idle (single-GPU configuration)."""
+    import torch
+    from paper_2602_09386_b200 import SMESEngine, _lib
+    if rank != 0:
+        return None
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    c = dict(c, beta=0.0)
+    params = _make_params(c, dev)
+    sweep, launches = {}, 0
+    reps = max(1000, args.steps)
+    for Bb in c["batches"]:
+        eng = SMESEngine(params, Bb, c["ks"], c["ka"], device=dev)
+        h_host, y_host = _host_inputs(c, Bb, rank)
+        eng.set_inputs(h_host.to(dev), y_host.to(dev))
+        st = torch.cuda.Stream(dev)
+        st.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(st):
+            eng.forward(with_loss=False)
+        torch.cuda.current_stream(dev).wait_stream(st)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            eng.forward(with_loss=False)
+        for _ in range(max(3, args.warmup)):
+            g.replay()
+        torch.cuda.synchronize()
+        c0 = _lib.launch_count
+        eng.forward(with_loss=False)
+        per = _lib.launch_count - c0
+        ts = []
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a, b in ev:
+            flush.zero_()
+            a.record()
+            g.replay()
+            b.record()
+        torch.cuda.synchronize()
+        ts = sorted(a.elapsed_time(b) for a, b in ev)
+        launches += per * reps
+        # end to end: pinned H2D of h, graph, D2H of the predictions
+        preds_host = torch.empty(c["T"], Bb, dtype=torch.float32).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = 200
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(n_e2e):
+            eng.h.copy_(h_host, non_blocking=True)
+            g.replay()
+            preds_host.copy_(eng.preds, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        sweep[str(Bb)] = {"p50_ms": ts[len(ts) // 2], "p99_ms": ts[min(len(ts) - 1, int(0.99 * len(ts)))],
+                          "samples_per_s": Bb / (ts[len(ts) // 2] / 1e3),
+                          "e2e_ms": e0.elapsed_time(e1) / n_e2e, "launches_per_batch": per}
+        last = (Bb, eng, h_host, preds_host)
+        del g
+    Bb, eng, h_host, preds_host = last
+    top = sweep[str(Bb)]
+    cpu = _cpu_sample(args.config, 2) if not args.no_cpu else None
+    return {"metric": f"SMES inference p50 latency per batch (B={Bb})", "value": top["p50_ms"], "unit": "ms",
+            "n_gpus": 1, "steps": reps, "warmup": max(3, args.warmup), "ms_per_step": top["p50_ms"],
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": Bb, "parallelism": "single-GPU",
+                       "l2": "flushed before every timed replay (256 MiB memset outside the event brackets)",
+                       "graph": "one CUDA graph per batch size"},
+            "e2e": {"value": top["e2e_ms"], "unit": "ms", "h2d_bytes_per_step": h_host.numel() * 2,
+                    "d2h_bytes_per_step": preds_host.numel() * 4,
+                    "api": "pinned H2D of h, graph replay of SMESEngine.forward, D2H of predictions"},
+            "gpu_launches": launches, "sweep": sweep, "cpu_baseline": cpu}
+
+
+def count_step_launches(step_fn):
     from paper_2602_09386_b200 import _lib
     import torch
     c0 = _lib.launch_count
-    eng.step()
+    step_fn()
     torch.cuda.synchronize()
     return _lib.launch_count - c0
 
 
-def per_kernel_times(eng, reps=5):
+def per_kernel_times(step_fn, reps=5):
     import contextlib
     import torch
     from paper_2602_09386_b200 import _lib
@@ -326,7 +534,7 @@ def per_kernel_times(eng, reps=5):
         torch.cuda._sleep(20_000_000)   # keep the GPU busy while the launches queue up
         _lib._timer = timer
         try:
-            eng.step()
+            step_fn()
         finally:
             _lib._timer = None
         torch.cuda.synchronize()
@@ -342,6 +550,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="BASELINE.json configuration (default c2, the headline)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="c5 all-to-all: NCCL all_to_all_single or the CUDA-IPC peer-memory put")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -125,6 +125,16 @@ def call(name: str, *args):
     return rc
 
 
+def tcall(tag_: str, name: str, *args):
+    """``call`` with a launch-site label (per-kernel timing in the bench)."""
+    global tag
+    tag = tag_
+    try:
+        return call(name, *args)
+    finally:
+        tag = None
+
+
 def ptr(t) -> int | None:
     """Device pointer of a tensor (None -> NULL)."""
     return None if t is None else t.data_ptr()

@@ -30,7 +30,7 @@ from __future__ import annotations
 import torch
 
 from . import _lib
-from ._lib import call, ptr
+from ._lib import call, ptr, tcall
 from .errors import ConfigError, ShapeError, StateError
 from .experts import ExpertShard
 
@@ -211,20 +211,20 @@ class EPRank:
     def f1(self):
         """Route + source plan + LB statistics + dispatch pack."""
         s, T, E, B, d = self._s(), self.T, self.E, self.B, self.d
-        call("smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
+        tcall("router_fwd", "smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
              ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
-        call("smes_route_batch", ptr(self.z), E, T * E, None, ptr(self.tw), T, B, E, self.ks, self.ka, self.rpw,
+        tcall("route", "smes_route_batch", ptr(self.z), E, T * E, None, ptr(self.tw), T, B, E, self.ks, self.ka, self.rpw,
              ptr(self.shared), ptr(self.adaptive), ptr(self.active), ptr(self.wsel), ptr(self.umask), ptr(self.usize),
              ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass), ptr(self.chunk_dmass), None,
              ptr(self.flag), 0, s)
-        call("smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
+        tcall("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
              ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), ptr(self.seg_half), s)
         # the source plan only places rows (row_of, gather arrays) and zeroes C's pad rows; X is not built
-        call("smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
+        tcall("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
              ptr(self.loads), None, self.ldh, None, d, ptr(self.row_of), self.umax, ptr(self.gather_inst),
              ptr(self.gather_exp), ptr(self.C_src), self.ldc, self.ldc, s)
-        call("smes_ep_pack", B, self.EW, ptr(self.umask), self.n, self.wpr, ptr(self.h), self.ldh, d, ptr(self.idx),
+        tcall("ep_pack", "smes_ep_pack", B, self.EW, ptr(self.umask), self.n, self.wpr, ptr(self.h), self.ldh, d, ptr(self.idx),
              ptr(self.pos), ptr(self.cnt), ptr(self.mask_send), ptr(self.h_send), s)
 
     def f2(self):
@@ -232,61 +232,61 @@ class EPRank:
         s, El, d, Br = self._s(), self.El, self.d, self.Br
         sh = self.shard
         umask = self.umask_recv.view(Br, self.wpr)
-        call("smes_plan_counts", Br, El, self.rpw_o, ptr(umask), ptr(self.chunk_union_o), ptr(self.usize_o), s)
-        call("smes_plan_reduce", self.C_o, El, ptr(self.chunk_union_o), ptr(self.chunk_zero_i), ptr(self.chunk_zero_d),
+        tcall("owner_plan", "smes_plan_counts", Br, El, self.rpw_o, ptr(umask), ptr(self.chunk_union_o), ptr(self.usize_o), s)
+        tcall("owner_plan", "smes_plan_reduce", self.C_o, El, ptr(self.chunk_union_o), ptr(self.chunk_zero_i), ptr(self.chunk_zero_d),
              ptr(self.chunk_zero_d), ptr(self.chunk_base_o), ptr(self.loads_o), ptr(self.stats_o), ptr(self.seg_pad_o),
              ptr(self.seg_log_o), ptr(self.totals_o), ptr(self.ticket_o), ptr(self.seg_half_o), s)
-        call("smes_ep_capacity_guard", El, sh.R, ptr(self.totals_o), ptr(self.seg_pad_o), ptr(self.loads_o),
+        tcall("owner_plan", "smes_ep_capacity_guard", El, sh.R, ptr(self.totals_o), ptr(self.seg_pad_o), ptr(self.loads_o),
              ptr(umask), Br * self.wpr, ptr(self.usize_o), Br, ptr(self.cap_flag), s)
-        call("smes_plan_scatter", Br, El, d, self.rpw_o, ptr(umask), ptr(self.chunk_base_o), ptr(self.seg_pad_o),
+        tcall("owner_scatter", "smes_plan_scatter", Br, El, d, self.rpw_o, ptr(umask), ptr(self.chunk_base_o), ptr(self.seg_pad_o),
              ptr(self.loads_o), ptr(self.h_recv), d, ptr(sh.X), sh.ld_in[0], ptr(self.row_of_o), self.umax_l,
              ptr(self.gather_inst_o), ptr(self.gather_exp_o), ptr(sh.Cm), sh.ldc, sh.ldc, s)
         sh.forward(s, self.seg_pad_o)
-        call("smes_ep_segments", 0, self.n, El, ptr(self.cnt_recv), ptr(self.seg_pad_o), self.slot_rows,
+        tcall("ep_segments", "smes_ep_segments", 0, self.n, El, ptr(self.cnt_recv), ptr(self.seg_pad_o), self.slot_rows,
              ptr(self.tab_own), s)
-        call("smes_ep_copy_rows", self.n * El, ptr(self.tab_own), 0, ptr(sh.P), sh.ldp * 4, ptr(self.P_send),
+        tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * El, ptr(self.tab_own), 0, ptr(sh.P), sh.ldp * 4, ptr(self.P_send),
              self.ldp * 4, self.ldp * 4, s)
 
     def f3(self):
         """Source: P into plan order -> statistics -> training combine -> C per owner."""
         s, T, E, B, K = self._s(), self.T, self.E, self.B, self.K
         Bg = B * self.n
-        call("smes_ep_segments", 1, self.n, self.El, ptr(self.loads), ptr(self.seg_pad), self.slot_rows,
+        tcall("ep_segments", "smes_ep_segments", 1, self.n, self.El, ptr(self.loads), ptr(self.seg_pad), self.slot_rows,
              ptr(self.tab_src), s)
-        call("smes_ep_copy_rows", self.n * self.El, ptr(self.tab_src), 1, ptr(self.P_recv), self.ldp * 4,
+        tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * self.El, ptr(self.tab_src), 1, ptr(self.P_recv), self.ldp * 4,
              ptr(self.P_src), self.ldp * 4, self.ldp * 4, s)
         call("smes_stats_finalize", E, K, float(Bg * T), 0, ptr(self.stats_raw), ptr(self.stats_out), ptr(self.freq32), s)
         lb_coef = self.beta * E / (K * Bg * T)
-        call("smes_combine_train", T, B, E, K, self.umax, ptr(self.umask), ptr(self.usize), ptr(self.row_of),
+        tcall("combine_train", "smes_combine_train", T, B, E, K, self.umax, ptr(self.umask), ptr(self.usize), ptr(self.row_of),
              ptr(self.active), ptr(self.wsel), ptr(self.head_b), ptr(self.P_src), self.ldp, ptr(self.logits),
              ptr(self.preds), ptr(self.labels), ptr(self.lam), ptr(self.loss_part), 1.0 / Bg, ptr(self.C_src),
              self.ldc, ptr(self.dz), ptr(self.freq32), lb_coef, ptr(self.part_db), None, None, self.grid, s)
-        call("smes_ep_copy_rows", self.n * self.El, ptr(self.tab_src), 0, ptr(self.C_src), self.ldc * 2,
+        tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * self.El, ptr(self.tab_src), 0, ptr(self.C_src), self.ldc * 2,
              ptr(self.C_send), self.ldc * 2, self.ldc * 2, s)
 
     def b1(self):
         """Owner: C into its plan order -> shard backward -> per-instance dX sums."""
         s, d, Br = self._s(), self.d, self.Br
         sh = self.shard
-        call("smes_ep_copy_rows", self.n * self.El, ptr(self.tab_own), 1, ptr(self.C_recv), self.ldc * 2, ptr(sh.Cm),
+        tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * self.El, ptr(self.tab_own), 1, ptr(self.C_recv), self.ldc * 2, ptr(sh.Cm),
              sh.ldc * 2, self.ldc * 2, s)
         sh.backward(s, self.seg_pad_o)
-        call("smes_unpermute", Br, d, ptr(self.usize_o), ptr(self.row_of_o), self.umax_l, ptr(sh.dX), d, None,
+        tcall("unpermute", "smes_unpermute", Br, d, ptr(self.usize_o), ptr(self.row_of_o), self.umax_l, ptr(sh.dX), d, None,
              ptr(self.dh_own), s)
 
     def b2(self):
         """Source: router backward and d_hidden; stage the replicated gradients for the all-reduce."""
         s, T, E, B, d = self._s(), self.T, self.E, self.B, self.d
-        call("smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
+        tcall("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
              ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
-        call("smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits, T * E, d,
+        tcall("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits, T * E, d,
              ptr(self.seg_router_split), ptr(self.rw_part), ptr(self.rb_part), s)
         call("smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d, ptr(self.g_router_w), s)
         call("smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E, ptr(self.g_router_b), s)
         call("smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
         self.g_head_w.copy_(self.shard.g_head_w)
         self.loss_part_f32.copy_(self.loss_part)
-        call("smes_ep_combine_dh", B, d, self.n, B, ptr(self.pos), ptr(self.dh_recv), ptr(self.dh_router),
+        tcall("ep_combine_dh", "smes_ep_combine_dh", B, d, self.n, B, ptr(self.pos), ptr(self.dh_recv), ptr(self.dh_router),
              ptr(self.d_hidden), s)
 
     def finish(self):

@@ -15,7 +15,7 @@ from __future__ import annotations
 
 import torch
 
-from ._lib import call, ptr
+from ._lib import call, ptr, tcall
 from .errors import ConfigError, ShapeError
 
 
@@ -84,20 +84,20 @@ class ExpertShard:
         """P of every packed row (X already scattered; seg_pad = padded expert offsets)."""
         E, R, T = self.E, self.R, self.T
         di = self.dims[-2]
-        call("smes_fold_heads", E, T, self.ldg, self.d_out, di, ptr(self.head_w), ptr(self.w_bf[-1]),
+        tcall("fold_heads", "smes_fold_heads", E, T, self.ldg, self.d_out, di, ptr(self.head_w), ptr(self.w_bf[-1]),
              ptr(self.b32[-1]), ptr(self.G), ptr(self.c), ptr(self.work), s)
         if len(self.layers) == 1:
-            call("smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.G), E, self.ldg, di, 0, ptr(seg_pad),
+            tcall("fc1_fwd_folded", "smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.G), E, self.ldg, di, 0, ptr(seg_pad),
                  ptr(self.c), 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
             return
         if self.fuse:
-            call("smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), ptr(self.b32[0]), ptr(self.G),
+            tcall("mlp_fwd", "smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), ptr(self.b32[0]), ptr(self.G),
                  ptr(self.c), self.ldg, E, self.d, di, ptr(seg_pad), ptr(self.bits), R, ptr(self.H), self.ld_in[1],
                  ptr(self.P), self.ldp, s)
             return
-        call("smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), E, di, self.d, 0, ptr(seg_pad),
+        tcall("fc1_fwd", "smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), E, di, self.d, 0, ptr(seg_pad),
              ptr(self.b32[0]), 1, ptr(self.bits), None, R, ptr(self.H), self.ld_in[1], 0, R, s)
-        call("smes_gemm_ragged_m", ptr(self.H), self.ld_in[1], R, ptr(self.G), E, self.ldg, di, 0, ptr(seg_pad),
+        tcall("fc2_fwd_folded", "smes_gemm_ragged_m", ptr(self.H), self.ld_in[1], R, ptr(self.G), E, self.ldg, di, 0, ptr(seg_pad),
              ptr(self.c), 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
 
     # ------------------------------------------------------------------ backward
@@ -108,23 +108,23 @@ class ExpertShard:
         di = self.dims[-2]
         inp = self.X if L == 1 else self.H
         if L == 2 and self.fuse:
-            call("smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G), self.ldg, ptr(self.w_bf[0]), E, self.d, di,
+            tcall("mlp_dgrad", "smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G), self.ldg, ptr(self.w_bf[0]), E, self.d, di,
                  ptr(seg_pad), ptr(self.bits), R, ptr(self.dX), self.d, ptr(self.dH), di, s)
         else:
             dst = self.dX if L == 1 else self.dH
-            call("smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G), E, di, self.ldg, 1, ptr(seg_pad), None,
+            tcall(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G), E, di, self.ldg, 1, ptr(seg_pad), None,
                  0, None, ptr(self.bits) if L == 2 else None, R, ptr(dst), di, 0, R, s)
-        call("smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm), self.ldc, R, E, self.q_rows, self.ldg,
+        tcall(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm), self.ldc, R, E, self.q_rows, self.ldg,
              ptr(seg_pad), ptr(self.Qt), None, s)
         gw, gb = self.g_layers[L - 1]
         csum = self.Qt[:, di, :]
-        call("smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qt), self.q_rows * self.ldg, ptr(csum),
+        tcall("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qt), self.q_rows * self.ldg, ptr(csum),
              self.q_rows * self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw), ptr(gb),
              ptr(self.work), ptr(self.g_head_w), s)
         if L == 2:
             gw0, gb0 = self.g_layers[0]
-            call("smes_gemm_ragged_k", ptr(self.dH), di, ptr(self.X), self.ld_in[0], R, E, di, self.d, ptr(seg_pad),
+            tcall("fc1_wgrad", "smes_gemm_ragged_k", ptr(self.dH), di, ptr(self.X), self.ld_in[0], R, E, di, self.d, ptr(seg_pad),
                  ptr(gw0), ptr(gb0), s)
             if not self.fuse:
-                call("smes_gemm_ragged_m", ptr(self.dH), di, R, ptr(self.w_bf[0]), E, self.d, di, 1, ptr(seg_pad),
+                tcall("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.dH), di, R, ptr(self.w_bf[0]), E, self.d, di, 1, ptr(seg_pad),
                      None, 0, None, None, R, ptr(self.dX), self.d, 0, R, s)
