@@ -83,6 +83,10 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                        long m_limit, void* stream);
 int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
                        const int* seg, float* C, float* db_out, void* stream);
+/* ragged-K with one P shared by every group: P row m is read as row (m % a_period) of a
+ * (p_rows, I) matrix (a_period a multiple of 64; 0 = ordinary ragged-K). */
+int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G,
+                                int I, int J, const int* seg, float* C, float* db_out, int a_period, void* stream);
 
 /* ---- K4 combine + heads + BCE: replaces reconstruct_task_reps (execution.py:161-191),
  *      _heads (model.py:202-208) and _weighted_bce (training.py:54-57). */
@@ -119,8 +123,10 @@ int smes_bias_from_csum(int E, int T, int d_out, const float* csum, const float*
  *      (model.py:202-208 composed with execution.py:126-158; backward training.py:146-191):
  *      G (E, ldg, d_in) bf16 = head_w W_e (rows >= T zero), c (E, ldg) = head_w b_e, so the head
  *      projections are P = H G_e^T + c_e (an N = ldg GEMM) and d_packed never materialises.
- *      smes_unfold_grads expands Qt (E, d_in, ldg) = per-expert H^T C into dW = head_w^T Q_e,
- *      db = head_w^T csum_e and dW_head = sum_e (Q_e W_e^T + csum_e b_e^T).
+ *      smes_unfold_grads expands Q (E, ldg, d_in) = per-expert C^T H (q_expert_stride = ldg*d_in) and
+ *      csum (per-expert column sums of C) into dW = head_w^T Q_e, db = head_w^T csum_e and
+ *      dW_head = sum_e (Q_e W_e^T + csum_e b_e^T).  Large banks (E*d_out*d_in >= 2^24) run both as
+ *      grouped tcgen05 GEMMs (Q split into bf16 hi + lo rows), small ones as split-K CUDA-core tiles.
  *      work: fp32 scratch of smes_fold_work_floats(E, T, d_out, d_in) floats (split-K partials). */
 int smes_fold_work_floats(int E, int T, int d_out, int d_in);
 int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* head_w, const void* W_bf16,

@@ -32,6 +32,7 @@ SIGNATURES = {
     "smes_plan_scatter": [I, I, I, I, P, P, P, P, P, L, P, L, P, I, P, P, P, L, I, P],
     "smes_gemm_ragged_m": [P, L, L, P, I, I, I, I, P, P, I, P, P, L, P, L, I, L, P],
     "smes_gemm_ragged_k": [P, L, P, L, L, I, I, I, P, P, P, P],
+    "smes_gemm_ragged_k_periodic": [P, L, L, P, L, L, I, I, I, P, P, P, I, P],
     "smes_combine_grid": [I, I, I],
     "smes_combine_fwd": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, L, P, P, P, P, P, P, I, P],
     "smes_combine_bwd": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, L, P, P, P, P, F, I, P, P, P, F, I, P, P, P, I, P],
@@ -70,7 +71,7 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_sca
                     "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
                     "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,
-                    "smes_fold_heads": 2, "smes_unfold_grads": 3,
+                    "smes_fold_heads": 2, "smes_unfold_grads": 3, "smes_gemm_ragged_k_periodic": 1,
                     "smes_mlp_fwd": 1, "smes_mlp_dgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2}

@@ -10,7 +10,7 @@
 // and the backward of the combine + heads (training.py:146-191) is rank T per row:
 //   d_packed[r] = sum_t C[r, t] head_w_t,    C[r, t] = sum_{(b,k) -> r} w[t,b,k] dlogit[t,b]
 //   dH[r]       = C[r] G_e  (then the previous pool's ReLU mask),
-//   dW_e        = head_w^T Q_e,   Q_e = C_e^T H_e  (T x d_in, summed over the rows of e),
+//   dW_e        = head_w^T Q_e,   Q_e = C_e^T H_e  (T x d_in, summed over the rows of e; layout (E, ldg, d_in)),
 //   db_e        = head_w^T csum_e,   csum_e[t] = sum_{r in e} C[r, t],
 //   dW_head     = sum_e (Q_e W_e^T + csum_e b_e^T).
 //
@@ -31,7 +31,7 @@ namespace smes {
 // the matching T x 64 fp32 slice of the other operand, and writes a T x 64 fp32 partial; a
 // fixed-order reduction over the splits (and experts) finishes the job.  Deterministic.
 //   FOLD   : part[s, e, t, k] = sum_{j in split s} head_w[t, j] W[e, j, k]     (tile rows j, cols k)
-//   UNFOLD : part[s, e, t, j] = sum_{k in split s} Qt[e, k, t]  W[e, j, k]     (tile rows j, cols k)
+//   UNFOLD : part[s, e, t, j] = sum_{k in split s} Q[e, t, k]  W[e, j, k]      (tile rows j, cols k)
 enum { TILE_FOLD = 0, TILE_UNFOLD = 1 };
 
 template <int TM, int MODE>
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_ou
     const int t = i >> 6, r = i & 63;
     float x = 0.f;
     if (t < T && r0 + r < nr)
-      x = MODE == TILE_FOLD ? head_w[(size_t)t * d_out + r0 + r] : Qt[(size_t)e * q_es + (size_t)(r0 + r) * ldg + t];
+      x = MODE == TILE_FOLD ? head_w[(size_t)t * d_out + r0 + r] : Qt[(size_t)e * q_es + (size_t)t * d_in + r0 + r];
     sX[t][r] = x;
   }
   __syncthreads();
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(256) unfold_finish_kernel(int E, int T, int d_
   }
 }
 
-// dW[e, j, k] = sum_t head_w[t, j] Qt[e, k, t];  db[e, j] = sum_t head_w[t, j] csum[e, t]
+// dW[e, j, k] = sum_t head_w[t, j] Q[e, t, k];  db[e, j] = sum_t head_w[t, j] csum[e, t]
 template <int TM>
 __global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_out, int d_in,
                                                         const float* __restrict__ Qt, long q_es,
@@ -167,9 +167,9 @@ __global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_ou
   __syncthreads();
   if (k < d_in) {
     float q[TM];
-    const float* qp = Qt + (size_t)e * q_es + (size_t)k * ldg;
+    const float* qp = Qt + (size_t)e * q_es + k;
 #pragma unroll
-    for (int t = 0; t < TM; ++t) q[t] = t < T ? qp[t] : 0.f;
+    for (int t = 0; t < TM; ++t) q[t] = t < T ? qp[(size_t)t * d_in] : 0.f;
     const int jn = min(32, d_out - j0);
     for (int jj = 0; jj < jn; ++jj) {
       float s = 0.f;
@@ -185,6 +185,111 @@ __global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_ou
   }
 }
 
+// ---------------------------------------------------------------- tensor-core path (large E*d_out*d_in)
+// The same algebra as grouped GEMMs (csrc/gemm.cu):
+//   G_e   = head_w W_e       : ragged-K over the rows j of W_e, P = head_w^T shared by every expert
+//   dW_e  = head_w^T Q_e     : ragged-K over t (head_w and Q_e split into bf16 hi + lo rows: ~fp32 accuracy)
+//   Y_e   = Q_e W_e^T        : ragged-M (K = d_in) -> dW_head = sum_e (Y_e + csum_e b_e^T)
+__global__ void fold_prep_kernel(int T, int ldg, int d_out, const float* __restrict__ head_w,
+                                 __nv_bfloat16* __restrict__ Pw /* (d_out, ldg) */,
+                                 __nv_bfloat16* __restrict__ Wp /* (128, d_out) */) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (Pw != nullptr && i < d_out * ldg) {
+    const int j = i / ldg, t = i % ldg;
+    Pw[i] = __float2bfloat16_rn(t < T ? head_w[(size_t)t * d_out + j] : 0.f);
+  }
+  if (Wp != nullptr && i < 128 * d_out) {
+    // rows [0,32): hi(head_w), [32,64): hi(head_w), [64,96): lo(head_w) -- paired with Q hi / lo / hi
+    const int m = i / d_out, j = i % d_out;
+    const int t = m & 31;
+    float v = 0.f;
+    if (m < 96 && t < T) {
+      const float w = head_w[(size_t)t * d_out + j];
+      const float hi = __bfloat162float(__float2bfloat16_rn(w));
+      v = m < 64 ? hi : w - hi;
+    }
+    Wp[i] = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void seg_arith_kernel(int n, int step, int32_t* __restrict__ seg) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i <= n) seg[i] = i * step;
+}
+
+// G (bf16) from the fp32 GEMM output; c[e, t] = head_w[t] . b[e]
+__global__ void fold_convert_kernel(int E, int T, int ldg, int d_out, int d_in, const float* __restrict__ Gf,
+                                    const float* __restrict__ head_w, const float* __restrict__ b,
+                                    __nv_bfloat16* __restrict__ G, float* __restrict__ c) {
+  const size_t n = (size_t)E * ldg * d_in;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    G[i] = __float2bfloat16_rn(Gf[i]);
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp < E * ldg) {
+    const int e = warp / ldg, t = warp % ldg;
+    float s = 0.f;
+    if (t < T)
+      for (int j = lane; j < d_out; j += 32) s = fmaf(head_w[(size_t)t * d_out + j], b[(size_t)e * d_out + j], s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) c[(size_t)e * ldg + t] = s;
+  }
+}
+
+// Qbf[e][m] (128 rows per expert): rows t and 64 + t hold bf16(Q), rows 32 + t the bf16 remainder, so
+// sum_m Wp[m] Qbf[m] = hi(w) hi(q) + hi(w) lo(q) + lo(w) hi(q) (~fp32 accurate); Y uses rows t, 32 + t
+__global__ void unfold_split_kernel(int E, int T, int d_in, const float* __restrict__ Q, long q_es,
+                                    __nv_bfloat16* __restrict__ Qbf) {
+  const size_t n = (size_t)E * 128 * d_in;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(i % d_in);
+    const int m = (int)((i / d_in) % 128);
+    const int e = (int)(i / ((size_t)128 * d_in));
+    const int t = m & 31;
+    float v = 0.f;
+    if (m < 96 && t < T) {
+      const float q = Q[(size_t)e * q_es + (size_t)t * d_in + k];
+      const float hi = __bfloat162float(__float2bfloat16_rn(q));
+      v = (m >= 32 && m < 64) ? q - hi : hi;
+    }
+    Qbf[i] = __float2bfloat16_rn(v);
+  }
+}
+
+// db[e, j] = sum_t head_w[t, j] csum[e, t]
+__global__ void unfold_db_kernel(int E, int T, int d_out, const float* __restrict__ csum, long cs_es,
+                                 const float* __restrict__ head_w, float* __restrict__ db) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= E * d_out) return;
+  const int e = i / d_out, j = i % d_out;
+  float s = 0.f;
+  for (int t = 0; t < T; ++t) s = fmaf(head_w[(size_t)t * d_out + j], csum[(size_t)e * cs_es + t], s);
+  db[i] = s;
+}
+
+// dW_head[t, j] = sum_e (Y[e*128 + t, j] + Y[e*128 + 32 + t, j] + csum[e, t] b[e, j]), fixed order
+__global__ void __launch_bounds__(256) unfold_head_reduce_kernel(int E, int T, int d_out, const float* __restrict__ Y,
+                                                                 const float* __restrict__ csum, long cs_es,
+                                                                 const float* __restrict__ b, float* __restrict__ out) {
+  __shared__ float red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.y, j = blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (j < d_out)
+    for (int e = warp; e < E; e += 8) {
+      const float* y = Y + ((size_t)e * 128) * d_out + j;
+      acc += (y[(size_t)t * d_out] + y[(size_t)(32 + t) * d_out]) + csum[(size_t)e * cs_es + t] * b[(size_t)e * d_out + j];
+    }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && j < d_out) {
+    float v = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += red[w][lane];
+    out[(size_t)t * d_out + j] = v;
+  }
+}
+
 }  // namespace smes
 
 using namespace smes;
@@ -192,12 +297,43 @@ using namespace smes;
 extern "C" {
 
 static int fold_tm(int T) { return T <= 8 ? 8 : T <= 16 ? 16 : 32; }
+static long a64(long x) { return (x + 63) / 64 * 64; }
+
+// tensor-core path for large banks (c3/c5); the split-K CUDA-core tiles otherwise
+static bool gemm_path(int E, int T, int d_out, int d_in) {
+  return (long)E * d_out * d_in >= (1L << 24) && d_out % 64 == 0 && d_in % 64 == 0 && T <= 32;
+}
+
+struct FoldWork {            // offsets in floats
+  long pw, seg, gf, wp, seg128, qbf, y, total;
+};
+static FoldWork fold_layout(int E, int T, int d_out, int d_in) {
+  const int ldg = (T + 7) / 8 * 8;
+  FoldWork w{};
+  long o = 0;
+  w.pw = o; o += a64((long)d_out * ldg / 2 + 1);
+  w.seg = o; o += a64(E + 1);
+  w.gf = o; o += a64((long)E * ldg * d_in);
+  const long fold_end = o;
+  o = 0;
+  w.wp = o; o += a64((long)128 * d_out / 2);
+  w.seg128 = o; o += a64(E + 1);
+  w.qbf = o; o += a64((long)E * 128 * d_in / 2);
+  w.y = o; o += a64((long)E * 128 * d_out);
+  w.total = o > fold_end ? o : fold_end;
+  return w;
+}
 
 int smes_fold_work_floats(int E, int T, int d_out, int d_in) {
   const int tm = fold_tm(T);
-  const long a = (long)((d_out + 63) / 64) * E * tm * d_in;       // fold partials
+  const long a = (long)((d_out + 63) / 64) * E * tm * d_in;       // fold partials (CUDA-core path)
   const long b = (long)((d_in + 63) / 64) * E * tm * d_out;       // unfold partials
-  return (int)(a > b ? a : b);
+  long m = a > b ? a : b;
+  if (gemm_path(E, T, d_out, d_in)) {
+    const long g = fold_layout(E, T, d_out, d_in).total;
+    m = g > m ? g : m;
+  }
+  return (int)m;
 }
 
 int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* head_w, const void* W, const float* b,
@@ -207,54 +343,91 @@ int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* hea
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   auto Wb = reinterpret_cast<const __nv_bfloat16*>(W);
   auto Gb = reinterpret_cast<__nv_bfloat16*>(G);
-  const int splits = (d_out + 63) / 64;
-  dim3 grid((d_in + 63) / 64, E, splits);
-  const int nfin = (int)(((long)E * ldg * d_in + 255) / 256);
-  const int nfin_c = (E * ldg * 32 + 255) / 256;
-  const int gfin = nfin > nfin_c ? nfin : nfin_c;
-  switch (fold_tm(T)) {
-    case 8:
-      fold_tile_kernel<8, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
-      fold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
-      break;
-    case 16:
-      fold_tile_kernel<16, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
-      fold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
-      break;
-    default:
-      fold_tile_kernel<32, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
-      fold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+  if (gemm_path(E, T, d_out, d_in) && ldg == (T + 7) / 8 * 8) {
+    const FoldWork w = fold_layout(E, T, d_out, d_in);
+    auto* Pw = reinterpret_cast<__nv_bfloat16*>(work + w.pw);
+    auto* seg = reinterpret_cast<int32_t*>(work + w.seg);
+    float* Gf = work + w.gf;
+    fold_prep_kernel<<<(d_out * ldg + 255) / 256, 256, 0, st>>>(T, ldg, d_out, head_w, Pw, nullptr);
+    seg_arith_kernel<<<(E + 256) / 256, 256, 0, st>>>(E, d_out, seg);
+    int rc = smes_gemm_ragged_k_periodic(Pw, ldg, d_out, W, d_in, (long)E * d_out, E, ldg, d_in, seg, Gf, nullptr,
+                                         d_out, stream);
+    if (rc) return rc;
+    const long n = (long)E * ldg * d_in;
+    const long blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
+    const long need = ((long)E * ldg * 32 + 255) / 256;
+    fold_convert_kernel<<<(int)(blocks > need ? blocks : need), 256, 0, st>>>(E, T, ldg, d_out, d_in, Gf, head_w, b,
+                                                                               Gb, c);
+  } else {
+    const int splits = (d_out + 63) / 64;
+    dim3 grid((d_in + 63) / 64, E, splits);
+    const int nfin = (int)(((long)E * ldg * d_in + 255) / 256);
+    const int nfin_c = (E * ldg * 32 + 255) / 256;
+    const int gfin = nfin > nfin_c ? nfin : nfin_c;
+    switch (fold_tm(T)) {
+      case 8:
+        fold_tile_kernel<8, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
+        fold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+        break;
+      case 16:
+        fold_tile_kernel<16, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
+        fold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+        break;
+      default:
+        fold_tile_kernel<32, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
+        fold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+    }
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SMES_OK : set_error(SMES_ERR_CUDA, "fold_heads: %s", cudaGetErrorString(e));
 }
 
-int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Qt, long q_es, const float* csum,
+int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q, long q_es, const float* csum,
                       long cs_es, const float* head_w, const void* W, const float* b, float* dW, float* db,
                       float* work, float* d_head_w, void* stream) {
   if (T < 1 || T > 32 || ldg < T) return set_error(SMES_ERR_SHAPE, "unfold_grads: T=%d ldg=%d", T, ldg);
   if (d_in % 8) return set_error(SMES_ERR_SHAPE, "unfold_grads: d_in=%d must be a multiple of 8", d_in);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   auto Wb = reinterpret_cast<const __nv_bfloat16*>(W);
-  dim3 g1((d_in + 127) / 128, (d_out + 31) / 32, E);
-  const int splits = (d_in + 63) / 64;
-  dim3 g2((d_out + 63) / 64, E, splits);
-  dim3 gfin((d_out + 31) / 32, T);
-  switch (fold_tm(T)) {
-    case 8:
-      unfold_dw_kernel<8><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Qt, q_es, csum, cs_es, head_w, dW, db);
-      fold_tile_kernel<8, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Qt, q_es, Wb, work);
-      unfold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
-      break;
-    case 16:
-      unfold_dw_kernel<16><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Qt, q_es, csum, cs_es, head_w, dW, db);
-      fold_tile_kernel<16, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Qt, q_es, Wb, work);
-      unfold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
-      break;
-    default:
-      unfold_dw_kernel<32><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Qt, q_es, csum, cs_es, head_w, dW, db);
-      fold_tile_kernel<32, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Qt, q_es, Wb, work);
-      unfold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+  if (gemm_path(E, T, d_out, d_in)) {
+    const FoldWork w = fold_layout(E, T, d_out, d_in);
+    auto* Wp = reinterpret_cast<__nv_bfloat16*>(work + w.wp);
+    auto* seg = reinterpret_cast<int32_t*>(work + w.seg128);
+    auto* Qbf = reinterpret_cast<__nv_bfloat16*>(work + w.qbf);
+    float* Y = work + w.y;
+    fold_prep_kernel<<<(128 * d_out + 255) / 256, 256, 0, st>>>(T, ldg, d_out, head_w, nullptr, Wp);
+    seg_arith_kernel<<<(E + 256) / 256, 256, 0, st>>>(E, 128, seg);
+    unfold_split_kernel<<<4096, 256, 0, st>>>(E, T, d_in, Q, q_es, Qbf);
+    int rc = smes_gemm_ragged_k_periodic(Wp, d_out, 128, Qbf, d_in, (long)E * 128, E, d_out, d_in, seg, dW, nullptr,
+                                         128, stream);
+    if (rc) return rc;
+    unfold_db_kernel<<<(E * d_out + 255) / 256, 256, 0, st>>>(E, T, d_out, csum, cs_es, head_w, db);
+    rc = smes_gemm_ragged_m(Qbf, d_in, (long)E * 128, W, E, d_out, d_in, 0, seg, nullptr, 0, nullptr, nullptr, 0, Y,
+                            d_out, 1, (long)E * 128, stream);
+    if (rc) return rc;
+    dim3 g((d_out + 31) / 32, T);
+    unfold_head_reduce_kernel<<<g, 256, 0, st>>>(E, T, d_out, Y, csum, cs_es, b, d_head_w);
+  } else {
+    dim3 g1((d_in + 127) / 128, (d_out + 31) / 32, E);
+    const int splits = (d_in + 63) / 64;
+    dim3 g2((d_out + 63) / 64, E, splits);
+    dim3 gfin((d_out + 31) / 32, T);
+    switch (fold_tm(T)) {
+      case 8:
+        unfold_dw_kernel<8><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, csum, cs_es, head_w, dW, db);
+        fold_tile_kernel<8, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, Wb, work);
+        unfold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+        break;
+      case 16:
+        unfold_dw_kernel<16><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, csum, cs_es, head_w, dW, db);
+        fold_tile_kernel<16, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, Wb, work);
+        unfold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+        break;
+      default:
+        unfold_dw_kernel<32><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, csum, cs_es, head_w, dW, db);
+        fold_tile_kernel<32, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, Wb, work);
+        unfold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+    }
   }
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SMES_OK : set_error(SMES_ERR_CUDA, "unfold_grads: %s", cudaGetErrorString(e));

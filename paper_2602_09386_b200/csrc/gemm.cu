@@ -41,6 +41,7 @@ struct GemmArgs {
   const uint32_t* bits_in;    // relu bitmask applied to the output (dgrad), or null
   int bits_ld;
   float* db_out;              // ragged-K: per-group column sums of P via Q's ones column (G, I), or null
+  int a_period;               // ragged-K: P rows are read modulo this period (a shared P for every group), or 0
 };
 
 // Shared-memory plan.  ragged-M tiles are epilogue(store)-paced at the c2 shapes, so every
@@ -187,7 +188,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, k0);
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, args.a_period ? k0 % args.a_period : k0);
 #pragma unroll
             for (int j = 0; j < NBBOX; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
           }
@@ -490,7 +492,7 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                        str, box)))
       return rc;
   }
-  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, nullptr};
+  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, nullptr, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (narrow) return launch<32, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
   // K-major B box is {64, 256} for N >= 256: requires BN == 256
@@ -498,8 +500,8 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
   return launch_m<128>(b_mn, out_fp32, ta, tb, tc, args, st);
 }
 
-int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
-                       const int* seg, float* C, float* db_out, void* stream) {
+int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G,
+                                int I, int J, const int* seg, float* C, float* db_out, int a_period, void* stream) {
   if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
   if (I <= 0 || J <= 0) return set_error(SMES_ERR_SHAPE, "empty wgrad I=%d J=%d", I, J);
   if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16)
@@ -507,7 +509,8 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
   CUtensorMap ta, tb, tc;
   int rc;
   {
-    uint64_t dims[2] = {(uint64_t)I, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldp * 2};
+    if (a_period < 0 || a_period % BK) return set_error(SMES_ERR_SHAPE, "wgrad: P period %d must be a multiple of 64", a_period);
+    uint64_t dims[2] = {(uint64_t)I, (uint64_t)(a_period ? p_rows : rows_cap)}, str[1] = {(uint64_t)ldp * 2};
     uint32_t box[2] = {64, 64};
     if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, P, dims, str, box))) return rc;
   }
@@ -522,11 +525,19 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
     uint32_t box[3] = {32, 32, 1};
     if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, str, box))) return rc;
   }
-  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out};
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out, a_period};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (J <= 16) return launch<16, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
-  if (J >= 256) return launch<256, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+  // BN = 256 halves the tile count; with a single i-tile (I <= 128: the folded-head wgrad) keep
+  // it only while the grid still covers every SM
+  const int tiles256 = G * ((I + BM - 1) / BM) * ((J + 255) / 256);
+  if (J >= 256 && (I > BM || tiles256 >= num_sms())) return launch<256, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
   return launch<128, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+}
+
+int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
+                       const int* seg, float* C, float* db_out, void* stream) {
+  return smes_gemm_ragged_k_periodic(P, ldp, rows_cap, Q, ldq, rows_cap, G, I, J, seg, C, db_out, 0, stream);
 }
 
 }  // extern "C"

@@ -60,8 +60,8 @@ class ExpertShard:
         di = self.dims[-2]
         self.G = z(E, self.ldg, di, dt=bf)
         self.c = z(E, self.ldg)
-        self.q_rows = di + 1                               # ones column -> per-expert sums of C
-        self.Qt = z(E, self.q_rows, self.ldg)
+        self.Qe = z(E, self.ldg, di)                       # per-expert C^T H
+        self.csum = z(E, self.ldg)                         # per-expert column sums of C
         self.work = z(call("smes_fold_work_floats", E, T, self.d_out, di))
         shapes = [(E, l.d_out, l.d_in) for l in layers] + [(E, l.d_out) for l in layers]
         sizes = [int(torch.Size(s).numel()) for s in shapes]
@@ -114,13 +114,12 @@ class ExpertShard:
             dst = self.dX if L == 1 else self.dH
             tcall(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G), E, di, self.ldg, 1, ptr(seg_pad), None,
                  0, None, ptr(self.bits) if L == 2 else None, R, ptr(dst), di, 0, R, s)
-        tcall(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm), self.ldc, R, E, self.q_rows, self.ldg,
-             ptr(seg_pad), ptr(self.Qt), None, s)
+        tcall(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(inp), self.ld_in[L - 1], R, E,
+              self.ldg, di, ptr(seg_pad), ptr(self.Qe), ptr(self.csum), s)
         gw, gb = self.g_layers[L - 1]
-        csum = self.Qt[:, di, :]
-        tcall("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qt), self.q_rows * self.ldg, ptr(csum),
-             self.q_rows * self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw), ptr(gb),
-             ptr(self.work), ptr(self.g_head_w), s)
+        tcall("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), self.ldg * di,
+              ptr(self.csum), self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw), ptr(gb),
+              ptr(self.work), ptr(self.g_head_w), s)
         if L == 2:
             gw0, gb0 = self.g_layers[0]
             tcall("fc1_wgrad", "smes_gemm_ragged_k", ptr(self.dH), di, ptr(self.X), self.ld_in[0], R, E, di, self.d, ptr(seg_pad),
