@@ -674,7 +674,7 @@ int smes_combine_grid(int B, int T, int d_out) {
   const int S = vpl > 0 ? d_out / (32 * vpl) : 1;
   const int G = CB_WARPS / (S > 0 ? S : 1);
   int need = (B + G - 1) / G;
-  int g = 148 * 2;     // ~1-2 resident CTAs per SM (register / smem bound); fewer head-grad partials
+  int g = 148 * 4;     // 4 resident CTAs per SM (register bound): latency hiding for the per-row gathers
   return need < g ? need : g;
 }
 

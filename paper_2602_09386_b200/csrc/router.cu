@@ -155,9 +155,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     double pooled[EPL];
 #pragma unroll
     for (int j = 0; j < EPL; ++j) pooled[j] = 0.0;
-    for (int t = 0; t < T; ++t) {
-      float zv[EPL];
-      load_task(t, zv);
+    auto stage1_task = [&](int t, const float (&zv)[EPL]) {
       double p[EPL];
       if (a.probs_in == nullptr) {
         uint32_t mk = 0;
@@ -179,8 +177,9 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        const double inv_sum = 1.0 / sum;
 #pragma unroll
-        for (int j = 0; j < EPL; ++j) p[j] = p[j] / sum;
+        for (int j = 0; j < EPL; ++j) p[j] *= inv_sum;
       } else {
         const double* pr = a.probs_in + ((long)t * a.B + b) * E;
 #pragma unroll
@@ -203,6 +202,18 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
           const int e = lane + 32 * j;
           if (e < E) po[e] = p[j];
         }
+      }
+    };
+    if (TP > 0) {
+      // T <= TP: fully unrolled task loop, logits indexed statically from registers
+#pragma unroll
+      for (int t = 0; t < (TP > 0 ? TP : 1); ++t)
+        if (t < T) stage1_task(t, zpre[t]);
+    } else {
+      for (int t = 0; t < T; ++t) {
+        float zv[EPL];
+        load_task(t, zv);
+        stage1_task(t, zv);
       }
     }
     // shared set S: top-K_s of pooled, (score desc, index asc)   (routing.py:261, :184-187)
@@ -233,9 +244,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
 
     // ---------------- Stage II per task: top-K_a of z_t with S excluded (routing.py:263-268)
     uint32_t in_union = taken;
-    for (int t = 0; t < T; ++t) {
-      float zv[EPL];
-      load_task(t, zv);
+    auto stage2_task = [&](int t, const float (&zv)[EPL]) {
       uint32_t picked = 0;
       const long ot = ((long)t * a.B + b);
       if (a.frozen) {
@@ -287,6 +296,17 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         }
       }
       (void)inv;
+    };
+    if (TP > 0) {
+#pragma unroll
+      for (int t = 0; t < (TP > 0 ? TP : 1); ++t)
+        if (t < T) stage2_task(t, zpre[t]);
+    } else {
+      for (int t = 0; t < T; ++t) {
+        float zv[EPL];
+        load_task(t, zv);
+        stage2_task(t, zv);
+      }
     }
     // union bitmask words and size (routing.py:272)
     int usz = 0;
