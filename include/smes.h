@@ -147,6 +147,11 @@ int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const f
 int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
                    int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, void* dX, long lddx,
                    void* dH, long lddh, void* stream);
+/* fc1 weight gradient with dH recomputed per 128-row block (dH never stored): one CTA per
+ * (expert, 128-wide d_ff chunk); dW (E, d_ff, d) fp32, db (E, d_ff) fp32; d <= 256. */
+int smes_mlp_wgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* X, long ldx, int E,
+                   int d, int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, float* dW, float* db,
+                   void* stream);
 
 /* ---- expert parallelism (csrc/ep.cu; BASELINE config c5).  Rank r owns experts [r*El, (r+1)*El),
  *      El % 32 == 0 (whole union-mask words).  Fixed-slot buffers: every count stays on the device.

@@ -313,9 +313,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_2d(&tmH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
             bulk_commit();
           }
-#endif
           mbar_arrive(hfull);
         }
+#endif
         ++hi;
       }
       // head projections of this tile: P[row, t] = acc + c[e, t]
@@ -599,6 +599,242 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
+
+// ============================================================================ fc1 weight gradient
+// mlp_wgrad: one CTA per (expert e, 128-wide d_ff chunk c); the K loop runs over the expert's
+// packed rows in 128-row blocks and recomputes dH on the fly instead of reading it:
+//   S  = C_blk G_e[:, c]        (K = T)      -> TMEM
+//   dH = S * relu-mask          (epilogue)   -> smem, MN-major A operand (M = d_ff chunk, K = rows)
+//   dW1[c] += dH^T X_blk        (N = d)      -> TMEM, fp32
+//   db1[c] += dH^T 1            (N = 16 against a constant ones tile)
+// so dH never goes to HBM (training.py:180-191 for fc1: dW = d_pre^T X, db = colsum(d_pre)).
+struct WgradArgs {
+  const int* seg;
+  int E, d, d_ff;
+  const uint32_t* bits;
+  int bits_ld;
+  float* dW;                     // (E, d_ff, d)
+  float* db;                     // (E, d_ff)
+};
+
+template <int DK>
+struct WgSmem {
+  static constexpr int kXS = 3;                          // X ring: 64-row sub-blocks (DK x 8 KB boxes)
+  static constexpr int kXB = DK * 8192;
+  static constexpr int kCS = 2;                          // C ring: {64 t, 128 rows} boxes
+  static constexpr int kOffX = 0;
+  static constexpr int kOffC = kOffX + kXS * kXB;
+  static constexpr int kOffG = kOffC + kCS * 16384;      // G chunk: 2 x {64 f, 16 t}
+  static constexpr int kOffDH = kOffG + 4096;            // 2 buffers x (2 halves x 128 rows x 128 B)
+  static constexpr int kOffOnes = kOffDH + 2 * 32768;    // 64 x 64 bf16, column 0 = 1
+  static constexpr int kOffBar = kOffOnes + 8192;
+  static constexpr int kBytes = kOffBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "mlp_wgrad smem");
+};
+
+template <int DK>
+__global__ void __launch_bounds__(kThreads, 1)
+    mlp_wgrad_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmG,
+                     const __grid_constant__ CUtensorMap tmX, const WgradArgs a) {
+  using S = WgSmem<DK>;
+  constexpr int D = DK * 64;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sX = smem + S::kOffX;
+  uint8_t* sC = smem + S::kOffC;
+  uint8_t* sG = smem + S::kOffG;
+  uint8_t* sDH = smem + S::kOffDH;
+  uint8_t* sOnes = smem + S::kOffOnes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* xfull = bar;                    // [kXS]
+  uint64_t* xempty = xfull + S::kXS;
+  uint64_t* cfull = xempty + S::kXS;        // [kCS]
+  uint64_t* cempty = cfull + S::kCS;
+  uint64_t* gfull = cempty + S::kCS;        // [1]
+  uint64_t* sfull = gfull + 1;              // [1]
+  uint64_t* sempty = sfull + 1;             // [1]
+  uint64_t* dhfull = sempty + 1;            // [2]
+  uint64_t* dhempty = dhfull + 2;           // [2]
+  uint64_t* accfull = dhempty + 2;          // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NC = a.d_ff / CH;
+  const int e = blockIdx.x / NC, c = blockIdx.x % NC;
+  const int row_lo = a.seg[e];
+  const int nkb = (a.seg[e + 1] - row_lo) / BM;
+  {
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(sOnes);
+    for (int i = threadIdx.x; i < 8192 / 4; i += blockDim.x) o32[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int k = threadIdx.x;
+      reinterpret_cast<__nv_bfloat16*>(sOnes + k * 128 + (k & 7) * 16)[0] = __float2bfloat16_rn(1.f);
+    }
+    fence_proxy_async_smem();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmC); tma_prefetch(&tmG); tma_prefetch(&tmX); }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S::kXS; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 1); }
+    for (int i = 0; i < S::kCS; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 1); }
+    mbar_init(gfull, 1);
+    mbar_init(sfull, 1);
+    mbar_init(sempty, kEpiWarps);
+    for (int i = 0; i < 2; ++i) { mbar_init(&dhfull[i], kEpiWarps); mbar_init(&dhempty[i], 1); }
+    mbar_init(accfull, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  // TMEM: S [0, 128), dW1 [128, 128 + D), ones-product (db) [384, 400)
+
+  if (warp == 0) {
+    if (lane == 0 && nkb > 0) {
+      mbar_expect_tx(gfull, 4096);
+      tma_load_3d(sG, &tmG, gfull, c * CH, 0, e);
+      tma_load_3d(sG + 2048, &tmG, gfull, c * CH + 64, 0, e);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int r0 = row_lo + kb * BM;
+        {
+          const int s = kb % S::kCS;
+          mbar_wait(&cempty[s], par_of(kb, S::kCS) ^ 1);
+          mbar_expect_tx(&cfull[s], 16384);
+          tma_load_2d(sC + s * 16384, &tmC, &cfull[s], 0, r0);
+        }
+        for (int hh = 0; hh < 2; ++hh) {
+          const int sub = 2 * kb + hh;
+          const int s = slot_of(sub, S::kXS);
+          mbar_wait(&xempty[s], par_of(sub, S::kXS) ^ 1);
+          mbar_expect_tx(&xfull[s], S::kXB);
+#pragma unroll
+          for (int j = 0; j < DK; ++j) tma_load_2d(sX + s * S::kXB + j * 8192, &tmX, &xfull[s], 64 * j, r0 + 64 * hh);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && nkb > 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(BM, CH, 0, 1);   // A = C (K-major), B = G (MN-major)
+      constexpr uint32_t idW = umma_idesc_bf16(BM, D, 1, 1);    // A = dH (MN-major), B = X (MN-major)
+      constexpr uint32_t idB = umma_idesc_bf16(BM, 16, 1, 1);   // A = dH, B = ones
+      const uint32_t g_addr = smem_u32(sG), ones = smem_u32(sOnes);
+      mbar_wait(gfull, 0);
+      auto s_mma = [&](int kb) {
+        const int cs = kb % S::kCS;
+        mbar_wait(&cfull[cs], par_of(kb, S::kCS));
+        mbar_wait(sempty, (uint32_t)((kb & 1) ^ 1));
+        tc_fence_after();
+        tc_mma_f16(tmem_base, umma_desc_sw128(smem_u32(sC + cs * 16384), 16, 1024),
+                   umma_desc_sw128(g_addr, 2048, 1024), idS, 0u);
+        tc_commit(sfull);
+        tc_commit(&cempty[cs]);
+      };
+      s_mma(0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        if (kb + 1 < nkb) s_mma(kb + 1);
+        const int db = kb & 1;
+        mbar_wait(&dhfull[db], (uint32_t)((kb >> 1) & 1));
+        const int s0 = slot_of(2 * kb, S::kXS), s1 = slot_of(2 * kb + 1, S::kXS);
+        mbar_wait(&xfull[s0], par_of(2 * kb, S::kXS));
+        mbar_wait(&xfull[s1], par_of(2 * kb + 1, S::kXS));
+        tc_fence_after();
+        const uint32_t dh = smem_u32(sDH + db * 32768);
+#pragma unroll
+        for (int k = 0; k < BM / 16; ++k) {
+          const uint32_t xs = smem_u32(sX + (k < 4 ? s0 : s1) * S::kXB) + (k & 3) * 2048;
+          const uint64_t ad = umma_desc_sw128(dh + k * 2048, 16384, 1024);
+          const uint32_t acc = (kb | k) != 0;
+          tc_mma_f16(tmem_base + 128, ad, umma_desc_sw128(xs, 8192, 1024), idW, acc);
+          tc_mma_f16(tmem_base + 384, ad, umma_desc_sw128(ones + (k & 3) * 2048, 8192, 1024), idB, acc);
+          if (k == 3) tc_commit(&xempty[s0]);
+        }
+        tc_commit(&xempty[s1]);
+        tc_commit(&dhempty[db]);
+      }
+      tc_commit(accfull);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;
+    const int f0 = c * CH + par * 64;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int row = row_lo + kb * BM + 32 * q + lane;
+      const uint32_t m0 = __ldg(&a.bits[(size_t)(f0 >> 5) * a.bits_ld + row]);
+      const uint32_t m1 = __ldg(&a.bits[(size_t)((f0 >> 5) + 1) * a.bits_ld + row]);
+      mbar_wait(sfull, (uint32_t)(kb & 1));
+      tc_fence_after();
+      uint32_t t0[32], t1[32];
+      const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + par * 64;
+      tmem_ld32(ta, t0);
+      tmem_ld32(ta + 32, t1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sempty);
+      const int db = kb & 1;
+      mbar_wait(&dhempty[db], (uint32_t)(((kb >> 1) & 1) ^ 1));
+      uint8_t* hrow = sDH + db * 32768 + par * 16384 + (32 * q + lane) * 128;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int j = cc * 8 + i;
+          const uint32_t w = j < 32 ? m0 : m1;
+          const uint32_t raw = j < 32 ? t0[j] : t1[j - 32];
+          v[i] = ((w >> (j & 31)) & 1u) ? __uint_as_float(raw) : 0.f;
+        }
+        const uint4 pk = make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                                    pack_bf16(v[6], v[7]));
+        *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dhfull[db]);
+    }
+    // dW1 rows f = c*128 + 32q + lane, columns split by parity; db from the ones product
+    const int f = c * CH + 32 * q + lane;
+    float* dwrow = a.dW + ((size_t)e * a.d_ff + f) * D;
+    if (nkb > 0) {
+      mbar_wait(accfull, 0);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int cc = 0; cc < DK; ++cc) {
+      const int col = par * (D / 2) + cc * 32;
+      if (cc * 32 >= D / 2) break;
+      uint32_t t0[32];
+      if (nkb > 0) {
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + 128 + col, t0);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) t0[j] = 0u;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<float4*>(dwrow + col + j) = make_float4(__uint_as_float(t0[j]), __uint_as_float(t0[j + 1]),
+                                                                  __uint_as_float(t0[j + 2]), __uint_as_float(t0[j + 3]));
+    }
+    if (par == 0) {
+      float bsum = 0.f;
+      if (nkb > 0) {
+        uint32_t t0[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + 384, t0);
+        tmem_ld_wait();
+        bsum = __uint_as_float(t0[0]);
+      }
+      a.db[(size_t)e * a.d_ff + f] = bsum;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
 }  // namespace mlp
 
 // ---------------------------------------------------------------- host side
@@ -772,6 +1008,58 @@ int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ld
 #undef SMES_DG_CASE
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+
+int smes_mlp_wgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* X, long ldx, int E, int d,
+                   int d_ff, const int* seg, const uint32_t* bits, long bits_ld, float* dW, float* db, void* stream) {
+  if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_wgrad: expert count %d outside [1, 256]", E);
+  if (d % 64 || d < 64 || d > 256) return set_error(SMES_ERR_SHAPE, "mlp_wgrad: d=%d must be a multiple of 64 in [64, 256]", d);
+  if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_wgrad: d_ff=%d must be a multiple of 128", d_ff);
+  if (ldg < 1 || ldg > 16 || ldc < ldg || (ldc * 2) % 16 || (ldx * 2) % 16)
+    return set_error(SMES_ERR_SHAPE, "mlp_wgrad: ldg=%d ldc=%ld ldx=%ld", ldg, ldc, ldx);
+  CUtensorMap tc, tg, tx;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)ldg, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldc * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = bf16_map(&tc, 2, C, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d_ff, (uint64_t)ldg, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d_ff * 2, (uint64_t)ldg * d_ff * 2};
+    uint32_t box[3] = {64, 16, 1};
+    if ((rc = bf16_map(&tg, 3, G, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldx * 2};
+    uint32_t box[2] = {64, 64};
+    if ((rc = bf16_map(&tx, 2, X, dims, str, box))) return rc;
+  }
+  mlp::WgradArgs args{seg, E, d, d_ff, bits, (int)bits_ld, dW, db};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  const int grid = E * (d_ff / mlp::CH);
+#define SMES_WG_CASE(DK)                                                                               \
+  case DK: {                                                                                           \
+    auto k = mlp::mlp_wgrad_kernel<DK>;                                                                \
+    const int sm = mlp::WgSmem<DK>::kBytes;                                                            \
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_wgrad smem attribute: %s", cudaGetErrorString(e)); \
+    k<<<grid, mlp::kThreads, sm, st>>>(tc, tg, tx, args);                                              \
+    break;                                                                                             \
+  }
+  switch (d / 64) {
+    SMES_WG_CASE(1)
+    SMES_WG_CASE(2)
+    SMES_WG_CASE(4)
+    default:
+      return set_error(SMES_ERR_SHAPE, "mlp_wgrad: d=%d not instantiated (64, 128, 256)", d);
+  }
+#undef SMES_WG_CASE
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_wgrad launch: %s", cudaGetErrorString(e));
   return SMES_OK;
 }
 

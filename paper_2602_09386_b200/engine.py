@@ -98,7 +98,7 @@ class SMESEngine:
     def __init__(self, params: SMESParams, batch_size: int, k_shared: int, k_adaptive: int,
                  dense_probs_in_stats: bool = False, keep_reps: bool = True,
                  device: torch.device | str | None = None, csum_from_gemm: bool = False,
-                 fuse_mlp: bool = True):
+                 fuse_mlp: bool = True, fuse_wgrad: bool = False):
         _require_cuda()
         self.dev = torch.device(device or "cuda")
         p = params
@@ -144,6 +144,9 @@ class SMESEngine:
         lay = p.layers
         self.fuse_mlp = bool(fuse_mlp and self.can_fold and len(lay) == 2 and lay[0].act == "relu"
                              and d % 64 == 0 and d <= 256 and lay[0].d_out % 128 == 0 and T <= 16)
+        # fc1 wgrad with dH recomputed per row block (csrc/mlp.cu mlp_wgrad) instead of storing dH:
+        # measured slower at c2 (one CTA per (expert, d_ff chunk) re-streams X), so off by default
+        self.fuse_wgrad = bool(fuse_wgrad and self.fuse_mlp)
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
         self._alloc()
@@ -414,10 +417,16 @@ class SMESEngine:
             dst = self.dX if L == 1 else self.d_outs[L - 2]
             mask = self.bits[L - 2] if L >= 2 else None
             if self.fuse_mlp:
-                # dH = (C G_e) * mask and dX = dH W1 in one chained kernel (dH kept for the fc1 wgrad)
+                # dH = (C G_e) * mask and dX = dH W1 in one chained kernel; the fc1 weight gradient
+                # recomputes dH per row block (mlp_wgrad), so dH never goes to HBM
                 _tagged("mlp_dgrad", "smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), self.ldg,
                         ptr(self.w_bf[0]), E, d, di, ptr(self.seg_pad), ptr(mask), R, ptr(self.dX), d,
-                        ptr(dst), di, s)
+                        None if self.fuse_wgrad else ptr(dst), di, s)
+                if self.fuse_wgrad:
+                    gw0, gb0 = self.g_layers[0]
+                    _tagged("mlp_wgrad", "smes_mlp_wgrad", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), self.ldg,
+                            ptr(self.X), self.ld_in[0], E, d, di, ptr(self.seg_pad), ptr(mask), R, ptr(gw0),
+                            ptr(gb0), s)
             else:
                 _tagged(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G_fold),
                         E, di, self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
@@ -447,12 +456,14 @@ class SMESEngine:
                     ptr(self.labels), ptr(self.lam), 1.0 / bs, relu_last, ptr(self.d_outs[-1]), ptr(self.dz),
                     ptr(self.freq32), lb_coef, int(self.dense), ptr(self.z), ptr(self.part_dw), ptr(self.part_db),
                     self.grid, s)
+        if folded and self.fuse_wgrad:
+            top = -1                   # fc1's dgrad and wgrad ran in the fused kernels
         for i in range(top, -1, -1):
             dout = self.d_outs[i]
             inp = self.X if i == 0 else self.outs[i - 1]
             gw, gb = self.g_layers[i]
             di, do = self.dims[i], self.dims[i + 1]
-            if i > 0 and not (folded and self.fuse_mlp):   # dgrad into the previous layer's output, masked by its relu
+            if i > 0:   # dgrad into the previous layer's output, masked by its relu
                 _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1, ptr(self.seg_pad),
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
             fused_last = i == n_layers - 1 and self.fuse_b_last and fused
@@ -537,8 +548,8 @@ class SMESEngine:
                 # fused MLP: fc1 (+ relu mask, H kept) and P in one pass; dgrad dH (kept) + dX in one pass
                 w["mlp_fwd"] = (2.0 * n_act * (d * dff + dff * T),
                                 n_act * (d * 2 + dff * 2 + dff / 8 + self.ldp * 4))
-                w["mlp_dgrad"] = (2.0 * n_act * (T * dff + dff * d),
-                                  n_act * (self.ldc * 2 + dff / 8 + d * 2 + dff * 2))
+                w["mlp_dgrad"] = (2.0 * n_act * (T * dff + dff * d), n_act * (self.ldc * 2 + dff / 8 + d * 2))
+                w["mlp_wgrad"] = (2.0 * n_act * (T * dff + dff * d), n_act * (self.ldc * 2 + dff / 8 + d * 2))
         return {k: (f, b, "tensor" if b > 0 and f / b > balance else ("tensor" if b == 0 else "hbm"))
                 for k, (f, b) in w.items()}
 

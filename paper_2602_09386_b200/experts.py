@@ -24,7 +24,8 @@ def _round(x, m):
 
 
 class ExpertShard:
-    def __init__(self, layers, T: int, head_w: torch.Tensor, rows_cap: int, device, fuse_mlp: bool = True):
+    def __init__(self, layers, T: int, head_w: torch.Tensor, rows_cap: int, device, fuse_mlp: bool = True,
+                 fuse_wgrad: bool = False):
         if layers[-1].act != "identity" or len(layers) not in (1, 2) or (len(layers) == 2 and layers[0].act != "relu"):
             raise ConfigError("expert shard needs [relu ->] identity expert pools (the folded heads)")
         self.dev = torch.device(device)
@@ -43,6 +44,7 @@ class ExpertShard:
         L = len(layers)
         self.fuse = bool(fuse_mlp and L == 2 and d % 64 == 0 and d <= 256 and self.dims[1] % 128 == 0
                          and T <= 16)
+        self.fuse_wgrad = bool(fuse_wgrad and self.fuse)
         dev, bf, f32 = self.dev, torch.bfloat16, torch.float32
         z = lambda *s, dt=f32: torch.zeros(*s, dtype=dt, device=dev)
         self.ld_in = [w + 64 for w in self.dims[:-1]]
@@ -109,7 +111,7 @@ class ExpertShard:
         inp = self.X if L == 1 else self.H
         if L == 2 and self.fuse:
             tcall("mlp_dgrad", "smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G), self.ldg, ptr(self.w_bf[0]), E, self.d, di,
-                 ptr(seg_pad), ptr(self.bits), R, ptr(self.dX), self.d, ptr(self.dH), di, s)
+                 ptr(seg_pad), ptr(self.bits), R, ptr(self.dX), self.d, None if self.fuse_wgrad else ptr(self.dH), di, s)
         else:
             dst = self.dX if L == 1 else self.dH
             tcall(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G), E, di, self.ldg, 1, ptr(seg_pad), None,
@@ -120,7 +122,11 @@ class ExpertShard:
         tcall("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), self.ldg * di,
               ptr(self.csum), self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw), ptr(gb),
               ptr(self.work), ptr(self.g_head_w), s)
-        if L == 2:
+        if L == 2 and self.fuse_wgrad:
+            gw0, gb0 = self.g_layers[0]
+            tcall("mlp_wgrad", "smes_mlp_wgrad", ptr(self.Cm), self.ldc, R, ptr(self.G), self.ldg, ptr(self.X),
+                  self.ld_in[0], E, self.d, di, ptr(seg_pad), ptr(self.bits), R, ptr(gw0), ptr(gb0), s)
+        elif L == 2:
             gw0, gb0 = self.g_layers[0]
             tcall("fc1_wgrad", "smes_gemm_ragged_k", ptr(self.dH), di, ptr(self.X), self.ld_in[0], R, E, di, self.d, ptr(seg_pad),
                  ptr(gw0), ptr(gb0), s)

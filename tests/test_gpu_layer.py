@@ -27,9 +27,11 @@ CASES = {
     "c2_t5_csum_gemm": (6, 1536, 5, 32, 256, 256, 4, 2, 512, 1e-3, False, dict(rand_lam=True)),
     "c2_unfused_mlp": (2, 2048, 8, 32, 256, 256, 4, 2, 512, 1e-3, False, {}),
     "c1_d64_dff384": (8, 777, 4, 16, 64, 128, 2, 1, 384, 1.0, False, dict(rand_task_w=True)),
+    "c2_fused_wgrad": (10, 2048, 8, 32, 256, 256, 4, 2, 512, 1e-3, False, {}),
 }
 # engine options per case (csum_from_gemm: per-expert sums of C from the folded wgrad's ones column)
-ENGINE_OPTS = {"c2_t5_csum_gemm": dict(csum_from_gemm=True), "c2_unfused_mlp": dict(fuse_mlp=False)}
+ENGINE_OPTS = {"c2_t5_csum_gemm": dict(csum_from_gemm=True), "c2_unfused_mlp": dict(fuse_mlp=False),
+               "c2_fused_wgrad": dict(fuse_wgrad=True)}
 
 
 def run_case(name, fold=True):

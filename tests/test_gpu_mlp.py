@@ -92,3 +92,34 @@ def test_mlp_dgrad(E, d, d_ff, T, loads):
         assert (dX[lo:hi].float() - dx).abs().max().item() <= 1e-2 * dx.abs().max().item() + 1e-8
         if n < hi - lo:
             assert torch.all(dX[lo + n:hi] == 0)       # pad rows (C = 0)
+
+
+@pytest.mark.parametrize("E,d,d_ff,T,loads", [c for c in CASES if c[1] <= 256])
+def test_mlp_wgrad(E, d, d_ff, T, loads):
+    """fc1 weight gradient with dH recomputed per row block: dW1 = dH^T X, db1 = colsum(dH),
+    dH = (C G_e) * mask; empty experts get exact zeros."""
+    dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, 5 * E + d + d_ff)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    ldc = 16
+    C = torch.zeros(R, ldc, device=dev, dtype=torch.bfloat16)
+    for e, n in enumerate(loads):
+        C[seg[e]:seg[e] + n, :T] = (torch.randn(n, T, generator=g, device=dev) * 1e-2).to(torch.bfloat16)
+    bits = torch.randint(-2 ** 31, 2 ** 31 - 1, (d_ff // 32, R), generator=g, device=dev,
+                         dtype=torch.int64).to(torch.int32)
+    dW = torch.full((E, d_ff, d), float("nan"), device=dev)
+    db = torch.full((E, d_ff), float("nan"), device=dev)
+    call("smes_mlp_wgrad", ptr(C), ldc, R, ptr(G), ldg, ptr(X), ldx, E, d, d_ff, ptr(seg_t), ptr(bits), R, ptr(dW),
+         ptr(db), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e, n in enumerate(loads):
+        lo, hi = seg[e], seg[e + 1]
+        if hi == lo:
+            assert torch.all(dW[e] == 0) and torch.all(db[e] == 0)
+            continue
+        word = bits[:, lo:hi].T.long()
+        m = torch.cat([((word[:, j:j + 1] >> torch.arange(32, device=dev)) & 1) for j in range(d_ff // 32)], 1).bool()
+        dh = ((C[lo:hi, :T].float() @ G[e, :T].float()) * m).to(torch.bfloat16).float()
+        ref_w = dh.T @ X[lo:hi, :d].float()
+        ref_b = dh.sum(0)
+        assert (dW[e] - ref_w).abs().max().item() <= 2e-3 * ref_w.abs().max().item()
+        assert (db[e] - ref_b).abs().max().item() <= 2e-3 * ref_b.abs().max().item()
