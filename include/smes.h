@@ -144,6 +144,11 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
 int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
                  const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* relu_bits,
                  long bits_ld, void* H, long ldh, float* P, long ldp, void* stream);
+/* smes_mlp_fwd2: the same forward on 2-CTA clusters (cta_group::2, M = 256 per MMA over two
+ * consecutive tiles of one expert; each CTA loads half of every W1 / G k-block). */
+int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
+                  const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* relu_bits,
+                  long bits_ld, void* H, long ldh, float* P, long ldp, void* stream);
 int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
                    int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, void* dX, long lddx,
                    void* dH, long lddh, void* stream);

@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ================= TMA producer
-      int xi = 0, wi = 0, gi = 0;
+      // ================= TMA producer: X tiles and W1 k-blocks (G: warp 2)
+      int xi = 0, wi = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int r0 = tile * BM;
         const int e = find_group(seg_s, a.E, r0);
@@ -163,20 +163,27 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(sX + s * 16384, &tmX, &xfull[s], kb * 64, r0);          // box {64 k, 128 rows}
         }
         for (int c = 0; c < NC; ++c) {
-          {
-            const int s = slot_of(gi, S::kGS);
-            mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
-            mbar_expect_tx(&gfull[s], 4096);
-            tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);          // box {64 f, 16 t, 1}
-            tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
-            ++gi;
-          }
           for (int kb = 0; kb < DK; ++kb, ++wi) {
             const int s = slot_of(wi, S::kWS);
             mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
             mbar_expect_tx(&wfull[s], 16384);
             tma_load_3d(sW + s * 16384, &tmW1, &wfull[s], kb * 64, c * CH, e);  // box {64 k, 128 n, 1}
           }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ================= G producer: released by the P-MMA, kept off the W1 stream
+      int gi = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int e = find_group(seg_s, a.E, tile * BM);
+        for (int c = 0; c < NC; ++c, ++gi) {
+          const int s = slot_of(gi, S::kGS);
+          mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+          mbar_expect_tx(&gfull[s], 4096);
+          tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);          // box {64 f, 16 t, 1}
+          tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
         }
       }
     }
@@ -199,12 +206,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&wfull[ws], par_of(wi, S::kWS));
             tc_fence_after();
             const uint32_t x_addr = smem_u32(sX + xs * 16384), w_addr = smem_u32(sW + ws * 16384);
-#ifndef SMES_EXP_NO_S
 #pragma unroll
             for (int k = 0; k < 4; ++k)
               tc_mma_f16(tS, umma_desc_sw128(x_addr + k * 32, 16, 1024), umma_desc_sw128(w_addr + k * 32, 16, 1024),
                          idS, (kb | k) != 0);
-#endif
             tc_commit(&wempty[ws]);
             if (c == NC - 1) tc_commit(&xempty[xs]);     // X k-block no longer needed by this tile
           }
@@ -228,14 +233,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c == 0) mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1));
           tc_fence_after();
           const uint32_t h_addr = smem_u32(sH), g_addr = smem_u32(sG + gs * 4096);
-#ifndef SMES_EXP_NO_P
 #pragma unroll
           for (int k = 0; k < CH / 16; ++k) {
             const int atom = k >> 2, kk = k & 3;
             tc_mma_f16(tP, umma_desc_sw128(h_addr + atom * 16384 + kk * 32, 16, 1024),
                        umma_desc_sw128(g_addr + atom * 2048 + kk * 32, 16, 1024), idP, (c | k) != 0);
           }
-#endif
           tc_commit(hempty);
           tc_commit(&gempty[gs]);
         }
@@ -272,7 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);       // accumulator drained into registers
-#ifndef SMES_EXP_NO_EPI
         sbias[lane] = bv0;
         sbias[32 + lane] = bv1;
         __syncwarp();
@@ -291,10 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
           a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
         }
-#endif
         // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
         mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
-#ifndef SMES_EXP_NO_EPI
         if (lane == 0) bulk_wait_read<0>();
         __syncwarp();
         uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
@@ -306,16 +306,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_proxy_async_smem();
         __syncwarp();
-#endif
         if (lane == 0) {
-#ifndef SMES_EXP_NO_EPI
           if (a.store_h) {
             tma_store_2d(&tmH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
             bulk_commit();
           }
           mbar_arrive(hfull);
         }
-#endif
         ++hi;
       }
       // head projections of this tile: P[row, t] = acc + c[e, t]
@@ -350,6 +347,337 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   if (warp == 2) tmem_dealloc(tmem_base, 512);
+}
+
+
+// ============================================================================ forward, CTA pairs
+// mlp_fwd2: the same chained forward on a 2-CTA cluster.  The pair runs two consecutive 128-row
+// tiles of one expert as one M = 256 tcgen05 MMA (cta_group::2): each CTA holds its own X tile and
+// HALF of every W1 / G k-block (N split), so the per-SM W1 traffic -- the L2 stream that bounds
+// the single-CTA kernel -- halves.  The leader CTA (rank 0) issues every MMA; transaction bytes of
+// both CTAs land on the leader's barriers; MMA completions are multicast to both CTAs; epilogue
+// handshakes arrive on the leader's barriers.  Work units are tile pairs inside an expert segment
+// (an odd tail tile runs with an idle peer row block whose outputs are not stored).
+template <int DK>
+struct Fwd2Smem {
+  static constexpr int kXS = DK <= 2 ? DK + 2 : DK <= 4 ? DK + 1 : DK;   // X ring (16 KB slots)
+  static constexpr int kWS = DK <= 4 ? 8 : 2;          // W1 half k-blocks (8 KB: 64 n x 64 k)
+  static constexpr int kGS = 2;                        // G halves (2 KB: 2 x {64 f, 8 t})
+  static constexpr int kOffX = 0;
+  static constexpr int kOffW = kOffX + kXS * 16384;
+  static constexpr int kOffG = kOffW + kWS * 8192;
+  static constexpr int kOffH = kOffG + kGS * 2048;
+  static constexpr int kOffBias = kOffH + 2 * 32768;   // H double-buffered
+  static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
+  static constexpr int kOffSeg = kOffBar + 512;
+  static constexpr int kBytes = kOffSeg + 2 * 257 * 4 + 1024;
+  static_assert(kBytes <= 232448, "mlp_fwd2 smem");
+};
+
+template <int DK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    mlp_fwd2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
+                    const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmH,
+                    const FwdArgs a) {
+  using S = Fwd2Smem<DK>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sX = smem + S::kOffX;
+  uint8_t* sW = smem + S::kOffW;
+  uint8_t* sG = smem + S::kOffG;
+  uint8_t* sH = smem + S::kOffH;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* xfull = bar;
+  uint64_t* xempty = xfull + S::kXS;
+  uint64_t* wfull = xempty + S::kXS;
+  uint64_t* wempty = wfull + S::kWS;
+  uint64_t* gfull = wempty + S::kWS;
+  uint64_t* gempty = gfull + S::kGS;
+  uint64_t* sfull = gempty + S::kGS;        // [2]
+  uint64_t* sempty = sfull + 2;             // [2]  (leader: 16 epilogue warps of the pair)
+  uint64_t* hfull = sempty + 2;             // [2]  (leader: 16)
+  uint64_t* hempty = hfull + 2;             // [2]
+  uint64_t* pfull = hempty + 2;             // [2]
+  uint64_t* pempty = pfull + 2;             // [2]  (leader: 8)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+  int* upref = seg_s + 257;                 // tile-pair units per expert, prefix
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int NC = a.d_ff / CH;
+  for (int i = threadIdx.x; i <= a.E; i += blockDim.x) seg_s[i] = a.seg[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int u = 0;
+    for (int e = 0; e < a.E; ++e) {
+      upref[e] = u;
+      u += ((seg_s[e + 1] - seg_s[e]) / BM + 1) / 2;
+    }
+    upref[a.E] = u;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmX); tma_prefetch(&tmW1); tma_prefetch(&tmG); tma_prefetch(&tmH);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S::kXS; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 1); }
+    for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 2 * kEpiWarps);
+      mbar_init(&pfull[i], 1); mbar_init(&pempty[i], kEpiWarps);
+    }
+    for (int i = 0; i < 2; ++i) { mbar_init(&hfull[i], 2 * kEpiWarps); mbar_init(&hempty[i], 1); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_units = upref[a.E];
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  // decode a unit: expert, first tile row, tiles in the pair (1 or 2)
+  auto decode = [&](int u, int& e, int& row_pair, int& nt) {
+    int lo = 0, hi = a.E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (upref[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    const int j = u - upref[e];
+    row_pair = seg_s[e] + 2 * j * BM;
+    const int tiles = (seg_s[e + 1] - seg_s[e]) / BM;
+    nt = min(2, tiles - 2 * j);
+  };
+  constexpr uint16_t kPair = 0x3;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer (both CTAs): own X tile, own half of W1 (G: warp 2)
+      int xi = 0, wi = 0;
+      for (int u = cl; u < num_units; u += ncl) {
+        int e, rp, nt;
+        decode(u, e, rp, nt);
+        const bool valid = (int)rank < nt;
+        const int r0 = rp + (int)rank * BM;
+        for (int kb = 0; kb < DK; ++kb, ++xi) {
+          const int s = slot_of(xi, S::kXS);
+          mbar_wait(&xempty[s], par_of(xi, S::kXS) ^ 1);
+          if (rank == 0) mbar_expect_tx(&xfull[s], nt * 16384);
+          if (valid) tma_load_2d_2sm(sX + s * 16384, &tmX, &xfull[s], kb * 64, r0);
+        }
+        for (int c = 0; c < NC; ++c) {
+          for (int kb = 0; kb < DK; ++kb, ++wi) {
+            const int s = slot_of(wi, S::kWS);
+            mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
+            if (rank == 0) mbar_expect_tx(&wfull[s], 2 * 8192);
+            tma_load_3d_2sm(sW + s * 8192, &tmW1, &wfull[s], kb * 64, c * CH + 64 * rank, e);
+          }
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ================= G producer (both CTAs): own 8 task rows of G[c]; released by the P-MMA, so it
+      // runs on its own warp and never holds back the W1 stream of the S-MMA
+      int gi = 0;
+      for (int u = cl; u < num_units; u += ncl) {
+        int e, rp, nt;
+        decode(u, e, rp, nt);
+        for (int c = 0; c < NC; ++c, ++gi) {
+          const int s = slot_of(gi, S::kGS);
+          mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+          if (rank == 0) mbar_expect_tx(&gfull[s], 2 * 2048);
+          tma_load_3d_2sm(sG + s * 2048, &tmG, &gfull[s], c * CH, 8 * rank, e);
+          tma_load_3d_2sm(sG + s * 2048 + 1024, &tmG, &gfull[s], c * CH + 64, 8 * rank, e);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ================= S-MMA issuer (leader): S_c = X W1[c]^T over the pair, M = 256
+      constexpr uint32_t idS = umma_idesc_bf16(2 * BM, CH, 0, 0);
+      int xi = 0, wi = 0, si = 0;
+      for (int u = cl; u < num_units; u += ncl) {
+        const int xbase = xi;
+        for (int c = 0; c < NC; ++c, ++si) {
+          const int sb = si & 1;
+          mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t tS = tmem_base + sb * CH;
+          for (int kb = 0; kb < DK; ++kb, ++wi) {
+            const int xs = slot_of(xbase + kb, S::kXS);
+            if (c == 0) mbar_wait(&xfull[xs], par_of(xbase + kb, S::kXS));
+            const int ws = slot_of(wi, S::kWS);
+            mbar_wait(&wfull[ws], par_of(wi, S::kWS));
+            tc_fence_after();
+            const uint32_t x_addr = smem_u32(sX + xs * 16384), w_addr = smem_u32(sW + ws * 8192);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16_2sm(tS, umma_desc_sw128(x_addr + k * 32, 16, 1024),
+                             umma_desc_sw128(w_addr + k * 32, 16, 1024), idS, (kb | k) != 0);
+            tc_commit_2sm_mc(&wempty[ws], kPair);
+            if (c == NC - 1) tc_commit_2sm_mc(&xempty[xs], kPair);
+          }
+          tc_commit_2sm_mc(&sfull[sb], kPair);
+        }
+        xi = xbase + DK;
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0 && rank == 0) {
+      // ================= P-MMA issuer (leader): P += H_c G[c]^T over the pair, N = 16
+      constexpr uint32_t idP = umma_idesc_bf16(2 * BM, 16, 0, 0);
+      int gi = 0, hi = 0, it = 0;
+      for (int u = cl; u < num_units; u += ncl, ++it) {
+        const int pb = it & 1;
+        const uint32_t tP = tmem_base + 256 + pb * 16;
+        for (int c = 0; c < NC; ++c, ++gi, ++hi) {
+          const int hb = hi & 1;
+          mbar_wait(&hfull[hb], (uint32_t)((hi >> 1) & 1));
+          const int gs = slot_of(gi, S::kGS);
+          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
+          if (c == 0) mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t h_addr = smem_u32(sH + hb * 32768), g_addr = smem_u32(sG + gs * 2048);
+#pragma unroll
+          for (int k = 0; k < CH / 16; ++k) {
+            const int atom = k >> 2, kk = k & 3;
+            tc_mma_f16_2sm(tP, umma_desc_sw128(h_addr + atom * 16384 + kk * 32, 16, 1024),
+                           umma_desc_sw128(g_addr + atom * 1024 + kk * 32, 16, 1024), idP, (c | k) != 0);
+          }
+          tc_commit_2sm_mc(&hempty[hb], kPair);
+          tc_commit_2sm_mc(&gempty[gs], kPair);
+        }
+        tc_commit_2sm_mc(&pfull[pb], kPair);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs): own 128 rows; handshakes on the leader's barriers.
+    // H is double-buffered and a unit's P is read after the NEXT unit's first chunk, so neither the
+    // P-MMA nor the head projections sit between two S chunks on the critical path.
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;
+    float* sbias = reinterpret_cast<float*>(smem + S::kOffBias) + (warp - 4) * 64;
+    const uint32_t lead_sempty0 = mapa_shared(smem_u32(&sempty[0]), 0);
+    const uint32_t lead_sempty1 = mapa_shared(smem_u32(&sempty[1]), 0);
+    const uint32_t lead_hfull0 = mapa_shared(smem_u32(&hfull[0]), 0);
+    const uint32_t lead_hfull1 = mapa_shared(smem_u32(&hfull[1]), 0);
+    const uint32_t lead_pempty0 = mapa_shared(smem_u32(&pempty[0]), 0);
+    const uint32_t lead_pempty1 = mapa_shared(smem_u32(&pempty[1]), 0);
+    int si = 0, hi = 0, it = 0;
+    // the unit whose P is pending: expert, row, validity
+    int p_e = -1, p_row = 0, p_it = 0;
+    bool p_valid = false;
+    auto store_p = [&]() {
+      const int pb = p_it & 1;
+      mbar_wait(&pfull[pb], (uint32_t)((p_it >> 1) & 1));
+      tc_fence_after();
+      if (par == 0) {
+        uint32_t t0[16];
+        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + 256 + pb * 16, t0);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(pb ? lead_pempty1 : lead_pempty0);
+        if (p_valid) {
+          float* prow = a.P + (size_t)p_row * a.ldp;
+          const float* ce = a.c + (size_t)p_e * a.ldg;
+#pragma unroll
+          for (int t = 0; t < 16; t += 4) {
+            if (t < a.ldp) {
+              float4 v;
+              v.x = __uint_as_float(t0[t + 0]) + ce[t + 0];
+              v.y = __uint_as_float(t0[t + 1]) + ce[t + 1];
+              v.z = __uint_as_float(t0[t + 2]) + ce[t + 2];
+              v.w = __uint_as_float(t0[t + 3]) + ce[t + 3];
+              *reinterpret_cast<float4*>(prow + t) = v;
+            }
+          }
+        }
+      }
+      p_e = -1;
+    };
+    for (int u = cl; u < num_units; u += ncl, ++it) {
+      int e, rp, nt;
+      decode(u, e, rp, nt);
+      const bool valid = (int)rank < nt;
+      const int r0 = rp + (int)rank * BM;
+      const int row = r0 + 32 * q + lane;
+      for (int c = 0; c < NC; ++c, ++si) {
+        const int n0 = c * CH + par * 64;
+        const float bv0 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + lane);
+        const float bv1 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + 32 + lane);
+        const int sb = si & 1;
+        mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        tc_fence_after();
+        float f[64];
+        {
+          uint32_t t0[32], t1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + sb * CH + par * 64;
+          tmem_ld32(ta, t0);
+          tmem_ld32(ta + 32, t1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = __uint_as_float(t1[j]); }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(sb ? lead_sempty1 : lead_sempty0);
+        sbias[lane] = bv0;
+        sbias[32 + lane] = bv1;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 64; j += 4) {
+          const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
+          f[j] = fmaxf(f[j] + bb.x, 0.f);
+          f[j + 1] = fmaxf(f[j + 1] + bb.y, 0.f);
+          f[j + 2] = fmaxf(f[j + 2] + bb.z, 0.f);
+          f[j + 3] = fmaxf(f[j + 3] + bb.w, 0.f);
+        }
+        if (valid) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
+            a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
+          }
+        }
+        const int hb = hi & 1;
+        mbar_wait(&hempty[hb], (uint32_t)(((hi >> 1) & 1) ^ 1));
+        if (lane == 0) bulk_wait_read<1>();     // this buffer's store (two chunks ago) has been read
+        __syncwarp();
+        uint8_t* hbuf = sH + hb * 32768 + par * 16384;
+        uint8_t* hrow = hbuf + (32 * q + lane) * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
+                                      pack_bf16(f[8 * cc + 4], f[8 * cc + 5]), pack_bf16(f[8 * cc + 6], f[8 * cc + 7]));
+          *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.store_h && valid) tma_store_2d(&tmH, hbuf + 32 * q * 128, n0, r0 + 32 * q);
+          bulk_commit();                          // one group per chunk (possibly empty) keeps wait_read<1> exact
+          mbar_arrive_cluster(hb ? lead_hfull1 : lead_hfull0);
+        }
+        ++hi;
+        if (c == 0 && p_e >= 0) store_p();      // previous unit's head projections
+      }
+      p_e = e; p_row = row; p_valid = valid; p_it = it;
+    }
+    if (p_e >= 0) store_p();
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, 512);
 }
 
 // ============================================================================ dgrad
@@ -945,6 +1273,67 @@ int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const f
 #undef SMES_FWD_CASE
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
+                 const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* bits, long bits_ld,
+                 void* H, long ldh, float* P, long ldp, void* stream) {
+  if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_fwd2: expert count %d outside [1, 256]", E);
+  if (d % 64 || d < 64 || d > 512) return set_error(SMES_ERR_SHAPE, "mlp_fwd2: d=%d must be a multiple of 64 in [64, 512]", d);
+  if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_fwd2: d_ff=%d must be a multiple of 128", d_ff);
+  if (ldg < 1 || ldg > 16 || ldp > 16 || ldp % 4 || ldp > ldg)
+    return set_error(SMES_ERR_SHAPE, "mlp_fwd2: ldg=%d ldp=%ld (need ldp <= ldg <= 16, ldp %% 4 == 0)", ldg, ldp);
+  if ((ldx * 2) % 16 || (ldh * 2) % 16) return set_error(SMES_ERR_SHAPE, "mlp_fwd2: row strides must be 16-byte aligned");
+  CUtensorMap tx, tw, tg, th;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldx * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = bf16_map(&tx, 2, X, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d, (uint64_t)d_ff, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d * 2, (uint64_t)d_ff * d * 2};
+    uint32_t box[3] = {64, 64, 1};                     // each CTA of the pair loads half of a W1 k-block
+    if ((rc = bf16_map(&tw, 3, W1, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d_ff, (uint64_t)ldg, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d_ff * 2, (uint64_t)ldg * d_ff * 2};
+    uint32_t box[3] = {64, 8, 1};                      // 8 task rows per CTA (N = 16 over the pair)
+    if ((rc = bf16_map(&tg, 3, G, dims, str, box))) return rc;
+  }
+  {
+    const void* hp = H != nullptr ? H : X;     // map unused when H is not stored
+    uint64_t dims[2] = {(uint64_t)d_ff, (uint64_t)rows_cap}, str[1] = {(uint64_t)(H != nullptr ? ldh : ldx) * 2};
+    uint32_t box[2] = {64, 32};
+    if (H == nullptr) dims[0] = (uint64_t)d;
+    if ((rc = bf16_map(&th, 2, hp, dims, str, box))) return rc;
+  }
+  mlp::FwdArgs args{seg, E, d, d_ff, (int)ldp, b1, c, ldg, bits, (int)bits_ld, P, H != nullptr ? 1 : 0};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+#define SMES_FWD_CASE(DK)                                                                              \
+  case DK: {                                                                                           \
+    auto k = mlp::mlp_fwd2_kernel<DK>;                                                                  \
+    const int sm = mlp::Fwd2Smem<DK>::kBytes;                                                           \
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd2 smem attribute: %s", cudaGetErrorString(e)); \
+    k<<<sm_count() & ~1, mlp::kThreads, sm, st>>>(tx, tw, tg, th, args);                                    \
+    break;                                                                                             \
+  }
+  switch (d / 64) {
+    SMES_FWD_CASE(1)
+    SMES_FWD_CASE(2)
+    SMES_FWD_CASE(4)
+    SMES_FWD_CASE(8)
+    default:
+      return set_error(SMES_ERR_SHAPE, "mlp_fwd2: d=%d not instantiated (64, 128, 256, 512)", d);
+  }
+#undef SMES_FWD_CASE
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd2 launch: %s", cudaGetErrorString(e));
   return SMES_OK;
 }
 

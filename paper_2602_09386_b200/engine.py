@@ -548,7 +548,8 @@ class SMESEngine:
                 # fused MLP: fc1 (+ relu mask, H kept) and P in one pass; dgrad dH (kept) + dX in one pass
                 w["mlp_fwd"] = (2.0 * n_act * (d * dff + dff * T),
                                 n_act * (d * 2 + dff * 2 + dff / 8 + self.ldp * 4))
-                w["mlp_dgrad"] = (2.0 * n_act * (T * dff + dff * d), n_act * (self.ldc * 2 + dff / 8 + d * 2))
+                w["mlp_dgrad"] = (2.0 * n_act * (T * dff + dff * d),
+                                  n_act * (self.ldc * 2 + dff / 8 + d * 2 + (0 if self.fuse_wgrad else dff * 2)))
                 w["mlp_wgrad"] = (2.0 * n_act * (T * dff + dff * d), n_act * (self.ldc * 2 + dff / 8 + d * 2))
         return {k: (f, b, "tensor" if b > 0 and f / b > balance else ("tensor" if b == 0 else "hbm"))
                 for k, (f, b) in w.items()}

@@ -35,8 +35,9 @@ CASES = [(8, 256, 512, 8, [300, 0, 129, 1, 128, 517, 0, 1000]),
          (2, 512, 256, 8, [200, 300])]
 
 
+@pytest.mark.parametrize("entry", ["smes_mlp_fwd", "smes_mlp_fwd2"])
 @pytest.mark.parametrize("E,d,d_ff,T,loads", CASES)
-def test_mlp_fwd(E, d, d_ff, T, loads):
+def test_mlp_fwd(E, d, d_ff, T, loads, entry):
     dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, E + d + d_ff)
     seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
     ldh = d_ff + 64
@@ -44,7 +45,7 @@ def test_mlp_fwd(E, d, d_ff, T, loads):
     bits = torch.zeros(d_ff // 32, R, dtype=torch.int32, device=dev)
     ldp = ldg
     P = torch.full((R, ldp), float("nan"), device=dev)
-    call("smes_mlp_fwd", ptr(X), ldx, R, ptr(W1), ptr(b1), ptr(G), ptr(c), ldg, E, d, d_ff, ptr(seg_t), ptr(bits), R,
+    call(entry, ptr(X), ldx, R, ptr(W1), ptr(b1), ptr(G), ptr(c), ldg, E, d, d_ff, ptr(seg_t), ptr(bits), R,
          ptr(H), ldh, ptr(P), ldp, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert torch.all(H[:, d_ff:] == 3.0)          # columns beyond d_ff untouched

@@ -41,6 +41,10 @@ def run(lib_path):
         call("smes_mlp_fwd", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), ptr(bits),
              R, ptr(H), dff + 64, ptr(P), 8, st)
 
+    def fwd2():
+        call("smes_mlp_fwd2", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), ptr(bits),
+             R, ptr(H), dff + 64, ptr(P), 8, st)
+
     def fwd_noh():
         call("smes_mlp_fwd", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), ptr(bits),
              R, None, 0, ptr(P), 8, st)
@@ -60,7 +64,7 @@ def run(lib_path):
              ptr(P), 8, 1, R, st)
 
     out = {}
-    for name, fn in [("mlp_fwd", fwd), ("mlp_fwd_noH", fwd_noh), ("mlp_dgrad", dgrad), ("mlp_dgrad_nodH", dgrad_nodh),
+    for name, fn in [("mlp_fwd", fwd), ("mlp_fwd2", fwd2), ("mlp_fwd_noH", fwd_noh), ("mlp_dgrad", dgrad), ("mlp_dgrad_nodH", dgrad_nodh),
                      ("unfused_fwd", unfused_fwd)]:
         for _ in range(3):
             fn()
