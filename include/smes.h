@@ -152,6 +152,11 @@ int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const 
 int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
                    int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, void* dX, long lddx,
                    void* dH, long lddh, void* stream);
+/* smes_mlp_dgrad2: the same dgrad on 2-CTA clusters (each CTA loads half of every W1 / G k-block);
+ * d in {128, 256}. */
+int smes_mlp_dgrad2(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
+                    int d_ff, const int* seg, const uint32_t* relu_bits, long bits_ld, void* dX, long lddx,
+                    void* dH, long lddh, void* stream);
 /* fc1 weight gradient with dH recomputed per 128-row block (dH never stored): one CTA per
  * (expert, 128-wide d_ff chunk); dW (E, d_ff, d) fp32, db (E, d_ff) fp32; d <= 256. */
 int smes_mlp_wgrad(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* X, long ldx, int E,

@@ -927,6 +927,291 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, 512);
 }
 
+// ============================================================================ dgrad, CTA pairs
+// mlp_dgrad2: the dgrad on 2-CTA clusters.  Each CTA of the pair loads half of every W1 k-block
+// (N = d split) and half of every G chunk (N = 128 f split); the leader issues M = 256 MMAs.
+// The single-CTA kernel streams 256 KB of W1 per 128-row tile from L2 and is bound by that stream
+// (ncu: producer waiting on W slots, epilogue waiting on S behind the starved dX MMAs).
+template <int DK>
+struct Dg2Smem {
+  static constexpr int kCS = 2;
+  static constexpr int kGS = 2;                         // G halves: {64 f, 16 t} = 2 KB
+  static constexpr int kWB = DK / 2 * 8192;             // W1 half k-block: DK/2 boxes {64 j, 64 f}
+  static constexpr int kWS = DK <= 2 ? 8 : 6;
+  static constexpr int kOffC = 0;
+  static constexpr int kOffG = kOffC + kCS * 16384;
+  static constexpr int kOffW = kOffG + kGS * 2048;
+  static constexpr int kOffH = kOffW + kWS * kWB;
+  static constexpr int kOffStg = kOffH + 32768;
+  static constexpr int kOffBar = kOffStg + kEpiWarps * 4096;
+  static constexpr int kOffSeg = kOffBar + 512;
+  static constexpr int kBytes = kOffSeg + 2 * 257 * 4 + 1024;
+  static_assert(kBytes <= 232448, "mlp_dgrad2 smem");
+};
+
+template <int DK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    mlp_dgrad2_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmG,
+                      const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmDX,
+                      const __grid_constant__ CUtensorMap tmDH, const DgradArgs a) {
+  using S = Dg2Smem<DK>;
+  constexpr int D = DK * 64;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sC = smem + S::kOffC;
+  uint8_t* sG = smem + S::kOffG;
+  uint8_t* sW = smem + S::kOffW;
+  uint8_t* sH = smem + S::kOffH;
+  uint8_t* sStg = smem + S::kOffStg;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* cfull = bar;
+  uint64_t* cempty = cfull + S::kCS;
+  uint64_t* gfull = cempty + S::kCS;
+  uint64_t* gempty = gfull + S::kGS;
+  uint64_t* wfull = gempty + S::kGS;
+  uint64_t* wempty = wfull + S::kWS;
+  uint64_t* sfull = wempty + S::kWS;       // [2]
+  uint64_t* sempty = sfull + 2;            // [2] (leader: 16)
+  uint64_t* hfull = sempty + 2;            // [1] (leader: 16)
+  uint64_t* hempty = hfull + 1;
+  uint64_t* dfull = hempty + 1;
+  uint64_t* dempty = dfull + 1;            // (leader: 16)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+  int* upref = seg_s + 257;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int NC = a.d_ff / CH;
+  for (int i = threadIdx.x; i <= a.E; i += blockDim.x) seg_s[i] = a.seg[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int u = 0;
+    for (int e = 0; e < a.E; ++e) {
+      upref[e] = u;
+      u += ((seg_s[e + 1] - seg_s[e]) / BM + 1) / 2;
+    }
+    upref[a.E] = u;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmC); tma_prefetch(&tmG); tma_prefetch(&tmW1); tma_prefetch(&tmDX); tma_prefetch(&tmDH);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int i = 0; i < S::kCS; ++i) { mbar_init(&cfull[i], 1); mbar_init(&cempty[i], 1); }
+    for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 2 * kEpiWarps); }
+    mbar_init(hfull, 2 * kEpiWarps);
+    mbar_init(hempty, 1);
+    mbar_init(dfull, 1);
+    mbar_init(dempty, 2 * kEpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int num_units = upref[a.E];
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  auto decode = [&](int u, int& e, int& row_pair, int& nt) {
+    int lo = 0, hi = a.E - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (upref[mid] <= u) lo = mid; else hi = mid - 1;
+    }
+    e = lo;
+    const int j = u - upref[e];
+    row_pair = seg_s[e] + 2 * j * BM;
+    const int tiles = (seg_s[e + 1] - seg_s[e]) / BM;
+    nt = min(2, tiles - 2 * j);
+  };
+  constexpr uint16_t kPair = 0x3;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int ci = 0, gi = 0, wi = 0;
+      for (int u = cl; u < num_units; u += ncl, ++ci) {
+        int e, rp, nt;
+        decode(u, e, rp, nt);
+        const bool valid = (int)rank < nt;
+        const int r0 = rp + (int)rank * BM;
+        {
+          const int s = slot_of(ci, S::kCS);
+          mbar_wait(&cempty[s], par_of(ci, S::kCS) ^ 1);
+          if (rank == 0) mbar_expect_tx(&cfull[s], nt * 16384);
+          if (valid) tma_load_2d_2sm(sC + s * 16384, &tmC, &cfull[s], 0, r0);
+        }
+        for (int c = 0; c < NC; ++c) {
+          {
+            const int s = slot_of(gi, S::kGS);
+            mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+            if (rank == 0) mbar_expect_tx(&gfull[s], 2 * 2048);
+            tma_load_3d_2sm(sG + s * 2048, &tmG, &gfull[s], c * CH + 64 * rank, 0, e);
+            ++gi;
+          }
+          for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
+            const int s = slot_of(wi, S::kWS);
+            mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
+            if (rank == 0) mbar_expect_tx(&wfull[s], 2 * S::kWB);
+#pragma unroll
+            for (int j = 0; j < DK / 2; ++j)
+              tma_load_3d_2sm(sW + s * S::kWB + j * 8192, &tmW1, &wfull[s], 64 * (j + rank * (DK / 2)),
+                              c * CH + kb * 64, e);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idS = umma_idesc_bf16(2 * BM, CH, 0, 1);
+      constexpr uint32_t idD = umma_idesc_bf16(2 * BM, D, 0, 1);
+      int ci = 0, gi = 0, wi = 0, si = 0, hi = 0, it = 0;
+      for (int u = cl; u < num_units; u += ncl, ++ci, ++it) {
+        const int cs = slot_of(ci, S::kCS);
+        mbar_wait(&cfull[cs], par_of(ci, S::kCS));
+        const uint32_t c_addr = smem_u32(sC + cs * 16384);
+        auto s_mma = [&](int c) {
+          const int sb = si & 1;
+          mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
+          const int gs = slot_of(gi, S::kGS);
+          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
+          tc_fence_after();
+          tc_mma_f16_2sm(tmem_base + sb * CH, umma_desc_sw128(c_addr, 16, 1024),
+                         umma_desc_sw128(smem_u32(sG + gs * 2048), 2048, 1024), idS, 0u);
+          tc_commit_2sm_mc(&sfull[sb], kPair);
+          tc_commit_2sm_mc(&gempty[gs], kPair);
+          ++gi; ++si;
+        };
+        s_mma(0);
+        for (int c = 0; c < NC; ++c) {
+          if (c + 1 < NC) s_mma(c + 1);
+          if (c == NC - 1) tc_commit_2sm_mc(&cempty[cs], kPair);
+          mbar_wait(hfull, (uint32_t)(hi & 1));
+          if (c == 0) mbar_wait(dempty, (uint32_t)((it & 1) ^ 1));
+          tc_fence_after();
+          const uint32_t h_addr = smem_u32(sH);
+          for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
+            const int ws = slot_of(wi, S::kWS);
+            mbar_wait(&wfull[ws], par_of(wi, S::kWS));
+            tc_fence_after();
+            const uint32_t w_addr = smem_u32(sW + ws * S::kWB);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16_2sm(tmem_base + 256, umma_desc_sw128(h_addr + kb * 16384 + k * 32, 16, 1024),
+                             umma_desc_sw128(w_addr + k * 2048, 8192, 1024), idD, (c | kb | k) != 0);
+            tc_commit_2sm_mc(&wempty[ws], kPair);
+          }
+          tc_commit_2sm_mc(hempty, kPair);
+          ++hi;
+        }
+        tc_commit_2sm_mc(dfull, kPair);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;
+    uint8_t* stg = sStg + (warp - 4) * 4096;
+    const uint32_t lead_sempty0 = mapa_shared(smem_u32(&sempty[0]), 0);
+    const uint32_t lead_sempty1 = mapa_shared(smem_u32(&sempty[1]), 0);
+    const uint32_t lead_hfull = mapa_shared(smem_u32(hfull), 0);
+    const uint32_t lead_dempty = mapa_shared(smem_u32(dempty), 0);
+    int si = 0, hi = 0, it = 0;
+    for (int u = cl; u < num_units; u += ncl, ++it) {
+      int e, rp, nt;
+      decode(u, e, rp, nt);
+      const bool valid = (int)rank < nt;
+      const int r0 = rp + (int)rank * BM;
+      const int row = r0 + 32 * q + lane;
+      for (int c = 0; c < NC; ++c, ++si) {
+        const int n0 = c * CH + par * 64;
+        const uint32_t m0 = valid ? __ldg(&a.bits[(size_t)(n0 >> 5) * a.bits_ld + row]) : 0u;
+        const uint32_t m1 = valid ? __ldg(&a.bits[(size_t)((n0 >> 5) + 1) * a.bits_ld + row]) : 0u;
+        const int sb = si & 1;
+        mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        tc_fence_after();
+        float f[64];
+        {
+          uint32_t t0[32], t1[32];
+          const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + sb * CH + par * 64;
+          tmem_ld32(ta, t0);
+          tmem_ld32(ta + 32, t1);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            f[j] = ((m0 >> j) & 1u) ? __uint_as_float(t0[j]) : 0.f;
+            f[32 + j] = ((m1 >> j) & 1u) ? __uint_as_float(t1[j]) : 0.f;
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(sb ? lead_sempty1 : lead_sempty0);
+        mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
+        if (a.store_dh && lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
+                                      pack_bf16(f[8 * cc + 4], f[8 * cc + 5]), pack_bf16(f[8 * cc + 6], f[8 * cc + 7]));
+          *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (a.store_dh && valid) {
+            tma_store_2d(&tmDH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
+            bulk_commit();
+          }
+          mbar_arrive_cluster(lead_hfull);
+        }
+        ++hi;
+      }
+      mbar_wait(dfull, (uint32_t)(it & 1));
+      tc_fence_after();
+      for (int cc = par; cc < DK; cc += 2) {
+        uint32_t t0[32], t1[32];
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;
+        tmem_ld32(ta, t0);
+        tmem_ld32(ta + 32, t1);
+        tmem_ld_wait();
+        if (cc + 2 >= DK) {   // last TMEM read of this tile: hand the accumulator back early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(lead_dempty);
+        }
+        if (!valid) continue;
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t* src = k < 4 ? t0 : t1;
+          const int o = (k & 3) * 8;
+          rowp[k ^ (lane & 7)] = make_uint4(
+              pack_bf16(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
+              pack_bf16(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
+              pack_bf16(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
+              pack_bf16(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmDX, stg, cc * 64, r0 + 32 * q);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, 512);
+}
+
 
 // ============================================================================ fc1 weight gradient
 // mlp_wgrad: one CTA per (expert e, 128-wide d_ff chunk c); the K loop runs over the expert's
@@ -1397,6 +1682,68 @@ int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ld
 #undef SMES_DG_CASE
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_mlp_dgrad2(const void* C, long ldc, long rows_cap, const void* G, int ldg, const void* W1, int E, int d,
+                   int d_ff, const int* seg, const uint32_t* bits, long bits_ld, void* dX, long lddx, void* dH,
+                   long lddh, void* stream) {
+  if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_dgrad2: expert count %d outside [1, 256]", E);
+  if (d % 64 || d < 64 || d > 256) return set_error(SMES_ERR_SHAPE, "mlp_dgrad2: d=%d must be a multiple of 64 in [64, 256]", d);
+  if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_dgrad2: d_ff=%d must be a multiple of 128", d_ff);
+  if (ldg < 1 || ldg > 16 || ldc < ldg || (ldc * 2) % 16 || (lddx * 2) % 16)
+    return set_error(SMES_ERR_SHAPE, "mlp_dgrad2: ldg=%d ldc=%ld lddx=%ld", ldg, ldc, lddx);
+  CUtensorMap tc, tg, tw, td, th;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)ldg, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldc * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = bf16_map(&tc, 2, C, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d_ff, (uint64_t)ldg, (uint64_t)E};
+    uint64_t str[2] = {(uint64_t)d_ff * 2, (uint64_t)ldg * d_ff * 2};
+    uint32_t box[3] = {64, 16, 1};                     // each CTA: one 64-wide f half of the chunk
+    if ((rc = bf16_map(&tg, 3, G, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[3] = {(uint64_t)d, (uint64_t)d_ff, (uint64_t)E};    // W1 (E, d_ff, d): element (j, f)
+    uint64_t str[2] = {(uint64_t)d * 2, (uint64_t)d_ff * d * 2};
+    uint32_t box[3] = {64, 64, 1};
+    if ((rc = bf16_map(&tw, 3, W1, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)rows_cap}, str[1] = {(uint64_t)lddx * 2};
+    uint32_t box[2] = {64, 32};
+    if ((rc = bf16_map(&td, 2, dX, dims, str, box))) return rc;
+  }
+  {
+    if (dH != nullptr && (lddh * 2) % 16) return set_error(SMES_ERR_SHAPE, "mlp_dgrad2: dH stride must be 16-byte aligned");
+    uint64_t dims[2] = {(uint64_t)(dH ? d_ff : d), (uint64_t)rows_cap}, str[1] = {(uint64_t)(dH ? lddh : lddx) * 2};
+    uint32_t box[2] = {64, 32};
+    if ((rc = bf16_map(&th, 2, dH ? dH : dX, dims, str, box))) return rc;
+  }
+  mlp::DgradArgs args{seg, E, d, d_ff, bits, (int)bits_ld, dH != nullptr ? 1 : 0};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  cudaError_t e;
+#define SMES_DG_CASE(DK)                                                                               \
+  case DK: {                                                                                           \
+    auto k = mlp::mlp_dgrad2_kernel<DK>;                                                                \
+    const int sm = mlp::Dg2Smem<DK>::kBytes;                                                            \
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad2 smem attribute: %s", cudaGetErrorString(e)); \
+    k<<<sm_count() & ~1, mlp::kThreads, sm, st>>>(tc, tg, tw, td, th, args);                                   \
+    break;                                                                                             \
+  }
+  switch (d / 64) {
+    SMES_DG_CASE(2)
+    SMES_DG_CASE(4)
+    default:
+      return set_error(SMES_ERR_SHAPE, "mlp_dgrad2: d=%d not instantiated (128, 256)", d);
+  }
+#undef SMES_DG_CASE
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad2 launch: %s", cudaGetErrorString(e));
   return SMES_OK;
 }
 

@@ -66,8 +66,11 @@ def test_mlp_fwd(E, d, d_ff, T, loads, entry):
         assert (got_p - p_ref).abs().max().item() <= 2e-3 * p_ref.abs().max().item() + 1e-4
 
 
+@pytest.mark.parametrize("entry", ["smes_mlp_dgrad", "smes_mlp_dgrad2"])
 @pytest.mark.parametrize("E,d,d_ff,T,loads", [c for c in CASES if c[1] <= 256])
-def test_mlp_dgrad(E, d, d_ff, T, loads):
+def test_mlp_dgrad(E, d, d_ff, T, loads, entry):
+    if entry == "smes_mlp_dgrad2" and d < 128:
+        pytest.skip("the 2-CTA dgrad splits d over the pair (d >= 128)")
     dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, 3 * E + d + d_ff)
     seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
     ldc = 16
@@ -78,7 +81,7 @@ def test_mlp_dgrad(E, d, d_ff, T, loads):
                          dtype=torch.int64).to(torch.int32)
     dX = torch.full((R, d), float("nan"), device=dev).to(torch.bfloat16)
     dH = torch.full((R, d_ff), float("nan"), device=dev).to(torch.bfloat16)
-    call("smes_mlp_dgrad", ptr(C), ldc, R, ptr(G), ldg, ptr(W1), E, d, d_ff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
+    call(entry, ptr(C), ldc, R, ptr(G), ldg, ptr(W1), E, d, d_ff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
          ptr(dH), d_ff, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     for e, n in enumerate(loads):

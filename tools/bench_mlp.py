@@ -53,6 +53,10 @@ def run(lib_path):
         call("smes_mlp_dgrad", ptr(C), 16, R, ptr(G), 8, ptr(W1), E, d, dff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
              ptr(dH), dff, st)
 
+    def dgrad2():
+        call("smes_mlp_dgrad2", ptr(C), 16, R, ptr(G), 8, ptr(W1), E, d, dff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
+             ptr(dH), dff, st)
+
     def dgrad_nodh():
         call("smes_mlp_dgrad", ptr(C), 16, R, ptr(G), 8, ptr(W1), E, d, dff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
              None, 0, st)
@@ -64,7 +68,7 @@ def run(lib_path):
              ptr(P), 8, 1, R, st)
 
     out = {}
-    for name, fn in [("mlp_fwd", fwd), ("mlp_fwd2", fwd2), ("mlp_fwd_noH", fwd_noh), ("mlp_dgrad", dgrad), ("mlp_dgrad_nodH", dgrad_nodh),
+    for name, fn in [("mlp_fwd", fwd), ("mlp_fwd2", fwd2), ("mlp_fwd_noH", fwd_noh), ("mlp_dgrad", dgrad), ("mlp_dgrad2", dgrad2), ("mlp_dgrad_nodH", dgrad_nodh),
                      ("unfused_fwd", unfused_fwd)]:
         for _ in range(3):
             fn()
