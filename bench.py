@@ -431,9 +431,9 @@ def run_ep(args, c, world, rank, local, dev):
 
 
 def run_infer(args, c, world, rank, local, dev):
-    """c4: fwd-only scoring through the reference-shaped forward (routers, routing, plan, experts,
-    combine, heads; task reps materialised), one CUDA graph per batch size, p50/p99 over
-    >= 1000 replays each.  Ranks > 0 idle (single-GPU configuration)."""
+    """c4: fwd-only scoring (routers, routing, plan, expert MLP with the folded heads, combine ->
+    predictions; `SMESEngine.score`), one CUDA graph per batch size, p50/p99 over >= 1000 replays
+    each.  Ranks > 0 idle (single-GPU configuration)."""
     import torch
     from paper_2602_09386_b200 import SMESEngine, _lib
     if rank != 0:
@@ -450,16 +450,16 @@ def run_infer(args, c, world, rank, local, dev):
         st = torch.cuda.Stream(dev)
         st.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(st):
-            eng.forward(with_loss=False)
+            eng.score()
         torch.cuda.current_stream(dev).wait_stream(st)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            eng.forward(with_loss=False)
+            eng.score()
         for _ in range(max(3, args.warmup)):
             g.replay()
         torch.cuda.synchronize()
         c0 = _lib.launch_count
-        eng.forward(with_loss=False)
+        eng.score()
         per = _lib.launch_count - c0
         ts = []
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
@@ -499,7 +499,7 @@ def run_infer(args, c, world, rank, local, dev):
                        "graph": "one CUDA graph per batch size"},
             "e2e": {"value": top["e2e_ms"], "unit": "ms", "h2d_bytes_per_step": h_host.numel() * 2,
                     "d2h_bytes_per_step": preds_host.numel() * 4,
-                    "api": "pinned H2D of h, graph replay of SMESEngine.forward, D2H of predictions"},
+                    "api": "pinned H2D of h, graph replay of SMESEngine.score, D2H of predictions"},
             "gpu_launches": launches, "sweep": sweep, "cpu_baseline": cpu}
 
 

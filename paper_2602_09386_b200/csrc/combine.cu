@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
   const int T = a.T, K = a.K, EW = (a.E + 31) >> 5, umax = a.umax;
   const int ldp = a.ldp;
   const bool has_p = a.P != nullptr;
+  const bool has_o = a.O != nullptr;           // scoring (no task reps): logits from P only
   extern __shared__ __align__(16) uint8_t smraw[];
   const GroupLayout L(umax, MAXT, ldp, umax, a.d_out);
   uint8_t* g0 = smraw + (size_t)gi * L.bytes;
@@ -190,10 +191,11 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
     __syncthreads();
     if (valid) {
       // gather every packed row of the instance (and its head projections) into smem at once
-      for (int i = gtid; i < U * cpr; i += gthreads) {
-        const int u = i / cpr, c = i - u * cpr;
-        cp_async16(s_o + (long)u * a.d_out + c * 8, a.O + (long)s_rows[u] * a.ldo + c * 8);
-      }
+      if (has_o)
+        for (int i = gtid; i < U * cpr; i += gthreads) {
+          const int u = i / cpr, c = i - u * cpr;
+          cp_async16(s_o + (long)u * a.d_out + c * 8, a.O + (long)s_rows[u] * a.ldo + c * 8);
+        }
       if (has_p)
         for (int i = gtid; i < U * pcr; i += gthreads) {
           const int u = i / pcr, c = i - u * pcr;
@@ -209,6 +211,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
     __syncthreads();
     if (valid) {
       // reps_t = sum_u w[u,t] O[u]   (every packed row read once)
+      if (has_o) {
       float acc[MAXT][VPL];
 #pragma unroll
       for (int t = 0; t < MAXT; ++t)
@@ -227,6 +230,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
 #pragma unroll
       for (int t = 0; t < MAXT; ++t)
         if (t < T) store_bf<VPL>(a.reps + ((long)t * a.B + b) * a.d_out + col, acc[t]);
+      }
       // logit_t = b_t + sum_u w[u,t] P[u,t]   (P = O head_W^T from the tensor-core GEMM)
       if (ws == 0 && has_p) {
         float sacc = 0.f;
@@ -689,7 +693,8 @@ int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint
   a.P = const_cast<float*>(P); a.ldp = (int)ldp;
   a.reps = reinterpret_cast<__nv_bfloat16*>(reps); a.logits = logits; a.preds = preds; a.labels = labels;
   a.lam = lam; a.loss_part = loss_part;
-  if (!reps) return set_error(SMES_ERR_STATE, "combine_fwd: reps buffer is required");
+  if (!reps && O) return set_error(SMES_ERR_STATE, "combine_fwd: reps buffer is required with O");
+  if (!O && !P) return set_error(SMES_ERR_STATE, "combine_fwd: scoring without O needs the head projections P");
   return combine_launch(false, a, grid, stream);
 }
 

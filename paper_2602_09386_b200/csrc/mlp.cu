@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t w = 0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
-          a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
+          if (a.bits != nullptr) a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
         }
         // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
         mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
@@ -643,7 +643,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t w = 0;
 #pragma unroll
             for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
-            a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
+            if (a.bits != nullptr) a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
           }
         }
         const int hb = hi & 1;

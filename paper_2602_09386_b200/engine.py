@@ -142,8 +142,13 @@ class SMESEngine:
         self._folded = False
         # fused expert MLP (csrc/mlp.cu) for folded training steps: relu fc1 + identity fc2
         lay = p.layers
-        self.fuse_mlp = bool(fuse_mlp and self.can_fold and len(lay) == 2 and lay[0].act == "relu"
-                             and d % 64 == 0 and d <= 256 and lay[0].d_out % 128 == 0 and T <= 16)
+        mlp_ok = bool(fuse_mlp and self.can_fold and len(lay) == 2 and lay[0].act == "relu"
+                      and d % 64 == 0 and lay[0].d_out % 128 == 0 and T <= 16)
+        # the fused kernels support d <= 512 (fwd) / 256 (dgrad); at d = 512 (c3) the fused forward
+        # measured slower than the tensor-bound fc1 GEMM + folded P GEMM, so both use d <= 256
+        self.fuse_mlp_fwd = mlp_ok and d <= 256
+        self.fuse_mlp = mlp_ok and d <= 256
+        self._fold_fresh = False            # G/c current for the loaded weights (inference scoring)
         # fc1 wgrad with dH recomputed per row block (csrc/mlp.cu mlp_wgrad) instead of storing dH:
         # measured slower at c2 (one CTA per (expert, d_ff chunk) re-streams X), so off by default
         self.fuse_wgrad = bool(fuse_wgrad and self.fuse_mlp)
@@ -263,6 +268,7 @@ class SMESEngine:
 
     def refresh_weights(self):
         """Copy fp32 master parameters into the bf16 / fp32 kernel operands."""
+        self._fold_fresh = False
         p, T, E, d = self.p, self.T, self.E, self.d
         dev = self.dev
         self.wr_bf = p.router_w.detach().reshape(T * E, d).to(dev, torch.bfloat16).contiguous()
@@ -300,7 +306,26 @@ class SMESEngine:
         self.forward_a()
         self.forward_b(with_loss=with_loss)
 
-    def forward_a(self, frozen: bool = False, fold: bool = False):
+    def score(self):
+        """Inference scoring (BASELINE c4: fwd only, no regularizer): predictions and logits.
+        With an identity last pool the heads are folded into it (P = H G_e^T + c_e), so neither the
+        hidden activations, the expert outputs O nor the task reps are written; otherwise this is
+        the reference-shaped forward.  G/c are folded once per ``refresh_weights``: a CUDA graph
+        captured from ``score`` must be re-captured after a weight refresh."""
+        if not self.can_fold:
+            self.forward(with_loss=False)
+            return
+        s = self._stream()
+        T, E, B = self.T, self.E, self.B
+        # the weights do not change between scoring calls: fold the heads once per weight refresh
+        self.forward_a(fold=True, store_hidden=False, refold=not self._fold_fresh)
+        self._fold_fresh = True
+        _tagged("combine_score", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask),
+                ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), None, self.d_out,
+                ptr(self.head_w), ptr(self.head_b), ptr(self.P), self.ldp, None, ptr(self.logits), ptr(self.preds),
+                None, ptr(self.lam), None, self.grid, s)
+
+    def forward_a(self, frozen: bool = False, fold: bool = False, store_hidden: bool = True, refold: bool = True):
         """Router GEMM -> routing -> plan -> expert GEMMs.  Ends with the per-expert
         LoadStats sums in ``stats_raw`` (the data-parallel exchange point).
         ``fold`` (training steps only, see csrc/fold.cu): the last identity pool is folded into
@@ -320,7 +345,7 @@ class SMESEngine:
              ptr(self.gather_exp), ptr(self.Cm), self.ldc, self.ldc, s)
         if fold and not self.can_fold:
             raise ConfigError("head folding needs an identity last expert pool and sparse LB statistics")
-        self.experts_forward(s, fold=fold)
+        self.experts_forward(s, fold=fold, store_hidden=store_hidden, refold=refold)
 
     def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
                   batch_scale: int | None = None, lb_batch: int | None = None):
@@ -358,11 +383,11 @@ class SMESEngine:
              ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), int(frozen), s)
 
-    def experts_forward(self, s, fold: bool = False):
+    def experts_forward(self, s, fold: bool = False, store_hidden: bool = True, refold: bool = True):
         R = self.rows_cap
         inp = self.X
         L = len(self.p.layers)
-        pre = [] if (fold and self.fuse_mlp) else (self.p.layers[:L - 1] if fold else self.p.layers)
+        pre = [] if (fold and self.fuse_mlp_fwd) else (self.p.layers[:L - 1] if fold else self.p.layers)
         for i, l in enumerate(pre):
             _tagged(f"fc{i + 1}_fwd", "smes_gemm_ragged_m", ptr(inp), self.ld_in[i], R, ptr(self.w_bf[i]), self.E,
                     self.dims[i + 1], self.dims[i], 0, ptr(self.seg_pad), ptr(self.b32[i]), ACT[l.act],
@@ -372,14 +397,16 @@ class SMESEngine:
         if fold:
             # P = H G_e^T + c_e with G_e = head_W W_last,e: the last pool and the heads in one N = T GEMM
             di = self.dims[L - 1]
-            _tagged("fold_heads", "smes_fold_heads", self.E, self.T, self.ldg, self.d_out, di, ptr(self.head_w),
-                    ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold), ptr(self.fold_work), s)
-            if self.fuse_mlp:
+            if refold:   # training steps refold every step (the weights move between steps)
+                _tagged("fold_heads", "smes_fold_heads", self.E, self.T, self.ldg, self.d_out, di,
+                        ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold),
+                        ptr(self.fold_work), s)
+            if self.fuse_mlp_fwd:
                 # fc1 (+ relu mask, H kept for the weight gradients) and P in one chained kernel
                 _tagged("mlp_fwd", "smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]),
                         ptr(self.b32[0]), ptr(self.G_fold), ptr(self.c_fold), self.ldg, self.E, self.d, di,
-                        ptr(self.seg_pad), ptr(self.bits[0]), R, ptr(self.outs[0]), self.ld_out[0], ptr(self.P),
-                        self.ldp, s)
+                        ptr(self.seg_pad), ptr(self.bits[0]) if store_hidden else None, R,
+                        ptr(self.outs[0]) if store_hidden else None, self.ld_out[0], ptr(self.P), self.ldp, s)
                 return
             _tagged(f"fc{L}_fwd_folded", "smes_gemm_ragged_m", ptr(inp), self.ld_in[L - 1], R, ptr(self.G_fold),
                     self.E, self.ldg, di, 0, ptr(self.seg_pad), ptr(self.c_fold), 0, None, None, 0, ptr(self.P),

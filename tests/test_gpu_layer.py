@@ -28,6 +28,7 @@ CASES = {
     "c2_unfused_mlp": (2, 2048, 8, 32, 256, 256, 4, 2, 512, 1e-3, False, {}),
     "c1_d64_dff384": (8, 777, 4, 16, 64, 128, 2, 1, 384, 1.0, False, dict(rand_task_w=True)),
     "c2_fused_wgrad": (10, 2048, 8, 32, 256, 256, 4, 2, 512, 1e-3, False, {}),
+    "c3_shape_d512": (11, 1024, 16, 64, 512, 512, 4, 2, 1024, 1e-3, False, {}),
 }
 # engine options per case (csum_from_gemm: per-expert sums of C from the folded wgrad's ones column)
 ENGINE_OPTS = {"c2_t5_csum_gemm": dict(csum_from_gemm=True), "c2_unfused_mlp": dict(fuse_mlp=False),
@@ -144,3 +145,22 @@ def test_graph_replay_is_deterministic():
     torch.cuda.synchronize()
     for a, b in zip(snap, (eng.g_layers[0][0], eng.g_router_w, eng.d_hidden, eng.loss_out)):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("name", ["c1_mlp", "c2_small_batch", "c3_shape_d512", "c1_single_relu"])
+def test_score_matches_oracle(name):
+    """Inference scoring (SMESEngine.score, BASELINE c4): predictions and logits from the folded
+    heads (no hidden / O / reps writes) against the oracle forward on the GPU's selections."""
+    seed, B, T, E, d, d_out, ks, ka, d_ff, rs, dense, extra = CASES[name]
+    p, h, y, lam, beta = make_case(seed, B, T, E, d, d_out, ks, ka, d_ff=d_ff, router_scale=rs, **extra)
+    eng = SMESEngine(to_engine_params(p, lam, beta), B, ks, ka)
+    eng.set_inputs(torch.tensor(h, device="cuda"))
+    eng.score()
+    torch.cuda.synchronize()
+    z = eng.z.double().cpu().numpy().reshape(B, T, E).transpose(1, 0, 2)
+    r = O.route_batch(z, ks, ka, p.task_weights)
+    assert np.array_equal(eng.active.cpu().numpy(), r.active)
+    plan = O.build_execution_plan(r.unions, E)
+    f = O.forward_sparse(h, p, ks, ka, logits=z, frozen=r, frozen_plan=plan)
+    assert rel(eng.logits.cpu().numpy(), f.head_logits) < BF16_TOL
+    assert rel(eng.preds.cpu().numpy(), f.predictions) < BF16_TOL
