@@ -378,7 +378,7 @@ def run_ep(args, c, world, rank, local, dev):
     h_host, y_host = _host_inputs(c, B, rank)
     rk.set_inputs(h_host.to(dev), y_host.to(dev))
     if world == 1:
-        comm = LoopbackComm([rk])
+        comm = LoopbackComm([rk], fused=args.transport == "peer")
     elif args.transport == "peer":
         comm = PeerComm(rk)
     else:
@@ -422,7 +422,8 @@ def run_ep(args, c, world, rank, local, dev):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": c["workload"], "global_batch": world * B, "per_gpu_batch": B,
                        "parallelism": f"ep{world}", "experts_per_gpu": El,
-                       "transport": "loopback (1 rank)" if world == 1 else args.transport,
+                       "transport": (f"loopback (1 rank, {args.transport} code path)" if world == 1
+                                     else args.transport),
                        "expert_rows_on_rank0": n_own,
                        "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)"},
             "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
@@ -552,8 +553,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU-baseline sample")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
                     help="BASELINE.json configuration (default c2, the headline)")
-    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
-                    help="c5 all-to-all: NCCL all_to_all_single or the CUDA-IPC peer-memory put")
+    ap.add_argument("--transport", default="peer", choices=["nccl", "peer"],
+                    help="c5 all-to-all: the fused CUDA-IPC peer-memory put (default) or NCCL all_to_all_single")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

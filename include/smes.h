@@ -184,6 +184,13 @@ int smes_ep_combine_dh(int B, int d, int n, long slot_rows, const int32_t* pos, 
 int smes_ep_capacity_guard(int E, long cap, const int32_t* totals, int32_t* seg_pad, int32_t* loads,
                            uint32_t* umask, long n_mask_words, int32_t* usize, long n_inst, int32_t* flag,
                            void* stream);
+/* fused dispatch / return over peer memory: the pack (resp. the segment gather) writes straight into
+ * slot `self` of every owner's (resp. source's) receive buffer through the peer pointer tables. */
+int smes_ep_pack_put(int B, int EW, const uint32_t* umask, int n, int wpr, const void* h_bf16, long ldh, int d,
+                     int self, int32_t* idx, int32_t* pos, int32_t* cnt, void* const* peer_mask_recv,
+                     void* const* peer_h_recv, void* stream);
+int smes_ep_copy_rows_put(int nseg, const int32_t* tab, int El, long slot_rows, int self, const void* src,
+                          long src_ld_bytes, void* const* peer_dst, long dst_ld_bytes, int row_bytes, void* stream);
 int smes_ep_put_slots(int n, int self, const void* send, long slot_bytes, long row_bytes, const int32_t* rows_used,
                       void* const* peer_recv_dev, void* stream);
 int smes_ep_signal_wait(int n, int self, void* const* peer_flags_dev, int32_t* my_flags, int epoch, void* stream);

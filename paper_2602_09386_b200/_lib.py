@@ -45,6 +45,8 @@ SIGNATURES = {
     "smes_ep_combine_dh": [I, I, I, L, P, P, P, P, P],
     "smes_ep_capacity_guard": [I, L, P, P, P, P, L, P, L, P, P],
     "smes_ep_put_slots": [I, I, P, L, L, P, P, P],
+    "smes_ep_pack_put": [I, I, P, I, I, P, L, I, I, P, P, P, P, P, P],
+    "smes_ep_copy_rows_put": [I, P, I, L, I, P, L, P, L, I, P],
     "smes_ep_signal_wait": [I, I, P, P, I, P],
     "smes_ipc_handle": [P, P],
     "smes_ipc_open": [P, P],
@@ -77,7 +79,8 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_sca
                     "smes_fold_heads": 2, "smes_unfold_grads": 3, "smes_gemm_ragged_k_periodic": 1,
                     "smes_mlp_fwd": 1, "smes_mlp_fwd2": 1, "smes_mlp_dgrad": 1, "smes_mlp_dgrad2": 1, "smes_mlp_wgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
-                    "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2}
+                    "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
+                    "smes_ep_copy_rows_put": 1}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 

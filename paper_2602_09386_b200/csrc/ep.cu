@@ -198,6 +198,85 @@ __global__ void ep_wait_kernel(int n, volatile int32_t* my_flags, int32_t epoch)
   __threadfence_system();
 }
 
+
+// ---------------------------------------------------------------- fused pack + put (peer memory)
+// The dispatch writes every packed row straight into slot `self` of the owner's receive buffer
+// (peer pointers from CUDA IPC: stores travel over NVLink), so no send buffer and no separate
+// all-to-all pass exist.  Same compaction order as ep_pack (instances ascending per owner).
+__global__ void __launch_bounds__(1024) ep_pack_index_put_kernel(int B, int EW, const uint32_t* __restrict__ umask,
+                                                                 int wpr, int self, int32_t* __restrict__ idx,
+                                                                 int32_t* __restrict__ pos, int32_t* __restrict__ cnt,
+                                                                 uint32_t* const* __restrict__ peer_mask) {
+  __shared__ int warp_tot[32];
+  __shared__ int base_s;
+  const int r = blockIdx.x;
+  uint32_t* mask_out = peer_mask[r] + (size_t)self * B * wpr;     // slot `self` of owner r
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) base_s = 0;
+  __syncthreads();
+  for (int b0 = 0; b0 < B; b0 += 1024) {
+    const int b = b0 + threadIdx.x;
+    bool pred = false;
+    if (b < B)
+      for (int w = 0; w < wpr; ++w) pred |= umask[(size_t)b * EW + r * wpr + w] != 0u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int off = base_s;
+    for (int w = 0; w < warp; ++w) off += warp_tot[w];
+    const int p = off + __popc(bal & ((1u << lane) - 1u));
+    if (b < B) {
+      pos[(size_t)r * B + b] = pred ? p : -1;
+      if (pred) {
+        idx[(size_t)r * B + p] = b;
+        for (int w = 0; w < wpr; ++w) mask_out[(size_t)p * wpr + w] = umask[(size_t)b * EW + r * wpr + w];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < 32; ++w) t += warp_tot[w];
+      base_s += t;
+    }
+    __syncthreads();
+  }
+  const int n = base_s;
+  if (threadIdx.x == 0) cnt[r] = n;
+  for (size_t i = (size_t)n * wpr + threadIdx.x; i < (size_t)B * wpr; i += blockDim.x) mask_out[i] = 0u;
+}
+
+__global__ void ep_pack_rows_put_kernel(int B, int d, int self, const int32_t* __restrict__ idx,
+                                        const int32_t* __restrict__ cnt, const __nv_bfloat16* __restrict__ h, long ldh,
+                                        __nv_bfloat16* const* __restrict__ peer_h) {
+  const int r = blockIdx.y;
+  __nv_bfloat16* out = peer_h[r] + (size_t)self * B * d;
+  const int vec = d / 8;
+  const long n = (long)cnt[r] * vec;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const long row = i / vec, c = (i - row * vec) * 8;
+    const int b = idx[(size_t)r * B + row];
+    *reinterpret_cast<uint4*>(out + row * d + c) = *reinterpret_cast<const uint4*>(h + (size_t)b * ldh + c);
+  }
+}
+
+// gather rows per segment straight into the destination peer's slot `self`:
+// segment i belongs to peer s = i / El; its slot row (tab[1]) is relative to s * slot_rows locally
+__global__ void ep_copy_rows_put_kernel(const int32_t* __restrict__ tab, int El, long slot_rows, int self,
+                                        const uint8_t* __restrict__ src, long src_ld, uint8_t* const* __restrict__ peer,
+                                        long dst_ld, int row_bytes) {
+  const int i = blockIdx.x;
+  const int s = i / El;
+  const int32_t* t = tab + (size_t)i * 3;
+  const long packed = t[0], drow = t[1] - (long)s * slot_rows + (long)self * slot_rows;
+  const int rows = t[2];
+  uint8_t* dst = peer[s];
+  const int vec = row_bytes / 16;
+  for (long k = threadIdx.x; k < (long)rows * vec; k += blockDim.x) {
+    const long r = k / vec, c = (k - r * vec) * 16;
+    *reinterpret_cast<uint4*>(dst + (drow + r) * dst_ld + c) = *reinterpret_cast<const uint4*>(src + (packed + r) * src_ld + c);
+  }
+}
+
 }  // namespace smes
 
 using namespace smes;
@@ -257,6 +336,32 @@ int smes_ep_capacity_guard(int E, long cap, const int32_t* totals, int32_t* seg_
                                                                                  umask, n_mask_words, usize, n_inst,
                                                                                  flag);
   return launch_ok("ep_capacity_guard");
+}
+
+
+int smes_ep_pack_put(int B, int EW, const uint32_t* umask, int n, int wpr, const void* h, long ldh, int d, int self,
+                     int32_t* idx, int32_t* pos, int32_t* cnt, void* const* peer_mask_recv,
+                     void* const* peer_h_recv, void* stream) {
+  if (n < 1 || n > 64 || wpr < 1 || n * wpr > EW) return set_error(SMES_ERR_SHAPE, "ep_pack_put: n=%d wpr=%d EW=%d", n, wpr, EW);
+  if (d % 8) return set_error(SMES_ERR_SHAPE, "ep_pack_put: d=%d must be a multiple of 8", d);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  ep_pack_index_put_kernel<<<n, 1024, 0, st>>>(B, EW, umask, wpr, self, idx, pos, cnt,
+                                              reinterpret_cast<uint32_t* const*>(peer_mask_recv));
+  dim3 g(296, n);
+  ep_pack_rows_put_kernel<<<g, 256, 0, st>>>(B, d, self, idx, cnt, reinterpret_cast<const __nv_bfloat16*>(h), ldh,
+                                            reinterpret_cast<__nv_bfloat16* const*>(peer_h_recv));
+  return launch_ok("ep_pack_put");
+}
+
+int smes_ep_copy_rows_put(int nseg, const int32_t* tab, int El, long slot_rows, int self, const void* src,
+                          long src_ld_bytes, void* const* peer_dst, long dst_ld_bytes, int row_bytes, void* stream) {
+  if (row_bytes % 16 || src_ld_bytes % 16 || dst_ld_bytes % 16)
+    return set_error(SMES_ERR_SHAPE, "ep_copy_rows_put: rows must be 16-byte multiples");
+  if (nseg == 0) return SMES_OK;
+  ep_copy_rows_put_kernel<<<nseg, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      tab, El, slot_rows, self, reinterpret_cast<const uint8_t*>(src), src_ld_bytes,
+      reinterpret_cast<uint8_t* const*>(peer_dst), dst_ld_bytes, row_bytes);
+  return launch_ok("ep_copy_rows_put");
 }
 
 int smes_ep_put_slots(int n, int self, const void* send, long slot_bytes, long row_bytes, const int32_t* rows_used,

@@ -177,6 +177,9 @@ class EPRank:
         self.C_recv = z(n, self.slot_rows, self.ldc, dt=bf)
         self.tab_own = z(n * El, 3, dt=i32)
         self.dh_own = z(n, B, d)
+        # fused transport: device tables of every rank's receive buffers (set by the transport);
+        # the pack / gather kernels then store straight into the peers' slots
+        self.peers = None
         self.refresh_weights()
 
     def head_w32(self):
@@ -224,6 +227,13 @@ class EPRank:
         tcall("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
              ptr(self.loads), None, self.ldh, None, d, ptr(self.row_of), self.umax, ptr(self.gather_inst),
              ptr(self.gather_exp), ptr(self.C_src), self.ldc, self.ldc, s)
+        if self.peers is not None:
+            pr = self.peers
+            tcall("ep_pack", "smes_ep_pack_put", B, self.EW, ptr(self.umask), self.n, self.wpr, ptr(self.h), self.ldh, d,
+                  self.rank, ptr(self.idx), ptr(self.pos), ptr(self.cnt), ptr(pr["mask"]), ptr(pr["h"]), s)
+            tcall("ep_pack", "smes_ep_put_slots", self.n, self.rank, ptr(self.loads), self.El * 4, self.El * 4, None,
+                  ptr(pr["cnt"]), s)
+            return
         tcall("ep_pack", "smes_ep_pack", B, self.EW, ptr(self.umask), self.n, self.wpr, ptr(self.h), self.ldh, d, ptr(self.idx),
              ptr(self.pos), ptr(self.cnt), ptr(self.mask_send), ptr(self.h_send), s)
 
@@ -244,6 +254,10 @@ class EPRank:
         sh.forward(s, self.seg_pad_o)
         tcall("ep_segments", "smes_ep_segments", 0, self.n, El, ptr(self.cnt_recv), ptr(self.seg_pad_o), self.slot_rows,
              ptr(self.tab_own), s)
+        if self.peers is not None:
+            tcall("ep_copy_rows", "smes_ep_copy_rows_put", self.n * El, ptr(self.tab_own), El, self.slot_rows,
+                  self.rank, ptr(sh.P), sh.ldp * 4, ptr(self.peers["P"]), self.ldp * 4, self.ldp * 4, s)
+            return
         tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * El, ptr(self.tab_own), 0, ptr(sh.P), sh.ldp * 4, ptr(self.P_send),
              self.ldp * 4, self.ldp * 4, s)
 
@@ -261,6 +275,11 @@ class EPRank:
              ptr(self.active), ptr(self.wsel), ptr(self.head_b), ptr(self.P_src), self.ldp, ptr(self.logits),
              ptr(self.preds), ptr(self.labels), ptr(self.lam), ptr(self.loss_part), 1.0 / Bg, ptr(self.C_src),
              self.ldc, ptr(self.dz), ptr(self.freq32), lb_coef, ptr(self.part_db), None, None, self.grid, s)
+        if self.peers is not None:
+            tcall("ep_copy_rows", "smes_ep_copy_rows_put", self.n * self.El, ptr(self.tab_src), self.El,
+                  self.slot_rows, self.rank, ptr(self.C_src), self.ldc * 2, ptr(self.peers["C"]), self.ldc * 2,
+                  self.ldc * 2, s)
+            return
         tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * self.El, ptr(self.tab_src), 0, ptr(self.C_src), self.ldc * 2,
              ptr(self.C_send), self.ldc * 2, self.ldc * 2, s)
 
@@ -320,14 +339,39 @@ class EPRank:
 
 
 # ---------------------------------------------------------------------- transports
-class LoopbackComm:
-    """n virtual ranks in one process (tests, single-GPU runs): slot copies on the device."""
+def _recv_tables(ranks_recv, dev):
+    """Device pointer tables {name: int64[n]} from per-rank receive tensors."""
+    return {k: torch.tensor([t.data_ptr() for t in v], dtype=torch.int64, device=dev) for k, v in ranks_recv.items()}
 
-    def __init__(self, ranks):
+
+def _recv_buffers(rank):
+    return {"mask": rank.umask_recv, "h": rank.h_recv, "cnt": rank.cnt_recv, "P": rank.P_recv, "C": rank.C_recv,
+            "dh": rank.dh_recv}
+
+
+class LoopbackComm:
+    """n virtual ranks in one process (tests, single-GPU runs).  ``fused=False``: slot copies
+    between send and receive buffers; ``fused=True``: the ranks' pack / gather kernels store
+    straight into each other's receive buffers (the peer-memory code path, on one device)."""
+
+    def __init__(self, ranks, fused: bool = False):
         self.ranks = ranks
+        self.fused = fused
+        if fused:
+            bufs = [_recv_buffers(r) for r in ranks]
+            tables = _recv_tables({k: [b[k] for b in bufs] for k in bufs[0]}, ranks[0].dev)
+            for r in ranks:
+                r.peers = tables
 
     def all_to_all(self, name):
         n = len(self.ranks)
+        if self.fused:
+            if name == "dh":
+                s = torch.cuda.current_stream(self.ranks[0].dev).cuda_stream
+                for r in self.ranks:
+                    call("smes_ep_put_slots", n, r.rank, ptr(r.dh_own), r.B * r.d * 4, r.B * r.d * 4, None,
+                         ptr(r.peers["dh"]), s)
+            return
         pairs = [r.exchanges(name) for r in self.ranks]
         for k in range(len(pairs[0])):
             for dst in range(n):
@@ -362,12 +406,13 @@ class NcclComm:
 
 
 class PeerComm:
-    """One rank per process, hand-written transport: every rank writes its slots straight into
-    the peers' receive buffers through CUDA-IPC-mapped peer memory (NVLink/NVSwitch), then a
-    flag handshake (csrc/ep.cu: smes_ep_put_slots, smes_ep_signal_wait).  Only the rows a slot
-    actually holds are moved for the h / P / C exchanges."""
+    """One rank per process, hand-written transport over CUDA-IPC-mapped peer memory
+    (NVLink/NVSwitch).  ``fused=True`` (default): the dispatch pack and the P / C segment
+    gathers store straight into the peers' receive slots (csrc/ep.cu smes_ep_pack_put,
+    smes_ep_copy_rows_put), so an exchange is only the flag handshake (smes_ep_signal_wait);
+    ``fused=False``: a put kernel moves the filled send slots (smes_ep_put_slots)."""
 
-    def __init__(self, rank, group=None):
+    def __init__(self, rank, group=None, fused: bool = True):
         import torch.distributed as dist
         self.dist, self.rank, self.group = dist, rank, group
         self.n, self.me = rank.n, rank.rank
@@ -379,6 +424,9 @@ class PeerComm:
         for name in ("dispatch", "P", "C", "dh"):
             for _, recv in rank.exchanges(name):
                 self._bufs[recv.data_ptr()] = self._open(recv)
+        self.fused = fused
+        if fused:
+            rank.peers = {k: self._bufs[t.data_ptr()] for k, t in _recv_buffers(rank).items()}
         torch.cuda.synchronize(dev)
         self.dist.barrier(group=self.group)
 
@@ -404,6 +452,11 @@ class PeerComm:
     def all_to_all(self, name):
         s = torch.cuda.current_stream(self.rank.dev).cuda_stream
         rk = self.rank
+        if self.fused and name != "dh":
+            # the data is already in the peers' slots: publish and wait for every peer's
+            self.epoch += 1
+            call("smes_ep_signal_wait", self.n, self.me, ptr(self.peer_flags), ptr(self.flags), self.epoch, s)
+            return
         used = {id(rk.h_send): (rk.cnt, rk.d * 2)}      # mask slots travel whole: empty slots must read zero
         for send, recv in rk.exchanges(name):
             slot_bytes = send[0].numel() * send.element_size()

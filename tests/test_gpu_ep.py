@@ -31,25 +31,28 @@ def _rank_params(p, lam, beta, r, n, dev="cuda"):
 
 
 CASES = {
-    # name: (seed, n, B_local, T, E, d, d_ff, ks, ka, router_scale, fuse)
-    "n2_mlp_fused": (0, 2, 512, 4, 64, 128, 256, 2, 1, 1.0, True),
-    "n2_mlp_unfused": (1, 2, 384, 4, 64, 128, 256, 2, 1, 1e-3, False),
-    "n4_t8": (2, 4, 256, 8, 128, 128, 256, 3, 2, 1.0, True),
-    "n1": (3, 1, 512, 4, 32, 128, 256, 2, 1, 1.0, True),
+    # name: (seed, n, B_local, T, E, d, d_ff, ks, ka, router_scale, fuse, peer_put)
+    "n2_mlp_fused": (0, 2, 512, 4, 64, 128, 256, 2, 1, 1.0, True, False),
+    "n2_mlp_unfused": (1, 2, 384, 4, 64, 128, 256, 2, 1, 1e-3, False, False),
+    "n4_t8": (2, 4, 256, 8, 128, 128, 256, 3, 2, 1.0, True, False),
+    "n1": (3, 1, 512, 4, 32, 128, 256, 2, 1, 1.0, True, False),
+    "n2_peer_put": (4, 2, 512, 4, 64, 128, 256, 2, 1, 1.0, True, True),
+    "n4_peer_put": (6, 4, 256, 8, 128, 128, 256, 3, 2, 1.0, True, True),
 }
 
 
 @pytest.mark.parametrize("name", list(CASES))
 def test_ep_parity(name):
-    seed, n, Bl, T, E, d, dff, ks, ka, rs, fuse = CASES[name]
+    seed, n, Bl, T, E, d, dff, ks, ka, rs, fuse, put = CASES[name]
     Bg = n * Bl
     p, h, y, lam, beta = make_case(seed, Bg, T, E, d, d, ks, ka, d_ff=dff, router_scale=rs, rand_lam=True)
     ranks = [EPRank(_rank_params(p, lam, beta, r, n), E, r, n, Bl, ks, ka, fuse_mlp=fuse) for r in range(n)]
     for r, rk in enumerate(ranks):
         rk.set_inputs(torch.tensor(h[r * Bl:(r + 1) * Bl], device="cuda"),
                       torch.tensor(y[:, r * Bl:(r + 1) * Bl], device="cuda", dtype=torch.float32))
-    step = ExpertParallelStep(ranks, LoopbackComm(ranks))
+    step = ExpertParallelStep(ranks, LoopbackComm(ranks, fused=put))
     step.step()
+    step.step()          # a second step: slots are reused (stale data must not leak)
     torch.cuda.synchronize()
     for rk in ranks:
         rk.check()
