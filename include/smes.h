@@ -123,16 +123,19 @@ int smes_bias_from_csum(int E, int T, int d_out, const float* csum, const float*
  *      (model.py:202-208 composed with execution.py:126-158; backward training.py:146-191):
  *      G (E, ldg, d_in) bf16 = head_w W_e (rows >= T zero), c (E, ldg) = head_w b_e, so the head
  *      projections are P = H G_e^T + c_e (an N = ldg GEMM) and d_packed never materialises.
- *      smes_unfold_grads expands Q (E, ldg, d_in) = per-expert C^T H (q_expert_stride = ldg*d_in) and
+ *      smes_unfold_grads expands Q = per-expert C^T H (element (e, t, k) at e*q_expert_stride +
+ *      t*q_task_stride + k*q_k_stride: (E, ldg, d_in) or (E, d_in(+1), ldg) layouts) and
  *      csum (per-expert column sums of C) into dW = head_w^T Q_e, db = head_w^T csum_e and
  *      dW_head = sum_e (Q_e W_e^T + csum_e b_e^T).  Large banks (E*d_out*d_in >= 2^24) run both as
  *      grouped tcgen05 GEMMs (Q split into bf16 hi + lo rows), small ones as split-K CUDA-core tiles.
  *      work: fp32 scratch of smes_fold_work_floats(E, T, d_out, d_in) floats (split-K partials). */
 int smes_fold_work_floats(int E, int T, int d_out, int d_in);
+int smes_fold_gemm_path(int E, int T, int d_out, int d_in);   /* 1: tensor-core fold/unfold path */
 int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* head_w, const void* W_bf16,
                     const float* b, void* G_bf16, float* c, float* work, void* stream);
-int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Qt, long q_expert_stride,
-                      const float* csum, long csum_expert_stride, const float* head_w, const void* W_bf16,
+int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q, long q_expert_stride,
+                      long q_task_stride, long q_k_stride, const float* csum, long csum_expert_stride,
+                      const float* head_w, const void* W_bf16,
                       const float* b, float* dW, float* db, float* work, float* d_head_w, void* stream);
 
 /* ---- fused expert MLP for training steps (csrc/mlp.cu): two chained tcgen05 MMAs per 128-row

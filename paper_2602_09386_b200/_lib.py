@@ -57,7 +57,8 @@ SIGNATURES = {
     "smes_mlp_dgrad2": [P, L, L, P, I, P, I, I, I, P, P, L, P, L, P, L, P],
     "smes_mlp_wgrad": [P, L, L, P, I, P, L, I, I, I, P, P, L, P, P, P],
     "smes_fold_heads": [I, I, I, I, I, P, P, P, P, P, P, P],
-    "smes_unfold_grads": [I, I, I, I, I, P, L, P, L, P, P, P, P, P, P, P, P],
+    "smes_unfold_grads": [I, I, I, I, I, P, L, L, L, P, L, P, P, P, P, P, P, P, P],
+    "smes_fold_gemm_path": [I, I, I, I],
     "smes_stats_finalize": [I, I, D, I, P, P, P, P],
     "smes_loss_finalize": [I, P, D, D, P, P, P],
     "smes_seg_colsum": [P, L, L, I, P, I, P, P, P],
@@ -68,7 +69,7 @@ SIGNATURES = {
 }
 _RESTYPE = {"smes_last_error": C.c_char_p}
 # entry points that return a value rather than a status
-_VALUE_FNS = {"smes_abi_version", "smes_fold_work_floats", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
+_VALUE_FNS = {"smes_abi_version", "smes_fold_work_floats", "smes_fold_gemm_path", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_last_error"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)

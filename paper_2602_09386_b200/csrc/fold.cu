@@ -37,8 +37,8 @@ enum { TILE_FOLD = 0, TILE_UNFOLD = 1 };
 template <int TM, int MODE>
 __global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_out, int d_in,
                                                         const float* __restrict__ head_w,
-                                                        const float* __restrict__ Qt, long q_es,
-                                                        const __nv_bfloat16* __restrict__ W,
+                                                        const float* __restrict__ Qt, long q_es, long q_ts,
+                                                        long q_ks, const __nv_bfloat16* __restrict__ W,
                                                         float* __restrict__ part) {
   __shared__ float sW[64][65];      // [r][c] (FOLD: r = j, c = k) / [c][r] transposed (UNFOLD: c = j, r = k)
   __shared__ float sX[TM][64];      // [t][r]
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_ou
     const int t = i >> 6, r = i & 63;
     float x = 0.f;
     if (t < T && r0 + r < nr)
-      x = MODE == TILE_FOLD ? head_w[(size_t)t * d_out + r0 + r] : Qt[(size_t)e * q_es + (size_t)t * d_in + r0 + r];
+      x = MODE == TILE_FOLD ? head_w[(size_t)t * d_out + r0 + r] : Qt[(size_t)e * q_es + (size_t)t * q_ts + (size_t)(r0 + r) * q_ks];
     sX[t][r] = x;
   }
   __syncthreads();
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(256) unfold_finish_kernel(int E, int T, int d_
 // dW[e, j, k] = sum_t head_w[t, j] Q[e, t, k];  db[e, j] = sum_t head_w[t, j] csum[e, t]
 template <int TM>
 __global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_out, int d_in,
-                                                        const float* __restrict__ Qt, long q_es,
-                                                        const float* __restrict__ csum, long cs_es,
+                                                        const float* __restrict__ Qt, long q_es, long q_ts,
+                                                        long q_ks, const float* __restrict__ csum, long cs_es,
                                                         const float* __restrict__ head_w, float* __restrict__ dW,
                                                         float* __restrict__ db) {
   __shared__ float sw[TM][32];
@@ -167,9 +167,9 @@ __global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_ou
   __syncthreads();
   if (k < d_in) {
     float q[TM];
-    const float* qp = Qt + (size_t)e * q_es + k;
+    const float* qp = Qt + (size_t)e * q_es + (size_t)k * q_ks;
 #pragma unroll
-    for (int t = 0; t < TM; ++t) q[t] = t < T ? qp[(size_t)t * d_in] : 0.f;
+    for (int t = 0; t < TM; ++t) q[t] = t < T ? qp[(size_t)t * q_ts] : 0.f;
     const int jn = min(32, d_out - j0);
     for (int jj = 0; jj < jn; ++jj) {
       float s = 0.f;
@@ -238,8 +238,8 @@ __global__ void fold_convert_kernel(int E, int T, int ldg, int d_out, int d_in, 
 
 // Qbf[e][m] (128 rows per expert): rows t and 64 + t hold bf16(Q), rows 32 + t the bf16 remainder, so
 // sum_m Wp[m] Qbf[m] = hi(w) hi(q) + hi(w) lo(q) + lo(w) hi(q) (~fp32 accurate); Y uses rows t, 32 + t
-__global__ void unfold_split_kernel(int E, int T, int d_in, const float* __restrict__ Q, long q_es,
-                                    __nv_bfloat16* __restrict__ Qbf) {
+__global__ void unfold_split_kernel(int E, int T, int d_in, const float* __restrict__ Q, long q_es, long q_ts,
+                                    long q_ks, __nv_bfloat16* __restrict__ Qbf) {
   const size_t n = (size_t)E * 128 * d_in;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % d_in);
@@ -248,7 +248,7 @@ __global__ void unfold_split_kernel(int E, int T, int d_in, const float* __restr
     const int t = m & 31;
     float v = 0.f;
     if (m < 96 && t < T) {
-      const float q = Q[(size_t)e * q_es + (size_t)t * d_in + k];
+      const float q = Q[(size_t)e * q_es + (size_t)t * q_ts + (size_t)k * q_ks];
       const float hi = __bfloat162float(__float2bfloat16_rn(q));
       v = (m >= 32 && m < 64) ? q - hi : hi;
     }
@@ -324,6 +324,8 @@ static FoldWork fold_layout(int E, int T, int d_out, int d_in) {
   return w;
 }
 
+int smes_fold_gemm_path(int E, int T, int d_out, int d_in) { return gemm_path(E, T, d_out, d_in) ? 1 : 0; }
+
 int smes_fold_work_floats(int E, int T, int d_out, int d_in) {
   const int tm = fold_tm(T);
   const long a = (long)((d_out + 63) / 64) * E * tm * d_in;       // fold partials (CUDA-core path)
@@ -366,15 +368,15 @@ int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* hea
     const int gfin = nfin > nfin_c ? nfin : nfin_c;
     switch (fold_tm(T)) {
       case 8:
-        fold_tile_kernel<8, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
+        fold_tile_kernel<8, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
         fold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
         break;
       case 16:
-        fold_tile_kernel<16, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
+        fold_tile_kernel<16, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
         fold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
         break;
       default:
-        fold_tile_kernel<32, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, Wb, work);
+        fold_tile_kernel<32, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
         fold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
     }
   }
@@ -382,7 +384,8 @@ int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* hea
   return e == cudaSuccess ? SMES_OK : set_error(SMES_ERR_CUDA, "fold_heads: %s", cudaGetErrorString(e));
 }
 
-int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q, long q_es, const float* csum,
+int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q, long q_es, long q_ts, long q_ks,
+                      const float* csum,
                       long cs_es, const float* head_w, const void* W, const float* b, float* dW, float* db,
                       float* work, float* d_head_w, void* stream) {
   if (T < 1 || T > 32 || ldg < T) return set_error(SMES_ERR_SHAPE, "unfold_grads: T=%d ldg=%d", T, ldg);
@@ -397,7 +400,7 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
     float* Y = work + w.y;
     fold_prep_kernel<<<(128 * d_out + 255) / 256, 256, 0, st>>>(T, ldg, d_out, head_w, nullptr, Wp);
     seg_arith_kernel<<<(E + 256) / 256, 256, 0, st>>>(E, 128, seg);
-    unfold_split_kernel<<<4096, 256, 0, st>>>(E, T, d_in, Q, q_es, Qbf);
+    unfold_split_kernel<<<4096, 256, 0, st>>>(E, T, d_in, Q, q_es, q_ts, q_ks, Qbf);
     int rc = smes_gemm_ragged_k_periodic(Wp, d_out, 128, Qbf, d_in, (long)E * 128, E, d_out, d_in, seg, dW, nullptr,
                                          128, stream);
     if (rc) return rc;
@@ -414,18 +417,21 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
     dim3 gfin((d_out + 31) / 32, T);
     switch (fold_tm(T)) {
       case 8:
-        unfold_dw_kernel<8><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, csum, cs_es, head_w, dW, db);
-        fold_tile_kernel<8, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, Wb, work);
+        unfold_dw_kernel<8><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es, head_w, dW, db);
+        fold_tile_kernel<8, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, q_ts, q_ks, Wb,
+                                                                work);
         unfold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
         break;
       case 16:
-        unfold_dw_kernel<16><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, csum, cs_es, head_w, dW, db);
-        fold_tile_kernel<16, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, Wb, work);
+        unfold_dw_kernel<16><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es, head_w, dW, db);
+        fold_tile_kernel<16, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, q_ts, q_ks, Wb,
+                                                                work);
         unfold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
         break;
       default:
-        unfold_dw_kernel<32><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, csum, cs_es, head_w, dW, db);
-        fold_tile_kernel<32, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, Wb, work);
+        unfold_dw_kernel<32><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es, head_w, dW, db);
+        fold_tile_kernel<32, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, q_ts, q_ks, Wb,
+                                                                work);
         unfold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
     }
   }

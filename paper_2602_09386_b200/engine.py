@@ -222,7 +222,17 @@ class SMESEngine:
             self.ldg = _round(T, 8)
             self.G_fold = z(E, self.ldg, di, dt=bf)         # head_w W_last (per expert), rows >= T zero
             self.c_fold = z(E, self.ldg)                    # head_w b_last
-            self.Qe = z(E, self.ldg, di)                    # per-expert C^T H (the folded pool's wgrad)
+            # folded pool's wgrad Q = C^T H per expert.  Small banks: Q^T = H^T C (I = d_in, N = T tile,
+            # the grid covers the SMs) in (E, d_in(+1), ldg) layout; large banks (tensor-core unfold):
+            # Q = C^T H in (E, ldg, d_in) with colsum(C) from the in-tile ones MMA
+            self.q_swapped = bool(call("smes_fold_gemm_path", E, T, self.d_out, di))
+            if self.q_swapped:
+                self.Qe = z(E, self.ldg, di)
+                self.q_strides = (self.ldg * di, di, 1)
+            else:
+                self.q_rows = di if self.fuse_b_last else di + 1   # + the ones column -> per-expert sums of C
+                self.Qe = z(E, self.q_rows, self.ldg)
+                self.q_strides = (self.q_rows * self.ldg, 1, self.ldg)
             self.csum_q = z(E, self.ldg)                    # per-expert column sums of C
             self.fold_work = z(call("smes_fold_work_floats", E, T, self.d_out, di))
         self.seg_half = z(2 * E + 1, dt=i32)
@@ -457,12 +467,23 @@ class SMESEngine:
             else:
                 _tagged(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G_fold),
                         E, di, self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
-            # Q_e = C_e^T H_e and csum_e = colsum(C_e) in one ragged-K GEMM (csum via the ones tile)
-            _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(inp), self.ld_in[L - 1],
-                    R, E, self.ldg, di, ptr(self.seg_pad), ptr(self.Qe), ptr(self.csum_q), s)
+            if self.q_swapped:
+                # Q_e = C_e^T H_e and csum_e = colsum(C_e) in one ragged-K GEMM (csum via the ones tile)
+                _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(inp),
+                        self.ld_in[L - 1], R, E, self.ldg, di, ptr(self.seg_pad), ptr(self.Qe), ptr(self.csum_q), s)
+                cs, cs_es = self.csum_q, self.ldg
+            else:
+                _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm),
+                        self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None, s)
+                if self.fuse_b_last:
+                    _tagged("csum", "smes_part_reduce", ptr(self.part_csum), self.grid, E * T, ptr(self.csum), s)
+                    cs, cs_es = self.csum, T
+                else:
+                    cs, cs_es = self.Qe[:, di, :], self.q_rows * self.ldg
             gw, gb = self.g_layers[L - 1]
-            _tagged("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), self.ldg * di,
-                    ptr(self.csum_q), self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw),
+            qes, qts, qks = self.q_strides
+            _tagged("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), qes, qts, qks,
+                    ptr(cs), cs_es, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw),
                     ptr(gb), ptr(self.fold_work), ptr(self.g_head_w), s)
             top = n_layers - 2
         elif fused:

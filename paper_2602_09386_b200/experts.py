@@ -119,7 +119,7 @@ class ExpertShard:
         tcall(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(inp), self.ld_in[L - 1], R, E,
               self.ldg, di, ptr(seg_pad), ptr(self.Qe), ptr(self.csum), s)
         gw, gb = self.g_layers[L - 1]
-        tcall("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), self.ldg * di,
+        tcall("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), self.ldg * di, di, 1,
               ptr(self.csum), self.ldg, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw), ptr(gb),
               ptr(self.work), ptr(self.g_head_w), s)
         if L == 2 and self.fuse_wgrad:

@@ -35,7 +35,7 @@ def test_fold_and_unfold(E, T, d_out, d_in):
     dW = torch.full((E, d_out, d_in), float("nan"), device=dev)
     db = torch.full((E, d_out), float("nan"), device=dev)
     dhw = torch.full((T, d_out), float("nan"), device=dev)
-    call("smes_unfold_grads", E, T, ldg, d_out, d_in, ptr(Qf), ldg * d_in, ptr(cs_full), ldg,
+    call("smes_unfold_grads", E, T, ldg, d_out, d_in, ptr(Qf), ldg * d_in, d_in, 1, ptr(cs_full), ldg,
          ptr(hw), ptr(W), ptr(b), ptr(dW), ptr(db), ptr(work), ptr(dhw), st)
     torch.cuda.synchronize()
     Q = Qf[:, :T].transpose(1, 2)                 # (E, d_in, T)
@@ -48,3 +48,32 @@ def test_fold_and_unfold(E, T, d_out, d_in):
     tol = 1e-5 if E * d_out * d_in < (1 << 24) else 1e-4
     for got, ref in ((dW, ref_dW), (db, ref_db), (dhw, ref_dhw)):
         assert (got - ref).abs().max().item() <= tol * ref.abs().max().item() + 1e-6
+
+
+@pytest.mark.parametrize("E,T,d_out,d_in", [(32, 8, 256, 512), (8, 13, 96, 64), (16, 8, 1024, 1024)])
+def test_unfold_k_major_layout(E, T, d_out, d_in):
+    """Q in (E, d_in, ldg) layout (the small-bank wgrad orientation) gives the same grads."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(7 * E + T)
+    ldg = (T + 7) // 8 * 8
+    hw = torch.randn(T, d_out, generator=g, device=dev)
+    W = (torch.randn(E, d_out, d_in, generator=g, device=dev) / d_in ** 0.5).to(torch.bfloat16)
+    b = torch.randn(E, d_out, generator=g, device=dev)
+    Qf = torch.zeros(E, ldg, d_in, device=dev)
+    Qf[:, :T] = torch.randn(E, T, d_in, generator=g, device=dev)
+    Qk = Qf.transpose(1, 2).contiguous()          # (E, d_in, ldg)
+    cs = torch.zeros(E, ldg, device=dev)
+    cs[:, :T] = torch.randn(E, T, generator=g, device=dev)
+    work = torch.zeros(call("smes_fold_work_floats", E, T, d_out, d_in), device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for Q, strides in ((Qf, (ldg * d_in, d_in, 1)), (Qk, (d_in * ldg, 1, ldg))):
+        dW = torch.zeros(E, d_out, d_in, device=dev)
+        db = torch.zeros(E, d_out, device=dev)
+        dhw = torch.zeros(T, d_out, device=dev)
+        call("smes_unfold_grads", E, T, ldg, d_out, d_in, ptr(Q), *strides, ptr(cs), ldg, ptr(hw), ptr(W), ptr(b),
+             ptr(dW), ptr(db), ptr(work), ptr(dhw), st)
+        torch.cuda.synchronize()
+        outs.append((dW.clone(), db.clone(), dhw.clone()))
+    for a, c in zip(outs[0], outs[1]):
+        assert torch.allclose(a, c, rtol=1e-5, atol=1e-6)
