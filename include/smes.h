@@ -202,6 +202,11 @@ int smes_ipc_open(const void* handle, void** dev_ptr_out);
 int smes_ipc_close(void* dev_ptr);
 
 /* ---- K5 LoadStats / loss: compute_load_stats (balance.py:54-80), total_loss (training.py:90-94). */
+/* every reduction of the training combine's per-CTA partials in one launch: loss_out {task, L_lb,
+ * total}, per-(expert, task) sums of C (optional), router bias grads (optional), head bias grads. */
+int smes_post_combine(int nparts, const float* part_csum, int n_csum, float* csum, const float* part_rb, int n_rb,
+                      float* rb, const float* part_db, int n_db, float* db, const double* loss_part, double inv_b,
+                      double beta, const double* stats_value, double* loss_out, void* stream);
 int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
                         float* freq_f32, void* stream);
 int smes_loss_finalize(int nparts, const double* part, double inv_b, double beta, const double* stats_value,

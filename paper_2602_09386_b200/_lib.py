@@ -64,6 +64,7 @@ SIGNATURES = {
     "smes_seg_colsum": [P, L, L, I, P, I, P, P, P],
     "smes_unpermute": [I, I, P, P, I, P, L, P, P, P],
     "smes_part_reduce": [P, I, I, P, P],
+    "smes_post_combine": [I, P, I, P, P, I, P, P, I, P, P, D, D, P, P, P],
     "smes_lb_grad": [I, I, I, I, P, P, P, L, L, P, F, I, P, P],
     "smes_bce_loss": [I, I, P, P, P, P, I, P, P],
 }
@@ -77,7 +78,7 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_sca
                     "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
                     "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,
-                    "smes_fold_heads": 2, "smes_unfold_grads": 3, "smes_gemm_ragged_k_periodic": 1,
+                    "smes_post_combine": 1, "smes_fold_heads": 2, "smes_unfold_grads": 3, "smes_gemm_ragged_k_periodic": 1,
                     "smes_mlp_fwd": 1, "smes_mlp_fwd2": 1, "smes_mlp_dgrad": 1, "smes_mlp_dgrad2": 1, "smes_mlp_wgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,

@@ -256,6 +256,73 @@ __global__ void bce_kernel(int T, int B, const float* __restrict__ pred, const f
   }
 }
 
+
+// Every reduction that depends only on the training combine's per-CTA partials, in one launch:
+// task loss (+ L_lb) -> loss_out, per-(expert, task) sums of C, router bias grads, head bias grads.
+// Blocks [0, n_cs) column tiles of csum, then router-bias tiles, then head-bias tiles, last block the
+// loss; each tile: 32 warps split the partials, fixed-order combine (deterministic).
+struct PostArgs {
+  int nparts;
+  const float* part_csum; int n_cs; float* csum;
+  const float* part_rb; int n_rb; float* rb;
+  const float* part_db; int n_db; float* db;
+  const double* loss_part; double inv_b, beta; const double* stats_value; double* loss_out;
+};
+
+__device__ __forceinline__ void tile_sum(const float* __restrict__ part, int nparts, int n, int tile,
+                                         float* __restrict__ out, float (*red)[33]) {
+  // 32 warps x 4 independent loads in flight per lane: ~nparts/128 dependent rounds
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int i = tile * 32 + lane;
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  if (i < n) {
+    int p = warp;
+    for (; p + 96 < nparts; p += 128) {
+      s0 += part[(long)p * n + i]; s1 += part[(long)(p + 32) * n + i];
+      s2 += part[(long)(p + 64) * n + i]; s3 += part[(long)(p + 96) * n + i];
+    }
+    for (; p < nparts; p += 32) s0 += part[(long)p * n + i];
+  }
+  red[warp][lane] = (s0 + s1) + (s2 + s3);
+  __syncthreads();
+  if (warp == 0 && i < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 32; ++w) t += red[w][lane];
+    out[i] = t;
+  }
+}
+
+__global__ void __launch_bounds__(1024) post_combine_kernel(const PostArgs a) {
+  __shared__ float red[32][33];
+  __shared__ double dred[32];
+  const int t_cs = a.part_csum ? (a.n_cs + 31) / 32 : 0;
+  const int t_rb = a.part_rb ? (a.n_rb + 31) / 32 : 0;
+  const int t_db = (a.n_db + 31) / 32;
+  int bid = blockIdx.x;
+  if (bid < t_cs) { tile_sum(a.part_csum, a.nparts, a.n_cs, bid, a.csum, red); return; }
+  bid -= t_cs;
+  if (bid < t_rb) { tile_sum(a.part_rb, a.nparts, a.n_rb, bid, a.rb, red); return; }
+  bid -= t_rb;
+  if (bid < t_db) { tile_sum(a.part_db, a.nparts, a.n_db, bid, a.db, red); return; }
+  // loss
+  double v = 0.0;
+  for (int i = threadIdx.x; i < a.nparts; i += blockDim.x) v += a.loss_part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) dred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < 32; ++i) s += dred[i];
+    const double task = s * a.inv_b;
+    const double lb = a.stats_value ? *a.stats_value : 0.0;
+    a.loss_out[0] = task;
+    a.loss_out[1] = lb;
+    a.loss_out[2] = task + a.beta * lb;
+  }
+}
+
 }  // namespace smes
 
 using namespace smes;
@@ -330,4 +397,14 @@ int smes_part_reduce(const float* part, int nparts, int n, float* out, void* str
   return launch_check("part_reduce");
 }
 
+
+int smes_post_combine(int nparts, const float* part_csum, int n_csum, float* csum, const float* part_rb, int n_rb,
+                      float* rb, const float* part_db, int n_db, float* db, const double* loss_part, double inv_b,
+                      double beta, const double* stats_value, double* loss_out, void* stream) {
+  PostArgs a{nparts, part_csum, n_csum, csum, part_rb, n_rb, rb, part_db, n_db, db, loss_part, inv_b, beta,
+             stats_value, loss_out};
+  const int blocks = (part_csum ? (n_csum + 31) / 32 : 0) + (part_rb ? (n_rb + 31) / 32 : 0) + (n_db + 31) / 32 + 1;
+  post_combine_kernel<<<blocks, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  return launch_check("post_combine");
+}
 }  // extern "C"

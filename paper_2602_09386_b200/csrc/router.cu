@@ -98,10 +98,15 @@ __device__ __forceinline__ void sorted_positions(uint32_t bits, int lane, int (&
   }
 }
 
-template <int EPL, int TP>
+// KS/KA > 0: budget fixed at compile time (selection loops unrolled); PLAIN: not frozen, no
+// probs_in / probs_out (the training and scoring path) -- the branches compile away.
+template <int EPL, int TP, int KS, int KA, bool PLAIN>
 __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int T = a.T, E = a.E, ks = a.ks, ka = a.ka, K = ks + ka;
+  const int T = a.T, E = a.E, ks = KS > 0 ? KS : a.ks, ka = KA > 0 ? KA : a.ka, K = ks + ka;
+  const bool frozen = !PLAIN && a.frozen;
+  const double* probs_in = PLAIN ? nullptr : a.probs_in;
+  double* probs_out = PLAIN ? nullptr : a.probs_out;
   const int EW = (E + 31) >> 5;
   extern __shared__ __align__(16) uint8_t sm[];
   // per-warp partials [warp][E]: union count, active count, sparse mass, dense mass
@@ -157,7 +162,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     for (int j = 0; j < EPL; ++j) pooled[j] = 0.0;
     auto stage1_task = [&](int t, const float (&zv)[EPL]) {
       double p[EPL];
-      if (a.probs_in == nullptr) {
+      if (probs_in == nullptr) {
         uint32_t mk = 0;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
@@ -181,7 +186,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
 #pragma unroll
         for (int j = 0; j < EPL; ++j) p[j] *= inv_sum;
       } else {
-        const double* pr = a.probs_in + ((long)t * a.B + b) * E;
+        const double* pr = probs_in + ((long)t * a.B + b) * E;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
           const int e = lane + 32 * j;
@@ -195,8 +200,8 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         pooled[j] += wt * p[j];
         c_dmass[j] += p[j];
       }
-      if (a.probs_out != nullptr) {
-        double* po = a.probs_out + ((long)t * a.B + b) * E;
+      if (probs_out != nullptr) {
+        double* po = probs_out + ((long)t * a.B + b) * E;
 #pragma unroll
         for (int j = 0; j < EPL; ++j) {
           const int e = lane + 32 * j;
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     }
     // shared set S: top-K_s of pooled, (score desc, index asc)   (routing.py:261, :184-187)
     uint32_t taken = 0;  // bit j: expert lane + 32 j is shared
-    if (a.frozen) {
+    if (frozen) {
       const int v = lane < ks ? a.shared[(long)b * ks + lane] : -1;
       for (int i = 0; i < ks; ++i) {
         const int bi = __shfl_sync(0xffffffffu, v, i);
@@ -247,7 +252,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     auto stage2_task = [&](int t, const float (&zv)[EPL]) {
       uint32_t picked = 0;
       const long ot = ((long)t * a.B + b);
-      if (a.frozen) {
+      if (frozen) {
         const int v = lane < ka ? a.adaptive[ot * ka + lane] : -1;
         for (int i = 0; i < ka; ++i) {
           const int bi = __shfl_sync(0xffffffffu, v, i);
@@ -310,7 +315,9 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     }
     // union bitmask words and size (routing.py:272)
     int usz = 0;
-    for (int j = 0; j < EW; ++j) {
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      if (j >= EW) break;
       uint32_t bit = 0;
 #pragma unroll
       for (int jj = 0; jj < EPL; ++jj)
@@ -393,11 +400,19 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
   const size_t smem = (size_t)RT_WARPS * (E + 1) * 24 + 64;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int epl = (E + 31) / 32;
-#define RT_LAUNCH_T(N, TPV)                                                                       \
+  const bool plain = !frozen && probs_in == nullptr && probs_out == nullptr;
+  const bool b42 = k_shared == 4 && k_adaptive == 2;
+#define RT_LAUNCH_K(N, TPV, KS, KA, PL)                                                           \
   {                                                                                               \
     if (smem > 48 * 1024)                                                                         \
-      cudaFuncSetAttribute(route_kernel<N, TPV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    route_kernel<N, TPV><<<C, RT_WARPS * 32, smem, st>>>(a);                                     \
+      cudaFuncSetAttribute(route_kernel<N, TPV, KS, KA, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                            \
+    route_kernel<N, TPV, KS, KA, PL><<<C, RT_WARPS * 32, smem, st>>>(a);                         \
+  }
+#define RT_LAUNCH_T(N, TPV)                                                                       \
+  {                                                                                               \
+    if (plain && b42) RT_LAUNCH_K(N, TPV, 4, 2, true)                                             \
+    else RT_LAUNCH_K(N, TPV, 0, 0, false)                                                         \
   }
 #define RT_LAUNCH(N)                                                                              \
   if (epl <= N) {                                                                                 \
@@ -408,6 +423,7 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
   RT_LAUNCH(1) RT_LAUNCH(2) RT_LAUNCH(4) RT_LAUNCH(8) RT_LAUNCH(16) RT_LAUNCH(32) {}
 #undef RT_LAUNCH
 #undef RT_LAUNCH_T
+#undef RT_LAUNCH_K
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "route_batch launch: %s", cudaGetErrorString(e));
   return SMES_OK;

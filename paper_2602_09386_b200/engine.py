@@ -374,8 +374,10 @@ class SMESEngine:
                     ptr(self.P), self.ldp, ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam),
                     ptr(self.loss_part), 1.0 / bs, ptr(self.Cm), self.ldc, ptr(self.dz), ptr(self.freq32), lb_coef,
                     ptr(self.part_db), ptr(self.part_csum), ptr(self.part_rb), self.grid, s)
-            _tagged("loss_finalize", "smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
-                    self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
+            # loss, per-(expert, task) sums of C, router / head bias grads: one reduction launch
+            _tagged("post_combine", "smes_post_combine", self.grid, ptr(self.part_csum), E * T, ptr(self.csum),
+                    ptr(self.part_rb), T * E, ptr(self.g_router_b), ptr(self.part_db), T, ptr(self.g_head_b),
+                    ptr(self.loss_part), 1.0 / B, self.beta, self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
             return
         _tagged("combine_fwd", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
@@ -476,8 +478,7 @@ class SMESEngine:
                 _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm),
                         self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None, s)
                 if self.fuse_b_last:
-                    _tagged("csum", "smes_part_reduce", ptr(self.part_csum), self.grid, E * T, ptr(self.csum), s)
-                    cs, cs_es = self.csum, T
+                    cs, cs_es = self.csum, T          # reduced by post_combine
                 else:
                     cs, cs_es = self.Qe[:, di, :], self.q_rows * self.ldg
             gw, gb = self.g_layers[L - 1]
@@ -516,10 +517,9 @@ class SMESEngine:
                      None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0, R, s)
             fused_last = i == n_layers - 1 and self.fuse_b_last and fused
             if fused_last:
-                # db = (per-expert sums of C) head_W: no bias tiles needed
+                # db = (per-expert sums of C, reduced by post_combine) head_W: no bias tiles needed
                 _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
                         di, ptr(self.seg_pad), ptr(gw), None, s)
-                _tagged(f"fc{i + 1}_bias", "smes_part_reduce", ptr(self.part_csum), self.grid, E * T, ptr(self.csum), s)
                 _tagged(f"fc{i + 1}_bias", "smes_bias_from_csum", E, T, do, ptr(self.csum), ptr(self.head_w), ptr(gb),
                         s)
             else:
@@ -539,7 +539,7 @@ class SMESEngine:
         _tagged("router_wgrad", "smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d,
                 ptr(self.g_router_w), s)
         if rb_fused:
-            _tagged("router_bias", "smes_part_reduce", ptr(self.part_rb), self.grid, T * E, ptr(self.g_router_b), s)
+            pass                          # reduced by post_combine
         else:
             _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
                     ptr(self.g_router_b), s)
@@ -548,7 +548,8 @@ class SMESEngine:
         if not getattr(self, "_fused_bwd", False):
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out,
                     ptr(self.g_head_w), s)
-        _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
+        if not getattr(self, "_fused_bwd", False):
+            _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
     def step(self):
         self.forward_a(fold=self.can_fold)
