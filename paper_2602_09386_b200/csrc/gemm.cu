@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr int MYCH = (NCH + 1) / 2;                // chunks per epilogue warp (column parity split)
   constexpr int NBBOX = BN / 64 > 0 ? BN / 64 : 1;   // 64-wide MN-major B boxes per stage
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::kOffB;
   uint8_t* sOnes = smem + S::kOffOnes;
@@ -322,9 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int h = 0; h < CPC / 32; ++h) {
               if (n + h * 32 < ncols) {
-                uint32_t w = 0;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
+                const uint32_t w = pos_mask32(f + h * 32);
                 args.bits_out[(size_t)((n >> 5) + h) * args.bits_ld + row] = w;
               }
             }

@@ -20,6 +20,8 @@
 //
 // Warp roles (384 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer (fwd: S only), w2 TMEM
 // allocator, w3 (fwd) P-MMA issuer, w4..w11 epilogue (warp w owns TMEM lanes 32*(w%4).. and the 64-column half (w-4)/4 of a chunk).
+#include <algorithm>
+
 #include "ptx.cuh"
 #include "smes_capi.h"
 
@@ -30,6 +32,29 @@ constexpr int BM = 128;          // rows per tile
 constexpr int CH = 128;          // d_ff columns per chunk
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
+#ifdef SMES_TRACE
+// experiment builds only: per-CTA cycles spent in each barrier wait (tools/trace_mlp.py)
+__device__ unsigned long long g_trace[148 * 16];
+#define TW(k, stmt)                                                      \
+  do {                                                                   \
+    const long long _t0 = clock64();                                     \
+    stmt;                                                                \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_trace[blockIdx.x * 16 + (k)], (unsigned long long)(clock64() - _t0)); \
+  } while (0)
+__device__ long long g_ev[4 * 12 * 64];
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define EV(r, i)                                                                       \
+  do {                                                                                 \
+    if (blockIdx.x < 4 && (i) < 64) g_ev[(blockIdx.x * 12 + (r)) * 64 + (i)] = clock64(); \
+  } while (0)
+#else
+#define TW(k, stmt) stmt
+#define EV(r, i)
+#endif
 
 struct FwdArgs {
   const int* seg;                // (E+1) padded segment offsets
@@ -103,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const FwdArgs a) {
   using S = FwdSmem<DK>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sX = smem + S::kOffX;
   uint8_t* sW = smem + S::kOffW;
   uint8_t* sG = smem + S::kOffG;
@@ -148,6 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int num_tiles = seg_s[a.E] / BM;
+#ifdef SMES_TRACE
+  const long long t_start = clock64();
+  if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 10] = gtimer();
+#endif
 
   if (warp == 0) {
     if (lane == 0) {
@@ -158,14 +187,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int e = find_group(seg_s, a.E, r0);
         for (int kb = 0; kb < DK; ++kb, ++xi) {
           const int s = slot_of(xi, S::kXS);
-          mbar_wait(&xempty[s], par_of(xi, S::kXS) ^ 1);
+          TW(0, mbar_wait(&xempty[s], par_of(xi, S::kXS) ^ 1));
           mbar_expect_tx(&xfull[s], 16384);
           tma_load_2d(sX + s * 16384, &tmX, &xfull[s], kb * 64, r0);          // box {64 k, 128 rows}
         }
         for (int c = 0; c < NC; ++c) {
           for (int kb = 0; kb < DK; ++kb, ++wi) {
             const int s = slot_of(wi, S::kWS);
-            mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
+            TW(1, mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1));
             mbar_expect_tx(&wfull[s], 16384);
             tma_load_3d(sW + s * 16384, &tmW1, &wfull[s], kb * 64, c * CH, e);  // box {64 k, 128 n, 1}
           }
@@ -180,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int e = find_group(seg_s, a.E, tile * BM);
         for (int c = 0; c < NC; ++c, ++gi) {
           const int s = slot_of(gi, S::kGS);
-          mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+          TW(2, mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1));
           mbar_expect_tx(&gfull[s], 4096);
           tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);          // box {64 f, 16 t, 1}
           tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
@@ -196,14 +225,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int xbase = xi;
         for (int c = 0; c < NC; ++c, ++si) {
           const int sb = si & 1;
-          mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
+          TW(3, mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1)));
+          EV(0, si);
           tc_fence_after();
           const uint32_t tS = tmem_base + sb * CH;
           for (int kb = 0; kb < DK; ++kb, ++wi) {
             const int xs = slot_of(xbase + kb, S::kXS);
-            if (c == 0) mbar_wait(&xfull[xs], par_of(xbase + kb, S::kXS));
+            if (c == 0) TW(4, mbar_wait(&xfull[xs], par_of(xbase + kb, S::kXS)));
             const int ws = slot_of(wi, S::kWS);
-            mbar_wait(&wfull[ws], par_of(wi, S::kWS));
+            TW(5, mbar_wait(&wfull[ws], par_of(wi, S::kWS)));
             tc_fence_after();
             const uint32_t x_addr = smem_u32(sX + xs * 16384), w_addr = smem_u32(sW + ws * 16384);
 #pragma unroll
@@ -214,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (c == NC - 1) tc_commit(&xempty[xs]);     // X k-block no longer needed by this tile
           }
           tc_commit(&sfull[sb]);
+          EV(1, si);
         }
         xi = xbase + DK;
       }
@@ -227,10 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pb = it & 1;
         const uint32_t tP = tmem_base + 256 + pb * 16;
         for (int c = 0; c < NC; ++c, ++gi, ++hi) {
-          mbar_wait(hfull, (uint32_t)(hi & 1));
+          TW(6, mbar_wait(hfull, (uint32_t)(hi & 1)));
           const int gs = slot_of(gi, S::kGS);
-          mbar_wait(&gfull[gs], par_of(gi, S::kGS));
-          if (c == 0) mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1));
+          TW(7, mbar_wait(&gfull[gs], par_of(gi, S::kGS)));
+          EV(6, gi);
+          if (c == 0) TW(8, mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1)));
           tc_fence_after();
           const uint32_t h_addr = smem_u32(sH), g_addr = smem_u32(sG + gs * 4096);
 #pragma unroll
@@ -241,6 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           tc_commit(hempty);
           tc_commit(&gempty[gs]);
+          EV(7, gi);
         }
         tc_commit(&pfull[pb]);
       }
@@ -251,16 +284,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int par = (warp - 4) >> 2;          // 64-column half of the chunk
     float* sbias = reinterpret_cast<float*>(smem + S::kOffBias) + (warp - 4) * 64;
     int si = 0, hi = 0, it = 0;
+    // fc1 bias of the next chunk is fetched one chunk ahead (its L2 latency was on the chain)
+    float bv0 = 0.f, bv1 = 0.f;
+    if ((int)blockIdx.x < num_tiles) {
+      const float* bp = a.b1 + (size_t)find_group(seg_s, a.E, blockIdx.x * BM) * a.d_ff + par * 64 + lane;
+      bv0 = __ldg(bp);
+      bv1 = __ldg(bp + 32);
+    }
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int r0 = tile * BM;
       const int e = find_group(seg_s, a.E, r0);
       const int row = r0 + 32 * q + lane;
       for (int c = 0; c < NC; ++c, ++si) {
         const int n0 = c * CH + par * 64;
-        const float bv0 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + lane);
-        const float bv1 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + 32 + lane);
+        float nb0 = 0.f, nb1 = 0.f;
+        {
+          const int nt = c + 1 < NC ? tile : tile + (int)gridDim.x, nc = c + 1 < NC ? c + 1 : 0;
+          if (nt < num_tiles) {
+            const int ne = nc ? e : find_group(seg_s, a.E, nt * BM);
+            const float* bp = a.b1 + (size_t)ne * a.d_ff + nc * CH + par * 64 + lane;
+            nb0 = __ldg(bp);
+            nb1 = __ldg(bp + 32);
+          }
+        }
         const int sb = si & 1;
-        mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        if (warp == 4) TW(9, mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1))); else mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        if (warp == 4 && lane == 0) EV(2, si);
         tc_fence_after();
         float f[64];
         {
@@ -275,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);       // accumulator drained into registers
+        if (warp == 4 && lane == 0) EV(3, si);
         sbias[lane] = bv0;
         sbias[32 + lane] = bv1;
         __syncwarp();
@@ -286,16 +336,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           f[j + 2] = fmaxf(f[j + 2] + bb.z, 0.f);
           f[j + 3] = fmaxf(f[j + 3] + bb.w, 0.f);
         }
+        if (warp == 4 && lane == 0) EV(8, si);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          uint32_t w = 0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
+          const uint32_t w = pos_mask32(f + h * 32);
           if (a.bits != nullptr) a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
         }
+        if (warp == 4 && lane == 0) EV(9, si);
         // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
-        mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
-        if (lane == 0) bulk_wait_read<0>();
+        if (warp == 4) TW(10, mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1))); else mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
+        if (warp == 4 && lane == 0) EV(4, si);
+        if (lane == 0) TW(12, bulk_wait_read<0>());
         __syncwarp();
         uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
 #pragma unroll
@@ -304,7 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                       pack_bf16(f[8 * cc + 4], f[8 * cc + 5]), pack_bf16(f[8 * cc + 6], f[8 * cc + 7]));
           *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
         }
+        if (warp == 4 && lane == 0) EV(10, si);
         fence_proxy_async_smem();
+        if (warp == 4 && lane == 0) EV(11, si);
         __syncwarp();
         if (lane == 0) {
           if (a.store_h) {
@@ -312,12 +365,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_commit();
           }
           mbar_arrive(hfull);
+          if (warp == 4) EV(5, si);
         }
         ++hi;
+        bv0 = nb0;
+        bv1 = nb1;
       }
       // head projections of this tile: P[row, t] = acc + c[e, t]
       const int pb = it & 1;
-      mbar_wait(&pfull[pb], (uint32_t)((it >> 1) & 1));
+      if (warp == 4) TW(11, mbar_wait(&pfull[pb], (uint32_t)((it >> 1) & 1))); else mbar_wait(&pfull[pb], (uint32_t)((it >> 1) & 1));
       tc_fence_after();
       if (par == 0) {
         uint32_t t0[16];
@@ -343,6 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (lane == 0) bulk_wait<0>();
   }
+#ifdef SMES_TRACE
+  if (threadIdx.x == 128) g_trace[blockIdx.x * 16 + 13] = clock64() - t_start;
+  if (threadIdx.x == 32) g_trace[blockIdx.x * 16 + 14] = clock64() - t_start;
+  if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 15] = clock64() - t_start;
+  if (threadIdx.x == 128) g_trace[blockIdx.x * 16 + 11] = gtimer();
+#endif
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -381,7 +443,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const FwdArgs a) {
   using S = Fwd2Smem<DK>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sX = smem + S::kOffX;
   uint8_t* sW = smem + S::kOffW;
   uint8_t* sG = smem + S::kOffG;
@@ -437,6 +499,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int num_units = upref[a.E];
+#ifdef SMES_TRACE
+  const long long t_start = clock64();
+  if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 10] = gtimer();
+  int n_my_units = 0;
+#endif
   const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   // decode a unit: expert, first tile row, tiles in the pair (1 or 2)
   auto decode = [&](int u, int& e, int& row_pair, int& nt) {
@@ -505,6 +572,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NC; ++c, ++si) {
           const int sb = si & 1;
           mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1));
+          EV(0, si);
           tc_fence_after();
           const uint32_t tS = tmem_base + sb * CH;
           for (int kb = 0; kb < DK; ++kb, ++wi) {
@@ -522,6 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             if (c == NC - 1) tc_commit_2sm_mc(&xempty[xs], kPair);
           }
           tc_commit_2sm_mc(&sfull[sb], kPair);
+          EV(1, si);
         }
         xi = xbase + DK;
       }
@@ -540,6 +609,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           const int gs = slot_of(gi, S::kGS);
           mbar_wait(&gfull[gs], par_of(gi, S::kGS));
           if (c == 0) mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1));
+          EV(6, gi);
           tc_fence_after();
           const uint32_t h_addr = smem_u32(sH + hb * 32768), g_addr = smem_u32(sG + gs * 2048);
 #pragma unroll
@@ -550,6 +620,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           tc_commit_2sm_mc(&hempty[hb], kPair);
           tc_commit_2sm_mc(&gempty[gs], kPair);
+          EV(7, gi);
         }
         tc_commit_2sm_mc(&pfull[pb], kPair);
       }
@@ -612,6 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float bv1 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + 32 + lane);
         const int sb = si & 1;
         mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        if (warp == 4 && lane == 0) EV(2, si);
         tc_fence_after();
         float f[64];
         {
@@ -626,6 +698,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(sb ? lead_sempty1 : lead_sempty0);
+        if (warp == 4 && lane == 0) EV(3, si);
         sbias[lane] = bv0;
         sbias[32 + lane] = bv1;
         __syncwarp();
@@ -640,14 +713,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (valid) {
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            uint32_t w = 0;
-#pragma unroll
-            for (int j = 0; j < 32; ++j) w |= (f[h * 32 + j] > 0.f ? 1u : 0u) << j;
+            const uint32_t w = pos_mask32(f + h * 32);
             if (a.bits != nullptr) a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
           }
         }
         const int hb = hi & 1;
         mbar_wait(&hempty[hb], (uint32_t)(((hi >> 1) & 1) ^ 1));
+        if (warp == 4 && lane == 0) EV(4, si);
         if (lane == 0) bulk_wait_read<1>();     // this buffer's store (two chunks ago) has been read
         __syncwarp();
         uint8_t* hbuf = sH + hb * 32768 + par * 16384;
@@ -664,6 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (a.store_h && valid) tma_store_2d(&tmH, hbuf + 32 * q * 128, n0, r0 + 32 * q);
           bulk_commit();                          // one group per chunk (possibly empty) keeps wait_read<1> exact
           mbar_arrive_cluster(hb ? lead_hfull1 : lead_hfull0);
+          if (warp == 4) EV(5, si);
         }
         ++hi;
         if (c == 0 && p_e >= 0) store_p();      // previous unit's head projections
@@ -673,6 +746,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (p_e >= 0) store_p();
     if (lane == 0) bulk_wait<0>();
   }
+#ifdef SMES_TRACE
+  if (threadIdx.x == 128) {
+    g_trace[blockIdx.x * 16 + 13] = clock64() - t_start;
+    for (int u = cl; u < num_units; u += ncl) ++n_my_units;
+    g_trace[blockIdx.x * 16 + 12] = n_my_units;
+  }
+  if (threadIdx.x == 32) g_trace[blockIdx.x * 16 + 14] = clock64() - t_start;
+  if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 15] = clock64() - t_start;
+  if (threadIdx.x == 128) g_trace[blockIdx.x * 16 + 11] = gtimer();
+#endif
   tc_fence_before();
   __syncthreads();
   cluster_sync();
@@ -706,7 +789,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using S = DgSmem<DK>;
   constexpr int D = DK * 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sC = smem + S::kOffC;
   uint8_t* sG = smem + S::kOffG;
   uint8_t* sW = smem + S::kOffW;
@@ -957,7 +1040,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   using S = Dg2Smem<DK>;
   constexpr int D = DK * 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sC = smem + S::kOffC;
   uint8_t* sG = smem + S::kOffG;
   uint8_t* sW = smem + S::kOffW;
@@ -1252,7 +1335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   using S = WgSmem<DK>;
   constexpr int D = DK * 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint8_t* sX = smem + S::kOffX;
   uint8_t* sC = smem + S::kOffC;
   uint8_t* sG = smem + S::kOffG;
@@ -1494,6 +1577,40 @@ static int sm_count() {
   return n;
 }
 
+// CTA-pair kernels: as many pairs as can be co-resident (GPC boundaries can leave an SM of a
+// pair unusable -- a grid of sm_count() CTAs would then run some pairs as a second wave).
+template <typename K>
+static int pair_grid(K kernel, int smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sm_count() & ~1);
+  cfg.blockDim = dim3(mlp::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nc = 0;
+  if (cudaOccupancyMaxActiveClusters(&nc, (void*)kernel, &cfg) != cudaSuccess || nc <= 0) {
+    cudaGetLastError();
+    return sm_count() & ~1;
+  }
+  return 2 * std::min(nc, sm_count() / 2);
+}
+#ifdef SMES_TRACE
+extern "C" int smes_debug_trace(void* host_out, int clear) {
+  if (clear == 3) {
+    auto k = smes::mlp::mlp_fwd2_kernel<4>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smes::mlp::Fwd2Smem<4>::kBytes);
+    return pair_grid(k, smes::mlp::Fwd2Smem<4>::kBytes);
+  }
+  static unsigned long long z[148 * 16];
+  if (clear == 2) return (int)cudaMemcpyFromSymbol(host_out, smes::mlp::g_ev, sizeof(long long) * 4 * 12 * 64);
+  if (clear) return (int)cudaMemcpyToSymbol(smes::mlp::g_trace, z, sizeof(z));
+  return (int)cudaMemcpyFromSymbol(host_out, smes::mlp::g_trace, sizeof(z));
+}
+#endif
+
 }  // namespace smes
 
 using namespace smes;
@@ -1605,7 +1722,7 @@ int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const 
     const int sm = mlp::Fwd2Smem<DK>::kBytes;                                                           \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd2 smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<sm_count() & ~1, mlp::kThreads, sm, st>>>(tx, tw, tg, th, args);                                    \
+    k<<<pair_grid(k, sm), mlp::kThreads, sm, st>>>(tx, tw, tg, th, args);                                    \
     break;                                                                                             \
   }
   switch (d / 64) {
@@ -1732,7 +1849,7 @@ int smes_mlp_dgrad2(const void* C, long ldc, long rows_cap, const void* G, int l
     const int sm = mlp::Dg2Smem<DK>::kBytes;                                                            \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad2 smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<sm_count() & ~1, mlp::kThreads, sm, st>>>(tc, tg, tw, td, th, args);                                   \
+    k<<<pair_grid(k, sm), mlp::kThreads, sm, st>>>(tc, tg, tw, td, th, args);                                   \
     break;                                                                                             \
   }
   switch (d / 64) {

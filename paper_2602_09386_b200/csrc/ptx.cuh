@@ -223,4 +223,18 @@ __device__ __forceinline__ void tc_commit_2sm_mc(uint64_t* bar, uint16_t cta_mas
       : "memory");
 }
 
+
+// relu bit-mask of 32 values (bit j: v[j] > 0) as a balanced OR tree: the 32 compares are
+// independent, the serial `w |= ... << j` chain cost ~700 cycles per chunk in the epilogues
+__device__ __forceinline__ uint32_t pos_mask32(const float* v) {
+  uint32_t m[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) m[j] = v[j] > 0.f ? (1u << j) : 0u;
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1)
+#pragma unroll
+    for (int j = 0; j < s; ++j) m[j] |= m[j + s];
+  return m[0];
+}
+
 }  // namespace smes

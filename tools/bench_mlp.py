@@ -49,6 +49,10 @@ def run(lib_path):
         call("smes_mlp_fwd", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), ptr(bits),
              R, None, 0, ptr(P), 8, st)
 
+    def fwd_nobits():
+        call("smes_mlp_fwd", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), None,
+             R, None, 0, ptr(P), 8, st)
+
     def dgrad():
         call("smes_mlp_dgrad", ptr(C), 16, R, ptr(G), 8, ptr(W1), E, d, dff, ptr(seg_t), ptr(bits), R, ptr(dX), d,
              ptr(dH), dff, st)
@@ -68,8 +72,11 @@ def run(lib_path):
              ptr(P), 8, 1, R, st)
 
     out = {}
-    for name, fn in [("mlp_fwd", fwd), ("mlp_fwd2", fwd2), ("mlp_fwd_noH", fwd_noh), ("mlp_dgrad", dgrad), ("mlp_dgrad2", dgrad2), ("mlp_dgrad_nodH", dgrad_nodh),
+    only = os.environ.get("ONLY")
+    for name, fn in [("mlp_fwd", fwd), ("mlp_fwd2", fwd2), ("mlp_fwd_noH", fwd_noh), ("mlp_fwd_noH_nobits", fwd_nobits), ("mlp_dgrad", dgrad), ("mlp_dgrad2", dgrad2), ("mlp_dgrad_nodH", dgrad_nodh),
                      ("unfused_fwd", unfused_fwd)]:
+        if only and not name.startswith(only):
+            continue
         for _ in range(3):
             fn()
         ts = []
