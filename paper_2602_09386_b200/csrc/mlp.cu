@@ -103,6 +103,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 
 // ============================================================================ forward
+// S accumulators (128 TMEM columns each): three, so the S-MMA of chunk c+2 does not wait for the
+// epilogue to drain chunk c (a double buffer left a ~380-cycle bubble per chunk, tools/mma_probe)
+constexpr int kSB = 3;
 template <int DK>     // d / 64
 struct FwdSmem {
   // X k-block ring (16 KB slots, spare slots prefetch the next tile), W1 k-block ring (16 KB:
@@ -140,9 +143,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* wempty = wfull + S::kWS;        // [kWS]
   uint64_t* gfull = wempty + S::kWS;        // [kGS]
   uint64_t* gempty = gfull + S::kGS;        // [kGS]
-  uint64_t* sfull = gempty + S::kGS;        // [2]
-  uint64_t* sempty = sfull + 2;             // [2]
-  uint64_t* hfull = sempty + 2;             // [1]
+  uint64_t* sfull = gempty + S::kGS;        // [kSB]
+  uint64_t* sempty = sfull + kSB;           // [kSB]
+  uint64_t* hfull = sempty + kSB;           // [1]
   uint64_t* hempty = hfull + 1;             // [1]
   uint64_t* pfull = hempty + 1;             // [2]
   uint64_t* pempty = pfull + 2;             // [2]
@@ -159,8 +162,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < S::kXS; ++i) { mbar_init(&xfull[i], 1); mbar_init(&xempty[i], 1); }
     for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
     for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
+    for (int i = 0; i < kSB; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps);
       mbar_init(&pfull[i], 1); mbar_init(&pempty[i], kEpiWarps / 2);
     }
     mbar_init(hfull, kEpiWarps);
@@ -224,8 +227,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         const int xbase = xi;
         for (int c = 0; c < NC; ++c, ++si) {
-          const int sb = si & 1;
-          TW(3, mbar_wait(&sempty[sb], (uint32_t)(((si >> 1) & 1) ^ 1)));
+          const int sb = slot_of(si, kSB);
+          TW(3, mbar_wait(&sempty[sb], par_of(si, kSB) ^ 1));
           EV(0, si);
           tc_fence_after();
           const uint32_t tS = tmem_base + sb * CH;
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int gi = 0, hi = 0, it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         const int pb = it & 1;
-        const uint32_t tP = tmem_base + 256 + pb * 16;
+        const uint32_t tP = tmem_base + kSB * CH + pb * 16;
         for (int c = 0; c < NC; ++c, ++gi, ++hi) {
           TW(6, mbar_wait(hfull, (uint32_t)(hi & 1)));
           const int gs = slot_of(gi, S::kGS);
@@ -307,8 +310,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             nb1 = __ldg(bp + 32);
           }
         }
-        const int sb = si & 1;
-        if (warp == 4) TW(9, mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1))); else mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        const int sb = slot_of(si, kSB);
+        if (warp == 4) TW(9, mbar_wait(&sfull[sb], par_of(si, kSB))); else mbar_wait(&sfull[sb], par_of(si, kSB));
         if (warp == 4 && lane == 0) EV(2, si);
         tc_fence_after();
         float f[64];
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       if (par == 0) {
         uint32_t t0[16];
-        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + 256 + pb * 16, t0);
+        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + kSB * CH + pb * 16, t0);
         tmem_ld_wait();
         tc_fence_before();
         __syncwarp();

@@ -41,7 +41,7 @@ def main(path):
 
     def fwd():
         call("smes_mlp_fwd2" if os.environ.get("FWD2") else "smes_mlp_fwd", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), ptr(bits),
-             R, ptr(H) if mode == "h" else None, dff + 64 if mode == "h" else 0, ptr(P), 8, st)
+             R, ptr(H) if mode == "h" else None, dff + 64 if mode == "h" else 0, ptr(P), 8, st) if mode != "x" else call("smes_mlp_fwd", ptr(X), d + 64, R, ptr(W1), ptr(b1), ptr(G), ptr(c), 8, E, d, dff, ptr(seg_t), None, R, None, 0, ptr(P), 8, st)
 
     print("fwd2 pair grid:", lib.smes_debug_trace(None, 3))
     for _ in range(3):
