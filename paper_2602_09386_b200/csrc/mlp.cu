@@ -776,9 +776,11 @@ struct DgSmem {
   static constexpr int kOffC = 0;
   static constexpr int kOffG = kOffC + kCS * 16384;
   static constexpr int kOffW = kOffG + kGS * 4096;
-  static constexpr int kOffH = kOffW + kWS * kWB;        // dH chunk: 2 x 16 KB atoms
-  static constexpr int kOffStg = kOffH + 32768;          // dX store staging: 8 warps x 4 KB
-  static constexpr int kOffBar = kOffStg + kEpiWarps * 4096;
+  // dH chunk double buffer (2 x 16 KB atoms each): the epilogue stages chunk c+1 while the dX
+  // MMAs read chunk c.  The dX store staging (8 warps x 4 KB) aliases the buffer the next chunk
+  // writes: every writer drains its own bulk stores (bulk_wait_read) before reusing it.
+  static constexpr int kOffH = kOffW + kWS * kWB;
+  static constexpr int kOffBar = kOffH + 2 * 32768;
   static constexpr int kOffSeg = kOffBar + 512;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 1024;
   static_assert(kBytes <= 232448, "mlp_dgrad smem");
@@ -797,7 +799,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sG = smem + S::kOffG;
   uint8_t* sW = smem + S::kOffW;
   uint8_t* sH = smem + S::kOffH;
-  uint8_t* sStg = smem + S::kOffStg;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* cfull = bar;                   // [kCS]
   uint64_t* cempty = cfull + S::kCS;
@@ -807,9 +808,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* wempty = wfull + S::kWS;
   uint64_t* sfull = wempty + S::kWS;       // [2]
   uint64_t* sempty = sfull + 2;
-  uint64_t* hfull = sempty + 2;            // [1]
-  uint64_t* hempty = hfull + 1;
-  uint64_t* dfull = hempty + 1;            // [1] dX accumulator
+  uint64_t* hfull = sempty + 2;            // [2]
+  uint64_t* hempty = hfull + 2;            // [2]
+  uint64_t* dfull = hempty + 2;            // [1] dX accumulator
   uint64_t* dempty = dfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
   int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
@@ -825,8 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
     for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], kEpiWarps); }
-    mbar_init(hfull, kEpiWarps);
-    mbar_init(hempty, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&hfull[i], kEpiWarps); mbar_init(&hempty[i], 1); }
     mbar_init(dfull, 1);
     mbar_init(dempty, kEpiWarps);
     fence_mbar_init();
@@ -898,11 +898,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NC; ++c) {
           if (c + 1 < NC) s_mma(c + 1);
           if (c == NC - 1) tc_commit(&cempty[cs]);
-          mbar_wait(hfull, (uint32_t)(hi & 1));
+          const int hb = hi & 1;
+          mbar_wait(&hfull[hb], (uint32_t)((hi >> 1) & 1));
           // the dX accumulator must be drained by the previous tile's epilogue
           if (c == 0) mbar_wait(dempty, (uint32_t)((it & 1) ^ 1));
           tc_fence_after();
-          const uint32_t h_addr = smem_u32(sH);
+          const uint32_t h_addr = smem_u32(sH + hb * 32768);
           for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
             const int ws = slot_of(wi, S::kWS);
             mbar_wait(&wfull[ws], par_of(wi, S::kWS));
@@ -914,7 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          umma_desc_sw128(w_addr + k * 2048, 8192, 1024), idD, (c | kb | k) != 0);
             tc_commit(&wempty[ws]);
           }
-          tc_commit(hempty);
+          tc_commit(&hempty[hb]);
           ++hi;
         }
         tc_commit(dfull);
@@ -923,7 +924,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int par = (warp - 4) >> 2;
-    uint8_t* stg = sStg + (warp - 4) * 4096;
     int si = 0, hi = 0, it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int r0 = tile * BM;
@@ -951,10 +951,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);
-        mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
-        if (a.store_dh && lane == 0) bulk_wait_read<0>();
+        const int hb = hi & 1;
+        mbar_wait(&hempty[hb], (uint32_t)(((hi >> 1) & 1) ^ 1));
+        if (lane == 0) bulk_wait_read<0>();     // own dH / dX-staging stores out of this buffer
         __syncwarp();
-        uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
+        uint8_t* hbuf = sH + hb * 32768;
+        uint8_t* hrow = hbuf + par * 16384 + (32 * q + lane) * 128;
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
@@ -965,16 +967,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           if (a.store_dh) {
-            tma_store_2d(&tmDH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
+            tma_store_2d(&tmDH, hbuf + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
             bulk_commit();
           }
-          mbar_arrive(hfull);
+          mbar_arrive(&hfull[hb]);
         }
         ++hi;
       }
       // dX tile: TMEM [256, 256 + D) -> bf16 -> TMA store, 64-column chunks split by parity
       mbar_wait(dfull, (uint32_t)(it & 1));
       tc_fence_after();
+      // all dX MMAs of the tile are complete, so neither dH buffer is read any more; stage in the
+      // one the next chunk writes
+      uint8_t* stg = sH + (hi & 1) * 32768 + (warp - 4) * 4096;
       for (int cc = par; cc < DK; cc += 2) {
         uint32_t t0[32], t1[32];
         const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;

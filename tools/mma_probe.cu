@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(384, 1) probe(int n_mma, int N, int mode, long
 // Pipeline probe: S-MMA issuer (k MMAs of N=128 per chunk into a double-buffered accumulator)
 // + 8 epilogue warps (wait sfull, tcgen05.ld 2 x 32 cols, arrive sempty) [+ P-MMA warp chained
 // through hfull/hempty when pm > 0].  Returns cycles per chunk.
-__global__ void __launch_bounds__(384, 1) pipe_probe(int chunks, int kmma, int pm, long long* out) {
+__global__ void __launch_bounds__(384, 1) pipe_probe(int chunks, int kmma, int pm, long long* out, int epi = 0) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 3 * 32768);
@@ -142,11 +142,39 @@ __global__ void __launch_bounds__(384, 1) pipe_probe(int chunks, int kmma, int p
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&sempty[sb]);
+      float f[64];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc += t0r[j] ^ t1r[j];
+      for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0r[j]); f[32 + j] = __uint_as_float(t1r[j]); }
+      if (epi & 1) {          // bias + relu through a warp-private smem broadcast
+        float* sbias = reinterpret_cast<float*>(sm + 98304 + 2048) + (warp - 4) * 64;
+        sbias[lane] = (float)si;
+        sbias[32 + lane] = (float)lane;
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 64; j += 4) {
+          const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
+          f[j] = fmaxf(f[j] + bb.x, 0.f); f[j + 1] = fmaxf(f[j + 1] + bb.y, 0.f);
+          f[j + 2] = fmaxf(f[j + 2] + bb.z, 0.f); f[j + 3] = fmaxf(f[j + 3] + bb.w, 0.f);
+        }
+      }
+      if (epi & 2) {          // relu bit-masks to global
+        for (int h = 0; h < 2; ++h) out[8 + (h * 8 + (warp - 4)) * 32 + lane] = pos_mask32(f + h * 32);
+      }
       if (pm > 0) {
         mbar_wait(hempty, (si & 1) ^ 1);
-        fence_proxy_async_smem();
+        if (epi & 4) {        // H tile (bf16, SW128) into smem
+          uint8_t* hrow = sm + 65536 + ((warp - 4) >> 2) * 16384 + (32 * q + lane) * 128;
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
+                                        pack_bf16(f[8 * cc + 4], f[8 * cc + 5]), pack_bf16(f[8 * cc + 6], f[8 * cc + 7]));
+            *reinterpret_cast<uint4*>(hrow + ((cc ^ (lane & 7)) << 4)) = pk;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) acc += __float_as_uint(f[j]);
+        }
+        if (!(epi & 8)) fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(hfull);
       }
@@ -231,7 +259,7 @@ __global__ void __launch_bounds__(384, 1) tma_probe(int n_mma, int inflight, con
 
 int main() {
   long long* d_out;
-  cudaMalloc(&d_out, 64);
+  cudaMalloc(&d_out, 1 << 16);
   const int smem = 3 * 32768 + 2048;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int grid : {1, 148}) {
@@ -266,15 +294,18 @@ int main() {
              (double)h[0] / n_mma, inflight ? (double)h[1] / h[2] : 0.0, e == cudaSuccess ? "" : cudaGetErrorString(e));
     }
   }
-  cudaFuncSetAttribute(pipe_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int pm : {0, 1, 8}) {
-    for (int kmma : {1, 4, 16}) {
+  const int smem3 = 3 * 32768 + 8192;
+  cudaFuncSetAttribute(pipe_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+  for (int epi : {0, 1, 2, 4, 7, 15}) {
+    const int pm = 8, kmma = 16;
+    {
       const int chunks = 256;
-      pipe_probe<<<148, 384, smem>>>(chunks, kmma, pm, d_out);
+      pipe_probe<<<148, 384, smem3>>>(chunks, kmma, pm, d_out, epi);
       cudaError_t e = cudaDeviceSynchronize();
       long long h[1];
       cudaMemcpy(h, d_out, 8, cudaMemcpyDeviceToHost);
-      printf("pipe: S-MMAs/chunk %2d P-MMAs/chunk %d: %.0f cycles/chunk %s\n", kmma, pm, (double)h[0] / chunks,
+      printf("pipe: epi %2d (bias-relu %d bits %d H-sts %d no-fence %d) S-MMAs/chunk %2d P-MMAs/chunk %d: %.0f cycles/chunk %s\n",
+             epi, epi & 1, (epi >> 1) & 1, (epi >> 2) & 1, (epi >> 3) & 1, kmma, pm, (double)h[0] / chunks,
              e == cudaSuccess ? "" : cudaGetErrorString(e));
     }
   }
