@@ -306,44 +306,71 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
   float my_db = 0.f;
   double my_loss = 0.0;
   for (int b = blockIdx.x * CB_WARPS + warp; b < a.B; b += gridDim.x * CB_WARPS) {
+    // one round trip for every per-instance table: row_of is read over its full umax width
+    // (entries past usize are never ranked), labels / lam / head bias ride along
     const int U = a.usize[b];
     for (int j = lane; j < EW; j += 32) s_um[j] = a.umask[(long)b * EW + j];
-    for (int u = lane; u < U; u += 32) s_rows[u] = a.row_of[(long)b * a.umax + u];
+    for (int u = lane; u < umax; u += 32) s_rows[u] = a.row_of[(long)b * a.umax + u];
     for (int i = lane; i < TK; i += 32) {
       const int t = i / K;
       const long o = ((long)t * a.B + b) * K + (i - t * K);
       s_act[i] = a.active[o];
       s_w[i] = a.wsel[o];
     }
+    float y = 0.f, lam_t = 0.f, hb = 0.f;
+    if (lane < T) {
+      y = a.labels[(long)lane * a.B + b];
+      lam_t = a.lam[lane];
+      hb = a.head_b[lane];
+    }
     __syncwarp();
-    // logits from the head projections: logit_t = b_t + sum_k w_k P[row_k, t]
-    float g_raw = 0.f, wf = 0.f;
-    int row_i = 0, t_i = 0;
-    for (int i = lane; i < TK; i += 32) {
-      t_i = i / K;
-      row_i = s_rows[union_rank(s_um, s_act[i])];
-      const float w = s_w[i];
-      g_raw = __ldg(a.P + (long)row_i * ldp + t_i);
-      s_gw[i] = w * g_raw;                      // w_k P_k  (scaled by dlogit below)
-      wf = w * __ldg(a.freq + s_act[i]);
-      s_wf[i] = wf;
+    // logits from the head projections: logit_t = b_t + sum_k w_k P[row_k, t]; the gathers of a
+    // lane's (task, slot) pairs are issued together (second and last round trip)
+    {
+      constexpr int kMaxI = 4;                  // TK <= 128 per warp pass
+      float gv[kMaxI], fv[kMaxI];
+#pragma unroll
+      for (int r = 0; r < kMaxI; ++r) {
+        const int i = lane + 32 * r;
+        gv[r] = 0.f; fv[r] = 0.f;
+        if (i < TK) {
+          const int t = i / K;
+          const int e = s_act[i];
+          gv[r] = __ldg(a.P + (long)s_rows[union_rank(s_um, e)] * ldp + t);
+          fv[r] = __ldg(a.freq + e);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kMaxI; ++r) {
+        const int i = lane + 32 * r;
+        if (i < TK) {
+          const float w = s_w[i];
+          s_gw[i] = w * gv[r];                  // w_k P_k  (scaled by dlogit below)
+          s_wf[i] = w * fv[r];
+        }
+      }
+      for (int i = lane + 32 * kMaxI; i < TK; i += 32) {
+        const int t = i / K;
+        const float w = s_w[i];
+        s_gw[i] = w * __ldg(a.P + (long)s_rows[union_rank(s_um, s_act[i])] * ldp + t);
+        s_wf[i] = w * __ldg(a.freq + s_act[i]);
+      }
     }
     __syncwarp();
     if (lane < T) {
       const int t = lane;
-      float lg = a.head_b[t];
+      float lg = hb;
       for (int k = 0; k < K; ++k) lg += s_gw[t * K + k];
       const float ez = expf(-fabsf(lg));                 // stable sigmoid (linalg.py:108-113)
       const float pos = 1.f / (1.f + ez);
       const float pr = lg >= 0.f ? pos : 1.f - pos;
       a.logits[(long)t * a.B + b] = lg;
       a.preds[(long)t * a.B + b] = pr;
-      const float y = a.labels[(long)t * a.B + b];
-      double pc = (double)pr;
-      pc = pc < 1e-7 ? 1e-7 : (pc > 1.0 - 1e-7 ? 1.0 - 1e-7 : pc);
-      my_loss += (double)a.lam[t] * -((double)y * log(pc) + (1.0 - (double)y) * log1p(-pc));
+      // BCE with the reference's clamp (training.py:54-71); logs in fp32, accumulated in fp64
+      const float pc = fminf(fmaxf(pr, 1e-7f), 1.f - 1e-7f);
+      my_loss += (double)lam_t * -((double)y * (double)logf(pc) + (1.0 - (double)y) * (double)log1pf(-pc));
       const bool inside = pr > 1e-7f && pr < 1.f - 1e-7f;
-      const float dl = inside ? a.lam[t] * a.inv_b * (pr - y) : 0.f;
+      const float dl = inside ? lam_t * a.inv_b * (pr - y) : 0.f;
       s_dl[t] = dl;
       my_db += dl;
     }
