@@ -172,27 +172,41 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
       run[j] = 0;
     }
   }
-  // phase 3: in-order walk; each row's copies land at consecutive positions per expert
-  for (int b = row0; b < rend; ++b) {
-    uint4 hv[VEC];
+  // phase 3: in-order walk; each row's copies land at consecutive positions per expert.  The next
+  // instance's hidden row and mask words are fetched while this one's copies are stored, and the
+  // per-copy metadata (row_of / gather tables) is written by the owning lanes in parallel.
+  uint4 hv[VEC];
+  uint32_t wv[EPL];
+  auto fetch = [&](int b, uint4 (&hh)[VEC], uint32_t (&ww)[EPL]) {
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       int col = (v * 32 + lane) * 8;
-      hv[v] = (h != nullptr && col < d) ? __ldg(reinterpret_cast<const uint4*>(h + (long)b * ldh + col))
-                                        : make_uint4(0, 0, 0, 0);
+      hh[v] = (h != nullptr && col < d && b < rend) ? __ldg(reinterpret_cast<const uint4*>(h + (long)b * ldh + col))
+                                                    : make_uint4(0, 0, 0, 0);
     }
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) ww[j] = (j < EW && b < rend) ? __ldg(&umask[(long)b * EW + j]) : 0u;
+  };
+  fetch(row0, hv, wv);
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int b = row0; b < rend; ++b) {
+    uint4 hn[VEC];
+    uint32_t wn[EPL];
+    fetch(b + 1, hn, wn);
     int u = 0;
-    for (int j = 0; j < EW; ++j) {
-      uint32_t word = __ldg(&umask[(long)b * EW + j]);
-      int my_r = 0;
 #pragma unroll
-      for (int jj = 0; jj < EPL; ++jj)
-        if (jj == j) my_r = run[jj];
+    for (int j = 0; j < EPL; ++j) {
+      if (j >= EW) break;
+      uint32_t word = wv[j];
+      const int my_r = run[j];
       if ((word >> lane) & 1u) {
-#pragma unroll
-        for (int jj = 0; jj < EPL; ++jj)
-          if (jj == j) run[jj]++;
+        run[j]++;
+        const int rank = u + __popc(word & lt);
+        row_of[(long)b * umax + rank] = my_r;
+        gather_inst[my_r] = b;
+        gather_exp[my_r] = j * 32 + lane;
       }
+      u += __popc(word);
       while (word) {
         int bit = __ffs(word) - 1;
         word &= word - 1;
@@ -202,14 +216,12 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
           int col = (v * 32 + lane) * 8;
           if (h != nullptr && col < d) *reinterpret_cast<uint4*>(X + (long)r * ldx + col) = hv[v];
         }
-        if (lane == 0) {
-          row_of[(long)b * umax + u] = r;
-          gather_inst[r] = b;
-          gather_exp[r] = j * 32 + bit;
-        }
-        ++u;
       }
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) hv[v] = hn[v];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) wv[j] = wn[j];
   }
 }
 

@@ -133,21 +133,29 @@ __global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize
       acc[v][4] = x1.x; acc[v][5] = x1.y; acc[v][6] = x1.z; acc[v][7] = x1.w;
     }
   }
+  // the instance's row indices come in one coalesced load (lane u holds row_of[u], read over the
+  // full umax width alongside usize), then are broadcast: the row gathers no longer wait on a
+  // dependent index load each
   const int U = usize[b];
-#pragma unroll 4
-  for (int u = 0; u < U; ++u) {
-    const long r = row_of[(long)b * umax + u];
+  for (int base = 0; base < umax; base += 32) {
+    const int myrow = base + lane < umax ? row_of[(long)b * umax + base + lane] : 0;
+    const int n = min(32, U - base);
+    if (n <= 0) break;
+#pragma unroll 8
+    for (int j = 0; j < n; ++j) {
+      const long r = __shfl_sync(0xffffffffu, myrow, j);
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const int c = (v * 32 + lane) * 8;
-      if (c < d) {
-        uint4 q = __ldg(reinterpret_cast<const uint4*>(dX + r * ldx + c));
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
+      for (int v = 0; v < VEC; ++v) {
+        const int c = (v * 32 + lane) * 8;
+        if (c < d) {
+          uint4 q = __ldg(reinterpret_cast<const uint4*>(dX + r * ldx + c));
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float2 f = __bfloat1622float2(h[i]);
-          acc[v][2 * i] += f.x;
-          acc[v][2 * i + 1] += f.y;
+          for (int i = 0; i < 4; ++i) {
+            float2 f = __bfloat1622float2(h[i]);
+            acc[v][2 * i] += f.x;
+            acc[v][2 * i + 1] += f.y;
+          }
         }
       }
     }
