@@ -5,7 +5,8 @@ package's (taskmoe 0.1.0) Python module API: the same function names,
 argument orders, result types and exception classes, on CUDA tensors.
 There is no CPU fallback: every entry point raises CudaError without a GPU.
 """
-from .errors import ConfigError, CudaError, NumericsError, ShapeError, StateError, TaskMoeError
+from .errors import (ConfigError, CudaError, DataFormatError, NumericsError, PoolError, PoolTimeout, ShapeError,
+                     StateError, TaskMoeError)
 from .engine import ExpertLayer, SMESEngine, SMESParams
 from .routing import (BatchRouting, RoutingBudget, RoutingDecision, naive_route_batch, progressive_route,
                       renormalized_weights, route_batch)
@@ -15,11 +16,15 @@ from .balance import LoadStats, SkewDiagnostics, compute_load_stats, lb_loss_gra
 from .linalg import Affine, init_affine
 from .model import ForwardResult, MoeModel, RouterBank, forward_sparse, init_model
 from .training import BackwardResult, backward, task_loss, total_loss
+from .checkpoint import load_model, save_model
+from .workspace import (DeviceWorkspace, LoadProfile, PageBlock, ReplayResult, WorkspacePool, provision,
+                        required_pages, simulate_replay)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "TaskMoeError", "ShapeError", "ConfigError", "NumericsError", "StateError", "CudaError",
+    "TaskMoeError", "ShapeError", "ConfigError", "NumericsError", "StateError", "CudaError", "DataFormatError",
+    "PoolError", "PoolTimeout",
     "SMESEngine", "SMESParams", "ExpertLayer",
     "RoutingBudget", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route", "naive_route_batch",
     "renormalized_weights",
@@ -29,4 +34,7 @@ __all__ = [
     "Affine", "init_affine",
     "ForwardResult", "MoeModel", "RouterBank", "forward_sparse", "init_model",
     "BackwardResult", "backward", "task_loss", "total_loss",
+    "load_model", "save_model",
+    "DeviceWorkspace", "LoadProfile", "PageBlock", "ReplayResult", "WorkspacePool", "provision", "required_pages",
+    "simulate_replay",
 ]

@@ -35,5 +35,17 @@ class StateError(TaskMoeError, *_base("StateError")):
     """Operation requires state that is missing or inconsistent."""
 
 
+class DataFormatError(TaskMoeError, *_base("DataFormatError")):
+    """Malformed data file (checkpoint); the message names the offending field."""
+
+
+class PoolError(TaskMoeError, *_base("PoolError")):
+    """Invalid workspace-pool operation (infeasible request, double release)."""
+
+
+class PoolTimeout(TaskMoeError, *_base("PoolTimeout")):
+    """An allocation deadline expired before pages became available."""
+
+
 class CudaError(TaskMoeError):
     """CUDA runtime/driver failure or missing device (no CPU fallback exists)."""

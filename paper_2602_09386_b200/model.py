@@ -78,7 +78,7 @@ class MoeModel:
         t = self.routers.num_tasks
         if self.head_w.shape != (t, pools[-1].d_out):
             raise ConfigError("heads must map d_out -> 1 for every task")
-        self.task_loss_weights = torch.as_tensor(self.task_loss_weights, dtype=torch.float32)
+        self.task_loss_weights = torch.as_tensor(self.task_loss_weights, dtype=torch.float64)
         if self.task_loss_weights.shape != (t,):
             raise ConfigError(f"expected {t} task loss weights")
         if bool((self.task_loss_weights < 0).any()) or self.lb_strength < 0:
