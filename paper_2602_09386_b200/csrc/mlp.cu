@@ -32,6 +32,12 @@ constexpr int BM = 128;          // rows per tile
 constexpr int CH = 128;          // d_ff columns per chunk
 constexpr int kThreads = 384;
 constexpr int kEpiWarps = 8;
+#ifndef SMES_FWD_XS         // ring depths of mlp_fwd (X / W1 k-block slots); 0 = the defaults below
+#define SMES_FWD_XS 0
+#endif
+#ifndef SMES_FWD_WS
+#define SMES_FWD_WS 0
+#endif
 #ifdef SMES_TRACE
 // experiment builds only: per-CTA cycles spent in each barrier wait (tools/trace_mlp.py)
 __device__ unsigned long long g_trace[148 * 16];
@@ -110,8 +116,8 @@ template <int DK>     // d / 64
 struct FwdSmem {
   // X k-block ring (16 KB slots, spare slots prefetch the next tile), W1 k-block ring (16 KB:
   // 128 n x 64 k, 1.5 chunks deep at d = 256), G chunk ring (4 KB: 2 x {64 f, 16 t})
-  static constexpr int kXS = DK <= 2 ? DK + 2 : DK <= 4 ? DK + 1 : DK;
-  static constexpr int kWS = DK <= 4 ? 6 : 3;
+  static constexpr int kXS = SMES_FWD_XS > 0 ? SMES_FWD_XS : DK <= 2 ? DK + 2 : DK <= 4 ? DK + 1 : DK;
+  static constexpr int kWS = SMES_FWD_WS > 0 ? SMES_FWD_WS : DK <= 4 ? 6 : 3;
   static constexpr int kGS = 2;
   static constexpr int kOffX = 0;
   static constexpr int kOffW = kOffX + kXS * 16384;
@@ -287,6 +293,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int par = (warp - 4) >> 2;          // 64-column half of the chunk
     float* sbias = reinterpret_cast<float*>(smem + S::kOffBias) + (warp - 4) * 64;
     int si = 0, hi = 0, it = 0;
+    // head projections P[row, t] = acc + c[e, t] of a finished tile are read after chunk 1 of the
+    // next tile: the tile's last P-MMA queues behind the S-MMAs already issued for that tile, and
+    // waiting for it at the tile boundary stalled the epilogue ~2.5 k cycles per tile
+    int p_e = -1, p_row = 0, p_it = 0;
+    auto store_p = [&]() {
+      const int pb = p_it & 1;
+      if (warp == 4) TW(11, mbar_wait(&pfull[pb], (uint32_t)((p_it >> 1) & 1))); else mbar_wait(&pfull[pb], (uint32_t)((p_it >> 1) & 1));
+      tc_fence_after();
+      if (par == 0) {
+        uint32_t t0[16];
+        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + kSB * CH + pb * 16, t0);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pempty[pb]);
+        float* prow = a.P + (size_t)p_row * a.ldp;
+        const float* ce = a.c + (size_t)p_e * a.ldg;
+#pragma unroll
+        for (int t = 0; t < 16; t += 4) {
+          if (t < a.ldp) {
+            float4 v;
+            v.x = __uint_as_float(t0[t + 0]) + ce[t + 0];
+            v.y = __uint_as_float(t0[t + 1]) + ce[t + 1];
+            v.z = __uint_as_float(t0[t + 2]) + ce[t + 2];
+            v.w = __uint_as_float(t0[t + 3]) + ce[t + 3];
+            *reinterpret_cast<float4*>(prow + t) = v;
+          }
+        }
+      }
+      p_e = -1;
+    };
     // fc1 bias of the next chunk is fetched one chunk ahead (its L2 latency was on the chain)
     float bv0 = 0.f, bv1 = 0.f;
     if ((int)blockIdx.x < num_tiles) {
@@ -373,33 +410,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++hi;
         bv0 = nb0;
         bv1 = nb1;
+        if (c == (NC > 1 ? 1 : 0) && p_e >= 0) store_p();     // previous tile's head projections
       }
-      // head projections of this tile: P[row, t] = acc + c[e, t]
-      const int pb = it & 1;
-      if (warp == 4) TW(11, mbar_wait(&pfull[pb], (uint32_t)((it >> 1) & 1))); else mbar_wait(&pfull[pb], (uint32_t)((it >> 1) & 1));
-      tc_fence_after();
-      if (par == 0) {
-        uint32_t t0[16];
-        tmem_ld16(tmem_base + ((uint32_t)(32 * q) << 16) + kSB * CH + pb * 16, t0);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&pempty[pb]);
-        float* prow = a.P + (size_t)row * a.ldp;
-        const float* ce = a.c + (size_t)e * a.ldg;
-#pragma unroll
-        for (int t = 0; t < 16; t += 4) {
-          if (t < a.ldp) {
-            float4 v;
-            v.x = __uint_as_float(t0[t + 0]) + ce[t + 0];
-            v.y = __uint_as_float(t0[t + 1]) + ce[t + 1];
-            v.z = __uint_as_float(t0[t + 2]) + ce[t + 2];
-            v.w = __uint_as_float(t0[t + 3]) + ce[t + 3];
-            *reinterpret_cast<float4*>(prow + t) = v;
-          }
-        }
-      }
+      p_e = e; p_row = row; p_it = it;
     }
+    if (p_e >= 0) store_p();
     if (lane == 0) bulk_wait<0>();
   }
 #ifdef SMES_TRACE

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(384, 1) pipe_probe(int chunks, int kmma, int p
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 8); }
     mbar_init(hfull, 8); mbar_init(hempty, 1);
+    mbar_init(&bar[7], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(slot, 512);
@@ -111,9 +112,11 @@ __global__ void __launch_bounds__(384, 1) pipe_probe(int chunks, int kmma, int p
       const int sb = si & 1;
       mbar_wait(&sempty[sb], ((si >> 1) & 1) ^ 1);
       tc_fence_after();
-      for (int k = 0; k < kmma; ++k)
+      for (int k = 0; k < kmma; ++k) {
         tc_mma_f16(tmem + sb * 128, umma_desc_sw128(a + (k & 3) * 32, 16, 1024),
                    umma_desc_sw128(b + (k & 3) * 32, 16, 1024), idesc, k != 0);
+        if ((epi & 16) && (k & 3) == 3) tc_commit(&bar[7]);     // per-k-block commit (stage release)
+      }
       tc_commit(&sfull[sb]);
     }
   } else if (warp == 3 && lane == 0 && pm > 0) {
@@ -296,7 +299,7 @@ int main() {
   }
   const int smem3 = 3 * 32768 + 8192;
   cudaFuncSetAttribute(pipe_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
-  for (int epi : {0, 1, 2, 4, 7, 15}) {
+  for (int epi : {0, 16, 7, 23}) {
     const int pm = 8, kmma = 16;
     {
       const int chunks = 256;
