@@ -940,6 +940,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;
     const int par = (warp - 4) >> 2;
     int si = 0, hi = 0, it = 0;
+    // dX of a finished tile is drained after chunk 0 of the next tile: that chunk's dH work then
+    // overlaps the tile's last dX MMAs, and the next dX MMAs start as soon as the drain is done
+    int d_it = -1, d_r0 = 0;
+    auto drain = [&]() {
+      // dX tile: TMEM [256, 256 + D) -> bf16 -> TMA store, 64-column chunks split by parity
+      mbar_wait(dfull, (uint32_t)(d_it & 1));
+      tc_fence_after();
+      // all dX MMAs of that tile are complete and the chunk just staged sits in the other dH
+      // buffer: stage in the one the next chunk writes
+      uint8_t* stg = sH + (hi & 1) * 32768 + (warp - 4) * 4096;
+      for (int cc = par; cc < DK; cc += 2) {
+        uint32_t t0[32], t1[32];
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;
+        tmem_ld32(ta, t0);
+        tmem_ld32(ta + 32, t1);
+        tmem_ld_wait();
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t* src = k < 4 ? t0 : t1;
+          const int o = (k & 3) * 8;
+          rowp[k ^ (lane & 7)] = make_uint4(
+              pack_bf16(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
+              pack_bf16(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
+              pack_bf16(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
+              pack_bf16(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmDX, stg, cc * 64, d_r0 + 32 * q);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty);
+      d_it = -1;
+    };
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int r0 = tile * BM;
       const int row = r0 + 32 * q + lane;
@@ -988,43 +1029,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(&hfull[hb]);
         }
         ++hi;
+        if (c == 0 && d_it >= 0) drain();      // previous tile's dX
       }
-      // dX tile: TMEM [256, 256 + D) -> bf16 -> TMA store, 64-column chunks split by parity
-      mbar_wait(dfull, (uint32_t)(it & 1));
-      tc_fence_after();
-      // all dX MMAs of the tile are complete, so neither dH buffer is read any more; stage in the
-      // one the next chunk writes
-      uint8_t* stg = sH + (hi & 1) * 32768 + (warp - 4) * 4096;
-      for (int cc = par; cc < DK; cc += 2) {
-        uint32_t t0[32], t1[32];
-        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;
-        tmem_ld32(ta, t0);
-        tmem_ld32(ta + 32, t1);
-        tmem_ld_wait();
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t* src = k < 4 ? t0 : t1;
-          const int o = (k & 3) * 8;
-          rowp[k ^ (lane & 7)] = make_uint4(
-              pack_bf16(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
-              pack_bf16(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
-              pack_bf16(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
-              pack_bf16(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmDX, stg, cc * 64, r0 + 32 * q);
-          bulk_commit();
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dempty);
+      d_it = it; d_r0 = r0;
     }
+    if (d_it >= 0) drain();
     if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
