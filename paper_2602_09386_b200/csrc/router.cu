@@ -361,6 +361,253 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
   }
 }
 
+
+// ============================================================================ task-grouped router
+// route_tg_kernel<T, E, KS, KA>: the same decisions as route_kernel for the training / scoring
+// path (not frozen, no probs in/out) with a different lane map: the warp's lanes are T groups of
+// L = 32/T, lane (t, q) owns task t's logits of experts [q*EPT, (q+1)*EPT), EPT = E/L.  Every
+// per-task reduction (softmax max / sum, Stage-II top-K_a, the active-set softmax) is then a
+// log2(L)-level shuffle done for all T tasks at once, where the expert-per-lane map needs a
+// 5-level warp reduction per task.  Stage-I pooling is a fixed-order reduce-scatter over the task
+// bits, leaving lane (t, q) with the pooled scores of experts q*EPT + t*R + i, R = EPT/T.
+// Tie rules as routing.py:184-187 (score desc, index asc); Stage I in fp64.
+template <int T, int E, int KS, int KA>
+#ifndef SMES_TG_MINB
+#define SMES_TG_MINB 8      // 32 warps per SM: occupancy beats the few spills (tools/route_time.py)
+#endif
+__global__ void __launch_bounds__(RT_WARPS * 32, SMES_TG_MINB) route_tg_kernel(const RouteArgs a) {
+  constexpr int L = 32 / T, EPT = E / L, R = EPT / T, K = KS + KA, EW = (E + 31) / 32;
+  static_assert(32 % T == 0 && E % L == 0 && EPT % T == 0 && E <= 64, "route_tg shape");
+  using mask_t = unsigned long long;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = lane / L, q = lane % L;
+  const int e0 = q * EPT;                     // first owned expert (Stage II / softmax view)
+  const int p0 = e0 + t * R;                  // first owned pooled expert (after reduce-scatter)
+  const mask_t own = (EPT == 64 ? ~0ull : ((1ull << EPT) - 1ull)) << e0;
+  extern __shared__ __align__(16) uint8_t sm[];
+  int32_t* s_union = reinterpret_cast<int32_t*>(sm);
+  int32_t* s_act = s_union + RT_WARPS * E;
+  double* s_mass = reinterpret_cast<double*>(s_act + RT_WARPS * E + (E & 1) * RT_WARPS);
+  double* s_dmass = s_mass + RT_WARPS * E;
+  // per-(task, expert) running partials of this warp's rows, one owner lane each (shared memory
+  // keeps them out of the register file: 4 x EPT accumulators spilled at 128 registers)
+  double* w_mass = s_dmass + RT_WARPS * E + (size_t)warp * 2 * T * E;     // [T][E]
+  double* w_dmass = w_mass + T * E;                                         // [T][E]
+  int32_t* w_act = reinterpret_cast<int32_t*>(s_dmass + RT_WARPS * E + (size_t)RT_WARPS * 2 * T * E) +
+                   (size_t)warp * (T + 1) * E;                              // [T][E] + union [E]
+  int32_t* w_union = w_act + T * E;
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    w_mass[t * E + e0 + j] = 0.0;
+    w_dmass[t * E + e0 + j] = 0.0;
+    w_act[t * E + e0 + j] = 0;
+    if (t == 0) w_union[e0 + j] = 0;
+  }
+  const double wt = a.tw[t];
+  const int chunk_rows = RT_WARPS * a.rows_per_warp;
+  const int row0 = blockIdx.x * chunk_rows + warp * a.rows_per_warp;
+  int bad = 0;
+  for (int r = 0; r < a.rows_per_warp; ++r) {
+    const int b = row0 + r;
+    if (b >= a.B) break;
+    float z[EPT];
+    {
+      const float* zr = a.z + (long)t * a.st + (long)b * a.sb + e0;
+      if constexpr (EPT % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < EPT; j += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(zr + j));
+          z[j] = v.x; z[j + 1] = v.y; z[j + 2] = v.z; z[j + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) z[j] = __ldg(zr + j);
+      }
+    }
+    // ---------------- Stage I (fp64): dense softmax per task, pooled = sum_t w_t p_t
+    uint32_t mk = 0;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      if (!isfinite(z[j])) bad = 1;
+      mk = max(mk, fkey(z[j]));
+    }
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) mk = max(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+    const double mx = (double)fkey_inv(mk);
+    double v[EPT], sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) { v[j] = exp((double)z[j] - mx); sum += v[j]; }
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    const double inv = 1.0 / sum;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const double pj = v[j] * inv;
+      w_dmass[t * E + e0 + j] += pj;
+      v[j] = wt * pj;
+    }
+    // reduce-scatter over the task bits (highest first): lane keeps the half its bit selects
+#pragma unroll
+    for (int s = 0, len = EPT; len > R; ++s, len >>= 1) {
+      const int o = (T >> (s + 1)) * L;
+      const bool upper = (lane & o) != 0;
+      const int half = len >> 1;
+#pragma unroll
+      for (int i = 0; i < EPT / 2; ++i) {
+        if (i < half) {
+          const double send = upper ? v[i] : v[i + half];
+          const double keep = upper ? v[i + half] : v[i];
+          v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+      }
+    }
+    // shared set: top-K_s of pooled, (score desc, index asc)   (routing.py:261)
+    mask_t smask = 0;
+    {
+      uint64_t pk[R];
+#pragma unroll
+      for (int i = 0; i < R; ++i) pk[i] = dkey(v[i]);
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        uint64_t bk = 0;
+        int bi = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+          if (!((smask >> (p0 + i)) & 1ull) && pk[i] > bk) { bk = pk[i]; bi = p0 + i; }
+        const uint32_t hi = (uint32_t)(bk >> 32), lo = (uint32_t)bk;
+        const uint32_t mh = __reduce_max_sync(0xffffffffu, hi);
+        const uint32_t ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        const int win = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? bi : 0x7fffffff);
+        smask |= 1ull << win;
+      }
+    }
+    // Stage II: top-K_a of z_t with the shared set excluded, within the task's L lanes
+    uint32_t tk[KA];
+    int ti[KA];
+#pragma unroll
+    for (int k = 0; k < KA; ++k) { tk[k] = 0; ti[k] = 0x7fffffff; }
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      if ((smask >> (e0 + j)) & 1ull) continue;
+      uint32_t ck = fkey(z[j]);
+      int ci = e0 + j;
+#pragma unroll
+      for (int k = 0; k < KA; ++k) {            // insertion into the descending list
+        if (ck > tk[k] || (ck == tk[k] && ci < ti[k])) {
+          const uint32_t xk = tk[k]; const int xi = ti[k];
+          tk[k] = ck; ti[k] = ci; ck = xk; ci = xi;
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) {           // merge the partner's list
+      uint32_t ok[KA];
+      int oi[KA];
+#pragma unroll
+      for (int k = 0; k < KA; ++k) {
+        ok[k] = __shfl_xor_sync(0xffffffffu, tk[k], o);
+        oi[k] = __shfl_xor_sync(0xffffffffu, ti[k], o);
+      }
+#pragma unroll
+      for (int m = 0; m < KA; ++m) {
+        uint32_t ck = ok[m];
+        int ci = oi[m];
+#pragma unroll
+        for (int k = 0; k < KA; ++k) {
+          if (ck > tk[k] || (ck == tk[k] && ci < ti[k])) {
+            const uint32_t xk = tk[k]; const int xi = ti[k];
+            tk[k] = ck; ti[k] = ci; ck = xk; ci = xi;
+          }
+        }
+      }
+    }
+    mask_t amask = 0;
+#pragma unroll
+    for (int k = 0; k < KA; ++k) amask |= 1ull << ti[k];
+    const mask_t act = smask | amask;
+    // renormalised weights: softmax of z over the active set (routing.py:203-211)
+    uint32_t ak = 0;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j)
+      if ((act >> (e0 + j)) & 1ull) ak = max(ak, fkey(z[j]));
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) ak = max(ak, __shfl_xor_sync(0xffffffffu, ak, o));
+    const float amx = fkey_inv(ak);
+    float ex[EPT], asum = 0.f;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      ex[j] = ((act >> (e0 + j)) & 1ull) ? expf(z[j] - amx) : 0.f;
+      asum += ex[j];
+    }
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) asum += __shfl_xor_sync(0xffffffffu, asum, o);
+    const long ot = (long)t * a.B + b;
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int e = e0 + j;
+      const mask_t below = (1ull << e) - 1ull;
+      if ((act >> e) & 1ull) {
+        const float w = ex[j] / asum;
+        const int pos = __popcll(act & below);
+        a.active[ot * K + pos] = e;
+        a.wsel[ot * K + pos] = w;
+        w_act[t * E + e] += 1;
+        w_mass[t * E + e] += (double)w;
+      }
+      if ((amask >> e) & 1ull) a.adaptive[ot * KA + __popcll(amask & below)] = e;
+      if (t == 0 && ((smask >> e) & 1ull)) a.shared[(long)b * KS + __popcll(smask & below)] = e;
+    }
+    // union over tasks (routing.py:272)
+    mask_t un = amask;
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) un |= __shfl_xor_sync(0xffffffffu, un, o);
+    un |= smask;
+    if (lane == 0) {
+#pragma unroll
+      for (int w = 0; w < EW; ++w) a.umask[(long)b * EW + w] = (uint32_t)(un >> (32 * w));
+      a.usize[b] = __popcll(un);
+    }
+    if (t == 0) {
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) w_union[e0 + j] += (int)((un >> (e0 + j)) & 1ull);
+    }
+  }
+  bad = __any_sync(0xffffffffu, bad);
+  if (bad && lane == 0) atomicOr(a.flag, 1);
+  // per-(task, expert) partials -> per-expert in task order (fixed order)
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) {
+    int ca = 0;
+    double m = 0.0, dm = 0.0;
+    for (int tt = 0; tt < T; ++tt) {
+      ca += w_act[tt * E + e];
+      m += w_mass[tt * E + e];
+      dm += w_dmass[tt * E + e];
+    }
+    s_union[warp * E + e] = w_union[e];
+    s_act[warp * E + e] = ca;
+    s_mass[warp * E + e] = m;
+    s_dmass[warp * E + e] = dm;
+  }
+  (void)own;
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int cu = 0, ca = 0;
+    double m = 0.0, dm = 0.0;
+    for (int w = 0; w < RT_WARPS; ++w) {
+      cu += s_union[w * E + e];
+      ca += s_act[w * E + e];
+      m += s_mass[w * E + e];
+      dm += s_dmass[w * E + e];
+    }
+    const long o = (long)blockIdx.x * E + e;
+    a.chunk_union[o] = cu;
+    a.chunk_active[o] = ca;
+    a.chunk_mass[o] = m;
+    a.chunk_dmass[o] = dm;
+  }
+}
+
 }  // namespace smes
 
 using namespace smes;
@@ -420,7 +667,17 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
     else if (T * N <= 32 && T <= 32 / N) RT_LAUNCH_T(N, (32 / N > 0 ? 32 / N : 1))               \
     else RT_LAUNCH_T(N, 0)                                                                        \
   } else
+  // task-grouped kernel: + per-warp (task, expert) partials (2 doubles + 1 int) and union counts
+  const size_t smem_tg = smem + (size_t)RT_WARPS * ((size_t)T * E * 20 + E * 4) + 64;
+#define RT_TG(TT, EE)                                                                             \
+  if (plain && b42 && T == TT && E == EE) {                                                        \
+    if (smem_tg > 48 * 1024)                                                                      \
+      cudaFuncSetAttribute(route_tg_kernel<TT, EE, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tg); \
+    route_tg_kernel<TT, EE, 4, 2><<<C, RT_WARPS * 32, smem_tg, st>>>(a);                            \
+  } else
+  RT_TG(8, 32) RT_TG(4, 32)
   RT_LAUNCH(1) RT_LAUNCH(2) RT_LAUNCH(4) RT_LAUNCH(8) RT_LAUNCH(16) RT_LAUNCH(32) {}
+#undef RT_TG
 #undef RT_LAUNCH
 #undef RT_LAUNCH_T
 #undef RT_LAUNCH_K
