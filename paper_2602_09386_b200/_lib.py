@@ -74,11 +74,26 @@ _VALUE_FNS = {"smes_abi_version", "smes_fold_work_floats", "smes_fold_gemm_path"
               "smes_last_error"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
+def _fold_gemm_path(E, T, d_out, d_in):      # csrc/fold.cu gemm_path()
+    return E * d_out * d_in >= (1 << 24) and d_out % 64 == 0 and d_in % 64 == 0 and T <= 32
+
+
+def _fold_launches(E, T, ldg, d_out, d_in, *_):
+    if _fold_gemm_path(E, T, d_out, d_in) and ldg == (T + 7) // 8 * 8:
+        return 4                              # prep, segments, ragged-K GEMM, convert
+    tm = 8 if T <= 8 else 16 if T <= 16 else 32
+    return 1 if d_out <= 256 and T <= 8 and ldg <= 8 else 2
+
+
+def _unfold_launches(E, T, ldg, d_out, d_in, *_):
+    return 7 if _fold_gemm_path(E, T, d_out, d_in) else 3
+
+
 KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_scatter": 1, "smes_gemm_ragged_m": 1,
                     "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
                     "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,
-                    "smes_post_combine": 1, "smes_fold_heads": 2, "smes_unfold_grads": 3, "smes_gemm_ragged_k_periodic": 1,
+                    "smes_post_combine": 1, "smes_fold_heads": _fold_launches, "smes_unfold_grads": _unfold_launches, "smes_gemm_ragged_k_periodic": 1,
                     "smes_mlp_fwd": 1, "smes_mlp_fwd2": 1, "smes_mlp_dgrad": 1, "smes_mlp_dgrad2": 1, "smes_mlp_wgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
@@ -130,7 +145,8 @@ def call(name: str, *args):
     if rc != 0:
         msg = lib.smes_last_error().decode(errors="replace")
         raise _CODE_TO_EXC.get(rc, errors.TaskMoeError)(msg)
-    launch_count += KERNELS_PER_CALL.get(name, 0)
+    k = KERNELS_PER_CALL.get(name, 0)
+    launch_count += k(*args) if callable(k) else k
     return rc
 
 
