@@ -86,7 +86,7 @@ def _fold_launches(E, T, ldg, d_out, d_in, *_):
 
 
 def _unfold_launches(E, T, ldg, d_out, d_in, *_):
-    return 7 if _fold_gemm_path(E, T, d_out, d_in) else 3
+    return 7 if _fold_gemm_path(E, T, d_out, d_in) else 2
 
 
 KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_scatter": 1, "smes_gemm_ragged_m": 1,

@@ -35,16 +35,15 @@ namespace smes {
 enum { TILE_FOLD = 0, TILE_UNFOLD = 1 };
 
 template <int TM, int MODE>
-__global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_out, int d_in,
-                                                        const float* __restrict__ head_w,
-                                                        const float* __restrict__ Qt, long q_es, long q_ts,
-                                                        long q_ks, const __nv_bfloat16* __restrict__ W,
-                                                        float* __restrict__ part) {
+__device__ __forceinline__ void fold_tile_body(int bx, int by, int bz, int gy, int T, int ldg, int d_out, int d_in,
+                                               const float* __restrict__ head_w, const float* __restrict__ Qt,
+                                               long q_es, long q_ts, long q_ks, const __nv_bfloat16* __restrict__ W,
+                                               float* __restrict__ part) {
   __shared__ float sW[64][65];      // [r][c] (FOLD: r = j, c = k) / [c][r] transposed (UNFOLD: c = j, r = k)
   __shared__ float sX[TM][64];      // [t][r]
-  const int e = blockIdx.y;
-  const int c0 = blockIdx.x * 64;   // output column tile (FOLD: k, UNFOLD: j)
-  const int r0 = blockIdx.z * 64;   // reduction split     (FOLD: j, UNFOLD: k)
+  const int e = by;
+  const int c0 = bx * 64;           // output column tile (FOLD: k, UNFOLD: j)
+  const int r0 = bz * 64;           // reduction split     (FOLD: j, UNFOLD: k)
   const int nr = MODE == TILE_FOLD ? d_out : d_in;
   const int nc = MODE == TILE_FOLD ? d_in : d_out;
   const __nv_bfloat16* We = W + (size_t)e * d_out * d_in;
@@ -86,10 +85,20 @@ __global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_ou
     for (int i = 0; i < TH; ++i) acc[i] = fmaf(sX[th * TH + i][r], w, acc[i]);
   }
   if (c0 + c < nc) {
-    const size_t base = ((size_t)blockIdx.z * gridDim.y + e) * TM;
+    const size_t base = ((size_t)bz * gy + e) * TM;
 #pragma unroll
     for (int i = 0; i < TH; ++i) part[(base + th * TH + i) * nc + c0 + c] = acc[i];
   }
+}
+
+template <int TM, int MODE>
+__global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_out, int d_in,
+                                                        const float* __restrict__ head_w,
+                                                        const float* __restrict__ Qt, long q_es, long q_ts,
+                                                        long q_ks, const __nv_bfloat16* __restrict__ W,
+                                                        float* __restrict__ part) {
+  fold_tile_body<TM, MODE>(blockIdx.x, blockIdx.y, blockIdx.z, gridDim.y, T, ldg, d_out, d_in, head_w, Qt, q_es, q_ts,
+                           q_ks, W, part);
 }
 
 // Single-launch fold for d_out <= 256 (the c1/c2 shapes): a block owns (64 columns k, expert e),
@@ -222,15 +231,15 @@ __global__ void __launch_bounds__(256) unfold_finish_kernel(int E, int T, int d_
 
 // dW[e, j, k] = sum_t head_w[t, j] Q[e, t, k];  db[e, j] = sum_t head_w[t, j] csum[e, t]
 template <int TM>
-__global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_out, int d_in,
-                                                        const float* __restrict__ Qt, long q_es, long q_ts,
-                                                        long q_ks, const float* __restrict__ csum, long cs_es,
-                                                        const float* __restrict__ head_w, float* __restrict__ dW,
-                                                        float* __restrict__ db) {
+__device__ __forceinline__ void unfold_dw_body(int bx, int by, int bz, int T, int ldg, int d_out, int d_in,
+                                               const float* __restrict__ Qt, long q_es, long q_ts, long q_ks,
+                                               const float* __restrict__ csum, long cs_es,
+                                               const float* __restrict__ head_w, float* __restrict__ dW,
+                                               float* __restrict__ db) {
   __shared__ float sw[TM][32];
-  const int e = blockIdx.z;
-  const int j0 = blockIdx.y * 32;
-  const int k = blockIdx.x * 128 + threadIdx.x;
+  const int e = bz;
+  const int j0 = by * 32;
+  const int k = bx * 128 + threadIdx.x;
   for (int i = threadIdx.x; i < TM * 32; i += 128) {
     const int t = i >> 5, j = j0 + (i & 31);
     sw[t][i & 31] = (t < T && j < d_out) ? head_w[(size_t)t * d_out + j] : 0.f;
@@ -249,10 +258,31 @@ __global__ void __launch_bounds__(128) unfold_dw_kernel(int T, int ldg, int d_ou
       dW[((size_t)e * d_out + j0 + jj) * d_in + k] = s;
     }
   }
-  if (blockIdx.x == 0 && threadIdx.x < 32 && j0 + threadIdx.x < d_out) {
+  if (bx == 0 && threadIdx.x < 32 && j0 + threadIdx.x < d_out) {
     float s = 0.f;
     for (int t = 0; t < T; ++t) s = fmaf(sw[t][threadIdx.x], csum[(size_t)e * cs_es + t], s);
     db[(size_t)e * d_out + j0 + threadIdx.x] = s;
+  }
+}
+
+// dW/db (unfold_dw_body) and the split partials of Y = Q W^T (fold_tile_body, UNFOLD) in one
+// launch: blocks [0, n1) take the first job, the rest the second -- one launch gap less per step
+template <int TM>
+__global__ void __launch_bounds__(128) unfold_pair_kernel(int E, int T, int ldg, int d_out, int d_in,
+                                                          const float* __restrict__ Qt, long q_es, long q_ts,
+                                                          long q_ks, const float* __restrict__ csum, long cs_es,
+                                                          const float* __restrict__ head_w,
+                                                          const __nv_bfloat16* __restrict__ W, float* __restrict__ dW,
+                                                          float* __restrict__ db, float* __restrict__ part) {
+  const int g1x = (d_in + 127) / 128, g1y = (d_out + 31) / 32, n1 = g1x * g1y * E;
+  const int bid = blockIdx.x;
+  if (bid < n1) {
+    unfold_dw_body<TM>(bid % g1x, (bid / g1x) % g1y, bid / (g1x * g1y), T, ldg, d_out, d_in, Qt, q_es, q_ts, q_ks,
+                       csum, cs_es, head_w, dW, db);
+  } else {
+    const int r = bid - n1, g2x = (d_out + 63) / 64;
+    fold_tile_body<TM, TILE_UNFOLD>(r % g2x, (r / g2x) % E, r / (g2x * E), E, T, ldg, d_out, d_in, nullptr, Qt, q_es,
+                                    q_ts, q_ks, W, part);
   }
 }
 
@@ -488,23 +518,21 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
     const int splits = (d_in + 63) / 64;
     dim3 g2((d_out + 63) / 64, E, splits);
     dim3 gfin((d_out + 31) / 32, T);
+    const int npair = (int)(g1.x * g1.y * g1.z + g2.x * g2.y * g2.z);
     switch (fold_tm(T)) {
       case 8:
-        unfold_dw_kernel<8><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es, head_w, dW, db);
-        fold_tile_kernel<8, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, q_ts, q_ks, Wb,
-                                                                work);
+        unfold_pair_kernel<8><<<npair, 128, 0, st>>>(E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
+                                                         head_w, Wb, dW, db, work);
         unfold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
         break;
       case 16:
-        unfold_dw_kernel<16><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es, head_w, dW, db);
-        fold_tile_kernel<16, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, q_ts, q_ks, Wb,
-                                                                work);
+        unfold_pair_kernel<16><<<npair, 128, 0, st>>>(E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
+                                                         head_w, Wb, dW, db, work);
         unfold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
         break;
       default:
-        unfold_dw_kernel<32><<<g1, 128, 0, st>>>(T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es, head_w, dW, db);
-        fold_tile_kernel<32, TILE_UNFOLD><<<g2, 128, 0, st>>>(T, ldg, d_out, d_in, nullptr, Q, q_es, q_ts, q_ks, Wb,
-                                                                work);
+        unfold_pair_kernel<32><<<npair, 128, 0, st>>>(E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
+                                                         head_w, Wb, dW, db, work);
         unfold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
     }
   }
