@@ -12,6 +12,7 @@ import subprocess
 import sys
 
 NAME_TAGS = [("mlp_fwd_kernel", "mlp_fwd"), ("mlp_dgrad_kernel", "mlp_dgrad"), ("route_kernel", "route"),
+             ("route_tg_kernel", "route"), ("fold_full_kernel", "fold_heads"),
              ("combine_train_kernel", "combine_train"), ("unpermute_kernel", "unpermute"),
              ("scatter_kernel", "plan_scatter")]
 # c2 training-step order of grouped_gemm_kernel launches (engine.step with fuse_mlp)
