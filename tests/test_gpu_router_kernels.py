@@ -1,0 +1,83 @@
+"""The training/scoring router entry (smes_route_batch, not frozen, no dense probabilities in or
+out) through both kernels: the expert-per-lane route_kernel and the task-grouped route_tg_kernel
+(T, E) in {(8, 32), (4, 32)} with (K_s, K_a) = (4, 2).  Against the oracle on the same fp32
+logits: selections and union masks index-exact, weights within fp32 1e-6, and the chunk
+histograms summed over chunks equal to the oracle's LoadStats sums (counts exact, sparse mass of
+the fp32 weights 1e-6 relative, dense fp64 mass 1e-9)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import smes_oracle as O
+from paper_2602_09386_b200 import _lib
+
+
+def _route(z32, ks, ka, tw):
+    call, ptr = _lib.call, _lib.ptr
+    T, B, E = z32.shape
+    K = ks + ka
+    dev = "cuda"
+    z = torch.tensor(z32, dtype=torch.float32, device=dev).permute(1, 0, 2).contiguous()   # (B, T, E)
+    rpw = call("smes_route_rows_per_warp", B)
+    C = call("smes_route_num_chunks", B, rpw)
+    i32 = lambda *s: torch.zeros(*s, dtype=torch.int32, device=dev)
+    f64 = lambda *s: torch.zeros(*s, dtype=torch.float64, device=dev)
+    out = dict(shared=i32(B, ks), adaptive=i32(T, B, ka), active=i32(T, B, K),
+               wsel=torch.zeros(T, B, K, device=dev), umask=i32(B, (E + 31) // 32), usize=i32(B),
+               cu=i32(C, E), ca=i32(C, E), cm=f64(C, E), cd=f64(C, E), flag=i32(1))
+    twt = torch.tensor(tw, dtype=torch.float64, device=dev)
+    call("smes_route_batch", ptr(z), E, T * E, None, ptr(twt), T, B, E, ks, ka, rpw, ptr(out["shared"]),
+         ptr(out["adaptive"]), ptr(out["active"]), ptr(out["wsel"]), ptr(out["umask"]), ptr(out["usize"]),
+         ptr(out["cu"]), ptr(out["ca"]), ptr(out["cm"]), ptr(out["cd"]), None, ptr(out["flag"]), 0,
+         torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+CASES = {
+    "tg_8x32_random": (8, 32, "random"),
+    "tg_8x32_reference_init": (8, 32, "init"),
+    "tg_8x32_ties": (8, 32, "ties"),
+    "tg_4x32_random": (4, 32, "random"),
+    "tg_4x32_ties": (4, 32, "ties"),
+    "lane_8x64_random": (8, 64, "random"),     # expert-per-lane kernel for comparison
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_router_kernel_vs_oracle(name):
+    T, E, kind = CASES[name]
+    ks, ka, B = 4, 2, 3000
+    rng = np.random.default_rng(hash(name) % 2 ** 32)
+    if kind == "random":
+        z = rng.normal(size=(T, B, E))
+    elif kind == "init":          # reference router init: |z| ~ 5e-4, Stage-I gaps ~1e-10
+        z = np.einsum("bd,ted->tbe", rng.normal(size=(B, 256)), rng.uniform(-1e-3 / 16, 1e-3 / 16, size=(T, E, 256)))
+    else:                         # heavy ties: 3 distinct values
+        z = rng.integers(0, 3, size=(T, B, E)).astype(np.float64)
+    z32 = np.asarray(z, dtype=np.float32).astype(np.float64)
+    tw = rng.uniform(0.5, 2.0, size=T)
+    g = _route(z32, ks, ka, tw)
+    ref = O.route_batch(z32, ks, ka, tw)
+    assert g["flag"][0] == 0
+    assert np.array_equal(g["shared"], ref.shared)
+    assert np.array_equal(g["adaptive"], ref.adaptive)
+    assert np.array_equal(g["active"], ref.active)
+    w_ref = np.take_along_axis(ref.weights, ref.active, axis=2)
+    assert np.abs(g["wsel"] - w_ref).max() < 1e-6
+    usize = np.array([len(u) for u in ref.unions])
+    assert np.array_equal(g["usize"], usize)
+    for b in range(0, B, 97):
+        bits = np.zeros(E, bool)
+        bits[ref.unions[b]] = True
+        words = [int(sum(1 << i for i in range(32) if bits[32 * w + i])) for w in range((E + 31) // 32)]
+        assert [int(x) & 0xFFFFFFFF for x in g["umask"][b]] == words
+    # chunk histograms -> LoadStats sums
+    counts = np.bincount(ref.active.reshape(-1), minlength=E)
+    assert np.array_equal(g["ca"].sum(0), counts)
+    assert np.array_equal(g["cu"].sum(0), np.bincount(np.concatenate(ref.unions), minlength=E))
+    sm = ref.weights.sum(axis=(0, 1))              # sums of fp32 weights: 1e-6 relative
+    assert (np.abs(g["cm"].sum(0) - sm) <= 1e-6 * sm + 1e-9).all()
+    assert np.abs(g["cd"].sum(0) - ref.full_probs.sum(axis=(0, 1))).max() < 1e-9 * B * T
