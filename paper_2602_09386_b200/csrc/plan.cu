@@ -90,11 +90,17 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     is_last = (t == (unsigned)(gridDim.x - 1));
   }
   __syncthreads();
-  if (is_last && tid == 0) {
-    __threadfence();
+  if (!is_last) return;
+  // last block: every expert's load in one parallel round trip (a serial chain of E volatile
+  // L2 loads here cost ~10 us), then the prefix by one thread from shared memory
+  __shared__ int32_t s_ld[1024];
+  __threadfence();
+  for (int i = tid; i < E; i += blockDim.x) s_ld[i] = ((volatile int32_t*)loads)[i];
+  __syncthreads();
+  if (tid == 0) {
     int p = 0, l = 0;
     for (int i = 0; i < E; ++i) {
-      int ld = ((volatile int32_t*)loads)[i];
+      const int ld = s_ld[i];
       const int len = (ld + SEG_ALIGN - 1) / SEG_ALIGN * SEG_ALIGN;
       seg_pad[i] = p;
       seg_log[i] = l;
