@@ -43,14 +43,23 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     s_m += chunk_mass[(long)c * E + e];
     s_dm += chunk_dmass[(long)c * E + e];
   }
-  // exclusive scan of chunk_union[:, e] in tiles of blockDim
-  for (int c0 = 0; c0 < C; c0 += blockDim.x) {
-    int c = c0 + tid;
-    int v = c < C ? chunk_union[(long)c * E + e] : 0;
-    int x = v;
+  // exclusive scan of chunk_union[:, e]: each thread owns a contiguous run of up to 16 chunks,
+  // loaded in one round trip; thread sums are scanned across the block, then written back
+  constexpr int PT = 16;
+  const int per = (C + blockDim.x - 1) / blockDim.x;
+  if (per <= PT) {
+    int v[PT];
+    int tsum = 0;
+    const int cb = tid * per;
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      v[k] = (k < per && cb + k < C) ? chunk_union[(long)(cb + k) * E + e] : 0;
+      tsum += v[k];
+    }
+    int x = tsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, o);
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
     if (lane == 31) warp_tot[warp] = x;
@@ -59,16 +68,46 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
       int w = lane < nw ? warp_tot[lane] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, w, o);
+        const int y = __shfl_up_sync(0xffffffffu, w, o);
         if (lane >= o) w += y;
       }
-      warp_tot[lane] = w;  // inclusive over warps
+      warp_tot[lane] = w;
     }
     __syncthreads();
-    int excl = x - v + (warp > 0 ? warp_tot[warp - 1] : 0) + carry;
-    if (c < C) chunk_base[(long)c * E + e] = excl;
-    carry += warp_tot[nw - 1];
-    __syncthreads();
+    int run = x - tsum + (warp > 0 ? warp_tot[warp - 1] : 0);
+#pragma unroll
+    for (int k = 0; k < PT; ++k) {
+      if (k < per && cb + k < C) chunk_base[(long)(cb + k) * E + e] = run;
+      run += v[k];
+    }
+    carry = warp_tot[nw - 1];
+  } else {
+    for (int c0 = 0; c0 < C; c0 += blockDim.x) {
+      int c = c0 + tid;
+      int v = c < C ? chunk_union[(long)c * E + e] : 0;
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) warp_tot[warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        int w = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int y = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += y;
+        }
+        warp_tot[lane] = w;  // inclusive over warps
+      }
+      __syncthreads();
+      int excl = x - v + (warp > 0 ? warp_tot[warp - 1] : 0) + carry;
+      if (c < C) chunk_base[(long)c * E + e] = excl;
+      carry += warp_tot[nw - 1];
+      __syncthreads();
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
