@@ -62,6 +62,13 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
                      const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
                      double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
                      unsigned int* ticket, int32_t* seg_half, void* stream);
+/* smes_plan_reduce + the LoadStats finalize of smes_stats_finalize in the same launch, for steps
+ * with no cross-device exchange of the raw sums in between (single GPU). */
+int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
+                           const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
+                           double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
+                           unsigned int* ticket, int32_t* seg_half, int K, double batch_times_tasks, int dense,
+                           double* stats_out, float* freq_f32, void* stream);
 int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
                      void* stream);
 int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,

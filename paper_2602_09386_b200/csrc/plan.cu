@@ -29,7 +29,8 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
                                     int32_t* __restrict__ loads, double* __restrict__ stats_raw,
                                     int32_t* __restrict__ seg_pad, int32_t* __restrict__ seg_log,
                                     int32_t* __restrict__ totals, unsigned int* __restrict__ ticket,
-                                    int32_t* __restrict__ seg_half) {
+                                    int32_t* __restrict__ seg_half, int K, double bt, int dense,
+                                    double* __restrict__ st_out, float* __restrict__ freq_f32) {
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[32];
   __shared__ double red[3][32];
@@ -154,6 +155,30 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     totals[1] = p;   // physical rows incl. padding
     totals[2] = l;   // N_act (logical rows)
     *ticket = 0u;
+  }
+  if (st_out != nullptr) {
+    // LoadStats finalize (balance.py:54-80) when no cross-device exchange sits between the sums
+    // and their use: the stats_finalize launch folded into the last block (same arithmetic)
+    double part = 0.0;
+    for (int i = tid; i < E; i += blockDim.x) {
+      const double cnt = ((volatile double*)stats_raw)[i];
+      const double f = cnt / bt;
+      const double m = (dense ? ((volatile double*)stats_raw)[2 * E + i] : ((volatile double*)stats_raw)[E + i]) / bt;
+      st_out[i] = f;
+      st_out[E + i] = m;
+      st_out[2 * E + i] = cnt;
+      freq_f32[i] = (float)f;
+      part += f * m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) red[0][warp] = part;
+    __syncthreads();
+    if (tid == 0) {
+      double v = 0.0;
+      for (int w = 0; w < nw; ++w) v += red[0][w];
+      st_out[3 * E] = ((double)E / (double)K) * v;
+    }
   }
 }
 
@@ -312,7 +337,25 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
                      void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
-                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half);
+                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half, 1, 1.0, 0, nullptr,
+                                         nullptr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
+                           const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
+                           double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
+                           unsigned int* ticket, int32_t* seg_half, int K, double batch_times_tasks, int dense,
+                           double* stats_out, float* freq_f32, void* stream) {
+  if (E > 1024) return set_error(SMES_ERR_SHAPE, "plan: E=%d exceeds 1024", E);
+  if (K < 1 || batch_times_tasks <= 0.0) return set_error(SMES_ERR_CONFIG, "plan_reduce_stats: K=%d B*T=%g", K,
+                                                          batch_times_tasks);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
+                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half, K, batch_times_tasks,
+                                         dense, stats_out, freq_f32);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
   return SMES_OK;

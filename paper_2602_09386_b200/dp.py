@@ -37,14 +37,16 @@ class DataParallelStep:
 
     # the three segments between the two collectives
     def _part_a(self):
+        # one rank: nothing to exchange, the plan reduce also finalizes the LoadStats
+        solo = self.world == 1
         if getattr(self.eng, "can_fold", False):
-            self.eng.forward_a(fold=True)     # training step: heads folded into the last pool
+            self.eng.forward_a(fold=True, finalize_stats=solo)     # heads folded into the last pool
         else:
-            self.eng.forward_a()
+            self.eng.forward_a(finalize_stats=solo)
 
     def _part_b(self):
         self.eng.forward_b(with_loss=True, batch_times_tasks=float(self.b_global * self.eng.T), train=True,
-                           batch_scale=self.b_local, lb_batch=self.b_local)
+                           batch_scale=self.b_local, lb_batch=self.b_local, stats_done=self.world == 1)
         self.eng.backward(batch_scale=self.b_local, lb_batch=self.b_local)
 
     def capture(self, warmup: int = 1):

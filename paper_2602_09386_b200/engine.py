@@ -335,7 +335,8 @@ class SMESEngine:
                 ptr(self.head_w), ptr(self.head_b), ptr(self.P), self.ldp, None, ptr(self.logits), ptr(self.preds),
                 None, ptr(self.lam), None, self.grid, s)
 
-    def forward_a(self, frozen: bool = False, fold: bool = False, store_hidden: bool = True, refold: bool = True):
+    def forward_a(self, frozen: bool = False, fold: bool = False, store_hidden: bool = True, refold: bool = True,
+                  finalize_stats: bool = False):
         """Router GEMM -> routing -> plan -> expert GEMMs.  Ends with the per-expert
         LoadStats sums in ``stats_raw`` (the data-parallel exchange point).
         ``fold`` (training steps only, see csrc/fold.cu): the last identity pool is folded into
@@ -346,9 +347,18 @@ class SMESEngine:
         _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
              ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
         self.route(s, frozen=frozen)
-        _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
-             ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),
-             ptr(self.seg_log), ptr(self.totals), ptr(self.ticket), ptr(self.seg_half), s)
+        if finalize_stats:
+            # single device: LoadStats over the local B*T, finalized by the plan reduce's last block
+            _tagged("plan_reduce", "smes_plan_reduce_stats", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
+                    ptr(self.chunk_mass), ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads),
+                    ptr(self.stats_raw), ptr(self.seg_pad), ptr(self.seg_log), ptr(self.totals), ptr(self.ticket),
+                    ptr(self.seg_half), self.K, float(B * T), int(self.dense), ptr(self.stats_out),
+                    ptr(self.freq32), s)
+        else:
+            _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
+                    ptr(self.chunk_mass), ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads),
+                    ptr(self.stats_raw), ptr(self.seg_pad), ptr(self.seg_log), ptr(self.totals), ptr(self.ticket),
+                    ptr(self.seg_half), s)
         _tagged("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
              ptr(self.loads), ptr(self.h), self.ldh, ptr(self.X), self.ld_in[0], ptr(self.row_of), self.umax,
              ptr(self.gather_inst),
@@ -358,12 +368,14 @@ class SMESEngine:
         self.experts_forward(s, fold=fold, store_hidden=store_hidden, refold=refold)
 
     def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
-                  batch_scale: int | None = None, lb_batch: int | None = None):
+                  batch_scale: int | None = None, lb_batch: int | None = None, stats_done: bool = False):
         """LoadStats finalize (global B*T under data parallelism) -> combine + heads + loss.
-        ``train`` (sparse LB reading) fuses the combine backward into the same pass."""
+        ``train`` (sparse LB reading) fuses the combine backward into the same pass.
+        ``stats_done``: forward_a(finalize_stats=True) already finalized the local statistics."""
         s = self._stream()
         T, E, B = self.T, self.E, self.B
-        self.stats_finalize(s, batch_times_tasks)
+        if not stats_done:
+            self.stats_finalize(s, batch_times_tasks)
         self._fused_bwd = bool(train and not self.dense)
         if self._fused_bwd:
             bs = B if batch_scale is None else batch_scale
@@ -552,8 +564,8 @@ class SMESEngine:
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
     def step(self):
-        self.forward_a(fold=self.can_fold)
-        self.forward_b(with_loss=True, train=True)
+        self.forward_a(fold=self.can_fold, finalize_stats=True)
+        self.forward_b(with_loss=True, train=True, stats_done=True)
         self.backward()
 
     # ------------------------------------------------------------------ accounting

@@ -39,14 +39,15 @@ class OracleEngine:
         self.stats_raw = torch.zeros(3 * self.E, dtype=torch.float64)
         self.grad_flat = None
 
-    def forward_a(self):
+    def forward_a(self, finalize_stats=False):    # the oracle finalizes in forward_b either way
         self.f = O.forward_sparse(self.h, self.p, KS, KA)
         r = self.f.routing
         self.stats_raw[: self.E] = torch.tensor(np.bincount(r.active.ravel(), minlength=self.E), dtype=torch.float64)
         self.stats_raw[self.E: 2 * self.E] = torch.tensor(r.weights.sum(axis=(0, 1)))
         self.stats_raw[2 * self.E:] = torch.tensor(r.full_probs.sum(axis=(0, 1)))
 
-    def forward_b(self, with_loss=True, batch_times_tasks=None, train=False, batch_scale=None, lb_batch=None):
+    def forward_b(self, with_loss=True, batch_times_tasks=None, train=False, batch_scale=None, lb_batch=None,
+                  stats_done=False):
         raw = self.stats_raw.numpy()
         bt = batch_times_tasks
         freq, mass = raw[: self.E] / bt, raw[self.E: 2 * self.E] / bt
