@@ -305,23 +305,58 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
   if (s_rb) for (int i = lane; i < TE; i += 32) s_rb[i] = 0.f;
   float my_db = 0.f;
   double my_loss = 0.0;
-  for (int b = blockIdx.x * CB_WARPS + warp; b < a.B; b += gridDim.x * CB_WARPS) {
-    // one round trip for every per-instance table: row_of is read over its full umax width
-    // (entries past usize are never ranked), labels / lam / head bias ride along
-    const int U = a.usize[b];
-    for (int j = lane; j < EW; j += 32) s_um[j] = a.umask[(long)b * EW + j];
-    for (int u = lane; u < umax; u += 32) s_rows[u] = a.row_of[(long)b * a.umax + u];
-    for (int i = lane; i < TK; i += 32) {
-      const int t = i / K;
-      const long o = ((long)t * a.B + b) * K + (i - t * K);
-      s_act[i] = a.active[o];
-      s_w[i] = a.wsel[o];
+  const float lam_t = lane < T ? a.lam[lane] : 0.f, hb = lane < T ? a.head_b[lane] : 0.f;
+  // The per-instance tables (usize, union mask, row_of over its full umax width, active, weights,
+  // labels) of the NEXT instance are fetched into registers while this one is processed, so each
+  // instance waits only on its P gathers.  Register path for E <= 64, umax <= 64, T*K <= 64.
+  const bool pf = EW <= 2 && umax <= 64 && TK <= 64;
+  const int stride = gridDim.x * CB_WARPS;
+  int pU = 0, pRows[2] = {0, 0}, pAct[2] = {0, 0};
+  uint32_t pUm[2] = {0u, 0u};
+  float pW[2] = {0.f, 0.f}, pY = 0.f;
+  auto fetch = [&](int b) {
+    pU = a.usize[b];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int j = lane + 32 * k;
+      if (j < EW) pUm[k] = a.umask[(long)b * EW + j];
+      if (j < umax) pRows[k] = a.row_of[(long)b * a.umax + j];
+      if (j < TK) {
+        const int t = j / K;
+        const long o = ((long)t * a.B + b) * K + (j - t * K);
+        pAct[k] = a.active[o];
+        pW[k] = a.wsel[o];
+      }
     }
-    float y = 0.f, lam_t = 0.f, hb = 0.f;
-    if (lane < T) {
-      y = a.labels[(long)lane * a.B + b];
-      lam_t = a.lam[lane];
-      hb = a.head_b[lane];
+    if (lane < T) pY = a.labels[(long)lane * a.B + b];
+  };
+  if (pf && blockIdx.x * CB_WARPS + warp < a.B) fetch(blockIdx.x * CB_WARPS + warp);
+  for (int b = blockIdx.x * CB_WARPS + warp; b < a.B; b += stride) {
+    int U;
+    float y = 0.f;
+    if (pf) {
+      U = pU;
+      y = pY;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int j = lane + 32 * k;
+        if (j < EW) s_um[j] = pUm[k];
+        if (j < umax) s_rows[j] = pRows[k];
+        if (j < TK) { s_act[j] = pAct[k]; s_w[j] = pW[k]; }
+      }
+      if (b + stride < a.B) fetch(b + stride);
+    } else {
+      // one round trip for every per-instance table
+      U = a.usize[b];
+      for (int j = lane; j < EW; j += 32) s_um[j] = a.umask[(long)b * EW + j];
+      for (int u = lane; u < umax; u += 32) s_rows[u] = a.row_of[(long)b * a.umax + u];
+      for (int i = lane; i < TK; i += 32) {
+        const int t = i / K;
+        const long o = ((long)t * a.B + b) * K + (i - t * K);
+        s_act[i] = a.active[o];
+        s_w[i] = a.wsel[o];
+      }
+      if (lane < T) y = a.labels[(long)lane * a.B + b];
     }
     __syncwarp();
     // logits from the head projections: logit_t = b_t + sum_k w_k P[row_k, t]; the gathers of a
