@@ -47,10 +47,17 @@ struct GemmArgs {
 // Shared-memory plan.  ragged-M tiles are epilogue(store)-paced at the c2 shapes, so every
 // epilogue warp double-buffers its 4 KB TMA-store staging chunk (ncu r1: the single-buffer
 // bulk wait was the top stall); ragged-K (wgrad) runs long K loops and stores once per tile.
+// ragged-K with BN = 256: 4 k-block stages, the epilogue's TMA-store staging aliased onto the
+// first stage slots (a long K loop stores once per tile; the producer starts the next tile only
+// after the staging reads completed).  fc1 wgrad at c2: 95 -> 85 us.
+#ifndef SMES_RK256_STAGES
+#define SMES_RK256_STAGES 4
+#endif
 template <int BN, int MODE>
 struct Smem {
-  static constexpr int kStages = MODE == MODE_RAGGED_K ? (BN == 256 ? 3 : BN == 128 ? 5 : 6)
+  static constexpr int kStages = MODE == MODE_RAGGED_K ? (BN == 256 ? SMES_RK256_STAGES : BN == 128 ? 5 : 6)
                                                        : (BN == 256 ? 3 : BN == 128 ? 4 : 6);
+  static constexpr bool kStgAlias = MODE == MODE_RAGGED_K && BN == 256 && SMES_RK256_STAGES > 3;
   static constexpr int kAccStages = MODE == MODE_RAGGED_K ? 1 : 2;
   static constexpr int kStgBufs = MODE == MODE_RAGGED_K ? 1 : 2;
   static constexpr int kA = BM * BK * 2;                         // 16 KB
@@ -58,8 +65,8 @@ struct Smem {
   static constexpr int kStg = 32 * 128;                          // 4 KB per staging buffer
   static constexpr int kOffB = kStages * kA;
   static constexpr int kOffOnes = kOffB + kStages * kB;                       // ragged-K: 64x64 bf16 ones tile
-  static constexpr int kOffStg = kOffOnes + (MODE == MODE_RAGGED_K ? 8192 : 0);
-  static constexpr int kOffBias = kOffStg + kEpiWarps * kStgBufs * kStg;      // 64 fp32 per epilogue warp
+  static constexpr int kOffStg = kStgAlias ? 0 : kOffOnes + (MODE == MODE_RAGGED_K ? 8192 : 0);
+  static constexpr int kOffBias = (kStgAlias ? kOffOnes + 8192 : kOffStg + kEpiWarps * kStgBufs * kStg);
   static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
   static constexpr int kOffSeg = kOffBar + 256;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 12 + 1024;   // + barriers + group table + alignment slack
@@ -98,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* sdone = tempty + 2;            // staging drained (aliased staging only)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdone + 1);
   int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
 
   const int warp = threadIdx.x >> 5;
@@ -125,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps * 32); }
+    mbar_init(sdone, kEpiWarps);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, S::kTmemCols);
@@ -168,9 +177,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int itp = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++itp) {
         int g, r0, c0, kb0, nkb;
         decode(tile, g, r0, c0, kb0, nkb);
+        if (S::kStgAlias && itp > 0) mbar_wait(sdone, (uint32_t)((itp - 1) & 1));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], S::kA + S::kB);
@@ -367,6 +378,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (S::kStgAlias) {
+        if (lane == 0) {
+          bulk_wait_read<0>();            // staging (= stage slots) read by the TMA stores
+          mbar_arrive(sdone);
+        }
+      }
     }
     if (lane == 0) bulk_wait<0>();
   }
