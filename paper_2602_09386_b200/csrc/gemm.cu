@@ -100,13 +100,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + S::kOffB;
   uint8_t* sOnes = smem + S::kOffOnes;
-  uint8_t* sStg = smem + S::kOffStg;
+  uint8_t* sStg = smem + S::kOffStg;       // (re-pointed below for the aliased ragged-K layout)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* sdone = tempty + 2;            // staging drained (aliased staging only)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sdone + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
 
   const int warp = threadIdx.x >> 5;
@@ -133,7 +132,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], kEpiWarps * 32); }
-    mbar_init(sdone, kEpiWarps);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, S::kTmemCols);
@@ -152,6 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     j_tiles = (args.N + BN - 1) / BN;
     num_tiles = args.G * i_tiles * j_tiles;
   }
+  // ring depth and store staging of the ragged-K BN = 256 layout (see Smem)
+  const bool one_tile = num_tiles <= (int)gridDim.x;
+  const int nst = (S::kStgAlias && !one_tile) ? kStages - 1 : kStages;
+  if (S::kStgAlias) sStg = one_tile ? smem : smem + S::kOffB + (kStages - 1) * S::kB;
   // decode: (group, row0 of A / i0, n0 / j0, k-block range)
   auto decode = [&](int tile, int& g, int& r0, int& c0, int& kb0, int& nkb) {
     if (MODE == MODE_RAGGED_M) {
@@ -177,11 +179,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
-      int itp = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++itp) {
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int g, r0, c0, kb0, nkb;
         decode(tile, g, r0, c0, kb0, nkb);
-        if (S::kStgAlias && itp > 0) mbar_wait(sdone, (uint32_t)((itp - 1) & 1));
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], S::kA + S::kB);
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < NBBOX; ++j) tma_load_2d(b + j * 8192, &tmB, &full[stage], c0 + 64 * j, k0);
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                          (kb | k) != 0);
           }
           tc_commit(&empty[stage]);        // smem slot free once these MMAs have read it
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
         }
         tc_commit(&tfull[acc]);            // accumulator ready (also fires for nkb == 0)
       }
@@ -378,12 +378,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (S::kStgAlias) {
-        if (lane == 0) {
-          bulk_wait_read<0>();            // staging (= stage slots) read by the TMA stores
-          mbar_arrive(sdone);
-        }
-      }
     }
     if (lane == 0) bulk_wait<0>();
   }
