@@ -458,6 +458,18 @@ class SMESEngine:
         n_layers = len(self.p.layers)
         fused = getattr(self, "_fused_bwd", False)
         folded = fused and self._folded
+        # The router backward needs only dz and h: it runs on a side stream next to the expert
+        # backward, whose wgrad GEMMs leave SMs idle (128 tiles on 148 SMs); joins before unpermute.
+        side = fused
+        if side:
+            main = torch.cuda.current_stream(self.dev)
+            if not hasattr(self, "_side"):
+                self._side = torch.cuda.Stream(self.dev)
+                self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
+            self._ev_fork.record(main)
+            self._side.wait_event(self._ev_fork)
+            self._router_backward(self._side.cuda_stream)
+            self._ev_join.record(self._side)
         top = n_layers - 1             # first pool handled by the generic dgrad/wgrad loop
         if folded:
             # the last (identity) pool through the folded heads (csrc/fold.cu):
@@ -542,19 +554,10 @@ class SMESEngine:
         if not (folded and (n_layers == 1 or self.fuse_mlp)):
             _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
                     ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
-        # router: dh_r = dz W_r ; dW_r = dz^T h ; db_r = colsum(dz)
-        _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
-             ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
-        rb_fused = self.fuse_rb and getattr(self, "_fused_bwd", False)
-        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits,
-                T * E, d, ptr(self.seg_router_split), ptr(self.rw_part), None if rb_fused else ptr(self.rb_part), s)
-        _tagged("router_wgrad", "smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d,
-                ptr(self.g_router_w), s)
-        if rb_fused:
-            pass                          # reduced by post_combine
+        if side:
+            main.wait_event(self._ev_join)
         else:
-            _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
-                    ptr(self.g_router_b), s)
+            self._router_backward(s)
         _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
              ptr(self.dh_router), ptr(self.d_hidden), s)
         if not getattr(self, "_fused_bwd", False):
@@ -562,6 +565,20 @@ class SMESEngine:
                     ptr(self.g_head_w), s)
         if not getattr(self, "_fused_bwd", False):
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
+
+    def _router_backward(self, s):
+        """dh_r = dz W_r ; dW_r = dz^T h (split-K + fixed-order reduce) ; db_r = colsum(dz)."""
+        T, E, B, d = self.T, self.E, self.B, self.d
+        _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
+                ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
+        rb_fused = self.fuse_rb and getattr(self, "_fused_bwd", False)
+        _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits,
+                T * E, d, ptr(self.seg_router_split), ptr(self.rw_part), None if rb_fused else ptr(self.rb_part), s)
+        _tagged("router_wgrad", "smes_part_reduce", ptr(self.rw_part), self.rw_splits, T * E * d,
+                ptr(self.g_router_w), s)
+        if not rb_fused:                  # else reduced by post_combine
+            _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
+                    ptr(self.g_router_b), s)
 
     def step(self):
         self.forward_a(fold=self.can_fold, finalize_stats=True)
