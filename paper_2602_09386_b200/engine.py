@@ -468,8 +468,8 @@ class SMESEngine:
                 self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
             self._ev_fork.record(main)
             self._side.wait_event(self._ev_fork)
-            self._router_backward(self._side.cuda_stream)
-            self._ev_join.record(self._side)
+            if not folded:
+                self._router_backward(self._side.cuda_stream)
         top = n_layers - 1             # first pool handled by the generic dgrad/wgrad loop
         if folded:
             # the last (identity) pool through the folded heads (csrc/fold.cu):
@@ -493,23 +493,11 @@ class SMESEngine:
             else:
                 _tagged(f"fc{L}_dgrad_folded", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.G_fold),
                         E, di, self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
-            if self.q_swapped:
-                # Q_e = C_e^T H_e and csum_e = colsum(C_e) in one ragged-K GEMM (csum via the ones tile)
-                _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(inp),
-                        self.ld_in[L - 1], R, E, self.ldg, di, ptr(self.seg_pad), ptr(self.Qe), ptr(self.csum_q), s)
-                cs, cs_es = self.csum_q, self.ldg
+            if side:      # Q = C^T H and the unfold need only C and H: next to the dgrad chain
+                self._last_pool_wgrad(self._side.cuda_stream, inp, di)
+                self._router_backward(self._side.cuda_stream)
             else:
-                _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm),
-                        self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None, s)
-                if self.fuse_b_last:
-                    cs, cs_es = self.csum, T          # reduced by post_combine
-                else:
-                    cs, cs_es = self.Qe[:, di, :], self.q_rows * self.ldg
-            gw, gb = self.g_layers[L - 1]
-            qes, qts, qks = self.q_strides
-            _tagged("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), qes, qts, qks,
-                    ptr(cs), cs_es, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw),
-                    ptr(gb), ptr(self.fold_work), ptr(self.g_head_w), s)
+                self._last_pool_wgrad(s, inp, di)
             top = n_layers - 2
         elif fused:
             # d_packed = C head_W (K = T padded to 16), relu mask of O if the last pool is relu
@@ -555,6 +543,7 @@ class SMESEngine:
             _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
                     ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
         if side:
+            self._ev_join.record(self._side)       # after every side-stream launch of this pass
             main.wait_event(self._ev_join)
         else:
             self._router_backward(s)
@@ -565,6 +554,28 @@ class SMESEngine:
                     ptr(self.g_head_w), s)
         if not getattr(self, "_fused_bwd", False):
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
+
+    def _last_pool_wgrad(self, s, inp, di):
+        """Folded last pool's weight gradients: Q_e = H_e^T C_e (ragged-K), then dW / db / dW_head
+        from Q and the per-(expert, task) sums of C (csrc/fold.cu)."""
+        T, E, R, L = self.T, self.E, self.rows_cap, len(self.p.layers)
+        if self.q_swapped:
+            # Q_e = C_e^T H_e and csum_e = colsum(C_e) in one ragged-K GEMM (csum via the ones tile)
+            _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(inp),
+                    self.ld_in[L - 1], R, E, self.ldg, di, ptr(self.seg_pad), ptr(self.Qe), ptr(self.csum_q), s)
+            cs, cs_es = self.csum_q, self.ldg
+        else:
+            _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm),
+                    self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None, s)
+            if self.fuse_b_last:
+                cs, cs_es = self.csum, T          # reduced by post_combine
+            else:
+                cs, cs_es = self.Qe[:, di, :], self.q_rows * self.ldg
+        gw, gb = self.g_layers[L - 1]
+        qes, qts, qks = self.q_strides
+        _tagged("unfold", "smes_unfold_grads", E, T, self.ldg, self.d_out, di, ptr(self.Qe), qes, qts, qks,
+                ptr(cs), cs_es, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw),
+                ptr(gb), ptr(self.fold_work), ptr(self.g_head_w), s)
 
     def _router_backward(self, s):
         """dh_r = dz W_r ; dW_r = dz^T h (split-K + fixed-order reduce) ; db_r = colsum(dz)."""
