@@ -46,7 +46,8 @@ class DataParallelStep:
 
     def _part_b(self):
         self.eng.forward_b(with_loss=True, batch_times_tasks=float(self.b_global * self.eng.T), train=True,
-                           batch_scale=self.b_local, lb_batch=self.b_local, stats_done=self.world == 1)
+                           batch_scale=self.b_local, lb_batch=self.b_local, stats_done=self.world == 1,
+                           defer_reduce=True)
         self.eng.backward(batch_scale=self.b_local, lb_batch=self.b_local)
 
     def capture(self, warmup: int = 1):

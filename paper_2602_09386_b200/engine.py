@@ -368,10 +368,13 @@ class SMESEngine:
         self.experts_forward(s, fold=fold, store_hidden=store_hidden, refold=refold)
 
     def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
-                  batch_scale: int | None = None, lb_batch: int | None = None, stats_done: bool = False):
+                  batch_scale: int | None = None, lb_batch: int | None = None, stats_done: bool = False,
+                  defer_reduce: bool = False):
         """LoadStats finalize (global B*T under data parallelism) -> combine + heads + loss.
         ``train`` (sparse LB reading) fuses the combine backward into the same pass.
-        ``stats_done``: forward_a(finalize_stats=True) already finalized the local statistics."""
+        ``stats_done``: forward_a(finalize_stats=True) already finalized the local statistics.
+        ``defer_reduce`` (training steps that call backward next): the post-combine reductions
+        (loss, sums of C, bias grads) are issued by backward, on its side stream."""
         s = self._stream()
         T, E, B = self.T, self.E, self.B
         if not stats_done:
@@ -386,10 +389,9 @@ class SMESEngine:
                     ptr(self.P), self.ldp, ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam),
                     ptr(self.loss_part), 1.0 / bs, ptr(self.Cm), self.ldc, ptr(self.dz), ptr(self.freq32), lb_coef,
                     ptr(self.part_db), ptr(self.part_csum), ptr(self.part_rb), self.grid, s)
-            # loss, per-(expert, task) sums of C, router / head bias grads: one reduction launch
-            _tagged("post_combine", "smes_post_combine", self.grid, ptr(self.part_csum), E * T, ptr(self.csum),
-                    ptr(self.part_rb), T * E, ptr(self.g_router_b), ptr(self.part_db), T, ptr(self.g_head_b),
-                    ptr(self.loss_part), 1.0 / B, self.beta, self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
+            self._post_pending = True
+            if not defer_reduce:
+                self._post_combine(s)
             return
         _tagged("combine_fwd", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask), ptr(self.usize),
              ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out, ptr(self.head_w),
@@ -468,8 +470,12 @@ class SMESEngine:
                 self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
             self._ev_fork.record(main)
             self._side.wait_event(self._ev_fork)
+            if getattr(self, "_post_pending", False):
+                self._post_combine(self._side.cuda_stream)
             if not folded:
                 self._router_backward(self._side.cuda_stream)
+        elif getattr(self, "_post_pending", False):
+            self._post_combine(s)
         top = n_layers - 1             # first pool handled by the generic dgrad/wgrad loop
         if folded:
             # the last (identity) pool through the folded heads (csrc/fold.cu):
@@ -555,6 +561,14 @@ class SMESEngine:
         if not getattr(self, "_fused_bwd", False):
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
 
+    def _post_combine(self, s):
+        """Loss, per-(expert, task) sums of C, router / head bias grads: one reduction launch."""
+        T, E, B = self.T, self.E, self.B
+        _tagged("post_combine", "smes_post_combine", self.grid, ptr(self.part_csum), E * T, ptr(self.csum),
+                ptr(self.part_rb), T * E, ptr(self.g_router_b), ptr(self.part_db), T, ptr(self.g_head_b),
+                ptr(self.loss_part), 1.0 / B, self.beta, self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
+        self._post_pending = False
+
     def _last_pool_wgrad(self, s, inp, di):
         """Folded last pool's weight gradients: Q_e = H_e^T C_e (ragged-K), then dW / db / dW_head
         from Q and the per-(expert, task) sums of C (csrc/fold.cu)."""
@@ -593,7 +607,7 @@ class SMESEngine:
 
     def step(self):
         self.forward_a(fold=self.can_fold, finalize_stats=True)
-        self.forward_b(with_loss=True, train=True, stats_done=True)
+        self.forward_b(with_loss=True, train=True, stats_done=True, defer_reduce=True)
         self.backward()
 
     # ------------------------------------------------------------------ accounting

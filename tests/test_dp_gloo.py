@@ -47,7 +47,7 @@ class OracleEngine:
         self.stats_raw[2 * self.E:] = torch.tensor(r.full_probs.sum(axis=(0, 1)))
 
     def forward_b(self, with_loss=True, batch_times_tasks=None, train=False, batch_scale=None, lb_batch=None,
-                  stats_done=False):
+                  stats_done=False, defer_reduce=False):
         raw = self.stats_raw.numpy()
         bt = batch_times_tasks
         freq, mass = raw[: self.E] / bt, raw[self.E: 2 * self.E] / bt
