@@ -463,11 +463,13 @@ class SMESEngine:
         # The router backward needs only dz and h: it runs on a side stream next to the expert
         # backward, whose wgrad GEMMs leave SMs idle (128 tiles on 148 SMs); joins before unpermute.
         side = fused
+        unpermute_side = False
         if side:
             main = torch.cuda.current_stream(self.dev)
             if not hasattr(self, "_side"):
                 self._side = torch.cuda.Stream(self.dev)
                 self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
+                self._ev_dx = torch.cuda.Event()
             self._ev_fork.record(main)
             self._side.wait_event(self._ev_fork)
             if getattr(self, "_post_pending", False):
@@ -491,6 +493,9 @@ class SMESEngine:
                 _tagged("mlp_dgrad", "smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), self.ldg,
                         ptr(self.w_bf[0]), E, d, di, ptr(self.seg_pad), ptr(mask), R, ptr(self.dX), d,
                         None if self.fuse_wgrad else ptr(dst), di, s)
+                if side:      # dX is final here: the un-permute can run on the side stream
+                    self._ev_dx.record(main)
+                    unpermute_side = True
                 if self.fuse_wgrad:
                     gw0, gb0 = self.g_layers[0]
                     _tagged("mlp_wgrad", "smes_mlp_wgrad", ptr(self.Cm), self.ldc, R, ptr(self.G_fold), self.ldg,
@@ -501,7 +506,7 @@ class SMESEngine:
                         E, di, self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
             if side:      # Q = C^T H and the unfold need only C and H: next to the dgrad chain
                 self._last_pool_wgrad(self._side.cuda_stream, inp, di)
-                self._router_backward(self._side.cuda_stream)
+                self._router_backward(self._side.cuda_stream, self._ev_dx if unpermute_side else None)
             else:
                 self._last_pool_wgrad(s, inp, di)
             top = n_layers - 2
@@ -553,8 +558,8 @@ class SMESEngine:
             main.wait_event(self._ev_join)
         else:
             self._router_backward(s)
-        _tagged("unpermute", "smes_unpermute", B, d, ptr(self.usize), ptr(self.row_of), self.umax, ptr(self.dX), d,
-             ptr(self.dh_router), ptr(self.d_hidden), s)
+        if not unpermute_side:
+            self._unpermute(s)
         if not getattr(self, "_fused_bwd", False):
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_dw), self.grid, T * self.d_out,
                     ptr(self.g_head_w), s)
@@ -591,11 +596,21 @@ class SMESEngine:
                 ptr(cs), cs_es, ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(gw),
                 ptr(gb), ptr(self.fold_work), ptr(self.g_head_w), s)
 
-    def _router_backward(self, s):
-        """dh_r = dz W_r ; dW_r = dz^T h (split-K + fixed-order reduce) ; db_r = colsum(dz)."""
+    def _unpermute(self, s):
+        """d_hidden[b] = dh_router[b] + sum of the instance's packed dX rows (training.py:192, 209-212)."""
+        _tagged("unpermute", "smes_unpermute", self.B, self.d, ptr(self.usize), ptr(self.row_of), self.umax,
+                ptr(self.dX), self.d, ptr(self.dh_router), ptr(self.d_hidden), s)
+
+    def _router_backward(self, s, dx_ready=None):
+        """dh_r = dz W_r ; dW_r = dz^T h (split-K + fixed-order reduce) ; db_r = colsum(dz).
+        ``dx_ready``: an event after which dX is final -- the un-permute then runs here, between
+        the router dgrad and wgrad (side-stream schedule of backward)."""
         T, E, B, d = self.T, self.E, self.B, self.d
         _tagged("router_dgrad", "smes_gemm_ragged_m", ptr(self.dz), T * E, self.B_pad, ptr(self.wr_bf), 1, d, T * E, 1,
                 ptr(self.seg_router), None, 0, None, None, 0, ptr(self.dh_router), d, 1, B, s)
+        if dx_ready is not None:
+            self._side.wait_event(dx_ready)
+            self._unpermute(s)
         rb_fused = self.fuse_rb and getattr(self, "_fused_bwd", False)
         _tagged("router_wgrad", "smes_gemm_ragged_k", ptr(self.dz), T * E, ptr(self.h), self.ldh, B, self.rw_splits,
                 T * E, d, ptr(self.seg_router_split), ptr(self.rw_part), None if rb_fused else ptr(self.rb_part), s)
