@@ -867,14 +867,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(sC + s * 16384, &tmC, &cfull[s], 0, r0);                   // box {64 t, 128 rows}
         }
         for (int c = 0; c < NC; ++c) {
-          {
-            const int s = slot_of(gi, S::kGS);
-            mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
-            mbar_expect_tx(&gfull[s], 4096);
-            tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);            // box {64 f, 16 t, 1}
-            tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
-            ++gi;
-          }
           for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
             const int s = slot_of(wi, S::kWS);
             mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
@@ -883,6 +875,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < DK; ++j)                                          // box {64 j, 64 f, 1}
               tma_load_3d(sW + s * S::kWB + j * 8192, &tmW1, &wfull[s], 64 * j, c * CH + kb * 64, e);
           }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ================= G producer: released by the S-MMA.  In the W1 producer's order a G chunk
+      // queued behind W1 k-blocks and held the in-order MMA issuer (S-MMA before dX-MMA) back
+      int gi = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int e = find_group(seg_s, a.E, tile * BM);
+        for (int c = 0; c < NC; ++c, ++gi) {
+          const int s = slot_of(gi, S::kGS);
+          mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+          mbar_expect_tx(&gfull[s], 4096);
+          tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);              // box {64 f, 16 t, 1}
+          tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
         }
       }
     }
@@ -907,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      idS, 0u);
           tc_commit(&sfull[sb]);
           tc_commit(&gempty[gs]);
+          EV(0, si);
           ++gi; ++si;
         };
         s_mma(0);
@@ -915,8 +924,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (c == NC - 1) tc_commit(&cempty[cs]);
           const int hb = hi & 1;
           mbar_wait(&hfull[hb], (uint32_t)((hi >> 1) & 1));
+          EV(1, hi);
           // the dX accumulator must be drained by the previous tile's epilogue
           if (c == 0) mbar_wait(dempty, (uint32_t)((it & 1) ^ 1));
+          EV(2, hi);
           tc_fence_after();
           const uint32_t h_addr = smem_u32(sH + hb * 32768);
           for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
@@ -931,6 +942,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_commit(&wempty[ws]);
           }
           tc_commit(&hempty[hb]);
+          EV(3, hi);
           ++hi;
         }
         tc_commit(dfull);
@@ -981,15 +993,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(dempty);
       d_it = -1;
     };
+    // relu-mask words of the next chunk are fetched one chunk ahead: the S-MMA (K = T) is always
+    // ready first, so a mask load issued at the chunk start stalled the epilogue ~1.5 k cycles
+    uint32_t nm0 = 0u, nm1 = 0u;
+    auto fetch_mask = [&](int tile, int c) {
+      if (tile < num_tiles) {
+        const int rr = tile * BM + 32 * q + lane, nn = c * CH + par * 64;
+        nm0 = __ldg(&a.bits[(size_t)(nn >> 5) * a.bits_ld + rr]);
+        nm1 = __ldg(&a.bits[(size_t)((nn >> 5) + 1) * a.bits_ld + rr]);
+      }
+    };
+    fetch_mask(blockIdx.x, 0);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int r0 = tile * BM;
       const int row = r0 + 32 * q + lane;
       for (int c = 0; c < NC; ++c, ++si) {
         const int n0 = c * CH + par * 64;
-        const uint32_t m0 = __ldg(&a.bits[(size_t)(n0 >> 5) * a.bits_ld + row]);
-        const uint32_t m1 = __ldg(&a.bits[(size_t)((n0 >> 5) + 1) * a.bits_ld + row]);
+        const uint32_t m0 = nm0, m1 = nm1;
+        if (c + 1 < NC) fetch_mask(tile, c + 1); else fetch_mask(tile + gridDim.x, 0);
         const int sb = si & 1;
         mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
+        if (warp == 4 && lane == 0) EV(4, si);
         tc_fence_after();
         float f[64];
         {
@@ -1007,8 +1031,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);
+        if (warp == 4 && lane == 0) EV(5, si);
         const int hb = hi & 1;
         mbar_wait(&hempty[hb], (uint32_t)(((hi >> 1) & 1) ^ 1));
+        if (warp == 4 && lane == 0) EV(6, si);
         if (lane == 0) bulk_wait_read<0>();     // own dH / dX-staging stores out of this buffer
         __syncwarp();
         uint8_t* hbuf = sH + hb * 32768;
@@ -1027,6 +1053,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             bulk_commit();
           }
           mbar_arrive(&hfull[hb]);
+          if (warp == 4) EV(7, si);
         }
         ++hi;
         if (c == 0 && d_it >= 0) drain();      // previous tile's dX
