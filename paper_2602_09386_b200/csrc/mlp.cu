@@ -1186,13 +1186,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (valid) tma_load_2d_2sm(sC + s * 16384, &tmC, &cfull[s], 0, r0);
         }
         for (int c = 0; c < NC; ++c) {
-          {
-            const int s = slot_of(gi, S::kGS);
-            mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
-            if (rank == 0) mbar_expect_tx(&gfull[s], 2 * 2048);
-            tma_load_3d_2sm(sG + s * 2048, &tmG, &gfull[s], c * CH + 64 * rank, 0, e);
-            ++gi;
-          }
           for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
             const int s = slot_of(wi, S::kWS);
             mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1);
@@ -1202,6 +1195,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tma_load_3d_2sm(sW + s * S::kWB + j * 8192, &tmW1, &wfull[s], 64 * (j + rank * (DK / 2)),
                               c * CH + kb * 64, e);
           }
+        }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ================= G producer (both CTAs, own half): off the W1 stream (see mlp_dgrad)
+      int gi = 0;
+      for (int u = cl; u < num_units; u += ncl) {
+        int e, rp, nt;
+        decode(u, e, rp, nt);
+        for (int c = 0; c < NC; ++c, ++gi) {
+          const int s = slot_of(gi, S::kGS);
+          mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1);
+          if (rank == 0) mbar_expect_tx(&gfull[s], 2 * 2048);
+          tma_load_3d_2sm(sG + s * 2048, &tmG, &gfull[s], c * CH + 64 * rank, 0, e);
         }
       }
     }
@@ -1260,6 +1268,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t lead_hfull = mapa_shared(smem_u32(hfull), 0);
     const uint32_t lead_dempty = mapa_shared(smem_u32(dempty), 0);
     int si = 0, hi = 0, it = 0;
+    // relu-mask words fetched one chunk ahead (see mlp_dgrad)
+    uint32_t nm0 = 0u, nm1 = 0u;
+    auto fetch_mask = [&](int u, int c) {
+      nm0 = nm1 = 0u;
+      if (u < num_units) {
+        int e2, rp2, nt2;
+        decode(u, e2, rp2, nt2);
+        if ((int)rank < nt2) {
+          const int rr = rp2 + (int)rank * BM + 32 * q + lane, nn = c * CH + par * 64;
+          nm0 = __ldg(&a.bits[(size_t)(nn >> 5) * a.bits_ld + rr]);
+          nm1 = __ldg(&a.bits[(size_t)((nn >> 5) + 1) * a.bits_ld + rr]);
+        }
+      }
+    };
+    fetch_mask(cl, 0);
     for (int u = cl; u < num_units; u += ncl, ++it) {
       int e, rp, nt;
       decode(u, e, rp, nt);
@@ -1268,8 +1291,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = r0 + 32 * q + lane;
       for (int c = 0; c < NC; ++c, ++si) {
         const int n0 = c * CH + par * 64;
-        const uint32_t m0 = valid ? __ldg(&a.bits[(size_t)(n0 >> 5) * a.bits_ld + row]) : 0u;
-        const uint32_t m1 = valid ? __ldg(&a.bits[(size_t)((n0 >> 5) + 1) * a.bits_ld + row]) : 0u;
+        const uint32_t m0 = nm0, m1 = nm1;
+        if (c + 1 < NC) fetch_mask(u, c + 1); else fetch_mask(u + ncl, 0);
         const int sb = si & 1;
         mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
         tc_fence_after();
