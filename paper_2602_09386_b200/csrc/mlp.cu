@@ -689,6 +689,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       p_e = -1;
     };
+    // fc1 bias of the next chunk fetched one chunk ahead (see mlp_fwd)
+    float nb0 = 0.f, nb1 = 0.f;
+    auto fetch_bias = [&](int u, int c) {
+      if (u < num_units) {
+        int e2, rp2, nt2;
+        decode(u, e2, rp2, nt2);
+        const float* bp = a.b1 + (size_t)e2 * a.d_ff + c * CH + par * 64 + lane;
+        nb0 = __ldg(bp);
+        nb1 = __ldg(bp + 32);
+      }
+    };
+    fetch_bias(cl, 0);
     for (int u = cl; u < num_units; u += ncl, ++it) {
       int e, rp, nt;
       decode(u, e, rp, nt);
@@ -697,8 +709,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const int row = r0 + 32 * q + lane;
       for (int c = 0; c < NC; ++c, ++si) {
         const int n0 = c * CH + par * 64;
-        const float bv0 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + lane);
-        const float bv1 = __ldg(a.b1 + (size_t)e * a.d_ff + n0 + 32 + lane);
+        const float bv0 = nb0, bv1 = nb1;
+        if (c + 1 < NC) fetch_bias(u, c + 1); else fetch_bias(u + ncl, 0);
         const int sb = si & 1;
         mbar_wait(&sfull[sb], (uint32_t)((si >> 1) & 1));
         if (warp == 4 && lane == 0) EV(2, si);
