@@ -188,18 +188,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ================= TMA producer: X tiles and W1 k-blocks (G: warp 2)
-      int xi = 0, wi = 0;
+    if (lane == 1) {
+      // ================= X producer (lane 1): its own thread, so the next tile's W1 k-blocks do
+      // not queue behind X loads that wait for the current tile's last chunk
+      int xi = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int r0 = tile * BM;
-        const int e = find_group(seg_s, a.E, r0);
         for (int kb = 0; kb < DK; ++kb, ++xi) {
           const int s = slot_of(xi, S::kXS);
           TW(0, mbar_wait(&xempty[s], par_of(xi, S::kXS) ^ 1));
           mbar_expect_tx(&xfull[s], 16384);
-          tma_load_2d(sX + s * 16384, &tmX, &xfull[s], kb * 64, r0);          // box {64 k, 128 rows}
+          tma_load_2d(sX + s * 16384, &tmX, &xfull[s], kb * 64, tile * BM);   // box {64 k, 128 rows}
         }
+      }
+    } else if (lane == 0) {
+      // ================= W1 producer (lane 0; G: warp 2)
+      int wi = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int r0 = tile * BM;
+        const int e = find_group(seg_s, a.E, r0);
         for (int c = 0; c < NC; ++c) {
           for (int kb = 0; kb < DK; ++kb, ++wi) {
             const int s = slot_of(wi, S::kWS);
