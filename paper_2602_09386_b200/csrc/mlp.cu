@@ -874,7 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int ci = 0, gi = 0, wi = 0;
+      int ci = 0, wi = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ci) {
         const int r0 = tile * BM;
         const int e = find_group(seg_s, a.E, r0);
@@ -1024,7 +1024,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     fetch_mask(blockIdx.x, 0);
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int r0 = tile * BM;
-      const int row = r0 + 32 * q + lane;
       for (int c = 0; c < NC; ++c, ++si) {
         const int n0 = c * CH + par * 64;
         const uint32_t m0 = nm0, m1 = nm1;
@@ -1191,7 +1190,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      int ci = 0, gi = 0, wi = 0;
+      int ci = 0, wi = 0;
       for (int u = cl; u < num_units; u += ncl, ++ci) {
         int e, rp, nt;
         decode(u, e, rp, nt);
@@ -1306,7 +1305,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       decode(u, e, rp, nt);
       const bool valid = (int)rank < nt;
       const int r0 = rp + (int)rank * BM;
-      const int row = r0 + 32 * q + lane;
       for (int c = 0; c < NC; ++c, ++si) {
         const int n0 = c * CH + par * 64;
         const uint32_t m0 = nm0, m1 = nm1;

@@ -19,7 +19,6 @@ namespace smes {
 
 constexpr int RT_WARPS = 4;
 constexpr int RT_MAX_E = 1024;
-constexpr int RT_MAX_EPL = RT_MAX_E / 32;
 
 struct RouteArgs {
   const float* z;          // logits, element (t,b,e) at z[t*st + b*sb + e]
@@ -383,7 +382,6 @@ __global__ void __launch_bounds__(RT_WARPS * 32, SMES_TG_MINB) route_tg_kernel(c
   const int t = lane / L, q = lane % L;
   const int e0 = q * EPT;                     // first owned expert (Stage II / softmax view)
   const int p0 = e0 + t * R;                  // first owned pooled expert (after reduce-scatter)
-  const mask_t own = (EPT == 64 ? ~0ull : ((1ull << EPT) - 1ull)) << e0;
   extern __shared__ __align__(16) uint8_t sm[];
   int32_t* s_union = reinterpret_cast<int32_t*>(sm);
   int32_t* s_act = s_union + RT_WARPS * E;
@@ -589,7 +587,6 @@ __global__ void __launch_bounds__(RT_WARPS * 32, SMES_TG_MINB) route_tg_kernel(c
     s_mass[warp * E + e] = m;
     s_dmass[warp * E + e] = dm;
   }
-  (void)own;
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
     int cu = 0, ca = 0;
