@@ -357,37 +357,46 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 4) TW(9, mbar_wait(&sfull[sb], par_of(si, kSB))); else mbar_wait(&sfull[sb], par_of(si, kSB));
         if (warp == 4 && lane == 0) EV(2, si);
         tc_fence_after();
+        // the two 32-column TMEM loads are split: the second is in flight while the first half's
+        // bias / ReLU / mask run (the chunk's 64 KB TMEM drain is as long as its S-MMA)
         float f[64];
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + sb * CH + par * 64;
         {
-          uint32_t t0[32], t1[32];
-          const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + sb * CH + par * 64;
+          uint32_t t0[32];
           tmem_ld32(ta, t0);
-          tmem_ld32(ta + 32, t1);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) { f[j] = __uint_as_float(t0[j]); f[32 + j] = __uint_as_float(t1[j]); }
+          for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(t0[j]);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[sb]);       // accumulator drained into registers
-        if (warp == 4 && lane == 0) EV(3, si);
+        uint32_t t1[32];
+        tmem_ld32(ta + 32, t1);
         sbias[lane] = bv0;
         sbias[32 + lane] = bv1;
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
-          const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
-          f[j] = fmaxf(f[j] + bb.x, 0.f);
-          f[j + 1] = fmaxf(f[j + 1] + bb.y, 0.f);
-          f[j + 2] = fmaxf(f[j + 2] + bb.z, 0.f);
-          f[j + 3] = fmaxf(f[j + 3] + bb.w, 0.f);
+        for (int hh = 0; hh < 2; ++hh) {
+          if (hh == 1) {
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[32 + j] = __uint_as_float(t1[j]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sempty[sb]);   // accumulator drained into registers
+            if (warp == 4 && lane == 0) EV(3, si);
+          }
+#pragma unroll
+          for (int j = 32 * hh; j < 32 * hh + 32; j += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
+            f[j] = fmaxf(f[j] + bb.x, 0.f);
+            f[j + 1] = fmaxf(f[j + 1] + bb.y, 0.f);
+            f[j + 2] = fmaxf(f[j + 2] + bb.z, 0.f);
+            f[j + 3] = fmaxf(f[j + 3] + bb.w, 0.f);
+          }
+          const uint32_t w = pos_mask32(f + hh * 32);
+          if (a.bits != nullptr) a.bits[(size_t)((n0 >> 5) + hh) * a.bits_ld + row] = w;
         }
         if (warp == 4 && lane == 0) EV(8, si);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const uint32_t w = pos_mask32(f + h * 32);
-          if (a.bits != nullptr) a.bits[(size_t)((n0 >> 5) + h) * a.bits_ld + row] = w;
-        }
+        if (warp == 4 && lane == 0) EV(9, si);
         if (warp == 4 && lane == 0) EV(9, si);
         // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
         if (warp == 4) TW(10, mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1))); else mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
