@@ -1109,9 +1109,9 @@ struct Dg2Smem {
   static constexpr int kOffC = 0;
   static constexpr int kOffG = kOffC + kCS * 16384;
   static constexpr int kOffW = kOffG + kGS * 2048;
+  // dH double buffer; the dX store staging aliases the buffer the next chunk writes (see mlp_dgrad)
   static constexpr int kOffH = kOffW + kWS * kWB;
-  static constexpr int kOffStg = kOffH + 32768;
-  static constexpr int kOffBar = kOffStg + kEpiWarps * 4096;
+  static constexpr int kOffBar = kOffH + 2 * 32768;
   static constexpr int kOffSeg = kOffBar + 512;
   static constexpr int kBytes = kOffSeg + 2 * 257 * 4 + 1024;
   static_assert(kBytes <= 232448, "mlp_dgrad2 smem");
@@ -1130,7 +1130,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sG = smem + S::kOffG;
   uint8_t* sW = smem + S::kOffW;
   uint8_t* sH = smem + S::kOffH;
-  uint8_t* sStg = smem + S::kOffStg;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* cfull = bar;
   uint64_t* cempty = cfull + S::kCS;
@@ -1140,9 +1139,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint64_t* wempty = wfull + S::kWS;
   uint64_t* sfull = wempty + S::kWS;       // [2]
   uint64_t* sempty = sfull + 2;            // [2] (leader: 16)
-  uint64_t* hfull = sempty + 2;            // [1] (leader: 16)
-  uint64_t* hempty = hfull + 1;
-  uint64_t* dfull = hempty + 1;
+  uint64_t* hfull = sempty + 2;            // [2] (leader: 16)
+  uint64_t* hempty = hfull + 2;            // [2]
+  uint64_t* dfull = hempty + 2;
   uint64_t* dempty = dfull + 1;            // (leader: 16)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dempty + 1);
   int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
@@ -1169,8 +1168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int i = 0; i < S::kGS; ++i) { mbar_init(&gfull[i], 1); mbar_init(&gempty[i], 1); }
     for (int i = 0; i < S::kWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 2 * kEpiWarps); }
-    mbar_init(hfull, 2 * kEpiWarps);
-    mbar_init(hempty, 1);
+    for (int i = 0; i < 2; ++i) { mbar_init(&hfull[i], 2 * kEpiWarps); mbar_init(&hempty[i], 1); }
     mbar_init(dfull, 1);
     mbar_init(dempty, 2 * kEpiWarps);
     fence_mbar_init();
@@ -1264,10 +1262,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int c = 0; c < NC; ++c) {
           if (c + 1 < NC) s_mma(c + 1);
           if (c == NC - 1) tc_commit_2sm_mc(&cempty[cs], kPair);
-          mbar_wait(hfull, (uint32_t)(hi & 1));
+          const int hb = hi & 1;
+          mbar_wait(&hfull[hb], (uint32_t)((hi >> 1) & 1));
           if (c == 0) mbar_wait(dempty, (uint32_t)((it & 1) ^ 1));
           tc_fence_after();
-          const uint32_t h_addr = smem_u32(sH);
+          const uint32_t h_addr = smem_u32(sH + hb * 32768);
           for (int kb = 0; kb < CH / 64; ++kb, ++wi) {
             const int ws = slot_of(wi, S::kWS);
             mbar_wait(&wfull[ws], par_of(wi, S::kWS));
@@ -1279,7 +1278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                              umma_desc_sw128(w_addr + k * 2048, 8192, 1024), idD, (c | kb | k) != 0);
             tc_commit_2sm_mc(&wempty[ws], kPair);
           }
-          tc_commit_2sm_mc(hempty, kPair);
+          tc_commit_2sm_mc(&hempty[hb], kPair);
           ++hi;
         }
         tc_commit_2sm_mc(dfull, kPair);
@@ -1288,12 +1287,54 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int par = (warp - 4) >> 2;
-    uint8_t* stg = sStg + (warp - 4) * 4096;
     const uint32_t lead_sempty0 = mapa_shared(smem_u32(&sempty[0]), 0);
     const uint32_t lead_sempty1 = mapa_shared(smem_u32(&sempty[1]), 0);
-    const uint32_t lead_hfull = mapa_shared(smem_u32(hfull), 0);
+    const uint32_t lead_hfull0 = mapa_shared(smem_u32(&hfull[0]), 0);
+    const uint32_t lead_hfull1 = mapa_shared(smem_u32(&hfull[1]), 0);
     const uint32_t lead_dempty = mapa_shared(smem_u32(dempty), 0);
     int si = 0, hi = 0, it = 0;
+    // dX of a finished unit is drained after chunk 0 of the next unit (see mlp_dgrad); staging in
+    // the dH buffer the next chunk writes
+    int d_it = -1, d_r0 = 0;
+    bool d_valid = false;
+    auto drain = [&]() {
+      uint8_t* stg = sH + (hi & 1) * 32768 + (warp - 4) * 4096;
+      mbar_wait(dfull, (uint32_t)(d_it & 1));
+      tc_fence_after();
+      for (int cc = par; cc < DK; cc += 2) {
+        uint32_t t0[32], t1[32];
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;
+        tmem_ld32(ta, t0);
+        tmem_ld32(ta + 32, t1);
+        tmem_ld_wait();
+        if (cc + 2 >= DK) {   // last TMEM read of this tile: hand the accumulator back early
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(lead_dempty);
+        }
+        if (!d_valid) continue;
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t* src = k < 4 ? t0 : t1;
+          const int o = (k & 3) * 8;
+          rowp[k ^ (lane & 7)] = make_uint4(
+              pack_bf16(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
+              pack_bf16(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
+              pack_bf16(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
+              pack_bf16(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmDX, stg, cc * 64, d_r0 + 32 * q);
+          bulk_commit();
+        }
+      }
+      d_it = -1;
+    };
     // relu-mask words fetched one chunk ahead (see mlp_dgrad)
     uint32_t nm0 = 0u, nm1 = 0u;
     auto fetch_mask = [&](int u, int c) {
@@ -1337,10 +1378,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(sb ? lead_sempty1 : lead_sempty0);
-        mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
-        if (a.store_dh && lane == 0) bulk_wait_read<0>();
+        const int hb = hi & 1;
+        mbar_wait(&hempty[hb], (uint32_t)(((hi >> 1) & 1) ^ 1));
+        if (lane == 0) bulk_wait_read<0>();     // own dH / dX-staging stores out of this buffer
         __syncwarp();
-        uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
+        uint8_t* hbuf = sH + hb * 32768;
+        uint8_t* hrow = hbuf + par * 16384 + (32 * q + lane) * 128;
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
@@ -1351,48 +1394,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           if (a.store_dh && valid) {
-            tma_store_2d(&tmDH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
+            tma_store_2d(&tmDH, hbuf + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
             bulk_commit();
           }
-          mbar_arrive_cluster(lead_hfull);
+          mbar_arrive_cluster(hb ? lead_hfull1 : lead_hfull0);
         }
         ++hi;
+        if (c == 0 && d_it >= 0) drain();      // previous unit's dX (see mlp_dgrad)
       }
-      mbar_wait(dfull, (uint32_t)(it & 1));
-      tc_fence_after();
-      for (int cc = par; cc < DK; cc += 2) {
-        uint32_t t0[32], t1[32];
-        const uint32_t ta = tmem_base + ((uint32_t)(32 * q) << 16) + 256 + cc * 64;
-        tmem_ld32(ta, t0);
-        tmem_ld32(ta + 32, t1);
-        tmem_ld_wait();
-        if (cc + 2 >= DK) {   // last TMEM read of this tile: hand the accumulator back early
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(lead_dempty);
-        }
-        if (!valid) continue;
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint32_t* src = k < 4 ? t0 : t1;
-          const int o = (k & 3) * 8;
-          rowp[k ^ (lane & 7)] = make_uint4(
-              pack_bf16(__uint_as_float(src[o]), __uint_as_float(src[o + 1])),
-              pack_bf16(__uint_as_float(src[o + 2]), __uint_as_float(src[o + 3])),
-              pack_bf16(__uint_as_float(src[o + 4]), __uint_as_float(src[o + 5])),
-              pack_bf16(__uint_as_float(src[o + 6]), __uint_as_float(src[o + 7])));
-        }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&tmDX, stg, cc * 64, r0 + 32 * q);
-          bulk_commit();
-        }
-      }
+      d_it = it; d_r0 = r0; d_valid = valid;
     }
+    if (d_it >= 0) drain();
     if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
