@@ -359,7 +359,7 @@ def run_dp(args, c, world, rank, local, dev):
             "config": {"workload": c["workload"], "global_batch": world * B, "per_gpu_batch": B,
                        "parallelism": f"dp{world}", "n_act_rows": n_act, "mean_union": n_act / B,
                        "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)",
-                       "graph": "fwd+bwd captured as 2 CUDA graphs around the LB-stats all-reduce"},
+                       "graph": ("fwd+bwd in one CUDA graph" if world == 1 else "fwd+bwd captured as 2 CUDA graphs around the LB-stats all-reduce")},
             "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "step_tflops": round(step_tflops, 1), "kernels": breakdown}

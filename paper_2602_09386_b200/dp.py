@@ -58,7 +58,15 @@ class DataParallelStep:
             for _ in range(warmup):
                 self.step_eager()
         torch.cuda.current_stream().wait_stream(st)
-        self._ga, self._gb = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        self._ga = torch.cuda.CUDAGraph()
+        if self.world == 1:
+            # nothing to exchange between the segments: one graph, one launch per step
+            self._gb = None
+            with torch.cuda.graph(self._ga):
+                self._part_a()
+                self._part_b()
+            return
+        self._gb = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self._ga):
             self._part_a()
         with torch.cuda.graph(self._gb):
@@ -83,6 +91,8 @@ class DataParallelStep:
         if self._ga is None:
             return self.step_eager()
         self._ga.replay()
+        if self._gb is None:
+            return
         self._allreduce_stats()
         self._gb.replay()
         self._allreduce_grads()
