@@ -330,7 +330,27 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
     }
     if (lane < T) pY = a.labels[(long)lane * a.B + b];
   };
-  if (pf && blockIdx.x * CB_WARPS + warp < a.B) fetch(blockIdx.x * CB_WARPS + warp);
+  // P / freq gathers of an instance whose tables sit in registers (pUm, pRows, pAct): issued for
+  // the NEXT instance in the middle of this one, so their latency overlaps its tail
+  float gn[2] = {0.f, 0.f}, fn[2] = {0.f, 0.f};
+  auto gather_next = [&]() {
+    const uint32_t w0 = __shfl_sync(0xffffffffu, pUm[0], 0), w1 = EW > 1 ? __shfl_sync(0xffffffffu, pUm[0], 1) : 0u;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int j = lane + 32 * k;
+      const int e = pAct[k];
+      const int rank = e < 32 ? __popc(w0 & ((1u << e) - 1u)) : __popc(w0) + __popc(w1 & ((1u << (e - 32)) - 1u));
+      const int r0 = __shfl_sync(0xffffffffu, pRows[0], rank & 31), r1 = __shfl_sync(0xffffffffu, pRows[1], rank & 31);
+      if (j < TK) {
+        gn[k] = __ldg(a.P + (long)(rank < 32 ? r0 : r1) * ldp + j / K);
+        fn[k] = __ldg(a.freq + e);
+      }
+    }
+  };
+  if (pf && blockIdx.x * CB_WARPS + warp < a.B) {
+    fetch(blockIdx.x * CB_WARPS + warp);
+    gather_next();
+  }
   for (int b = blockIdx.x * CB_WARPS + warp; b < a.B; b += stride) {
     int U;
     float y = 0.f;
@@ -344,7 +364,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
         if (j < umax) s_rows[j] = pRows[k];
         if (j < TK) { s_act[j] = pAct[k]; s_w[j] = pW[k]; }
       }
-      if (b + stride < a.B) fetch(b + stride);
+      if (b + stride < a.B) fetch(b + stride);   // next instance's tables, in flight from here
     } else {
       // one round trip for every per-instance table
       U = a.usize[b];
@@ -361,7 +381,21 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
     __syncwarp();
     // logits from the head projections: logit_t = b_t + sum_k w_k P[row_k, t]; the gathers of a
     // lane's (task, slot) pairs are issued together (second and last round trip)
-    {
+    if (pf) {
+      // this instance's gathers were issued during the previous one
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int i = lane + 32 * k;
+        if (i < TK) {
+          const float w = s_w[i];
+          s_gw[i] = w * gn[k];
+          s_wf[i] = w * fn[k];
+        }
+      }
+      // next instance's gathers: its tables were fetched at the top of this iteration; the loads
+      // overlap the rest of this instance (loss, dlogit, C rows, dz)
+      if (b + stride < a.B) gather_next();
+    } else {
       constexpr int kMaxI = 4;                  // TK <= 128 per warp pass
       float gv[kMaxI], fv[kMaxI];
 #pragma unroll
