@@ -77,12 +77,37 @@ def _dist_env():
 
 # --------------------------------------------------------------------------- CPU legs
 
-CPU_SAMPLE = {"c2": 2048, "c3": 512, "c4": 1024, "c5": 128}
+# bounded CPU samples of each configuration: c2 runs the FULL 16384 batch;
+# c3 / c5 full batches need minutes and tens of GB of f64 (T,B,E) arrays per step
+CPU_SAMPLE = {"c2": 16384, "c3": 4096, "c4": 1024, "c5": 256}
+
+
+def _host_cpu():
+    """CPU model and the BLAS numpy runs on (threadpoolctl), for the cpu_baseline record."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    blas = None
+    try:
+        from threadpoolctl import threadpool_info
+        libs = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if libs:
+            b = libs[0]
+            blas = f"{b.get('internal_api')} {b.get('version')} ({b.get('num_threads')} threads)"
+    except Exception:
+        pass
+    return model, blas
 
 
 def _cpu_sample(cfg_name: str, steps: int, warm: int = 1):
     """Time the oracle port (the reference's algorithm restated in NumPy f64) on a bounded
-    sub-batch of the configuration: forward_sparse + backward (forward only for c4)."""
+    (sub-)batch of the configuration: forward_sparse + backward (forward only for c4).
+    Median of ``steps`` after ``warm`` warm-up steps (the cli.py:333-345 convention)."""
     from oracle import smes_oracle as O
     c = CONFIGS[cfg_name]
     b_sample = CPU_SAMPLE[cfg_name]
@@ -103,9 +128,13 @@ def _cpu_sample(cfg_name: str, steps: int, warm: int = 1):
     med = statistics.median(times)
     cores = len(os.sched_getaffinity(0))
     what = "forward_sparse" if fwd_only else "forward_sparse+backward"
+    full = c.get("B") == b_sample
+    model, blas = _host_cpu()
     return {"value": b_sample / med, "unit": UNIT, "cores": cores, "kind": "port",
-            "sample": f"{cfg_name} shape at B={b_sample} (sub-batch), oracle/smes_oracle.py {what}, "
-                      f"median of {steps} steps after {warm} warm-up, numpy f64 with {cores} host threads"}
+            "sample": f"{cfg_name} shape at B={b_sample} ({'the full batch' if full else 'sub-batch'}), "
+                      f"oracle/smes_oracle.py {what}, median of {steps} steps after {warm} warm-up, "
+                      f"numpy f64 with {cores} host threads",
+            "full_batch": full, "cpu_model": model, "blas": blas}
 
 
 def run_reference(args):
@@ -211,6 +240,61 @@ def _host_inputs(c, B, rank):
     rates = torch.tensor(np.resize([0.3, 0.1, 0.05, 0.2], c["T"]), dtype=torch.float32)[:, None]
     y_host = (torch.rand(c["T"], B, generator=gh) < rates).float().pin_memory()
     return h_host, y_host
+
+
+def _oracle_params(params):
+    """The bench's SMESParams as the oracle sees them: the kernel operands (bf16 router and
+    expert weights, fp32 biases and heads) upcast to f64 -- identical operands."""
+    from oracle import smes_oracle as O
+    f64 = lambda t, bf=False: (t.detach().to(torch_bf16()) if bf else t.detach()).double().cpu().numpy()
+    return O.LayerParams(router_w=f64(params.router_w, True), router_b=f64(params.router_b),
+                         layers=[(f64(l.weight, True), f64(l.bias), l.act) for l in params.layers],
+                         head_w=f64(params.head_w), head_b=f64(params.head_b))
+
+
+def torch_bf16():
+    import torch
+    return torch.bfloat16
+
+
+def parity_sample(src, params, labels, n_rows=256, full_loss=True):
+    """Checker run next to the CPU baseline (oracle = test infrastructure, never measured): on an
+    evenly spaced row subset of the batch the timed steps just processed, the router logits against
+    RouterBank.logits (routing.py:101-103), the expert selections index-exact against route_batch
+    (routing.py:235-281), and predictions + BCE of those rows against forward_sparse with the GPU's
+    selections (model.py:284-300, training.py:54-57).  Also the full-batch loss against the BCE of
+    the GPU's own predictions (the loss reduction)."""
+    import torch
+    from oracle import smes_oracle as O
+    T, E, B, ks, ka = src.T, src.E, src.B, src.ks, src.ka
+    rows = np.linspace(0, B - 1, min(n_rows, B)).astype(np.int64)
+    p = _oracle_params(params)
+    h = src.h.double().cpu().numpy()[rows]
+    z = src.z.double().cpu().numpy().reshape(B, T, E)[rows].transpose(1, 0, 2)
+    zr = O.router_logits(h, p)
+    z_rel = float(np.abs(z - zr).max() / np.abs(zr).max())
+    r = O.route_batch(z, ks, ka, p.task_weights)
+    act = src.active.cpu().numpy()[:, rows]
+    sel_ok = bool(np.array_equal(act, r.active) and np.array_equal(src.shared.cpu().numpy()[rows], r.shared))
+    plan = O.build_execution_plan(r.unions, E)
+    f = O.forward_sparse(h, p, ks, ka, logits=z, frozen=r, frozen_plan=plan)
+    preds = src.preds.double().cpu().numpy()
+    y = labels.double().cpu().numpy()
+    pr_rel = float(np.abs(preds[:, rows] - f.predictions).max() / np.abs(f.predictions).max())
+    lam = np.ones(T)
+    bce_gpu_rows = O.weighted_bce(preds[:, rows], y[:, rows], lam)
+    bce_ora_rows = O.weighted_bce(f.predictions, y[:, rows], lam)
+    loss = src.loss_out.double().cpu().numpy()
+    bce_full = O.weighted_bce(preds, y, lam)
+    ok = sel_ok and z_rel < 1e-5 and pr_rel < 2e-2 and abs(bce_gpu_rows - bce_ora_rows) < 2e-2 * bce_ora_rows \
+        and (not full_loss or abs(loss[0] - bce_full) < 1e-5 * bce_full)
+    return {"ok": bool(ok), "rows": int(len(rows)), "selections_index_exact": sel_ok,
+            "router_logits_rel": z_rel, "predictions_rel": pr_rel,
+            "bce_rows_gpu": bce_gpu_rows, "bce_rows_oracle": bce_ora_rows,
+            "loss_gpu": float(loss[0]), "loss_from_gpu_preds": bce_full,
+            "stage1_min_margin": float(O.stage1_margin(z, ks)) if ks > 0 else None,
+            "tolerances": "logits 1e-5 (identical bf16 operands, fp32 accumulate), selections exact, "
+                          "predictions / BCE 2e-2 (bf16), loss reduction 1e-5"}
 
 
 def _roofline(kern, work, peaks, peak_src):
@@ -342,7 +426,10 @@ def run_dp(args, c, world, rank, local, dev):
            "api": "pipeline.HostStepPipeline.step (pinned H2D of each step's inputs, double-buffered on a copy "
                   "stream and overlapped with the previous step; D2H of each step's loss)"}
     n_act = eng.n_act()
-    kern = per_kernel_times(eng.step, reps=5)
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        parity = parity_sample(eng, eng.p, eng.labels, full_loss=world == 1)
+    kern = per_kernel_times(eng.step, reps=5, serial=eng)
     peaks, peak_src = _peaks()
     work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
     roofline, breakdown = _roofline(kern, work, peaks, peak_src)
@@ -361,8 +448,10 @@ def run_dp(args, c, world, rank, local, dev):
                        "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)",
                        "graph": ("fwd+bwd in one CUDA graph" if world == 1 else "fwd+bwd captured as 2 CUDA graphs around the LB-stats all-reduce")},
             "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-            "step_tflops": round(step_tflops, 1), "kernels": breakdown}
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "parity": parity,
+            "step_tflops": round(step_tflops, 1), "kernels": breakdown,
+            "kernels_note": "per-kernel CUDA-event times from an eager step with the backward side stream "
+                            "serialised onto the timing stream (so each kernel is timed alone, like ncu)"}
 
 
 def run_ep(args, c, world, rank, local, dev):
@@ -400,18 +489,45 @@ def run_ep(args, c, world, rank, local, dev):
            "api": "pipeline.HostStepPipeline.step over ep.ExpertParallelStep.step"}
     rk.check()
     n_own = int(rk.totals_o[2].item())
+    n_src = int(rk.totals[2].item())
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        parity = parity_sample(rk, rk.p, rk.labels, full_loss=world == 1)
     kern = per_kernel_times(ep.step, reps=2)
     peaks, peak_src = _peaks()
     sh = rk.shard
-    d, dff, T = c["d"], c["d_ff"], c["T"]
+    d, dff, T, E, El, K = c["d"], c["d_ff"], c["T"], c["E"], rk.El, rk.K
     bal = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
     fl = 2.0 * n_own * d * dff
-    work = {"fc1_fwd": (fl, n_own * (d + dff) * 2), "fc1_dgrad": (fl, n_own * (d + dff) * 2),
+    sent = int(rk.cnt.sum().item())
+    Br = rk.Br
+    # algorithmic (flops, bytes) per launch tag of one EP step on this rank (SURVEY 8d formulas;
+    # n_src = packed rows of the local batch over all E experts, n_own = rows this rank's experts run)
+    work = {"router_fwd": (2.0 * B * d * T * E, B * (d * 2 + T * E * 4)),
+            "router_dgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 4)),
+            "router_wgrad": (2.0 * B * d * T * E, B * (T * E * 2 + d * 2)),
+            "route": (0.0, B * (T * E * 4 + T * K * 8 + c["ks"] * 4 + rk.EW * 4 + 4)),
+            "plan_reduce": (0.0, rk.C * E * 24),
+            "plan_scatter": (0.0, B * (rk.EW * 4 + rk.umax * 4) + n_src * (8 + rk.ldc * 2)),
+            "ep_pack": (0.0, B * (d * 2 + rk.EW * 4) + sent * (d * 2 + rk.wpr * 4)),
+            "owner_plan": (0.0, Br * rk.wpr * 4 * 2 + rk.C_o * El * 8),
+            "owner_scatter": (0.0, Br * d * 2 + n_own * (d * 2 + 8 + sh.ldc * 2)),
+            "fold_heads": (2.0 * El * T * d * dff, El * d * dff * 2 + El * sh.ldg * dff * 2),
+            "fc1_fwd": (fl, n_own * (d + dff) * 2 + n_own * dff / 8),
+            "fc1_dgrad": (fl, n_own * (d + dff) * 2),
             "fc1_wgrad": (fl, n_own * (d + dff) * 2),
+            "mlp_fwd": (fl + 2.0 * n_own * dff * T, n_own * (d * 2 + dff * 2 + dff / 8 + sh.ldp * 4)),
+            "mlp_dgrad": (fl + 2.0 * n_own * dff * T, n_own * (sh.ldc * 2 + dff / 8 + d * 2 + dff * 2)),
             "fc2_fwd_folded": (2.0 * n_own * dff * T, n_own * (dff * 2 + sh.ldp * 4)),
             "fc2_dgrad_folded": (2.0 * n_own * dff * T, n_own * (sh.ldc * 2 + dff * 2 + dff / 8)),
-            "fc2_wgrad_folded": (2.0 * n_own * dff * T, n_own * (dff * 2 + sh.ldc * 2))}
-    work = {k: (f, b, "tensor" if f / b > bal else "hbm") for k, (f, b) in work.items()}
+            "fc2_wgrad_folded": (2.0 * n_own * dff * T, n_own * (dff * 2 + sh.ldc * 2)),
+            "unfold": (4.0 * El * T * d * dff, El * dff * sh.ldg * 4 + El * d * dff * 6),
+            "ep_segments": (0.0, El * rk.n * 12),
+            "ep_copy_rows": (0.0, 2 * (n_own + n_src) * (rk.ldp * 4 + rk.ldc * 2)),
+            "combine_train": (0.0, B * (rk.umax * T * 4 + T * K * 8 + T * 16 + T * E * 2) + n_src * rk.ldc * 2),
+            "unpermute": (0.0, n_own * d * 2 + Br * d * 4),
+            "ep_combine_dh": (0.0, rk.n * B * d * 4 + B * d * 8)}
+    work = {k: (f, b, "tensor" if b > 0 and f / b > bal else "hbm") for k, (f, b) in work.items()}
     roofline, breakdown = _roofline(kern, work, peaks, peak_src)
     expert_flops = 3 * fl + 3 * 2.0 * n_own * dff * T
     cpu = _cpu_sample(args.config, 1) if (rank == 0 and not args.no_cpu) else None
@@ -427,7 +543,7 @@ def run_ep(args, c, world, rank, local, dev):
                        "expert_rows_on_rank0": n_own,
                        "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)"},
             "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "parity": parity,
             "step_tflops": round(expert_flops / (ms * 1e-3) / 1e12, 1), "kernels": breakdown}
 
 
@@ -443,6 +559,7 @@ def run_infer(args, c, world, rank, local, dev):
     c = dict(c, beta=0.0)
     params = _make_params(c, dev)
     sweep, launches = {}, 0
+    clocks_all = []
     reps = max(1000, args.steps)
     for Bb in c["batches"]:
         eng = SMESEngine(params, Bb, c["ks"], c["ka"], device=dev)
@@ -464,12 +581,14 @@ def run_infer(args, c, world, rank, local, dev):
         per = _lib.launch_count - c0
         ts = []
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-        for a, b in ev:
-            flush.zero_()
-            a.record()
-            g.replay()
-            b.record()
-        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            for a, b in ev:
+                flush.zero_()
+                a.record()
+                g.replay()
+                b.record()
+            torch.cuda.synchronize()
+        clocks_all.append(clk.summary())
         ts = sorted(a.elapsed_time(b) for a, b in ev)
         launches += per * reps
         # end to end: pinned H2D of h, graph, D2H of the predictions
@@ -491,6 +610,12 @@ def run_infer(args, c, world, rank, local, dev):
         del g
     Bb, eng, h_host, preds_host = last
     top = sweep[str(Bb)]
+    # roofline of the largest batch's scoring pass: per-kernel CUDA events (eager, one stream)
+    n_act = eng.n_act()
+    kern = per_kernel_times(eng.score, reps=5, serial=eng)
+    peaks, peak_src = _peaks()
+    work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
     cpu = _cpu_sample(args.config, 2) if not args.no_cpu else None
     return {"metric": f"SMES inference p50 latency per batch (B={Bb})", "value": top["p50_ms"], "unit": "ms",
             "n_gpus": 1, "steps": reps, "warmup": max(3, args.warmup), "ms_per_step": top["p50_ms"],
@@ -501,7 +626,17 @@ def run_infer(args, c, world, rank, local, dev):
             "e2e": {"value": top["e2e_ms"], "unit": "ms", "h2d_bytes_per_step": h_host.numel() * 2,
                     "d2h_bytes_per_step": preds_host.numel() * 4,
                     "api": "pinned H2D of h, graph replay of SMESEngine.score, D2H of predictions"},
-            "gpu_launches": launches, "sweep": sweep, "cpu_baseline": cpu}
+            "gpu_launches": launches, "sweep": sweep, "cpu_baseline": cpu, "clocks": _merge_clocks(clocks_all),
+            "roofline": roofline, "kernels": breakdown}
+
+
+def _merge_clocks(cl):
+    """One clocks record over the per-batch-size samplers (median of medians, union of reasons)."""
+    med = [c["sm_mhz"] for c in cl if c.get("sm_mhz")]
+    return {"sm_mhz": float(statistics.median(med)) if med else None,
+            "sm_max_mhz": next((c["sm_max_mhz"] for c in cl if c.get("sm_max_mhz")), None),
+            "reasons": sorted({r for c in cl for r in c.get("reasons", [])}),
+            "samples": sum(c.get("samples", 0) for c in cl), "per_batch": cl}
 
 
 def count_step_launches(step_fn):
@@ -513,7 +648,7 @@ def count_step_launches(step_fn):
     return _lib.launch_count - c0
 
 
-def per_kernel_times(step_fn, reps=5):
+def per_kernel_times(step_fn, reps=5, serial=None):
     import contextlib
     import torch
     from paper_2602_09386_b200 import _lib
@@ -529,6 +664,8 @@ def per_kernel_times(step_fn, reps=5):
         rec.append((tag, a, b))
 
     acc = {}
+    if serial is not None:
+        serial.serial = True        # one stream: the events bracket exactly the tagged launch
     for _ in range(reps):
         rec.clear()
         torch.cuda.synchronize()
@@ -541,6 +678,8 @@ def per_kernel_times(step_fn, reps=5):
         torch.cuda.synchronize()
         for tag, a, b in rec:
             acc[tag] = acc.get(tag, 0.0) + a.elapsed_time(b)
+    if serial is not None:
+        serial.serial = False
     return {k: v / reps for k, v in acc.items()}
 
 

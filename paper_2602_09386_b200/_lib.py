@@ -101,6 +101,7 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_plan_reduce": 1, "smes_plan_red
                     "smes_ep_copy_rows_put": 1}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
+trace = None    # optional list: every successful call appends (tag, kernels launched) -- ncu launch tags
 
 _lib = None
 
@@ -147,7 +148,10 @@ def call(name: str, *args):
         msg = lib.smes_last_error().decode(errors="replace")
         raise _CODE_TO_EXC.get(rc, errors.TaskMoeError)(msg)
     k = KERNELS_PER_CALL.get(name, 0)
-    launch_count += k(*args) if callable(k) else k
+    k = k(*args) if callable(k) else k
+    launch_count += k
+    if trace is not None and k:
+        trace.append((tag or name, k))
     return rc
 
 

@@ -154,6 +154,9 @@ class SMESEngine:
         self.fuse_wgrad = bool(fuse_wgrad and self.fuse_mlp)
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
+        # serial: every launch on the caller's stream (no backward side stream) -- the bench's
+        # per-kernel CUDA-event timing needs it, since events only see the stream they are on
+        self.serial = False
         self._alloc()
         self.refresh_weights()
 
@@ -277,25 +280,42 @@ class SMESEngine:
         self.h = self.h_full[:, :d]                 # strided view; kernels get ptr + ldh
 
     def refresh_weights(self):
-        """Copy fp32 master parameters into the bf16 / fp32 kernel operands."""
+        """Copy the fp32 master parameters into the bf16 / fp32 kernel operands.
+
+        The operand buffers are allocated once and refreshed with ``copy_``: a CUDA graph captured
+        from ``step``/``score`` keeps reading the same addresses, so an optimizer update followed by
+        ``refresh_weights`` is seen by the next replay (no re-capture needed)."""
         self._fold_fresh = False
         p, T, E, d = self.p, self.T, self.E, self.d
         dev = self.dev
-        self.wr_bf = p.router_w.detach().reshape(T * E, d).to(dev, torch.bfloat16).contiguous()
-        self.br = p.router_b.detach().reshape(T * E).to(dev, torch.float32).contiguous()
-        self.w_bf = [l.weight.detach().to(dev, torch.bfloat16).contiguous() for l in p.layers]
-        self.b32 = [l.bias.detach().to(dev, torch.float32).contiguous() for l in p.layers]
-        self.head_w = p.head_w.detach().to(dev, torch.float32).contiguous()
-        self.head_w_bf = self.head_w.to(torch.bfloat16).reshape(1, T, -1).contiguous()
-        ldc = _round(T, 16)
-        hwt = torch.zeros(1, self.head_w.shape[1], ldc, dtype=torch.bfloat16, device=dev)
-        hwt[0, :, :T] = self.head_w.t().to(torch.bfloat16)
-        self.head_wT_bf = hwt
-        self.head_b = p.head_b.detach().to(dev, torch.float32).contiguous()
+        if tuple(p.router_w.shape) != (T, E, d) or len(p.layers) != len(self.dims) - 1:
+            raise ShapeError("refresh_weights: parameter shapes changed; build a new engine")
         tw = p.task_weights if p.task_weights is not None else torch.ones(T)
-        self.tw = tw.detach().to(dev, torch.float64).contiguous()
         lam = p.task_loss_weights if p.task_loss_weights is not None else torch.ones(T)
-        self.lam = lam.detach().to(dev, torch.float32).contiguous()
+        src = {
+            "wr_bf": (p.router_w.detach().reshape(T * E, d), torch.bfloat16),
+            "br": (p.router_b.detach().reshape(T * E), torch.float32),
+            "head_w": (p.head_w.detach(), torch.float32),
+            "head_b": (p.head_b.detach(), torch.float32),
+            "tw": (torch.as_tensor(tw).detach(), torch.float64),
+            "lam": (torch.as_tensor(lam).detach(), torch.float32),
+        }
+        first = not hasattr(self, "wr_bf")
+        for name, (t, dt) in src.items():
+            if first:
+                setattr(self, name, torch.empty(t.shape, dtype=dt, device=dev))
+            getattr(self, name).copy_(t.to(dev))
+        if first:
+            self.w_bf = [torch.empty(l.weight.shape, dtype=torch.bfloat16, device=dev) for l in p.layers]
+            self.b32 = [torch.empty(l.bias.shape, dtype=torch.float32, device=dev) for l in p.layers]
+            self.head_w_bf = torch.empty(1, T, self.head_w.shape[1], dtype=torch.bfloat16, device=dev)
+            self.head_wT_bf = torch.zeros(1, self.head_w.shape[1], _round(T, 16), dtype=torch.bfloat16, device=dev)
+        for dst, l in zip(self.w_bf, p.layers):
+            dst.copy_(l.weight.detach().to(dev))
+        for dst, l in zip(self.b32, p.layers):
+            dst.copy_(l.bias.detach().to(dev))
+        self.head_w_bf[0].copy_(self.head_w)
+        self.head_wT_bf[0, :, :T].copy_(self.head_w.t())
         self.beta = float(p.lb_strength)
 
     # ------------------------------------------------------------------ steps
@@ -462,7 +482,7 @@ class SMESEngine:
         folded = fused and self._folded
         # The router backward needs only dz and h: it runs on a side stream next to the expert
         # backward, whose wgrad GEMMs leave SMs idle (128 tiles on 148 SMs); joins before unpermute.
-        side = fused
+        side = fused and not self.serial
         unpermute_side = False
         if side:
             main = torch.cuda.current_stream(self.dev)
@@ -642,6 +662,8 @@ class SMESEngine:
              "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4)),
              "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8),
              "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12)),
+             "combine_score": (0.0, B * (U * self.ldp * 4 + U * 4 + T * K * 8 + T * 8)),
+             "plan_reduce": (0.0, self.C * E * 24 + E * 40),
              "combine_bwd": (0.0, B * (U * do * 2 * 2 + T * K * 8 + T * 8 + T * E * 2)),
              "unpermute": (0.0, B * (U * d * 2 + d * 8))}
         for i in range(len(self.dims) - 1):

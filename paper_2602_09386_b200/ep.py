@@ -32,7 +32,7 @@ import torch
 from . import _lib
 from ._lib import call, ptr, tcall
 from .errors import ConfigError, ShapeError, StateError
-from .experts import ExpertShard
+from .experts import ExpertShard, refresh_into
 
 U32 = torch.int32   # mask words travel as int32 storage
 
@@ -188,16 +188,18 @@ class EPRank:
         return self._head_w
 
     def refresh_weights(self):
+        """Copy the master parameters into the kernel operands (allocated once, then ``copy_``:
+        stable addresses for graph replays)."""
         p, T, E, d = self.p, self.T, self.E, self.d
-        self.wr_bf = p.router_w.detach().reshape(T * E, d).to(self.dev, torch.bfloat16).contiguous()
-        self.br = p.router_b.detach().reshape(T * E).to(self.dev, torch.float32).contiguous()
+        tw = p.task_weights if p.task_weights is not None else torch.ones(T)
+        lam = p.task_loss_weights if p.task_loss_weights is not None else torch.ones(T)
+        refresh_into(self, "wr_bf", p.router_w.detach().reshape(T * E, d), torch.bfloat16)
+        refresh_into(self, "br", p.router_b.detach().reshape(T * E), torch.float32)
         self.head_w = self.head_w32()
         self.head_w.copy_(p.head_w.detach())
-        self.head_b = p.head_b.detach().to(self.dev, torch.float32).contiguous()
-        tw = p.task_weights if p.task_weights is not None else torch.ones(T)
-        self.tw = tw.detach().to(self.dev, torch.float64).contiguous()
-        lam = p.task_loss_weights if p.task_loss_weights is not None else torch.ones(T)
-        self.lam = lam.detach().to(self.dev, torch.float32).contiguous()
+        refresh_into(self, "head_b", p.head_b.detach(), torch.float32)
+        refresh_into(self, "tw", torch.as_tensor(tw).detach(), torch.float64)
+        refresh_into(self, "lam", torch.as_tensor(lam).detach(), torch.float32)
         self.beta = float(p.lb_strength)
         self.shard.refresh_weights()
 

@@ -23,6 +23,17 @@ def _round(x, m):
     return (x + m - 1) // m * m
 
 
+def refresh_into(obj, name: str, src: torch.Tensor, dtype) -> torch.Tensor:
+    """``obj.name`` <- src (cast to dtype) in place; allocated on first use so device addresses
+    captured by a CUDA graph stay valid across weight refreshes."""
+    cur = getattr(obj, name, None)
+    if cur is None or cur.shape != src.shape or cur.dtype != dtype:
+        cur = torch.empty(src.shape, dtype=dtype, device=obj.dev)
+        setattr(obj, name, cur)
+    cur.copy_(src)
+    return cur
+
+
 class ExpertShard:
     def __init__(self, layers, T: int, head_w: torch.Tensor, rows_cap: int, device, fuse_mlp: bool = True,
                  fuse_wgrad: bool = False):
@@ -78,8 +89,13 @@ class ExpertShard:
         self.refresh_weights()
 
     def refresh_weights(self):
-        self.w_bf = [l.weight.detach().to(self.dev, torch.bfloat16).contiguous() for l in self.layers]
-        self.b32 = [l.bias.detach().to(self.dev, torch.float32).contiguous() for l in self.layers]
+        """bf16 / fp32 operands, allocated once and refreshed in place (graph-stable addresses)."""
+        if not hasattr(self, "w_bf"):
+            self.w_bf = [torch.empty(l.weight.shape, dtype=torch.bfloat16, device=self.dev) for l in self.layers]
+            self.b32 = [torch.empty(l.bias.shape, dtype=torch.float32, device=self.dev) for l in self.layers]
+        for l, w, b in zip(self.layers, self.w_bf, self.b32):
+            w.copy_(l.weight.detach())
+            b.copy_(l.bias.detach())
 
     # ------------------------------------------------------------------ forward
     def forward(self, s, seg_pad):

@@ -259,16 +259,20 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
     eng.forward_b(with_loss=False)
     eng.step_id += 1
     T, E = eng.T, eng.E
-    routing = BatchRouting(eng.z, T, B, E, model.budget, eng.tw, eng.shared, eng.adaptive, eng.active, eng.wsel,
-                           eng.umask, eng.usize, eng.chunk_union, eng.chunk_active, eng.chunk_mass, eng.chunk_dmass,
-                           eng.rpw, z_strides=(E, T * E))
-    plan = ExecutionPlan(E, B, eng.umax, eng.rows_cap, eng.seg_pad, eng.seg_log, eng.loads, eng.totals, eng.row_of,
-                         eng.gather_inst, eng.gather_exp, eng.stats_raw, eng.usize)
+    # the result owns its arrays (the reference returns fresh arrays): clone the engine's buffers so a
+    # later forward through the same cached engine cannot rewrite this result's routing or plan
+    c = lambda t: t.clone()
+    z = c(eng.z)
+    routing = BatchRouting(z, T, B, E, model.budget, c(eng.tw), c(eng.shared), c(eng.adaptive), c(eng.active),
+                           c(eng.wsel), c(eng.umask), c(eng.usize), c(eng.chunk_union), c(eng.chunk_active),
+                           c(eng.chunk_mass), c(eng.chunk_dmass), eng.rpw, z_strides=(E, T * E))
+    plan = ExecutionPlan(E, B, eng.umax, eng.rows_cap, c(eng.seg_pad), c(eng.seg_log), c(eng.loads), c(eng.totals),
+                         c(eng.row_of), c(eng.gather_inst), c(eng.gather_exp), c(eng.stats_raw), routing.usize)
     n_act = eng.n_act()
     flops = n_act * sum(eng.dims[i] * eng.dims[i + 1] for i in range(len(eng.dims) - 1))
     if counter is not None:
         counter.add(flops)
     return ForwardResult("sparse", eng.preds.clone(), eng.logits.clone(), eng.reps.float(), routing, plan, flops,
-                         hidden=eng.h if keep_cache else None,
-                         router_logits=eng.z.view(B, T, E).transpose(0, 1) if keep_cache else None,
+                         hidden=eng.h.clone() if keep_cache else None,
+                         router_logits=z.view(B, T, E).transpose(0, 1) if keep_cache else None,
                          _engine=eng, _step=eng.step_id, _enc=enc)

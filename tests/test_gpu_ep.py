@@ -58,6 +58,7 @@ def test_ep_parity(name):
         rk.check()
     # --- oracle on the concatenated batch with the GPU's logits
     z = np.concatenate([rk.z.double().cpu().numpy().reshape(Bl, T, E) for rk in ranks], 0).transpose(1, 0, 2)
+    assert rel(z, O.router_logits(h, p)) < 1e-5          # RouterBank.logits (routing.py:101-103)
     route = O.route_batch(z, ks, ka, p.task_weights)
     act = np.concatenate([rk.active.cpu().numpy() for rk in ranks], 1)
     assert np.array_equal(act, route.active)

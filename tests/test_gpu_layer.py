@@ -63,6 +63,8 @@ def test_layer_parity(name, fold):
         assert eng._folded, "identity last pool + sparse stats must take the folded training path"
     T, E, B, ks, ka = eng.T, eng.E, eng.B, eng.ks, eng.ka
     z = eng.z.double().cpu().numpy().reshape(B, T, E).transpose(1, 0, 2)
+    # router logits against RouterBank.logits (routing.py:101-103) on the identical bf16 operands
+    assert rel(z, O.router_logits(h, p)) < FP32_TOL
 
     # --- routing: index-exact on the GPU's logits (routing.py:235-281)
     r = O.route_batch(z, ks, ka, p.task_weights)
@@ -158,6 +160,7 @@ def test_score_matches_oracle(name):
     eng.score()
     torch.cuda.synchronize()
     z = eng.z.double().cpu().numpy().reshape(B, T, E).transpose(1, 0, 2)
+    assert rel(z, O.router_logits(h, p)) < FP32_TOL
     r = O.route_batch(z, ks, ka, p.task_weights)
     assert np.array_equal(eng.active.cpu().numpy(), r.active)
     plan = O.build_execution_plan(r.unions, E)

@@ -1,25 +1,40 @@
-"""Short eager driver for ncu: builds the c2 engine (bench config) and runs a few
-eager fwd+bwd steps.  Not a benchmark -- numbers under ncu are never reported."""
-import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-import bench
-from paper_2602_09386_b200 import ExpertLayer, SMESEngine, SMESParams
+"""Short eager driver for ncu: builds the bench engine of a configuration (bench._make_params,
+bench._host_inputs) and runs a few eager fwd+bwd steps with the backward side stream serialised,
+so the launch order under ncu is the Python call order.  The launch-site tag of every kernel of
+the last step goes to gpurun_out/step_tags.json (tools/ncu_traffic.py maps ncu rows to tags with
+it).  Not a benchmark -- numbers under ncu are never reported.
 
-steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-c = bench.CFG
+    python tools/profile_step.py [steps] [--config c2|c3]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+
+import bench
+from paper_2602_09386_b200 import SMESEngine, _lib
+
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "c2"
+if cfg in args:
+    args.remove(cfg)
+steps = int(args[0]) if args else 3
+c = bench.CONFIGS[cfg]
 dev = torch.device("cuda", 0)
-g = torch.Generator().manual_seed(0)
-u = lambda shape, s: ((torch.rand(*shape, generator=g, dtype=torch.float64) * 2 - 1) * s).float().to(dev)
-T, E, d, dff, do = c["T"], c["E"], c["d"], c["d_ff"], c["d_out"]
-params = SMESParams(router_w=u((T, E, d), 1e-3 / d ** 0.5), router_b=torch.zeros(T, E, device=dev),
-                    layers=[ExpertLayer(u((E, dff, d), d ** -0.5), torch.zeros(E, dff, device=dev), "relu"),
-                            ExpertLayer(u((E, do, dff), dff ** -0.5), torch.zeros(E, do, device=dev), "identity")],
-                    head_w=u((T, do), do ** -0.5), head_b=torch.zeros(T, device=dev), lb_strength=c["beta"])
-eng = SMESEngine(params, c["B"], c["ks"], c["ka"], device=dev)
-eng.set_inputs(torch.randn(c["B"], d, generator=g).to(torch.bfloat16).to(dev),
-               (torch.rand(T, c["B"], generator=g) < 0.2).float().to(dev))
-for _ in range(steps):
+B = c["B"]
+eng = SMESEngine(bench._make_params(c, dev), B, c["ks"], c["ka"], device=dev)
+h, y = bench._host_inputs(c, B, 0)
+eng.set_inputs(h.to(dev), y.to(dev))
+eng.serial = True
+for i in range(steps):
+    if i == steps - 1:
+        _lib.trace = []
     eng.step()
 torch.cuda.synchronize()
-print("n_act", eng.n_act())
+tags = [t for t, k in _lib.trace for _ in range(k)]
+os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+json.dump({"config": cfg, "launches_per_step": len(tags), "tags": tags},
+          open(os.path.join(ROOT, "gpurun_out", "step_tags.json"), "w"), indent=1)
+print("n_act", eng.n_act(), "launches/step", len(tags))
