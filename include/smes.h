@@ -182,7 +182,9 @@ int smes_mlp_wgrad(const void* C, long ldc, long rows_cap, const void* G, int ld
  *      smes_ep_combine_dh: d_hidden[b] = dh_router[b] + sum_r dh_recv[r][pos[r][b]] (fixed owner order)
  *      smes_ep_capacity_guard: empty the owner plan and raise flag if its rows exceed the workspace
  *      smes_ep_put_slots / smes_ep_signal_wait: peer-memory all-to-all (CUDA IPC pointers, flag epochs)
- *      smes_ipc_handle / smes_ipc_open / smes_ipc_close: CUDA IPC plumbing (64-byte handles). */
+ *      smes_ipc_handle / smes_ipc_open / smes_ipc_close: CUDA IPC plumbing (64-byte handles).
+ *      smes_ipc_handle also returns dev_ptr's offset inside its allocation: the peer maps the
+ *      allocation base and must add it. */
 int smes_ep_pack(int B, int EW, const uint32_t* umask, int n, int wpr, const void* h_bf16, long ldh, int d,
                  int32_t* idx, int32_t* pos, int32_t* cnt, uint32_t* mask_out, void* h_out_bf16, void* stream);
 int smes_ep_segments(int mode, int n, int El, const int32_t* cnt, const int32_t* seg_pad, long slot_rows,
@@ -204,7 +206,7 @@ int smes_ep_copy_rows_put(int nseg, const int32_t* tab, int El, long slot_rows, 
 int smes_ep_put_slots(int n, int self, const void* send, long slot_bytes, long row_bytes, const int32_t* rows_used,
                       void* const* peer_recv_dev, void* stream);
 int smes_ep_signal_wait(int n, int self, void* const* peer_flags_dev, int32_t* my_flags, int epoch, void* stream);
-int smes_ipc_handle(void* dev_ptr, void* handle_out);
+int smes_ipc_handle(void* dev_ptr, void* handle_out, long* offset_out);
 int smes_ipc_open(const void* handle, void** dev_ptr_out);
 int smes_ipc_close(void* dev_ptr);
 

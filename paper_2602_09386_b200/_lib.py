@@ -49,7 +49,7 @@ SIGNATURES = {
     "smes_ep_pack_put": [I, I, P, I, I, P, L, I, I, P, P, P, P, P, P],
     "smes_ep_copy_rows_put": [I, P, I, L, I, P, L, P, L, I, P],
     "smes_ep_signal_wait": [I, I, P, P, I, P],
-    "smes_ipc_handle": [P, P],
+    "smes_ipc_handle": [P, P, P],
     "smes_ipc_open": [P, P],
     "smes_ipc_close": [P],
     "smes_mlp_fwd": [P, L, L, P, P, P, P, I, I, I, I, P, P, L, P, L, P, L, P],

@@ -382,11 +382,30 @@ int smes_ep_signal_wait(int n, int self, void* const* peer_flags_dev, int32_t* m
 }
 
 // CUDA IPC helpers for the peer-memory transport (handles travel through torch.distributed)
-int smes_ipc_handle(void* dev_ptr, void* handle_out /* 64 bytes */) {
+// The IPC handle names the whole cudaMalloc allocation that contains dev_ptr, and the peer's
+// cudaIpcOpenMemHandle returns that allocation's BASE.  Tensors from a caching allocator sit at an
+// offset inside a larger segment, so the offset travels with the handle (offset_out) and the peer
+// adds it to the mapped base (smes_ipc_open).
+int smes_ipc_handle(void* dev_ptr, void* handle_out /* 64 bytes */, long* offset_out) {
   cudaIpcMemHandle_t h;
   cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  static GetRange get_range = nullptr;
+  if (get_range == nullptr) {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || fp == nullptr)
+      return set_error(SMES_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    get_range = reinterpret_cast<GetRange>(fp);
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (unsigned long long)dev_ptr) != 0)
+    return set_error(SMES_ERR_CUDA, "cuMemGetAddressRange failed for %p", dev_ptr);
   memcpy(handle_out, &h, sizeof(h));
+  if (offset_out) *offset_out = (long)((unsigned long long)dev_ptr - base);
   return SMES_OK;
 }
 

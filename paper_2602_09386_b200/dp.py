@@ -80,6 +80,11 @@ class DataParallelStep:
         if self.world > 1:
             dist.all_reduce(self.eng.grad_flat, op=dist.ReduceOp.SUM, group=self.group)
             self.eng.grad_flat.div_(self.world)
+            # the reported objective is the global-batch one: the task term is a per-rank mean over
+            # an equal shard (average it), L_lb already uses the all-reduced statistics (identical
+            # on every rank), so averaging [task, lb, total] gives the global values
+            dist.all_reduce(self.eng.loss_out, op=dist.ReduceOp.SUM, group=self.group)
+            self.eng.loss_out.div_(self.world)
 
     def step_eager(self):
         self._part_a()

@@ -422,6 +422,7 @@ class PeerComm:
         self.flags = torch.zeros(self.n, dtype=torch.int32, device=dev)
         self.epoch = 0
         self._bufs = {}
+        self._mapped = {}
         self.peer_flags = self._open(self.flags)
         for name in ("dispatch", "P", "C", "dh"):
             for _, recv in rank.exchanges(name):
@@ -433,23 +434,37 @@ class PeerComm:
         self.dist.barrier(group=self.group)
 
     def _open(self, t):
+        """Map every peer's copy of ``t``: the IPC handle names the cudaMalloc segment holding it,
+        so each rank also publishes the tensor's offset inside that segment (caching-allocator
+        tensors rarely sit at a segment base) and the opener adds it to the mapped base."""
         import ctypes as C
-        lib = _lib.load()
         h = (C.c_uint8 * 64)()
-        call("smes_ipc_handle", ptr(t), C.cast(h, C.c_void_p))
-        mine = bytes(h)
+        off = C.c_long(0)
+        call("smes_ipc_handle", ptr(t), C.cast(h, C.c_void_p), C.byref(off))
+        mine = (bytes(h), int(off.value))
         allh = [None] * self.n
         self.dist.all_gather_object(allh, mine, group=self.group)
         ptrs = []
-        for r, hb in enumerate(allh):
+        for r, (hb, o) in enumerate(allh):
             if r == self.me:
                 ptrs.append(t.data_ptr())
-            else:
+                continue
+            key = hb
+            base = self._mapped.get(key)
+            if base is None:        # one mapping per (peer, segment): a segment may hold several buffers
                 out = C.c_void_p()
                 hh = (C.c_uint8 * 64).from_buffer_copy(hb)
                 call("smes_ipc_open", C.cast(hh, C.c_void_p), C.byref(out))
-                ptrs.append(out.value)
+                base = self._mapped[key] = out.value
+            ptrs.append(base + o)
         return torch.tensor(ptrs, dtype=torch.int64, device=t.device)
+
+    def close(self):
+        """Unmap the peers' segments (after a final synchronize)."""
+        torch.cuda.synchronize(self.rank.dev)
+        for base in self._mapped.values():
+            call("smes_ipc_close", base)
+        self._mapped.clear()
 
     def all_to_all(self, name):
         s = torch.cuda.current_stream(self.rank.dev).cuda_stream

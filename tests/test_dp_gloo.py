@@ -62,6 +62,7 @@ class OracleEngine:
         parts = [g for pair in bw.layers for g in pair] + [bw.router_w, bw.router_b, bw.head_w, bw.head_b]
         self.grad_flat = torch.tensor(np.concatenate([np.ravel(a) for a in parts]))
         self.lb_value = value
+        self.loss_out = torch.tensor([bw.task_value, value, bw.task_value + BETA * value], dtype=torch.float64)
 
 
 def _worker(rank, world, port, out):
@@ -74,7 +75,7 @@ def _worker(rank, world, port, out):
     step = DataParallelStep(eng, use_graphs=False)
     step.step()
     if rank == 0:
-        out.put((eng.grad_flat.numpy(), eng.lb_value))
+        out.put((eng.grad_flat.numpy(), eng.lb_value, eng.loss_out.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -94,7 +95,7 @@ def test_dp_two_ranks_equals_single_process():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for pr in procs:
         pr.start()
-    grad, lb = q.get(timeout=120)
+    grad, lb, loss = q.get(timeout=120)
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
@@ -105,3 +106,5 @@ def test_dp_two_ranks_equals_single_process():
     ref = np.concatenate([np.ravel(a) for a in parts])
     assert np.abs(grad - ref).max() <= 1e-12 * np.abs(ref).max()
     assert abs(lb - bw.lb_value) < 1e-12
+    # the all-reduced objective is the global-batch one (dp.py _allreduce_grads)
+    assert np.allclose(loss, [bw.task_value, bw.lb_value, bw.total], rtol=1e-12)

@@ -36,7 +36,8 @@ if r == 0:
     worst = max(np.abs(mine[k] - refg[k]).max() / max(np.abs(refg[k]).max(), 1e-30) for k in refg)
     lref = ref.loss_out.cpu().numpy()
     print(f"dp2 vs single: max rel grad diff {worst:.3e}; loss {loss} vs {lref}", flush=True)
-    assert worst < 2e-2 and np.allclose(loss, lref, rtol=2e-2)
+    # the DP loss is all-reduced (global-batch objective): equal to one process up to fp32 order
+    assert worst < 2e-2 and np.allclose(loss, lref, rtol=1e-5)
     print("DP2 OK")
 dist.barrier()
 dist.destroy_process_group()
