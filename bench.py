@@ -410,6 +410,7 @@ def run_dp(args, c, world, rank, local, dev):
     eng = SMESEngine(_make_params(c, dev), B, c["ks"], c["ka"], device=dev)
     h_host, y_host = _host_inputs(c, B, rank)
     eng.set_inputs(h_host.to(dev), y_host.to(dev))
+    eng.keep_logits = False        # the training step does not write the router logits (fused front)
     dp = DataParallelStep(eng)
     dp.capture(warmup=1)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
@@ -428,6 +429,11 @@ def run_dp(args, c, world, rank, local, dev):
     n_act = eng.n_act()
     parity = None
     if rank == 0 and not args.no_cpu:
+        # one more step of the same batch with the logits written out, for the checker
+        eng.keep_logits = True
+        dp.step_eager()
+        torch.cuda.synchronize()
+        eng.keep_logits = False
         parity = parity_sample(eng, eng.p, eng.labels, full_loss=world == 1)
     kern = per_kernel_times(eng.step, reps=5, serial=eng)
     peaks, peak_src = _peaks()

@@ -53,6 +53,20 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
                      double* chunk_mass, double* chunk_dmass, double* probs_out, int32_t* flag, int frozen,
                      void* stream);
 
+/* ---- K0+K1 fused router front: RouterBank.logits (routing.py:101-103, via Affine.apply
+ *      linalg.py:143-149) on the tensor cores, feeding route_batch (routing.py:235-281) straight
+ *      from TMEM, two threads per row.  Same outputs and numerics as smes_route_batch (Stage I in
+ *      fp64; per-chunk histograms over chunks of sub_rows = 4 * rows_per_warp rows).  z_out
+ *      (B, T*E) fp32 is optional; chunk_dmass may be null (dense mass not computed).
+ *      h (B, ldh) bf16, w_r (T*E, d) bf16, b_r (T*E) fp32.  Supported shapes: see
+ *      smes_route_front_supported (E in {16, 32}, T*E <= 256, d % 64 == 0, budget 4+2 or 2+1). */
+int smes_route_front_supported(int T, int E, int d, int k_shared, int k_adaptive);
+int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r, const double* task_weights,
+                     int T, int B, int E, int d, int k_shared, int k_adaptive, int sub_rows, int32_t* shared,
+                     int32_t* adaptive, int32_t* active, float* wsel, uint32_t* umask, int32_t* usize,
+                     int32_t* chunk_union, int32_t* chunk_active, double* chunk_mass, double* chunk_dmass,
+                     int32_t* flag, float* z_out, void* stream);
+
 /* ---- K2 execution plan: replaces build_execution_plan (execution.py:85-123)
  *      and the gather hidden[plan.gather_instances] (model.py:301).
  *      Segments are padded to 128 rows (seg_pad); seg_log are the reference's

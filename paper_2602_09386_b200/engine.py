@@ -154,6 +154,11 @@ class SMESEngine:
         self.fuse_wgrad = bool(fuse_wgrad and self.fuse_mlp)
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
+        # fused router front (csrc/front.cu): router GEMM -> routing straight from TMEM, so the
+        # logits never round-trip HBM.  ``keep_logits`` still writes z (the API's router_logits,
+        # the dense-reading backward and the parity checks read it); training steps turn it off.
+        self.use_front = bool(call("smes_route_front_supported", T, E, d, ks, ka))
+        self.keep_logits = True
         # serial: every launch on the caller's stream (no backward side stream) -- the bench's
         # per-kernel CUDA-event timing needs it, since events only see the stream they are on
         self.serial = False
@@ -363,10 +368,21 @@ class SMESEngine:
         the task heads, so its output O and the task reps are not materialised."""
         s = self._stream()
         T, E, B, d = self.T, self.E, self.B, self.d
-        # router logits z = h W_r^T + b_r  (B, T*E) fp32
-        _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0, ptr(self.seg_router),
-             ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
-        self.route(s, frozen=frozen)
+        if self.use_front and not frozen:
+            # router GEMM + progressive router in one kernel (routing.py:101-103 + :235-281)
+            # keep_logits off (training steps): neither z nor the dense mass (read only by the dense
+            # LB reading and by the API's full_probs / compute_load_stats(dense_probs=True))
+            full = self.keep_logits or self.dense
+            _tagged("route_front", "smes_route_front", ptr(self.h), self.ldh, ptr(self.wr_bf), ptr(self.br),
+                    ptr(self.tw), T, B, E, d, self.ks, self.ka, 4 * self.rpw, ptr(self.shared), ptr(self.adaptive),
+                    ptr(self.active), ptr(self.wsel), ptr(self.umask), ptr(self.usize), ptr(self.chunk_union),
+                    ptr(self.chunk_active), ptr(self.chunk_mass), ptr(self.chunk_dmass) if full else None,
+                    ptr(self.flag), ptr(self.z) if full else None, s)
+        else:
+            # router logits z = h W_r^T + b_r  (B, T*E) fp32
+            _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0,
+                    ptr(self.seg_router), ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
+            self.route(s, frozen=frozen)
         if finalize_stats:
             # single device: LoadStats over the local B*T, finalized by the plan reduce's last block
             _tagged("plan_reduce", "smes_plan_reduce_stats", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
@@ -660,6 +676,11 @@ class SMESEngine:
              "dpacked_gemm": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2)),
              "head_wgrad": (2.0 * n_act * do * T, n_act * (self.ldc * 2 + do * 2)),
              "route": (0.0, B * (T * E * 4 + T * K * 8 + self.ks * 4 + (E + 31) // 32 * 4 + 4)),
+             # fused front: h read once, selections/weights/union written; z only with keep_logits
+             "route_front": (2.0 * B * d * T * E, B * (d * 2 + T * K * 8 + T * self.ka * 4 + self.ks * 4
+                                                       + (E + 31) // 32 * 4 + 4
+                                                       + (T * E * 4 if (self.keep_logits or self.dense) else 0))
+                             + self.C * E * 24),
              "plan_scatter": (0.0, B * (d * 2 + U * d * 2 + U * 4) + n_act * 8),
              "combine_fwd": (0.0, B * (U * do * 2 + T * K * 8 + T * do * 2 * (self.reps is not None) + T * 12)),
              "combine_score": (0.0, B * (U * self.ldp * 4 + U * 4 + T * K * 8 + T * 8)),
