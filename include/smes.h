@@ -59,7 +59,7 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
  *      fp64; per-chunk histograms over chunks of sub_rows = 4 * rows_per_warp rows).  z_out
  *      (B, T*E) fp32 is optional; chunk_dmass may be null (dense mass not computed).
  *      h (B, ldh) bf16, w_r (T*E, d) bf16, b_r (T*E) fp32.  Supported shapes: see
- *      smes_route_front_supported (E in {16, 32}, T*E <= 256, d % 64 == 0, budget 4+2 or 2+1). */
+ *      smes_route_front_supported (E in {16, 32}, T*E <= 256, d in {64, ..., 256}, budget 4+2 or 2+1). */
 int smes_route_front_supported(int T, int E, int d, int k_shared, int k_adaptive);
 int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r, const double* task_weights,
                      int T, int B, int E, int d, int k_shared, int k_adaptive, int sub_rows, int32_t* shared,
