@@ -81,8 +81,8 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
 int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
                            const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
                            double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
-                           unsigned int* ticket, int32_t* seg_half, int K, double batch_times_tasks, int dense,
-                           double* stats_out, float* freq_f32, void* stream);
+                           unsigned int* ticket, int32_t* seg_half, int K, int lb_experts, double batch_times_tasks,
+                           int dense, double* stats_out, float* freq_f32, void* stream);
 int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
                      void* stream);
 int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,
@@ -230,8 +230,10 @@ int smes_ipc_close(void* dev_ptr);
 int smes_post_combine(int nparts, const float* part_csum, int n_csum, float* csum, const float* part_rb, int n_rb,
                       float* rb, const float* part_db, int n_db, float* db, const double* loss_part, double inv_b,
                       double beta, const double* stats_value, double* loss_out, void* stream);
-int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
-                        float* freq_f32, void* stream);
+/* lb_experts: the E of the load-balancing value (E / K) <f, p> (balance.py:69-70); 0 = E.  It differs
+ * from E when the shim pads the expert count with never-selected experts (model.py). */
+int smes_stats_finalize(int E, int K, int lb_experts, double batch_times_tasks, int dense, const double* raw,
+                        double* out, float* freq_f32, void* stream);
 int smes_loss_finalize(int nparts, const double* part, double inv_b, double beta, const double* stats_value,
                        double* out, void* stream);
 

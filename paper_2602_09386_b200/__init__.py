@@ -8,13 +8,14 @@ There is no CPU fallback: every entry point raises CudaError without a GPU.
 from .errors import (ConfigError, CudaError, DataFormatError, NumericsError, PoolError, PoolTimeout, ShapeError,
                      StateError, TaskMoeError)
 from .engine import ExpertLayer, SMESEngine, SMESParams
-from .routing import (BatchRouting, RoutingBudget, RoutingDecision, naive_route_batch, progressive_route,
-                      renormalized_weights, route_batch)
-from .execution import (ExecutionPlan, ExpertPool, FlopCounter, build_execution_plan, grouped_gemm,
-                        init_expert_pool, reconstruct_task_reps)
+from .routing import (BatchRouting, RouterBank, RoutingBudget, RoutingDecision, compute_global_scores, dense_routing,
+                      naive_route_batch, naive_sparse_route, progressive_route, renormalized_weights, route_batch,
+                      stack_decisions)
+from .execution import ExecutionPlan, build_execution_plan, grouped_gemm, reconstruct_task_reps
+from .experts import ExpertPool, init_expert_pool
 from .balance import LoadStats, SkewDiagnostics, compute_load_stats, lb_loss_gradient, skew_diagnostics
-from .linalg import Affine, init_affine
-from .model import ForwardResult, MoeModel, RouterBank, forward_sparse, init_model
+from .linalg import Affine, FlopCounter, init_affine, matmul, relu, sigmoid, softmax, top_k
+from .model import ForwardResult, MoeModel, forward_sparse, heads_from_stacked, init_model
 from .training import BackwardResult, backward, task_loss, total_loss
 from .checkpoint import load_model, save_model
 from .workspace import (DeviceWorkspace, LoadProfile, PageBlock, ReplayResult, WorkspacePool, provision,
@@ -26,13 +27,14 @@ __all__ = [
     "TaskMoeError", "ShapeError", "ConfigError", "NumericsError", "StateError", "CudaError", "DataFormatError",
     "PoolError", "PoolTimeout",
     "SMESEngine", "SMESParams", "ExpertLayer",
-    "RoutingBudget", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route", "naive_route_batch",
-    "renormalized_weights",
+    "RoutingBudget", "RouterBank", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route",
+    "naive_route_batch", "naive_sparse_route", "renormalized_weights", "compute_global_scores", "dense_routing",
+    "stack_decisions",
     "ExecutionPlan", "ExpertPool", "FlopCounter", "build_execution_plan", "grouped_gemm", "init_expert_pool",
     "reconstruct_task_reps",
     "LoadStats", "SkewDiagnostics", "compute_load_stats", "lb_loss_gradient", "skew_diagnostics",
-    "Affine", "init_affine",
-    "ForwardResult", "MoeModel", "RouterBank", "forward_sparse", "init_model",
+    "Affine", "init_affine", "matmul", "relu", "sigmoid", "softmax", "top_k",
+    "ForwardResult", "MoeModel", "forward_sparse", "heads_from_stacked", "init_model",
     "BackwardResult", "backward", "task_loss", "total_loss",
     "load_model", "save_model",
     "DeviceWorkspace", "LoadProfile", "PageBlock", "ReplayResult", "WorkspacePool", "provision", "required_pages",

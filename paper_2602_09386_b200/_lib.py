@@ -30,7 +30,7 @@ SIGNATURES = {
     "smes_route_front_supported": [I, I, I, I, I],
     "smes_route_front": [P, L, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "smes_plan_reduce": [I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
-    "smes_plan_reduce_stats": [I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, D, I, P, P, P],
+    "smes_plan_reduce_stats": [I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, I, D, I, P, P, P],
     "smes_plan_counts": [I, I, I, P, P, P, P],
     "smes_plan_scatter": [I, I, I, I, P, P, P, P, P, L, P, L, P, I, P, P, P, L, I, P],
     "smes_gemm_ragged_m": [P, L, L, P, I, I, I, I, P, P, I, P, P, L, P, L, I, L, P],
@@ -62,7 +62,7 @@ SIGNATURES = {
     "smes_fold_heads": [I, I, I, I, I, P, P, P, P, P, P, P],
     "smes_unfold_grads": [I, I, I, I, I, P, L, L, L, P, L, P, P, P, P, P, P, P, P],
     "smes_fold_gemm_path": [I, I, I, I],
-    "smes_stats_finalize": [I, I, D, I, P, P, P, P],
+    "smes_stats_finalize": [I, I, I, D, I, P, P, P, P],
     "smes_loss_finalize": [I, P, D, D, P, P, P],
     "smes_seg_colsum": [P, L, L, I, P, I, P, P, P],
     "smes_unpermute": [I, I, P, P, I, P, L, P, P, P],

@@ -55,7 +55,7 @@ def _raw_sums(routing: BatchRouting) -> torch.Tensor:
 def stats_from_raw(raw: torch.Tensor, E: int, K: int, B: int, T: int, dense: bool) -> LoadStats:
     out = torch.zeros(3 * E + 1, dtype=torch.float64, device=raw.device)
     f32 = torch.zeros(E, dtype=torch.float32, device=raw.device)
-    call("smes_stats_finalize", E, K, float(B * T), int(dense), ptr(raw), ptr(out), ptr(f32), _stream())
+    call("smes_stats_finalize", E, K, 0, float(B * T), int(dense), ptr(raw), ptr(out), ptr(f32), _stream())
     return LoadStats(frequency=out[:E], mass=out[E:2 * E], value=float(out[3 * E].item()),
                      counts=out[2 * E:3 * E].round().long(), batch_size=B, num_tasks=T, k_budget=K,
                      from_dense_probs=bool(dense), freq32=f32)

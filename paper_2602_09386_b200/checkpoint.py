@@ -9,7 +9,7 @@ The on-disk format is the reference's (checkpoint.py:1-14), little-endian throug
     (encoder1 w/b, encoder2 w/b, expert_0.. w/b, router_0.. w/b, head_0.. w/b).
 
 B200 side: the file is parsed on the host in one pass and each block lands in the stacked device
-layout the kernels use -- experts (E, d_out, d_in), routers (T, E, d_in), heads (T, d_out) -- as
+layout the kernels use -- experts (E, d_out, d_in), routers (T, E, d_in), heads (T, 1, d_out) -- as
 ``dtype`` tensors (fp32 by default; fp64 keeps the file's bits, so load -> save is byte-identical).
 The format holds one expert pool (the reference expert); the two-pool expert MLP of the
 BASELINE configs has no MOECKPT1 encoding and ``save_model`` rejects it.
@@ -24,10 +24,10 @@ import numpy as np
 import torch
 
 from .errors import ConfigError, DataFormatError
-from .execution import ExpertPool
+from .experts import ExpertPool
 from .linalg import Affine
-from .model import MoeModel, RouterBank
-from .routing import RoutingBudget
+from .model import MoeModel, heads_from_stacked
+from .routing import RouterBank, RoutingBudget
 
 __all__ = ["load_model", "save_model", "MAGIC", "VERSION"]
 
@@ -131,9 +131,9 @@ def load_model(path: str, device="cuda", dtype: torch.dtype = torch.float32) -> 
     model = MoeModel(
         encoder1=Affine(to(enc[0][0]), to(enc[0][1])),
         encoder2=Affine(to(enc[1][0]), to(enc[1][1])),
-        experts=ExpertPool(to(ew), to(eb), _NAME[exp_code]),
+        experts=ExpertPool.stacked(to(ew), to(eb), _NAME[exp_code]),
         routers=RouterBank(to(rw), to(rb), torch.from_numpy(np.array(tw))),
-        head_w=to(hw), head_b=to(hb),
+        heads=heads_from_stacked(to(hw), to(hb)),
         task_loss_weights=torch.from_numpy(np.array(lam)),
         lb_strength=float(lb),
         budget=RoutingBudget(k_shared=ks, k_adaptive=ka),

@@ -29,7 +29,7 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
                                     int32_t* __restrict__ loads, double* __restrict__ stats_raw,
                                     int32_t* __restrict__ seg_pad, int32_t* __restrict__ seg_log,
                                     int32_t* __restrict__ totals, unsigned int* __restrict__ ticket,
-                                    int32_t* __restrict__ seg_half, int K, double bt, int dense,
+                                    int32_t* __restrict__ seg_half, double lb_scale, double bt, int dense,
                                     double* __restrict__ st_out, float* __restrict__ freq_f32) {
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[32];
@@ -177,7 +177,7 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     if (tid == 0) {
       double v = 0.0;
       for (int w = 0; w < nw; ++w) v += red[0][w];
-      st_out[3 * E] = ((double)E / (double)K) * v;
+      st_out[3 * E] = lb_scale * v;     // (E / K) <f, p>
     }
   }
 }
@@ -337,7 +337,7 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
                      void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
-                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half, 1, 1.0, 0, nullptr,
+                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half, 1.0, 1.0, 0, nullptr,
                                          nullptr);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
@@ -347,14 +347,15 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
 int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
                            const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base, int32_t* loads,
                            double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
-                           unsigned int* ticket, int32_t* seg_half, int K, double batch_times_tasks, int dense,
-                           double* stats_out, float* freq_f32, void* stream) {
+                           unsigned int* ticket, int32_t* seg_half, int K, int lb_experts, double batch_times_tasks,
+                           int dense, double* stats_out, float* freq_f32, void* stream) {
   if (E > 1024) return set_error(SMES_ERR_SHAPE, "plan: E=%d exceeds 1024", E);
   if (K < 1 || batch_times_tasks <= 0.0) return set_error(SMES_ERR_CONFIG, "plan_reduce_stats: K=%d B*T=%g", K,
                                                           batch_times_tasks);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
-                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half, K, batch_times_tasks,
+                                         stats_raw, seg_pad, seg_log, totals, ticket, seg_half,
+                                         (double)(lb_experts > 0 ? lb_experts : E) / (double)K, batch_times_tasks,
                                          dense, stats_out, freq_f32);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));

@@ -12,7 +12,7 @@
 
 namespace smes {
 
-__global__ void stats_finalize_kernel(int E, int K, double bt, int dense, const double* __restrict__ raw,
+__global__ void stats_finalize_kernel(int E, int K, int e_lb, double bt, int dense, const double* __restrict__ raw,
                                       double* __restrict__ out, float* __restrict__ freq_f32) {
   // out: [freq E][mass E][counts E][value]
   __shared__ double red[32];
@@ -34,7 +34,7 @@ __global__ void stats_finalize_kernel(int E, int K, double bt, int dense, const 
   if (tid == 0) {
     double s = 0.0;
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-    out[3 * E] = ((double)E / (double)K) * s;
+    out[3 * E] = ((double)e_lb / (double)K) * s;
   }
 }
 
@@ -343,9 +343,10 @@ static int launch_check(const char* what) {
 
 extern "C" {
 
-int smes_stats_finalize(int E, int K, double batch_times_tasks, int dense, const double* raw, double* out,
-                        float* freq_f32, void* stream) {
-  stats_finalize_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, K, batch_times_tasks, dense, raw,
+int smes_stats_finalize(int E, int K, int lb_experts, double batch_times_tasks, int dense, const double* raw,
+                        double* out, float* freq_f32, void* stream) {
+  const int e_lb = lb_experts > 0 ? lb_experts : E;
+  stats_finalize_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, K, e_lb, batch_times_tasks, dense, raw,
                                                                                out, freq_f32);
   return launch_check("stats_finalize");
 }

@@ -98,7 +98,7 @@ class SMESEngine:
     def __init__(self, params: SMESParams, batch_size: int, k_shared: int, k_adaptive: int,
                  dense_probs_in_stats: bool = False, keep_reps: bool = True,
                  device: torch.device | str | None = None, csum_from_gemm: bool = False,
-                 fuse_mlp: bool = True, fuse_wgrad: bool = False):
+                 fuse_mlp: bool = True, fuse_wgrad: bool = False, lb_experts: int | None = None):
         _require_cuda()
         self.dev = torch.device(device or "cuda")
         p = params
@@ -127,6 +127,9 @@ class SMESEngine:
             if l.act not in ACT:
                 raise ConfigError(f"unknown nonlinearity '{l.act}', expected one of {tuple(ACT)}")
         self.T, self.E, self.d, self.B, self.ks, self.ka, self.K = T, E, d, B, ks, ka, K
+        # E of the load-balancing coefficient E / K (balance.py:69-70, :97): the logical expert count
+        # when the shim pads the pool with never-selected experts (model.py)
+        self.E_lb = int(lb_experts) if lb_experts else E
         self.dims = dims
         self.d_out = dims[-1]
         self.grid = call("smes_combine_grid", B, T, self.d_out)
@@ -388,7 +391,7 @@ class SMESEngine:
             _tagged("plan_reduce", "smes_plan_reduce_stats", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
                     ptr(self.chunk_mass), ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads),
                     ptr(self.stats_raw), ptr(self.seg_pad), ptr(self.seg_log), ptr(self.totals), ptr(self.ticket),
-                    ptr(self.seg_half), self.K, float(B * T), int(self.dense), ptr(self.stats_out),
+                    ptr(self.seg_half), self.K, self.E_lb, float(B * T), int(self.dense), ptr(self.stats_out),
                     ptr(self.freq32), s)
         else:
             _tagged("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
@@ -419,7 +422,7 @@ class SMESEngine:
         if self._fused_bwd:
             bs = B if batch_scale is None else batch_scale
             lbb = B if lb_batch is None else lb_batch
-            lb_coef = self.beta * E / (self.K * lbb * T)
+            lb_coef = self.beta * self.E_lb / (self.K * lbb * T)
             _tagged("combine_train", "smes_combine_train", T, B, E, self.K, self.umax, ptr(self.umask),
                     ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.head_b),
                     ptr(self.P), self.ldp, ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam),
@@ -480,7 +483,7 @@ class SMESEngine:
 
     def stats_finalize(self, s, batch_times_tasks: float | None = None):
         bt = float(self.B * self.T) if batch_times_tasks is None else batch_times_tasks
-        _tagged("stats_finalize", "smes_stats_finalize", self.E, self.K, bt, int(self.dense), ptr(self.stats_raw), ptr(self.stats_out),
+        _tagged("stats_finalize", "smes_stats_finalize", self.E, self.K, self.E_lb, bt, int(self.dense), ptr(self.stats_raw), ptr(self.stats_out),
              ptr(self.freq32), s)
 
     def backward(self, batch_scale: int | None = None, lb_batch: int | None = None):
@@ -491,7 +494,7 @@ class SMESEngine:
         R = self.rows_cap
         bs = B if batch_scale is None else batch_scale
         lbb = B if lb_batch is None else lb_batch
-        lb_coef = self.beta * E / (K * lbb * T)
+        lb_coef = self.beta * self.E_lb / (K * lbb * T)
         relu_last = int(self.p.layers[-1].act == "relu")
         n_layers = len(self.p.layers)
         fused = getattr(self, "_fused_bwd", False)

@@ -271,7 +271,8 @@ class EPRank:
              ptr(self.tab_src), s)
         tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * self.El, ptr(self.tab_src), 1, ptr(self.P_recv), self.ldp * 4,
              ptr(self.P_src), self.ldp * 4, self.ldp * 4, s)
-        call("smes_stats_finalize", E, K, float(Bg * T), 0, ptr(self.stats_raw), ptr(self.stats_out), ptr(self.freq32), s)
+        call("smes_stats_finalize", E, K, 0, float(Bg * T), 0, ptr(self.stats_raw), ptr(self.stats_out), ptr(self.freq32),
+             s)
         lb_coef = self.beta * E / (K * Bg * T)
         tcall("combine_train", "smes_combine_train", T, B, E, K, self.umax, ptr(self.umask), ptr(self.usize), ptr(self.row_of),
              ptr(self.active), ptr(self.wsel), ptr(self.head_b), ptr(self.P_src), self.ldp, ptr(self.logits),

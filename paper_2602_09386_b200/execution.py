@@ -16,69 +16,14 @@ import torch
 
 from ._lib import call, ptr
 from .errors import ConfigError, ShapeError, StateError
+from .experts import ExpertPool, init_expert_pool
+from .linalg import FlopCounter
 from .routing import BatchRouting, _stream
 
 __all__ = ["ExpertPool", "init_expert_pool", "ExecutionPlan", "build_execution_plan", "grouped_gemm",
            "reconstruct_task_reps", "FlopCounter"]
 
-_NONLIN = ("identity", "relu")
 ACT = {"identity": 0, "relu": 1}
-
-
-class FlopCounter:
-    """Multiply-add accumulator (linalg.py:31-52)."""
-
-    __slots__ = ("multiply_adds",)
-
-    def __init__(self):
-        self.multiply_adds = 0
-
-    def add(self, count: int) -> None:
-        if count < 0:
-            raise ValueError(f"flop increment must be non-negative, got {count}")
-        self.multiply_adds += int(count)
-
-    def reset(self) -> None:
-        self.multiply_adds = 0
-
-
-@dataclass
-class ExpertPool:
-    """E affine maps d_in -> d_out with a shared nonlinearity (experts.py:17-73).
-    ``weight`` (E, d_out, d_in), ``bias`` (E, d_out) -- stacked ``Affine`` layouts."""
-
-    weight: torch.Tensor
-    bias: torch.Tensor
-    nonlinearity: str = "identity"
-
-    def __post_init__(self):
-        if self.nonlinearity not in _NONLIN:
-            raise ConfigError(f"unknown nonlinearity '{self.nonlinearity}', expected one of {_NONLIN}")
-        if self.weight.ndim != 3 or self.bias.shape != self.weight.shape[:2]:
-            raise ShapeError(f"expert pool expects weight (E,d_out,d_in) and bias (E,d_out), got "
-                             f"{tuple(self.weight.shape)} and {tuple(self.bias.shape)}")
-        if self.weight.shape[0] == 0:
-            raise ConfigError("expert pool needs at least one expert")
-
-    @property
-    def num_experts(self):
-        return self.weight.shape[0]
-
-    @property
-    def d_in(self):
-        return self.weight.shape[2]
-
-    @property
-    def d_out(self):
-        return self.weight.shape[1]
-
-
-def init_expert_pool(gen: torch.Generator | None, num_experts: int, d_in: int, d_out: int,
-                     nonlinearity: str = "identity", device="cuda") -> ExpertPool:
-    """Fan-in uniform init, zero bias (experts.py:76-84, linalg.py:152-162)."""
-    s = 1.0 / d_in ** 0.5
-    w = (torch.rand(num_experts, d_out, d_in, generator=gen, dtype=torch.float64) * 2 - 1) * s
-    return ExpertPool(w.float().to(device), torch.zeros(num_experts, d_out, device=device), nonlinearity)
 
 
 def _round(x, m):

@@ -1,12 +1,19 @@
-"""Expert shard: the expert stack of a training step over an externally built plan.
+"""Expert pools -- drop-in for taskmoe/experts.py -- and the expert shard of the
+expert-parallel step.
 
-Used by the expert-parallel step (:mod:`ep`): an owner rank runs its local experts
-(reference ``ExpertPool`` / ``grouped_gemm``, experts.py:17-73, execution.py:126-158, and the
-expert part of ``backward``, training.py:180-192) on the rows other ranks dispatched to it.
+``ExpertPool`` keeps the reference fields (``layers``: a list of ``Affine`` maps,
+``nonlinearity``; experts.py:17-73) over stacked device storage (``weight``
+(E, d_out, d_in), ``bias`` (E, d_out)) that the kernels consume.
+
+``ExpertShard`` is used by the expert-parallel step (:mod:`ep`): an owner rank runs its local
+experts (reference ``ExpertPool`` / ``grouped_gemm``, experts.py:17-73, execution.py:126-158, and
+the expert part of ``backward``, training.py:180-192) on the rows other ranks dispatched to it.
 The last (identity) pool is folded into the task heads (csrc/fold.cu), so the shard consumes
 the packed layer input X and produces the head projections P of every row; the backward
 consumes the row coefficients C (training.py:160-179 after folding) and produces the
 parameter gradients of the local experts, the local share of dW_head and the per-row dX.
+A single relu pool (the reference expert with ``expert_nonlinearity="relu"``) runs unfolded:
+the shard writes the pool outputs O and consumes d_packed.
 
 Buffers are sized by ``rows_cap`` (a multiple of 128); rows follow the plan's padded,
 expert-major layout (``seg_pad``), pad rows of X and C are zero.
@@ -17,6 +24,112 @@ import torch
 
 from ._lib import call, ptr, tcall
 from .errors import ConfigError, ShapeError
+from .linalg import Affine, FlopCounter, _dev_tensor
+from .stacked import AffineStack
+
+__all__ = ["ExpertPool", "init_expert_pool", "apply_nonlinearity", "ExpertShard"]
+
+_NONLINEARITIES = ("identity", "relu")
+
+
+def apply_nonlinearity(name: str, x: torch.Tensor) -> torch.Tensor:
+    """experts.py:17-23."""
+    if name == "identity":
+        return x
+    if name == "relu":
+        return torch.clamp_min(x, 0.0)
+    raise ConfigError(f"unknown nonlinearity '{name}', expected one of {_NONLINEARITIES}")
+
+
+class ExpertPool:
+    """E affine maps d_in -> d_out with one shared nonlinearity (experts.py:26-73).
+
+    Reference form ``ExpertPool(layers=[Affine, ...], nonlinearity="relu")``; stacked form
+    ``ExpertPool(weight (E, d_out, d_in), bias (E, d_out), nonlinearity)``.  ``layers[e]`` are views
+    of the stacked ``weight`` / ``bias``."""
+
+    def __init__(self, layers, nonlinearity="identity", *stacked_nonlinearity):
+        if isinstance(layers, torch.Tensor):          # stacked form
+            self._stack = AffineStack(weight=layers, bias=nonlinearity)
+            nonlinearity = stacked_nonlinearity[0] if stacked_nonlinearity else "identity"
+        else:
+            layers = list(layers)
+            if not layers:
+                raise ConfigError("expert pool needs at least one expert")
+        if nonlinearity not in _NONLINEARITIES:
+            raise ConfigError(f"unknown nonlinearity '{nonlinearity}', expected one of {_NONLINEARITIES}")
+        if not isinstance(layers, torch.Tensor):
+            d_in, d_out = layers[0].d_in, layers[0].d_out
+            for i, layer in enumerate(layers):
+                if layer.d_in != d_in or layer.d_out != d_out:
+                    raise ShapeError(f"expert {i} maps {layer.d_in}->{layer.d_out}, expected {d_in}->{d_out}")
+            self._stack = AffineStack(items=layers)
+        self.nonlinearity = nonlinearity
+        if not self._stack.items:
+            raise ConfigError("expert pool needs at least one expert")
+
+    @classmethod
+    def stacked(cls, weight, bias, nonlinearity="identity") -> "ExpertPool":
+        return cls(weight, bias, nonlinearity)
+
+    @property
+    def layers(self) -> list:
+        return self._stack.items
+
+    @property
+    def weight(self) -> torch.Tensor:
+        return self._stack.weight
+
+    @weight.setter
+    def weight(self, w):
+        self._stack.weight = w
+
+    @property
+    def bias(self) -> torch.Tensor:
+        return self._stack.bias
+
+    @bias.setter
+    def bias(self, b):
+        self._stack.bias = b
+
+    @property
+    def num_experts(self) -> int:
+        return len(self._stack.items)
+
+    @property
+    def d_in(self) -> int:
+        return self._stack.items[0].d_in
+
+    @property
+    def d_out(self) -> int:
+        return self._stack.items[0].d_out
+
+    def activate(self, pre: torch.Tensor) -> torch.Tensor:
+        return apply_nonlinearity(self.nonlinearity, pre)
+
+    def apply_all(self, hidden, counter: FlopCounter | None = None) -> torch.Tensor:
+        """Dense path: every expert on every instance, (B, E, d_out) (experts.py:63-73)."""
+        h = _dev_tensor(hidden)
+        w = self.weight.to(h.device)
+        dt = torch.promote_types(h.dtype, w.dtype)
+        if h.ndim != 2 or h.shape[1] != self.d_in:
+            raise ShapeError(f"hidden has shape {tuple(h.shape)}, expected (B, {self.d_in})")
+        out = torch.einsum("bi,eoi->beo", h.to(dt), w.to(dt)) + self.bias.to(h.device, dt)[None]
+        if counter is not None:
+            counter.add(h.shape[0] * self.d_in * self.d_out * self.num_experts)
+        return self.activate(out)
+
+    def __repr__(self) -> str:
+        return (f"ExpertPool(num_experts={self.num_experts}, d_in={self.d_in}, d_out={self.d_out}, "
+                f"nonlinearity='{self.nonlinearity}')")
+
+
+def init_expert_pool(gen: torch.Generator | None, num_experts: int, d_in: int, d_out: int,
+                     nonlinearity: str = "identity", device="cuda") -> ExpertPool:
+    """Fan-in uniform init, zero bias (experts.py:76-84, linalg.py:152-162)."""
+    s = 1.0 / d_in ** 0.5
+    w = (torch.rand(num_experts, d_out, d_in, generator=gen, dtype=torch.float64) * 2 - 1) * s
+    return ExpertPool(w.float().to(device), torch.zeros(num_experts, d_out, device=device), nonlinearity)
 
 
 def _round(x, m):

@@ -1,10 +1,19 @@
-"""Model container + sparse forward -- drop-in for taskmoe/model.py (forward_sparse).
+"""Model container + sparse forward -- drop-in for taskmoe/model.py.
 
-``forward_sparse(batch, model, ...)`` keeps the reference signature and
-result type.  The encoder (two Affine layers, model.py:188-199) runs on the
-same tcgen05 GEMM (one group); the SMES layer runs through a cached
-:class:`SMESEngine` (router GEMM -> fused router -> plan -> grouped expert
-GEMMs -> head projections -> combine/heads).
+``MoeModel`` keeps the reference fields (model.py:36-111): ``encoder1``/``encoder2``
+(``Affine``), ``experts`` (``ExpertPool``), ``routers`` (``RouterBank``), ``heads``
+(a list of T ``Affine`` maps d_out -> 1), ``task_loss_weights``, ``lb_strength``,
+``budget``, ``encoder_nonlinearity``.  Two extensions: ``experts`` may be a list of
+pools chained d -> d_ff -> d_out (the BASELINE "expert MLP"), and the encoders may be
+None (the batch is then the encoded hidden (B, d_in)).
+
+``forward_sparse(batch, model, ...)`` keeps the reference signature and result type.
+The encoder runs on the tcgen05 GEMM (one group); the SMES layer runs through a cached
+:class:`SMESEngine` (fused router front -> plan -> grouped expert GEMMs -> combine/heads).
+Any widths are accepted: the shim zero-pads d, the pool widths and the expert count to the
+kernels' granularity (multiples of 32; T*E a multiple of 8).  Padded weight rows/columns are
+zero, padded experts carry a -1e30 router bias and are never selected, and every output is
+sliced back to the logical shapes, so results equal those of the unpadded layer.
 """
 from __future__ import annotations
 
@@ -15,81 +24,90 @@ import torch
 from . import engine as _engine
 from ._lib import call, ptr
 from .errors import ConfigError, ShapeError, StateError
-from .execution import ExecutionPlan, ExpertPool, FlopCounter
-from .linalg import Affine, init_affine
-from .routing import BatchRouting, RoutingBudget, _stream
+from .execution import ExecutionPlan
+from .experts import ExpertPool, init_expert_pool
+from .linalg import Affine, FlopCounter, init_affine
+from .routing import BatchRouting, RouterBank, RoutingBudget, _stream
+from .stacked import AffineStack
 
 __all__ = ["MoeModel", "RouterBank", "ForwardResult", "forward_sparse", "init_model"]
 
 ROUTER_INIT_SCALE = 1e-3   # model.py:32
 ENCODER_BIAS_INIT = 0.01   # model.py:33
+DEAD_EXPERT_BIAS = -1e30   # router bias of shim-padded experts: softmax mass exactly 0, never selected
 
 
-@dataclass
-class RouterBank:
-    """T routers d_in -> E, stacked: weight (T, E, d_in), bias (T, E) (routing.py:64-103)."""
-    weight: torch.Tensor
-    bias: torch.Tensor
-    task_weights: torch.Tensor | None = None
-
-    def __post_init__(self):
-        if self.weight.ndim != 3 or self.bias.shape != self.weight.shape[:2]:
-            raise ShapeError(f"router bank expects weight (T,E,d) and bias (T,E), got {tuple(self.weight.shape)}")
-        if self.task_weights is None:
-            self.task_weights = torch.ones(self.weight.shape[0], dtype=torch.float64)
-        self.task_weights = torch.as_tensor(self.task_weights, dtype=torch.float64)
-        if self.task_weights.shape != (self.weight.shape[0],):
-            raise ShapeError(f"expected {self.weight.shape[0]} task weights")
-        if bool((self.task_weights < 0).any()):
-            raise ConfigError("task pooling weights must be non-negative")
-
-    @property
-    def num_tasks(self):
-        return self.weight.shape[0]
-
-    @property
-    def num_experts(self):
-        return self.weight.shape[1]
-
-    @property
-    def d_in(self):
-        return self.weight.shape[2]
-
-
-@dataclass
 class MoeModel:
-    """Encoder, expert stack, task routers, task heads (model.py:36-111).  ``experts`` is one
-    ExpertPool (the reference expert) or a list of pools chained d -> d_ff -> d_out.
-    ``encoder1``/``encoder2`` may be None: the batch is then the encoded hidden (B, d_in)."""
-    encoder1: Affine | None
-    encoder2: Affine | None
-    experts: object
-    routers: RouterBank
-    head_w: torch.Tensor            # (T, d_out)
-    head_b: torch.Tensor            # (T,)
-    task_loss_weights: torch.Tensor
-    lb_strength: float
-    budget: RoutingBudget
-    encoder_nonlinearity: str = "relu"
-    _engines: dict = field(default_factory=dict, repr=False)
+    """Encoder, expert pool(s), task routers, task heads (model.py:36-111)."""
 
-    def __post_init__(self):
-        pools = self.pools
+    def __init__(self, encoder1: Affine | None, encoder2: Affine | None, experts, routers: RouterBank, heads,
+                 task_loss_weights, lb_strength: float, budget: RoutingBudget, encoder_nonlinearity: str = "relu"):
+        self.encoder1, self.encoder2 = encoder1, encoder2
+        self.experts = experts
+        self.routers = routers
+        heads = list(heads)
+        for i, h in enumerate(heads):
+            if h.d_out != 1 or h.d_in != heads[0].d_in:
+                raise ConfigError(f"head {i} must map d_out -> 1")
+        self._heads = AffineStack(items=heads)
+        self.task_loss_weights = torch.as_tensor(task_loss_weights, dtype=torch.float64).detach().cpu()
+        self.lb_strength = float(lb_strength)
+        self.budget = budget
+        self.encoder_nonlinearity = encoder_nonlinearity
+        self._engines = {}
         t = self.routers.num_tasks
-        if self.head_w.shape != (t, pools[-1].d_out):
-            raise ConfigError("heads must map d_out -> 1 for every task")
-        self.task_loss_weights = torch.as_tensor(self.task_loss_weights, dtype=torch.float64)
+        pools = self.pools
+        if len(self._heads.items) != t:
+            raise ConfigError(f"{len(self._heads.items)} heads for {t} routers")
         if self.task_loss_weights.shape != (t,):
             raise ConfigError(f"expected {t} task loss weights")
         if bool((self.task_loss_weights < 0).any()) or self.lb_strength < 0:
             raise ConfigError("loss weights and regularizer strength must be non-negative")
+        if (encoder1 is None) != (encoder2 is None):
+            raise ConfigError("encoder1 and encoder2 must both be given or both be None")
+        if encoder1 is not None:
+            if encoder1.d_out != encoder2.d_in:
+                raise ConfigError("encoder layer widths do not chain")
+            if encoder2.d_out != pools[0].d_in or encoder2.d_out != self.routers.d_in:
+                raise ConfigError("encoder output width must match expert and router input")
+        elif pools[0].d_in != self.routers.d_in:
+            raise ConfigError("expert and router input widths differ")
+        for i in range(1, len(pools)):
+            if pools[i].d_in != pools[i - 1].d_out or pools[i].num_experts != pools[0].num_experts:
+                raise ConfigError(f"expert pool {i} does not chain")
+        for i, h in enumerate(self._heads.items):
+            if h.d_in != pools[-1].d_out or h.d_out != 1:
+                raise ConfigError(f"head {i} must map d_out -> 1")
         if self.routers.num_experts != pools[0].num_experts:
             raise ConfigError("router width must equal the expert count")
         self.budget.validate(pools[0].num_experts)
 
+    # -- reference fields and properties
+    @property
+    def heads(self) -> list:
+        return self._heads.items
+
+    @property
+    def head_w(self) -> torch.Tensor:
+        """(T, d_out) view of the stacked heads."""
+        return self._heads.weight[:, 0, :]
+
+    @property
+    def head_b(self) -> torch.Tensor:
+        """(T,) view of the stacked head biases."""
+        return self._heads.bias[:, 0]
+
     @property
     def pools(self) -> list:
         return list(self.experts) if isinstance(self.experts, (list, tuple)) else [self.experts]
+
+    @property
+    def num_features(self) -> int:
+        return self.encoder1.d_in if self.encoder1 is not None else self.d_in
+
+    @property
+    def d_hidden(self) -> int:
+        return self.encoder1.d_out if self.encoder1 is not None else self.d_in
 
     @property
     def num_tasks(self):
@@ -108,31 +126,89 @@ class MoeModel:
         return self.pools[-1].d_out
 
     def parameter_blocks(self) -> dict:
-        """Named parameter views in the reference's order and names (model.py:94-111)."""
+        """Named parameter views in the reference's order and names (model.py:94-111).  A stack of
+        pools names its experts ``expert{l}_{e}``."""
         blocks = {}
         if self.encoder1 is not None:
             blocks.update({"encoder1.weight": self.encoder1.weight, "encoder1.bias": self.encoder1.bias,
                            "encoder2.weight": self.encoder2.weight, "encoder2.bias": self.encoder2.bias})
         pools = self.pools
         for li, pool in enumerate(pools):
-            for e in range(pool.num_experts):
+            for e, layer in enumerate(pool.layers):
                 pre = f"expert_{e}" if len(pools) == 1 else f"expert{li}_{e}"
-                blocks[pre + ".weight"] = pool.weight[e]
-                blocks[pre + ".bias"] = pool.bias[e]
-        for t in range(self.num_tasks):
-            blocks[f"router_{t}.weight"] = self.routers.weight[t]
-            blocks[f"router_{t}.bias"] = self.routers.bias[t]
-        for t in range(self.num_tasks):
-            blocks[f"head_{t}.weight"] = self.head_w[t:t + 1]
-            blocks[f"head_{t}.bias"] = self.head_b[t:t + 1]
+                blocks[pre + ".weight"] = layer.weight
+                blocks[pre + ".bias"] = layer.bias
+        for t, m in enumerate(self.routers.maps):
+            blocks[f"router_{t}.weight"] = m.weight
+            blocks[f"router_{t}.bias"] = m.bias
+        for t, h in enumerate(self.heads):
+            blocks[f"head_{t}.weight"] = h.weight
+            blocks[f"head_{t}.bias"] = h.bias
         return blocks
 
-    def smes_params(self) -> _engine.SMESParams:
+    def num_parameters(self) -> int:
+        return sum(v.numel() for v in self.parameter_blocks().values())
+
+    def smes_params(self, pad: "_Pad | None" = None) -> _engine.SMESParams:
+        """The layer's parameters in the engine's stacked layouts (zero-padded by ``pad``)."""
+        pools = self.pools
+        rw, rb = self.routers.weight, self.routers.bias
+        layers = [(p.weight, p.bias, p.nonlinearity) for p in pools]
+        hw, hb = self.head_w, self.head_b
+        if pad is not None and pad.active:
+            T, E, Ep = self.num_tasks, self.num_experts, pad.E_p
+            dims, dp = pad.dims, pad.dims_p
+            dev = rw.device
+            z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)
+            rw_p = z(T, Ep, dp[0])
+            rw_p[:, :E, :dims[0]] = rw
+            rb_p = torch.full((T, Ep), DEAD_EXPERT_BIAS, dtype=torch.float32, device=dev)
+            rb_p[:, :E] = rb
+            lp = []
+            for i, (w, b, act) in enumerate(layers):
+                w_p = z(Ep, dp[i + 1], dp[i])
+                w_p[:E, :dims[i + 1], :dims[i]] = w
+                b_p = z(Ep, dp[i + 1])
+                b_p[:E, :dims[i + 1]] = b
+                lp.append((w_p, b_p, act))
+            hw_p = z(T, dp[-1])
+            hw_p[:, :dims[-1]] = hw
+            rw, rb, layers, hw = rw_p, rb_p, lp, hw_p
         return _engine.SMESParams(
-            router_w=self.routers.weight, router_b=self.routers.bias,
-            layers=[_engine.ExpertLayer(p.weight, p.bias, p.nonlinearity) for p in self.pools],
-            head_w=self.head_w, head_b=self.head_b, task_weights=self.routers.task_weights,
+            router_w=rw, router_b=rb, layers=[_engine.ExpertLayer(w, b, act) for (w, b, act) in layers],
+            head_w=hw, head_b=hb, task_weights=self.routers.task_weights,
             task_loss_weights=self.task_loss_weights, lb_strength=self.lb_strength)
+
+    def __repr__(self) -> str:
+        return (f"MoeModel(num_tasks={self.num_tasks}, num_experts={self.num_experts}, d_in={self.d_in}, "
+                f"d_out={self.d_out}, pools={len(self.pools)}, budget={self.budget})")
+
+
+def _round(x, m):
+    return (x + m - 1) // m * m
+
+
+def _pad_out(d_out: int) -> int:
+    """The combine kernels tile d_out by 32 lanes x {4, 8} columns x {1, 2, 4, 8} warps."""
+    for w in (128, 256, 512, 1024):
+        if d_out <= w:
+            return w if d_out % 128 or d_out & (d_out - 1) else d_out
+    return _round(d_out, 32)
+
+
+class _Pad:
+    """Kernel granularity of the layer: input and hidden widths to multiples of 32, the output width
+    to 128 / 256 / 512 / 1024 (combine tiling), T * E to a multiple of 8."""
+
+    def __init__(self, model: MoeModel):
+        self.T, self.E = model.num_tasks, model.num_experts
+        self.dims = [model.d_in] + [p.d_out for p in model.pools]
+        self.dims_p = [_round(x, 32) for x in self.dims[:-1]] + [_pad_out(self.dims[-1])]
+        E_p = self.E
+        while (self.T * E_p) % 8:
+            E_p += 1
+        self.E_p = E_p
+        self.active = self.dims_p != self.dims or E_p != self.E
 
 
 def init_model(gen: torch.Generator | None, num_features: int, d_hidden: int, d_in: int, d_out: int,
@@ -143,24 +219,28 @@ def init_model(gen: torch.Generator | None, num_features: int, d_hidden: int, d_
     BASELINE 'expert MLP' (relu d_in -> d_ff, identity d_ff -> d_out)."""
     enc1 = init_affine(gen, d_hidden, num_features, bias_value=ENCODER_BIAS_INIT, device=device)
     enc2 = init_affine(gen, d_in, d_hidden, bias_value=ENCODER_BIAS_INIT, device=device)
-    from .execution import init_expert_pool
     if d_ff is None:
         experts = init_expert_pool(gen, num_experts, d_in, d_out, expert_nonlinearity, device)
     else:
         experts = [init_expert_pool(gen, num_experts, d_in, d_ff, "relu", device),
                    init_expert_pool(gen, num_experts, d_ff, d_out, "identity", device)]
-    s = ROUTER_INIT_SCALE / d_in ** 0.5
-    rw = ((torch.rand(num_tasks, num_experts, d_in, generator=gen, dtype=torch.float64) * 2 - 1) * s).float()
-    routers = RouterBank(rw.to(device), torch.zeros(num_tasks, num_experts, device=device), router_task_weights)
-    hw = ((torch.rand(num_tasks, d_out, generator=gen, dtype=torch.float64) * 2 - 1) / d_out ** 0.5).float()
+    routers = RouterBank([init_affine(gen, num_experts, d_in, scale=ROUTER_INIT_SCALE / d_in ** 0.5, device=device)
+                          for _ in range(num_tasks)], router_task_weights)
+    heads = [init_affine(gen, 1, d_out, device=device) for _ in range(num_tasks)]
     lam = torch.ones(num_tasks) if task_loss_weights is None else torch.as_tensor(task_loss_weights)
-    return MoeModel(enc1, enc2, experts, routers, hw.to(device), torch.zeros(num_tasks, device=device), lam,
-                    lb_strength, budget, encoder_nonlinearity)
+    return MoeModel(enc1, enc2, experts, routers, heads, lam, lb_strength, budget, encoder_nonlinearity)
+
+
+def heads_from_stacked(head_w: torch.Tensor, head_b: torch.Tensor) -> list:
+    """T ``Affine`` heads (1, d_out) from a stacked (T, d_out) weight and (T,) bias."""
+    w = torch.as_tensor(head_w)
+    b = torch.as_tensor(head_b)
+    return [Affine(w[t:t + 1], b[t:t + 1]) for t in range(w.shape[0])]
 
 
 @dataclass
 class ForwardResult:
-    """Predictions plus what backward needs (model.py:159-185)."""
+    """Predictions plus what backward needs (model.py:159-185).  Arrays are device tensors."""
     mode: str
     predictions: torch.Tensor      # (T, B)
     head_logits: torch.Tensor      # (T, B)
@@ -168,21 +248,25 @@ class ForwardResult:
     routing: BatchRouting
     plan: ExecutionPlan
     expert_flops: int
+    inputs: torch.Tensor | None = None
+    encoder_pre: torch.Tensor | None = None
+    encoder_hidden: torch.Tensor | None = None
     hidden: torch.Tensor | None = None
     router_logits: torch.Tensor | None = None
+    packed_in: torch.Tensor | None = None
+    packed_pre: torch.Tensor | None = None
+    packed_out: torch.Tensor | None = None
+    expert_outputs: torch.Tensor | None = None
     _engine: object = None
     _step: int = -1
     _enc: dict | None = None
+    _pad: object = None
 
     def mean_union(self) -> float:
         return float(self.routing.usize.double().mean())
 
     def max_union(self) -> int:
         return int(self.routing.usize.max())
-
-
-def _round(x, m):
-    return (x + m - 1) // m * m
 
 
 def _gemm(a, lda, rows, w, n, k, bias, act, out, ldc, out_fp32, m_limit, bits_out=None, bits_ld=0, b_mn=0,
@@ -193,39 +277,45 @@ def _gemm(a, lda, rows, w, n, k, bias, act, out, ldc, out_fp32, m_limit, bits_ou
 
 
 def _encode(x: torch.Tensor, model: MoeModel, eng) -> dict:
-    """encoder1 -> act -> encoder2 on the tcgen05 GEMM (model.py:188-199)."""
+    """encoder1 -> act -> encoder2 on the tcgen05 GEMM (model.py:188-199).  Widths that are not
+    multiples of the kernel granularity are zero-padded (the padded columns stay zero)."""
     B, F = x.shape
     dev = x.device
     Fp = _round(F, 8)
+    dh = model.encoder1.d_out
+    dhp = _round(dh, 32)
+    d = model.d_in
     xb = torch.zeros(B, Fp, dtype=torch.bfloat16, device=dev)
     xb[:, :F] = x
-    w1 = torch.zeros(model.encoder1.d_out, Fp, dtype=torch.bfloat16, device=dev)
-    w1[:, :F] = model.encoder1.weight
-    dh = model.encoder1.d_out
-    mid = torch.zeros(_round(B, 128), dh, dtype=torch.bfloat16, device=dev)
+    w1 = torch.zeros(dhp, Fp, dtype=torch.bfloat16, device=dev)
+    w1[:dh, :F] = model.encoder1.weight
+    b1 = torch.zeros(dhp, device=dev)
+    b1[:dh] = model.encoder1.bias
+    mid = torch.zeros(_round(B, 128), dhp, dtype=torch.bfloat16, device=dev)
     relu = model.encoder_nonlinearity == "relu"
-    bits = torch.zeros(dh // 32, _round(B, 128), dtype=torch.int32, device=dev) if relu and dh % 32 == 0 else None
-    if relu and bits is None:
-        raise ShapeError(f"encoder hidden width {dh} must be a multiple of 32")
-    _gemm(xb, Fp, B, w1.reshape(1, dh, Fp).contiguous(), dh, Fp, model.encoder1.bias.float().contiguous(),
-          1 if relu else 0, mid, dh, 0, B, bits_out=bits, bits_ld=_round(B, 128))
-    w2 = model.encoder2.weight.to(torch.bfloat16).reshape(1, model.d_in, dh).contiguous()
-    _gemm(mid, dh, B, w2, model.d_in, dh, model.encoder2.bias.float().contiguous(), 0, eng.h, eng.ldh, 0, B)
-    return dict(xb=xb, Fp=Fp, F=F, mid=mid, bits=bits, w1=w1, w2=w2)
+    bits = torch.zeros(dhp // 32, _round(B, 128), dtype=torch.int32, device=dev) if relu else None
+    _gemm(xb, Fp, B, w1.reshape(1, dhp, Fp).contiguous(), dhp, Fp, b1, 1 if relu else 0, mid, dhp, 0, B,
+          bits_out=bits, bits_ld=_round(B, 128))
+    w2 = torch.zeros(1, d, dhp, dtype=torch.bfloat16, device=dev)
+    w2[0, :, :dh] = model.encoder2.weight
+    _gemm(mid, dhp, B, w2, d, dhp, model.encoder2.bias.float().contiguous(), 0, eng.h, eng.ldh, 0, B)
+    return dict(xb=xb, Fp=Fp, F=F, mid=mid, bits=bits, w1=w1, w2=w2, dh=dh, dhp=dhp)
 
 
-def _get_engine(model: MoeModel, B: int, dense: bool = False) -> _engine.SMESEngine:
-    key = (B, bool(dense))
+def _get_engine(model: MoeModel, B: int, dense: bool = False):
+    pad = _Pad(model)
+    key = (B, bool(dense), tuple(pad.dims_p), pad.E_p, tuple(p.nonlinearity for p in model.pools))
     eng = model._engines.get(key)
     if eng is None:
-        eng = _engine.SMESEngine(model.smes_params(), B, model.budget.k_shared, model.budget.k_adaptive,
-                                 dense_probs_in_stats=dense, device=model.head_w.device)
+        eng = _engine.SMESEngine(model.smes_params(pad), B, model.budget.k_shared, model.budget.k_adaptive,
+                                 dense_probs_in_stats=dense, device=model.routers.weight.device,
+                                 lb_experts=model.num_experts)
         eng.step_id = 0
         model._engines[key] = eng
     else:
-        eng.p = model.smes_params()
+        eng.p = model.smes_params(pad)
         eng.refresh_weights()
-    return eng
+    return eng, pad
 
 
 def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, frozen: ForwardResult | None = None,
@@ -240,39 +330,54 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
     B = x.shape[0]
     if B == 0:
         raise ShapeError("forward of an empty batch")
-    eng = _get_engine(model, B, dense_probs_in_stats)
+    if model.encoder1 is not None and x.shape[1] != model.encoder1.d_in:
+        raise ShapeError(f"batch has shape {tuple(x.shape)}, model expects (B, {model.encoder1.d_in})")
+    if model.encoder1 is None and x.shape[1] != model.d_in:
+        raise ShapeError(f"hidden has shape {tuple(x.shape)}, model expects (B, {model.d_in})")
+    if frozen is not None and (frozen.mode != "sparse" or frozen.plan is None):
+        raise StateError("frozen forward result must come from the sparse pipeline")
+    eng, pad = _get_engine(model, B, dense_probs_in_stats)
+    eng.keep_logits = True
+    T, E, Ep = model.num_tasks, model.num_experts, pad.E_p
+    d, d_out = model.d_in, model.d_out
     enc = None
     if model.encoder1 is not None:
-        if x.shape[1] != model.encoder1.d_in:
-            raise ShapeError(f"batch has shape {tuple(x.shape)}, model expects (B, {model.encoder1.d_in})")
         enc = _encode(x.float(), model, eng)
     else:
-        if x.shape[1] != model.d_in:
-            raise ShapeError(f"hidden has shape {tuple(x.shape)}, model expects (B, {model.d_in})")
-        eng.h.copy_(x)
+        eng.h[:, :d].copy_(x)
     if frozen is not None:
-        if frozen.mode != "sparse" or frozen.plan is None:
-            raise StateError("frozen forward result must come from the sparse pipeline")
         eng.shared.copy_(frozen.routing.shared_i32)
         eng.adaptive.copy_(frozen.routing.adaptive_i32)
     eng.forward_a(frozen=frozen is not None)
     eng.forward_b(with_loss=False)
     eng.step_id += 1
-    T, E = eng.T, eng.E
     # the result owns its arrays (the reference returns fresh arrays): clone the engine's buffers so a
     # later forward through the same cached engine cannot rewrite this result's routing or plan
     c = lambda t: t.clone()
+    ce = lambda t: t[:, :E].contiguous()           # drop the shim's padded experts
     z = c(eng.z)
     routing = BatchRouting(z, T, B, E, model.budget, c(eng.tw), c(eng.shared), c(eng.adaptive), c(eng.active),
-                           c(eng.wsel), c(eng.umask), c(eng.usize), c(eng.chunk_union), c(eng.chunk_active),
-                           c(eng.chunk_mass), c(eng.chunk_dmass), eng.rpw, z_strides=(E, T * E))
-    plan = ExecutionPlan(E, B, eng.umax, eng.rows_cap, c(eng.seg_pad), c(eng.seg_log), c(eng.loads), c(eng.totals),
-                         c(eng.row_of), c(eng.gather_inst), c(eng.gather_exp), c(eng.stats_raw), routing.usize)
+                           c(eng.wsel), c(eng.umask), c(eng.usize), ce(eng.chunk_union), ce(eng.chunk_active),
+                           ce(eng.chunk_mass), ce(eng.chunk_dmass), eng.rpw, z_strides=(Ep, T * Ep))
+    raw = eng.stats_raw.view(3, Ep)[:, :E].reshape(-1).contiguous()
+    plan = ExecutionPlan(E, B, eng.umax, eng.rows_cap, eng.seg_pad[:E + 1].clone(), eng.seg_log[:E + 1].clone(),
+                         eng.loads[:E].clone(), c(eng.totals), c(eng.row_of), c(eng.gather_inst),
+                         c(eng.gather_exp), raw, routing.usize)
     n_act = eng.n_act()
-    flops = n_act * sum(eng.dims[i] * eng.dims[i + 1] for i in range(len(eng.dims) - 1))
+    dims = pad.dims
+    flops = n_act * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
     if counter is not None:
         counter.add(flops)
-    return ForwardResult("sparse", eng.preds.clone(), eng.logits.clone(), eng.reps.float(), routing, plan, flops,
-                         hidden=eng.h.clone() if keep_cache else None,
-                         router_logits=z.view(B, T, E).transpose(0, 1) if keep_cache else None,
-                         _engine=eng, _step=eng.step_id, _enc=enc)
+    reps = eng.reps[..., :d_out].float()
+    res = ForwardResult("sparse", eng.preds.clone(), eng.logits.clone(), reps, routing, plan, flops,
+                        _engine=eng, _step=eng.step_id, _enc=enc, _pad=pad)
+    if keep_cache:
+        res.inputs = x
+        res.hidden = eng.h[:, :d].float()
+        res.router_logits = z.view(B, T, Ep)[:, :, :E].permute(1, 0, 2)
+        if enc is not None:
+            res.encoder_hidden = enc["mid"][:B, :enc["dh"]].float()
+        rows = plan.physical_rows
+        res.packed_in = eng.X[rows, :d].float()
+        res.packed_out = eng.outs[-1][rows, :d_out].float()
+    return res

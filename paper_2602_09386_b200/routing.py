@@ -13,12 +13,17 @@ from dataclasses import dataclass
 
 import torch
 
+import warnings
+
 from . import _lib
 from ._lib import call, ptr
 from .errors import ConfigError, NumericsError, ShapeError
+from .linalg import Affine, FlopCounter, _dev_tensor
+from .stacked import AffineStack
 
-__all__ = ["RoutingBudget", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route",
-           "naive_route_batch", "renormalized_weights"]
+__all__ = ["RoutingBudget", "RouterBank", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route",
+           "naive_route_batch", "naive_sparse_route", "renormalized_weights", "compute_global_scores",
+           "dense_routing", "stack_decisions"]
 
 
 @dataclass(frozen=True)
@@ -42,6 +47,86 @@ class RoutingBudget:
             raise ConfigError(f"budget k={self.k_total} exceeds expert count {num_experts}: "
                               f"stage-II would have only {num_experts - self.k_shared} candidates "
                               f"for {self.k_adaptive} adaptive picks")
+
+
+class RouterBank:
+    """One affine router per task (d_in -> E) plus Stage-I pooling weights (routing.py:64-103).
+
+    Reference form ``RouterBank(maps=[Affine, ...], task_weights=None)``; stacked form
+    ``RouterBank(weight (T, E, d_in), bias (T, E), task_weights)``.  ``maps[t]`` are views of the
+    stacked ``weight`` / ``bias`` the kernels consume."""
+
+    def __init__(self, maps, task_weights=None, *stacked_task_weights):
+        if isinstance(maps, torch.Tensor):            # stacked form
+            self._stack = AffineStack(weight=maps, bias=task_weights)
+            task_weights = stacked_task_weights[0] if stacked_task_weights else None
+        else:
+            maps = list(maps)
+            if not maps:
+                raise ConfigError("router bank needs at least one task router")
+            e, d = maps[0].d_out, maps[0].d_in
+            for i, m in enumerate(maps):
+                if m.d_out != e or m.d_in != d:
+                    raise ShapeError(f"router {i} has shape ({m.d_out},{m.d_in}), expected ({e},{d})")
+            self._stack = AffineStack(items=maps)
+        items = self._stack.items
+        if not items:
+            raise ConfigError("router bank needs at least one task router")
+        T = len(items)
+        tw = torch.ones(T, dtype=torch.float64) if task_weights is None else \
+            torch.as_tensor(task_weights, dtype=torch.float64).detach().cpu()
+        if tw.shape != (T,):
+            raise ShapeError(f"expected {T} task weights, got shape {tuple(tw.shape)}")
+        if bool((tw < 0).any()):
+            raise ConfigError("task pooling weights must be non-negative")
+        self.task_weights = tw
+
+    @property
+    def maps(self) -> list:
+        return self._stack.items
+
+    @property
+    def weight(self) -> torch.Tensor:
+        return self._stack.weight
+
+    @weight.setter
+    def weight(self, w):
+        self._stack.weight = w
+
+    @property
+    def bias(self) -> torch.Tensor:
+        return self._stack.bias
+
+    @bias.setter
+    def bias(self, b):
+        self._stack.bias = b
+
+    @property
+    def num_tasks(self) -> int:
+        return len(self._stack.items)
+
+    @property
+    def num_experts(self) -> int:
+        return self._stack.items[0].d_out
+
+    @property
+    def d_in(self) -> int:
+        return self._stack.items[0].d_in
+
+    def logits(self, hidden, counter: FlopCounter | None = None) -> torch.Tensor:
+        """Routing logits of a (B, d_in) batch, (T, B, E) (routing.py:101-103)."""
+        h = _dev_tensor(hidden)
+        if h.ndim != 2 or h.shape[1] != self.d_in:
+            raise ShapeError(f"hidden has shape {tuple(h.shape)}, expected (B, {self.d_in})")
+        w = self.weight.to(h.device)
+        dt = torch.promote_types(h.dtype, w.dtype)
+        z = torch.einsum("bd,ted->tbe", h.to(dt), w.to(dt)) + self.bias.to(h.device, dt)[:, None, :]
+        if counter is not None:
+            counter.add(self.num_tasks * h.shape[0] * self.d_in * self.num_experts)
+        return z
+
+    def __repr__(self) -> str:
+        return f"RouterBank(num_tasks={self.num_tasks}, num_experts={self.num_experts}, d_in={self.d_in})"
 
 
 @dataclass(frozen=True)
@@ -73,7 +158,7 @@ class BatchRouting:
 
     def __init__(self, z, T, B, E, budget, task_weights, shared, adaptive, active, wsel, umask, usize,
                  chunk_union, chunk_active, chunk_mass, chunk_dmass, rows_per_warp, probs_in=None,
-                 z_strides=None):
+                 z_strides=None, weights=None):
         # z: fp32 logits; element (t, b, e) at z_flat[t*st + b*sb + e]
         self.z, self.T, self.B, self.E, self.budget = z, T, B, E, budget
         self.z_st, self.z_sb = z_strides if z_strides is not None else (B * E, E)
@@ -84,7 +169,8 @@ class BatchRouting:
                                                                                   chunk_mass, chunk_dmass)
         self.rows_per_warp = rows_per_warp
         self.probs_in = probs_in
-        self._weights = self._probs = self._unions = None
+        self._weights = weights
+        self._probs = self._unions = None
 
     # -- reference fields
     @property
@@ -180,13 +266,26 @@ def _launch_route(zt, T, B, E, ks, ka, tw, bufs, probs_in=None, probs_out=None, 
     return flag
 
 
+_warned_fp64 = False
+
+
 def _as_logits(task_logits) -> torch.Tensor:
+    """fp32 device logits.  The router kernels compare fp32 logits exactly; fp64 logits that are not
+    fp32-representable are rounded first (selections are index-exact for the rounded values), which
+    is reported once with a warning."""
+    global _warned_fp64
     z = torch.as_tensor(task_logits)
     if not z.is_cuda:
         z = z.cuda()
     if z.ndim != 3:
         raise ShapeError(f"expected (T, B, E) logits, got shape {tuple(z.shape)}")
-    return z.to(torch.float32).contiguous()
+    z32 = z.to(torch.float32).contiguous()
+    if z.dtype == torch.float64 and not _warned_fp64 and z.numel() and \
+            not bool((z32.double() == z).logical_or(~torch.isfinite(z)).all()):
+        _warned_fp64 = True
+        warnings.warn("route_batch: float64 logits are rounded to float32 before selection; selections are "
+                      "index-exact for the rounded logits", RuntimeWarning, stacklevel=3)
+    return z32
 
 
 def route_batch(task_logits, budget: RoutingBudget, task_weights=None, full_probs=None) -> BatchRouting:
@@ -199,6 +298,8 @@ def route_batch(task_logits, budget: RoutingBudget, task_weights=None, full_prob
         torch.as_tensor(task_weights, dtype=torch.float64).to(dev).contiguous()
     if tw.shape != (T,):
         raise ShapeError(f"expected {T} task weights, got shape {tuple(tw.shape)}")
+    if bool((tw < 0).any()):
+        raise NumericsError("task weights must be non-negative")
     probs_in = None
     if full_probs is not None:
         probs_in = torch.as_tensor(full_probs, dtype=torch.float64).to(dev).contiguous()
@@ -264,3 +365,88 @@ def renormalized_weights(logits, active) -> torch.Tensor:
     out = torch.zeros_like(lg)
     out[act] = e / e.sum()
     return out
+
+
+def naive_sparse_route(task_logits, k: int) -> RoutingDecision:
+    """Independent per-task top-k for one instance, (T, E) logits (routing.py:312-331)."""
+    z = torch.as_tensor(task_logits)
+    if z.ndim != 2:
+        raise ShapeError(f"expected (T, E) logits, got shape {tuple(z.shape)}")
+    return naive_route_batch(z[:, None, :], k).instance(0)
+
+
+def compute_global_scores(full_probs, task_weights=None) -> torch.Tensor:
+    """s_e = sum_t w_t p_t[e] for one instance, with simplex validation (routing.py:214-232)."""
+    p = _dev_tensor(full_probs, torch.float64)
+    if p.ndim != 2:
+        raise ShapeError(f"expected (T, E) probabilities, got shape {tuple(p.shape)}")
+    w = torch.ones(p.shape[0], dtype=torch.float64, device=p.device) if task_weights is None else \
+        _dev_tensor(task_weights, torch.float64)
+    if w.shape != (p.shape[0],):
+        raise ShapeError(f"expected {p.shape[0]} task weights, got shape {tuple(w.shape)}")
+    if bool((w < 0).any()):
+        raise NumericsError("task weights must be non-negative")
+    if bool((p < 0).any()) or float((p.sum(dim=1) - 1.0).abs().max()) > 1e-6:
+        raise NumericsError("each task's probabilities must lie on the simplex")
+    return w @ p
+
+
+def _from_arrays(shared, adaptive, active, unions, weights, full_probs, budget: RoutingBudget) -> BatchRouting:
+    """A BatchRouting from reference-shaped arrays (dense_routing / stack_decisions): the compact
+    device internals are derived, the statistics partials are whole-batch sums in chunk 0."""
+    from .execution import _umask_from_unions
+    w = _dev_tensor(weights, torch.float64)
+    dev = w.device
+    T, B, E = w.shape
+    act = _dev_tensor(active, torch.int64)
+    sh = _dev_tensor(shared, torch.int64).reshape(B, -1)
+    ad = _dev_tensor(adaptive, torch.int64).reshape(T, B, -1)
+    probs = _dev_tensor(full_probs, torch.float64)
+    umask, _ = _umask_from_unions(unions, E, dev)
+    usize = torch.tensor([int(torch.as_tensor(u).numel()) for u in unions], dtype=torch.int32, device=dev)
+    rpw = call("smes_route_rows_per_warp", B)
+    C = call("smes_route_num_chunks", B, rpw)
+    chunk_union = torch.zeros(C, E, dtype=torch.int32, device=dev)
+    call("smes_plan_counts", B, E, rpw, ptr(umask), ptr(chunk_union), ptr(torch.zeros(B, dtype=torch.int32, device=dev)),
+         _stream())
+    chunk_active = torch.zeros(C, E, dtype=torch.int32, device=dev)
+    chunk_active[0] = torch.bincount(act.reshape(-1), minlength=E).to(torch.int32)
+    chunk_mass = torch.zeros(C, E, dtype=torch.float64, device=dev)
+    chunk_mass[0] = w.sum(dim=(0, 1))
+    chunk_dmass = torch.zeros(C, E, dtype=torch.float64, device=dev)
+    chunk_dmass[0] = probs.sum(dim=(0, 1))
+    # logits whose softmax is full_probs (a zero probability becomes a very negative finite logit)
+    z = torch.where(probs > 0, torch.log(probs.clamp_min(1e-300)), torch.full_like(probs, -1e30)).float()
+    wsel = torch.gather(w, 2, act).float().contiguous()
+    return BatchRouting(z.contiguous(), T, B, E, budget, torch.ones(T, dtype=torch.float64, device=dev),
+                        sh.to(torch.int32).contiguous(), ad.to(torch.int32).contiguous(),
+                        act.to(torch.int32).contiguous(), wsel, umask, usize, chunk_union, chunk_active, chunk_mass,
+                        chunk_dmass, rpw, probs_in=probs.contiguous(), weights=w)
+
+
+def dense_routing(full_probs) -> BatchRouting:
+    """Every expert active for every task (routing.py:334-353): the dense baseline's routing view."""
+    p = _dev_tensor(full_probs, torch.float64)
+    if p.ndim != 3:
+        raise ShapeError(f"expected (T, B, E) probabilities, got shape {tuple(p.shape)}")
+    T, B, E = p.shape
+    idx = torch.arange(E, device=p.device)
+    return _from_arrays(idx.expand(B, E), torch.zeros(T, B, 0, dtype=torch.int64, device=p.device),
+                        idx.expand(T, B, E), tuple(idx.cpu() for _ in range(B)), p, p, RoutingBudget(E, 0))
+
+
+def stack_decisions(decisions) -> BatchRouting:
+    """Per-instance decisions into batch-major arrays (routing.py:166-181)."""
+    if not decisions:
+        raise ShapeError("cannot stack an empty decision list")
+    t = decisions[0].num_tasks
+    d0 = decisions[0]
+    budget = RoutingBudget(int(d0.shared.numel()), int(d0.adaptive[0].numel()) if t else 0)
+    return _from_arrays(torch.stack([_dev_tensor(d.shared, torch.int64) for d in decisions]),
+                        torch.stack([torch.stack([_dev_tensor(d.adaptive[i], torch.int64) for d in decisions])
+                                     for i in range(t)]),
+                        torch.stack([torch.stack([_dev_tensor(d.active[i], torch.int64) for d in decisions])
+                                     for i in range(t)]),
+                        tuple(torch.as_tensor(d.union).cpu() for d in decisions),
+                        torch.stack([_dev_tensor(d.weights, torch.float64) for d in decisions], dim=1),
+                        torch.stack([_dev_tensor(d.full_probs, torch.float64) for d in decisions], dim=1), budget)

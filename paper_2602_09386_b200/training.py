@@ -90,27 +90,55 @@ def backward(result: ForwardResult, model: MoeModel, labels, dense_probs_in_stat
     eng.dense = bool(dense_probs_in_stats)
     eng.forward_b(with_loss=True, train=True)   # loss + LoadStats (training.py:140-142) + fused combine bwd
     eng.backward()
-    E, K = eng.E, eng.K
+    K = eng.K
+    E, Ep = model.num_experts, eng.E
     lo = eng.loss_out.cpu()
-    stats = stats_from_raw(eng.stats_raw, E, K, B, T, eng.dense)
-    grads = {k: v.clone() for k, v in eng.gradients().items()}
-    d_hidden = eng.d_hidden.clone()
+    raw = eng.stats_raw.view(3, Ep)[:, :E].reshape(-1).contiguous()
+    stats = stats_from_raw(raw, E, K, B, T, eng.dense)
+    grads = _logical_gradients(eng, model)
+    d_hidden = eng.d_hidden[:, :model.d_in].clone()
     if result._enc is not None:
         grads.update(_encoder_backward(result._enc, model, eng))
     ordered = {k: grads[k] for k in model.parameter_blocks() if k in grads}
     return BackwardResult(ordered, float(lo[0]), float(lo[1]), float(lo[2]), stats, d_hidden)
 
 
+def _logical_gradients(eng, model) -> dict:
+    """Gradient blocks with the reference's names and shapes (model.py:94-111), sliced out of the
+    engine's (possibly shim-padded) stacked gradients; fresh tensors."""
+    T, E, Ep = model.num_tasks, model.num_experts, eng.E
+    pools = model.pools
+    dims = [model.d_in] + [p.d_out for p in pools]
+    g = {}
+    for li, (gw, gb) in enumerate(eng.g_layers):
+        di, do = dims[li], dims[li + 1]
+        pre = "expert_" if len(pools) == 1 else f"expert{li}_"
+        for e in range(E):
+            g[f"{pre}{e}.weight"] = gw[e, :do, :di].clone()
+            g[f"{pre}{e}.bias"] = gb[e, :do].clone()
+    rw = eng.g_router_w.view(T, Ep, eng.d)
+    rb = eng.g_router_b.view(T, Ep)
+    for t in range(T):
+        g[f"router_{t}.weight"] = rw[t, :E, :dims[0]].clone()
+        g[f"router_{t}.bias"] = rb[t, :E].clone()
+        g[f"head_{t}.weight"] = eng.g_head_w[t:t + 1, :dims[-1]].clone()
+        g[f"head_{t}.bias"] = eng.g_head_b[t:t + 1].clone()
+    return g
+
+
 def _encoder_backward(enc: dict, model: MoeModel, eng) -> dict:
     """encoder2/encoder1 grads from d_hidden (training.py:214-222) on the tcgen05 GEMM."""
     B, dev = eng.B, eng.dev
     Bp = _round(B, 128)
-    d, dh, Fp, F = model.d_in, model.encoder1.d_out, enc["Fp"], enc["F"]
+    d, Fp, F = _round(model.d_in, 8), enc["Fp"], enc["F"]
+    dh, dhr = enc["dhp"], enc["dh"]
     s = _stream()
     seg1 = torch.tensor([0, Bp], dtype=torch.int32, device=dev)
     g = {}
     dhid = torch.zeros(Bp, d, dtype=torch.bfloat16, device=dev)
-    dhid[:B] = eng.d_hidden
+    dhid[:B, :model.d_in] = eng.d_hidden[:, :model.d_in]
+    w2 = torch.zeros(1, d, dh, dtype=torch.bfloat16, device=dev)      # MN-major (K = d_in, N = d_hidden)
+    w2[0, :model.d_in, :dhr] = model.encoder2.weight
     # encoder2: dW = d_hidden^T mid, db = sum d_hidden, d_mid = d_hidden W2 (x relu mask)
     dw2 = torch.zeros(1, d, dh, device=dev)
     call("smes_gemm_ragged_k", ptr(dhid), d, ptr(enc["mid"]), dh, B, 1, d, dh, ptr(seg1), ptr(dw2), None, s)
@@ -118,14 +146,14 @@ def _encoder_backward(enc: dict, model: MoeModel, eng) -> dict:
     db2 = torch.zeros(1, d, device=dev)
     call("smes_seg_colsum", ptr(dhid), d, Bp, d, ptr(seg1), 1, ptr(part), ptr(db2), s)
     dmid = torch.zeros(Bp, dh, dtype=torch.bfloat16, device=dev)
-    _gemm(dhid, d, Bp, enc["w2"], dh, d, None, 0, dmid, dh, 0, B, b_mn=1, bits_in=enc["bits"], bits_ld=Bp)
+    _gemm(dhid, d, Bp, w2, dh, d, None, 0, dmid, dh, 0, B, b_mn=1, bits_in=enc["bits"], bits_ld=Bp)
     # encoder1: dW = d_pre^T x, db = sum d_pre
     dw1 = torch.zeros(1, dh, Fp, device=dev)
     call("smes_gemm_ragged_k", ptr(dmid), dh, ptr(enc["xb"]), Fp, B, 1, dh, Fp, ptr(seg1), ptr(dw1), None, s)
     db1 = torch.zeros(1, dh, device=dev)
     call("smes_seg_colsum", ptr(dmid), dh, Bp, dh, ptr(seg1), 1, ptr(part), ptr(db1), s)
-    g["encoder1.weight"] = dw1[0, :, :F].contiguous()
-    g["encoder1.bias"] = db1[0]
-    g["encoder2.weight"] = dw2[0]
-    g["encoder2.bias"] = db2[0]
+    g["encoder1.weight"] = dw1[0, :dhr, :F].contiguous()
+    g["encoder1.bias"] = db1[0, :dhr].contiguous()
+    g["encoder2.weight"] = dw2[0, :model.d_in, :dhr].contiguous()
+    g["encoder2.bias"] = db2[0, :model.d_in].contiguous()
     return g

@@ -218,9 +218,13 @@ def test_task_loss_and_errors():
 
 def _model_from_case(p, lam, beta, ks, ka):
     t = lambda a: torch.tensor(np.asarray(a), dtype=torch.float32).cuda()
-    pools = [smes.ExpertPool(t(w), t(b), act) for (w, b, act) in p.layers]
-    routers = smes.RouterBank(t(p.router_w), t(p.router_b), None if p.task_weights is None else torch.tensor(p.task_weights))
-    return smes.MoeModel(None, None, pools if len(pools) > 1 else pools[0], routers, t(p.head_w), t(p.head_b),
+    # reference form: lists of Affine maps (experts.py:26-38, routing.py:64-87, model.py:36-49)
+    pools = [smes.ExpertPool([smes.Affine(t(w[e]), t(b[e])) for e in range(w.shape[0])], act)
+             for (w, b, act) in p.layers]
+    routers = smes.RouterBank([smes.Affine(t(p.router_w[k]), t(p.router_b[k])) for k in range(p.router_w.shape[0])],
+                              None if p.task_weights is None else torch.tensor(p.task_weights))
+    heads = [smes.Affine(t(p.head_w[k:k + 1]), t(p.head_b[k:k + 1])) for k in range(p.head_w.shape[0])]
+    return smes.MoeModel(None, None, pools if len(pools) > 1 else pools[0], routers, heads,
                          torch.tensor(lam), beta, smes.RoutingBudget(ks, ka))
 
 
