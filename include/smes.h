@@ -67,6 +67,16 @@ int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r,
                      int32_t* chunk_union, int32_t* chunk_active, double* chunk_mass, double* chunk_dmass,
                      int32_t* flag, float* z_out, void* stream);
 
+/* ---- combine backward from a given upstream gradient of the task reps (the autograd form of the
+ *      layer, SMESLayer): training.py:160-179 with d_reps (T, B, d_out) fp32 in place of
+ *      dlogit x head_w, plus the sparse-reading LB term lb_coef * w (f - <w, f>) (balance.py:83-99).
+ *      Writes d_packed (rows, ldo) bf16 (x relu mask of O when relu_last) and the full dz rows
+ *      (B, ldz) bf16, zero off the active sets.  Deterministic (fixed-order sums). */
+int smes_combine_bwd_reps(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask,
+                          const int32_t* usize, const int32_t* row_of, const int32_t* active, const float* wsel,
+                          const void* O, long ldo, int relu_last, const float* d_reps, const float* freq,
+                          float lb_coef, void* dpacked, void* dz, long ldz, void* stream);
+
 /* ---- K2 execution plan: replaces build_execution_plan (execution.py:85-123)
  *      and the gather hidden[plan.gather_instances] (model.py:301).
  *      Segments are padded to 128 rows (seg_pad); seg_log are the reference's

@@ -18,6 +18,7 @@ from .linalg import Affine, FlopCounter, init_affine, matmul, relu, sigmoid, sof
 from .model import ForwardResult, MoeModel, forward_sparse, heads_from_stacked, init_model
 from .training import BackwardResult, backward, task_loss, total_loss
 from .checkpoint import load_model, save_model
+from .layer import SMESLayer
 from .workspace import (DeviceWorkspace, LoadProfile, PageBlock, ReplayResult, WorkspacePool, provision,
                         required_pages, simulate_replay)
 
@@ -36,7 +37,7 @@ __all__ = [
     "Affine", "init_affine", "matmul", "relu", "sigmoid", "softmax", "top_k",
     "ForwardResult", "MoeModel", "forward_sparse", "heads_from_stacked", "init_model",
     "BackwardResult", "backward", "task_loss", "total_loss",
-    "load_model", "save_model",
+    "load_model", "save_model", "SMESLayer",
     "DeviceWorkspace", "LoadProfile", "PageBlock", "ReplayResult", "WorkspacePool", "provision", "required_pages",
     "simulate_replay",
 ]

@@ -75,7 +75,7 @@ struct Plan {
   static constexpr int kOffSum = kOffCnt + TPR * E * BM;         // [2 parity][TPR][128] fp64 partial sums
   static constexpr int kOffUn = kOffSum + 2 * TPR * BM * 8;      // [TPR][128] u32 union words
   static constexpr int kOffBar = kOffUn + TPR * BM * 4;
-  static constexpr int kBytes = kOffBar + 256 + 1024;
+  static constexpr int kBytes = kOffBar + 512 + 1024;
   static_assert(E <= 32, "one union word per row");
   static_assert(TPR * 4 * BM * 9 <= TPR * E * BM * 4, "candidate lists fit the mass region");
   static_assert(kBytes <= 232448, "front smem plan exceeds 227 KB");
@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
   uint64_t* wempty = wfull + S::kWStages;
   uint64_t* hfull = wempty + S::kWStages;
   uint64_t* hempty = hfull + 1;
-  uint64_t* tfull = hempty + 1;          // [2 accumulators][4 chunks]
-  uint64_t* tempty = tfull + 8;
+  uint64_t* tfull = hempty + 1;          // [2 accumulators][16 chunks]
+  uint64_t* tempty = tfull + 32;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
   const int ncols = N <= 64 ? 128 : N <= 128 ? 256 : 512;   // two accumulators, power of two
   const int num_tiles = (a.B + BM - 1) / BM;
   const int nkb = (a.d + BK - 1) / BK;
-  const int NC = N % 64 == 0 ? 64 : N;      // columns per chunk
+  // columns per chunk: <= 64 (the W_r ring slot), a multiple of E (whole tasks per chunk)
+  const int NC = N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
   const int nch = N / NC;
 
   for (int i = threadIdx.x; i < N; i += blockDim.x) sbias[i] = a.bias[i];
@@ -194,7 +195,7 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
     for (int s = 0; s < S::kWStages; ++s) { mbar_init(&wfull[s], 1); mbar_init(&wempty[s], 1); }
     mbar_init(hfull, 1);
     mbar_init(hempty, 1);
-    for (int s = 0; s < 8; ++s) mbar_init(&tfull[s], 1);
+    for (int s = 0; s < 32; ++s) mbar_init(&tfull[s], 1);
     for (int s = 0; s < 2; ++s) mbar_init(&tempty[s], kEpi<TPR>);
     fence_mbar_init();
   }
@@ -250,7 +251,7 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
             tc_commit(&wempty[stage]);
             if (++stage == S::kWStages) { stage = 0; phase ^= 1; }
           }
-          tc_commit(&tfull[acc * 4 + c]);
+          tc_commit(&tfull[acc * 16 + c]);
         }
         tc_commit(hempty);                 // every MMA of this tile has read h
       }
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
       const bool valid = b < a.B;
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + acc * N;
 #ifdef SMES_FRONT_GEMM_ONLY
-      for (int c = 0; c < nch; ++c) mbar_wait(&tfull[acc * 4 + c], (it >> 1) & 1);
+      for (int c = 0; c < nch; ++c) mbar_wait(&tfull[acc * 16 + c], (it >> 1) & 1);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       continue;
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
         int chunk = 0, next_chunk_task = 0;
         for (int t = 0; t < T; ++t) {
           if (t == next_chunk_task) {        // first task of a chunk: wait for its MMAs
-            mbar_wait(&tfull[acc * 4 + chunk], (it >> 1) & 1);
+            mbar_wait(&tfull[acc * 16 + chunk], (it >> 1) & 1);
             tc_fence_after();
             ++chunk;
             next_chunk_task += NC / E;
@@ -613,7 +614,7 @@ int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r,
   CUtensorMap ta, tb;
   int rc;
   if ((rc = front_map(&ta, h, (uint64_t)d, (uint64_t)B, (uint64_t)ldh, 128))) return rc;
-  const int nc = (T * E) % 64 == 0 ? 64 : T * E;      // W_r chunk rows (see Plan)
+  const int nc = (T * E) % 64 == 0 ? 64 : (T * E) % 32 == 0 ? 32 : 16;      // W_r chunk rows (see kernel)
   if ((rc = front_map(&tb, w_r, (uint64_t)d, (uint64_t)(T * E), (uint64_t)d, (uint32_t)nc))) return rc;
   front::Args a{b_r, task_weights, T, B, d, sub_rows, shared, adaptive, active, wsel, umask, usize,
                 chunk_union, chunk_active, chunk_mass, chunk_dmass, flag, z_out};

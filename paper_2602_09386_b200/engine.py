@@ -364,7 +364,7 @@ class SMESEngine:
                 None, ptr(self.lam), None, self.grid, s)
 
     def forward_a(self, frozen: bool = False, fold: bool = False, store_hidden: bool = True, refold: bool = True,
-                  finalize_stats: bool = False):
+                  finalize_stats: bool = False, heads: bool = True):
         """Router GEMM -> routing -> plan -> expert GEMMs.  Ends with the per-expert
         LoadStats sums in ``stats_raw`` (the data-parallel exchange point).
         ``fold`` (training steps only, see csrc/fold.cu): the last identity pool is folded into
@@ -404,7 +404,7 @@ class SMESEngine:
              ptr(self.gather_exp), ptr(self.Cm), self.ldc, self.ldc, s)
         if fold and not self.can_fold:
             raise ConfigError("head folding needs an identity last expert pool and sparse LB statistics")
-        self.experts_forward(s, fold=fold, store_hidden=store_hidden, refold=refold)
+        self.experts_forward(s, fold=fold, store_hidden=store_hidden, refold=refold, heads=heads)
 
     def forward_b(self, with_loss: bool = True, batch_times_tasks: float | None = None, train: bool = False,
                   batch_scale: int | None = None, lb_batch: int | None = None, stats_done: bool = False,
@@ -448,7 +448,8 @@ class SMESEngine:
              ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), int(frozen), s)
 
-    def experts_forward(self, s, fold: bool = False, store_hidden: bool = True, refold: bool = True):
+    def experts_forward(self, s, fold: bool = False, store_hidden: bool = True, refold: bool = True,
+                        heads: bool = True):
         R = self.rows_cap
         inp = self.X
         L = len(self.p.layers)
@@ -476,6 +477,8 @@ class SMESEngine:
             _tagged(f"fc{L}_fwd_folded", "smes_gemm_ragged_m", ptr(inp), self.ld_in[L - 1], R, ptr(self.G_fold),
                     self.E, self.ldg, di, 0, ptr(self.seg_pad), ptr(self.c_fold), 0, None, None, 0, ptr(self.P),
                     self.ldp, 1, R, s)
+            return
+        if not heads:                    # the layer without its heads (SMESLayer): O is the output
             return
         # head projections of every packed row: P = O head_W^T (tcgen05 GEMM, N = T)
         _tagged("head_proj", "smes_gemm_ragged_m", ptr(self.outs[-1]), self.d_out, R, ptr(self.head_w_bf), 1, self.T,
@@ -658,6 +661,52 @@ class SMESEngine:
         if not rb_fused:                  # else reduced by post_combine
             _tagged("router_bias", "smes_part_reduce", ptr(self.rb_part), self.rw_splits, T * E,
                     ptr(self.g_router_b), s)
+
+    # ------------------------------------------------------------------ layer form (no heads)
+    def forward_layer(self):
+        """Forward of the layer without its heads and loss (SMESLayer): routing, plan, every expert
+        pool with O kept, LoadStats and the task reps (execution.py:161-191)."""
+        s = self._stream()
+        T, E, B = self.T, self.E, self.B
+        self.forward_a(fold=False, heads=False)
+        self.stats_finalize(s)
+        _tagged("combine_fwd", "smes_combine_fwd", T, B, E, self.K, self.d_out, self.umax, ptr(self.umask),
+                ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]), self.d_out,
+                ptr(self.head_w), ptr(self.head_b), None, self.ldp, ptr(self.reps), ptr(self.logits),
+                ptr(self.preds), None, ptr(self.lam), None, self.grid, s)
+
+    def backward_reps(self, d_reps: torch.Tensor, d_lb: float):
+        """Reverse of ``forward_layer`` for an upstream gradient d_reps (T, B, d_out) fp32 and the
+        gradient d_lb of the returned L_lb: combine backward + LB term (csrc/layer.cu), then every
+        pool's dgrad / wgrad, the router backward and the un-permute (training.py:160-212)."""
+        s = self._stream()
+        T, E, B, K = self.T, self.E, self.B, self.K
+        R = self.rows_cap
+        if d_reps.shape != (T, B, self.d_out) or d_reps.dtype != torch.float32 or not d_reps.is_contiguous():
+            raise ShapeError(f"d_reps must be a contiguous fp32 ({T}, {B}, {self.d_out}) tensor")
+        self._fused_bwd = False
+        lb_coef = float(d_lb) * self.E_lb / (K * B * T)
+        self.d_outs[-1].zero_()
+        n_layers = len(self.p.layers)
+        _tagged("combine_bwd", "smes_combine_bwd_reps", T, B, E, K, self.d_out, self.umax, ptr(self.umask),
+                ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
+                self.d_out, int(self.p.layers[-1].act == "relu"), ptr(d_reps), ptr(self.freq32), lb_coef,
+                ptr(self.d_outs[-1]), ptr(self.dz), T * E, s)
+        for i in range(n_layers - 1, -1, -1):
+            dout = self.d_outs[i]
+            inp = self.X if i == 0 else self.outs[i - 1]
+            gw, gb = self.g_layers[i]
+            di, do = self.dims[i], self.dims[i + 1]
+            if i > 0:
+                _tagged(f"fc{i + 1}_dgrad", "smes_gemm_ragged_m", ptr(dout), do, R, ptr(self.w_bf[i]), E, di, do, 1,
+                        ptr(self.seg_pad), None, 0, None, ptr(self.bits[i - 1]), R, ptr(self.d_outs[i - 1]), di, 0,
+                        R, s)
+            _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do, di,
+                    ptr(self.seg_pad), ptr(gw), ptr(gb), s)
+        _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E,
+                self.d, self.dims[1], 1, ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), self.d, 0, R, s)
+        self._router_backward(s)
+        self._unpermute(s)
 
     def step(self):
         self.forward_a(fold=self.can_fold, finalize_stats=True)

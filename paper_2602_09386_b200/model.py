@@ -156,24 +156,7 @@ class MoeModel:
         layers = [(p.weight, p.bias, p.nonlinearity) for p in pools]
         hw, hb = self.head_w, self.head_b
         if pad is not None and pad.active:
-            T, E, Ep = self.num_tasks, self.num_experts, pad.E_p
-            dims, dp = pad.dims, pad.dims_p
-            dev = rw.device
-            z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)
-            rw_p = z(T, Ep, dp[0])
-            rw_p[:, :E, :dims[0]] = rw
-            rb_p = torch.full((T, Ep), DEAD_EXPERT_BIAS, dtype=torch.float32, device=dev)
-            rb_p[:, :E] = rb
-            lp = []
-            for i, (w, b, act) in enumerate(layers):
-                w_p = z(Ep, dp[i + 1], dp[i])
-                w_p[:E, :dims[i + 1], :dims[i]] = w
-                b_p = z(Ep, dp[i + 1])
-                b_p[:E, :dims[i + 1]] = b
-                lp.append((w_p, b_p, act))
-            hw_p = z(T, dp[-1])
-            hw_p[:, :dims[-1]] = hw
-            rw, rb, layers, hw = rw_p, rb_p, lp, hw_p
+            rw, rb, layers, hw = pad_params(rw, rb, layers, hw, pad)
         return _engine.SMESParams(
             router_w=rw, router_b=rb, layers=[_engine.ExpertLayer(w, b, act) for (w, b, act) in layers],
             head_w=hw, head_b=hb, task_weights=self.routers.task_weights,
@@ -200,15 +183,40 @@ class _Pad:
     """Kernel granularity of the layer: input and hidden widths to multiples of 32, the output width
     to 128 / 256 / 512 / 1024 (combine tiling), T * E to a multiple of 8."""
 
-    def __init__(self, model: MoeModel):
-        self.T, self.E = model.num_tasks, model.num_experts
-        self.dims = [model.d_in] + [p.d_out for p in model.pools]
+    def __init__(self, model: "MoeModel | None" = None, T: int = 0, E: int = 0, dims=None):
+        if model is not None:
+            T, E, dims = model.num_tasks, model.num_experts, [model.d_in] + [p.d_out for p in model.pools]
+        self.T, self.E = T, E
+        self.dims = list(dims)
         self.dims_p = [_round(x, 32) for x in self.dims[:-1]] + [_pad_out(self.dims[-1])]
         E_p = self.E
         while (self.T * E_p) % 8:
             E_p += 1
         self.E_p = E_p
         self.active = self.dims_p != self.dims or E_p != self.E
+
+
+def pad_params(rw, rb, layers, hw, pad: _Pad):
+    """Zero-padded copies of router / pool / head parameters at the kernels' granularity; the padded
+    experts get a -1e30 router bias (never selected, softmax mass exactly 0)."""
+    T, E, Ep = pad.T, pad.E, pad.E_p
+    dims, dp = pad.dims, pad.dims_p
+    dev = rw.device
+    z = lambda *s: torch.zeros(*s, dtype=torch.float32, device=dev)
+    rw_p = z(T, Ep, dp[0])
+    rw_p[:, :E, :dims[0]] = rw
+    rb_p = torch.full((T, Ep), DEAD_EXPERT_BIAS, dtype=torch.float32, device=dev)
+    rb_p[:, :E] = rb
+    lp = []
+    for i, (w, b, act) in enumerate(layers):
+        w_p = z(Ep, dp[i + 1], dp[i])
+        w_p[:E, :dims[i + 1], :dims[i]] = w
+        b_p = z(Ep, dp[i + 1])
+        b_p[:E, :dims[i + 1]] = b
+        lp.append((w_p, b_p, act))
+    hw_p = z(T, dp[-1])
+    hw_p[:, :dims[-1]] = hw
+    return rw_p, rb_p, lp, hw_p
 
 
 def init_model(gen: torch.Generator | None, num_features: int, d_hidden: int, d_in: int, d_out: int,

@@ -53,6 +53,8 @@ CASES = {
     "c2_ties": (8, 32, 256, 4, 2, 3000, "ties"),
     "c2_d192_ragged_B": (8, 32, 192, 4, 2, 1000, "init"),
     "t2_e16_one_chunk": (2, 16, 64, 2, 1, 300, "x1000"),
+    "t5_e32_chunk32": (5, 32, 256, 4, 2, 1536, "init"),
+    "t3_e16_chunk16": (3, 16, 128, 2, 1, 640, "x1000"),
     "c1_shape": (4, 16, 128, 2, 1, 1024, "init"),
     "t16_e16": (16, 16, 128, 4, 2, 777, "x1000"),
     "small_B": (8, 32, 256, 4, 2, 5, "x1000"),
