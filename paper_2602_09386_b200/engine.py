@@ -265,18 +265,28 @@ class SMESEngine:
         self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
         self.dX = z(R, d, dt=bf)
         self.dz = z(self.B_pad, T * E, dt=bf)
-        # all parameter gradients live in ONE flat fp32 buffer (a single data-parallel all-reduce)
-        shapes = [(E, l.d_out, l.d_in) for l in self.p.layers] + [(E, l.d_out) for l in self.p.layers]
-        shapes += [(T * E, d), (T * E,), (T, self.d_out), (T,)]
+        # all parameter gradients live in ONE flat fp32 buffer, laid out in the order the backward
+        # finishes them so data parallelism can reduce contiguous buckets as they complete:
+        #   [W_0, b_0, ..., W_{L-2}, b_{L-2}] [W_{L-1}, b_{L-1}, head_w, head_b] [router_w, router_b]
+        nl = len(self.p.layers)
+        shapes = []
+        for l in self.p.layers:
+            shapes += [(E, l.d_out, l.d_in), (E, l.d_out)]
+        shapes += [(T, self.d_out), (T,), (T * E, d), (T * E,)]
         sizes = [int(torch.Size(sh).numel()) for sh in shapes]
         self.grad_flat = z(sum(sizes))
-        views, off = [], 0
+        views, off, offs = [], 0, []
         for sh, n in zip(shapes, sizes):
+            offs.append(off)
             views.append(self.grad_flat[off:off + n].view(sh))
             off += n
-        nl = len(self.p.layers)
-        self.g_layers = [(views[i], views[nl + i]) for i in range(nl)]
-        self.g_router_w, self.g_router_b, self.g_head_w, self.g_head_b = views[2 * nl:]
+        self.g_layers = [(views[2 * i], views[2 * i + 1]) for i in range(nl)]
+        self.g_head_w, self.g_head_b, self.g_router_w, self.g_router_b = views[2 * nl:]
+        last, router = offs[2 * (nl - 1)], offs[2 * nl + 2]
+        # gradient buckets (name -> slice of grad_flat), in completion order of the backward
+        self.grad_buckets = {"pools_first": slice(0, last), "last_pool_heads": slice(last, router),
+                             "router": slice(router, off)}
+        self.on_grads = None     # optional callback(bucket name, cuda stream) once a bucket is final
         self.colsum_part = z(R // 128, max(max(self.dims), T * E))
         self.dh_router = z(B, d)
         self.d_hidden = z(B, d)
@@ -500,6 +510,7 @@ class SMESEngine:
         lb_coef = self.beta * self.E_lb / (K * lbb * T)
         relu_last = int(self.p.layers[-1].act == "relu")
         n_layers = len(self.p.layers)
+        side_hooks = False       # the side stream announced its gradient buckets itself
         fused = getattr(self, "_fused_bwd", False)
         folded = fused and self._folded
         # The router backward needs only dz and h: it runs on a side stream next to the expert
@@ -548,7 +559,12 @@ class SMESEngine:
                         E, di, self.ldg, 1, ptr(self.seg_pad), None, 0, None, ptr(mask), R, ptr(dst), di, 0, R, s)
             if side:      # Q = C^T H and the unfold need only C and H: next to the dgrad chain
                 self._last_pool_wgrad(self._side.cuda_stream, inp, di)
+                if self.on_grads is not None:
+                    self.on_grads("last_pool_heads", self._side)
                 self._router_backward(self._side.cuda_stream, self._ev_dx if unpermute_side else None)
+                if self.on_grads is not None:
+                    self.on_grads("router", self._side)
+                side_hooks = self.on_grads is not None
             else:
                 self._last_pool_wgrad(s, inp, di)
             top = n_layers - 2
@@ -595,6 +611,8 @@ class SMESEngine:
         if not (folded and (n_layers == 1 or self.fuse_mlp)):
             _tagged("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.d_outs[0]), self.dims[1], R, ptr(self.w_bf[0]), E, d, self.dims[1], 1,
                     ptr(self.seg_pad), None, 0, None, None, R, ptr(self.dX), d, 0, R, s)
+        if side_hooks:
+            self.on_grads("pools_first", main)    # every pool but the last: final on the main stream
         if side:
             self._ev_join.record(self._side)       # after every side-stream launch of this pass
             main.wait_event(self._ev_join)
@@ -607,6 +625,10 @@ class SMESEngine:
                     ptr(self.g_head_w), s)
         if not getattr(self, "_fused_bwd", False):
             _tagged("head_reduce", "smes_part_reduce", ptr(self.part_db), self.grid, T, ptr(self.g_head_b), s)
+        if self.on_grads is not None and not side_hooks:
+            cur = torch.cuda.current_stream(self.dev)
+            for name in self.grad_buckets:
+                self.on_grads(name, cur)
 
     def _post_combine(self, s):
         """Loss, per-(expert, task) sums of C, router / head bias grads: one reduction launch."""

@@ -253,7 +253,7 @@ class EPRank:
         tcall("owner_scatter", "smes_plan_scatter", Br, El, d, self.rpw_o, ptr(umask), ptr(self.chunk_base_o), ptr(self.seg_pad_o),
              ptr(self.loads_o), ptr(self.h_recv), d, ptr(sh.X), sh.ld_in[0], ptr(self.row_of_o), self.umax_l,
              ptr(self.gather_inst_o), ptr(self.gather_exp_o), ptr(sh.Cm), sh.ldc, sh.ldc, s)
-        sh.forward(s, self.seg_pad_o)
+        sh.forward(s, self.seg_pad_o, self.totals_o)
         tcall("ep_segments", "smes_ep_segments", 0, self.n, El, ptr(self.cnt_recv), ptr(self.seg_pad_o), self.slot_rows,
              ptr(self.tab_own), s)
         if self.peers is not None:
@@ -292,7 +292,7 @@ class EPRank:
         sh = self.shard
         tcall("ep_copy_rows", "smes_ep_copy_rows", self.n * self.El, ptr(self.tab_own), 1, ptr(self.C_recv), self.ldc * 2, ptr(sh.Cm),
              sh.ldc * 2, self.ldc * 2, s)
-        sh.backward(s, self.seg_pad_o)
+        sh.backward(s, self.seg_pad_o, self.totals_o)
         tcall("unpermute", "smes_unpermute", Br, d, ptr(self.usize_o), ptr(self.row_of_o), self.umax_l, ptr(sh.dX), d, None,
              ptr(self.dh_own), s)
 

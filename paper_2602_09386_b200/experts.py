@@ -150,8 +150,11 @@ def refresh_into(obj, name: str, src: torch.Tensor, dtype) -> torch.Tensor:
 class ExpertShard:
     def __init__(self, layers, T: int, head_w: torch.Tensor, rows_cap: int, device, fuse_mlp: bool = True,
                  fuse_wgrad: bool = False):
-        if layers[-1].act != "identity" or len(layers) not in (1, 2) or (len(layers) == 2 and layers[0].act != "relu"):
-            raise ConfigError("expert shard needs [relu ->] identity expert pools (the folded heads)")
+        # folded heads: [relu ->] identity pools.  Unfolded: one relu pool (the reference expert with
+        # expert_nonlinearity="relu"), whose outputs O are kept and projected onto the heads.
+        self.folded = layers[-1].act == "identity"
+        if len(layers) not in (1, 2) or (len(layers) == 2 and (layers[0].act != "relu" or not self.folded)):
+            raise ConfigError("expert shard needs [relu ->] identity expert pools or one relu pool")
         self.dev = torch.device(device)
         self.layers = layers
         self.E = layers[0].weight.shape[0]
@@ -199,6 +202,16 @@ class ExpertShard:
         self.g_layers = [(views[i], views[L + i]) for i in range(L)]
         self.g_head_w = z(T, self.d_out)                   # this shard's share of dW_head
         self.head_w = head_w
+        if not self.folded:
+            # unfolded single relu pool: O and its relu mask, d_packed = (C head_w) x mask
+            self.O = z(R, self.d_out, dt=bf)
+            self.bits = z(self.d_out // 32, R, dt=torch.int32)
+            self.dO = z(R, self.d_out, dt=bf)
+            # one group over every row; callers pass the plan's [0, padded rows] table instead (seg_one)
+            self.seg_all = torch.tensor([0, R], dtype=torch.int32, device=dev)
+            self.head_w_bf = torch.empty(1, T, self.d_out, dtype=bf, device=dev)
+            self.head_wT_bf = torch.zeros(1, self.d_out, self.ldc, dtype=bf, device=dev)
+            self.g_head_w3 = self.g_head_w.view(1, T, self.d_out)
         self.refresh_weights()
 
     def refresh_weights(self):
@@ -209,12 +222,24 @@ class ExpertShard:
         for l, w, b in zip(self.layers, self.w_bf, self.b32):
             w.copy_(l.weight.detach())
             b.copy_(l.bias.detach())
+        if not self.folded:
+            self.head_w_bf[0].copy_(self.head_w)
+            self.head_wT_bf[0, :, :self.T].copy_(self.head_w.t())
 
     # ------------------------------------------------------------------ forward
-    def forward(self, s, seg_pad):
+    def forward(self, s, seg_pad, seg_one=None):
         """P of every packed row (X already scattered; seg_pad = padded expert offsets)."""
         E, R, T = self.E, self.R, self.T
         di = self.dims[-2]
+        if not self.folded:
+            # O = relu(X W^T + b) (+ mask), then P = O head_w^T over every row (N = T)
+            tcall("fc1_fwd", "smes_gemm_ragged_m", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]), E, self.d_out,
+                  self.d, 0, ptr(seg_pad), ptr(self.b32[0]), 1, ptr(self.bits), None, R, ptr(self.O), self.d_out, 0,
+                  R, s)
+            tcall("head_proj", "smes_gemm_ragged_m", ptr(self.O), self.d_out, R, ptr(self.head_w_bf), 1, T,
+                  self.d_out, 0, ptr(self.seg_all if seg_one is None else seg_one), None, 0, None, None, 0, ptr(self.P),
+                  self.ldp, 1, R, s)
+            return
         tcall("fold_heads", "smes_fold_heads", E, T, self.ldg, self.d_out, di, ptr(self.head_w), ptr(self.w_bf[-1]),
              ptr(self.b32[-1]), ptr(self.G), ptr(self.c), ptr(self.work), s)
         if len(self.layers) == 1:
@@ -232,11 +257,25 @@ class ExpertShard:
              ptr(self.c), 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
 
     # ------------------------------------------------------------------ backward
-    def backward(self, s, seg_pad):
+    def backward(self, s, seg_pad, seg_one=None):
         """From C (row coefficients, pad rows zero): expert grads, dW_head share, dX."""
         E, R, T = self.E, self.R, self.T
         L = len(self.layers)
         di = self.dims[-2]
+        if not self.folded:
+            # d_packed = (C head_w) x relu mask; dW, db (ones column of X); dX; dW_head share = C^T O
+            tcall("dpacked_gemm", "smes_gemm_ragged_m", ptr(self.Cm), self.ldc, R, ptr(self.head_wT_bf), 1,
+                  self.d_out, self.ldc, 0, ptr(self.seg_all if seg_one is None else seg_one), None, 0, None,
+                  ptr(self.bits), R, ptr(self.dO),
+                  self.d_out, 0, R, s)
+            gw, gb = self.g_layers[0]
+            tcall("fc1_wgrad", "smes_gemm_ragged_k", ptr(self.dO), self.d_out, ptr(self.X), self.ld_in[0], R, E,
+                  self.d_out, self.d, ptr(seg_pad), ptr(gw), ptr(gb), s)
+            tcall("fc1_dgrad", "smes_gemm_ragged_m", ptr(self.dO), self.d_out, R, ptr(self.w_bf[0]), E, self.d,
+                  self.d_out, 1, ptr(seg_pad), None, 0, None, None, R, ptr(self.dX), self.d, 0, R, s)
+            tcall("head_wgrad", "smes_gemm_ragged_k", ptr(self.Cm), self.ldc, ptr(self.O), self.d_out, R, 1, T,
+                  self.d_out, ptr(self.seg_all if seg_one is None else seg_one), ptr(self.g_head_w3), None, s)
+            return
         inp = self.X if L == 1 else self.H
         if L == 2 and self.fuse:
             tcall("mlp_dgrad", "smes_mlp_dgrad", ptr(self.Cm), self.ldc, R, ptr(self.G), self.ldg, ptr(self.w_bf[0]), E, self.d, di,

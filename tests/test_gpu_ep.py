@@ -38,6 +38,9 @@ CASES = {
     "n1": (3, 1, 512, 4, 32, 128, 256, 2, 1, 1.0, True, False),
     "n2_peer_put": (4, 2, 512, 4, 64, 128, 256, 2, 1, 1.0, True, True),
     "n4_peer_put": (6, 4, 256, 8, 128, 128, 256, 3, 2, 1.0, True, True),
+    # the reference expert (one relu pool, experts.py:17-73): unfolded shard, O kept, P = O head_w^T
+    "n2_single_relu": (7, 2, 512, 4, 64, 128, None, 2, 1, 1.0, True, False),
+    "n4_single_relu_put": (8, 4, 256, 8, 128, 128, None, 3, 2, 1.0, True, True),
 }
 
 

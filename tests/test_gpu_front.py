@@ -6,6 +6,8 @@ bf16 operands (fp32 accumulation: 1e-5 relative).  Routing: index-exact against 
 route_batch (routing.py:235-281) on those logits, weights within fp32 1e-6, and bit-identical
 selections / union masks / histograms to smes_route_batch (the route kernels) on the same z.
 Cases include reference-init logits (Stage-I gaps ~1e-10) and exact ties in both stages."""
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -65,7 +67,7 @@ CASES = {
 def test_route_front_vs_oracle_and_route_kernel(name):
     T, E, d, ks, ka, B, kind = CASES[name]
     assert _lib.call("smes_route_front_supported", T, E, d, ks, ka)
-    rng = np.random.default_rng(abs(hash(name)) % 2 ** 32)
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
     scale = {"init": 1e-3, "x1000": 1.0, "ties": 0.0}[kind] / d ** 0.5
     h = torch.tensor(rng.normal(size=(B, d)), dtype=torch.bfloat16, device="cuda")
     w = torch.tensor(rng.uniform(-scale, scale, size=(T * E, d)), dtype=torch.bfloat16, device="cuda")

@@ -4,6 +4,8 @@ out) through both kernels: the expert-per-lane route_kernel and the task-grouped
 logits: selections and union masks index-exact, weights within fp32 1e-6, and the chunk
 histograms summed over chunks equal to the oracle's LoadStats sums (counts exact, sparse mass of
 the fp32 weights 1e-6 relative, dense fp64 mass 1e-9)."""
+import zlib
+
 import numpy as np
 import pytest
 import torch
@@ -50,7 +52,7 @@ CASES = {
 def test_router_kernel_vs_oracle(name):
     T, E, kind = CASES[name]
     ks, ka, B = 4, 2, 3000
-    rng = np.random.default_rng(hash(name) % 2 ** 32)
+    rng = np.random.default_rng(zlib.crc32(name.encode()))
     if kind == "random":
         z = rng.normal(size=(T, B, E))
     elif kind == "init":          # reference router init: |z| ~ 5e-4, Stage-I gaps ~1e-10
