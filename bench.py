@@ -411,8 +411,16 @@ def run_dp(args, c, world, rank, local, dev):
     h_host, y_host = _host_inputs(c, B, rank)
     eng.set_inputs(h_host.to(dev), y_host.to(dev))
     eng.keep_logits = False        # the training step does not write the router logits (fused front)
-    dp = DataParallelStep(eng)
-    dp.capture(warmup=1)
+    # N > 1: LoadStats over CUDA-IPC peer memory + gradient buckets overlapped with the backward;
+    # the whole step (collectives included) is one CUDA graph.  SMES_DP_SAFE=1: NCCL statistics,
+    # one gradient all-reduce after the backward, two graphs (round-1 path).
+    safe = os.environ.get("SMES_DP_SAFE") == "1"
+    dp = DataParallelStep(eng, stats="group" if safe else "peer", overlap=not safe)
+    try:
+        dp.capture(warmup=1)
+    except Exception as err:     # a graph capture the NCCL build refuses: keep the eager step
+        print(f"dp capture failed ({err}); eager step", file=sys.stderr, flush=True)
+        dp._ga = dp._gb = None
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
     for _ in range(args.warmup):
         dp.step()

@@ -77,6 +77,14 @@ int smes_combine_bwd_reps(int T, int B, int E, int K, int d_out, int umax, const
                           const void* O, long ldo, int relu_last, const float* d_reps, const float* freq,
                           float lb_coef, void* dpacked, void* dz, long ldz, void* stream);
 
+/* ---- one-shot all-reduce of a small f64 vector over CUDA-IPC-mapped peer memory (NVLink): the
+ *      data-parallel exchange of the 3E LoadStats sums (balance.py:62-70).  recv buffers are
+ *      [2][n][count] f64 on every rank, flags [n] int32, epoch_ctr 1 int32 (device-side epoch:
+ *      graph capturable).  out may alias in.  Result: sum in rank order, identical on every rank. */
+int smes_peer_allreduce_f64(int n, int me, int count, const double* in, void* const* peer_recv_dev,
+                            int32_t* const* peer_flags_dev, const double* my_recv, int32_t* my_flags,
+                            int32_t* epoch_ctr, double* out, void* stream);
+
 /* ---- K2 execution plan: replaces build_execution_plan (execution.py:85-123)
  *      and the gather hidden[plan.gather_instances] (model.py:301).
  *      Segments are padded to 128 rows (seg_pad); seg_log are the reference's

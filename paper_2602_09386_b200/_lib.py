@@ -28,6 +28,7 @@ SIGNATURES = {
     "smes_route_num_chunks": [I, I],
     "smes_route_batch": [P, L, L, P, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, P],
     "smes_route_front_supported": [I, I, I, I, I],
+    "smes_peer_allreduce_f64": [I, I, I, P, P, P, P, P, P, P, P],
     "smes_combine_bwd_reps": [I, I, I, I, I, I, P, P, P, P, P, P, L, I, P, P, F, P, P, L, P],
     "smes_route_front": [P, L, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
     "smes_plan_reduce": [I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
@@ -93,7 +94,7 @@ def _unfold_launches(E, T, ldg, d_out, d_in, *_):
     return 7 if _fold_gemm_path(E, T, d_out, d_in) else 2
 
 
-KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_combine_bwd_reps": 1, "smes_plan_reduce": 1, "smes_plan_reduce_stats": 1, "smes_plan_scatter": 1, "smes_gemm_ragged_m": 1,
+KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_allreduce_f64": 1, "smes_combine_bwd_reps": 1, "smes_plan_reduce": 1, "smes_plan_reduce_stats": 1, "smes_plan_scatter": 1, "smes_gemm_ragged_m": 1,
                     "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
                     "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,

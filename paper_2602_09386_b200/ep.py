@@ -408,6 +408,35 @@ class NcclComm:
             self.dist.all_reduce(t, group=self.group)
 
 
+def ipc_peer_pointers(t: torch.Tensor, me: int, n: int, group, mapped: dict) -> torch.Tensor:
+    """Map every rank's copy of ``t`` (CUDA IPC; the process group carries the handles) and return
+    the n device pointers as an int64 device tensor (entry ``me`` is ``t`` itself).  The IPC handle
+    names the cudaMalloc segment holding ``t``, so each rank also publishes the tensor's offset
+    inside that segment (caching-allocator tensors rarely sit at a segment base) and the opener
+    adds it to the mapped base.  ``mapped`` caches one mapping per (peer, segment)."""
+    import ctypes as C
+    import torch.distributed as dist
+    h = (C.c_uint8 * 64)()
+    off = C.c_long(0)
+    call("smes_ipc_handle", ptr(t), C.cast(h, C.c_void_p), C.byref(off))
+    mine = (bytes(h), int(off.value))
+    allh = [None] * n
+    dist.all_gather_object(allh, mine, group=group)
+    ptrs = []
+    for r, (hb, o) in enumerate(allh):
+        if r == me:
+            ptrs.append(t.data_ptr())
+            continue
+        base = mapped.get(hb)
+        if base is None:        # a segment may hold several buffers
+            out = C.c_void_p()
+            hh = (C.c_uint8 * 64).from_buffer_copy(hb)
+            call("smes_ipc_open", C.cast(hh, C.c_void_p), C.byref(out))
+            base = mapped[hb] = out.value
+        ptrs.append(base + o)
+    return torch.tensor(ptrs, dtype=torch.int64, device=t.device)
+
+
 class PeerComm:
     """One rank per process, hand-written transport over CUDA-IPC-mapped peer memory
     (NVLink/NVSwitch).  ``fused=True`` (default): the dispatch pack and the P / C segment
@@ -435,30 +464,7 @@ class PeerComm:
         self.dist.barrier(group=self.group)
 
     def _open(self, t):
-        """Map every peer's copy of ``t``: the IPC handle names the cudaMalloc segment holding it,
-        so each rank also publishes the tensor's offset inside that segment (caching-allocator
-        tensors rarely sit at a segment base) and the opener adds it to the mapped base."""
-        import ctypes as C
-        h = (C.c_uint8 * 64)()
-        off = C.c_long(0)
-        call("smes_ipc_handle", ptr(t), C.cast(h, C.c_void_p), C.byref(off))
-        mine = (bytes(h), int(off.value))
-        allh = [None] * self.n
-        self.dist.all_gather_object(allh, mine, group=self.group)
-        ptrs = []
-        for r, (hb, o) in enumerate(allh):
-            if r == self.me:
-                ptrs.append(t.data_ptr())
-                continue
-            key = hb
-            base = self._mapped.get(key)
-            if base is None:        # one mapping per (peer, segment): a segment may hold several buffers
-                out = C.c_void_p()
-                hh = (C.c_uint8 * 64).from_buffer_copy(hb)
-                call("smes_ipc_open", C.cast(hh, C.c_void_p), C.byref(out))
-                base = self._mapped[key] = out.value
-            ptrs.append(base + o)
-        return torch.tensor(ptrs, dtype=torch.int64, device=t.device)
+        return ipc_peer_pointers(t, self.me, self.n, self.group, self._mapped)
 
     def close(self):
         """Unmap the peers' segments (after a final synchronize)."""

@@ -1,6 +1,9 @@
 """Two data-parallel ranks of the REAL engine on one GPU (gloo over CUDA tensors): the rank
-results must equal one process on the concatenated batch (DP exactness of the graph-captured
-step incl. its side stream).  torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dp2_on_one_gpu.py"""
+results must equal one process on the concatenated batch (DP exactness of the step incl. its
+backward side stream).  Optional arguments: ``peer`` -- LoadStats through the one-shot CUDA-IPC
+peer all-reduce (csrc/comm.cu); ``overlap`` -- gradient buckets reduced on a communication stream
+as the backward finishes them.
+torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dp2_on_one_gpu.py [peer] [overlap]"""
 import os
 import sys
 
@@ -20,7 +23,7 @@ p, h, y, lam, beta = make_case(7, B * n, 8, 32, 256, 256, 4, 2, d_ff=512, router
 eng = SMESEngine(to_engine_params(p, lam, beta), B, 4, 2)
 eng.set_inputs(torch.tensor(h[r * B:(r + 1) * B], device="cuda"),
                torch.tensor(y[:, r * B:(r + 1) * B], device="cuda", dtype=torch.float32))
-step = DataParallelStep(eng)
+step = DataParallelStep(eng, stats="peer" if "peer" in sys.argv else "group", overlap="overlap" in sys.argv)
 step.capture()
 for _ in range(3):
     step.step()
