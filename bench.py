@@ -36,6 +36,9 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # BASELINE.json configs (Appendix A assumptions for the fields it leaves open)
+    "c1": dict(T=4, E=16, ks=2, ka=1, d=128, d_ff=256, d_out=128, B=1024, beta=0.01, mode="fwd32", scaling="weak",
+               workload="c1: SMES layer fwd+loss, KuaiRand-shaped batch 1024, 4 tasks, 16 experts, shared top-2 + "
+                        "private top-1, d_model=128, expert MLP 128->256->128, fp32 (bf16x3 tensor-core GEMMs)"),
     "c2": dict(T=8, E=32, ks=4, ka=2, d=256, d_ff=512, d_out=256, B=16384, beta=0.01, mode="dp", scaling="weak",
                workload="c2: SMES fwd+bwd, 8 tasks, 32 experts, shared top-4 + private top-2, d_model=256, "
                         "expert MLP 256->512->256, batch 16384 per GPU, bf16"),
@@ -55,6 +58,7 @@ CONFIGS = {
 CFG = CONFIGS["c2"]
 WORKLOAD = CFG["workload"]
 METRIC = "SMES fwd+bwd samples/sec"
+METRIC_C1 = "SMES fwd+loss samples/sec (fp32)"
 UNIT = "samples/s"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -79,7 +83,7 @@ def _dist_env():
 
 # bounded CPU samples of each configuration: c2 runs the FULL 16384 batch;
 # c3 / c5 full batches need minutes and tens of GB of f64 (T,B,E) arrays per step
-CPU_SAMPLE = {"c2": 16384, "c3": 4096, "c4": 1024, "c5": 256}
+CPU_SAMPLE = {"c1": 1024, "c2": 16384, "c3": 4096, "c4": 1024, "c5": 256}
 
 
 def _host_cpu():
@@ -115,7 +119,7 @@ def _cpu_sample(cfg_name: str, steps: int, warm: int = 1):
     p = O.init_layer_params(rng, c["d"], c["d_out"], c["E"], c["T"], d_ff=c["d_ff"])
     h = rng.normal(size=(b_sample, c["d"]))
     y = (rng.uniform(size=(c["T"], b_sample)) < np.resize([0.3, 0.1, 0.05, 0.2], c["T"])[:, None]).astype(float)
-    fwd_only = c["mode"] == "infer"
+    fwd_only = c["mode"] in ("infer", "fwd32")
     times = []
     for i in range(warm + steps):
         t0 = time.perf_counter()
@@ -146,7 +150,7 @@ def run_reference(args):
     steps = max(1, min(args.steps, 5))
     cb = _cpu_sample(args.config, steps, warm=min(1, args.warmup))
     b_sample = CPU_SAMPLE[args.config]
-    metric = METRIC if c["mode"] != "infer" else "SMES inference samples/sec"
+    metric = {"infer": "SMES inference samples/sec", "fwd32": METRIC_C1}.get(c["mode"], METRIC)
     line = {"impl": "reference", "metric": metric, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus,
             "steps": steps, "warmup": min(1, args.warmup), "ms_per_step": 1e3 * b_sample / cb["value"],
             "higher_is_better": True, "scaling": c.get("scaling", "weak"), "vs_baseline": None, "dtype": "f64",
@@ -390,6 +394,8 @@ def run_ours(args):
         line = run_dp(args, c, world, rank, local, dev)
     elif mode == "ep":
         line = run_ep(args, c, world, rank, local, dev)
+    elif mode == "fwd32":
+        line = run_fwd32(args, c, world, rank, local, dev)
     else:
         line = run_infer(args, c, world, rank, local, dev)
     if rank == 0 and line is not None:
@@ -642,6 +648,109 @@ def run_infer(args, c, world, rank, local, dev):
                     "api": "pinned H2D of h, graph replay of SMESEngine.score, D2H of predictions"},
             "gpu_launches": launches, "sweep": sweep, "cpu_baseline": cpu, "clocks": _merge_clocks(clocks_all),
             "roofline": roofline, "kernels": breakdown}
+
+
+def run_fwd32(args, c, world, rank, local, dev):
+    """c1: the SMES layer forward + loss in fp32 (fp32.SMESForwardF32: bf16x3 tensor-core GEMMs, fp64
+    Stage-I routing, fp32 combine/heads/BCE), one CUDA graph per step.  N > 1: independent replicas
+    (batch-sharded, weak scaling; the forward has no cross-rank exchange but the LB statistics,
+    which the fwd+loss value reads only for the regularizer term -- replicas report their own)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2602_09386_b200 import _lib
+    from paper_2602_09386_b200.fp32 import SMESForwardF32
+    B = c["B"]
+    params = _make_params(c, dev)
+    eng = SMESForwardF32(params, B, c["ks"], c["ka"], device=dev)
+    gh = torch.Generator(device="cpu").manual_seed(1000 + rank)
+    h_host = torch.randn(B, c["d"], generator=gh).pin_memory()
+    rates = torch.tensor(np.resize([0.3, 0.1, 0.05, 0.2], c["T"]), dtype=torch.float32)[:, None]
+    y_host = (torch.rand(c["T"], B, generator=gh) < rates).float().pin_memory()
+    eng.set_inputs(h_host.to(dev), y_host.to(dev))
+    st = torch.cuda.Stream(dev)
+    st.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(st):
+        eng.forward(with_loss=True)
+    torch.cuda.current_stream(dev).wait_stream(st)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        eng.forward(with_loss=True)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        g.replay()
+    per_step = count_step_launches(lambda: eng.forward(with_loss=True))
+    ms, clocks = _timed_steps(g.replay, args.steps, world, dev, flush, local)
+    # end to end: pinned H2D of h and labels, the graph, D2H of the loss
+    loss_host = torch.empty(3, dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for e0, e1 in ev:
+        flush.zero_()                     # outside the bracket, as in the device-timed loop
+        e0.record()
+        eng.h.copy_(h_host, non_blocking=True)
+        eng.labels.copy_(y_host, non_blocking=True)
+        g.replay()
+        loss_host.copy_(eng.loss_out, non_blocking=True)
+        e1.record()
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([sum(a.elapsed_time(b) for a, b in ev) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e_ms = e_ms.item()
+    parity = None
+    if rank == 0 and not args.no_cpu:
+        parity = parity_fp32(eng, params)
+    n_act = eng.n_act()
+    kern = per_kernel_times(lambda: eng.forward(with_loss=True), reps=5)
+    peaks, peak_src = _peaks()
+    work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    cpu = _cpu_sample(args.config, 3) if (rank == 0 and not args.no_cpu) else None
+    if rank != 0:
+        return None
+    return {"metric": METRIC_C1, "value": world * B / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": c["workload"], "global_batch": world * B, "per_gpu_batch": B,
+                       "parallelism": f"replicas{world}", "n_act_rows": n_act,
+                       "l2": "flushed between steps (256 MiB memset outside the per-step event brackets)",
+                       "graph": "fwd+loss in one CUDA graph"},
+            "e2e": {"value": world * B / (e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": h_host.numel() * 4 + y_host.numel() * 4, "d2h_bytes_per_step": 24,
+                    "ms_per_step": e_ms,
+                    "api": "per step: pinned H2D of h and labels, graph replay of SMESForwardF32.forward, D2H of "
+                           "the loss (CUDA events around the three; L2 flushed between steps)"},
+            "gpu_launches": per_step * args.steps, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "parity": parity, "kernels": breakdown,
+            "kernels_note": "per-kernel CUDA-event times from an eager forward on one stream"}
+
+
+def parity_fp32(eng, params):
+    """Checker (oracle = test infrastructure): the whole c1 batch against the f64 oracle on the same
+    fp32 operands -- logits, selections (index-exact on the GPU's logits), predictions, loss."""
+    from oracle import smes_oracle as O
+    T, E, B, ks, ka = eng.T, eng.E, eng.B, eng.ks, eng.ka
+    f64 = lambda t: t.detach().double().cpu().numpy()
+    p = O.LayerParams(router_w=f64(params.router_w), router_b=f64(params.router_b),
+                      layers=[(f64(l.weight), f64(l.bias), l.act) for l in params.layers],
+                      head_w=f64(params.head_w), head_b=f64(params.head_b))
+    h = f64(eng.h)
+    z = eng.z.double().cpu().numpy().reshape(B, T, E).transpose(1, 0, 2)
+    zr = O.router_logits(h, p)
+    z_rel = float(np.abs(z - zr).max() / np.abs(zr).max())
+    r = O.route_batch(z, ks, ka)
+    sel_ok = bool(np.array_equal(eng.active.cpu().numpy(), r.active))
+    f = O.forward_sparse(h, p, ks, ka, logits=z, frozen=r)
+    pr_rel = float(np.abs(f64(eng.preds) - f.predictions).max() / np.abs(f.predictions).max())
+    bw = O.backward(f, p, f64(eng.labels), None, params.lb_strength)
+    lo = eng.loss_out.double().cpu().numpy()
+    loss_rel = abs(lo[2] - bw.total) / abs(bw.total)
+    ok = sel_ok and z_rel < 1e-5 and pr_rel < 1e-5 and loss_rel < 1e-5
+    return {"ok": bool(ok), "rows": int(B), "selections_index_exact": sel_ok, "router_logits_rel": z_rel,
+            "predictions_rel": pr_rel, "loss_gpu": float(lo[2]), "loss_oracle": float(bw.total),
+            "loss_rel": float(loss_rel), "tolerances": "fp32 1e-5 relative (north star), selections exact"}
 
 
 def _merge_clocks(cl):

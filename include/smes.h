@@ -55,8 +55,10 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
 
 /* ---- K0+K1 fused router front: RouterBank.logits (routing.py:101-103, via Affine.apply
  *      linalg.py:143-149) on the tensor cores, feeding route_batch (routing.py:235-281) straight
- *      from TMEM, two threads per row.  Same outputs and numerics as smes_route_batch (Stage I in
- *      fp64; per-chunk histograms over chunks of sub_rows = 4 * rows_per_warp rows).  z_out
+ *      from TMEM, two threads per row.  Same outputs as smes_route_batch (per-chunk histograms
+ *      over chunks of sub_rows = 4 * rows_per_warp rows).  Stage I: fp32 exponentials with fp64
+ *      sums and a certified error bound; rows whose shared set the bound cannot decide are
+ *      recomputed entirely in fp64, so the selections equal an fp64 Stage I.  z_out
  *      (B, T*E) fp32 is optional; chunk_dmass may be null (dense mass not computed).
  *      h (B, ldh) bf16, w_r (T*E, d) bf16, b_r (T*E) fp32.  Supported shapes: see
  *      smes_route_front_supported (E in {16, 32}, T*E <= 256, d in {64, ..., 256}, budget 4+2 or 2+1). */
@@ -66,6 +68,9 @@ int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r,
                      int32_t* adaptive, int32_t* active, float* wsel, uint32_t* umask, int32_t* usize,
                      int32_t* chunk_union, int32_t* chunk_active, double* chunk_mass, double* chunk_dmass,
                      int32_t* flag, float* z_out, void* stream);
+/* diagnostic: count (atomically, into *dev_counter) the rows later smes_route_front launches send
+ * through the fp64 recompute; NULL turns counting off. */
+void smes_route_front_count_exact(int32_t* dev_counter);
 
 /* ---- combine backward from a given upstream gradient of the task reps (the autograd form of the
  *      layer, SMESLayer): training.py:160-179 with d_reps (T, B, d_out) fp32 in place of
@@ -270,6 +275,27 @@ int smes_lb_grad(int T, int B, int E, int K, const int32_t* active, const float*
                  long zsb, const float* freq, float coef, int dense, float* out, void* stream);
 int smes_bce_loss(int T, int B, const float* pred, const float* labels, const float* lam, double* part, int nparts,
                   int32_t* bad, void* stream);
+
+/* ---- fp32 arithmetic mode (BASELINE c1, the north star's fp32 1e-5 contract; the reference is
+ *      float64 NumPy, linalg.py:3-8).  Dense contractions run on the tensor cores as bf16x3
+ *      products: every fp32 operand is stored as three bf16 planes [x0 | x1 | x2] along K
+ *      (x = x0 + x1 + x2, 24 significant bits) and the six leading cross terms accumulate in fp32.
+ *      smes_gemm_ragged_m_x3: C = act(A W_g^T + b_g), A (rows, >= 3K) and W (G, N, 3K) in planes,
+ *        fp32 out; replaces grouped_gemm (execution.py:126-158) and RouterBank.logits
+ *        (routing.py:101-103) in fp32.  K % 64 == 0.
+ *      smes_split_bf16x3: fp32 (rows, cols) -> planes (rows, 3 cols); rows_dev (optional, device)
+ *        caps the row count (the plan's padded row total).
+ *      smes_combine_fwd_f32: reconstruct_task_reps (execution.py:161-191) + _heads
+ *        (model.py:202-208) + clamped BCE partials (training.py:54-57), fp32 O and reps. */
+int smes_gemm_ragged_m_x3(const void* A3, long lda, long rows_cap, const void* W3, int G, int N, int K,
+                          const int* seg, const float* bias, int act, float* C, long ldc, long m_limit, void* stream);
+int smes_split_bf16x3(long rows, int cols, const float* src, long lds, void* dst, long ldd, const int32_t* rows_dev,
+                      void* stream);
+int smes_combine_fwd_f32_grid(int B);
+int smes_combine_fwd_f32(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
+                         const int32_t* row_of, const int32_t* active, const float* wsel, const float* O, long ldo,
+                         const float* head_w, const float* head_b, float* reps, float* logits, float* preds,
+                         const float* labels, const float* lam, double* loss_part, int grid, void* stream);
 
 #ifdef __cplusplus
 }

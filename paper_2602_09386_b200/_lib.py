@@ -28,6 +28,7 @@ SIGNATURES = {
     "smes_route_num_chunks": [I, I],
     "smes_route_batch": [P, L, L, P, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, P],
     "smes_route_front_supported": [I, I, I, I, I],
+    "smes_route_front_count_exact": [P],
     "smes_peer_allreduce_f64": [I, I, I, P, P, P, P, P, P, P, P],
     "smes_combine_bwd_reps": [I, I, I, I, I, I, P, P, P, P, P, P, L, I, P, P, F, P, P, L, P],
     "smes_route_front": [P, L, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
@@ -72,11 +73,16 @@ SIGNATURES = {
     "smes_post_combine": [I, P, I, P, P, I, P, P, I, P, P, D, D, P, P, P],
     "smes_lb_grad": [I, I, I, I, P, P, P, L, L, P, F, I, P, P],
     "smes_bce_loss": [I, I, P, P, P, P, I, P, P],
+    "smes_gemm_ragged_m_x3": [P, L, L, P, I, I, I, P, P, I, P, L, L, P],
+    "smes_split_bf16x3": [L, I, P, L, P, L, P, P],
+    "smes_combine_fwd_f32_grid": [I],
+    "smes_combine_fwd_f32": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, P, P, P, P, P, I, P],
 }
 _RESTYPE = {"smes_last_error": C.c_char_p}
 # entry points that return a value rather than a status
 _VALUE_FNS = {"smes_abi_version", "smes_route_front_supported", "smes_fold_work_floats", "smes_fold_gemm_path", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
-              "smes_last_error"}
+              "smes_combine_fwd_f32_grid", "smes_last_error",
+              "smes_route_front_count_exact"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
 def _fold_gemm_path(E, T, d_out, d_in):      # csrc/fold.cu gemm_path()
@@ -102,7 +108,8 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_all
                     "smes_mlp_fwd": 1, "smes_mlp_fwd2": 1, "smes_mlp_dgrad": 1, "smes_mlp_dgrad2": 1, "smes_mlp_wgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
-                    "smes_ep_copy_rows_put": 1}
+                    "smes_ep_copy_rows_put": 1, "smes_gemm_ragged_m_x3": 1, "smes_split_bf16x3": 1,
+                    "smes_combine_fwd_f32": 1}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 trace = None    # optional list: every successful call appends (tag, kernels launched) -- ncu launch tags

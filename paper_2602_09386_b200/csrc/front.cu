@@ -4,27 +4,31 @@
 //   z[b, t*E + e] = h[b] . W_r[t*E + e] + b_r[t*E + e]          (RouterBank.logits, routing.py:101-103)
 //   route_batch over z                                            (routing.py:235-281)
 //
-// A 128-row tile of h (TMA, SW128) times the whole router bank W_r (N = T*E <= 256
-// columns, K-major) accumulates in TMEM (tcgen05.mma, fp32); two accumulators let the
-// MMA of the next tile run under the routing of this one.  The routing epilogue reads
-// the logits from TMEM (epilogue thread i of a lane quarter owns TMEM lane i = row)
-// with four threads per row, in the four warps that share a lane quarter:
-//   Stage I   (split by expert quarters) p_t = softmax(z_t) and pooled = sum_t w_t p_t
-//             in fp64, as route_kernel: exp, sums and pooling in double, the quarter
-//             sums of each task exchanged through shared memory (fixed order); every
-//             thread keeps its quarter's top-K_s, and the four sorted lists are merged
-//             into shared = top-K_s of pooled, (score desc, index asc)  (routing.py:256-261).
-//   Stage II  (split by tasks, t = g, g + 4, ...) exact fp32 compare of z_t with the
-//             shared set excluded (:263-268), weights = softmax of z_t over the active
-//             set (:203-211, :273), union bitmask (:272).
-//   LoadStats partials per chunk of `sub_rows` rows (the plan's chunk, 4 * rows_per_warp):
-//             union counts, active counts, sparse and (DM) dense mass per expert.  Each
-//             thread leaves dense per-row partials in shared memory; a fixed-order reduce
-//             over rows and threads produces the chunk sums (no atomics, deterministic;
-//             balance.py:65-68, execution.py:109-113).
+// A tile of h rows (TMA, SW128; 128 MMA rows, `rpc` <= 128 of them routed by this CTA so the
+// grid covers every SM) times the whole router bank W_r (N = T*E <= 256 columns, K-major)
+// accumulates in TMEM (tcgen05.mma, fp32); two accumulators let the MMA of the next tile run
+// under the routing of this one.  Epilogue thread (g, lane) of lane quarter q owns row
+// 32q + lane (its TMEM lane) and the tasks t = g, g + TPR, ...:
 //
-// Warp roles (640 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
-// w4..w19 routing epilogue (warp w: lane quarter (w - 4) & 3, row thread g = (w - 4) >> 2).
+//   Stage I  pooled[e] = sum_t w_t softmax(z_t)[e] and shared = top-K_s(pooled), ties to the
+//            lowest index (routing.py:256-261).  Reference-init routers give pooled gaps down to
+//            1e-10, so the SET must come out as an fp64 evaluation would give it.
+//            Fast path: exp in fp32 (__expf), softmax sums and pooling in fp64, and a rigorous
+//            per-expert bound on the fp32 exp error (documented __expf bound: (2 + 1.173|x|)
+//            ulp, plus the argument rounding; inflated 1.5x).  The set is accepted when every
+//            selected expert's lower bound exceeds every unselected expert's upper bound.
+//            Rows that fail (near-ties: ~5 % at reference init, ~0 at trained scale) are
+//            staged to shared memory and recomputed entirely in fp64 by whole warps (lane =
+//            expert), then their set replaces the fast one.  Selections stay index-exact.
+//   Stage II (same tasks) exact fp32 compare of z_t with the shared set excluded (:263-268),
+//            weights = softmax of z_t over the active set (:203-211, :273), union (:272).
+//   LoadStats partials per chunk of `sub_rows` rows (the plan's chunk, 4 * rows_per_warp):
+//            union counts, active counts (bit-sliced counters), sparse and (DM) dense mass per
+//            expert, reduced in a fixed row order (no atomics; balance.py:65-68,
+//            execution.py:109-113).
+//
+// Warp roles (384 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer, w2 TMEM allocator,
+// w4..w11 routing epilogue (warp w: lane quarter (w - 4) & 3, task thread g = (w - 4) >> 2).
 #include "ptx.cuh"
 #include "smes_capi.h"
 
@@ -34,14 +38,15 @@ namespace front {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-// TPR threads per row (2 or 4): 4 non-epilogue warps + 4 * TPR epilogue warps
-template <int TPR> constexpr int kThreads = 128 + 128 * TPR;
-template <int TPR> constexpr int kEpi = 128 * TPR;
+constexpr int TPR = 2;                       // task threads per row
+constexpr int kThreads = 128 + 128 * TPR;
+constexpr int kEpi = 128 * TPR;
+constexpr int kNPlanes = 4;                  // bit-sliced active counters (up to 15 tasks per thread)
 
 struct Args {
   const float* bias;       // (T*E) router bias
   const double* tw;        // (T,) Stage-I pooling weights
-  int T, B, d, sub_rows;
+  int T, B, d, sub_rows, rpc;
   int32_t* shared;         // (B, KS)
   int32_t* adaptive;       // (T, B, KA)
   int32_t* active;         // (T, B, K)
@@ -54,32 +59,49 @@ struct Args {
   double* chunk_dmass;     // written only with DM (dense-mass statistics requested)
   int32_t* flag;           // non-finite logits (sticky)
   float* z_out;            // optional (B, T*E) fp32 logits
+  int32_t* n_exact;        // optional: rows whose shared set needed the fp64 recompute (summed)
 };
 
-template <int E, int TPR>
+template <int E, bool DM>
 struct Plan {
+  static constexpr int EQ = E / TPR;
   // the router GEMM is issued in N chunks of (up to) 64 columns, each committed on its own
   // barrier, so Stage I of the first tasks runs while the MMAs of the later tasks stream W_r
-  static constexpr int kWStages = 4;
+  static constexpr int kWStages = DM ? 3 : 4;     // (DM: the dense-mass array needs the space)
   static constexpr int kH = BM * BK * 2;          // 16 KB per k-block of h (d <= 256: 4 blocks)
   static constexpr int kW = 64 * BK * 2;          // 8 KB per (chunk, k-block) of W_r
   static constexpr int kOffW = 4 * kH;
   static constexpr int kOffBias = kOffW + kWStages * kW;         // T*E floats (<= 1 KB)
-  static constexpr int kOffTw = kOffBias + 1024;                 // T doubles (<= 32)
-  static constexpr int kOffM = kOffTw + 256;                     // [T][128] fp32 task maxima (T <= 16)
-  // [TPR threads][E][128] fp32 per-row sparse-mass partials (Stage II); before that, the
-  // per-thread top-K_s candidates [TPR][4][128] fp64 keys + [TPR][4][128] u8 indices (Stage I)
-  static constexpr int kOffMass = kOffM + 16 * BM * 4;
-  static constexpr int kOffDm = kOffMass + TPR * E * BM * 4;     // [E][128] fp32 dense mass
-  static constexpr int kOffCnt = kOffDm + E * BM * 4;            // [TPR][E/4][128] u32, 4 packed u8 counts
-  static constexpr int kOffSum = kOffCnt + TPR * E * BM;         // [2 parity][TPR][128] fp64 partial sums
-  static constexpr int kOffUn = kOffSum + 2 * TPR * BM * 8;      // [TPR][128] u32 union words
-  static constexpr int kOffBar = kOffUn + TPR * BM * 4;
+  static constexpr int kOffTw = kOffBias + 1024;                 // T doubles (<= 16)
+  static constexpr int kOffM = kOffTw + 128;                     // [16][128] fp32 task maxima
+  // R1 (64 KB), reused phase by phase: the Stage-I exchange of pooled partials [TPR][EQ][128]
+  // fp64 + exp error bounds [TPR][128] fp32; the fp64 recompute's staged logits; in Stage II
+  // the per-thread logit rows [kEpi][E] and the sparse-mass partials [TPR][E][128] (at 32 KB)
+  static constexpr int kR1 = 32 * 1024 + TPR * BM * (E + 1) * 4;
+  static constexpr int kOffR1 = kOffM + 16 * BM * 4;
+  static constexpr int kOffCand = kOffR1 + kR1;                  // [TPR][4][128] u64 keys + u8 indices
+  // per-row arrays the chunk statistics read across experts: row stride E + 1 (E/4 + 1) words, so
+  // both the per-row writers (lane = row) and the readers (lane = expert) are bank-conflict free
+  static constexpr int kOffDm = kOffCand + TPR * 4 * BM * 9 + 64;   // [TPR][128][E + 1] fp32 dense mass
+  static constexpr int kOffCnt = kOffDm + (DM ? TPR * BM * (E + 1) * 4 : 0);   // [TPR][128][E/4 + 1] u8 x 4
+  static constexpr int kOffLoHi = kOffCnt + TPR * BM * (E / 4 + 1) * 4;       // [TPR][2][128] fp64
+  static constexpr int kOffUn = kOffLoHi + TPR * 2 * BM * 8;             // [TPR][128] u32 union words
+  static constexpr int kOffSlot = kOffUn + TPR * BM * 4;                 // [128] slot, [CAPMAX] set, counter
+  static constexpr int kOffBar = kOffSlot + (BM + 96 + 4) * 4;
   static constexpr int kBytes = kOffBar + 512 + 1024;
   static_assert(E <= 32, "one union word per row");
-  static_assert(TPR * 4 * BM * 9 <= TPR * E * BM * 4, "candidate lists fit the mass region");
+  static_assert(TPR * EQ * BM * 12 <= kR1, "exchange fits R1");
+  static_assert(kEpi * E * 4 <= 32 * 1024, "Stage-II logit rows fit the first 32 KB of R1");
   static_assert(kBytes <= 232448, "front smem plan exceeds 227 KB");
 };
+
+// e^x as ex2.approx.ftz(x log2 e): the CUDA __expf algorithm (max error (2 + 1.173 |x|) ulp for
+// normal results), without its subnormal fix-up (results below 2^-126 flush to 0)
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
+}
 
 __device__ __forceinline__ void bar_named(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -114,31 +136,6 @@ __device__ __forceinline__ void load_task(uint32_t taddr, const float* sbias, in
   }
 }
 
-// columns [c, c + N) of this thread's TMEM lane (warp-collective), N in {4, 8, 16}
-template <int N>
-__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
-  uint32_t r[N];
-  if constexpr (N == 8) {
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-                 : "r"(taddr));
-  } else if constexpr (N == 16) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-  } else {
-    static_assert(N == 4, "row-slice width");
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(taddr));
-  }
-#pragma unroll
-  for (int j = 0; j < N; ++j) v[j] = __uint_as_float(r[j]);
-}
-
 template <int E>
 __device__ __forceinline__ float tree_max(const float (&z)[E]) {
   float m[E / 2];
@@ -150,13 +147,39 @@ __device__ __forceinline__ float tree_max(const float (&z)[E]) {
     for (int j = 0; j < s; ++j) m[j] = fmaxf(m[j], m[j + s]);
   return m[0];
 }
+template <int E>
+__device__ __forceinline__ float tree_min(const float (&z)[E]) {
+  float m[E / 2];
+#pragma unroll
+  for (int j = 0; j < E / 2; ++j) m[j] = fminf(z[j], z[j + E / 2]);
+#pragma unroll
+  for (int s = E / 4; s > 0; s >>= 1)
+#pragma unroll
+    for (int j = 0; j < s; ++j) m[j] = fminf(m[j], m[j + s]);
+  return m[0];
+}
 
-template <int E, int KS, int KA, bool DM, int TPR>
-__global__ void __launch_bounds__(kThreads<TPR>, 1)
+// (key desc, index asc) arg-max over a group of G lanes (G = E <= 32, aligned), 64-bit keys
+template <int G>
+__device__ __forceinline__ void group_argmax(unsigned long long& key, int& idx) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, key, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    const bool take = (k2 > key) | ((k2 == key) & (i2 < idx));
+    key = take ? k2 : key;
+    idx = take ? i2 : idx;
+  }
+}
+
+template <int E, int KS, int KA, bool DM>
+__global__ void __launch_bounds__(kThreads, 1)
     route_front_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const Args a) {
-  using S = Plan<E, TPR>;
+  using S = Plan<E, DM>;
   constexpr int K = KS + KA;
+  constexpr int EQ = S::EQ;
+  static_assert(TPR == 2, "the Stage-I exchange pairs two task threads per row");
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sH = smem;
@@ -164,13 +187,21 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
   float* sbias = reinterpret_cast<float*>(smem + S::kOffBias);
   double* stw = reinterpret_cast<double*>(smem + S::kOffTw);
   float* s_m = reinterpret_cast<float*>(smem + S::kOffM);
-  float* s_mass = reinterpret_cast<float*>(smem + S::kOffMass);
-  unsigned long long* s_ckey = reinterpret_cast<unsigned long long*>(smem + S::kOffMass);   // Stage I only
-  uint8_t* s_cidx = smem + S::kOffMass + TPR * 4 * BM * 8;
+  uint8_t* r1 = smem + S::kOffR1;
+  double* x_pp = reinterpret_cast<double*>(r1);                          // [TPR][EQ][BM]
+  float* x_pe = reinterpret_cast<float*>(r1 + TPR * EQ * BM * 8);        // [TPR][BM] exp error bounds
+  float* s_stage = reinterpret_cast<float*>(r1);                         // [CAP][T][E]
+  float* s_scr = reinterpret_cast<float*>(r1);                           // [kEpi][E] (Stage II)
+  float* s_mass = reinterpret_cast<float*>(r1 + 32 * 1024);              // [TPR][BM][E + 1]
+  unsigned long long* s_ckey = reinterpret_cast<unsigned long long*>(smem + S::kOffCand);
+  uint8_t* s_cidx = smem + S::kOffCand + TPR * 4 * BM * 8;
   float* s_dm = reinterpret_cast<float*>(smem + S::kOffDm);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(smem + S::kOffCnt);
-  double* s_sum = reinterpret_cast<double*>(smem + S::kOffSum);
+  double* s_lohi = reinterpret_cast<double*>(smem + S::kOffLoHi);
   uint32_t* s_un = reinterpret_cast<uint32_t*>(smem + S::kOffUn);
+  int* s_slot = reinterpret_cast<int*>(smem + S::kOffSlot);              // [BM]
+  uint32_t* s_fix = reinterpret_cast<uint32_t*>(s_slot + BM);            // [<= 96]
+  int* s_nf = s_slot + BM + 96;
   uint64_t* wfull = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
   uint64_t* wempty = wfull + S::kWStages;
   uint64_t* hfull = wempty + S::kWStages;
@@ -182,21 +213,24 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = a.T, N = T * E;
   const int ncols = N <= 64 ? 128 : N <= 128 ? 256 : 512;   // two accumulators, power of two
-  const int num_tiles = (a.B + BM - 1) / BM;
+  const int rpc = a.rpc;
+  const int num_tiles = (a.B + rpc - 1) / rpc;
   const int nkb = (a.d + BK - 1) / BK;
   // columns per chunk: <= 64 (the W_r ring slot), a multiple of E (whole tasks per chunk)
   const int NC = N % 64 == 0 ? 64 : N % 32 == 0 ? 32 : 16;
   const int nch = N / NC;
+  const int cap = min(96, S::kR1 / (N * 4));                 // rows per fp64 recompute round
 
   for (int i = threadIdx.x; i < N; i += blockDim.x) sbias[i] = a.bias[i];
   for (int i = threadIdx.x; i < T; i += blockDim.x) stw[i] = a.tw[i];
+  if (threadIdx.x == 0) *s_nf = 0;
   if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < S::kWStages; ++s) { mbar_init(&wfull[s], 1); mbar_init(&wempty[s], 1); }
     mbar_init(hfull, 1);
     mbar_init(hempty, 1);
     for (int s = 0; s < 32; ++s) mbar_init(&tfull[s], 1);
-    for (int s = 0; s < 2; ++s) mbar_init(&tempty[s], kEpi<TPR>);
+    for (int s = 0; s < 2; ++s) mbar_init(&tempty[s], kEpi);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, ncols);
@@ -214,7 +248,7 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
         mbar_wait(hempty, (it & 1) ^ 1);
         mbar_expect_tx(hfull, nkb * S::kH);
-        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sH + kb * S::kH, &tmA, hfull, kb * BK, tile * BM);
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sH + kb * S::kH, &tmA, hfull, kb * BK, tile * rpc);
         for (int c = 0; c < nch; ++c) {
           for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&wempty[stage], phase ^ 1);
@@ -257,130 +291,240 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
       }
     }
   } else if (warp >= 4) {
-    // ================= routing epilogue: four threads per row
-    constexpr int EQ = E / TPR;              // Stage-I experts per thread
+    // ================= routing epilogue
     const int q = (warp - 4) & 3;
     const int g = (warp - 4) >> 2;
-    const int j0 = g * EQ;
     const int r_loc = 32 * q + lane;
     const int quad_bar = 1 + q;              // the TPR warps of this lane quarter
-    const int nsub = BM / a.sub_rows;
+    const int tid = threadIdx.x - 128;
     const int C = (a.B + a.sub_rows - 1) / a.sub_rows;
-    int it = 0, bad = 0;
+    const int nsub = rpc / a.sub_rows;
+    int it = 0, bad = 0, n_exact = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int acc = it & 1;
-      const int b = tile * BM + r_loc;
-      const bool valid = b < a.B;
+      const int b = tile * rpc + r_loc;
+      const bool valid = r_loc < rpc && b < a.B;
       const uint32_t taddr = tmem_base + ((uint32_t)(32 * q) << 16) + acc * N;
+      const uint32_t tpar = (it >> 1) & 1;
 #ifdef SMES_FRONT_GEMM_ONLY
-      for (int c = 0; c < nch; ++c) mbar_wait(&tfull[acc * 16 + c], (it >> 1) & 1);
+      for (int c = 0; c < nch; ++c) mbar_wait(&tfull[acc * 16 + c], tpar);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       continue;
 #endif
+      int waited = 0;
+      auto wait_task = [&](int t) {          // the MMA chunks up to task t's are committed
+        const int ct = (t * E) / NC;
+        while (waited <= ct) {
+          mbar_wait(&tfull[acc * 16 + waited], tpar);
+          ++waited;
+        }
+        tc_fence_after();
+      };
 
-      // ---------------- Stage I (fp64): this thread's quarter of the experts of every task
-      double pp[EQ];
-      {
-        float dm[EQ];
+      // ---------------- Stage I, fast path: this thread's tasks, every expert
+      uint32_t smask = 0;
+      bool exact_needed = false;
+      if constexpr (KS > 0 || DM) {
+        double pp[E];
+        float emax = 0.f;          // max over this thread's tasks of the relative exp error bound
 #pragma unroll
-        for (int j = 0; j < EQ; ++j) { pp[j] = 0.0; dm[j] = 0.f; }
-        int chunk = 0, next_chunk_task = 0;
-        for (int t = 0; t < T; ++t) {
-          if (t == next_chunk_task) {        // first task of a chunk: wait for its MMAs
-            mbar_wait(&tfull[acc * 16 + chunk], (it >> 1) & 1);
-            tc_fence_after();
-            ++chunk;
-            next_chunk_task += NC / E;
-          }
-          float zq[EQ];                       // this quarter's logits
-          tmem_ldn<EQ>(taddr + t * E + j0, zq);
+        for (int j = 0; j < E; ++j) pp[j] = 0.0;
+        bool first = true;
+        for (int t = g; t < T; t += TPR) {
+          wait_task(t);
           float z[E];
-          load_task<E>(taddr, sbias, t, z);   // (waits for both loads)
-          const float mf = tree_max<E>(z);
-          if (g == t % TPR) s_m[t * BM + r_loc] = mf;
-          const double m = (double)mf;
-#pragma unroll
-          for (int j = 0; j < EQ; ++j) {
-            zq[j] += sbias[t * E + j0 + j];
-            bad |= !isfinite(zq[j]);
-          }
+          load_task<E>(taddr, sbias, t, z);
+          const float mx = tree_max<E>(z), mn = tree_min<E>(z);
+          s_m[t * BM + r_loc] = mx;
           if (a.z_out != nullptr && valid) {
-            float4* zo = reinterpret_cast<float4*>(a.z_out + (size_t)b * N + t * E + j0);
+            float4* zo = reinterpret_cast<float4*>(a.z_out + (size_t)b * N + t * E);
 #pragma unroll
-            for (int j = 0; j < EQ; j += 4) zo[j / 4] = make_float4(zq[j], zq[j + 1], zq[j + 2], zq[j + 3]);
+            for (int j = 0; j < E; j += 4) zo[j / 4] = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
           }
-          double ev[EQ], s = 0.0;
+          double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < EQ; ++j) { ev[j] = exp((double)zq[j] - m); s += ev[j]; }
-          double* slot = s_sum + (t & 1) * TPR * BM;
-          slot[g * BM + r_loc] = s;
-          bar_named(quad_bar, 32 * TPR);
-          double stot = slot[r_loc];
+          for (int j = 0; j < E; ++j) {
+            z[j] = fast_exp(z[j] - mx);
+            s4[j & 3] += (double)z[j];
+          }
+          const double ssum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          bad |= !(isfinite(mx) & isfinite(mn) & isfinite(ssum));
+          const double qd = stw[t] / ssum;
 #pragma unroll
-          for (int h = 1; h < TPR; ++h) stot += slot[h * BM + r_loc];     // fixed order
-          const double inv = 1.0 / stot;
-          const double wt = stw[t];
+          for (int j = 0; j < E; ++j) pp[j] = fma(qd, (double)z[j], pp[j]);
+          // relative error of every w_t p_tj: the exp of the numerator and of the sum, each within
+          // (2 + 1.173 |x|) ulp (fast_exp, |x| <= mx - mn) + the argument rounding; flushed results
+          // (< 2^-126) are covered by the absolute slack of the certification
+          emax = fmaxf(emax, (3.f + 2.f * (mx - mn)) * 0x1p-23f);
+          if constexpr (DM) {
+            const float qf = (float)(1.0 / ssum);
 #pragma unroll
-          for (int j = 0; j < EQ; ++j) {
-            const double p = ev[j] * inv;
-            pp[j] = fma(wt, p, pp[j]);
-            if (DM) dm[j] += (float)p;
+            for (int j = 0; j < E; ++j) {
+              float* dp = s_dm + (g * BM + r_loc) * (E + 1) + j;
+              *dp = first ? qf * z[j] : fmaf(qf, z[j], *dp);
+            }
+          }
+          first = false;
+        }
+        if constexpr (DM) {
+          if (first || !valid) {
+#pragma unroll
+            for (int j = 0; j < E; ++j) s_dm[(g * BM + r_loc) * (E + 1) + j] = 0.f;
           }
         }
-        if (DM) {
+        if constexpr (KS > 0) {
+          // exchange: thread g owns experts [g EQ, (g + 1) EQ); pooled = own partial + partner's
+          // (fp64 addition commutes, so both threads would get the same value)
+          const int oh = 1 - g;
 #pragma unroll
-          for (int j = 0; j < EQ; ++j) s_dm[(j0 + j) * BM + r_loc] = valid ? dm[j] : 0.f;
+          for (int j = 0; j < EQ; ++j) x_pp[(oh * EQ + j) * BM + r_loc] = g == 0 ? pp[EQ + j] : pp[j];
+          x_pe[g * BM + r_loc] = emax;
+          bar_named(quad_bar, 32 * TPR);
+          double pq[EQ];
+#pragma unroll
+          for (int j = 0; j < EQ; ++j) pq[j] = (g == 0 ? pp[j] : pp[EQ + j]) + x_pp[(g * EQ + j) * BM + r_loc];
+          // pooled error <= 1.5 x 2 x max eps x pooled (both exp errors, 1.5x margin); the fp64
+          // arithmetic and the fp32 -> fp64 products add < 2^-48 relative
+          const double erel = 3.0 * (double)fmaxf(x_pe[r_loc], x_pe[BM + r_loc]) + 0x1p-48;
+          const int j0 = g * EQ;
+          // shared set: top-K_s of pooled, (score desc, index asc).  pooled >= 0, so the fp64 bit
+          // patterns order like unsigned integers.  Each thread sorts its half, the lists merge
+          // through shared memory.
+          unsigned long long pk[EQ];
+#pragma unroll
+          for (int j = 0; j < EQ; ++j) pk[j] = (unsigned long long)__double_as_longlong(pq[j]);
+          uint32_t taken = 0;
+#pragma unroll
+          for (int k = 0; k < KS; ++k) {
+            unsigned long long best = 0ull;
+            int bi = -1;
+#pragma unroll
+            for (int j = 0; j < EQ; ++j) {
+              const bool take = !((taken >> j) & 1u) & ((bi < 0) | (pk[j] > best));
+              best = take ? pk[j] : best;
+              bi = take ? j : bi;
+            }
+            if (k < EQ) taken |= 1u << bi;
+            s_ckey[(g * KS + k) * BM + r_loc] = k < EQ ? best : 0ull;
+            s_cidx[(g * KS + k) * BM + r_loc] = k < EQ ? (uint8_t)(j0 + bi) : (uint8_t)255;
+          }
+          bar_named(quad_bar, 32 * TPR);
+          int head[TPR];
+#pragma unroll
+          for (int h = 0; h < TPR; ++h) head[h] = 0;
+#pragma unroll
+          for (int k = 0; k < KS; ++k) {
+            unsigned long long best = 0ull;
+            int bidx = 255, bg = 0;
+#pragma unroll
+            for (int h = 0; h < TPR; ++h) {
+              const bool ok = head[h] < KS;
+              const int slot = (h * KS + (ok ? head[h] : 0)) * BM + r_loc;
+              const unsigned long long key = s_ckey[slot];
+              const int idx = s_cidx[slot];
+              const bool take = ok & (idx != 255) & ((bidx == 255) | (key > best) | ((key == best) & (idx < bidx)));
+              best = take ? key : best;
+              bidx = take ? idx : bidx;
+              bg = take ? h : bg;
+            }
+            smask |= 1u << bidx;
+#pragma unroll
+            for (int h = 0; h < TPR; ++h) head[h] += (h == bg);
+          }
+          // certify the set: min over selected of (pooled - err) > max over the rest of (pooled + err)
+          double lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < EQ; ++j) {
+            const double err = pq[j] * erel + 0x1p-100;
+            const bool sel = (smask >> (j0 + j)) & 1u;
+            lo = sel ? fmin(lo, pq[j] - err) : lo;
+            hi = sel ? hi : fmax(hi, pq[j] + err);
+          }
+          s_lohi[(g * 2) * BM + r_loc] = lo;
+          s_lohi[(g * 2 + 1) * BM + r_loc] = hi;
+          bar_named(quad_bar, 32 * TPR);
+          const double lo_all = fmin(s_lohi[0 * BM + r_loc], s_lohi[2 * BM + r_loc]);
+          const double hi_all = fmax(s_lohi[1 * BM + r_loc], s_lohi[3 * BM + r_loc]);
+          exact_needed = valid && !(lo_all > hi_all);
         }
       }
-      // shared set: top-K_s of pooled, (score desc, index asc).  pooled >= 0, so the fp64 bit
-      // patterns order like unsigned integers.  Each thread sorts its quarter, the four lists
-      // are merged through shared memory.
-      uint32_t smask = 0;
+
+      // ---------------- Stage I, exact path: rows the fast path could not certify, in fp64
       if constexpr (KS > 0) {
-        unsigned long long pk[EQ];
+        if (g == 0) s_slot[r_loc] = exact_needed ? atomicAdd(s_nf, 1) : -1;
+        bar_named(5, kEpi);
+        const int nf = *s_nf;
+        const int slot = s_slot[r_loc];
+#ifdef SMES_FRONT_NO_EXACT
+        if (nf < 0)
+#endif
+        for (int base = 0; base < nf; base += cap) {
+          const bool mine = slot >= base && slot < base + cap;
+          if (__any_sync(0xffffffffu, mine)) {        // warp-uniform TMEM loads
+            for (int t = g; t < T; t += TPR) {
+              float z[E];
+              load_task<E>(taddr, sbias, t, z);
+              if (mine) {
+                float4* dst = reinterpret_cast<float4*>(s_stage + ((size_t)(slot - base) * T + t) * E);
 #pragma unroll
-        for (int j = 0; j < EQ; ++j) pk[j] = (unsigned long long)__double_as_longlong(pp[j]);
-        uint32_t taken = 0;
-#pragma unroll
-        for (int k = 0; k < KS; ++k) {
-          unsigned long long best = 0ull;
-          int bi = -1;
-#pragma unroll
-          for (int j = 0; j < EQ; ++j) {
-            const bool take = !((taken >> j) & 1u) & ((bi < 0) | (pk[j] > best));
-            best = take ? pk[j] : best;
-            bi = take ? j : bi;
+                for (int j = 0; j < E; j += 4) dst[j / 4] = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
+              }
+            }
           }
-          if (k < EQ) taken |= 1u << bi;
-          s_ckey[(g * KS + k) * BM + r_loc] = k < EQ ? best : 0ull;
-          s_cidx[(g * KS + k) * BM + r_loc] = k < EQ ? (uint8_t)(j0 + bi) : (uint8_t)255;
-        }
-        bar_named(quad_bar, 32 * TPR);
-        int head[TPR];
+          bar_named(5, kEpi);
+          // whole warps: lane = expert (E = 16: two rows per warp)
+          constexpr int RPW = 32 / E;
+          const int nrows = min(cap, nf - base);
+          const int wi = warp - 4;
+          const int e = lane % E;
+          for (int r0 = wi * RPW; r0 < nrows; r0 += (kEpi / 32) * RPW) {
+            const int sr = r0 + lane / E;
+            const bool act = sr < nrows;
+            double pooled = 0.0;
+            // four tasks at a time: their shuffle / exp chains are independent (latency overlap)
+            for (int t0 = 0; t0 < T; t0 += 4) {
+              float zz[4], m[4];
 #pragma unroll
-        for (int h = 0; h < TPR; ++h) head[h] = 0;
+              for (int u = 0; u < 4; ++u) {
+                zz[u] = (act && t0 + u < T) ? s_stage[((size_t)sr * T + t0 + u) * E + e] : 0.f;
+                m[u] = zz[u];
+              }
 #pragma unroll
-        for (int k = 0; k < KS; ++k) {
-          unsigned long long best = 0ull;
-          int bidx = 255, bg = 0;
+              for (int o = E / 2; o > 0; o >>= 1)
 #pragma unroll
-          for (int h = 0; h < TPR; ++h) {
-            const bool ok = head[h] < KS;
-            const int slot = (h * KS + (ok ? head[h] : 0)) * BM + r_loc;
-            const unsigned long long key = s_ckey[slot];
-            const int idx = s_cidx[slot];
-            // (key desc, index asc); exhausted lists and empty slots (index 255) never win
-            const bool take = ok & (idx != 255) & ((bidx == 255) | (key > best) | ((key == best) & (idx < bidx)));
-            best = take ? key : best;
-            bidx = take ? idx : bidx;
-            bg = take ? h : bg;
+                for (int u = 0; u < 4; ++u) m[u] = fmaxf(m[u], __shfl_xor_sync(0xffffffffu, m[u], o));
+              double ev[4], sm[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) { ev[u] = exp((double)zz[u] - (double)m[u]); sm[u] = ev[u]; }
+#pragma unroll
+              for (int o = E / 2; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) sm[u] += __shfl_xor_sync(0xffffffffu, sm[u], o);
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (t0 + u < T) pooled = fma(stw[t0 + u], ev[u] / sm[u], pooled);
+            }
+            uint32_t set = 0;
+            // pooled >= 0: its bit pattern orders as an unsigned key.  A taken expert drops to key 0
+            // with index +inf, so it loses every later round (also to a live expert with pooled 0)
+            unsigned long long mykey = (unsigned long long)__double_as_longlong(pooled);
+            int myidx = e;
+#pragma unroll
+            for (int k = 0; k < KS; ++k) {
+              unsigned long long key = mykey;
+              int idx = myidx;
+              group_argmax<E>(key, idx);
+              set |= 1u << idx;
+              if (idx == e) { mykey = 0ull; myidx = 0x7fffffff; }
+            }
+            if (act && e == 0) s_fix[sr] = set;
           }
-          smask |= 1u << bidx;
-#pragma unroll
-          for (int h = 0; h < TPR; ++h) head[h] += (h == bg);
+          bar_named(5, kEpi);
+          if (mine) smask = s_fix[slot - base];
         }
         if (g == 0 && valid) {
+          n_exact += slot >= 0;
           uint32_t m = smask;
 #pragma unroll
           for (int k = 0; k < KS; ++k) {
@@ -389,17 +533,27 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
           }
         }
       }
-      bar_named(quad_bar, 32 * TPR);    // candidate reads done: the region becomes the mass partials
 
-      // ---------------- Stage II: tasks g, g + 4, ...
-      uint32_t cnt_p[E / 4];            // active counts, four u8 per word
+      // ---------------- Stage II: tasks g, g + TPR, ...
+      uint32_t cnt[kNPlanes];           // bit-sliced per-expert active counters
 #pragma unroll
-      for (int j = 0; j < E / 4; ++j) cnt_p[j] = 0u;
+      for (int p = 0; p < kNPlanes; ++p) cnt[p] = 0u;
+#pragma unroll
+      for (int j = 0; j < E; ++j) s_mass[(g * BM + r_loc) * (E + 1) + j] = 0.f;
+      constexpr int SW = E / 4 - 1;     // 16-byte chunk swizzle of the per-thread logit row
+      float* my_row = s_scr + tid * E;
       uint32_t un = smask;
-      bool first = true;
+#ifdef SMES_FRONT_NO_STAGE2
+      if (T < 0)
+#endif
       for (int t = g; t < T; t += TPR) {
+        if constexpr (KS == 0 && !DM) wait_task(t);
         float z[E];
         load_task<E>(taddr, sbias, t, z);
+        if constexpr (KS == 0 && !DM) {     // no Stage I: the finiteness check (routing.py:246-247) is here
+#pragma unroll
+          for (int j = 0; j < E; ++j) bad |= !isfinite(z[j]);
+        }
         float tz[KA > 0 ? KA : 1];
         int ti[KA > 0 ? KA : 1];
 #pragma unroll
@@ -426,64 +580,93 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
         for (int k = 0; k < KA; ++k) amask |= 1u << ti[k];
         const uint32_t act = smask | amask;
         un |= amask;
+        {   // bit-sliced add of the active set to the per-expert counters
+          uint32_t c = act;
+#pragma unroll
+          for (int p = 0; p < kNPlanes; ++p) { const uint32_t nc = cnt[p] & c; cnt[p] ^= c; c = nc; }
+        }
         // max over the active set: with K_a >= 1 the row maximum is always active (shared, or the
         // first adaptive pick), so it is the task maximum of Stage I
         float amx;
-        if constexpr (KA > 0) {
+        if constexpr (KA > 0 && (KS > 0 || DM)) {
           amx = s_m[t * BM + r_loc];
         } else {
           amx = -INFINITY;
 #pragma unroll
           for (int j = 0; j < E; ++j) amx = ((act >> j) & 1u) ? fmaxf(amx, z[j]) : amx;
         }
+        // the K active logits, ascending expert index, through this thread's shared-memory row
+#pragma unroll
+        for (int c = 0; c < E / 4; ++c)
+          *reinterpret_cast<float4*>(my_row + ((c ^ (tid & SW)) << 2)) =
+              make_float4(z[4 * c], z[4 * c + 1], z[4 * c + 2], z[4 * c + 3]);
+        int idx[K];
+        float ev[K];
+        {
+          uint32_t m = act;
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int j = __ffs(m) - 1;
+            m &= m - 1;
+            idx[k] = j;
+            ev[k] = my_row[((((j >> 2) ^ (tid & SW))) << 2) | (j & 3)];
+          }
+        }
         float asum = 0.f;
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-          z[j] = ((act >> j) & 1u) ? __expf(z[j] - amx) : 0.f;
-          asum += z[j];
+        for (int k = 0; k < K; ++k) {
+          ev[k] = fast_exp(ev[k] - amx);
+          asum += ev[k];
         }
         const float ainv = 1.f / asum;
+#pragma unroll
+        for (int k = 0; k < K; ++k) ev[k] *= ainv;
         const size_t ot = (size_t)t * a.B + b;
-        int32_t* act_out = a.active + ot * K;
-        float* w_out = a.wsel + ot * K;
-        int32_t* ad_out = a.adaptive + ot * (KA > 0 ? KA : 1);
-        int pos = 0, apos = 0;
+        if (valid) {
+          int32_t* act_out = a.active + ot * K;
+          float* w_out = a.wsel + ot * K;
+          if constexpr (K % 2 == 0) {       // 8-byte aligned rows
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-          const uint32_t bit = (act >> j) & 1u;
-          const float w = z[j] * ainv;
-          if (valid && bit) { act_out[pos] = j; w_out[pos] = w; }
-          pos += bit;
-          if (KA > 0) {
-            const uint32_t abit = (amask >> j) & 1u;
-            if (valid && abit) ad_out[apos] = j;
-            apos += abit;
+            for (int k = 0; k < K; k += 2) {
+              *reinterpret_cast<int2*>(act_out + k) = make_int2(idx[k], idx[k + 1]);
+              *reinterpret_cast<float2*>(w_out + k) = make_float2(ev[k], ev[k + 1]);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) { act_out[k] = idx[k]; w_out[k] = ev[k]; }
           }
-          cnt_p[j >> 2] += bit << (8 * (j & 3));
-          float* mp = s_mass + (g * E + j) * BM + r_loc;
-          *mp = first ? w : *mp + w;
-        }
-        first = false;
-      }
-      if (first) {                      // no task for this thread (T < TPR)
+          if constexpr (KA > 0) {
+            int32_t* ad_out = a.adaptive + ot * KA;
+            uint32_t m = amask;
 #pragma unroll
-        for (int j = 0; j < E; ++j) s_mass[(g * E + j) * BM + r_loc] = 0.f;
+            for (int k = 0; k < KA; ++k) { ad_out[k] = __ffs(m) - 1; m &= m - 1; }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) s_mass[(g * BM + r_loc) * (E + 1) + idx[k]] += ev[k];
       }
       // the accumulator is consumed: the MMA may start the tile after next in it
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      // bit planes -> four u8 counts per word (expert 4w + i in byte i): x * 0x204081 spreads the
+      // four bits of a nibble to bit 0 of four bytes without carries
 #pragma unroll
-      for (int j = 0; j < E / 4; ++j) s_cnt[(g * (E / 4) + j) * BM + r_loc] = valid ? cnt_p[j] : 0u;
+      for (int w = 0; w < E / 4; ++w) {
+        uint32_t packed = 0u;
+#pragma unroll
+        for (int p = 0; p < kNPlanes; ++p) packed |= ((((cnt[p] >> (4 * w)) & 15u) * 0x204081u) & 0x01010101u) << p;
+        s_cnt[(g * BM + r_loc) * (E / 4 + 1) + w] = valid ? packed : 0u;
+      }
       s_un[g * BM + r_loc] = valid ? un : 0u;
       if (!valid) {
 #pragma unroll
-        for (int j = 0; j < E; ++j) s_mass[(g * E + j) * BM + r_loc] = 0.f;
-        if (DM && g == 0) {
+        for (int j = 0; j < E; ++j) s_mass[(g * BM + r_loc) * (E + 1) + j] = 0.f;
+        if (DM) {
 #pragma unroll
-          for (int j = 0; j < E; ++j) s_dm[j * BM + r_loc] = 0.f;
+          for (int j = 0; j < E; ++j) s_dm[(g * BM + r_loc) * (E + 1) + j] = 0.f;
         }
       }
-      bar_named(5, kEpi<TPR>);
+      bar_named(5, kEpi);
       if (g == 0 && valid) {
         uint32_t u = 0;
 #pragma unroll
@@ -492,25 +675,25 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
         a.usize[b] = __popc(u);
       }
       // ---------------- per-chunk statistics in row order (deterministic)
-      const int tid = threadIdx.x - 128;
-      for (int pr = tid; pr < nsub * E; pr += kEpi<TPR>) {
+#ifdef SMES_FRONT_NO_STATS
+      if (nsub < 0)
+#endif
+      for (int pr = tid; pr < nsub * E; pr += kEpi) {
         const int sc = pr / E, e = pr - sc * E;
-        const int c = tile * nsub + sc;
+        const int c = (tile * rpc) / a.sub_rows + sc;
         if (c >= C) continue;
         int cu = 0, ca = 0;
         double m = 0.0, dmv = 0.0;
-        const int sh = 8 * (e & 3), wj = e >> 2;
         for (int r = sc * a.sub_rows; r < (sc + 1) * a.sub_rows; ++r) {
           uint32_t ur = 0;
 #pragma unroll
-          for (int h = 0; h < TPR; ++h) ur |= s_un[h * BM + r];
-          cu += (ur >> e) & 1u;
-#pragma unroll
           for (int h = 0; h < TPR; ++h) {
-            ca += (s_cnt[(h * (E / 4) + wj) * BM + r] >> sh) & 0xffu;
-            m += (double)s_mass[(h * E + e) * BM + r];
+            ur |= s_un[h * BM + r];
+            ca += (s_cnt[(h * BM + r) * (E / 4 + 1) + (e >> 2)] >> (8 * (e & 3))) & 0xffu;
+            m += (double)s_mass[(h * BM + r) * (E + 1) + e];
+            if (DM) dmv += (double)s_dm[(h * BM + r) * (E + 1) + e];
           }
-          if (DM) dmv += (double)s_dm[e * BM + r];
+          cu += (ur >> e) & 1u;
         }
         const size_t o = (size_t)c * E + e;
         a.chunk_union[o] = cu;
@@ -518,10 +701,16 @@ __global__ void __launch_bounds__(kThreads<TPR>, 1)
         a.chunk_mass[o] = m;
         if (DM) a.chunk_dmass[o] = dmv;
       }
-      bar_named(5, kEpi<TPR>);
+      if (tid == 0) *s_nf = 0;          // every read of the counter happened before the last barrier
+      bar_named(5, kEpi);
     }
     bad = __any_sync(0xffffffffu, bad);
     if (bad && lane == 0) atomicOr(a.flag, 1);
+    if (a.n_exact != nullptr) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(0xffffffffu, n_exact, o);
+      if (lane == 0 && n_exact) atomicAdd(a.n_exact, n_exact);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -556,23 +745,20 @@ static int front_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t r
   return SMES_OK;
 }
 
-#ifndef SMES_FRONT_TPR
-#define SMES_FRONT_TPR 2
-#endif
+static int32_t* g_front_counter = nullptr;   // diagnostic: rows routed through the fp64 recompute
 
 template <int E, int KS, int KA, bool DM>
 static int front_launch(const CUtensorMap& ta, const CUtensorMap& tb, const front::Args& a, int grid,
                         cudaStream_t st) {
-  constexpr int TPR = SMES_FRONT_TPR;
-  auto kern = front::route_front_kernel<E, KS, KA, DM, TPR>;
-  constexpr int bytes = front::Plan<E, TPR>::kBytes;
+  auto kern = front::route_front_kernel<E, KS, KA, DM>;
+  constexpr int bytes = front::Plan<E, DM>::kBytes;
   static bool attr = false;
   if (!attr) {
     cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (ea != cudaSuccess) return set_error(SMES_ERR_CUDA, "route_front smem attribute: %s", cudaGetErrorString(ea));
     attr = true;
   }
-  kern<<<grid, front::kThreads<TPR>, bytes, st>>>(ta, tb, a);
+  kern<<<grid, front::kThreads, bytes, st>>>(ta, tb, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "route_front launch: %s", cudaGetErrorString(e));
   return SMES_OK;
@@ -591,6 +777,8 @@ static int front_dispatch(const CUtensorMap& ta, const CUtensorMap& tb, const fr
 using namespace smes;
 
 extern "C" {
+
+void smes_route_front_count_exact(int32_t* dev_counter) { g_front_counter = dev_counter; }
 
 int smes_route_front_supported(int T, int E, int d, int k_shared, int k_adaptive) {
   const bool e_ok = E == 16 || E == 32;
@@ -616,13 +804,18 @@ int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r,
   if ((rc = front_map(&ta, h, (uint64_t)d, (uint64_t)B, (uint64_t)ldh, 128))) return rc;
   const int nc = (T * E) % 64 == 0 ? 64 : (T * E) % 32 == 0 ? 32 : 16;      // W_r chunk rows (see kernel)
   if ((rc = front_map(&tb, w_r, (uint64_t)d, (uint64_t)(T * E), (uint64_t)d, (uint32_t)nc))) return rc;
-  front::Args a{b_r, task_weights, T, B, d, sub_rows, shared, adaptive, active, wsel, umask, usize,
-                chunk_union, chunk_active, chunk_mass, chunk_dmass, flag, z_out};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int tiles = (B + 127) / 128;
+  // rows per CTA: a multiple of the statistics chunk, <= 128, small enough that the grid covers
+  // every SM (c2: 112 rows x 147 CTAs instead of 128 x 128)
+  int rpc = (B + sms - 1) / sms;
+  rpc = (rpc + sub_rows - 1) / sub_rows * sub_rows;
+  if (rpc > 128) rpc = 128;
+  const int tiles = (B + rpc - 1) / rpc;
   const int grid = tiles < sms ? tiles : sms;
+  front::Args a{b_r, task_weights, T, B, d, sub_rows, rpc, shared, adaptive, active, wsel, umask, usize,
+                chunk_union, chunk_active, chunk_mass, chunk_dmass, flag, z_out, g_front_counter};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool dm = chunk_dmass != nullptr;
   if (E == 16) return front_dispatch<16>(ta, tb, a, grid, k_shared, dm, st);

@@ -42,7 +42,15 @@ struct GemmArgs {
   int bits_ld;
   float* db_out;              // ragged-K: per-group column sums of P via Q's ones column (G, I), or null
   int a_period;               // ragged-K: P rows are read modulo this period (a shared P for every group), or 0
+  int x3;                     // ragged-M fp32 mode: K of one bf16 plane (A, W = three planes hi|mid|lo), or 0
 };
+
+// fp32-accurate products from bf16 planes: x = x0 + x1 + x2 with x_i = bf16(x - x_0 - .. - x_{i-1})
+// (8 significant bits each, 24 in all).  The six leading cross terms a_i b_j (i + j <= 2) are summed
+// as one GEMM over a virtual K of 6 planes; the dropped terms are below 2^-24 relative.  Virtual
+// plane s reads A plane (kX3A >> 4s) & 15 and W plane (kX3B >> 4s) & 15.
+constexpr uint32_t kX3A = 0x210100u;   // a0 a0 a1 a0 a1 a2
+constexpr uint32_t kX3B = 0x012010u;   // b0 b1 b0 b2 b1 b0
 
 // Shared-memory plan.  ragged-M tiles are epilogue(store)-paced at the c2 shapes, so every
 // epilogue warp double-buffers its 4 KB TMA-store staging chunk (ncu r1: the single-buffer
@@ -189,9 +197,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* b = sB + stage * S::kB;
           const int k0 = (kb0 + kb) * BK;
           if (MODE == MODE_RAGGED_M) {
-            tma_load_2d(a, &tmA, &full[stage], k0, r0);                       // box {64 k, 128 rows}
+            int ka = k0, kw = k0;
+            if (args.x3) {           // virtual plane -> (A plane, W plane)
+              const int sp = k0 / args.x3, kin = k0 - sp * args.x3;
+              ka = (int)((kX3A >> (4 * sp)) & 15u) * args.x3 + kin;
+              kw = (int)((kX3B >> (4 * sp)) & 15u) * args.x3 + kin;
+            }
+            tma_load_2d(a, &tmA, &full[stage], ka, r0);                       // box {64 k, 128 rows}
             if (!B_MN) {
-              tma_load_3d(b, &tmB, &full[stage], k0, c0, g);                  // box {64 k, BN n, 1}
+              tma_load_3d(b, &tmB, &full[stage], kw, c0, g);                  // box {64 k, BN n, 1}
             } else {
 #pragma unroll
               for (int j = 0; j < BN / 64; ++j)                               // box {64 n, 64 k, 1}
@@ -501,12 +515,45 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
                        str, box)))
       return rc;
   }
-  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, nullptr, 0};
+  GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, nullptr, 0, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (narrow) return launch<32, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
   // K-major B box is {64, 256} for N >= 256: requires BN == 256
   if (N >= 256) return launch_m<256>(b_mn, out_fp32, ta, tb, tc, args, st);
   return launch_m<128>(b_mn, out_fp32, ta, tb, tc, args, st);
+}
+
+int smes_gemm_ragged_m_x3(const void* A3, long lda, long rows_cap, const void* W3, int G, int N, int K,
+                          const int* seg, const float* bias, int act, float* C, long ldc, long m_limit, void* stream) {
+  if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
+  if (N <= 0 || K <= 0 || rows_cap <= 0) return set_error(SMES_ERR_SHAPE, "empty GEMM N=%d K=%d", N, K);
+  if (K % BK) return set_error(SMES_ERR_SHAPE, "fp32 (bf16x3) GEMM needs K %% 64 == 0 (K=%d)", K);
+  if ((lda * 2) % 16 || (ldc * 4) % 16 || lda < 3L * K)
+    return set_error(SMES_ERR_SHAPE, "fp32 GEMM: A stride %ld must hold 3 planes of K=%d, 16-byte aligned", lda, K);
+  const bool narrow = N <= 32;
+  CUtensorMap ta, tb, tc;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)3 * K, (uint64_t)rows_cap}, str[1] = {(uint64_t)lda * 2};
+    uint32_t box[2] = {64, 128};
+    if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, A3, dims, str, box))) return rc;
+  }
+  {  // W3 (G, N, 3K): planes along K
+    uint64_t dims[3] = {(uint64_t)3 * K, (uint64_t)N, (uint64_t)G};
+    uint64_t str[2] = {(uint64_t)3 * K * 2, (uint64_t)N * 3 * K * 2};
+    uint32_t box[3] = {64, (uint32_t)(narrow ? 32 : N >= 256 ? 256 : 128), 1};
+    if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, W3, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)N, (uint64_t)m_limit}, str[1] = {(uint64_t)ldc * 4};
+    uint32_t box[2] = {32, 32};
+    if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, C, dims, str, box))) return rc;
+  }
+  GemmArgs args{seg, G, N, 6 * K, 0, bias, act, nullptr, nullptr, 0, nullptr, 0, K};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (narrow) return launch<32, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
+  if (N >= 256) return launch<256, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
+  return launch<128, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
 }
 
 int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G,
@@ -534,7 +581,7 @@ int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void
     uint32_t box[3] = {32, 32, 1};
     if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, str, box))) return rc;
   }
-  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out, a_period};
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out, a_period, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (J <= 16) return launch<16, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
   // BN = 256 halves the tile count; with a single i-tile (I <= 128: the folded-head wgrad) keep

@@ -183,12 +183,15 @@ class _Pad:
     """Kernel granularity of the layer: input and hidden widths to multiples of 32, the output width
     to 128 / 256 / 512 / 1024 (combine tiling), T * E to a multiple of 8."""
 
-    def __init__(self, model: "MoeModel | None" = None, T: int = 0, E: int = 0, dims=None):
+    def __init__(self, model: "MoeModel | None" = None, T: int = 0, E: int = 0, dims=None, fp32: bool = False):
         if model is not None:
             T, E, dims = model.num_tasks, model.num_experts, [model.d_in] + [p.d_out for p in model.pools]
         self.T, self.E = T, E
         self.dims = list(dims)
-        self.dims_p = [_round(x, 32) for x in self.dims[:-1]] + [_pad_out(self.dims[-1])]
+        if fp32:   # bf16x3 GEMMs: contraction widths in whole 64-column k-blocks
+            self.dims_p = [_round(x, 64) for x in self.dims[:-1]] + [_round(self.dims[-1], 32)]
+        else:
+            self.dims_p = [_round(x, 32) for x in self.dims[:-1]] + [_pad_out(self.dims[-1])]
         E_p = self.E
         while (self.T * E_p) % 8:
             E_p += 1
@@ -269,6 +272,7 @@ class ForwardResult:
     _step: int = -1
     _enc: dict | None = None
     _pad: object = None
+    precision: str = "bf16"
 
     def mean_union(self) -> float:
         return float(self.routing.usize.double().mean())
@@ -310,11 +314,58 @@ def _encode(x: torch.Tensor, model: MoeModel, eng) -> dict:
     return dict(xb=xb, Fp=Fp, F=F, mid=mid, bits=bits, w1=w1, w2=w2, dh=dh, dhp=dhp)
 
 
-def _get_engine(model: MoeModel, B: int, dense: bool = False):
-    pad = _Pad(model)
-    key = (B, bool(dense), tuple(pad.dims_p), pad.E_p, tuple(p.nonlinearity for p in model.pools))
+def _encode_f32(x: torch.Tensor, model: MoeModel, eng) -> dict:
+    """encoder1 -> act -> encoder2 in fp32 (bf16x3 GEMMs, model.py:188-199)."""
+    from .fp32 import split_planes
+    B, F = x.shape
+    dev = x.device
+    Fp = _round(F, 64)
+    dh = model.encoder1.d_out
+    dhp = _round(dh, 64)
+    d = model.d_in
+    xf = torch.zeros(B, Fp, device=dev)
+    xf[:, :F] = x
+    x3 = split_planes(xf)
+    w1 = torch.zeros(dhp, Fp, device=dev)
+    w1[:dh, :F] = model.encoder1.weight
+    b1 = torch.zeros(dhp, device=dev)
+    b1[:dh] = model.encoder1.bias
+    mid = torch.zeros(B, dhp, device=dev)
+    relu = model.encoder_nonlinearity == "relu"
+    seg = torch.tensor([0, _round(B, 128)], dtype=torch.int32, device=dev)
+    w13 = split_planes(w1)          # operands stay referenced until the GEMMs are queued (stream-ordered reuse)
+    call("smes_gemm_ragged_m_x3", ptr(x3), 3 * Fp, B, ptr(w13), 1, dhp, Fp, ptr(seg), ptr(b1),
+         1 if relu else 0, ptr(mid), dhp, B, _stream())
+    w2 = torch.zeros(d, dhp, device=dev)
+    w2[:, :dh] = model.encoder2.weight
+    dp = eng.d
+    out = torch.zeros(B, dp, device=dev)
+    b2 = torch.zeros(dp, device=dev)
+    b2[:d] = model.encoder2.bias
+    w2p = torch.zeros(dp, dhp, device=dev)
+    w2p[:d] = w2
+    mid3, w23 = split_planes(mid), split_planes(w2p)
+    call("smes_gemm_ragged_m_x3", ptr(mid3), 3 * dhp, B, ptr(w23), 1, dp, dhp, ptr(seg),
+         ptr(b2), 0, ptr(out), dp, B, _stream())
+    eng.h.copy_(out)
+    return dict(mid=mid, dh=dh, dhp=dhp, F=F, Fp=Fp, planes=(x3, w13, mid3, w23))
+
+
+def _get_engine(model: MoeModel, B: int, dense: bool = False, precision: str = "bf16"):
+    if precision not in ("bf16", "fp32"):
+        raise ConfigError(f"unknown precision '{precision}', expected 'bf16' or 'fp32'")
+    fp32 = precision == "fp32"
+    pad = _Pad(model, fp32=fp32)
+    key = (B, bool(dense), tuple(pad.dims_p), pad.E_p, tuple(p.nonlinearity for p in model.pools), precision)
     eng = model._engines.get(key)
-    if eng is None:
+    if eng is None and fp32:
+        from .fp32 import SMESForwardF32
+        eng = SMESForwardF32(model.smes_params(pad), B, model.budget.k_shared, model.budget.k_adaptive,
+                             device=model.routers.weight.device, lb_experts=model.num_experts,
+                             dense_probs_in_stats=dense)
+        eng.step_id = 0
+        model._engines[key] = eng
+    elif eng is None:
         eng = _engine.SMESEngine(model.smes_params(pad), B, model.budget.k_shared, model.budget.k_adaptive,
                                  dense_probs_in_stats=dense, device=model.routers.weight.device,
                                  lb_experts=model.num_experts)
@@ -327,9 +378,14 @@ def _get_engine(model: MoeModel, B: int, dense: bool = False):
 
 
 def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, frozen: ForwardResult | None = None,
-                   keep_cache: bool = True, dense_probs_in_stats: bool = False) -> ForwardResult:
+                   keep_cache: bool = True, dense_probs_in_stats: bool = False,
+                   precision: str = "bf16") -> ForwardResult:
     """Sparse pipeline (model.py:267-324) on the B200 kernels.  With ``frozen`` the previous
-    selections are reused and only the mixture weights are recomputed (model.py:284-300)."""
+    selections are reused and only the mixture weights are recomputed (model.py:284-300).
+
+    ``precision``: "bf16" (default; bf16 operands, fp32 accumulation, the training path) or
+    "fp32" (fp32 operands and activations, GEMMs as bf16x3 tensor-core products -- the north
+    star's fp32 1e-5 contract; forward only, see fp32.py)."""
     x = torch.as_tensor(batch)
     if not x.is_cuda:
         x = x.cuda()
@@ -344,7 +400,9 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
         raise ShapeError(f"hidden has shape {tuple(x.shape)}, model expects (B, {model.d_in})")
     if frozen is not None and (frozen.mode != "sparse" or frozen.plan is None):
         raise StateError("frozen forward result must come from the sparse pipeline")
-    eng, pad = _get_engine(model, B, dense_probs_in_stats)
+    eng, pad = _get_engine(model, B, dense_probs_in_stats, precision)
+    if precision == "fp32":
+        return _forward_sparse_f32(x, model, counter, frozen, keep_cache, eng, pad)
     eng.keep_logits = True
     T, E, Ep = model.num_tasks, model.num_experts, pad.E_p
     d, d_out = model.d_in, model.d_out
@@ -388,4 +446,53 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
         rows = plan.physical_rows
         res.packed_in = eng.X[rows, :d].float()
         res.packed_out = eng.outs[-1][rows, :d_out].float()
+    return res
+
+
+def _forward_sparse_f32(x, model: MoeModel, counter, frozen, keep_cache, eng, pad) -> ForwardResult:
+    """fp32 forward (fp32.SMESForwardF32): same result type; ``backward`` of it is refused."""
+    B = x.shape[0]
+    T, E, Ep = model.num_tasks, model.num_experts, pad.E_p
+    d, d_out = model.d_in, model.d_out
+    enc = None
+    if model.encoder1 is not None:
+        enc = _encode_f32(x.float(), model, eng)
+    else:
+        eng.h[:, :d].copy_(x)
+    if frozen is not None:
+        eng.shared.copy_(frozen.routing.shared_i32)
+        eng.adaptive.copy_(frozen.routing.adaptive_i32)
+    eng.forward(with_loss=False, frozen=frozen is not None)
+    eng.check_finite()
+    eng.step_id += 1
+    c = lambda t: t.clone()
+    ce = lambda t: t[:, :E].contiguous()
+    z = c(eng.z)
+    routing = BatchRouting(z, T, B, E, model.budget, c(eng.tw), c(eng.shared), c(eng.adaptive), c(eng.active),
+                           c(eng.wsel), c(eng.umask), c(eng.usize), ce(eng.chunk_union), ce(eng.chunk_active),
+                           ce(eng.chunk_mass), ce(eng.chunk_dmass), eng.rpw, z_strides=(Ep, T * Ep))
+    raw = eng.stats_raw.view(3, Ep)[:, :E].reshape(-1).contiguous()
+    plan = ExecutionPlan(E, B, eng.umax, eng.rows_cap, eng.seg_pad[:E + 1].clone(), eng.seg_log[:E + 1].clone(),
+                         eng.loads[:E].clone(), c(eng.totals), c(eng.row_of), c(eng.gather_inst),
+                         c(eng.gather_exp), raw, routing.usize)
+    n_act = eng.n_act()
+    dims = pad.dims
+    flops = n_act * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+    if counter is not None:
+        counter.add(flops)
+    reps = eng.reps[..., :d_out].clone()
+    # mode "sparse" keeps the reference's result contract; _engine is withheld so backward refuses it
+    res = ForwardResult("sparse", eng.preds.clone(), eng.logits.clone(), reps, routing, plan, flops,
+                        _engine=None, _step=eng.step_id, _enc=enc, _pad=pad)
+    res.precision = "fp32"
+    if keep_cache:
+        res.inputs = x
+        res.hidden = eng.h[:, :d].clone()
+        res.router_logits = z.view(B, T, Ep)[:, :, :E].permute(1, 0, 2)
+        if enc is not None:
+            res.encoder_hidden = enc["mid"][:B, :enc["dh"]].clone()
+        rows = plan.physical_rows
+        res.packed_in = eng.X3[rows, :d].float() + eng.X3[rows, pad.dims_p[0]:pad.dims_p[0] + d].float() + \
+            eng.X3[rows, 2 * pad.dims_p[0]:2 * pad.dims_p[0] + d].float()
+        res.packed_out = eng.outs[-1][rows, :d_out].clone()
     return res

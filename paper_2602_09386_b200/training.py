@@ -75,6 +75,9 @@ class BackwardResult:
 def backward(result: ForwardResult, model: MoeModel, labels, dense_probs_in_stats: bool = False) -> BackwardResult:
     """Exact gradients of the total loss (training.py:119-226); selections fixed."""
     eng = result._engine
+    if getattr(result, "precision", "bf16") == "fp32":
+        raise StateError("backward of an fp32-precision forward is not provided (the fp32 mode is forward + "
+                         "loss, BASELINE c1); run forward_sparse with precision='bf16' for training")
     if eng is None or result.mode != "sparse":
         raise StateError("backward needs a sparse forward result produced by this package")
     if getattr(eng, "step_id", None) != result._step:

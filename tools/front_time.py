@@ -30,8 +30,15 @@ for path in paths:
     st = torch.cuda.current_stream().cuda_stream
     zo = torch.zeros(B, T * E, device="cuda") if os.environ.get("ZOUT") else None
     f = lambda: call("smes_route_front", ptr(h), d, ptr(w), ptr(bias), ptr(tw), T, B, E, d, ks, ka, 4 * rpw,
-                              ptr(sh), ptr(ad), ptr(ac), ptr(ws), ptr(um), ptr(us), ptr(cu), ptr(ca), ptr(cm), ptr(cd),
+                              ptr(sh), ptr(ad), ptr(ac), ptr(ws), ptr(um), ptr(us), ptr(cu), ptr(ca), ptr(cm), ptr(cd) if os.environ.get("DM") else None,
                               ptr(fl), ptr(zo), st)
+    cnt = torch.zeros(1, dtype=torch.int32, device="cuda")
+    if hasattr(_lib.load(), "smes_route_front_count_exact"):
+        call("smes_route_front_count_exact", ptr(cnt))
+        f()
+        torch.cuda.synchronize()
+        print("rows through the fp64 recompute:", int(cnt.item()), "of", B)
+        call("smes_route_front_count_exact", None)
     for _ in range(5):
         f()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
