@@ -67,7 +67,10 @@ struct Plan {
   static constexpr int EQ = E / TPR;
   // the router GEMM is issued in N chunks of (up to) 64 columns, each committed on its own
   // barrier, so Stage I of the first tasks runs while the MMAs of the later tasks stream W_r
-  static constexpr int kWStages = DM ? 3 : 4;     // (DM: the dense-mass array needs the space)
+#ifndef SMES_FRONT_WSTAGES
+#define SMES_FRONT_WSTAGES 6
+#endif
+  static constexpr int kWStages = DM ? 3 : SMES_FRONT_WSTAGES;   // (DM: the dense-mass array needs the space)
   static constexpr int kH = BM * BK * 2;          // 16 KB per k-block of h (d <= 256: 4 blocks)
   static constexpr int kW = 64 * BK * 2;          // 8 KB per (chunk, k-block) of W_r
   static constexpr int kOffW = 4 * kH;

@@ -47,10 +47,10 @@ struct GemmArgs {
 
 // fp32-accurate products from bf16 planes: x = x0 + x1 + x2 with x_i = bf16(x - x_0 - .. - x_{i-1})
 // (8 significant bits each, 24 in all).  The six leading cross terms a_i b_j (i + j <= 2) are summed
-// as one GEMM over a virtual K of 6 planes; the dropped terms are below 2^-24 relative.  Virtual
-// plane s reads A plane (kX3A >> 4s) & 15 and W plane (kX3B >> 4s) & 15.
-constexpr uint32_t kX3A = 0x210100u;   // a0 a0 a1 a0 a1 a2
-constexpr uint32_t kX3B = 0x012010u;   // b0 b1 b0 b2 b1 b0
+// as one GEMM over a virtual K of 6 planes, smallest terms first; the dropped terms are below
+// 2^-24 relative.  Virtual plane s reads A plane (kX3A >> 4s) & 15 and W plane (kX3B >> 4s) & 15.
+constexpr uint32_t kX3A = 0x001012u;   // a2 a1 a0 a1 a0 a0
+constexpr uint32_t kX3B = 0x010210u;   // b0 b1 b2 b0 b1 b0
 
 // Shared-memory plan.  ragged-M tiles are epilogue(store)-paced at the c2 shapes, so every
 // epilogue warp double-buffers its 4 KB TMA-store staging chunk (ncu r1: the single-buffer

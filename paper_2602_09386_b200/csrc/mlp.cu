@@ -210,6 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kb = 0; kb < DK; ++kb, ++wi) {
             const int s = slot_of(wi, S::kWS);
             TW(1, mbar_wait(&wempty[s], par_of(wi, S::kWS) ^ 1));
+#ifdef SMES_FWD_EXP_NO_W1      // timing experiment only (wrong results): W1 streamed for the first tile only
+            if (tile != (int)blockIdx.x) { mbar_arrive(&wfull[s]); continue; }
+#endif
             mbar_expect_tx(&wfull[s], 16384);
             tma_load_3d(sW + s * 16384, &tmW1, &wfull[s], kb * 64, c * CH, e);  // box {64 k, 128 n, 1}
           }

@@ -28,6 +28,7 @@ eng = SMESEngine(bench._make_params(c, dev), B, c["ks"], c["ka"], device=dev)
 h, y = bench._host_inputs(c, B, 0)
 eng.set_inputs(h.to(dev), y.to(dev))
 eng.serial = True
+eng.keep_logits = False        # as the bench's training step (no router-logit output)
 for i in range(steps):
     if i == steps - 1:
         _lib.trace = []
