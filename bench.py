@@ -455,6 +455,16 @@ def run_dp(args, c, world, rank, local, dev):
     roofline, breakdown = _roofline(kern, work, peaks, peak_src)
     expert_flops = sum(work[t][0] for t in kern if t in work and (t.startswith("fc") or t.startswith("mlp_"))
                        and not t.endswith("bias"))
+    # the expert MLP as the reference computes it (no head folding): fc1 + fc2 forward, dgrad of
+    # both, wgrad of both = 3 x 2 x N_act x (d d_ff + d_ff d_out) FLOP per step
+    nominal = 3 * 2.0 * n_act * (c["d"] * c["d_ff"] + c["d_ff"] * c["d_out"])
+    expert_gemm = {"nominal_flop_per_step": nominal,
+                   "nominal_tflops": round(nominal / (ms * 1e-3) / 1e12, 1),
+                   "nominal_frac_of_bf16_peak": round(nominal / (ms * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
+                   "note": "nominal = the unfolded expert MLP (what the reference computes) over the whole step "
+                           "time; the kernels run the folded algebra (DESIGN.md section 2), fewer FLOPs"}
+    comparator = gemm_comparator(eng, peaks) if rank == 0 else None
+    api = e2e_api(c, dev, args.steps) if (rank == 0 and world == 1 and args.config == "c2") else None
     step_tflops = (expert_flops + sum(work[t][0] for t in ("router_fwd", "router_dgrad", "router_wgrad"))) / (
         ms * 1e-3) / 1e12
     cpu = _cpu_sample(args.config, 2) if (rank == 0 and not args.no_cpu) else None
@@ -469,9 +479,97 @@ def run_dp(args, c, world, rank, local, dev):
                        "graph": ("fwd+bwd in one CUDA graph" if world == 1 else "fwd+bwd captured as 2 CUDA graphs around the LB-stats all-reduce")},
             "e2e": e2e, "gpu_launches": per_step_launches * args.steps,
             "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks, "parity": parity,
-            "step_tflops": round(step_tflops, 1), "kernels": breakdown,
+            "step_tflops": round(step_tflops, 1), "expert_gemm": expert_gemm, "gemm_comparator": comparator,
+            "e2e_api": api, "kernels": breakdown,
             "kernels_note": "per-kernel CUDA-event times from an eager step with the backward side stream "
                             "serialised onto the timing stream (so each kernel is timed alone, like ncu)"}
+
+
+def gemm_comparator(eng, peaks, reps=10):
+    """Library anchor for the grouped GEMM: the fc1 forward of this batch (padded expert segments,
+    X (rows, d) x W1_e^T) through our tcgen05 kernel (smes_gemm_ragged_m, no epilogue) and through
+    torch._grouped_mm (PyTorch's CUTLASS grouped GEMM) on the same operands, CUDA events, L2 warm."""
+    import torch
+    from paper_2602_09386_b200._lib import call, ptr
+    E, d, dff = eng.E, eng.d, eng.dims[1]
+    rows = int(eng.seg_pad[E].item())
+    a = eng.X[:rows, :d].contiguous()
+    w = eng.w_bf[0]                                   # (E, d_ff, d)
+    out = torch.empty(rows, dff, dtype=torch.bfloat16, device=a.device)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def ours():
+        call("smes_gemm_ragged_m", ptr(a), d, rows, ptr(w), E, dff, d, 0, ptr(eng.seg_pad), None, 0, None, None, 0,
+             ptr(out), dff, 0, rows, st)
+
+    def timeit(fn):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+    flop = 2.0 * rows * d * dff
+    res = {"shape": f"fc1 forward, {rows} padded rows in {E} expert groups, K={d}, N={dff}, bf16 -> bf16",
+           "ours_ms": None, "torch_grouped_mm_ms": None}
+    t = timeit(ours)
+    res["ours_ms"] = round(t, 4)
+    res["ours_tflops"] = round(flop / (t * 1e-3) / 1e12, 1)
+    try:
+        offs = eng.seg_pad[1:E + 1].contiguous()
+        wt = w.transpose(1, 2)                       # (E, d, d_ff) view: the layout grouped_mm wants
+        ref = torch._grouped_mm(a, wt, offs=offs)
+        t2 = timeit(lambda: torch._grouped_mm(a, wt, offs=offs))
+        ours()
+        torch.cuda.synchronize()
+        res["torch_grouped_mm_ms"] = round(t2, 4)
+        res["torch_grouped_mm_tflops"] = round(flop / (t2 * 1e-3) / 1e12, 1)
+        res["max_rel_diff"] = float((out.float() - ref.float()).abs().max() / ref.float().abs().max())
+    except Exception as err:           # library path unavailable on this build: say so
+        res["torch_grouped_mm_error"] = str(err)[:200]
+    res["bf16_peak_tflops"] = peaks["bf16_tflops"]
+    return res
+
+
+def e2e_api(c, dev, steps):
+    """The drop-in API end to end (the calls a user of the reference makes): forward_sparse on a
+    host batch (H2D inside), backward with host labels (H2D), the loss read back (D2H) and the
+    gradient blocks returned as fresh device tensors -- per step, CUDA events, L2 flushed between
+    steps outside the brackets."""
+    import torch
+    import paper_2602_09386_b200 as smes
+    params = _make_params(c, dev)
+    T, E = c["T"], c["E"]
+    pools = [smes.ExpertPool([smes.Affine(l.weight[e], l.bias[e]) for e in range(E)], l.act) for l in params.layers]
+    routers = smes.RouterBank([smes.Affine(params.router_w[t], params.router_b[t]) for t in range(T)])
+    heads = [smes.Affine(params.head_w[t:t + 1], params.head_b[t:t + 1]) for t in range(T)]
+    model = smes.MoeModel(None, None, pools, routers, heads, torch.ones(T), c["beta"],
+                          smes.RoutingBudget(c["ks"], c["ka"]))
+    h_host, y_host = _host_inputs(c, c["B"], 0)
+    x_host = h_host.float().pin_memory()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        res = smes.forward_sparse(x_host, model)
+        smes.backward(res, model, y_host)
+    n = max(5, min(steps, 20))
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+    for e0, e1 in ev:
+        flush.zero_()
+        e0.record()
+        res = smes.forward_sparse(x_host, model)
+        bw = smes.backward(res, model, y_host)
+        e1.record()
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / n
+    return {"value": c["B"] / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "loss": bw.total,
+            "h2d_bytes_per_step": x_host.numel() * 4 + y_host.numel() * 4, "d2h_bytes_per_step": 24,
+            "api": "paper_2602_09386_b200.forward_sparse(host batch) + backward(result, model, host labels): "
+                   "reference-shaped results (routing, plan, task reps, named gradient blocks), host syncs "
+                   "for the reference's validation and float losses"}
 
 
 def run_ep(args, c, world, rank, local, dev):

@@ -68,6 +68,17 @@ int smes_route_front(const void* h, long ldh, const void* w_r, const float* b_r,
                      int32_t* adaptive, int32_t* active, float* wsel, uint32_t* umask, int32_t* usize,
                      int32_t* chunk_union, int32_t* chunk_active, double* chunk_mass, double* chunk_dmass,
                      int32_t* flag, float* z_out, void* stream);
+/* ---- K1 (row, task) router: smes_route_batch in training / scoring mode (not frozen, no dense
+ *      probabilities in or out, chunk_dmass NULL) for E in {16, 32, 64}, T <= min(32, E), budget 4+2
+ *      or 2+1 -- smes_route_batch dispatches here itself.  Thread per (row, task); Stage I in fp32
+ *      with a certified bound and an fp64 recompute of undecidable rows (selections as fp64). */
+int smes_route_rt_supported(int T, int E, int k_shared, int k_adaptive);
+int smes_route_rt(const float* z, long stride_t, long stride_b, const double* task_weights, int T, int B, int E,
+                  int k_shared, int k_adaptive, int rows_per_warp, int32_t* shared, int32_t* adaptive,
+                  int32_t* active, float* wsel, uint32_t* umask, int32_t* usize, int32_t* chunk_union,
+                  int32_t* chunk_active, double* chunk_mass, double* chunk_dmass, int32_t* flag, void* stream);
+void smes_route_count_exact(int32_t* dev_counter);
+
 /* diagnostic: count (atomically, into *dev_counter) the rows later smes_route_front launches send
  * through the fp64 recompute; NULL turns counting off. */
 void smes_route_front_count_exact(int32_t* dev_counter);

@@ -8,6 +8,7 @@ There is no CPU fallback: every entry point raises CudaError without a GPU.
 from .errors import (ConfigError, CudaError, DataFormatError, NumericsError, PoolError, PoolTimeout, ShapeError,
                      StateError, TaskMoeError)
 from .engine import ExpertLayer, SMESEngine, SMESParams
+from .engine import workspace_bytes as engine_workspace_bytes
 from .routing import (BatchRouting, RouterBank, RoutingBudget, RoutingDecision, compute_global_scores, dense_routing,
                       naive_route_batch, naive_sparse_route, progressive_route, renormalized_weights, route_batch,
                       stack_decisions)
@@ -27,7 +28,7 @@ __version__ = "0.1.0"
 __all__ = [
     "TaskMoeError", "ShapeError", "ConfigError", "NumericsError", "StateError", "CudaError", "DataFormatError",
     "PoolError", "PoolTimeout",
-    "SMESEngine", "SMESParams", "ExpertLayer",
+    "SMESEngine", "SMESParams", "ExpertLayer", "engine_workspace_bytes",
     "RoutingBudget", "RouterBank", "BatchRouting", "RoutingDecision", "route_batch", "progressive_route",
     "naive_route_batch", "naive_sparse_route", "renormalized_weights", "compute_global_scores", "dense_routing",
     "stack_decisions",

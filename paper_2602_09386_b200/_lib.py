@@ -29,6 +29,9 @@ SIGNATURES = {
     "smes_route_batch": [P, L, L, P, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, P],
     "smes_route_front_supported": [I, I, I, I, I],
     "smes_route_front_count_exact": [P],
+    "smes_route_count_exact": [P],
+    "smes_route_rt_supported": [I, I, I, I],
+    "smes_route_rt": [P, L, L, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P],
     "smes_peer_allreduce_f64": [I, I, I, P, P, P, P, P, P, P, P],
     "smes_combine_bwd_reps": [I, I, I, I, I, I, P, P, P, P, P, P, L, I, P, P, F, P, P, L, P],
     "smes_route_front": [P, L, P, P, P, I, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P, P],
@@ -82,7 +85,7 @@ _RESTYPE = {"smes_last_error": C.c_char_p}
 # entry points that return a value rather than a status
 _VALUE_FNS = {"smes_abi_version", "smes_route_front_supported", "smes_fold_work_floats", "smes_fold_gemm_path", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_combine_fwd_f32_grid", "smes_last_error",
-              "smes_route_front_count_exact"}
+              "smes_route_front_count_exact", "smes_route_count_exact", "smes_route_rt_supported"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
 def _fold_gemm_path(E, T, d_out, d_in):      # csrc/fold.cu gemm_path()
@@ -109,7 +112,7 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_all
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
                     "smes_ep_copy_rows_put": 1, "smes_gemm_ragged_m_x3": 1, "smes_split_bf16x3": 1,
-                    "smes_combine_fwd_f32": 1}
+                    "smes_combine_fwd_f32": 1, "smes_route_rt": 1}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 trace = None    # optional list: every successful call appends (tag, kernels launched) -- ncu launch tags

@@ -106,6 +106,38 @@ __device__ __forceinline__ float fast_exp(float x) {
   return y;
 }
 
+// e^x - 1 for x <= 0 with relative accuracy (route_rt.cu): degree-8 Taylor for |x| < 1/4, else
+// fast_exp(x) - 1; kEpsY bounds the relative error with the argument rounding, with margin
+constexpr float kEpsY = 16.f * 0x1p-23f;
+__device__ __forceinline__ float expm1_neg(float x) {
+  float p = fmaf(x, 1.f / 40320.f, 1.f / 5040.f);
+  p = fmaf(x, p, 1.f / 720.f);
+  p = fmaf(x, p, 1.f / 120.f);
+  p = fmaf(x, p, 1.f / 24.f);
+  p = fmaf(x, p, 1.f / 6.f);
+  p = fmaf(x, p, 0.5f);
+  p = fmaf(x, p, 1.f);
+  p *= x;
+  const float e = fast_exp(x) - 1.f;
+  return x > -0.25f ? p : e;
+}
+template <int E> constexpr int kLog2E = E == 16 ? 4 : 5;
+__device__ __forceinline__ uint32_t okey(float f) {   // order-preserving key of a float of any sign
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+template <int E>
+__device__ __forceinline__ float tree_sum(const float (&z)[E]) {
+  float m[E / 2];
+#pragma unroll
+  for (int j = 0; j < E / 2; ++j) m[j] = z[j] + z[j + E / 2];
+#pragma unroll
+  for (int s = E / 4; s > 0; s >>= 1)
+#pragma unroll
+    for (int j = 0; j < s; ++j) m[j] = m[j] + m[j + s];
+  return m[0];
+}
+
 __device__ __forceinline__ void bar_named(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
@@ -329,10 +361,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t smask = 0;
       bool exact_needed = false;
       if constexpr (KS > 0 || DM) {
-        double pp[E];
-        float emax = 0.f;          // max over this thread's tasks of the relative exp error bound
+        // pooled_e = sum_t w_t / S_t + P_e with y_te = exp(z_te - max_t) - 1, S_t = E + sum_e y_te and
+        // P_e = sum_t (w_t / S_t) y_te: the first term is common to every expert, so the shared set
+        // is the top-K_s of P, which fp32 holds to ~1e-3 of the pooled scores' rounding error at
+        // reference init (|y| ~ 1e-3; route_rt.cu has the bound)
+        float pp[E];
+        float perr = 0.f;          // absolute error bound of this thread's partial P (every expert)
 #pragma unroll
-        for (int j = 0; j < E; ++j) pp[j] = 0.0;
+        for (int j = 0; j < E; ++j) pp[j] = 0.f;
         bool first = true;
         for (int t = g; t < T; t += TPR) {
           wait_task(t);
@@ -345,27 +381,24 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int j = 0; j < E; j += 4) zo[j / 4] = make_float4(z[j], z[j + 1], z[j + 2], z[j + 3]);
           }
-          double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
-          for (int j = 0; j < E; ++j) {
-            z[j] = fast_exp(z[j] - mx);
-            s4[j & 3] += (double)z[j];
-          }
-          const double ssum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          for (int j = 0; j < E; ++j) z[j] = expm1_neg(z[j] - mx);
+          const float ysum = tree_sum<E>(z);
+          const float ssum = (float)E + ysum;
           bad |= !(isfinite(mx) & isfinite(mn) & isfinite(ssum));
-          const double qd = stw[t] / ssum;
+          const float q = (float)stw[t] / ssum;
 #pragma unroll
-          for (int j = 0; j < E; ++j) pp[j] = fma(qd, (double)z[j], pp[j]);
-          // relative error of every w_t p_tj: the exp of the numerator and of the sum, each within
-          // (2 + 1.173 |x|) ulp (fast_exp, |x| <= mx - mn) + the argument rounding; flushed results
-          // (< 2^-126) are covered by the absolute slack of the certification
-          emax = fmaxf(emax, (3.f + 2.f * (mx - mn)) * 0x1p-23f);
+          for (int j = 0; j < E; ++j) pp[j] = fmaf(q, z[j], pp[j]);
+          // |error| of q y_tj <= q |y|max (eps_y + rho_t + 3u), rho_t the relative error of S_t;
+          // the fp32 accumulation over this thread's tasks and the partner's adds (T/TPR + 1) u
+          const float rho = (kLog2E<E> * 0x1p-24f + kEpsY) * (-ysum) / ssum + 0x1p-24f;
+          perr += q * (-expm1_neg(mn - mx)) * (kEpsY + rho + (3 + T / TPR + 2) * 0x1p-24f);
           if constexpr (DM) {
-            const float qf = (float)(1.0 / ssum);
+            const float qf = 1.f / ssum;
 #pragma unroll
             for (int j = 0; j < E; ++j) {
               float* dp = s_dm + (g * BM + r_loc) * (E + 1) + j;
-              *dp = first ? qf * z[j] : fmaf(qf, z[j], *dp);
+              *dp = first ? qf * (1.f + z[j]) : fmaf(qf, 1.f + z[j], *dp);
             }
           }
           first = false;
@@ -380,23 +413,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           // exchange: thread g owns experts [g EQ, (g + 1) EQ); pooled = own partial + partner's
           // (fp64 addition commutes, so both threads would get the same value)
           const int oh = 1 - g;
+          float* x_pf = reinterpret_cast<float*>(x_pp);                     // [TPR][EQ][BM] fp32 partials
 #pragma unroll
-          for (int j = 0; j < EQ; ++j) x_pp[(oh * EQ + j) * BM + r_loc] = g == 0 ? pp[EQ + j] : pp[j];
-          x_pe[g * BM + r_loc] = emax;
+          for (int j = 0; j < EQ; ++j) x_pf[(oh * EQ + j) * BM + r_loc] = g == 0 ? pp[EQ + j] : pp[j];
+          x_pe[g * BM + r_loc] = perr;
           bar_named(quad_bar, 32 * TPR);
-          double pq[EQ];
+          float pq[EQ];
 #pragma unroll
-          for (int j = 0; j < EQ; ++j) pq[j] = (g == 0 ? pp[j] : pp[EQ + j]) + x_pp[(g * EQ + j) * BM + r_loc];
-          // pooled error <= 1.5 x 2 x max eps x pooled (both exp errors, 1.5x margin); the fp64
-          // arithmetic and the fp32 -> fp64 products add < 2^-48 relative
-          const double erel = 3.0 * (double)fmaxf(x_pe[r_loc], x_pe[BM + r_loc]) + 0x1p-48;
+          for (int j = 0; j < EQ; ++j) pq[j] = (g == 0 ? pp[j] : pp[EQ + j]) + x_pf[(g * EQ + j) * BM + r_loc];
+          // x 1.5 margin, + an absolute floor for flushed exps
+          const double e_abs = 1.5 * ((double)x_pe[r_loc] + (double)x_pe[BM + r_loc]) + 0x1p-100;
           const int j0 = g * EQ;
           // shared set: top-K_s of pooled, (score desc, index asc).  pooled >= 0, so the fp64 bit
           // patterns order like unsigned integers.  Each thread sorts its half, the lists merge
           // through shared memory.
           unsigned long long pk[EQ];
 #pragma unroll
-          for (int j = 0; j < EQ; ++j) pk[j] = (unsigned long long)__double_as_longlong(pq[j]);
+          for (int j = 0; j < EQ; ++j) pk[j] = okey(pq[j]);     // P may be negative: order-preserving key
           uint32_t taken = 0;
 #pragma unroll
           for (int k = 0; k < KS; ++k) {
@@ -439,10 +472,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           double lo = INFINITY, hi = -INFINITY;
 #pragma unroll
           for (int j = 0; j < EQ; ++j) {
-            const double err = pq[j] * erel + 0x1p-100;
             const bool sel = (smask >> (j0 + j)) & 1u;
-            lo = sel ? fmin(lo, pq[j] - err) : lo;
-            hi = sel ? hi : fmax(hi, pq[j] + err);
+            lo = sel ? fmin(lo, (double)pq[j] - e_abs) : lo;
+            hi = sel ? hi : fmax(hi, (double)pq[j] + e_abs);
           }
           s_lohi[(g * 2) * BM + r_loc] = lo;
           s_lohi[(g * 2 + 1) * BM + r_loc] = hi;

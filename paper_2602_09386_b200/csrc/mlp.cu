@@ -112,18 +112,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // S accumulators (128 TMEM columns each): three, so the S-MMA of chunk c+2 does not wait for the
 // epilogue to drain chunk c (a double buffer left a ~380-cycle bubble per chunk, tools/mma_probe)
 constexpr int kSB = 3;
+// H staging tiles in shared memory (the P-MMA operand and the TMA-store source).  Two tiles (the
+// epilogue writing chunk c + 1 while the P-MMA / store of chunk c read theirs, W1 ring 6 -> 4)
+// measured 123 us against 120 us for one at c2, so one it is (SMES_FWD_HB=2 builds the other)
+#ifndef SMES_FWD_HB
+#define SMES_FWD_HB 1
+#endif
+constexpr int kHBMax = SMES_FWD_HB;
 template <int DK>     // d / 64
 struct FwdSmem {
   // X k-block ring (16 KB slots, spare slots prefetch the next tile), W1 k-block ring (16 KB:
   // 128 n x 64 k, 1.5 chunks deep at d = 256), G chunk ring (4 KB: 2 x {64 f, 16 t})
   static constexpr int kXS = SMES_FWD_XS > 0 ? SMES_FWD_XS : DK <= 2 ? DK + 2 : DK <= 4 ? DK + 1 : DK;
-  static constexpr int kWS = SMES_FWD_WS > 0 ? SMES_FWD_WS : DK <= 4 ? 6 : 3;
+  static constexpr int kHB = DK <= 4 ? kHBMax : 1;       // d = 512: the X ring takes the space
+  static constexpr int kWS = SMES_FWD_WS > 0 ? SMES_FWD_WS : DK <= 4 ? (kHB == 2 ? 4 : 6) : 3;
   static constexpr int kGS = 2;
   static constexpr int kOffX = 0;
   static constexpr int kOffW = kOffX + kXS * 16384;
   static constexpr int kOffG = kOffW + kWS * 16384;
-  static constexpr int kOffH = kOffG + kGS * 4096;      // 2 x 16 KB atoms (128 rows x 64 cols)
-  static constexpr int kOffBias = kOffH + 32768;        // 64 fp32 per epilogue warp
+  static constexpr int kOffH = kOffG + kGS * 4096;      // kHB x (2 x 16 KB atoms: 128 rows x 64 cols)
+  static constexpr int kOffBias = kOffH + kHB * 32768;  // 64 fp32 per epilogue warp
   static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
   static constexpr int kOffSeg = kOffBar + 512;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 1024;
@@ -151,9 +159,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* gempty = gfull + S::kGS;        // [kGS]
   uint64_t* sfull = gempty + S::kGS;        // [kSB]
   uint64_t* sempty = sfull + kSB;           // [kSB]
-  uint64_t* hfull = sempty + kSB;           // [1]
-  uint64_t* hempty = hfull + 1;             // [1]
-  uint64_t* pfull = hempty + 1;             // [2]
+  uint64_t* hfull = sempty + kSB;           // [S::kHB]
+  uint64_t* hempty = hfull + S::kHB;           // [S::kHB]
+  uint64_t* pfull = hempty + S::kHB;           // [2]
   uint64_t* pempty = pfull + 2;             // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty + 2);
   int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
@@ -172,8 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&pfull[i], 1); mbar_init(&pempty[i], kEpiWarps / 2);
     }
-    mbar_init(hfull, kEpiWarps);
-    mbar_init(hempty, 1);
+    for (int i = 0; i < S::kHB; ++i) { mbar_init(&hfull[i], kEpiWarps); mbar_init(&hempty[i], 1); }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -276,20 +283,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int pb = it & 1;
         const uint32_t tP = tmem_base + kSB * CH + pb * 16;
         for (int c = 0; c < NC; ++c, ++gi, ++hi) {
-          TW(6, mbar_wait(hfull, (uint32_t)(hi & 1)));
+          const int hb = hi % S::kHB;
+          TW(6, mbar_wait(&hfull[hb], (uint32_t)((hi / S::kHB) & 1)));
           const int gs = slot_of(gi, S::kGS);
           TW(7, mbar_wait(&gfull[gs], par_of(gi, S::kGS)));
           EV(6, gi);
           if (c == 0) TW(8, mbar_wait(&pempty[pb], (uint32_t)(((it >> 1) & 1) ^ 1)));
           tc_fence_after();
-          const uint32_t h_addr = smem_u32(sH), g_addr = smem_u32(sG + gs * 4096);
+          const uint32_t h_addr = smem_u32(sH + hb * 32768), g_addr = smem_u32(sG + gs * 4096);
 #pragma unroll
           for (int k = 0; k < CH / 16; ++k) {
             const int atom = k >> 2, kk = k & 3;
             tc_mma_f16(tP, umma_desc_sw128(h_addr + atom * 16384 + kk * 32, 16, 1024),
                        umma_desc_sw128(g_addr + atom * 2048 + kk * 32, 16, 1024), idP, (c | k) != 0);
           }
-          tc_commit(hempty);
+          tc_commit(&hempty[hb]);
           tc_commit(&gempty[gs]);
           EV(7, gi);
         }
@@ -401,12 +409,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (warp == 4 && lane == 0) EV(8, si);
         if (warp == 4 && lane == 0) EV(9, si);
         if (warp == 4 && lane == 0) EV(9, si);
-        // H smem tile is free once the previous chunk's P-MMA has read it (and our TMA store too)
-        if (warp == 4) TW(10, mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1))); else mbar_wait(hempty, (uint32_t)((hi & 1) ^ 1));
+        // H smem tile hb is free once the P-MMA of the chunk that last used it has read it (and our
+        // TMA store of it too; with two tiles the store of the other one may still be reading)
+        const int hb = hi % S::kHB;
+        uint8_t* sHb = sH + hb * 32768;
+        if (warp == 4) TW(10, mbar_wait(&hempty[hb], (uint32_t)(((hi / S::kHB) & 1) ^ 1)));
+        else mbar_wait(&hempty[hb], (uint32_t)(((hi / S::kHB) & 1) ^ 1));
         if (warp == 4 && lane == 0) EV(4, si);
-        if (lane == 0) TW(12, bulk_wait_read<0>());
+        if (lane == 0) {
+          if (S::kHB == 2) TW(12, bulk_wait_read<1>()); else TW(12, bulk_wait_read<0>());
+        }
         __syncwarp();
-        uint8_t* hrow = sH + par * 16384 + (32 * q + lane) * 128;
+        uint8_t* hrow = sHb + par * 16384 + (32 * q + lane) * 128;
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc) {
           const uint4 pk = make_uint4(pack_bf16(f[8 * cc], f[8 * cc + 1]), pack_bf16(f[8 * cc + 2], f[8 * cc + 3]),
@@ -419,10 +433,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           if (a.store_h) {
-            tma_store_2d(&tmH, sH + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
-            bulk_commit();
+            tma_store_2d(&tmH, sHb + par * 16384 + 32 * q * 128, n0, r0 + 32 * q);
           }
-          mbar_arrive(hfull);
+          bulk_commit();                  // (an empty group without a store: the wait counts stay aligned)
+          mbar_arrive(&hfull[hb]);
           if (warp == 4) EV(5, si);
         }
         ++hi;

@@ -637,6 +637,13 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
                      "budget k=%d exceeds expert count %d: stage-II would have only %d candidates for %d adaptive picks",
                      k_shared + k_adaptive, E, E - k_shared, k_adaptive);
   if (k_shared + k_adaptive > 32) return set_error(SMES_ERR_CONFIG, "budget k=%d exceeds 32", k_shared + k_adaptive);
+  // training / scoring mode without dense-mass statistics: the (row, task) router (route_rt.cu)
+  if (!frozen && probs_in == nullptr && probs_out == nullptr && chunk_dmass == nullptr &&
+      smes_route_rt_supported(T, E, k_shared, k_adaptive) && (stride_t % 4) == 0 && (stride_b % 4) == 0 &&
+      (reinterpret_cast<uintptr_t>(z) % 16) == 0)
+    return smes_route_rt(z, stride_t, stride_b, task_weights, T, B, E, k_shared, k_adaptive, rows_per_warp, shared,
+                         adaptive, active, wsel, umask, usize, chunk_union, chunk_active, chunk_mass, chunk_dmass,
+                         flag, stream);
   RouteArgs a{z, stride_t, stride_b, probs_in, task_weights, T, B, E, k_shared, k_adaptive, rows_per_warp,
               shared, adaptive, active, wsel, umask, usize, chunk_union, chunk_active, chunk_mass, chunk_dmass,
               probs_out, flag, frozen};

@@ -18,6 +18,7 @@ Kernel sequence (reference functions in taskmoe/ they replace):
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import torch
@@ -92,15 +93,57 @@ def _round(x, m):
     return (x + m - 1) // m * m
 
 
+def row_buffer_specs(T: int, E: int, B: int, k_shared: int, k_adaptive: int, dims, acts) -> list:
+    """The engine's buffers sized by the packed-row capacity -- the per-batch part of its memory that
+    a ``DeviceWorkspace`` block can back (workspace.py:42-57 sizes blocks by packed rows):
+    (attribute, shape, dtype) in carve order.  ``dims`` = [d, widths of the pools], ``acts`` their
+    nonlinearities."""
+    umax = min(E, k_shared + T * k_adaptive)
+    R = _round(B * umax + E * 127, 128)
+    bf, i32, f32 = torch.bfloat16, torch.int32, torch.float32
+    ld_in = [w + 64 for w in dims[:-1]]
+    specs = [("gather_inst", (R,), i32), ("gather_exp", (R,), i32), ("X", (R, ld_in[0]), bf)]
+    for i, w in enumerate(dims[1:]):
+        last = i == len(dims) - 2
+        specs.append((f"outs.{i}", (R, w if last else ld_in[i + 1]), bf))
+    for i, (w, act) in enumerate(zip(dims[1:], acts)):
+        if act == "relu":
+            specs.append((f"bits.{i}", (w // 32, R), i32))
+    specs += [("P", (R, _round(T, 8)), f32), ("Cm", (R, _round(T, 16)), bf)]
+    for i, w in enumerate(dims[1:]):
+        specs.append((f"d_outs.{i}", (R, w), bf))
+    specs += [("dX", (R, dims[0]), bf), ("colsum_part", (R // 128, max(max(dims), T * E)), f32)]
+    return specs
+
+
+def workspace_bytes(params: "SMESParams", batch_size: int, k_shared: int, k_adaptive: int,
+                    align: int = 256) -> int:
+    """Bytes of one engine's packed-row buffers (carved 256-byte aligned): the block a
+    ``WorkspacePool`` grants per concurrent stream (``DeviceWorkspace.carve``)."""
+    dims = [params.d_in] + [l.d_out for l in params.layers]
+    specs = row_buffer_specs(params.num_tasks, params.num_experts, int(batch_size), int(k_shared),
+                             int(k_adaptive), dims, [l.act for l in params.layers])
+    off = 0
+    for _, shape, dt in specs:
+        off = -(-off // align) * align + math.prod(shape) * torch.empty((), dtype=dt).element_size()
+    return off
+
+
 class SMESEngine:
     """Fixed-shape executor of the SMES hot path on one GPU."""
 
     def __init__(self, params: SMESParams, batch_size: int, k_shared: int, k_adaptive: int,
                  dense_probs_in_stats: bool = False, keep_reps: bool = True,
                  device: torch.device | str | None = None, csum_from_gemm: bool = False,
-                 fuse_mlp: bool = True, fuse_wgrad: bool = False, lb_experts: int | None = None):
+                 fuse_mlp: bool = True, fuse_wgrad: bool = False, lb_experts: int | None = None,
+                 workspace=None):
+        """``workspace``: optional ``(DeviceWorkspace, PageBlock)``.  The packed-row buffers (the
+        per-batch memory, ``row_buffer_specs``) are then carved from that block of the pool's HBM
+        arena instead of being allocated, so concurrent serving streams share one provisioned pool
+        (taskmoe/workspace.py:42-262); give the block back with ``pool.release(block, stream=s)``."""
         _require_cuda()
         self.dev = torch.device(device or "cuda")
+        self._ws = workspace
         p = params
         self.p = p
         T, E, d = p.num_tasks, p.num_experts, p.d_in
@@ -175,6 +218,17 @@ class SMESEngine:
         z = lambda *s, dt=f32: torch.zeros(*s, dtype=dt, device=dev)
         EW = (E + 31) // 32
         R = self.rows_cap
+        # packed-row buffers: carved from the workspace block when one is bound, else allocated
+        specs = row_buffer_specs(T, E, B, self.ks, self.ka, self.dims, [l.act for l in self.p.layers])
+        if self._ws is not None:
+            ws, block = self._ws
+            bufs = ws.carve(block, [(shape, dt) for _, shape, dt in specs])
+            for b_ in bufs:
+                b_.zero_()
+        else:
+            bufs = [torch.zeros(shape, dtype=dt, device=dev) for _, shape, dt in specs]
+        rows = dict(zip([n for n, _, _ in specs], bufs))
+        self.workspace_nbytes = sum(b_.numel() * b_.element_size() for b_ in bufs)
         self.z = z(B, T * E)
         self.shared = z(B, self.ks, dt=i32)
         self.adaptive = z(T, B, self.ka, dt=i32)
@@ -195,28 +249,27 @@ class SMESEngine:
         self.ticket = z(1, dt=i32)
         self.flag = z(1, dt=i32)
         self.row_of = z(B, self.umax, dt=i32)
-        self.gather_inst = z(R, dt=i32)
-        self.gather_exp = z(R, dt=i32)
+        self.gather_inst = rows["gather_inst"]
+        self.gather_exp = rows["gather_exp"]
         # every wgrad Q operand (each layer's input and h) carries 64 extra columns whose first one
         # is 1.0: the wgrad GEMM's extra N=64 tile then yields the bias gradient (sum over rows)
         self.ld_in = [w + 64 for w in self.dims[:-1]]           # leading dims of layer inputs
-        self.X = z(R, self.ld_in[0], dt=bf)
+        self.X = rows["X"]
         self.X[:, d] = 1.0
         self.outs = []
         for i, w in enumerate(self.dims[1:]):
             last = i == len(self.dims) - 2
-            o = z(R, w if last else self.ld_in[i + 1], dt=bf)
+            o = rows[f"outs.{i}"]
             if not last:
                 o[:, w] = 1.0
             self.outs.append(o)
         self.ld_out = [o.shape[1] for o in self.outs]
-        self.bits = [z(w // 32, R, dt=torch.int32) if l.act == "relu" else None
-                     for i, (w, l) in enumerate(zip(self.dims[1:], self.p.layers))]
+        self.bits = [rows.get(f"bits.{i}") for i in range(len(self.p.layers))]
         self.reps = z(T, B, self.d_out, dt=bf)     # required by the backward (head grads)
         self.ldp = _round(T, 8)
-        self.P = z(R, self.ldp)                     # head projections P = O head_W^T of every packed row
+        self.P = rows["P"]                          # head projections P = O head_W^T of every packed row
         self.ldc = _round(T, 16)
-        self.Cm = z(R, self.ldc, dt=bf)             # C[row, t] = w[row, t] * dlogit_t (training step)
+        self.Cm = rows["Cm"]                        # C[row, t] = w[row, t] * dlogit_t (training step)
         self.hw_part = z(2 * E, T, self.d_out)      # dW_head split-K partials (expert halves)
         # bias grads folded into the training combine: last (identity) pool via per-(expert, task)
         # sums of C, router via column sums of dz (per-warp smem accumulators, fixed-order reduce)
@@ -262,8 +315,8 @@ class SMESEngine:
         self.rw_part = z(self.rw_splits, T * E, d)
         self.rb_part = z(self.rw_splits, T * E)
         # backward
-        self.d_outs = [z(R, w, dt=bf) for w in self.dims[1:]]   # gradient w.r.t. each layer's output
-        self.dX = z(R, d, dt=bf)
+        self.d_outs = [rows[f"d_outs.{i}"] for i in range(len(self.dims) - 1)]   # grad w.r.t. each pool's output
+        self.dX = rows["dX"]
         self.dz = z(self.B_pad, T * E, dt=bf)
         # all parameter gradients live in ONE flat fp32 buffer, laid out in the order the backward
         # finishes them so data parallelism can reduce contiguous buckets as they complete:
@@ -287,7 +340,7 @@ class SMESEngine:
         self.grad_buckets = {"pools_first": slice(0, last), "last_pool_heads": slice(last, router),
                              "router": slice(router, off)}
         self.on_grads = None     # optional callback(bucket name, cuda stream) once a bucket is final
-        self.colsum_part = z(R // 128, max(max(self.dims), T * E))
+        self.colsum_part = rows["colsum_part"]
         self.dh_router = z(B, d)
         self.d_hidden = z(B, d)
         self.part_dw = z(self.grid, T, self.d_out)
@@ -456,7 +509,9 @@ class SMESEngine:
         _tagged("route", "smes_route_batch", ptr(self.z), E, T * E, ptr(probs_in), ptr(self.tw), T, B, E, self.ks, self.ka,
              self.rpw, ptr(self.shared), ptr(self.adaptive), ptr(self.active), ptr(self.wsel), ptr(self.umask),
              ptr(self.usize), ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
-             ptr(self.chunk_dmass), ptr(probs_out), ptr(self.flag), int(frozen), s)
+             # the dense mass only for the dense LB reading and the API (full_probs / dense stats)
+             ptr(self.chunk_dmass) if (self.keep_logits or self.dense or frozen) else None, ptr(probs_out),
+             ptr(self.flag), int(frozen), s)
 
     def experts_forward(self, s, fold: bool = False, store_hidden: bool = True, refold: bool = True,
                         heads: bool = True):

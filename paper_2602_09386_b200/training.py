@@ -108,24 +108,30 @@ def backward(result: ForwardResult, model: MoeModel, labels, dense_probs_in_stat
 
 def _logical_gradients(eng, model) -> dict:
     """Gradient blocks with the reference's names and shapes (model.py:94-111), sliced out of the
-    engine's (possibly shim-padded) stacked gradients; fresh tensors."""
+    engine's (possibly shim-padded) stacked gradients.  One copy of the engine's flat gradient
+    buffer backs every block, so the result owns its memory (a later step cannot rewrite it) for a
+    single device copy instead of one per block."""
     T, E, Ep = model.num_tasks, model.num_experts, eng.E
     pools = model.pools
     dims = [model.d_in] + [p.d_out for p in pools]
+    flat = eng.grad_flat.clone()
+    own = lambda v: flat[v.data_ptr() // 4 - eng.grad_flat.data_ptr() // 4:][:v.numel()].view(v.shape)
     g = {}
     for li, (gw, gb) in enumerate(eng.g_layers):
         di, do = dims[li], dims[li + 1]
+        gw, gb = own(gw), own(gb)
         pre = "expert_" if len(pools) == 1 else f"expert{li}_"
         for e in range(E):
-            g[f"{pre}{e}.weight"] = gw[e, :do, :di].clone()
-            g[f"{pre}{e}.bias"] = gb[e, :do].clone()
-    rw = eng.g_router_w.view(T, Ep, eng.d)
-    rb = eng.g_router_b.view(T, Ep)
+            g[f"{pre}{e}.weight"] = gw[e, :do, :di]
+            g[f"{pre}{e}.bias"] = gb[e, :do]
+    rw = own(eng.g_router_w).view(T, Ep, eng.d)
+    rb = own(eng.g_router_b).view(T, Ep)
+    hw, hb = own(eng.g_head_w), own(eng.g_head_b)
     for t in range(T):
-        g[f"router_{t}.weight"] = rw[t, :E, :dims[0]].clone()
-        g[f"router_{t}.bias"] = rb[t, :E].clone()
-        g[f"head_{t}.weight"] = eng.g_head_w[t:t + 1, :dims[-1]].clone()
-        g[f"head_{t}.bias"] = eng.g_head_b[t:t + 1].clone()
+        g[f"router_{t}.weight"] = rw[t, :E, :dims[0]]
+        g[f"router_{t}.bias"] = rb[t, :E]
+        g[f"head_{t}.weight"] = hw[t:t + 1, :dims[-1]]
+        g[f"head_{t}.bias"] = hb[t:t + 1]
     return g
 
 

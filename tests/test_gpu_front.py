@@ -60,8 +60,8 @@ CASES = {
     "c1_shape": (4, 16, 128, 2, 1, 1024, "init"),
     "t16_e16": (16, 16, 128, 4, 2, 777, "x1000"),
     "small_B": (8, 32, 256, 4, 2, 5, "x1000"),
-    # logits ~1e-7: nearly every row's Stage-I gaps sit below the fp32 bound, so the fp64
-    # recompute takes most rows, in several rounds of its shared-memory staging
+    # logits ~1e-7: Stage-I gaps ~1e-12, decided by the deviation form (y = e^x - 1 keeps its
+    # relative accuracy); exact ties ("ties") take the fp64 recompute
     "c2_all_rows_exact": (8, 32, 256, 4, 2, 8192, "tiny"),
     "t16_e16_all_rows_exact": (16, 16, 128, 4, 2, 2000, "tiny"),
 }
@@ -91,8 +91,8 @@ def test_route_front_vs_oracle_and_route_kernel(name):
     finally:
         _lib.call("smes_route_front_count_exact", None)
     n_exact = int(cnt.item())
-    if kind == "tiny":
-        assert n_exact > B // 2, n_exact          # the fp64 recompute really ran, over several rounds
+    if kind == "ties":
+        assert n_exact > 0, n_exact               # exact pooled ties go through the fp64 recompute
     if kind == "x1000":
         assert n_exact <= B // 20, n_exact
     assert g["flag"][0] == 0

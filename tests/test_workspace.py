@@ -208,3 +208,63 @@ def test_device_arena_and_stream_ordered_release():
     nxt = pool.allocate(16, timeout=10.0)           # waits for the deferred release, no host sync
     assert nxt.start == 0 and pool.releases == 1
     assert float(x.float().sum()) == 64000.0        # the stream's write landed before the reuse
+
+
+def test_engine_workspace_bytes_matches_specs():
+    """The per-engine block size is the aligned sum of the packed-row buffers (no GPU needed)."""
+    from paper_2602_09386_b200.engine import ExpertLayer, SMESParams, row_buffer_specs, workspace_bytes
+    T, E, d, dff = 4, 16, 128, 256
+    z = lambda *s: torch.zeros(*s)
+    p = SMESParams(router_w=z(T, E, d), router_b=z(T, E),
+                   layers=[ExpertLayer(z(E, dff, d), z(E, dff), "relu"), ExpertLayer(z(E, d, dff), z(E, d), "identity")],
+                   head_w=z(T, d), head_b=z(T))
+    specs = row_buffer_specs(T, E, 1000, 2, 1, [d, dff, d], ["relu", "identity"])
+    names = [n for n, _, _ in specs]
+    assert names[:3] == ["gather_inst", "gather_exp", "X"] and "bits.0" in names and "bits.1" not in names
+    R = (1000 * 6 + 16 * 127 + 127) // 128 * 128
+    assert dict((n, s) for n, s, _ in specs)["X"] == (R, d + 64)
+    nb = workspace_bytes(p, 1000, 2, 1)
+    raw = sum(torch.Size(s).numel() * torch.empty((), dtype=dt).element_size() for _, s, dt in specs)
+    assert raw <= nb < raw + 256 * len(specs)
+
+
+@pytest.mark.gpu
+def test_engines_share_a_device_workspace_pool():
+    """Two scoring engines (BASELINE c4 streams) draw their packed-row buffers from blocks of ONE
+    provisioned HBM arena, run concurrently on two CUDA streams, and give identical predictions to
+    engines with private buffers (workspace.py:42-262 semantics: one grant per in-flight batch)."""
+    from paper_2602_09386_b200 import SMESEngine
+    from paper_2602_09386_b200.engine import workspace_bytes
+    from tests.helpers import make_case, to_engine_params
+    B, T, E, d = 1024, 8, 32, 128
+    p, h, y, lam, beta = make_case(21, B, T, E, d, d, 4, 2, d_ff=256)
+    params = to_engine_params(p, lam, beta)
+    page = 1 << 16
+    per = -(-workspace_bytes(params, B, 4, 2) // page)
+    pool = WorkspacePool(page_count=2 * per, page_size=page)
+    ws = DeviceWorkspace(pool)
+    blocks = [pool.allocate(per) for _ in range(2)]
+    hs = [torch.tensor(h, device="cuda"), torch.tensor(h[::-1].copy(), device="cuda")]
+    shared = [SMESEngine(params, B, 4, 2, workspace=(ws, blk)) for blk in blocks]
+    assert shared[0].X.data_ptr() >= ws.arena.data_ptr()
+    assert shared[1].X.data_ptr() >= ws.arena.data_ptr() + blocks[1].start * page
+    assert shared[0].workspace_nbytes <= per * page
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for eng, x, s in zip(shared, hs, streams):
+        with torch.cuda.stream(s):
+            eng.set_inputs(x)
+            eng.score()
+    for blk, s in zip(blocks, streams):
+        pool.release(blk, stream=s)          # pages come back once each stream's work is done
+    torch.cuda.synchronize()
+    for eng, x in zip(shared, hs):
+        ref = SMESEngine(params, B, 4, 2)
+        ref.set_inputs(x)
+        ref.score()
+        torch.cuda.synchronize()
+        assert torch.equal(eng.preds, ref.preds)
+    again = pool.allocate(2 * per, timeout=10.0)
+    assert again.start == 0
+    with pytest.raises(PoolError, match="cannot hold"):
+        SMESEngine(params, B, 4, 2, workspace=(ws, WorkspacePool(1, page).allocate(1)))
