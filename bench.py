@@ -681,6 +681,7 @@ def run_infer(args, c, world, rank, local, dev):
     reps = max(1000, args.steps)
     for Bb in c["batches"]:
         eng = SMESEngine(params, Bb, c["ks"], c["ka"], device=dev)
+        eng.keep_logits = False        # scoring does not return the router logits / dense statistics
         h_host, y_host = _host_inputs(c, Bb, rank)
         eng.set_inputs(h_host.to(dev), y_host.to(dev))
         st = torch.cuda.Stream(dev)

@@ -434,6 +434,18 @@ class SMESEngine:
         the task heads, so its output O and the task reps are not materialised."""
         s = self._stream()
         T, E, B, d = self.T, self.E, self.B, self.d
+        # the head fold (G_e = head_W W_last,e, c_e) depends on the weights only: it runs on the side
+        # stream under the router and the plan, joined before the expert kernels
+        self._fold_ev = None
+        if fold and refold and self.can_fold and not self.serial:
+            if not hasattr(self, "_side"):
+                self._side = torch.cuda.Stream(self.dev)
+            fork = torch.cuda.Event()
+            fork.record(torch.cuda.current_stream(self.dev))
+            self._side.wait_event(fork)
+            self._fold(self._side.cuda_stream)
+            self._fold_ev = torch.cuda.Event()
+            self._fold_ev.record(self._side)
         if self.use_front and not frozen:
             # router GEMM + progressive router in one kernel (routing.py:101-103 + :235-281)
             # keep_logits off (training steps): neither z nor the dense mass (read only by the dense
@@ -528,10 +540,11 @@ class SMESEngine:
         if fold:
             # P = H G_e^T + c_e with G_e = head_W W_last,e: the last pool and the heads in one N = T GEMM
             di = self.dims[L - 1]
-            if refold:   # training steps refold every step (the weights move between steps)
-                _tagged("fold_heads", "smes_fold_heads", self.E, self.T, self.ldg, self.d_out, di,
-                        ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold),
-                        ptr(self.fold_work), s)
+            if getattr(self, "_fold_ev", None) is not None:      # folded on the side stream (forward_a)
+                torch.cuda.current_stream(self.dev).wait_event(self._fold_ev)
+                self._fold_ev = None
+            elif refold:   # training steps refold every step (the weights move between steps)
+                self._fold(s)
             if self.fuse_mlp_fwd:
                 # fc1 (+ relu mask, H kept for the weight gradients) and P in one chained kernel
                 _tagged("mlp_fwd", "smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]),
@@ -548,6 +561,12 @@ class SMESEngine:
         # head projections of every packed row: P = O head_W^T (tcgen05 GEMM, N = T)
         _tagged("head_proj", "smes_gemm_ragged_m", ptr(self.outs[-1]), self.d_out, R, ptr(self.head_w_bf), 1, self.T,
                 self.d_out, 0, ptr(self.totals), None, 0, None, None, 0, ptr(self.P), self.ldp, 1, R, s)
+
+    def _fold(self, s):
+        di = self.dims[-2]
+        _tagged("fold_heads", "smes_fold_heads", self.E, self.T, self.ldg, self.d_out, di,
+                ptr(self.head_w), ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold),
+                ptr(self.fold_work), s)
 
     def stats_finalize(self, s, batch_times_tasks: float | None = None):
         bt = float(self.B * self.T) if batch_times_tasks is None else batch_times_tasks
