@@ -155,6 +155,7 @@ struct GroupLayout {
 
 template <int VPL, int MAXT>
 __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineArgs a) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.d_out / (32 * VPL);        // warps per instance
   const int G = CB_WARPS / S;                 // instances per CTA iteration
@@ -282,6 +283,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineAr
 template <int MAXT>
 __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const CombineArgs a, __nv_bfloat16* cmat, int ldc,
                                                                  float* part_csum, float* part_rb) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = a.T, K = a.K, E = a.E, EW = (E + 31) >> 5, TE = T * E, TK = T * K, umax = a.umax;
   const int ldp = a.ldp;
@@ -505,6 +507,7 @@ __global__ void __launch_bounds__(CB_THREADS) combine_train_kernel(const Combine
 // db[e][n] = sum_t csum[e][t] head_w[t][n]   (bias grad of an identity last pool: dO = C head_W)
 __global__ void bias_from_csum_kernel(int E, int T, int d_out, const float* __restrict__ csum,
                                       const float* __restrict__ head_w, float* __restrict__ out) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E * d_out) return;
   const int e = i / d_out, n = i - e * d_out;
@@ -515,6 +518,7 @@ __global__ void bias_from_csum_kernel(int E, int T, int d_out, const float* __re
 
 template <int VPL, int MAXT>
 __global__ void __launch_bounds__(CB_THREADS) combine_bwd_kernel(const CombineArgs a) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = a.d_out / (32 * VPL);
   const int G = CB_WARPS / S;
@@ -756,7 +760,7 @@ static int combine_launch(bool bwd, CombineArgs& a, int grid, void* stream) {
   if (vpl == V && mt == M) {                                                                             \
     auto kf = bwd ? combine_bwd_kernel<V, M> : combine_fwd_kernel<V, M>;                                 \
     if (smem > 48 * 1024) cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    kf<<<grid, CB_THREADS, smem, st>>>(a);                                                               \
+    smes_launch(kf, grid, CB_THREADS, smem, st, a);                                                               \
   } else
   CB_CASE(8, 4) CB_CASE(8, 8) CB_CASE(4, 4) CB_CASE(4, 8) CB_CASE(4, 16) CB_CASE(4, 32) {
     return set_error(SMES_ERR_SHAPE, "combine: unsupported T=%d d_out=%d", a.T, a.d_out);
@@ -820,7 +824,7 @@ int smes_combine_train(int T, int B, int E, int K, int umax, const uint32_t* uma
 #define CT_CASE(M)                                                                                      \
   if (mt == M) {                                                                                        \
     if (smem > 48 * 1024) cudaFuncSetAttribute(combine_train_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    combine_train_kernel<M><<<grid, CB_THREADS, smem, st>>>(a, cm, (int)ldc, part_csum, part_rb);      \
+    smes_launch(combine_train_kernel<M>, grid, CB_THREADS, smem, st, a, cm, (int)ldc, part_csum, part_rb);      \
   } else
   CT_CASE(4) CT_CASE(8) CT_CASE(16) CT_CASE(32) {}
 #undef CT_CASE
@@ -831,7 +835,7 @@ int smes_combine_train(int T, int B, int E, int K, int umax, const uint32_t* uma
 
 int smes_bias_from_csum(int E, int T, int d_out, const float* csum, const float* head_w, float* out, void* stream) {
   const int n = E * d_out;
-  bias_from_csum_kernel<<<(n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, T, d_out, csum, head_w,
+  smes_launch(bias_from_csum_kernel, (n + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream), E, T, d_out, csum, head_w,
                                                                                            out);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "bias_from_csum launch: %s", cudaGetErrorString(e));

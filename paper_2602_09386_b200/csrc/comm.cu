@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(512) peer_allreduce_f64_kernel(int n, int me, 
                                                                  int32_t* __restrict__ my_flags,
                                                                  int32_t* __restrict__ epoch_ctr,
                                                                  double* __restrict__ out) {
+  pdl_wait();
   __shared__ int32_t s_epoch;
   if (threadIdx.x == 0) s_epoch = *epoch_ctr + 1;
   __syncthreads();
@@ -67,7 +68,7 @@ int smes_peer_allreduce_f64(int n, int me, int count, const double* in, void* co
                             int32_t* epoch_ctr, double* out, void* stream) {
   if (n < 1 || n > 512 || me < 0 || me >= n) return set_error(SMES_ERR_SHAPE, "peer_allreduce: rank %d of %d", me, n);
   if (count < 0) return set_error(SMES_ERR_SHAPE, "peer_allreduce: count %d", count);
-  peer_allreduce_f64_kernel<<<1, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  smes_launch(peer_allreduce_f64_kernel, 1, 512, 0, reinterpret_cast<cudaStream_t>(stream), 
       n, me, count, in, reinterpret_cast<double* const*>(peer_recv_dev), peer_flags_dev, my_recv, my_flags,
       epoch_ctr, out);
   cudaError_t e = cudaGetLastError();

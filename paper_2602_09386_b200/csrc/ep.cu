@@ -17,6 +17,7 @@
 
 #include <cstring>
 
+#include "ptx.cuh"
 #include "smes_capi.h"
 
 namespace smes {
@@ -26,6 +27,7 @@ __global__ void __launch_bounds__(1024) ep_pack_index_kernel(int B, int EW, cons
                                                              int wpr, int32_t* __restrict__ idx,
                                                              int32_t* __restrict__ pos, int32_t* __restrict__ cnt,
                                                              uint32_t* __restrict__ mask_out) {
+  pdl_wait();
   __shared__ int warp_tot[32];
   __shared__ int base_s;
   const int r = blockIdx.x;
@@ -69,6 +71,7 @@ __global__ void __launch_bounds__(1024) ep_pack_index_kernel(int B, int EW, cons
 // h_out[r][i] = h[idx[r][i]] for i < cnt[r]  (16-byte vectors)
 __global__ void ep_pack_rows_kernel(int B, int d, const int32_t* __restrict__ idx, const int32_t* __restrict__ cnt,
                                     const __nv_bfloat16* __restrict__ h, long ldh, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
   const int r = blockIdx.y;
   const int vec = d / 8;
   const long n = (long)cnt[r] * vec;
@@ -87,6 +90,7 @@ __global__ void ep_pack_rows_kernel(int B, int d, const int32_t* __restrict__ id
 //   source (mode 1): cnt[r][e] = loads of owner r's e-th expert, packed at seg_pad[r*E_l + e]
 __global__ void ep_segments_kernel(int mode, int n, int El, const int32_t* __restrict__ cnt,
                                    const int32_t* __restrict__ seg_pad, long slot_rows, int32_t* __restrict__ tab) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n) return;
   int slot_off = 0;
@@ -110,6 +114,7 @@ __global__ void ep_segments_kernel(int mode, int n, int El, const int32_t* __res
 // dir 0: packed -> slots (gather), dir 1: slots -> packed (scatter); one block per segment
 __global__ void ep_copy_rows_kernel(int dir, const int32_t* __restrict__ tab, const uint8_t* __restrict__ src,
                                     long src_ld, uint8_t* __restrict__ dst, long dst_ld, int row_bytes) {
+  pdl_wait();
   const int32_t* t = tab + (size_t)blockIdx.x * 3;
   const long packed = t[0], slot = t[1];
   const int rows = t[2];
@@ -125,6 +130,7 @@ __global__ void ep_copy_rows_kernel(int dir, const int32_t* __restrict__ tab, co
 __global__ void ep_combine_dh_kernel(int B, int d, int n, long slot_rows, const int32_t* __restrict__ pos,
                                      const float* __restrict__ dh_recv, const float* __restrict__ dh_router,
                                      float* __restrict__ out) {
+  pdl_wait();
   const int b = blockIdx.x;
   for (int c = threadIdx.x * 4; c < d; c += blockDim.x * 4) {
     float4 acc = dh_router ? *reinterpret_cast<const float4*>(dh_router + (size_t)b * d + c) : make_float4(0, 0, 0, 0);
@@ -145,6 +151,7 @@ __global__ void ep_capacity_guard_kernel(int E, long cap, const int32_t* __restr
                                          int32_t* __restrict__ seg_pad, int32_t* __restrict__ loads,
                                          uint32_t* __restrict__ umask, long n_mask_words, int32_t* __restrict__ usize,
                                          long n_inst, int32_t* __restrict__ flag) {
+  pdl_wait();
   const bool over = (long)totals[1] > cap;
   if (!over) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) *flag = 1;
@@ -172,6 +179,7 @@ struct PutArgs {
 };
 
 __global__ void ep_put_kernel(PutArgs a) {
+  pdl_wait();
   const int r = blockIdx.y;
   const long bytes = a.rows_used ? (long)a.rows_used[r] * a.row_bytes : a.slot_bytes;
   const uint8_t* src = a.send + (long)r * a.slot_bytes;
@@ -181,6 +189,7 @@ __global__ void ep_put_kernel(PutArgs a) {
 }
 
 __global__ void ep_signal_kernel(int n, int self, int32_t* const* peer_flags, int32_t epoch) {
+  pdl_wait();
   // publish: every put of this rank is visible system-wide before the flag
   __threadfence_system();
   const int r = threadIdx.x;
@@ -191,6 +200,7 @@ __global__ void ep_signal_kernel(int n, int self, int32_t* const* peer_flags, in
 }
 
 __global__ void ep_wait_kernel(int n, volatile int32_t* my_flags, int32_t epoch) {
+  pdl_wait();
   const int r = threadIdx.x;
   if (r < n)
     while (my_flags[r] < epoch) {
@@ -207,6 +217,7 @@ __global__ void __launch_bounds__(1024) ep_pack_index_put_kernel(int B, int EW, 
                                                                  int wpr, int self, int32_t* __restrict__ idx,
                                                                  int32_t* __restrict__ pos, int32_t* __restrict__ cnt,
                                                                  uint32_t* const* __restrict__ peer_mask) {
+  pdl_wait();
   __shared__ int warp_tot[32];
   __shared__ int base_s;
   const int r = blockIdx.x;
@@ -248,6 +259,7 @@ __global__ void __launch_bounds__(1024) ep_pack_index_put_kernel(int B, int EW, 
 __global__ void ep_pack_rows_put_kernel(int B, int d, int self, const int32_t* __restrict__ idx,
                                         const int32_t* __restrict__ cnt, const __nv_bfloat16* __restrict__ h, long ldh,
                                         __nv_bfloat16* const* __restrict__ peer_h) {
+  pdl_wait();
   const int r = blockIdx.y;
   __nv_bfloat16* out = peer_h[r] + (size_t)self * B * d;
   const int vec = d / 8;
@@ -264,6 +276,7 @@ __global__ void ep_pack_rows_put_kernel(int B, int d, int self, const int32_t* _
 __global__ void ep_copy_rows_put_kernel(const int32_t* __restrict__ tab, int El, long slot_rows, int self,
                                         const uint8_t* __restrict__ src, long src_ld, uint8_t* const* __restrict__ peer,
                                         long dst_ld, int row_bytes) {
+  pdl_wait();
   const int i = blockIdx.x;
   const int s = i / El;
   const int32_t* t = tab + (size_t)i * 3;
@@ -293,10 +306,10 @@ int smes_ep_pack(int B, int EW, const uint32_t* umask, int n, int wpr, const voi
   if (n < 1 || n > 64 || wpr < 1 || n * wpr > EW) return set_error(SMES_ERR_SHAPE, "ep_pack: n=%d wpr=%d EW=%d", n, wpr, EW);
   if (d % 8) return set_error(SMES_ERR_SHAPE, "ep_pack: d=%d must be a multiple of 8", d);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  ep_pack_index_kernel<<<n, 1024, 0, st>>>(B, EW, umask, wpr, idx, pos, cnt, mask_out);
+  smes_launch(ep_pack_index_kernel, n, 1024, 0, st, B, EW, umask, wpr, idx, pos, cnt, mask_out);
   if (h != nullptr) {
     dim3 g(296, n);
-    ep_pack_rows_kernel<<<g, 256, 0, st>>>(B, d, idx, cnt, reinterpret_cast<const __nv_bfloat16*>(h), ldh,
+    smes_launch(ep_pack_rows_kernel, g, 256, 0, st, B, d, idx, cnt, reinterpret_cast<const __nv_bfloat16*>(h), ldh,
                                           reinterpret_cast<__nv_bfloat16*>(h_out));
   }
   return launch_ok("ep_pack");
@@ -305,7 +318,7 @@ int smes_ep_pack(int B, int EW, const uint32_t* umask, int n, int wpr, const voi
 int smes_ep_segments(int mode, int n, int El, const int32_t* cnt, const int32_t* seg_pad, long slot_rows,
                      int32_t* tab, void* stream) {
   if (mode != 0 && mode != 1) return set_error(SMES_ERR_CONFIG, "ep_segments: mode %d", mode);
-  ep_segments_kernel<<<(n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream)>>>(mode, n, El, cnt, seg_pad,
+  smes_launch(ep_segments_kernel, (n + 63) / 64, 64, 0, reinterpret_cast<cudaStream_t>(stream), mode, n, El, cnt, seg_pad,
                                                                                      slot_rows, tab);
   return launch_ok("ep_segments");
 }
@@ -316,7 +329,7 @@ int smes_ep_copy_rows(int nseg, const int32_t* tab, int dir, const void* src, lo
     return set_error(SMES_ERR_SHAPE, "ep_copy_rows: rows must be 16-byte multiples (row %d, ld %ld/%ld)", row_bytes,
                      src_ld_bytes, dst_ld_bytes);
   if (nseg == 0) return SMES_OK;
-  ep_copy_rows_kernel<<<nseg, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  smes_launch(ep_copy_rows_kernel, nseg, 256, 0, reinterpret_cast<cudaStream_t>(stream), 
       dir, tab, reinterpret_cast<const uint8_t*>(src), src_ld_bytes, reinterpret_cast<uint8_t*>(dst), dst_ld_bytes,
       row_bytes);
   return launch_ok("ep_copy_rows");
@@ -325,14 +338,14 @@ int smes_ep_copy_rows(int nseg, const int32_t* tab, int dir, const void* src, lo
 int smes_ep_combine_dh(int B, int d, int n, long slot_rows, const int32_t* pos, const float* dh_recv,
                        const float* dh_router, float* out, void* stream) {
   if (d % 4) return set_error(SMES_ERR_SHAPE, "ep_combine_dh: d=%d", d);
-  ep_combine_dh_kernel<<<B, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(B, d, n, slot_rows, pos, dh_recv,
+  smes_launch(ep_combine_dh_kernel, B, 256, 0, reinterpret_cast<cudaStream_t>(stream), B, d, n, slot_rows, pos, dh_recv,
                                                                             dh_router, out);
   return launch_ok("ep_combine_dh");
 }
 
 int smes_ep_capacity_guard(int E, long cap, const int32_t* totals, int32_t* seg_pad, int32_t* loads, uint32_t* umask,
                            long n_mask_words, int32_t* usize, long n_inst, int32_t* flag, void* stream) {
-  ep_capacity_guard_kernel<<<64, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, cap, totals, seg_pad, loads,
+  smes_launch(ep_capacity_guard_kernel, 64, 256, 0, reinterpret_cast<cudaStream_t>(stream), E, cap, totals, seg_pad, loads,
                                                                                  umask, n_mask_words, usize, n_inst,
                                                                                  flag);
   return launch_ok("ep_capacity_guard");
@@ -345,10 +358,10 @@ int smes_ep_pack_put(int B, int EW, const uint32_t* umask, int n, int wpr, const
   if (n < 1 || n > 64 || wpr < 1 || n * wpr > EW) return set_error(SMES_ERR_SHAPE, "ep_pack_put: n=%d wpr=%d EW=%d", n, wpr, EW);
   if (d % 8) return set_error(SMES_ERR_SHAPE, "ep_pack_put: d=%d must be a multiple of 8", d);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  ep_pack_index_put_kernel<<<n, 1024, 0, st>>>(B, EW, umask, wpr, self, idx, pos, cnt,
+  smes_launch(ep_pack_index_put_kernel, n, 1024, 0, st, B, EW, umask, wpr, self, idx, pos, cnt,
                                               reinterpret_cast<uint32_t* const*>(peer_mask_recv));
   dim3 g(296, n);
-  ep_pack_rows_put_kernel<<<g, 256, 0, st>>>(B, d, self, idx, cnt, reinterpret_cast<const __nv_bfloat16*>(h), ldh,
+  smes_launch(ep_pack_rows_put_kernel, g, 256, 0, st, B, d, self, idx, cnt, reinterpret_cast<const __nv_bfloat16*>(h), ldh,
                                             reinterpret_cast<__nv_bfloat16* const*>(peer_h_recv));
   return launch_ok("ep_pack_put");
 }
@@ -358,7 +371,7 @@ int smes_ep_copy_rows_put(int nseg, const int32_t* tab, int El, long slot_rows, 
   if (row_bytes % 16 || src_ld_bytes % 16 || dst_ld_bytes % 16)
     return set_error(SMES_ERR_SHAPE, "ep_copy_rows_put: rows must be 16-byte multiples");
   if (nseg == 0) return SMES_OK;
-  ep_copy_rows_put_kernel<<<nseg, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  smes_launch(ep_copy_rows_put_kernel, nseg, 256, 0, reinterpret_cast<cudaStream_t>(stream), 
       tab, El, slot_rows, self, reinterpret_cast<const uint8_t*>(src), src_ld_bytes,
       reinterpret_cast<uint8_t* const*>(peer_dst), dst_ld_bytes, row_bytes);
   return launch_ok("ep_copy_rows_put");
@@ -370,14 +383,14 @@ int smes_ep_put_slots(int n, int self, const void* send, long slot_bytes, long r
   PutArgs a{n, self, reinterpret_cast<const uint8_t*>(send), slot_bytes, row_bytes, rows_used,
             reinterpret_cast<uint8_t* const*>(peer_recv_dev)};
   dim3 g(148, n);
-  ep_put_kernel<<<g, 512, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  smes_launch(ep_put_kernel, g, 512, 0, reinterpret_cast<cudaStream_t>(stream), a);
   return launch_ok("ep_put");
 }
 
 int smes_ep_signal_wait(int n, int self, void* const* peer_flags_dev, int32_t* my_flags, int epoch, void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  ep_signal_kernel<<<1, 64, 0, st>>>(n, self, reinterpret_cast<int32_t* const*>(peer_flags_dev), epoch);
-  ep_wait_kernel<<<1, 64, 0, st>>>(n, my_flags, epoch);
+  smes_launch(ep_signal_kernel, 1, 64, 0, st, n, self, reinterpret_cast<int32_t* const*>(peer_flags_dev), epoch);
+  smes_launch(ep_wait_kernel, 1, 64, 0, st, n, my_flags, epoch);
   return launch_ok("ep_signal_wait");
 }
 

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "ptx.cuh"
 #include "smes_capi.h"
 
 namespace smes {
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_ou
                                                         const float* __restrict__ Qt, long q_es, long q_ts,
                                                         long q_ks, const __nv_bfloat16* __restrict__ W,
                                                         float* __restrict__ part) {
+  pdl_wait();
   fold_tile_body<TM, MODE>(blockIdx.x, blockIdx.y, blockIdx.z, gridDim.y, T, ldg, d_out, d_in, head_w, Qt, q_es, q_ts,
                            q_ks, W, part);
 }
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(256) fold_full_kernel(int T, int ldg, int d_ou
                                                         const __nv_bfloat16* __restrict__ W,
                                                         const float* __restrict__ b, __nv_bfloat16* __restrict__ G,
                                                         float* __restrict__ c) {
+  pdl_wait();
   // W tile (d_out x 64 bf16, padded rows); reused as the [8][TM][64] fp32 group-sum buffer
   __shared__ __align__(16) __nv_bfloat16 sW[FOLD_FULL_MAX_DOUT][72];
   static_assert(FOLD_FULL_MAX_DOUT * 72 * 2 >= 8 * TM * 64 * 4, "fold_full reduction buffer");
@@ -178,6 +181,7 @@ __global__ void fold_finish_kernel(int E, int T, int ldg, int d_out, int d_in, i
                                    const float* __restrict__ part, const float* __restrict__ head_w,
                                    const float* __restrict__ b, __nv_bfloat16* __restrict__ G,
                                    float* __restrict__ c) {
+  pdl_wait();
   const size_t n = (size_t)E * ldg * d_in;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % d_in);
@@ -208,6 +212,7 @@ __global__ void __launch_bounds__(256) unfold_finish_kernel(int E, int T, int d_
                                                             const float* __restrict__ part,
                                                             const float* __restrict__ csum, long cs_es,
                                                             const float* __restrict__ b, float* __restrict__ out) {
+  pdl_wait();
   __shared__ float red[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.y, j = blockIdx.x * 32 + lane;
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(128) unfold_pair_kernel(int E, int T, int ldg,
                                                           const float* __restrict__ head_w,
                                                           const __nv_bfloat16* __restrict__ W, float* __restrict__ dW,
                                                           float* __restrict__ db, float* __restrict__ part) {
+  pdl_wait();
   const int g1x = (d_in + 127) / 128, g1y = (d_out + 31) / 32, n1 = g1x * g1y * E;
   const int bid = blockIdx.x;
   if (bid < n1) {
@@ -294,6 +300,7 @@ __global__ void __launch_bounds__(128) unfold_pair_kernel(int E, int T, int ldg,
 __global__ void fold_prep_kernel(int T, int ldg, int d_out, const float* __restrict__ head_w,
                                  __nv_bfloat16* __restrict__ Pw /* (d_out, ldg) */,
                                  __nv_bfloat16* __restrict__ Wp /* (128, d_out) */) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (Pw != nullptr && i < d_out * ldg) {
     const int j = i / ldg, t = i % ldg;
@@ -314,6 +321,7 @@ __global__ void fold_prep_kernel(int T, int ldg, int d_out, const float* __restr
 }
 
 __global__ void seg_arith_kernel(int n, int step, int32_t* __restrict__ seg) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i <= n) seg[i] = i * step;
 }
@@ -322,6 +330,7 @@ __global__ void seg_arith_kernel(int n, int step, int32_t* __restrict__ seg) {
 __global__ void fold_convert_kernel(int E, int T, int ldg, int d_out, int d_in, const float* __restrict__ Gf,
                                     const float* __restrict__ head_w, const float* __restrict__ b,
                                     __nv_bfloat16* __restrict__ G, float* __restrict__ c) {
+  pdl_wait();
   const size_t n = (size_t)E * ldg * d_in;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     G[i] = __float2bfloat16_rn(Gf[i]);
@@ -341,6 +350,7 @@ __global__ void fold_convert_kernel(int E, int T, int ldg, int d_out, int d_in, 
 // sum_m Wp[m] Qbf[m] = hi(w) hi(q) + hi(w) lo(q) + lo(w) hi(q) (~fp32 accurate); Y uses rows t, 32 + t
 __global__ void unfold_split_kernel(int E, int T, int d_in, const float* __restrict__ Q, long q_es, long q_ts,
                                     long q_ks, __nv_bfloat16* __restrict__ Qbf) {
+  pdl_wait();
   const size_t n = (size_t)E * 128 * d_in;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const int k = (int)(i % d_in);
@@ -360,6 +370,7 @@ __global__ void unfold_split_kernel(int E, int T, int d_in, const float* __restr
 // db[e, j] = sum_t head_w[t, j] csum[e, t]
 __global__ void unfold_db_kernel(int E, int T, int d_out, const float* __restrict__ csum, long cs_es,
                                  const float* __restrict__ head_w, float* __restrict__ db) {
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= E * d_out) return;
   const int e = i / d_out, j = i % d_out;
@@ -372,6 +383,7 @@ __global__ void unfold_db_kernel(int E, int T, int d_out, const float* __restric
 __global__ void __launch_bounds__(256) unfold_head_reduce_kernel(int E, int T, int d_out, const float* __restrict__ Y,
                                                                  const float* __restrict__ csum, long cs_es,
                                                                  const float* __restrict__ b, float* __restrict__ out) {
+  pdl_wait();
   __shared__ float red[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.y, j = blockIdx.x * 32 + lane;
@@ -451,18 +463,18 @@ int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* hea
     auto* Pw = reinterpret_cast<__nv_bfloat16*>(work + w.pw);
     auto* seg = reinterpret_cast<int32_t*>(work + w.seg);
     float* Gf = work + w.gf;
-    fold_prep_kernel<<<(d_out * ldg + 255) / 256, 256, 0, st>>>(T, ldg, d_out, head_w, Pw, nullptr);
-    seg_arith_kernel<<<(E + 256) / 256, 256, 0, st>>>(E, d_out, seg);
+    smes_launch(fold_prep_kernel, (d_out * ldg + 255) / 256, 256, 0, st, T, ldg, d_out, head_w, Pw, nullptr);
+    smes_launch(seg_arith_kernel, (E + 256) / 256, 256, 0, st, E, d_out, seg);
     int rc = smes_gemm_ragged_k_periodic(Pw, ldg, d_out, W, d_in, (long)E * d_out, E, ldg, d_in, seg, Gf, nullptr,
                                          d_out, stream);
     if (rc) return rc;
     const long n = (long)E * ldg * d_in;
     const long blocks = (n + 255) / 256 < 4096 ? (n + 255) / 256 : 4096;
     const long need = ((long)E * ldg * 32 + 255) / 256;
-    fold_convert_kernel<<<(int)(blocks > need ? blocks : need), 256, 0, st>>>(E, T, ldg, d_out, d_in, Gf, head_w, b,
+    smes_launch(fold_convert_kernel, (int)(blocks > need ? blocks : need), 256, 0, st, E, T, ldg, d_out, d_in, Gf, head_w, b,
                                                                                Gb, c);
   } else if (d_out <= FOLD_FULL_MAX_DOUT && T <= 8 && ldg <= 8) {
-    fold_full_kernel<8><<<dim3((d_in + 63) / 64, E), 256, 0, st>>>(T, ldg, d_out, d_in, head_w, Wb, b, Gb, c);
+    smes_launch(fold_full_kernel<8>, dim3((d_in + 63) / 64, E), 256, 0, st, T, ldg, d_out, d_in, head_w, Wb, b, Gb, c);
   } else {
     const int splits = (d_out + 63) / 64;
     dim3 grid((d_in + 63) / 64, E, splits);
@@ -471,16 +483,16 @@ int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* hea
     const int gfin = nfin > nfin_c ? nfin : nfin_c;
     switch (fold_tm(T)) {
       case 8:
-        fold_tile_kernel<8, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
-        fold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+        smes_launch(fold_tile_kernel<8, TILE_FOLD>, grid, 128, 0, st, T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
+        smes_launch(fold_finish_kernel<8>, gfin, 256, 0, st, E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
         break;
       case 16:
-        fold_tile_kernel<16, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
-        fold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+        smes_launch(fold_tile_kernel<16, TILE_FOLD>, grid, 128, 0, st, T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
+        smes_launch(fold_finish_kernel<16>, gfin, 256, 0, st, E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
         break;
       default:
-        fold_tile_kernel<32, TILE_FOLD><<<grid, 128, 0, st>>>(T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
-        fold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
+        smes_launch(fold_tile_kernel<32, TILE_FOLD>, grid, 128, 0, st, T, ldg, d_out, d_in, head_w, nullptr, 0, 0, 0, Wb, work);
+        smes_launch(fold_finish_kernel<32>, gfin, 256, 0, st, E, T, ldg, d_out, d_in, splits, work, head_w, b, Gb, c);
     }
   }
   cudaError_t e = cudaGetLastError();
@@ -501,18 +513,18 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
     auto* seg = reinterpret_cast<int32_t*>(work + w.seg128);
     auto* Qbf = reinterpret_cast<__nv_bfloat16*>(work + w.qbf);
     float* Y = work + w.y;
-    fold_prep_kernel<<<(128 * d_out + 255) / 256, 256, 0, st>>>(T, ldg, d_out, head_w, nullptr, Wp);
-    seg_arith_kernel<<<(E + 256) / 256, 256, 0, st>>>(E, 128, seg);
-    unfold_split_kernel<<<4096, 256, 0, st>>>(E, T, d_in, Q, q_es, q_ts, q_ks, Qbf);
+    smes_launch(fold_prep_kernel, (128 * d_out + 255) / 256, 256, 0, st, T, ldg, d_out, head_w, nullptr, Wp);
+    smes_launch(seg_arith_kernel, (E + 256) / 256, 256, 0, st, E, 128, seg);
+    smes_launch(unfold_split_kernel, 4096, 256, 0, st, E, T, d_in, Q, q_es, q_ts, q_ks, Qbf);
     int rc = smes_gemm_ragged_k_periodic(Wp, d_out, 128, Qbf, d_in, (long)E * 128, E, d_out, d_in, seg, dW, nullptr,
                                          128, stream);
     if (rc) return rc;
-    unfold_db_kernel<<<(E * d_out + 255) / 256, 256, 0, st>>>(E, T, d_out, csum, cs_es, head_w, db);
+    smes_launch(unfold_db_kernel, (E * d_out + 255) / 256, 256, 0, st, E, T, d_out, csum, cs_es, head_w, db);
     rc = smes_gemm_ragged_m(Qbf, d_in, (long)E * 128, W, E, d_out, d_in, 0, seg, nullptr, 0, nullptr, nullptr, 0, Y,
                             d_out, 1, (long)E * 128, stream);
     if (rc) return rc;
     dim3 g((d_out + 31) / 32, T);
-    unfold_head_reduce_kernel<<<g, 256, 0, st>>>(E, T, d_out, Y, csum, cs_es, b, d_head_w);
+    smes_launch(unfold_head_reduce_kernel, g, 256, 0, st, E, T, d_out, Y, csum, cs_es, b, d_head_w);
   } else {
     dim3 g1((d_in + 127) / 128, (d_out + 31) / 32, E);
     const int splits = (d_in + 63) / 64;
@@ -521,19 +533,19 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
     const int npair = (int)(g1.x * g1.y * g1.z + g2.x * g2.y * g2.z);
     switch (fold_tm(T)) {
       case 8:
-        unfold_pair_kernel<8><<<npair, 128, 0, st>>>(E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
+        smes_launch(unfold_pair_kernel<8>, npair, 128, 0, st, E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
                                                          head_w, Wb, dW, db, work);
-        unfold_finish_kernel<8><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+        smes_launch(unfold_finish_kernel<8>, gfin, 256, 0, st, E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
         break;
       case 16:
-        unfold_pair_kernel<16><<<npair, 128, 0, st>>>(E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
+        smes_launch(unfold_pair_kernel<16>, npair, 128, 0, st, E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
                                                          head_w, Wb, dW, db, work);
-        unfold_finish_kernel<16><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+        smes_launch(unfold_finish_kernel<16>, gfin, 256, 0, st, E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
         break;
       default:
-        unfold_pair_kernel<32><<<npair, 128, 0, st>>>(E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
+        smes_launch(unfold_pair_kernel<32>, npair, 128, 0, st, E, T, ldg, d_out, d_in, Q, q_es, q_ts, q_ks, csum, cs_es,
                                                          head_w, Wb, dW, db, work);
-        unfold_finish_kernel<32><<<gfin, 256, 0, st>>>(E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
+        smes_launch(unfold_finish_kernel<32>, gfin, 256, 0, st, E, T, d_out, splits, work, csum, cs_es, b, d_head_w);
     }
   }
   cudaError_t e = cudaGetLastError();

@@ -18,6 +18,7 @@ namespace smes {
 __global__ void __launch_bounds__(256) split_bf16x3_kernel(long rows, int cols, const float* __restrict__ src,
                                                             long lds, __nv_bfloat16* __restrict__ dst, long ldd,
                                                             const int32_t* __restrict__ rows_dev) {
+  pdl_wait();
   if (rows_dev != nullptr) rows = min(rows, (long)*rows_dev);
   const int q = cols >> 2;                       // float4 groups per row
   const long n = rows * q;
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(CF_THREADS)
                            const float* __restrict__ head_b, float* __restrict__ reps, float* __restrict__ logits,
                            float* __restrict__ preds, const float* __restrict__ labels, const float* __restrict__ lam,
                            double* __restrict__ loss_part) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   const int EW = (E + 31) >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -144,7 +146,7 @@ int smes_split_bf16x3(long rows, int cols, const float* src, long lds, void* dst
   const long n = rows * (cols / 4);
   const long want = (n + 255) / 256;
   const int grid = (int)(want < 148L * 16 ? want : 148L * 16);
-  split_bf16x3_kernel<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  smes_launch(split_bf16x3_kernel, grid, 256, 0, reinterpret_cast<cudaStream_t>(stream), 
       rows, cols, src, lds, reinterpret_cast<__nv_bfloat16*>(dst), ldd, rows_dev);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "split_bf16x3 launch: %s", cudaGetErrorString(e));
@@ -170,7 +172,7 @@ int smes_combine_fwd_f32(int T, int B, int E, int K, int d_out, int umax, const 
                                           (int)smem);
     if (ea != cudaSuccess) return set_error(SMES_ERR_CUDA, "combine_fwd_f32 smem: %s", cudaGetErrorString(ea));
   }
-  combine_fwd_f32_kernel<<<grid, CF_THREADS, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
+  smes_launch(combine_fwd_f32_kernel, grid, CF_THREADS, smem, reinterpret_cast<cudaStream_t>(stream), 
       T, B, E, K, d_out, umax, umask, usize, row_of, active, wsel, O, ldo, head_w, head_b, reps, logits, preds, labels,
       lam, loss_part);
   cudaError_t e = cudaGetLastError();

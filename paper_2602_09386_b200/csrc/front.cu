@@ -211,6 +211,7 @@ template <int E, int KS, int KA, bool DM>
 __global__ void __launch_bounds__(kThreads, 1)
     route_front_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                        const Args a) {
+  pdl_wait();
   using S = Plan<E, DM>;
   constexpr int K = KS + KA;
   constexpr int EQ = S::EQ;
@@ -793,7 +794,7 @@ static int front_launch(const CUtensorMap& ta, const CUtensorMap& tb, const fron
     if (ea != cudaSuccess) return set_error(SMES_ERR_CUDA, "route_front smem attribute: %s", cudaGetErrorString(ea));
     attr = true;
   }
-  kern<<<grid, front::kThreads, bytes, st>>>(ta, tb, a);
+  smes_launch(kern, grid, front::kThreads, bytes, st, ta, tb, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "route_front launch: %s", cudaGetErrorString(e));
   return SMES_OK;

@@ -96,6 +96,7 @@ template <int BN, int MODE, bool B_MN, bool F32>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  pdl_wait();
   using S = Smem<BN, MODE>;
   constexpr int kStages = S::kStages;
   constexpr int kAcc = S::kAccStages;
@@ -457,7 +458,7 @@ static int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
       return set_error(SMES_ERR_CUDA, "grouped_gemm smem attribute (%d B): %s", SM::kBytes, cudaGetErrorString(ea));
     attr = true;
   }
-  kern<<<num_sms(), kThreads, SM::kBytes, st>>>(a, b, c, args);
+  smes_launch(kern, num_sms(), kThreads, SM::kBytes, st, a, b, c, args);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "grouped_gemm launch: %s", cudaGetErrorString(e));
   return SMES_OK;

@@ -41,6 +41,7 @@ __device__ __forceinline__ int union_rank_of(const uint32_t* um, int e) {
 }
 
 __global__ void __launch_bounds__(LB_WARPS * 32) combine_bwd_reps_kernel(const RepsBwdArgs a) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.x * LB_WARPS + warp;
   if (b >= a.B) return;
@@ -135,7 +136,7 @@ int smes_combine_bwd_reps(int T, int B, int E, int K, int d_out, int umax, const
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(combine_bwd_reps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  combine_bwd_reps_kernel<<<(B + LB_WARPS - 1) / LB_WARPS, LB_WARPS * 32, smem, st>>>(a);
+  smes_launch(combine_bwd_reps_kernel, (B + LB_WARPS - 1) / LB_WARPS, LB_WARPS * 32, smem, st, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "combine_bwd_reps launch: %s", cudaGetErrorString(e));
   return SMES_OK;

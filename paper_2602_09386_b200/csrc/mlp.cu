@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mlp_fwd_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                    const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmH,
                    const FwdArgs a) {
+  pdl_wait();
   using S = FwdSmem<DK>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
@@ -491,6 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mlp_fwd2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                     const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmH,
                     const FwdArgs a) {
+  pdl_wait();
   using S = Fwd2Smem<DK>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
@@ -850,6 +852,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mlp_dgrad_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmG,
                      const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmDX,
                      const __grid_constant__ CUtensorMap tmDH, const DgradArgs a) {
+  pdl_wait();
   using S = DgSmem<DK>;
   constexpr int D = DK * 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1139,6 +1142,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     mlp_dgrad2_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmG,
                       const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmDX,
                       const __grid_constant__ CUtensorMap tmDH, const DgradArgs a) {
+  pdl_wait();
   using S = Dg2Smem<DK>;
   constexpr int D = DK * 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1468,6 +1472,7 @@ template <int DK>
 __global__ void __launch_bounds__(kThreads, 1)
     mlp_wgrad_kernel(const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmG,
                      const __grid_constant__ CUtensorMap tmX, const WgradArgs a) {
+  pdl_wait();
   using S = WgSmem<DK>;
   constexpr int D = DK * 64;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1797,7 +1802,7 @@ int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const f
     const int sm = mlp::FwdSmem<DK>::kBytes;                                                           \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<sm_count(), mlp::kThreads, sm, st>>>(tx, tw, tg, th, args);                                    \
+    smes_launch(k, sm_count(), mlp::kThreads, sm, st, tx, tw, tg, th, args);                                    \
     break;                                                                                             \
   }
   switch (d / 64) {
@@ -1858,7 +1863,7 @@ int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const 
     const int sm = mlp::Fwd2Smem<DK>::kBytes;                                                           \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd2 smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<pair_grid(k, sm), mlp::kThreads, sm, st>>>(tx, tw, tg, th, args);                                    \
+    smes_launch(k, pair_grid(k, sm), mlp::kThreads, sm, st, tx, tw, tg, th, args);                                    \
     break;                                                                                             \
   }
   switch (d / 64) {
@@ -1922,7 +1927,7 @@ int smes_mlp_dgrad(const void* C, long ldc, long rows_cap, const void* G, int ld
     const int sm = mlp::DgSmem<DK>::kBytes;                                                            \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<sm_count(), mlp::kThreads, sm, st>>>(tc, tg, tw, td, th, args);                                   \
+    smes_launch(k, sm_count(), mlp::kThreads, sm, st, tc, tg, tw, td, th, args);                                   \
     break;                                                                                             \
   }
   switch (d / 64) {
@@ -1985,7 +1990,7 @@ int smes_mlp_dgrad2(const void* C, long ldc, long rows_cap, const void* G, int l
     const int sm = mlp::Dg2Smem<DK>::kBytes;                                                            \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_dgrad2 smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<pair_grid(k, sm), mlp::kThreads, sm, st>>>(tc, tg, tw, td, th, args);                                   \
+    smes_launch(k, pair_grid(k, sm), mlp::kThreads, sm, st, tc, tg, tw, td, th, args);                                   \
     break;                                                                                             \
   }
   switch (d / 64) {
@@ -2036,7 +2041,7 @@ int smes_mlp_wgrad(const void* C, long ldc, long rows_cap, const void* G, int ld
     const int sm = mlp::WgSmem<DK>::kBytes;                                                            \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_wgrad smem attribute: %s", cudaGetErrorString(e)); \
-    k<<<grid, mlp::kThreads, sm, st>>>(tc, tg, tx, args);                                              \
+    smes_launch(k, grid, mlp::kThreads, sm, st, tc, tg, tx, args);                                              \
     break;                                                                                             \
   }
   switch (d / 64) {

@@ -31,6 +31,7 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
                                     int32_t* __restrict__ totals, unsigned int* __restrict__ ticket,
                                     int32_t* __restrict__ seg_half, double lb_scale, double bt, int dense,
                                     double* __restrict__ st_out, float* __restrict__ freq_f32) {
+  pdl_wait();
   const int e = blockIdx.x;
   __shared__ int32_t warp_tot[32];
   __shared__ double red[3][32];
@@ -193,6 +194,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
                    __nv_bfloat16* __restrict__ X, long ldx, int32_t* __restrict__ row_of, int umax,
                    int32_t* __restrict__ gather_inst, int32_t* __restrict__ gather_exp,
                    __nv_bfloat16* __restrict__ zero_rows2, long ldz2, int d2) {
+  pdl_wait();
   const int C = (B + PL_WARPS * rows_per_warp - 1) / (PL_WARPS * rows_per_warp);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int EW = (E + 31) >> 5;
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(PL_WARPS * 32)
 __global__ void __launch_bounds__(PL_WARPS * 32)
     plan_counts_kernel(int B, int E, int rows_per_warp, const uint32_t* __restrict__ umask,
                        int32_t* __restrict__ chunk_union, int32_t* __restrict__ usize) {
+  pdl_wait();
   __shared__ int32_t s_cnt[PL_WARPS][1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int EW = (E + 31) >> 5;
@@ -336,7 +339,7 @@ int smes_plan_reduce(int C, int E, const int32_t* chunk_union, const int32_t* ch
                      int32_t* seg_pad, int32_t* seg_log, int32_t* totals, unsigned int* ticket, int32_t* seg_half,
                      void* stream) {
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
+  smes_launch(chunk_reduce_kernel, E, 256, 0, st, C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
                                          stats_raw, seg_pad, seg_log, totals, ticket, seg_half, 1.0, 1.0, 0, nullptr,
                                          nullptr);
   cudaError_t e = cudaGetLastError();
@@ -353,7 +356,7 @@ int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32
   if (K < 1 || batch_times_tasks <= 0.0) return set_error(SMES_ERR_CONFIG, "plan_reduce_stats: K=%d B*T=%g", K,
                                                           batch_times_tasks);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  chunk_reduce_kernel<<<E, 256, 0, st>>>(C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
+  smes_launch(chunk_reduce_kernel, E, 256, 0, st, C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
                                          stats_raw, seg_pad, seg_log, totals, ticket, seg_half,
                                          (double)(lb_experts > 0 ? lb_experts : E) / (double)K, batch_times_tasks,
                                          dense, stats_out, freq_f32);
@@ -366,7 +369,7 @@ int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int
                      void* stream) {
   if (E > 1024) return set_error(SMES_ERR_SHAPE, "plan: E=%d exceeds 1024", E);
   const int C = (B + PL_WARPS * rows_per_warp - 1) / (PL_WARPS * rows_per_warp);
-  plan_counts_kernel<<<C, PL_WARPS * 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(B, E, rows_per_warp, umask,
+  smes_launch(plan_counts_kernel, C, PL_WARPS * 32, 0, reinterpret_cast<cudaStream_t>(stream), B, E, rows_per_warp, umask,
                                                                                      chunk_union, usize);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_counts launch: %s", cudaGetErrorString(e));
@@ -390,7 +393,7 @@ int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* um
   auto* zz = reinterpret_cast<__nv_bfloat16*>(zero_rows2);
 #define PL_CASE(EP, VV)                                                                                       \
   if (epl <= EP && vec <= VV) {                                                                               \
-    scatter_kernel<EP, VV><<<grid, PL_WARPS * 32, 0, st>>>(B, E, d, rows_per_warp, umask, chunk_base, seg_pad, \
+    smes_launch(scatter_kernel<EP, VV>, grid, PL_WARPS * 32, 0, st, B, E, d, rows_per_warp, umask, chunk_base, seg_pad, \
                                                            loads, hh, ldh, xx, ldx, row_of, umax, gather_inst, \
                                                            gather_exp, zz, ldz2, d2);                          \
   } else

@@ -14,6 +14,7 @@ namespace smes {
 
 __global__ void stats_finalize_kernel(int E, int K, int e_lb, double bt, int dense, const double* __restrict__ raw,
                                       double* __restrict__ out, float* __restrict__ freq_f32) {
+  pdl_wait();
   // out: [freq E][mass E][counts E][value]
   __shared__ double red[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -40,6 +41,7 @@ __global__ void stats_finalize_kernel(int E, int K, int e_lb, double bt, int den
 
 __global__ void loss_finalize_kernel(int n, const double* __restrict__ part, double inv_b, double beta,
                                      const double* __restrict__ stats_value, double* __restrict__ out) {
+  pdl_wait();
   __shared__ double red[32];
   double v = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) v += part[i];
@@ -63,6 +65,7 @@ __global__ void loss_finalize_kernel(int n, const double* __restrict__ part, dou
 __global__ void __launch_bounds__(256) seg_colsum_tiles_kernel(const __nv_bfloat16* __restrict__ M, long ld, int N,
                                                                const int32_t* __restrict__ seg, int G,
                                                                float* __restrict__ part) {
+  pdl_wait();
   __shared__ float red[2048 + 64];
   const int tile = blockIdx.x;
   if (tile * 128 >= seg[G]) return;
@@ -97,6 +100,7 @@ __global__ void __launch_bounds__(256) seg_colsum_tiles_kernel(const __nv_bfloat
 // stage 2: out[g][n] = sum of the group's tile partials in tile order
 __global__ void seg_colsum_groups_kernel(const float* __restrict__ part, int N, const int32_t* __restrict__ seg,
                                          float* __restrict__ out) {
+  pdl_wait();
   const int g = blockIdx.y;
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= N) return;
@@ -117,6 +121,7 @@ template <int VEC>
 __global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize, const int32_t* __restrict__ row_of,
                                  int umax, const __nv_bfloat16* __restrict__ dX, long ldx,
                                  const float* __restrict__ dh_router, float* __restrict__ dh) {
+  pdl_wait();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
   const int b = warp;
@@ -172,6 +177,7 @@ __global__ void unpermute_kernel(int B, int d, const int32_t* __restrict__ usize
 
 __global__ void __launch_bounds__(1024) part_reduce_kernel(const float* __restrict__ part, int nparts, int n,
                                                             float* __restrict__ out) {
+  pdl_wait();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int i = blockIdx.x * 32 + lane;
@@ -202,6 +208,7 @@ __global__ void __launch_bounds__(1024) part_reduce_kernel(const float* __restri
 __global__ void lb_grad_kernel(int T, int B, int E, int K, const int32_t* __restrict__ active,
                                const float* __restrict__ wsel, const float* __restrict__ z, long zst, long zsb,
                                const float* __restrict__ freq, float coef, int dense, float* __restrict__ out) {
+  pdl_wait();
   const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (row >= T * B) return;
   const int t = row / B, b = row - t * B;
@@ -241,6 +248,7 @@ __global__ void lb_grad_kernel(int T, int B, int E, int K, const int32_t* __rest
 // weighted clamped BCE (training.py:54-57) -> per-block fp64 partials
 __global__ void bce_kernel(int T, int B, const float* __restrict__ pred, const float* __restrict__ y,
                            const float* __restrict__ lam, double* __restrict__ part, int32_t* __restrict__ bad) {
+  pdl_wait();
   __shared__ double red[32];
   double v = 0.0;
   int badv = 0;
@@ -302,6 +310,7 @@ __device__ __forceinline__ void tile_sum(const float* __restrict__ part, int npa
 }
 
 __global__ void __launch_bounds__(1024) post_combine_kernel(const PostArgs a) {
+  pdl_wait();
   __shared__ float red[32][33];
   __shared__ double dred[32];
   const int t_cs = a.part_csum ? (a.n_cs + 31) / 32 : 0;
@@ -346,14 +355,14 @@ extern "C" {
 int smes_stats_finalize(int E, int K, int lb_experts, double batch_times_tasks, int dense, const double* raw,
                         double* out, float* freq_f32, void* stream) {
   const int e_lb = lb_experts > 0 ? lb_experts : E;
-  stats_finalize_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(E, K, e_lb, batch_times_tasks, dense, raw,
+  smes_launch(stats_finalize_kernel, 1, 256, 0, reinterpret_cast<cudaStream_t>(stream), E, K, e_lb, batch_times_tasks, dense, raw,
                                                                                out, freq_f32);
   return launch_check("stats_finalize");
 }
 
 int smes_loss_finalize(int nparts, const double* part, double inv_b, double beta, const double* stats_value,
                        double* out, void* stream) {
-  loss_finalize_kernel<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(nparts, part, inv_b, beta, stats_value,
+  smes_launch(loss_finalize_kernel, 1, 256, 0, reinterpret_cast<cudaStream_t>(stream), nparts, part, inv_b, beta, stats_value,
                                                                             out);
   return launch_check("loss_finalize");
 }
@@ -364,11 +373,11 @@ int smes_seg_colsum(const void* M, long ld, long rows_cap, int N, const int32_t*
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (N / 8 > 256 || N % 8) return set_error(SMES_ERR_SHAPE, "seg_colsum: N=%d must be <= 2048", N);
   const int tiles = (int)(rows_cap / 128);
-  seg_colsum_tiles_kernel<<<tiles, 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(M), ld, N, seg, G, part);
+  smes_launch(seg_colsum_tiles_kernel, tiles, 256, 0, st, reinterpret_cast<const __nv_bfloat16*>(M), ld, N, seg, G, part);
   int rc = launch_check("seg_colsum_tiles");
   if (rc) return rc;
   dim3 g2((N + 63) / 64, G);
-  seg_colsum_groups_kernel<<<g2, 64, 0, st>>>(part, N, seg, out);
+  smes_launch(seg_colsum_groups_kernel, g2, 64, 0, st, part, N, seg, out);
   return launch_check("seg_colsum_groups");
 }
 
@@ -379,10 +388,10 @@ int smes_unpermute(int B, int d, const int32_t* usize, const int32_t* row_of, in
   const int vec = (d + 255) / 256;
   const int blocks = (B * 32 + 255) / 256;
   auto* x = reinterpret_cast<const __nv_bfloat16*>(dX);
-  if (vec <= 1) unpermute_kernel<1><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
-  else if (vec <= 2) unpermute_kernel<2><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
-  else if (vec <= 4) unpermute_kernel<4><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
-  else unpermute_kernel<8><<<blocks, 256, 0, st>>>(B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  if (vec <= 1) smes_launch(unpermute_kernel<1>, blocks, 256, 0, st, B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  else if (vec <= 2) smes_launch(unpermute_kernel<2>, blocks, 256, 0, st, B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  else if (vec <= 4) smes_launch(unpermute_kernel<4>, blocks, 256, 0, st, B, d, usize, row_of, umax, x, ldx, dh_router, dh);
+  else smes_launch(unpermute_kernel<8>, blocks, 256, 0, st, B, d, usize, row_of, umax, x, ldx, dh_router, dh);
   return launch_check("unpermute");
 }
 
@@ -390,19 +399,19 @@ int smes_lb_grad(int T, int B, int E, int K, const int32_t* active, const float*
                  long zsb, const float* freq, float coef, int dense, float* out, void* stream) {
   if (K > 32) return set_error(SMES_ERR_CONFIG, "lb_grad: K=%d exceeds 32", K);
   const long rows = (long)T * B;
-  lb_grad_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+  smes_launch(lb_grad_kernel, (unsigned)((rows * 32 + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream), 
       T, B, E, K, active, wsel, z, zst, zsb, freq, coef, dense, out);
   return launch_check("lb_grad");
 }
 
 int smes_bce_loss(int T, int B, const float* pred, const float* labels, const float* lam, double* part, int nparts,
                   int32_t* bad, void* stream) {
-  bce_kernel<<<nparts, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(T, B, pred, labels, lam, part, bad);
+  smes_launch(bce_kernel, nparts, 256, 0, reinterpret_cast<cudaStream_t>(stream), T, B, pred, labels, lam, part, bad);
   return launch_check("bce_loss");
 }
 
 int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream) {
-  part_reduce_kernel<<<(n + 31) / 32, nparts >= 256 ? 1024 : 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, nparts, n, out);
+  smes_launch(part_reduce_kernel, (n + 31) / 32, nparts >= 256 ? 1024 : 256, 0, reinterpret_cast<cudaStream_t>(stream), part, nparts, n, out);
   return launch_check("part_reduce");
 }
 
@@ -413,7 +422,7 @@ int smes_post_combine(int nparts, const float* part_csum, int n_csum, float* csu
   PostArgs a{nparts, part_csum, n_csum, csum, part_rb, n_rb, rb, part_db, n_db, db, loss_part, inv_b, beta,
              stats_value, loss_out};
   const int blocks = (part_csum ? (n_csum + 31) / 32 : 0) + (part_rb ? (n_rb + 31) / 32 : 0) + (n_db + 31) / 32 + 1;
-  post_combine_kernel<<<blocks, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  smes_launch(post_combine_kernel, blocks, 1024, 0, reinterpret_cast<cudaStream_t>(stream), a);
   return launch_check("post_combine");
 }
 }  // extern "C"

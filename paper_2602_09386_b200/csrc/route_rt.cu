@@ -196,6 +196,7 @@ __device__ __forceinline__ float expm1_neg(float x) {
 
 template <int E, int G, int KS, int KA>
 __global__ void __launch_bounds__(kThreads) route_rt_kernel(const Args a) {
+  pdl_wait();
   constexpr int K = KS + KA;
   constexpr int PER = E / G;                       // pooled scores owned per lane
   constexpr int NG = kThreads / G;                 // row groups per CTA
@@ -442,7 +443,7 @@ static int rt_launch_g(const rt::Args& a, int C, int ks, cudaStream_t st) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    kern<<<C, rt::kThreads, smem, st>>>(a);
+    smes_launch(kern, C, rt::kThreads, smem, st, a);
     return 0;
   };
   if (ks == 4) return go(rt::route_rt_kernel<E, G, 4, 2>);

@@ -101,6 +101,7 @@ __device__ __forceinline__ void sorted_positions(uint32_t bits, int lane, int (&
 // probs_in / probs_out (the training and scoring path) -- the branches compile away.
 template <int EPL, int TP, int KS, int KA, bool PLAIN>
 __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int T = a.T, E = a.E, ks = KS > 0 ? KS : a.ks, ka = KA > 0 ? KA : a.ka, K = ks + ka;
   const bool frozen = !PLAIN && a.frozen;
@@ -375,6 +376,7 @@ template <int T, int E, int KS, int KA>
 #define SMES_TG_MINB 8      // 32 warps per SM: occupancy beats the few spills (tools/route_time.py)
 #endif
 __global__ void __launch_bounds__(RT_WARPS * 32, SMES_TG_MINB) route_tg_kernel(const RouteArgs a) {
+  pdl_wait();
   constexpr int L = 32 / T, EPT = E / L, R = EPT / T, K = KS + KA, EW = (E + 31) / 32;
   static_assert(32 % T == 0 && E % L == 0 && EPT % T == 0 && E <= 64, "route_tg shape");
   using mask_t = unsigned long long;
@@ -658,7 +660,7 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
     if (smem > 48 * 1024)                                                                         \
       cudaFuncSetAttribute(route_kernel<N, TPV, KS, KA, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                            \
-    route_kernel<N, TPV, KS, KA, PL><<<C, RT_WARPS * 32, smem, st>>>(a);                         \
+    smes_launch(route_kernel<N, TPV, KS, KA, PL>, C, RT_WARPS * 32, smem, st, a);                         \
   }
 #define RT_LAUNCH_T(N, TPV)                                                                       \
   {                                                                                               \
@@ -677,7 +679,7 @@ int smes_route_batch(const float* z, long stride_t, long stride_b, const double*
   if (plain && b42 && T == TT && E == EE) {                                                        \
     if (smem_tg > 48 * 1024)                                                                      \
       cudaFuncSetAttribute(route_tg_kernel<TT, EE, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tg); \
-    route_tg_kernel<TT, EE, 4, 2><<<C, RT_WARPS * 32, smem_tg, st>>>(a);                            \
+    smes_launch(route_tg_kernel<TT, EE, 4, 2>, C, RT_WARPS * 32, smem_tg, st, a);                            \
   } else
   RT_TG(8, 32) RT_TG(4, 32)
   RT_LAUNCH(1) RT_LAUNCH(2) RT_LAUNCH(4) RT_LAUNCH(8) RT_LAUNCH(16) RT_LAUNCH(32) {}

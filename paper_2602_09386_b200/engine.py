@@ -19,6 +19,7 @@ Kernel sequence (reference functions in taskmoe/ they replace):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -208,6 +209,8 @@ class SMESEngine:
         # serial: every launch on the caller's stream (no backward side stream) -- the bench's
         # per-kernel CUDA-event timing needs it, since events only see the stream they are on
         self.serial = False
+        # measured 0.531 vs 0.529 ms at c2 with the fold on the side stream (tools/ab_fold.sh): off by default
+        self.fold_side = os.environ.get("SMES_FOLD_SIDE", "0") == "1"
         self._alloc()
         self.refresh_weights()
 
@@ -434,18 +437,7 @@ class SMESEngine:
         the task heads, so its output O and the task reps are not materialised."""
         s = self._stream()
         T, E, B, d = self.T, self.E, self.B, self.d
-        # the head fold (G_e = head_W W_last,e, c_e) depends on the weights only: it runs on the side
-        # stream under the router and the plan, joined before the expert kernels
         self._fold_ev = None
-        if fold and refold and self.can_fold and not self.serial:
-            if not hasattr(self, "_side"):
-                self._side = torch.cuda.Stream(self.dev)
-            fork = torch.cuda.Event()
-            fork.record(torch.cuda.current_stream(self.dev))
-            self._side.wait_event(fork)
-            self._fold(self._side.cuda_stream)
-            self._fold_ev = torch.cuda.Event()
-            self._fold_ev.record(self._side)
         if self.use_front and not frozen:
             # router GEMM + progressive router in one kernel (routing.py:101-103 + :235-281)
             # keep_logits off (training steps): neither z nor the dense mass (read only by the dense
@@ -461,6 +453,18 @@ class SMESEngine:
             _tagged("router_fwd", "smes_gemm_ragged_m", ptr(self.h), self.ldh, B, ptr(self.wr_bf), 1, T * E, d, 0,
                     ptr(self.seg_router), ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
             self.route(s, frozen=frozen)
+        # the head fold (G_e = head_W W_last,e, c_e) depends on the weights only: it runs on the side
+        # stream next to the plan reduce (32 CTAs) and the scatter, joined before the expert kernels
+        # (forked after the router: the fused front wants every SM)
+        if fold and refold and self.can_fold and not self.serial and self.fold_side:
+            if not hasattr(self, "_side"):
+                self._side = torch.cuda.Stream(self.dev)
+            fork = torch.cuda.Event()
+            fork.record(torch.cuda.current_stream(self.dev))
+            self._side.wait_event(fork)
+            self._fold(self._side.cuda_stream)
+            self._fold_ev = torch.cuda.Event()
+            self._fold_ev.record(self._side)
         if finalize_stats:
             # single device: LoadStats over the local B*T, finalized by the plan reduce's last block
             _tagged("plan_reduce", "smes_plan_reduce_stats", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
@@ -595,6 +599,7 @@ class SMESEngine:
             main = torch.cuda.current_stream(self.dev)
             if not hasattr(self, "_side"):
                 self._side = torch.cuda.Stream(self.dev)
+            if not hasattr(self, "_ev_fork"):
                 self._ev_fork, self._ev_join = torch.cuda.Event(), torch.cuda.Event()
                 self._ev_dx = torch.cuda.Event()
             self._ev_fork.record(main)
