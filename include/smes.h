@@ -117,6 +117,9 @@ int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32
                            double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
                            unsigned int* ticket, int32_t* seg_half, int K, int lb_experts, double batch_times_tasks,
                            int dense, double* stats_out, float* freq_f32, void* stream);
+/* int32 elements of the ``ticket`` work buffer smes_plan_reduce / smes_plan_reduce_stats need
+ * (zero-initialised once by the caller; the kernels keep it replay-safe themselves). */
+int smes_plan_reduce_work_ints(int C, int E);
 int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
                      void* stream);
 int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,

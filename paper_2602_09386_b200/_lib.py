@@ -30,6 +30,7 @@ SIGNATURES = {
     "smes_route_front_supported": [I, I, I, I, I],
     "smes_route_front_count_exact": [P],
     "smes_route_count_exact": [P],
+    "smes_plan_reduce_work_ints": [I, I],
     "smes_route_rt_supported": [I, I, I, I],
     "smes_route_rt": [P, L, L, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P],
     "smes_peer_allreduce_f64": [I, I, I, P, P, P, P, P, P, P, P],
@@ -85,7 +86,8 @@ _RESTYPE = {"smes_last_error": C.c_char_p}
 # entry points that return a value rather than a status
 _VALUE_FNS = {"smes_abi_version", "smes_route_front_supported", "smes_fold_work_floats", "smes_fold_gemm_path", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_combine_fwd_f32_grid", "smes_last_error",
-              "smes_route_front_count_exact", "smes_route_count_exact", "smes_route_rt_supported"}
+              "smes_route_front_count_exact", "smes_route_count_exact", "smes_route_rt_supported",
+              "smes_plan_reduce_work_ints"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
 def _fold_gemm_path(E, T, d_out, d_in):      # csrc/fold.cu gemm_path()

@@ -45,10 +45,16 @@ def _raw_sums(routing: BatchRouting) -> torch.Tensor:
     dev = routing.umask.device
     i32 = torch.int32
     raw = torch.zeros(3 * E, dtype=torch.float64, device=dev)
+    # every scratch buffer stays referenced until the kernel is queued: a temporary freed inside the
+    # argument list could be handed out again by the caching allocator for the next one
+    scratch = [torch.zeros(C, E, dtype=i32, device=dev), torch.zeros(E, dtype=i32, device=dev),
+               torch.zeros(E + 1, dtype=i32, device=dev), torch.zeros(E + 1, dtype=i32, device=dev),
+               torch.zeros(3, dtype=i32, device=dev),
+               torch.zeros(call("smes_plan_reduce_work_ints", C, E), dtype=i32, device=dev)]
+    base, loads, seg_pad, seg_log, totals, work = scratch
     call("smes_plan_reduce", C, E, ptr(routing.chunk_union), ptr(routing.chunk_active), ptr(routing.chunk_mass),
-         ptr(routing.chunk_dmass), ptr(torch.zeros(C, E, dtype=i32, device=dev)), ptr(torch.zeros(E, dtype=i32, device=dev)),
-         ptr(raw), ptr(torch.zeros(E + 1, dtype=i32, device=dev)), ptr(torch.zeros(E + 1, dtype=i32, device=dev)),
-         ptr(torch.zeros(3, dtype=i32, device=dev)), ptr(torch.zeros(1, dtype=i32, device=dev)), None, _stream())
+         ptr(routing.chunk_dmass), ptr(base), ptr(loads), ptr(raw), ptr(seg_pad), ptr(seg_log), ptr(totals), ptr(work),
+         None, _stream())
     return raw
 
 

@@ -249,7 +249,7 @@ class SMESEngine:
         self.seg_pad = z(E + 1, dt=i32)
         self.seg_log = z(E + 1, dt=i32)
         self.totals = z(3, dt=i32)     # {0, padded rows, N_act}; [0:2] is the one-group segment table
-        self.ticket = z(1, dt=i32)
+        self.ticket = z(call("smes_plan_reduce_work_ints", self.C, E), dt=i32)
         self.flag = z(1, dt=i32)
         self.row_of = z(B, self.umax, dt=i32)
         self.gather_inst = rows["gather_inst"]

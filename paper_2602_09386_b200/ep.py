@@ -96,7 +96,7 @@ class EPRank:
         self.seg_pad = z(E + 1, dt=i32)
         self.seg_log = z(E + 1, dt=i32)
         self.totals = z(3, dt=i32)
-        self.ticket = z(1, dt=i32)
+        self.ticket = z(call("smes_plan_reduce_work_ints", self.C, E), dt=i32)
         self.flag = z(1, dt=i32)            # non-finite logits (route)
         self.cap_flag = z(1, dt=i32)        # owner plan exceeded the shard's row capacity
         self.seg_half = z(2 * E + 1, dt=i32)
@@ -167,7 +167,7 @@ class EPRank:
         self.seg_pad_o = z(El + 1, dt=i32)
         self.seg_log_o = z(El + 1, dt=i32)
         self.totals_o = z(3, dt=i32)
-        self.ticket_o = z(1, dt=i32)
+        self.ticket_o = z(call("smes_plan_reduce_work_ints", self.C_o, El), dt=i32)
         self.seg_half_o = z(2 * El + 1, dt=i32)
         self.row_of_o = z(Br, self.umax_l, dt=i32)
         self.shard = ExpertShard(p.layers, T, self.head_w32(), self.rows_own, dev, fuse_mlp=fuse_mlp)

@@ -148,7 +148,7 @@ def build_execution_plan(unions, num_experts: int, device=None) -> ExecutionPlan
     seg_pad = torch.zeros(E + 1, dtype=i32, device=dev)
     seg_log = torch.zeros(E + 1, dtype=i32, device=dev)
     totals = torch.zeros(3, dtype=i32, device=dev)
-    ticket = torch.zeros(1, dtype=i32, device=dev)
+    ticket = torch.zeros(call("smes_plan_reduce_work_ints", C, E), dtype=i32, device=dev)
     row_of = torch.zeros(max(B, 1), umax, dtype=i32, device=dev)
     gather_inst = torch.full((rows_cap,), -1, dtype=i32, device=dev)
     gather_exp = torch.zeros(rows_cap, dtype=i32, device=dev)

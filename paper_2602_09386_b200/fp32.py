@@ -93,7 +93,7 @@ class SMESForwardF32:
         self.seg_pad = z(E + 1, dt=i32)
         self.seg_log = z(E + 1, dt=i32)
         self.totals = z(3, dt=i32)
-        self.ticket = z(1, dt=i32)
+        self.ticket = z(call("smes_plan_reduce_work_ints", self.C, E), dt=i32)
         self.seg_half = z(2 * E + 1, dt=i32)
         self.flag = z(1, dt=i32)
         self.row_of = z(B, self.umax, dt=i32)
