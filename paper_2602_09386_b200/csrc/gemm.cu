@@ -17,6 +17,7 @@
 //
 // Warp roles (256 threads, 1 CTA/SM): w0 TMA producer, w1 MMA issuer,
 // w2 TMEM allocator, w4..w7 epilogue (warp q%4 owns TMEM lanes 32q..32q+31).
+#include <cstdlib>
 #include "ptx.cuh"
 #include "smes_capi.h"
 
@@ -402,6 +403,273 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc(tmem_base, S::kTmemCols);
 }
 
+// ============================================================================ CTA pairs
+// Ragged-M GEMM on CTA pairs (cta_group::2, cluster of 2): a unit is two 128-row tiles of the SAME
+// group (the second one empty when the group has an odd tile count) times a 256-wide N tile.  Each
+// CTA loads its own A tile and its 128-column half of the B tile; the leader issues M = 256 MMAs
+// that read both CTAs' smem, and every CTA drains its own 128 TMEM lanes.  Per CTA the B stream
+// is half of the single-CTA kernel's, so the large banks (c3 / c5 fc1, N >= 1024) are no longer
+// bound by the L2 -> SMEM fill rate (torch._grouped_mm ran the c3 fc1 10 % faster than the
+// single-CTA kernel).
+template <bool B_MN, bool F32>
+struct PairSmem {
+  static constexpr int BN = 256;
+  static constexpr int kStages = 4;
+  static constexpr int kA = BM * BK * 2;            // 16 KB: own 128 rows
+  static constexpr int kB = (BN / 2) * BK * 2;      // 16 KB: own half of the N tile
+  static constexpr int kStg = 32 * 128;
+  static constexpr int kOffB = kStages * kA;
+  static constexpr int kOffStg = kOffB + kStages * kB;
+  static constexpr int kOffBias = kOffStg + kEpiWarps * 2 * kStg;
+  static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
+  static constexpr int kOffSeg = kOffBar + 256;
+  static constexpr int kBytes = kOffSeg + 2 * 258 * 4 + 1024;
+  static_assert(kBytes <= 232448, "pair GEMM smem");
+};
+
+template <bool B_MN, bool F32>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    grouped_gemm_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                             const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  pdl_wait();
+  using S = PairSmem<B_MN, F32>;
+  constexpr int BN = S::BN;
+  constexpr int kStages = S::kStages;
+  constexpr int CPC = F32 ? 32 : 64;                 // output columns per 128-byte staged row chunk
+  constexpr int NCH = BN / CPC;
+  constexpr int MYCH = NCH / 2;
+  constexpr uint16_t kPair = 0x3;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::kOffB;
+  uint8_t* sStg = smem + S::kOffStg;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+  int* upref = seg_s + 258;                          // tile-pair units per group, prefix
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  for (int i = threadIdx.x; i <= args.G; i += blockDim.x) seg_s[i] = args.seg[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int u = 0;
+    for (int g = 0; g < args.G; ++g) {
+      upref[g] = u;
+      u += ((seg_s[g + 1] - seg_s[g]) / BM + 1) / 2;
+    }
+    upref[args.G] = u;
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmC); }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 2 * kEpiWarps); }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int n_tiles = (args.N + BN - 1) / BN;
+  const int num_units = upref[args.G] * n_tiles;
+  const int nkb = (args.K + BK - 1) / BK;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  // unit -> group, first row of the tile pair, tiles in the pair (1 or 2), n0
+  auto decode = [&](int u, int& g, int& rp, int& nt, int& n0) {
+    const int pu = u / n_tiles;
+    n0 = (u - pu * n_tiles) * BN;
+    int lo = 0, hi = args.G - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (upref[mid] <= pu) lo = mid; else hi = mid - 1;
+    }
+    g = lo;
+    const int j = pu - upref[g];
+    rp = seg_s[g] + 2 * j * BM;
+    nt = min(2, (seg_s[g + 1] - seg_s[g]) / BM - 2 * j);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer (both CTAs): own A tile, own half of the B tile
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cl; u < num_units; u += ncl) {
+        int g, rp, nt, n0;
+        decode(u, g, rp, nt, n0);
+        const bool valid = (int)rank < nt;
+        const int r0 = rp + (int)rank * BM;
+        const int nb = n0 + (int)rank * (BN / 2);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[stage], nt * S::kA + 2 * S::kB);
+          uint8_t* a = sA + stage * S::kA;
+          uint8_t* b = sB + stage * S::kB;
+          const int k0 = kb * BK;
+          if (valid) tma_load_2d_2sm(a, &tmA, &full[stage], k0, r0);                 // {64 k, 128 rows}
+          if (!B_MN) {
+            tma_load_3d_2sm(b, &tmB, &full[stage], k0, nb, g);                         // {64 k, 128 n, 1}
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) tma_load_3d_2sm(b + j * 8192, &tmB, &full[stage], nb + 64 * j, k0, g);
+          }
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ================= MMA issuer (leader): M = 256 over the pair, N = 256
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN, 0, B_MN ? 1 : 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = cl; u < num_units; u += ncl, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * S::kA);
+          const uint32_t b_addr = smem_u32(sB + stage * S::kB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? umma_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                                     : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+            tc_mma_f16_2sm(tmem_d, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit_2sm_mc(&empty[stage], kPair);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm_mc(&tfull[acc], kPair);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs): own 128 rows; releases the accumulator on the leader
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;
+    uint8_t* stg0 = sStg + (warp - 4) * 2 * S::kStg;
+    float* sbias = reinterpret_cast<float*>(smem + S::kOffBias) + (warp - 4) * 64;
+    const uint32_t lead_tempty0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t lead_tempty1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    const int ncols = args.N;
+    int it = 0, nstore = 0;
+    for (int u = cl; u < num_units; u += ncl, ++it) {
+      int g, rp, nt, n0;
+      decode(u, g, rp, nt, n0);
+      const bool valid = (int)rank < nt;
+      const int r0 = rp + (int)rank * BM;
+      const int row = r0 + 32 * q + lane;
+      uint32_t mw[MYCH][2];
+      float bv[MYCH][2];
+#pragma unroll
+      for (int i = 0; i < MYCH; ++i) {
+        const int n = n0 + (par + 2 * i) * CPC;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          mw[i][h] = 0u;
+          bv[i][h] = 0.f;
+          if (valid && h * 32 < CPC && n + 32 * h < ncols) {
+            if (args.bits_in != nullptr) mw[i][h] = __ldg(&args.bits_in[(size_t)((n >> 5) + h) * args.bits_ld + row]);
+            if (args.bias != nullptr && n + 32 * h + lane < ncols)
+              bv[i][h] = __ldg(args.bias + (size_t)g * args.N + n + 32 * h + lane);
+          }
+        }
+      }
+      const int acc = it & 1;
+      mbar_wait(&tfull[acc], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(32 * q) << 16) + acc * BN;
+#pragma unroll
+      for (int i = 0; i < MYCH; ++i) {
+        const int cc = par + 2 * i;
+        const int n = n0 + cc * CPC;
+        if (n >= ncols) break;
+        float f[CPC];
+#pragma unroll
+        for (int h = 0; h < CPC / 32; ++h) {
+          uint32_t t[32];
+          tmem_ld32(tbase + cc * CPC + 32 * h, t);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) f[32 * h + j] = __uint_as_float(t[j]);
+        }
+        if (!valid) continue;            // (warp-uniform: the whole CTA holds the pair's empty tile)
+        if (args.bias != nullptr) {
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < CPC / 32; ++h) sbias[32 * h + lane] = bv[i][h];
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < CPC; j += 4) {
+            const float4 bb = *reinterpret_cast<const float4*>(sbias + j);
+            f[j] += bb.x; f[j + 1] += bb.y; f[j + 2] += bb.z; f[j + 3] += bb.w;
+          }
+        }
+        if (args.act == 1) {
+#pragma unroll
+          for (int j = 0; j < CPC; ++j) f[j] = f[j] > 0.f ? f[j] : 0.f;
+        }
+        if (args.bits_out != nullptr) {
+#pragma unroll
+          for (int h = 0; h < CPC / 32; ++h) {
+            if (n + h * 32 < ncols) args.bits_out[(size_t)((n >> 5) + h) * args.bits_ld + row] = pos_mask32(f + h * 32);
+          }
+        }
+        if (args.bits_in != nullptr) {
+#pragma unroll
+          for (int h = 0; h < CPC / 32; ++h) {
+            const uint32_t w = mw[i][h];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) f[h * 32 + j] = ((w >> j) & 1u) ? f[h * 32 + j] : 0.f;
+          }
+        }
+        uint8_t* stg = stg0 + (nstore & 1) * S::kStg;
+        ++nstore;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          uint4 pk;
+          if (F32) {
+            pk = make_uint4(__float_as_uint(f[4 * c]), __float_as_uint(f[4 * c + 1]), __float_as_uint(f[4 * c + 2]),
+                            __float_as_uint(f[4 * c + 3]));
+          } else {
+            pk = make_uint4(pack_bf16(f[8 * c], f[8 * c + 1]), pack_bf16(f[8 * c + 2], f[8 * c + 3]),
+                            pack_bf16(f[8 * c + 4], f[8 * c + 5]), pack_bf16(f[8 * c + 6], f[8 * c + 7]));
+          }
+          rowp[c ^ (lane & 7)] = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tmC, stg, n, r0 + 32 * q);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? lead_tempty1 : lead_tempty0);
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, 2 * BN);
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -464,6 +732,32 @@ static int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap&
   return SMES_OK;
 }
 
+template <bool B_MN, bool F32>
+static int launch_pair(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const GemmArgs& args,
+                       cudaStream_t st) {
+  auto kern = grouped_gemm_pair_kernel<B_MN, F32>;
+  using SM = PairSmem<B_MN, F32>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::kBytes);
+    if (ea != cudaSuccess)
+      return set_error(SMES_ERR_CUDA, "grouped_gemm_pair smem attribute (%d B): %s", SM::kBytes, cudaGetErrorString(ea));
+    attr = true;
+  }
+  smes_launch(kern, num_sms() / 2 * 2, kThreads, SM::kBytes, st, a, b, c, args);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "grouped_gemm_pair launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+static bool pair_enabled() {
+  static const int on = [] {
+    const char* v = std::getenv("SMES_GEMM_PAIR");
+    return (v == nullptr || v[0] != '0') ? 1 : 0;
+  }();
+  return on != 0;
+}
+
 template <int BN>
 static int launch_m(bool b_mn, bool f32, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                     const GemmArgs& args, cudaStream_t st) {
@@ -519,6 +813,20 @@ int smes_gemm_ragged_m(const void* A, long lda, long rows_cap, const void* W, in
   GemmArgs args{seg, G, N, K, 0, bias, act, bits_out, bits_in, (int)bits_ld, nullptr, 0, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (narrow) return launch<32, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
+  // CTA pairs for the large banks (N a multiple of 256, many rows): half the B stream per CTA
+  if (pair_enabled() && N % 256 == 0 && K >= 256 && rows_cap >= 64L * 1024) {
+    CUtensorMap tb2;
+    if (!b_mn) {  // W (G, N, K) K-major, box {64 k, 128 n, 1}: each CTA its half of the 256-wide tile
+      uint64_t dims[3] = {(uint64_t)K, (uint64_t)N, (uint64_t)G};
+      uint64_t str[2] = {(uint64_t)K * 2, (uint64_t)N * K * 2};
+      uint32_t box[3] = {64, 128, 1};
+      if ((rc = make_map(&tb2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, W, dims, str, box))) return rc;
+    } else {
+      tb2 = tb;    // MN-major boxes are {64 n, 64 k, 1} already
+    }
+    if (b_mn) return out_fp32 ? launch_pair<true, true>(ta, tb2, tc, args, st) : launch_pair<true, false>(ta, tb2, tc, args, st);
+    return out_fp32 ? launch_pair<false, true>(ta, tb2, tc, args, st) : launch_pair<false, false>(ta, tb2, tc, args, st);
+  }
   // K-major B box is {64, 256} for N >= 256: requires BN == 256
   if (N >= 256) return launch_m<256>(b_mn, out_fp32, ta, tb, tc, args, st);
   return launch_m<128>(b_mn, out_fp32, ta, tb, tc, args, st);

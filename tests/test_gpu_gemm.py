@@ -245,3 +245,55 @@ def test_ragged_k_wgrad_narrow(I, J):
             assert torch.all(out[e] == 0)
             continue
         assert (out[e] - ref).abs().max().item() / ref.abs().max().item() < 1e-5
+
+
+@pytest.mark.parametrize("N,K,b_mn,act,f32", [(1024, 512, 0, 1, 0), (512, 1024, 1, 0, 0), (256, 256, 0, 0, 1),
+                                              (768, 256, 1, 0, 1)])
+def test_ragged_m_cta_pairs(N, K, b_mn, act, f32):
+    """The CTA-pair kernel (cta_group::2, taken for N % 256 == 0, K >= 256 and >= 64 K rows): odd
+    and even tile counts per group (a pair's second tile empty), empty groups, bias + relu + mask
+    (forward), the relu mask applied to the output (dgrad, MN-major B), bf16 and fp32 outputs."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(N + K + b_mn)
+    loads = [20000, 0, 129, 17000, 128, 30517, 1]          # 157, 0, 2, 133, 1, 239, 1 tiles
+    E = len(loads)
+    seg, x = _packed(loads, K, g, dev)
+    R = x.shape[0]
+    assert R >= 64 * 1024
+    xb = x.to(torch.bfloat16).contiguous()
+    if b_mn:
+        w = (torch.randn(E, K, N, generator=g, device=dev) / K ** 0.5).to(torch.bfloat16).contiguous()
+        weff = w.float()                                      # (E, K, N): out = x w
+    else:
+        w = (torch.randn(E, N, K, generator=g, device=dev) / K ** 0.5).to(torch.bfloat16).contiguous()
+        weff = w.float().transpose(1, 2)
+    b = torch.randn(E, N, generator=g, device=dev).contiguous() if not b_mn else None
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    odt = torch.float32 if f32 else torch.bfloat16
+    out = torch.full((R, N), float("nan"), device=dev).to(odt)
+    bits_out = torch.zeros(N // 32, R, dtype=torch.int32, device=dev) if act else None
+    mask_in = torch.randint(0, 2 ** 31, (N // 32, R), generator=g, device=dev, dtype=torch.int32) if b_mn else None
+    call("smes_gemm_ragged_m", ptr(xb), K, R, ptr(w), E, N, K, b_mn, ptr(seg_t), ptr(b), act, ptr(bits_out),
+         ptr(mask_in), R, ptr(out), N, int(f32), R, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, n = seg[e], loads[e]
+        if n == 0:
+            continue
+        ref = xb[lo:lo + n].float() @ weff[e]
+        if b is not None:
+            ref = ref + b[e]
+        if act:
+            ref = ref.clamp_min(0)
+        if mask_in is not None:
+            m = ((mask_in[:, lo:lo + n].T.long().unsqueeze(2) >> torch.arange(32, device=dev)) & 1).reshape(n, N)
+            ref = ref * m
+        got = out[lo:lo + n].float()
+        err = (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
+        assert err < 1e-2, (e, err)
+        if bits_out is not None:
+            word = bits_out[:, lo:lo + n].T.contiguous()
+            expect = got > 0
+            for j in range(N // 32):
+                mm = ((word[:, j:j + 1].long() >> torch.arange(32, device=dev)) & 1).bool()
+                assert torch.equal(mm, expect[:, 32 * j:32 * j + 32])
