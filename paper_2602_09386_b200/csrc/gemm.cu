@@ -670,6 +670,211 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem_base, 2 * BN);
 }
 
+// Ragged-K (weight gradient) on CTA pairs: C_g[i, j] = sum_{m in g} P[m, i] Q[m, j] with a unit =
+// (group, two 128-row i tiles, 256-wide j tile); each CTA loads its own i tile of P (MN-major) and
+// its half of the j tile of Q (MN-major), the leader's M = 256 MMAs run the group's whole K range.
+// db_g[i] = sum_m P[m, i] (the fused bias gradient) comes from a second N = 16 MMA against a
+// constant ones operand (K-major: row n = 0 of the leader's half is all ones), TMEM columns
+// BN .. BN + 15, on the unit's first j tile.
+struct PairKSmem {
+  static constexpr int BN = 256;
+  static constexpr int kStages = 5;
+  static constexpr int kA = BM * BK * 2;            // 16 KB: own 128 i x 64 k (2 MN-major boxes)
+  static constexpr int kB = (BN / 2) * BK * 2;      // 16 KB: own 128 j x 64 k
+  static constexpr int kStg = 32 * 128;
+  static constexpr int kOffB = kStages * kA;
+  static constexpr int kOffOnes = kOffB + kStages * kB;           // 1 KB: 8 n rows x 64 k, K-major SW128
+  static constexpr int kOffStg = kOffOnes + 1024;
+  static constexpr int kOffBar = kOffStg + kEpiWarps * kStg;
+  static constexpr int kOffSeg = kOffBar + 256;
+  static constexpr int kBytes = kOffSeg + 258 * 4 + 1024;
+  static_assert(kBytes <= 232448, "pair ragged-K smem");
+};
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    grouped_gemm_pair_k_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                               const __grid_constant__ CUtensorMap tmC, const GemmArgs args) {
+  pdl_wait();
+  using S = PairKSmem;
+  constexpr int BN = S::BN;
+  constexpr int kStages = S::kStages;
+  constexpr int CPC = 32;                            // fp32 output: 32 columns per 128-byte row chunk
+  constexpr int NCH = BN / CPC;
+  constexpr int MYCH = NCH / 2;
+  constexpr uint16_t kPair = 0x3;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S::kOffB;
+  uint8_t* sOnes = smem + S::kOffOnes;
+  uint8_t* sStg = smem + S::kOffStg;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+  int* seg_s = reinterpret_cast<int*>(smem + S::kOffSeg);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool fused_bias = args.db_out != nullptr;
+  for (int i = threadIdx.x; i <= args.G; i += blockDim.x) seg_s[i] = args.seg[i];
+  {  // ones operand: K-major, 8 n rows of 64 k (one SW128 atom); n = 0 of the leader's half is 1.0
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(sOnes);
+    const uint32_t one2 = rank == 0 ? 0x3F803F80u : 0u;            // two bf16 1.0
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) o32[i] = (i < 32) ? one2 : 0u;   // row 0 = 128 B
+    fence_proxy_async_smem();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); tma_prefetch(&tmC); }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * kEpiWarps);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int i_tiles = (args.I + BM - 1) / BM;
+  const int i_pairs = (i_tiles + 1) / 2;
+  const int j_tiles = (args.N + BN - 1) / BN;
+  const int per_g = i_pairs * j_tiles;
+  const int num_units = args.G * per_g;
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  auto decode = [&](int u, int& g, int& i0, int& ni, int& j0, int& kb0, int& nkb) {
+    g = u / per_g;
+    const int r = u - g * per_g;
+    const int ip = r / j_tiles;
+    j0 = (r - ip * j_tiles) * BN;
+    i0 = ip * 2 * BM;
+    ni = min(2, i_tiles - 2 * ip);
+    kb0 = seg_s[g] / BK;
+    nkb = (seg_s[g + 1] - seg_s[g]) / BK;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ================= TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = cl; u < num_units; u += ncl) {
+        int g, i0, ni, j0, kb0, nkb;
+        decode(u, g, i0, ni, j0, kb0, nkb);
+        const bool valid = (int)rank < ni;
+        const int ia = i0 + (int)rank * BM;
+        const int jb = j0 + (int)rank * (BN / 2);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_expect_tx(&full[stage], ni * S::kA + 2 * S::kB);
+          uint8_t* a = sA + stage * S::kA;
+          uint8_t* b = sB + stage * S::kB;
+          const int k0 = (kb0 + kb) * BK;
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) tma_load_2d_2sm(a + j * 8192, &tmA, &full[stage], ia + 64 * j, k0);
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j) tma_load_2d_2sm(b + j * 8192, &tmB, &full[stage], jb + 64 * j, k0);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ================= MMA issuer (leader)
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, BN, 1, 1);
+      constexpr uint32_t idesc_bias = umma_idesc_bf16(2 * BM, 16, 1, 0);
+      const uint32_t ones_addr = smem_u32(sOnes);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = cl; u < num_units; u += ncl, ++it) {
+        int g, i0, ni, j0, kb0, nkb;
+        decode(u, g, i0, ni, j0, kb0, nkb);
+        mbar_wait(tempty, (it & 1) ^ 1);
+        tc_fence_after();
+        const bool with_bias = fused_bias && j0 == 0;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * S::kA);
+          const uint32_t b_addr = smem_u32(sB + stage * S::kB);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = umma_desc_sw128(a_addr + k * 2048, 8192, 1024);
+            tc_mma_f16_2sm(tmem_base, ad, umma_desc_sw128(b_addr + k * 2048, 8192, 1024), idesc, (kb | k) != 0);
+            if (with_bias)
+              tc_mma_f16_2sm(tmem_base + BN, ad, umma_desc_sw128(ones_addr + k * 32, 16, 1024), idesc_bias,
+                             (kb | k) != 0);
+          }
+          tc_commit_2sm_mc(&empty[stage], kPair);
+          if (++stage == kStages) { stage = 0; phase ^= 1; }
+        }
+        tc_commit_2sm_mc(tfull, kPair);     // (also fires for an empty group: the epilogue writes zeros)
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= epilogue (both CTAs): own 128 i rows of C_g (fp32)
+    const int q = warp & 3;
+    const int par = (warp - 4) >> 2;
+    uint8_t* stg = sStg + (warp - 4) * S::kStg;
+    const uint32_t lead_tempty = mapa_shared(smem_u32(tempty), 0);
+    int it = 0;
+    for (int u = cl; u < num_units; u += ncl, ++it) {
+      int g, i0, ni, j0, kb0, nkb;
+      decode(u, g, i0, ni, j0, kb0, nkb);
+      const bool valid = (int)rank < ni;
+      const int ia = i0 + (int)rank * BM;
+      const int row = ia + 32 * q + lane;       // output row i
+      mbar_wait(tfull, it & 1);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(32 * q) << 16);
+      if (fused_bias && j0 == 0 && par == 0) {
+        uint32_t t0[32];
+        tmem_ld32(tbase + BN, t0);
+        tmem_ld_wait();
+        if (valid && row < args.I) args.db_out[(size_t)g * args.I + row] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
+      }
+#pragma unroll
+      for (int i = 0; i < MYCH; ++i) {
+        const int cc = par + 2 * i;
+        const int n = j0 + cc * CPC;
+        if (n >= args.N) break;
+        uint32_t t[32];
+        tmem_ld32(tbase + cc * CPC, t);
+        tmem_ld_wait();
+        if (!valid) continue;
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        uint4* rowp = reinterpret_cast<uint4*>(stg + lane * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint4 pk = nkb > 0 ? make_uint4(t[4 * c], t[4 * c + 1], t[4 * c + 2], t[4 * c + 3]) : make_uint4(0, 0, 0, 0);
+          rowp[c ^ (lane & 7)] = pk;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&tmC, stg, n, ia + 32 * q, g);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lead_tempty);
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  if (warp == 2) tmem_dealloc_2sm(tmem_base, 512);
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -892,6 +1097,24 @@ int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void
   }
   GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out, a_period, 0};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // CTA pairs for the large wgrad banks (I spans >= 2 i tiles, J >= 256, many rows)
+  // measured neutral at c3 under the power cap (fc1 wgrad 1.84 / 1.83 ms paired vs 1.89 / 1.79 ms,
+  // tools/ab_pairk.sh): off unless SMES_GEMM_PAIR_K=1
+  const char* pk_env = std::getenv("SMES_GEMM_PAIR_K");
+  const bool pair_k = pk_env != nullptr && pk_env[0] == '1';
+  if (pair_enabled() && pair_k && a_period == 0 && I >= 2 * BM && J >= 256 && rows_cap >= 64L * 1024) {
+    auto kern = grouped_gemm_pair_k_kernel;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, PairKSmem::kBytes);
+      if (ea != cudaSuccess) return set_error(SMES_ERR_CUDA, "pair ragged-K smem attribute: %s", cudaGetErrorString(ea));
+      attr = true;
+    }
+    smes_launch(kern, num_sms() / 2 * 2, kThreads, PairKSmem::kBytes, st, ta, tb, tc, args);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "pair ragged-K launch: %s", cudaGetErrorString(e));
+    return SMES_OK;
+  }
   if (J <= 16) return launch<16, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
   // BN = 256 halves the tile count; with a single i-tile (I <= 128: the folded-head wgrad) keep
   // it only while the grid still covers every SM

@@ -297,3 +297,42 @@ def test_ragged_m_cta_pairs(N, K, b_mn, act, f32):
             for j in range(N // 32):
                 mm = ((word[:, j:j + 1].long() >> torch.arange(32, device=dev)) & 1).bool()
                 assert torch.equal(mm, expect[:, 32 * j:32 * j + 32])
+
+
+@pytest.mark.parametrize("I,J,bias", [(1024, 576, True), (384, 320, True), (512, 256, False)])
+def test_ragged_k_wgrad_cta_pairs(I, J, bias, monkeypatch):
+    """The CTA-pair wgrad (SMES_GEMM_PAIR_K=1; I >= 256, J >= 256 and >= 64 K rows): i-tile pairs with an empty
+    second tile (I = 384), partial j tiles (J = 576, 320), empty groups, the fused bias column."""
+    monkeypatch.setenv("SMES_GEMM_PAIR_K", "1")
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(11 * I + J)
+    loads = [30000, 0, 77, 36000, 128, 1]
+    E = len(loads)
+    seg, pm = _packed(loads, I, g, dev)
+    _, qm = _packed(loads, J, g, dev)
+    R = pm.shape[0]
+    assert R >= 64 * 1024
+    pb = pm.to(torch.bfloat16)
+    qb = torch.zeros(R, J + 64, dtype=torch.bfloat16, device=dev)
+    qb[:, :J] = qm.to(torch.bfloat16)
+    qb[:, J] = 1.0
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    out = torch.full((E, I, J), float("nan"), device=dev)
+    db = torch.full((E, I), float("nan"), device=dev) if bias else None
+    call("smes_gemm_ragged_k", ptr(pb), I, ptr(qb), J + 64, R, E, I, J, ptr(seg_t), ptr(out), ptr(db),
+         torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    for e in range(E):
+        lo, hi = seg[e], seg[e + 1]
+        ref = pb[lo:hi].float().T @ qb[lo:hi, :J].float()
+        if loads[e] == 0:
+            assert torch.all(out[e] == 0)
+            if bias:
+                assert torch.all(db[e] == 0)
+            continue
+        # fp32 accumulation over up to 36 K rows: ~1e-4 of the largest entry (the single-CTA kernel
+        # gives the same error on these operands)
+        assert (out[e] - ref).abs().max().item() / ref.abs().max().item() < 3e-4, e
+        if bias:
+            refb = pb[lo:hi].float().sum(0)
+            assert (db[e] - refb).abs().max().item() / refb.abs().max().item() < 3e-4, e
