@@ -120,6 +120,17 @@ int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32
 /* int32 elements of the ``ticket`` work buffer smes_plan_reduce / smes_plan_reduce_stats need
  * (zero-initialised once by the caller; the kernels keep it replay-safe themselves). */
 int smes_plan_reduce_work_ints(int C, int E);
+/* plan reduce + LoadStats finalize (as smes_plan_reduce_stats) and the head fold of a training
+ * step (as smes_fold_heads) in one launch, for the shapes smes_fold_full_supported accepts (the
+ * fold's blocks run in the slack of the reduce's E column-scan blocks). */
+int smes_fold_full_supported(int E, int T, int ldg, int d_out, int d_in);
+int smes_plan_reduce_stats_fold(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
+                                const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base,
+                                int32_t* loads, double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
+                                unsigned int* ticket, int32_t* seg_half, int K, int lb_experts,
+                                double batch_times_tasks, int dense, double* stats_out, float* freq_f32, int T,
+                                int ldg, int d_out, int d_in, const float* head_w, const void* W, const float* b,
+                                void* G, float* c, void* stream);
 int smes_plan_counts(int B, int E, int rows_per_warp, const uint32_t* umask, int32_t* chunk_union, int32_t* usize,
                      void* stream);
 int smes_plan_scatter(int B, int E, int d, int rows_per_warp, const uint32_t* umask, const int32_t* chunk_base,

@@ -31,6 +31,9 @@ SIGNATURES = {
     "smes_route_front_count_exact": [P],
     "smes_route_count_exact": [P],
     "smes_plan_reduce_work_ints": [I, I],
+    "smes_fold_full_supported": [I, I, I, I, I],
+    "smes_plan_reduce_stats_fold": [I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, I, D, I, P, P, I, I, I, I, P, P, P, P, P,
+                                    P],
     "smes_route_rt_supported": [I, I, I, I],
     "smes_route_rt": [P, L, L, P, I, I, I, I, I, I, P, P, P, P, P, P, P, P, P, P, P, P],
     "smes_peer_allreduce_f64": [I, I, I, P, P, P, P, P, P, P, P],
@@ -87,7 +90,7 @@ _RESTYPE = {"smes_last_error": C.c_char_p}
 _VALUE_FNS = {"smes_abi_version", "smes_route_front_supported", "smes_fold_work_floats", "smes_fold_gemm_path", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_combine_fwd_f32_grid", "smes_last_error",
               "smes_route_front_count_exact", "smes_route_count_exact", "smes_route_rt_supported",
-              "smes_plan_reduce_work_ints"}
+              "smes_plan_reduce_work_ints", "smes_fold_full_supported"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
 def _fold_gemm_path(E, T, d_out, d_in):      # csrc/fold.cu gemm_path()
@@ -114,7 +117,8 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_all
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
                     "smes_ep_copy_rows_put": 1, "smes_gemm_ragged_m_x3": 1, "smes_split_bf16x3": 1,
-                    "smes_combine_fwd_f32": 1, "smes_route_rt": 1}
+                    "smes_combine_fwd_f32": 1, "smes_route_rt": 1,
+                    "smes_plan_reduce_stats_fold": 1}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 trace = None    # optional list: every successful call appends (tag, kernels launched) -- ncu launch tags

@@ -23,6 +23,7 @@
 #include <stdint.h>
 
 #include "ptx.cuh"
+#include "fold_full.cuh"
 #include "smes_capi.h"
 
 namespace smes {
@@ -103,10 +104,6 @@ __global__ void __launch_bounds__(128) fold_tile_kernel(int T, int ldg, int d_ou
                            q_ks, W, part);
 }
 
-// Single-launch fold for d_out <= 256 (the c1/c2 shapes): a block owns (64 columns k, expert e),
-// loads all of W_e[:, k-tile] (d_out x 64 bf16, one memory latency) and head_w, and reduces over
-// the full d_out -- no split partials, no finish pass.  Blocks with k-tile 0 also write c_e.
-constexpr int FOLD_FULL_MAX_DOUT = 256;
 template <int TM>
 __global__ void __launch_bounds__(256) fold_full_kernel(int T, int ldg, int d_out, int d_in,
                                                         const float* __restrict__ head_w,
@@ -114,65 +111,8 @@ __global__ void __launch_bounds__(256) fold_full_kernel(int T, int ldg, int d_ou
                                                         const float* __restrict__ b, __nv_bfloat16* __restrict__ G,
                                                         float* __restrict__ c) {
   pdl_wait();
-  // W tile (d_out x 64 bf16, padded rows); reused as the [8][TM][64] fp32 group-sum buffer
-  __shared__ __align__(16) __nv_bfloat16 sW[FOLD_FULL_MAX_DOUT][72];
-  static_assert(FOLD_FULL_MAX_DOUT * 72 * 2 >= 8 * TM * 64 * 4, "fold_full reduction buffer");
-  __shared__ float sX[TM][FOLD_FULL_MAX_DOUT + 4];
-  const int e = blockIdx.y, k0 = blockIdx.x * 64, tid = threadIdx.x;
-  const __nv_bfloat16* We = W + (size_t)e * d_out * d_in;
-  for (int idx = tid; idx < d_out * 8; idx += 256) {
-    const int row = idx >> 3, cg = (idx & 7) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (k0 + cg < d_in) v = __ldg(reinterpret_cast<const uint4*>(We + (size_t)row * d_in + k0 + cg));
-    *reinterpret_cast<uint4*>(&sW[row][cg]) = v;
-  }
-  for (int i = tid; i < TM * d_out; i += 256) {
-    const int t = i / d_out, j = i - t * d_out;
-    sX[t][j] = t < T ? head_w[(size_t)t * d_out + j] : 0.f;
-  }
-  __syncthreads();
-  // thread = (column pair cp, j-group g): all TM tasks for 2 columns over d_out/8 rows j, then a
-  // fixed-order sum of the 8 j-groups through shared memory
-  const int cp = tid & 31, g = tid >> 5;
-  const int jn = (d_out + 7) / 8, ja = g * jn, jb = min(d_out, ja + jn);
-  float acc[TM][2];
-#pragma unroll
-  for (int t = 0; t < TM; ++t) { acc[t][0] = 0.f; acc[t][1] = 0.f; }
-  for (int j = ja; j < jb; ++j) {
-    const float2 w = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&sW[j][2 * cp]));
-#pragma unroll
-    for (int t = 0; t < TM; ++t) {
-      const float x = sX[t][j];
-      acc[t][0] = fmaf(x, w.x, acc[t][0]);
-      acc[t][1] = fmaf(x, w.y, acc[t][1]);
-    }
-  }
-  __syncthreads();                                           // sW is reused as the reduction buffer
-  float* red = reinterpret_cast<float*>(&sW[0][0]);          // [8 groups][TM][64]
-#pragma unroll
-  for (int t = 0; t < TM; ++t) {
-    red[(g * TM + t) * 64 + 2 * cp] = acc[t][0];
-    red[(g * TM + t) * 64 + 2 * cp + 1] = acc[t][1];
-  }
-  __syncthreads();
-  for (int i = tid; i < TM * 64; i += 256) {
-    const int t = i >> 6, col = i & 63;
-    float v = 0.f;
-#pragma unroll
-    for (int gg = 0; gg < 8; ++gg) v += red[(gg * TM + t) * 64 + col];
-    if (t < ldg && k0 + col < d_in) G[((size_t)e * ldg + t) * d_in + k0 + col] = __float2bfloat16_rn(v);
-  }
-  if (blockIdx.x == 0) {
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int t = warp; t < ldg; t += 8) {
-      float s = 0.f;
-      if (t < T)
-        for (int j = lane; j < d_out; j += 32) s = fmaf(sX[t][j], b[(size_t)e * d_out + j], s);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) c[(size_t)e * ldg + t] = s;
-    }
-  }
+  extern __shared__ __align__(16) uint8_t fsm[];
+  fold_full_body<TM>(blockIdx.x, blockIdx.y, T, ldg, d_out, d_in, head_w, W, b, G, c, fsm);
 }
 
 // G[e, t, k] = sum_s part[s, e, t, k] (bf16, rows >= T zero);  c[e, t] = head_w[t] . b[e]
@@ -439,6 +379,11 @@ static FoldWork fold_layout(int E, int T, int d_out, int d_in) {
 
 int smes_fold_gemm_path(int E, int T, int d_out, int d_in) { return gemm_path(E, T, d_out, d_in) ? 1 : 0; }
 
+int smes_fold_full_supported(int E, int T, int ldg, int d_out, int d_in) {
+  return !gemm_path(E, T, d_out, d_in) && d_out <= FOLD_FULL_MAX_DOUT && T >= 1 && T <= 8 && ldg <= 8 && ldg >= T &&
+         d_in % 8 == 0 && E >= 1;
+}
+
 int smes_fold_work_floats(int E, int T, int d_out, int d_in) {
   const int tm = fold_tm(T);
   const long a = (long)((d_out + 63) / 64) * E * tm * d_in;       // fold partials (CUDA-core path)
@@ -474,7 +419,8 @@ int smes_fold_heads(int E, int T, int ldg, int d_out, int d_in, const float* hea
     smes_launch(fold_convert_kernel, (int)(blocks > need ? blocks : need), 256, 0, st, E, T, ldg, d_out, d_in, Gf, head_w, b,
                                                                                Gb, c);
   } else if (d_out <= FOLD_FULL_MAX_DOUT && T <= 8 && ldg <= 8) {
-    smes_launch(fold_full_kernel<8>, dim3((d_in + 63) / 64, E), 256, 0, st, T, ldg, d_out, d_in, head_w, Wb, b, Gb, c);
+    smes_launch(fold_full_kernel<8>, dim3((d_in + 63) / 64, E), 256, fold_full_smem_bytes<8>(), st, T, ldg, d_out, d_in,
+                head_w, Wb, b, Gb, c);
   } else {
     const int splits = (d_out + 63) / 64;
     dim3 grid((d_in + 63) / 64, E, splits);

@@ -13,6 +13,7 @@
 // (zero rows) so GEMM tiles never straddle experts; logical offsets are kept
 // alongside for the reference-facing ExecutionPlan view.
 #include "ptx.cuh"
+#include "fold_full.cuh"
 #include "smes_capi.h"
 
 namespace smes {
@@ -25,7 +26,7 @@ constexpr int SEG_ALIGN = 128;
 // its cross-block flag / aggregate round trips cost more than the column loads save.)  The last block to
 // finish derives the padded / logical segment offsets (ticket counter, reset
 // in-kernel so the kernel is CUDA-graph replayable).
-__global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ chunk_union,
+__device__ __forceinline__ void chunk_reduce_body(int nblocks, int e, int C, int E, const int32_t* __restrict__ chunk_union,
                                     const int32_t* __restrict__ chunk_active, const double* __restrict__ chunk_mass,
                                     const double* __restrict__ chunk_dmass, int32_t* __restrict__ chunk_base,
                                     int32_t* __restrict__ loads, double* __restrict__ stats_raw,
@@ -33,8 +34,6 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
                                     int32_t* __restrict__ totals, unsigned int* __restrict__ ticket,
                                     int32_t* __restrict__ seg_half, double lb_scale, double bt, int dense,
                                     double* __restrict__ st_out, float* __restrict__ freq_f32) {
-  pdl_wait();
-  const int e = blockIdx.x;
   __shared__ int32_t warp_tot[32];
   __shared__ double red[3][32];
   __shared__ bool is_last;
@@ -130,7 +129,7 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
     stats_raw[2 * E + e] = dm;   // dense mass sum
     __threadfence();
     unsigned int t = atomicAdd(ticket, 1u);
-    is_last = (t == (unsigned)(gridDim.x - 1));
+    is_last = (t == (unsigned)(nblocks - 1));
   }
   __syncthreads();
   if (!is_last) return;
@@ -183,6 +182,51 @@ __global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ ch
       st_out[3 * E] = lb_scale * v;     // (E / K) <f, p>
     }
   }
+}
+
+__global__ void chunk_reduce_kernel(int C, int E, const int32_t* __restrict__ chunk_union,
+                                    const int32_t* __restrict__ chunk_active, const double* __restrict__ chunk_mass,
+                                    const double* __restrict__ chunk_dmass, int32_t* __restrict__ chunk_base,
+                                    int32_t* __restrict__ loads, double* __restrict__ stats_raw,
+                                    int32_t* __restrict__ seg_pad, int32_t* __restrict__ seg_log,
+                                    int32_t* __restrict__ totals, unsigned int* __restrict__ ticket,
+                                    int32_t* __restrict__ seg_half, double lb_scale, double bt, int dense,
+                                    double* __restrict__ st_out, float* __restrict__ freq_f32) {
+  pdl_wait();
+  chunk_reduce_body(gridDim.x, blockIdx.x, C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
+                    stats_raw, seg_pad, seg_log, totals, ticket, seg_half, lb_scale, bt, dense, st_out, freq_f32);
+}
+
+// The plan reduce (blocks [0, E)) and the head fold of a training step (blocks [E, E + nx E),
+// fold_full.cuh) in one launch: the reduce's E column-scan blocks leave most SMs idle, so the
+// fold (which depends on the weights only) runs in that slack instead of as its own kernel on
+// the forward's critical path.
+struct FoldArgsPR {
+  int T, ldg, d_out, d_in;
+  const float* head_w;
+  const __nv_bfloat16* W;
+  const float* b;
+  __nv_bfloat16* G;
+  float* c;
+};
+__global__ void __launch_bounds__(256)
+    plan_reduce_fold_kernel(int C, int E, const int32_t* __restrict__ chunk_union, const int32_t* __restrict__ chunk_active,
+                            const double* __restrict__ chunk_mass, const double* __restrict__ chunk_dmass,
+                            int32_t* __restrict__ chunk_base, int32_t* __restrict__ loads, double* __restrict__ stats_raw,
+                            int32_t* __restrict__ seg_pad, int32_t* __restrict__ seg_log, int32_t* __restrict__ totals,
+                            unsigned int* __restrict__ ticket, int32_t* __restrict__ seg_half, double lb_scale,
+                            double bt, int dense, double* __restrict__ st_out, float* __restrict__ freq_f32,
+                            const FoldArgsPR f) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint8_t fsm[];
+  if ((int)blockIdx.x >= E) {
+    const int nx = (f.d_in + 63) / 64;
+    const int k = blockIdx.x - E;
+    fold_full_body<8>(k % nx, k / nx, f.T, f.ldg, f.d_out, f.d_in, f.head_w, f.W, f.b, f.G, f.c, fsm);
+    return;
+  }
+  chunk_reduce_body(E, blockIdx.x, C, E, chunk_union, chunk_active, chunk_mass, chunk_dmass, chunk_base, loads,
+                    stats_raw, seg_pad, seg_log, totals, ticket, seg_half, lb_scale, bt, dense, st_out, freq_f32);
 }
 
 // grid = C + E blocks.  Blocks < C: stable scatter of chunk c's (instance, expert)
@@ -364,6 +408,36 @@ int smes_plan_reduce_stats(int C, int E, const int32_t* chunk_union, const int32
               (double)(lb_experts > 0 ? lb_experts : E) / (double)K, batch_times_tasks, dense, stats_out, freq_f32);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce launch: %s", cudaGetErrorString(e));
+  return SMES_OK;
+}
+
+int smes_plan_reduce_stats_fold(int C, int E, const int32_t* chunk_union, const int32_t* chunk_active,
+                                const double* chunk_mass, const double* chunk_dmass, int32_t* chunk_base,
+                                int32_t* loads, double* stats_raw, int32_t* seg_pad, int32_t* seg_log, int32_t* totals,
+                                unsigned int* ticket, int32_t* seg_half, int K, int lb_experts,
+                                double batch_times_tasks, int dense, double* stats_out, float* freq_f32, int T,
+                                int ldg, int d_out, int d_in, const float* head_w, const void* W, const float* b,
+                                void* G, float* c, void* stream) {
+  if (E > 1024) return set_error(SMES_ERR_SHAPE, "plan: E=%d exceeds 1024", E);
+  if (K < 1 || batch_times_tasks <= 0.0) return set_error(SMES_ERR_CONFIG, "plan_reduce_stats: K=%d B*T=%g", K,
+                                                          batch_times_tasks);
+  if (!smes_fold_full_supported(E, T, ldg, d_out, d_in))
+    return set_error(SMES_ERR_SHAPE, "plan_reduce_stats_fold: fold shape T=%d ldg=%d d_out=%d d_in=%d", T, ldg, d_out,
+                     d_in);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const FoldArgsPR f{T, ldg, d_out, d_in, head_w, reinterpret_cast<const __nv_bfloat16*>(W), b,
+                     reinterpret_cast<__nv_bfloat16*>(G), c};
+  const int nfold = ((d_in + 63) / 64) * E;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(plan_reduce_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fold_full_smem_bytes<8>());
+    attr = true;
+  }
+  smes_launch(plan_reduce_fold_kernel, E + nfold, 256, fold_full_smem_bytes<8>(), st, C, E, chunk_union, chunk_active,
+              chunk_mass, chunk_dmass, chunk_base, loads, stats_raw, seg_pad, seg_log, totals, ticket, seg_half,
+              (double)(lb_experts > 0 ? lb_experts : E) / (double)K, batch_times_tasks, dense, stats_out, freq_f32, f);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "plan_reduce_fold launch: %s", cudaGetErrorString(e));
   return SMES_OK;
 }
 

@@ -211,6 +211,7 @@ class SMESEngine:
         self.serial = False
         # measured 0.531 vs 0.529 ms at c2 with the fold on the side stream (tools/ab_fold.sh): off by default
         self.fold_side = os.environ.get("SMES_FOLD_SIDE", "0") == "1"
+        self.fold_in_reduce = False        # set in _alloc once the fold buffers exist
         self._alloc()
         self.refresh_weights()
 
@@ -302,6 +303,8 @@ class SMESEngine:
                 self.q_strides = (self.q_rows * self.ldg, 1, self.ldg)
             self.csum_q = z(E, self.ldg)                    # per-expert column sums of C
             self.fold_work = z(call("smes_fold_work_floats", E, T, self.d_out, di))
+            self.fold_in_reduce = bool(call("smes_fold_full_supported", E, T, self.ldg, self.d_out, di)) and \
+                os.environ.get("SMES_FOLD_IN_REDUCE", "1") == "1"
         self.seg_half = z(2 * E + 1, dt=i32)
         self.logits = z(T, B)
         self.preds = z(T, B)
@@ -465,7 +468,19 @@ class SMESEngine:
             self._fold(self._side.cuda_stream)
             self._fold_ev = torch.cuda.Event()
             self._fold_ev.record(self._side)
-        if finalize_stats:
+        fold_now = bool(fold and refold and self.can_fold and self._fold_ev is None and self.fold_in_reduce)
+        self._folded_in_reduce = False
+        if finalize_stats and fold_now:
+            # plan reduce + LoadStats finalize + the head fold in one launch (the fold's blocks run in
+            # the slack of the reduce's E column scans instead of as their own kernel)
+            _tagged("plan_reduce", "smes_plan_reduce_stats_fold", self.C, E, ptr(self.chunk_union),
+                    ptr(self.chunk_active), ptr(self.chunk_mass), ptr(self.chunk_dmass), ptr(self.chunk_base),
+                    ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad), ptr(self.seg_log), ptr(self.totals),
+                    ptr(self.ticket), ptr(self.seg_half), self.K, self.E_lb, float(B * T), int(self.dense),
+                    ptr(self.stats_out), ptr(self.freq32), T, self.ldg, self.d_out, self.dims[-2], ptr(self.head_w),
+                    ptr(self.w_bf[-1]), ptr(self.b32[-1]), ptr(self.G_fold), ptr(self.c_fold), s)
+            self._folded_in_reduce = True
+        elif finalize_stats:
             # single device: LoadStats over the local B*T, finalized by the plan reduce's last block
             _tagged("plan_reduce", "smes_plan_reduce_stats", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active),
                     ptr(self.chunk_mass), ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads),
@@ -547,6 +562,8 @@ class SMESEngine:
             if getattr(self, "_fold_ev", None) is not None:      # folded on the side stream (forward_a)
                 torch.cuda.current_stream(self.dev).wait_event(self._fold_ev)
                 self._fold_ev = None
+            elif getattr(self, "_folded_in_reduce", False):      # folded by the plan reduce launch
+                self._folded_in_reduce = False
             elif refold:   # training steps refold every step (the weights move between steps)
                 self._fold(s)
             if self.fuse_mlp_fwd:
@@ -856,6 +873,9 @@ class SMESEngine:
             w[f"fc{L}_dgrad_folded"] = (2.0 * n_act * di * T, n_act * (self.ldc * 2 + di * 2 + di / 8))
             w[f"fc{L}_wgrad_folded"] = (2.0 * n_act * di * T, n_act * (di * 2 + self.ldc * 2))
             w["fold_heads"] = (2.0 * E * T * do * di, E * do * di * 2 + E * lg * di * 2)
+            if self.fold_in_reduce:     # the training step folds inside the plan-reduce launch
+                fl, by = w["fold_heads"]
+                w["plan_reduce"] = (fl, w["plan_reduce"][1] + by)
             w["unfold"] = (4.0 * E * T * do * di, E * di * lg * 4 + E * do * di * (4 + 2))
             if self.fuse_mlp:
                 dff = self.dims[1]
