@@ -301,7 +301,7 @@ def parity_sample(src, params, labels, n_rows=256, full_loss=True):
                           "predictions / BCE 2e-2 (bf16), loss reduction 1e-5"}
 
 
-def _roofline(kern, work, peaks, peak_src):
+def _roofline(kern, work, peaks, peak_src, config="c2"):
     breakdown = {}
     for tag, t_ms in kern.items():
         fl, by, bound = work.get(tag, (0.0, 0.0, "hbm"))
@@ -313,7 +313,7 @@ def _roofline(kern, work, peaks, peak_src):
     dominant = breakdown[dom]
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if config == "c2" and os.path.exists(tpath):      # the committed ncu capture is of the c2 step
         try:
             traffic = json.load(open(tpath)).get(dom)
         except Exception:
@@ -452,7 +452,7 @@ def run_dp(args, c, world, rank, local, dev):
     kern = per_kernel_times(eng.step, reps=5, serial=eng)
     peaks, peak_src = _peaks()
     work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
-    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src, args.config)
     expert_flops = sum(work[t][0] for t in kern if t in work and (t.startswith("fc") or t.startswith("mlp_"))
                        and not t.endswith("bias"))
     # the expert MLP as the reference computes it (no head folding): fc1 + fc2 forward, dgrad of
@@ -646,7 +646,7 @@ def run_ep(args, c, world, rank, local, dev):
             "unpermute": (0.0, n_own * d * 2 + Br * d * 4),
             "ep_combine_dh": (0.0, rk.n * B * d * 4 + B * d * 8)}
     work = {k: (f, b, "tensor" if b > 0 and f / b > bal else "hbm") for k, (f, b) in work.items()}
-    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src, args.config)
     expert_flops = 3 * fl + 3 * 2.0 * n_own * dff * T
     cpu = _cpu_sample(args.config, 1) if (rank == 0 and not args.no_cpu) else None
     if rank != 0:
@@ -734,7 +734,7 @@ def run_infer(args, c, world, rank, local, dev):
     kern = per_kernel_times(eng.score, reps=5, serial=eng)
     peaks, peak_src = _peaks()
     work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
-    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src, args.config)
     cpu = _cpu_sample(args.config, 2) if not args.no_cpu else None
     return {"metric": f"SMES inference p50 latency per batch (B={Bb})", "value": top["p50_ms"], "unit": "ms",
             "n_gpus": 1, "steps": reps, "warmup": max(3, args.warmup), "ms_per_step": top["p50_ms"],
@@ -805,7 +805,7 @@ def run_fwd32(args, c, world, rank, local, dev):
     kern = per_kernel_times(lambda: eng.forward(with_loss=True), reps=5)
     peaks, peak_src = _peaks()
     work = eng.work_model(n_act, balance=peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9))
-    roofline, breakdown = _roofline(kern, work, peaks, peak_src)
+    roofline, breakdown = _roofline(kern, work, peaks, peak_src, args.config)
     cpu = _cpu_sample(args.config, 3) if (rank == 0 and not args.no_cpu) else None
     if rank != 0:
         return None
