@@ -32,6 +32,8 @@ SIGNATURES = {
     "smes_route_count_exact": [P],
     "smes_plan_reduce_work_ints": [I, I],
     "smes_fold_full_supported": [I, I, I, I, I],
+    "smes_gemm_ragged_k_split_work": [I, I, I, I, I],
+    "smes_gemm_ragged_k_split": [P, L, P, L, L, I, I, I, P, P, P, I, P, P],
     "smes_plan_reduce_stats_fold": [I, I, P, P, P, P, P, P, P, P, P, P, P, P, I, I, D, I, P, P, I, I, I, I, P, P, P, P, P,
                                     P],
     "smes_route_rt_supported": [I, I, I, I],
@@ -85,12 +87,12 @@ SIGNATURES = {
     "smes_combine_fwd_f32_grid": [I],
     "smes_combine_fwd_f32": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, P, P, P, P, P, I, P],
 }
-_RESTYPE = {"smes_last_error": C.c_char_p}
+_RESTYPE = {"smes_last_error": C.c_char_p, "smes_gemm_ragged_k_split_work": C.c_long}
 # entry points that return a value rather than a status
 _VALUE_FNS = {"smes_abi_version", "smes_route_front_supported", "smes_fold_work_floats", "smes_fold_gemm_path", "smes_route_rows_per_warp", "smes_route_num_chunks", "smes_combine_grid",
               "smes_combine_fwd_f32_grid", "smes_last_error",
               "smes_route_front_count_exact", "smes_route_count_exact", "smes_route_rt_supported",
-              "smes_plan_reduce_work_ints", "smes_fold_full_supported"}
+              "smes_plan_reduce_work_ints", "smes_fold_full_supported", "smes_gemm_ragged_k_split_work"}
 
 # kernels launched per successful call (for the bench's gpu_launches count)
 def _fold_gemm_path(E, T, d_out, d_in):      # csrc/fold.cu gemm_path()
@@ -118,7 +120,8 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_all
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
                     "smes_ep_copy_rows_put": 1, "smes_gemm_ragged_m_x3": 1, "smes_split_bf16x3": 1,
                     "smes_combine_fwd_f32": 1, "smes_route_rt": 1,
-                    "smes_plan_reduce_stats_fold": 1}
+                    "smes_plan_reduce_stats_fold": 1,
+                    "smes_gemm_ragged_k_split": lambda *a: 1 if a[11] <= 1 else 2}
 launch_count = 0
 _timer = None   # optional callable(name) -> context manager, used by the bench's per-kernel timing
 trace = None    # optional list: every successful call appends (tag, kernels launched) -- ncu launch tags

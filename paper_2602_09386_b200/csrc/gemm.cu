@@ -44,6 +44,7 @@ struct GemmArgs {
   float* db_out;              // ragged-K: per-group column sums of P via Q's ones column (G, I), or null
   int a_period;               // ragged-K: P rows are read modulo this period (a shared P for every group), or 0
   int x3;                     // ragged-M fp32 mode: K of one bf16 plane (A, W = three planes hi|mid|lo), or 0
+  int ksplit;                 // ragged-K: K split into this many contiguous parts (partials at group s G + g), or 0
 };
 
 // fp32-accurate products from bf16 planes: x = x0 + x1 + x2 with x_i = bf16(x - x_0 - .. - x_{i-1})
@@ -158,14 +159,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     i_tiles = (args.I + BM - 1) / BM;
     j_tiles = (args.N + BN - 1) / BN;
-    num_tiles = args.G * i_tiles * j_tiles;
+    num_tiles = args.G * i_tiles * j_tiles * (args.ksplit > 1 ? args.ksplit : 1);
   }
   // ring depth and store staging of the ragged-K BN = 256 layout (see Smem)
   const bool one_tile = num_tiles <= (int)gridDim.x;
   const int nst = (S::kStgAlias && !one_tile) ? kStages - 1 : kStages;
   if (S::kStgAlias) sStg = one_tile ? smem : smem + S::kOffB + (kStages - 1) * S::kB;
-  // decode: (group, row0 of A / i0, n0 / j0, k-block range)
-  auto decode = [&](int tile, int& g, int& r0, int& c0, int& kb0, int& nkb) {
+  // decode: (group, row0 of A / i0, n0 / j0, k-block range); go = output group (split-K partial slot)
+  const int ks = args.ksplit > 1 ? args.ksplit : 1;
+  auto decode = [&](int tile, int& g, int& r0, int& c0, int& kb0, int& nkb, int& go) {
     if (MODE == MODE_RAGGED_M) {
       int mt = tile / n_tiles;
       r0 = mt * BM;
@@ -173,14 +175,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       g = find_group(seg_s, args.G, r0);
       kb0 = 0;
       nkb = (args.K + BK - 1) / BK;
+      go = g;
     } else {
       const int per = i_tiles * j_tiles;
-      g = tile / per;
-      const int r = tile - g * per;
+      const int gs = tile / per;
+      g = gs / ks;
+      const int sp = gs - g * ks;
+      const int r = tile - gs * per;
       r0 = (r / j_tiles) * BM;
       c0 = (r % j_tiles) * BN;
-      kb0 = seg_s[g] / BK;
-      nkb = (seg_s[g + 1] - seg_s[g]) / BK;
+      const int tot = (seg_s[g + 1] - seg_s[g]) / BK;
+      const int chunk = (tot + ks - 1) / ks;
+      kb0 = seg_s[g] / BK + sp * chunk;
+      nkb = max(0, min(chunk, tot - sp * chunk));
+      go = sp * args.G + g;
     }
   };
 
@@ -190,8 +198,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int g, r0, c0, kb0, nkb;
-        decode(tile, g, r0, c0, kb0, nkb);
+        int g, r0, c0, kb0, nkb, go;
+        decode(tile, g, r0, c0, kb0, nkb, go);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], S::kA + S::kB);
@@ -236,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        int g, r0, c0, kb0, nkb;
-        decode(tile, g, r0, c0, kb0, nkb);
+        int g, r0, c0, kb0, nkb, go;
+        decode(tile, g, r0, c0, kb0, nkb, go);
         const int acc = it % kAcc;
         const uint32_t aphase = (it / kAcc) & 1;
         mbar_wait(&tempty[acc], aphase ^ 1);
@@ -276,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ncols = args.N;
     int it = 0, nstore = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      int g, r0, c0, kb0, nkb;
-      decode(tile, g, r0, c0, kb0, nkb);
+      int g, r0, c0, kb0, nkb, go;
+      decode(tile, g, r0, c0, kb0, nkb, go);
       const int row = r0 + 32 * q + lane;    // this thread's output row (packed row or i)
       // prefetch (before waiting for the MMA): relu bit-mask words and bias values of my chunks
       uint32_t mw[MYCH][2];
@@ -307,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t t0[32];
         tmem_ld32(tmem_base + ((uint32_t)(32 * q) << 16) + BN, t0);
         tmem_ld_wait();
-        if (row < args.I) args.db_out[(size_t)g * args.I + row] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
+        if (row < args.I) args.db_out[(size_t)go * args.I + row] = nkb > 0 ? __uint_as_float(t0[0]) : 0.f;
       }
 #pragma unroll
       for (int i = 0; i < MYCH; ++i) {
@@ -388,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (lane == 0) {
           if (MODE == MODE_RAGGED_M) tma_store_2d(&tmC, stg, n, r0 + 32 * q);
-          else tma_store_3d(&tmC, stg, n, r0 + 32 * q, g);
+          else tma_store_3d(&tmC, stg, n, r0 + 32 * q, go);
           bulk_commit();
         }
       }
@@ -875,6 +883,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 2) tmem_dealloc_2sm(tmem_base, 512);
 }
 
+// split-K partials of the ragged-K GEMM -> C (and db), summed over the splits in order
+__global__ void __launch_bounds__(256) ksplit_reduce_kernel(int S, long n_c, long n_db, const float* __restrict__ part_c,
+                                                            const float* __restrict__ part_db, float* __restrict__ C,
+                                                            float* __restrict__ db) {
+  pdl_wait();
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n_c + n_db; i += (long)gridDim.x * blockDim.x) {
+    float v = 0.f;
+    if (i < n_c) {
+      for (int s = 0; s < S; ++s) v += part_c[(long)s * n_c + i];
+      C[i] = v;
+    } else {
+      const long k = i - n_c;
+      for (int s = 0; s < S; ++s) v += part_db[(long)s * n_db + k];
+      db[k] = v;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1121,6 +1147,53 @@ int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void
   const int tiles256 = G * ((I + BM - 1) / BM) * ((J + 255) / 256);
   if (J >= 256 && (I > BM || tiles256 >= num_sms())) return launch<256, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
   return launch<128, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+}
+
+long smes_gemm_ragged_k_split_work(int G, int I, int J, int splits, int with_db) {
+  return (long)splits * G * I * J + (with_db ? (long)splits * G * I : 0);
+}
+
+int smes_gemm_ragged_k_split(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
+                             const int* seg, float* C, float* db_out, int splits, float* work, void* stream) {
+  if (splits <= 1) return smes_gemm_ragged_k_periodic(P, ldp, rows_cap, Q, ldq, rows_cap, G, I, J, seg, C, db_out, 0,
+                                                      stream);
+  if (G < 1 || G * splits > 65535) return set_error(SMES_ERR_SHAPE, "wgrad split: %d groups x %d splits", G, splits);
+  if (I <= 0 || J <= 0) return set_error(SMES_ERR_SHAPE, "empty wgrad I=%d J=%d", I, J);
+  if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16) return set_error(SMES_ERR_SHAPE, "wgrad strides must be 16-byte aligned");
+  if (work == nullptr) return set_error(SMES_ERR_STATE, "wgrad split: work buffer required");
+  CUtensorMap ta, tb, tc;
+  int rc;
+  {
+    uint64_t dims[2] = {(uint64_t)I, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldp * 2};
+    uint32_t box[2] = {64, 64};
+    if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, P, dims, str, box))) return rc;
+  }
+  {
+    uint64_t dims[2] = {(uint64_t)J, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
+    uint32_t box[2] = {64, 64};
+    if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Q, dims, str, box))) return rc;
+  }
+  {  // partials [splits][G][I][J] in the work buffer
+    uint64_t dims[3] = {(uint64_t)J, (uint64_t)I, (uint64_t)G * splits};
+    uint64_t str[2] = {(uint64_t)J * 4, (uint64_t)I * J * 4};
+    uint32_t box[3] = {32, 32, 1};
+    if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, work, dims, str, box))) return rc;
+  }
+  const long n_c = (long)G * I * J, n_db = db_out ? (long)G * I : 0;
+  float* part_db = db_out ? work + (long)splits * n_c : nullptr;
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, part_db, 0, 0, splits};
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (J <= 16) rc = launch<16, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+  else if (J >= 256) rc = launch<256, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+  else rc = launch<128, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+  if (rc) return rc;
+  const long n = n_c + n_db;
+  const long want = (n + 255) / 256;
+  smes_launch(ksplit_reduce_kernel, (int)(want < 148L * 8 ? want : 148L * 8), 256, 0, st, splits, n_c, n_db, work,
+              part_db, C, db_out);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "wgrad split reduce: %s", cudaGetErrorString(e));
+  return SMES_OK;
 }
 
 int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,

@@ -57,6 +57,24 @@ __device__ __forceinline__ uint64_t dkey(double d) {
 
 // arg-max over the warp of (value desc, expert index asc); lane owns experts lane + 32 j.
 // Candidates with a set bit in `excl` (bit j) or e >= E are ignored.  Returns the expert.
+// e^x - 1 for x <= 0 with relative accuracy (the front / route_rt helper): degree-8 Taylor for
+// |x| < 1/4, else ex2.approx(x log2 e) - 1; kRtEpsY bounds the relative error with margin
+constexpr float kRtEpsY = 16.f * 0x1p-23f;
+__device__ __forceinline__ float rt_expm1_neg(float x) {
+  float p = fmaf(x, 1.f / 40320.f, 1.f / 5040.f);
+  p = fmaf(x, p, 1.f / 720.f);
+  p = fmaf(x, p, 1.f / 120.f);
+  p = fmaf(x, p, 1.f / 24.f);
+  p = fmaf(x, p, 1.f / 6.f);
+  p = fmaf(x, p, 0.5f);
+  p = fmaf(x, p, 1.f);
+  p *= x;
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 1.4426950408889634f));
+  e -= 1.f;
+  return x > -0.25f ? p : e;
+}
+
 template <int EPL>
 __device__ __forceinline__ int warp_argmax_key32(const uint32_t (&k)[EPL], uint32_t excl, int lane, int E) {
   uint32_t bk = 0;
@@ -156,6 +174,84 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         }
       }
     };
+    // ---------------- Stage I, fast path (training / scoring rows without dense statistics):
+    // deviation form in fp32 (front.cu / route_rt.cu): P_e = sum_t (w_t / S_t) y_te with
+    // y = e^(z - max) - 1 and S_t = E + sum_e y_te ranks like the pooled scores; the set is accepted
+    // when a certified bound separates it, else this row (the whole warp) takes the fp64 path below
+    uint32_t taken = 0;  // bit j: expert lane + 32 j is shared
+    bool exact = true;
+    if (PLAIN && a.chunk_dmass == nullptr && ks > 0) {
+      float P[EPL];
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) P[j] = 0.f;
+      float perr = 0.f;
+      auto fast_task = [&](int t, const float (&zv)[EPL]) {
+        uint32_t mk = 0, nk = 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          const int e = lane + 32 * j;
+          if (e < E) {
+            if (!isfinite(zv[j])) bad = 1;
+            mk = max(mk, fkey(zv[j]));
+            nk = min(nk, fkey(zv[j]));
+          }
+        }
+        const float mx = fkey_inv(__reduce_max_sync(0xffffffffu, mk));
+        const float mn = fkey_inv(__reduce_min_sync(0xffffffffu, nk));
+        float y[EPL], ys = 0.f;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) {
+          const int e = lane + 32 * j;
+          y[j] = e < E ? rt_expm1_neg(zv[j] - mx) : 0.f;
+          ys += y[j];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ys += __shfl_xor_sync(0xffffffffu, ys, o);
+        const float ssum = (float)E + ys;
+        const float q = (float)a.tw[t] / ssum;
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) P[j] = fmaf(q, y[j], P[j]);
+        // |error| of q y_tj <= q |y|max (eps_y + rho_t + 3u) (rho_t: S's EPL + 5 roundings and the y
+        // errors, relative to S); the accumulation over the tasks adds T u
+        const float rho = ((EPL + 5) * 0x1p-24f + kRtEpsY) * (-ys) / ssum + 0x1p-24f;
+        perr += q * (-rt_expm1_neg(mn - mx)) * (kRtEpsY + rho + (3 + T) * 0x1p-24f);
+      };
+      if (TP > 0) {
+#pragma unroll
+        for (int t = 0; t < (TP > 0 ? TP : 1); ++t)
+          if (t < T) fast_task(t, zpre[t]);
+      } else {
+        for (int t = 0; t < T; ++t) {
+          float zv[EPL];
+          load_task(t, zv);
+          fast_task(t, zv);
+        }
+      }
+      uint32_t pk[EPL];
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        const uint32_t u = __float_as_uint(P[j]);
+        pk[j] = (u & 0x80000000u) ? ~u : (u | 0x80000000u);     // order-preserving (P may be negative)
+      }
+      for (int i = 0; i < ks; ++i) {
+        const int bi = warp_argmax_key32<EPL>(pk, taken, lane, E);
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+      }
+      const float e_abs = 1.5f * perr + 0x1p-100f;
+      float lo = INFINITY, hi = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+        if (e < E) {
+          if ((taken >> j) & 1u) lo = fminf(lo, P[j] - e_abs);
+          else hi = fmaxf(hi, P[j] + e_abs);
+        }
+      }
+      const float lo_all = fkey_inv(__reduce_min_sync(0xffffffffu, fkey(lo)));
+      const float hi_all = fkey_inv(__reduce_max_sync(0xffffffffu, fkey(hi)));
+      exact = !(lo_all > hi_all);
+      if (exact) taken = 0;
+    }
     // ---------------- Stage I (fp64): pooled = sum_t w_t softmax(z_t)   (routing.py:256-260)
     double pooled[EPL];
 #pragma unroll
@@ -209,21 +305,24 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
         }
       }
     };
-    if (TP > 0) {
-      // T <= TP: fully unrolled task loop, logits indexed statically from registers
+    if (exact) {
+      if (TP > 0) {
+        // T <= TP: fully unrolled task loop, logits indexed statically from registers
 #pragma unroll
-      for (int t = 0; t < (TP > 0 ? TP : 1); ++t)
-        if (t < T) stage1_task(t, zpre[t]);
-    } else {
-      for (int t = 0; t < T; ++t) {
-        float zv[EPL];
-        load_task(t, zv);
-        stage1_task(t, zv);
+        for (int t = 0; t < (TP > 0 ? TP : 1); ++t)
+          if (t < T) stage1_task(t, zpre[t]);
+      } else {
+        for (int t = 0; t < T; ++t) {
+          float zv[EPL];
+          load_task(t, zv);
+          stage1_task(t, zv);
+        }
       }
     }
     // shared set S: top-K_s of pooled, (score desc, index asc)   (routing.py:261, :184-187)
-    uint32_t taken = 0;  // bit j: expert lane + 32 j is shared
-    if (frozen) {
+    if (!exact) {
+      // decided by the fast path
+    } else if (frozen) {
       const int v = lane < ks ? a.shared[(long)b * ks + lane] : -1;
       for (int i = 0; i < ks; ++i) {
         const int bi = __shfl_sync(0xffffffffu, v, i);
@@ -357,7 +456,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32) route_kernel(const RouteArgs a)
     a.chunk_union[o] = cu;
     a.chunk_active[o] = ca;
     a.chunk_mass[o] = m;
-    a.chunk_dmass[o] = dm;
+    if (a.chunk_dmass != nullptr) a.chunk_dmass[o] = dm;
   }
 }
 
@@ -603,7 +702,7 @@ __global__ void __launch_bounds__(RT_WARPS * 32, SMES_TG_MINB) route_tg_kernel(c
     a.chunk_union[o] = cu;
     a.chunk_active[o] = ca;
     a.chunk_mass[o] = m;
-    a.chunk_dmass[o] = dm;
+    if (a.chunk_dmass != nullptr) a.chunk_dmass[o] = dm;
   }
 }
 

@@ -212,6 +212,7 @@ class SMESEngine:
         # measured 0.531 vs 0.529 ms at c2 with the fold on the side stream (tools/ab_fold.sh): off by default
         self.fold_side = os.environ.get("SMES_FOLD_SIDE", "0") == "1"
         self.fold_in_reduce = False        # set in _alloc once the fold buffers exist
+        self.q_splits = 1
         self._alloc()
         self.refresh_weights()
 
@@ -301,6 +302,11 @@ class SMESEngine:
                 self.q_rows = di if self.fuse_b_last else di + 1   # + the ones column -> per-expert sums of C
                 self.Qe = z(E, self.q_rows, self.ldg)
                 self.q_strides = (self.q_rows * self.ldg, 1, self.ldg)
+                tiles = E * ((self.q_rows + 127) // 128)
+                # measured no faster at c2 (77 vs 75 us eager, tools/ab_split.sh): off unless SMES_WGRAD_SPLIT > 1
+                self.q_splits = int(os.environ.get("SMES_WGRAD_SPLIT", 1))
+                if self.q_splits > 1:
+                    self.q_work = z(call("smes_gemm_ragged_k_split_work", E, self.q_rows, self.ldg, self.q_splits, 0))
             self.csum_q = z(E, self.ldg)                    # per-expert column sums of C
             self.fold_work = z(call("smes_fold_work_floats", E, T, self.d_out, di))
             self.fold_in_reduce = bool(call("smes_fold_full_supported", E, T, self.ldg, self.d_out, di)) and \
@@ -744,8 +750,14 @@ class SMESEngine:
                     self.ld_in[L - 1], R, E, self.ldg, di, ptr(self.seg_pad), ptr(self.Qe), ptr(self.csum_q), s)
             cs, cs_es = self.csum_q, self.ldg
         else:
-            _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm),
-                    self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None, s)
+            if self.q_splits > 1:
+                # few long groups (E x 4 tiles < the SMs): the K range split so every SM streams H
+                _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k_split", ptr(inp), self.ld_in[L - 1],
+                        ptr(self.Cm), self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None,
+                        self.q_splits, ptr(self.q_work), s)
+            else:
+                _tagged(f"fc{L}_wgrad_folded", "smes_gemm_ragged_k", ptr(inp), self.ld_in[L - 1], ptr(self.Cm),
+                        self.ldc, R, E, self.q_rows, self.ldg, ptr(self.seg_pad), ptr(self.Qe), None, s)
             if self.fuse_b_last:
                 cs, cs_es = self.csum, T          # reduced by post_combine
             else:

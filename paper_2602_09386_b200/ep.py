@@ -220,7 +220,8 @@ class EPRank:
              ptr(self.br), 0, None, None, 0, ptr(self.z), T * E, 1, B, s)
         tcall("route", "smes_route_batch", ptr(self.z), E, T * E, None, ptr(self.tw), T, B, E, self.ks, self.ka, self.rpw,
              ptr(self.shared), ptr(self.adaptive), ptr(self.active), ptr(self.wsel), ptr(self.umask), ptr(self.usize),
-             ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass), ptr(self.chunk_dmass), None,
+             # no dense-mass statistics (EP trains with the sparse LB reading): the router's fast Stage I
+             ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass), None, None,
              ptr(self.flag), 0, s)
         tcall("plan_reduce", "smes_plan_reduce", self.C, E, ptr(self.chunk_union), ptr(self.chunk_active), ptr(self.chunk_mass),
              ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads), ptr(self.stats_raw), ptr(self.seg_pad),

@@ -56,6 +56,11 @@ CASES = {
     "rt_4x16_init": (4, 16, "init"),           # c1 shape
     "rt_3x16_ties": (3, 16, "ties"),
     "rt_5x32_tiny": (5, 32, "tiny"),
+    # expert-per-lane kernel without dense statistics: its fp32 deviation-form Stage I (E > 64, c5)
+    "lanefast_32x256_init": (32, 256, "init"),
+    "lanefast_32x256_ties": (32, 256, "ties"),
+    "lanefast_8x128_random": (8, 128, "random"),
+    "lanefast_4x96_tiny": (4, 96, "tiny"),
 }
 
 
@@ -63,7 +68,7 @@ CASES = {
 def test_router_kernel_vs_oracle(name):
     T, E, kind = CASES[name]
     ks, ka, B = (2, 1, 3001) if E == 16 else (4, 2, 3000)
-    rt = name.startswith("rt_")
+    rt = name.startswith("rt_") or name.startswith("lanefast_")
     rng = np.random.default_rng(zlib.crc32(name.encode()))
     if kind == "random":
         z = rng.normal(size=(T, B, E))
@@ -80,8 +85,9 @@ def test_router_kernel_vs_oracle(name):
         g = _route(z32, ks, ka, tw, dm=not rt)
     finally:
         _lib.call("smes_route_count_exact", None)
-    if rt:
+    if name.startswith("rt_"):
         assert _lib.call("smes_route_rt_supported", T, E, ks, ka)
+    if name.startswith("rt_"):          # (the expert-per-lane kernel does not count its fallback rows)
         n_exact = int(cnt.item())
         if kind == "ties":
             assert n_exact > 0, n_exact           # exact pooled ties go through the fp64 recompute
