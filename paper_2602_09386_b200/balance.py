@@ -58,13 +58,24 @@ def _raw_sums(routing: BatchRouting) -> torch.Tensor:
     return raw
 
 
-def stats_from_raw(raw: torch.Tensor, E: int, K: int, B: int, T: int, dense: bool) -> LoadStats:
+def finalize_stats(raw: torch.Tensor, E: int, K: int, B: int, T: int, dense: bool):
+    """Device LoadStats arrays from the raw sums: ``out`` = [frequency, mass, counts, value] (fp64)
+    and the fp32 frequency the LB gradient kernel reads.  No host sync."""
     out = torch.zeros(3 * E + 1, dtype=torch.float64, device=raw.device)
     f32 = torch.zeros(E, dtype=torch.float32, device=raw.device)
     call("smes_stats_finalize", E, K, 0, float(B * T), int(dense), ptr(raw), ptr(out), ptr(f32), _stream())
-    return LoadStats(frequency=out[:E], mass=out[E:2 * E], value=float(out[3 * E].item()),
-                     counts=out[2 * E:3 * E].round().long(), batch_size=B, num_tasks=T, k_budget=K,
-                     from_dense_probs=bool(dense), freq32=f32)
+    return out, f32
+
+
+def load_stats(out: torch.Tensor, f32: torch.Tensor, value: float, E: int, K: int, B: int, T: int,
+               dense: bool) -> LoadStats:
+    return LoadStats(frequency=out[:E], mass=out[E:2 * E], value=value, counts=out[2 * E:3 * E].round().long(),
+                     batch_size=B, num_tasks=T, k_budget=K, from_dense_probs=bool(dense), freq32=f32)
+
+
+def stats_from_raw(raw: torch.Tensor, E: int, K: int, B: int, T: int, dense: bool) -> LoadStats:
+    out, f32 = finalize_stats(raw, E, K, B, T, dense)
+    return load_stats(out, f32, float(out[3 * E].item()), E, K, B, T, dense)
 
 
 def compute_load_stats(routing: BatchRouting, dense_probs: bool = False) -> LoadStats:

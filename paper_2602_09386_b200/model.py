@@ -17,6 +17,7 @@ sliced back to the logical shapes, so results equal those of the unpadded layer.
 """
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field
 
 import torch
@@ -249,6 +250,35 @@ def heads_from_stacked(head_w: torch.Tensor, head_b: torch.Tensor) -> list:
     return [Affine(w[t:t + 1], b[t:t + 1]) for t in range(w.shape[0])]
 
 
+class _Deferred:
+    """A result field computed on first access from data the result already owns."""
+    __slots__ = ("fn",)
+
+    def __init__(self, fn):
+        self.fn = fn
+
+
+class _Lazy:
+    """Dataclass field descriptor: stores values as given, evaluates a :class:`_Deferred` once on
+    first read.  The reference fills these eagerly (model.py:307-324); here the row gathers and
+    fp32 widenings nobody reads cost nothing, and reading them later gives the same arrays."""
+
+    def __set_name__(self, owner, name):
+        self.key = "_lz_" + name
+
+    def __get__(self, obj, owner=None):
+        if obj is None:
+            return None                       # the dataclass default
+        v = obj.__dict__.get(self.key)
+        if isinstance(v, _Deferred):
+            v = v.fn()
+            obj.__dict__[self.key] = v
+        return v
+
+    def __set__(self, obj, value):
+        obj.__dict__[self.key] = value
+
+
 @dataclass
 class ForwardResult:
     """Predictions plus what backward needs (model.py:159-185).  Arrays are device tensors."""
@@ -258,15 +288,15 @@ class ForwardResult:
     task_reps: torch.Tensor        # (T, B, d_out)
     routing: BatchRouting
     plan: ExecutionPlan
-    expert_flops: int
+    expert_flops: int = _Lazy()    # (the logical row count is a device value: read on first access)
     inputs: torch.Tensor | None = None
     encoder_pre: torch.Tensor | None = None
     encoder_hidden: torch.Tensor | None = None
     hidden: torch.Tensor | None = None
     router_logits: torch.Tensor | None = None
-    packed_in: torch.Tensor | None = None
+    packed_in: torch.Tensor | None = _Lazy()
     packed_pre: torch.Tensor | None = None
-    packed_out: torch.Tensor | None = None
+    packed_out: torch.Tensor | None = _Lazy()
     expert_outputs: torch.Tensor | None = None
     _engine: object = None
     _step: int = -1
@@ -404,6 +434,7 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
     if precision == "fp32":
         return _forward_sparse_f32(x, model, counter, frozen, keep_cache, eng, pad)
     eng.keep_logits = True
+    _settle(eng)
     T, E, Ep = model.num_tasks, model.num_experts, pad.E_p
     d, d_out = model.d_in, model.d_out
     enc = None
@@ -429,24 +460,47 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
     plan = ExecutionPlan(E, B, eng.umax, eng.rows_cap, eng.seg_pad[:E + 1].clone(), eng.seg_log[:E + 1].clone(),
                          eng.loads[:E].clone(), c(eng.totals), c(eng.row_of), c(eng.gather_inst),
                          c(eng.gather_exp), raw, routing.usize)
-    n_act = eng.n_act()
     dims = pad.dims
-    flops = n_act * sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+    per_row = sum(dims[i] * dims[i + 1] for i in range(len(dims) - 1))
+    # expert_flops needs the logical row count, a device value: read on first access (a host sync
+    # here would stall the caller's next launches behind the whole forward)
+    flops = _Deferred(lambda: int(plan.totals[2].item()) * per_row)
     if counter is not None:
-        counter.add(flops)
+        counter.add(flops.fn())
     reps = eng.reps[..., :d_out].float()
     res = ForwardResult("sparse", eng.preds.clone(), eng.logits.clone(), reps, routing, plan, flops,
                         _engine=eng, _step=eng.step_id, _enc=enc, _pad=pad)
     if keep_cache:
         res.inputs = x
-        res.hidden = eng.h[:, :d].float()
+        # without encoders the hidden is the batch itself (the kernels read its bf16 copy)
+        hidden = x.float() if enc is None else eng.h[:, :d].float()
+        res.hidden = hidden
         res.router_logits = z.view(B, T, Ep)[:, :, :E].permute(1, 0, 2)
         if enc is not None:
             res.encoder_hidden = enc["mid"][:B, :enc["dh"]].float()
-        rows = plan.physical_rows
-        res.packed_in = eng.X[rows, :d].float()
-        res.packed_out = eng.outs[-1][rows, :d_out].float()
+        # packed_in = hidden[gather_instances] (model.py:301) from arrays the result owns; packed_out
+        # reads the engine's expert outputs until the engine's next forward, which first gathers
+        # them into a copy this result owns (_settle)
+        res.packed_in = _Deferred(lambda: hidden[plan.gather_instances])
+        state = {"rows": None}
+        res.packed_out = _Deferred(lambda: (state["rows"] if state["rows"] is not None
+                                            else eng.outs[-1][plan.physical_rows, :d_out]).float())
+
+        def settle(r):
+            if isinstance(r.__dict__.get("_lz_packed_out"), _Deferred):
+                state["rows"] = eng.outs[-1][plan.physical_rows, :d_out]
+        eng._pending = [(weakref.ref(res), settle)]
     return res
+
+
+def _settle(eng) -> None:
+    """Before a forward rewrites the engine's buffers: earlier results still alive take their own
+    copy of what their deferred fields read from the engine."""
+    for ref, settle in getattr(eng, "_pending", ()):
+        r = ref()
+        if r is not None:
+            settle(r)
+    eng._pending = []
 
 
 def _forward_sparse_f32(x, model: MoeModel, counter, frozen, keep_cache, eng, pad) -> ForwardResult:

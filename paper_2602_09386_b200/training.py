@@ -13,7 +13,7 @@ from dataclasses import dataclass
 import torch
 
 from ._lib import call, ptr
-from .balance import LoadStats, stats_from_raw
+from .balance import LoadStats, finalize_stats, load_stats
 from .errors import NumericsError, ShapeError, StateError
 from .model import ForwardResult, MoeModel, _gemm, _round
 from .routing import _stream
@@ -86,24 +86,29 @@ def backward(result: ForwardResult, model: MoeModel, labels, dense_probs_in_stat
     T, B = result.predictions.shape
     if y.shape != (T, B):
         raise ShapeError(f"labels shape {tuple(y.shape)} does not match predictions ({T}, {B})")
-    y = y.to(eng.dev)
-    if not bool(((y == 0) | (y == 1)).all()):
-        raise NumericsError("labels must be 0 or 1")
+    # pageable labels copy without waiting for the queued forward; pinned ones are copied before
+    # returning control (the caller may reuse the buffer)
+    y = y.to(eng.dev, non_blocking=not y.is_pinned())
+    # the label check runs on the device and is read back with the losses: one host sync per call
+    bad = ((y != 0) & (y != 1)).any()
     eng.labels.copy_(y)
     eng.dense = bool(dense_probs_in_stats)
     eng.forward_b(with_loss=True, train=True)   # loss + LoadStats (training.py:140-142) + fused combine bwd
     eng.backward()
     K = eng.K
     E, Ep = model.num_experts, eng.E
-    lo = eng.loss_out.cpu()
     raw = eng.stats_raw.view(3, Ep)[:, :E].reshape(-1).contiguous()
-    stats = stats_from_raw(raw, E, K, B, T, eng.dense)
+    out, f32 = finalize_stats(raw, E, K, B, T, eng.dense)
     grads = _logical_gradients(eng, model)
     d_hidden = eng.d_hidden[:, :model.d_in].clone()
     if result._enc is not None:
         grads.update(_encoder_backward(result._enc, model, eng))
+    host = torch.cat([eng.loss_out, out[3 * E:], bad.double().view(1)]).cpu()
+    if host[4] != 0:
+        raise NumericsError("labels must be 0 or 1")
+    stats = load_stats(out, f32, float(host[3]), E, K, B, T, eng.dense)
     ordered = {k: grads[k] for k in model.parameter_blocks() if k in grads}
-    return BackwardResult(ordered, float(lo[0]), float(lo[1]), float(lo[2]), stats, d_hidden)
+    return BackwardResult(ordered, float(host[0]), float(host[1]), float(host[2]), stats, d_hidden)
 
 
 def _logical_gradients(eng, model) -> dict:
@@ -119,19 +124,20 @@ def _logical_gradients(eng, model) -> dict:
     g = {}
     for li, (gw, gb) in enumerate(eng.g_layers):
         di, do = dims[li], dims[li + 1]
-        gw, gb = own(gw), own(gb)
         pre = "expert_" if len(pools) == 1 else f"expert{li}_"
-        for e in range(E):
-            g[f"{pre}{e}.weight"] = gw[e, :do, :di]
-            g[f"{pre}{e}.bias"] = gb[e, :do]
-    rw = own(eng.g_router_w).view(T, Ep, eng.d)
-    rb = own(eng.g_router_b).view(T, Ep)
-    hw, hb = own(eng.g_head_w), own(eng.g_head_b)
+        # one unbind per stack (the views in one call, not 2E indexing ops)
+        for e, (w, b) in enumerate(zip(own(gw)[:E, :do, :di].unbind(0), own(gb)[:E, :do].unbind(0))):
+            g[f"{pre}{e}.weight"] = w
+            g[f"{pre}{e}.bias"] = b
+    rw = own(eng.g_router_w).view(T, Ep, eng.d)[:, :E, :dims[0]].unbind(0)
+    rb = own(eng.g_router_b).view(T, Ep)[:, :E].unbind(0)
+    hw = own(eng.g_head_w)[:, :dims[-1]].split(1)
+    hb = own(eng.g_head_b).split(1)
     for t in range(T):
-        g[f"router_{t}.weight"] = rw[t, :E, :dims[0]]
-        g[f"router_{t}.bias"] = rb[t, :E]
-        g[f"head_{t}.weight"] = hw[t:t + 1, :dims[-1]]
-        g[f"head_{t}.bias"] = hb[t:t + 1]
+        g[f"router_{t}.weight"] = rw[t]
+        g[f"router_{t}.bias"] = rb[t]
+        g[f"head_{t}.weight"] = hw[t]
+        g[f"head_{t}.bias"] = hb[t]
     return g
 
 

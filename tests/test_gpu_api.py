@@ -260,6 +260,33 @@ def test_forward_sparse_backward_api(d_ff):
         smes.backward(res, model, torch.tensor(y))       # stale: the engine ran another forward
 
 
+def test_deferred_cache_fields_survive_engine_reuse():
+    """packed_in / packed_out / expert_flops are filled on first read (model.py:301-324 fills them
+    eagerly); a result still alive when the engine runs the next forward keeps its own values."""
+    B, T, E, d, ks, ka = 384, 4, 16, 64, 2, 1
+    p, h, y, lam, beta = make_case(23, B, T, E, d, d, ks, ka)
+    model = _model_from_case(p, lam, beta, ks, ka)
+    x = torch.tensor(h, dtype=torch.float32).cuda()
+    res = smes.forward_sparse(x, model)
+    n_rows = res.plan.total_rows
+    assert res.expert_flops == n_rows * d * d
+    gi = res.plan.gather_instances
+    f = O.forward_sparse(h, p, ks, ka, logits=res.router_logits.double().cpu().numpy())
+    # the second forward (another batch through the same cached engine) rewrites the engine rows
+    res2 = smes.forward_sparse(torch.tensor(h[::-1].copy(), dtype=torch.float32).cuda(), model)
+    assert torch.equal(res.packed_in, res.hidden[gi])
+    assert rel(res.packed_out.cpu().numpy(), f.layer_outs[-1]) < BF16_TOL
+    assert res.packed_out.shape == (n_rows, d)
+    assert res2.packed_out.shape == (res2.plan.total_rows, d)
+    assert torch.equal(res2.packed_in, res2.hidden[res2.plan.gather_instances])
+    assert res.expert_flops == n_rows * d * d
+    with pytest.raises(smes.NumericsError):
+        yb = torch.tensor(y)
+        yb[1, 3] = 0.5
+        smes.backward(res2, model, yb)
+    smes.forward_sparse(x, model, keep_cache=False)
+
+
 def test_encoder_path_vs_autograd():
     """Full reference model (encoder + SMES layer) vs a float64 torch-autograd restatement
     of the same graph with the GPU's selections frozen."""
