@@ -7,6 +7,8 @@
 //   seg_colsum     : per-expert bias gradients db_e = sum_{rows in e} d_pre (training.py:190)
 //   unpermute      : d_hidden[b] = d_router[b] + sum_u dX[row(b,u)] (training.py:192, :212)
 //   part_reduce    : per-CTA partials -> one vector (head grads, training.py:151-152)
+#include <algorithm>
+#include <cstdint>
 #include "ptx.cuh"
 #include "smes_capi.h"
 
@@ -200,6 +202,20 @@ __global__ void __launch_bounds__(1024) part_reduce_kernel(const float* __restri
     float t = 0.f;
     for (int w = 0; w < nw; ++w) t += red[w][lane];
     out[i] = t;
+  }
+}
+
+// out = sum_p part[p] for a handful of partials, in partial order (deterministic)
+__global__ void __launch_bounds__(256) part_sum_few_kernel(const float4* __restrict__ part, int nparts, int n4,
+                                                           float4* __restrict__ out) {
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += gridDim.x * blockDim.x) {
+    float4 acc = part[i];
+    for (int p = 1; p < nparts; ++p) {
+      const float4 v = part[(long)p * n4 + i];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    out[i] = acc;
   }
 }
 
@@ -411,6 +427,16 @@ int smes_bce_loss(int T, int B, const float* pred, const float* labels, const fl
 }
 
 int smes_part_reduce(const float* part, int nparts, int n, float* out, void* stream) {
+  if (nparts <= 8 && n % 4 == 0 && (reinterpret_cast<uintptr_t>(part) % 16) == 0 &&
+      (reinterpret_cast<uintptr_t>(out) % 16) == 0) {
+    // few partials over a long vector (the router wgrad at large T*E*d): one float4 per thread; the
+    // column-block kernel below would launch n / 32 CTAs with most warps idle
+    const int n4 = n / 4;
+    const int blocks = (int)std::min<long>((n4 + 255) / 256, 148L * 16);
+    smes_launch(part_sum_few_kernel, blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream),
+                reinterpret_cast<const float4*>(part), nparts, n4, reinterpret_cast<float4*>(out));
+    return launch_check("part_reduce");
+  }
   smes_launch(part_reduce_kernel, (n + 31) / 32, nparts >= 256 ? 1024 : 256, 0, reinterpret_cast<cudaStream_t>(stream), part, nparts, n, out);
   return launch_check("part_reduce");
 }

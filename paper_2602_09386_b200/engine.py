@@ -130,6 +130,20 @@ def workspace_bytes(params: "SMESParams", batch_size: int, k_shared: int, k_adap
     return off
 
 
+def router_wgrad_splits(B_pad: int, I: int, J: int, dev) -> int:
+    """Split-K factor of the router weight gradient (dW_r = dz^T h, K = the batch): enough
+    (split, tile) work units for ~2 rounds of the persistent grid, no more -- every split writes an I x J fp32
+    partial that part_reduce reads back (at T*E = 8192, d = 1024 the former fixed 64 splits moved
+    4.3 GB per step).  Tiles are 128 x 256 (x 128 for J < 256), csrc/gemm.cu."""
+    try:
+        n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    except Exception:
+        n_sms = 148
+    tiles = -(-I // 128) * (-(-J // 256) if J >= 256 else -(-J // 128))
+    # whole rounds of the persistent GEMM grid: floor, so the last round is not nearly empty
+    return max(1, min(64, B_pad // 256, 2 * n_sms // tiles))
+
+
 class SMESEngine:
     """Fixed-shape executor of the SMES hot path on one GPU."""
 
@@ -321,7 +335,7 @@ class SMESEngine:
         self.freq32 = z(E)
         self.seg_router = torch.tensor([0, self.B_pad], dtype=i32, device=dev)
         # router wgrad reduces over B: split the batch into 256-row groups (split-K), reduce after
-        self.rw_splits = max(1, min(64, self.B_pad // 256))
+        self.rw_splits = router_wgrad_splits(self.B_pad, T * E, d, dev)
         edges = [min(self.B_pad, (self.B_pad // self.rw_splits) // 128 * 128 * i) for i in range(self.rw_splits)]
         self.seg_router_split = torch.tensor(edges + [self.B_pad], dtype=i32, device=dev)
         self.rw_part = z(self.rw_splits, T * E, d)

@@ -32,6 +32,7 @@ import torch
 from . import _lib
 from ._lib import call, ptr, tcall
 from .errors import ConfigError, ShapeError, StateError
+from .engine import router_wgrad_splits
 from .experts import ExpertShard, refresh_into
 
 U32 = torch.int32   # mask words travel as int32 storage
@@ -117,7 +118,7 @@ class EPRank:
         self.dz = z(self.B_pad, T * E, dt=bf)
         self.part_db = z(self.grid, T)
         self.seg_router = torch.tensor([0, self.B_pad], dtype=i32, device=dev)
-        self.rw_splits = max(1, min(64, self.B_pad // 256))
+        self.rw_splits = router_wgrad_splits(self.B_pad, T * E, d, dev)
         edges = [min(self.B_pad, (self.B_pad // self.rw_splits) // 128 * 128 * i) for i in range(self.rw_splits)]
         self.seg_router_split = torch.tensor(edges + [self.B_pad], dtype=i32, device=dev)
         self.rw_part = z(self.rw_splits, T * E, d)

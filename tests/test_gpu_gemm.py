@@ -336,3 +336,18 @@ def test_ragged_k_wgrad_cta_pairs(I, J, bias, monkeypatch):
         if bias:
             refb = pb[lo:hi].float().sum(0)
             assert (db[e] - refb).abs().max().item() / refb.abs().max().item() < 3e-4, e
+
+
+@pytest.mark.parametrize("nparts,n", [(1, 4096), (2, 8 * 1024 * 1024), (3, 1028), (8, 4096), (9, 4096),
+                                      (64, 65536), (2, 1001)])
+def test_part_reduce_split_k_partials(nparts, n):
+    """smes_part_reduce (the split-K partial sum of the router / head weight gradients): the
+    few-partials float4 path (nparts <= 8, n % 4 == 0) and the column-block path, against torch."""
+    g = torch.Generator(device="cuda").manual_seed(nparts * 31 + n)
+    part = torch.randn(nparts, n, generator=g, device="cuda")
+    out = torch.full((n,), float("nan"), device="cuda")
+    call("smes_part_reduce", ptr(part), nparts, n, ptr(out), torch.cuda.current_stream().cuda_stream)
+    ref = part.double().sum(0)
+    assert torch.allclose(out.double(), ref, rtol=1e-5, atol=1e-5 * nparts)
+    if nparts == 1:
+        assert torch.equal(out, part[0])

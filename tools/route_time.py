@@ -10,6 +10,11 @@ for path in sys.argv[1:]:
     K = ks + ka
     g = torch.Generator(device="cuda").manual_seed(0)
     z = torch.randn(T, B, E, device="cuda", generator=g) * float(os.environ.get("ZSCALE", "1"))
+    # LAYOUT=bte: z stored (B, T, E) as the engines write it (stride_t = E, stride_b = T * E)
+    bte = os.environ.get("LAYOUT") == "bte"
+    if bte:
+        z = z.permute(1, 0, 2).contiguous()
+    st_t, st_b = (E, T * E) if bte else (B * E, E)
     tw = torch.ones(T, dtype=torch.float64, device="cuda")
     rpw = call("smes_route_rows_per_warp", B)
     C = call("smes_route_num_chunks", B, rpw)
@@ -21,7 +26,7 @@ for path in sys.argv[1:]:
     cm, cd = torch.zeros(C, E, dtype=torch.float64, device="cuda"), torch.zeros(C, E, dtype=torch.float64, device="cuda")
     fl = i32(1)
     st = torch.cuda.current_stream().cuda_stream
-    f = lambda: call("smes_route_batch", ptr(z), B * E, E, None, ptr(tw), T, B, E, ks, ka, rpw, ptr(sh), ptr(ad), ptr(ac), ptr(ws), ptr(um), ptr(us), ptr(cu), ptr(ca), ptr(cm), ptr(cd) if os.environ.get("DM") else None, None, ptr(fl), 0, st)
+    f = lambda: call("smes_route_batch", ptr(z), st_t, st_b, None, ptr(tw), T, B, E, ks, ka, rpw, ptr(sh), ptr(ad), ptr(ac), ptr(ws), ptr(um), ptr(us), ptr(cu), ptr(ca), ptr(cm), ptr(cd) if os.environ.get("DM") else None, None, ptr(fl), 0, st)
     for _ in range(5): f()
     s, e = torch.cuda.Event(True), torch.cuda.Event(True)
     torch.cuda.synchronize(); s.record()
