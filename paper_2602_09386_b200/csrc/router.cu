@@ -19,6 +19,9 @@ namespace smes {
 
 constexpr int RT_WARPS = 4;
 constexpr int RT_MAX_E = 1024;
+#ifndef SMES_RPW_DIV
+#define SMES_RPW_DIV 4      // plan chunks: ~SMES_RPW_DIV CTAs of RT_WARPS warps per SM
+#endif
 
 struct RouteArgs {
   const float* z;          // logits, element (t,b,e) at z[t*st + b*sb + e]
@@ -715,7 +718,7 @@ using namespace smes;
 extern "C" {
 
 int smes_route_rows_per_warp(int B) {
-  int target = B / (148 * 4 * RT_WARPS);
+  int target = B / (148 * SMES_RPW_DIV * RT_WARPS);
   int rpw = 1;
   while (rpw * 2 <= target && rpw < 64) rpw *= 2;
   return rpw;

@@ -139,6 +139,8 @@ def router_wgrad_splits(B_pad: int, I: int, J: int, dev) -> int:
         n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
     except Exception:
         n_sms = 148
+    if os.environ.get("SMES_RW_SPLITS"):          # A/B measurements (tools/)
+        return max(1, min(64, B_pad // 256, int(os.environ["SMES_RW_SPLITS"])))
     tiles = -(-I // 128) * (-(-J // 256) if J >= 256 else -(-J // 128))
     # whole rounds of the persistent GEMM grid: floor, so the last round is not nearly empty
     return max(1, min(64, B_pad // 256, 2 * n_sms // tiles))
