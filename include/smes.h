@@ -156,6 +156,20 @@ int smes_gemm_ragged_k(const void* P, long ldp, const void* Q, long ldq, long ro
  * (p_rows, I) matrix (a_period a multiple of 64; 0 = ordinary ragged-K). */
 int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G,
                                 int I, int J, const int* seg, float* C, float* db_out, int a_period, void* stream);
+/* ragged-K with Q gathered: packed row r of Q is row gather[r] of src ((n_src, ld_src) bf16; -1 =
+ * a zero row), read by TMA gather4 -- the packed copy of the layer input (the reference's
+ * `hidden[plan.gather_instances]`, model.py:301) is never written (the fc1 weight gradient,
+ * training.py:184-191).  gather: rows_cap int32, 16-byte aligned. */
+int smes_gemm_ragged_k_gather(const void* P, long ldp, const void* src, long ld_src, long n_src, const int32_t* gather,
+                              long rows_cap, int G, int I, int J, const int* seg, float* C, float* db_out,
+                              void* stream);
+
+/* ragged-K with the K range of every group split into `splits` contiguous parts (more work units
+ * than SMs for few, long groups): fp32 partials in `work` (smes_gemm_ragged_k_split_work floats),
+ * then summed over the splits in order into C (and db_out). */
+long smes_gemm_ragged_k_split_work(int G, int I, int J, int splits, int with_db);
+int smes_gemm_ragged_k_split(const void* P, long ldp, const void* Q, long ldq, long rows_cap, int G, int I, int J,
+                             const int* seg, float* C, float* db_out, int splits, float* work, void* stream);
 
 /* ---- K4 combine + heads + BCE: replaces reconstruct_task_reps (execution.py:161-191),
  *      _heads (model.py:202-208) and _weighted_bce (training.py:54-57). */
@@ -216,6 +230,12 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
 int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
                  const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* relu_bits,
                  long bits_ld, void* H, long ldh, float* P, long ldp, void* stream);
+/* smes_mlp_fwd_gather: the same with X gathered from its source rows (X row r = src row gather[r],
+ * -1 = zeros; TMA gather4), replacing the gather of model.py:301 -- no packed X in HBM. */
+int smes_mlp_fwd_gather(const void* src, long ld_src, long n_src, const int32_t* gather, long rows_cap,
+                        const void* W1, const float* b1, const void* G, const float* c, int ldg, int E, int d,
+                        int d_ff, const int* seg, uint32_t* relu_bits, long bits_ld, void* H, long ldh, float* P,
+                        long ldp, void* stream);
 /* smes_mlp_fwd2: the same forward on 2-CTA clusters (cta_group::2, M = 256 per MMA over two
  * consecutive tiles of one expert; each CTA loads half of every W1 / G k-block). */
 int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,

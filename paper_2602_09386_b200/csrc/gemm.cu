@@ -29,6 +29,11 @@ constexpr int kThreads = 384;   // 4 non-epilogue warps + 8 epilogue warps (2 pe
 constexpr int kEpiWarps = 8;
 
 enum { MODE_RAGGED_M = 0, MODE_RAGGED_K = 1 };
+// lanes of the producer warp issuing gathered rows (TMA gather4) in the ragged-K kernel
+#ifndef SMES_GATHER_LANES
+#define SMES_GATHER_LANES 8
+#endif
+constexpr int kGatherLanes = SMES_GATHER_LANES;
 
 struct GemmArgs {
   const int* seg;             // (G+1) padded group offsets in rows (multiples of BM)
@@ -45,6 +50,8 @@ struct GemmArgs {
   int a_period;               // ragged-K: P rows are read modulo this period (a shared P for every group), or 0
   int x3;                     // ragged-M fp32 mode: K of one bf16 plane (A, W = three planes hi|mid|lo), or 0
   int ksplit;                 // ragged-K: K split into this many contiguous parts (partials at group s G + g), or 0
+  const int* gather;          // ragged-K: Q row r is source row gather[r] (tmB maps the source, box {64, 1};
+                              // -1 reads zeros), or null
 };
 
 // fp32-accurate products from bf16 planes: x = x0 + x1 + x2 with x_i = bf16(x - x_0 - .. - x_{i-1})
@@ -79,7 +86,8 @@ struct Smem {
   static constexpr int kOffBias = (kStgAlias ? kOffOnes + 8192 : kOffStg + kEpiWarps * kStgBufs * kStg);
   static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
   static constexpr int kOffSeg = kOffBar + 256;
-  static constexpr int kBytes = kOffSeg + 257 * 4 + 12 + 1024;   // + barriers + group table + alignment slack
+  static constexpr int kOffIdx = (kOffSeg + 257 * 4 + 12 + 15) / 16 * 16;   // ragged-K gather: 8 x 64 row indices
+  static constexpr int kBytes = kOffIdx + (MODE == MODE_RAGGED_K ? 2048 : 0) + 1024;   // + alignment slack
   static constexpr int kTmemCols = 2 * BN;
   static_assert(kBytes <= 232448, "shared memory plan exceeds 227 KB");
 };
@@ -193,7 +201,55 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    if (MODE == MODE_RAGGED_K && args.gather != nullptr && lane < kGatherLanes) {
+      // ================= TMA producer, gathered Q: each k-block's 64 rows straight from the source
+      // rows (TMA gather4, 4 rows per op), issued by kGatherLanes lanes together (one issuing
+      // thread managed ~1 op / 75 cycles).  Each lane copies its own row indices to shared memory
+      // (LDGSTS) 4 k-blocks ahead of their use, through an 8-slot ring.
+      constexpr unsigned kMask = (1u << kGatherLanes) - 1u;
+      int* sIdx = reinterpret_cast<int*>(smem + S::kOffIdx);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int g, r0, c0, kb0, nkb, go;
+        decode(tile, g, r0, c0, kb0, nkb, go);
+        auto pf = [&](int kb) {
+          if (kb < nkb) {
+            const int* src = args.gather + (long)(kb0 + kb) * BK;
+#pragma unroll
+            for (int q = lane; q < BK / 4; q += kGatherLanes) cp_async16(sIdx + (kb & 7) * BK + 4 * q, src + 4 * q);
+          }
+          cp_async_commit();
+        };
+#pragma unroll
+        for (int p = 0; p < 4; ++p) pf(p);
+        for (int kb = 0; kb < nkb; ++kb) {
+          pf(kb + 4);
+          cp_async_wait<4>();
+          uint8_t* a = sA + stage * S::kA;
+          uint8_t* b = sB + stage * S::kB;
+          const int k0 = (kb0 + kb) * BK;
+          if (lane == 0) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], S::kA + S::kB);
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(a + j * 8192, &tmA, &full[stage], r0 + 64 * j, args.a_period ? k0 % args.a_period : k0);
+          }
+          __syncwarp(kMask);
+          const int4* ix = reinterpret_cast<const int4*>(sIdx + (kb & 7) * BK);
+#pragma unroll
+          for (int q = lane; q < BK / 4; q += kGatherLanes) {
+            const int4 r = ix[q];
+#pragma unroll
+            for (int j = 0; j < NBBOX; ++j)
+              tma_gather4(b + j * 8192 + q * 512, &tmB, &full[stage], c0 + 64 * j, r.x, r.y, r.z, r.w);
+          }
+          if (++stage == nst) { stage = 0; phase ^= 1; }
+        }
+      }
+      cp_async_wait<0>();
+    } else if (lane == 0) {
       // ================= TMA producer
       int stage = 0;
       uint32_t phase = 0;
@@ -1096,8 +1152,9 @@ int smes_gemm_ragged_m_x3(const void* A3, long lda, long rows_cap, const void* W
   return launch<128, MODE_RAGGED_M, false, true>(ta, tb, tc, args, st);
 }
 
-int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G,
-                                int I, int J, const int* seg, float* C, float* db_out, int a_period, void* stream) {
+static int ragged_k_impl(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G, int I,
+                         int J, const int* seg, float* C, float* db_out, int a_period, const int* gather, long n_src,
+                         void* stream) {
   if (G < 1 || G > 256) return set_error(SMES_ERR_SHAPE, "group count %d outside [1, 256]", G);
   if (I <= 0 || J <= 0) return set_error(SMES_ERR_SHAPE, "empty wgrad I=%d J=%d", I, J);
   if ((ldp * 2) % 16 || (ldq * 2) % 16 || (J * 4) % 16)
@@ -1111,8 +1168,9 @@ int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void
     if ((rc = make_map(&ta, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, P, dims, str, box))) return rc;
   }
   {
-    uint64_t dims[2] = {(uint64_t)J, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldq * 2};
-    uint32_t box[2] = {64, 64};
+    // gathered: Q is the source ((n_src, ldq) rows), one row per box (4 per gather4 op)
+    uint64_t dims[2] = {(uint64_t)J, (uint64_t)(gather ? n_src : rows_cap)}, str[1] = {(uint64_t)ldq * 2};
+    uint32_t box[2] = {64, gather ? 1u : 64u};
     if ((rc = make_map(&tb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, Q, dims, str, box))) return rc;
   }
   {
@@ -1121,14 +1179,15 @@ int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void
     uint32_t box[3] = {32, 32, 1};
     if ((rc = make_map(&tc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, C, dims, str, box))) return rc;
   }
-  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out, a_period, 0};
+  GemmArgs args{seg, G, J, 0, I, nullptr, 0, nullptr, nullptr, 0, db_out, a_period, 0, 0, gather};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // CTA pairs for the large wgrad banks (I spans >= 2 i tiles, J >= 256, many rows)
   // measured neutral at c3 under the power cap (fc1 wgrad 1.84 / 1.83 ms paired vs 1.89 / 1.79 ms,
   // tools/ab_pairk.sh): off unless SMES_GEMM_PAIR_K=1
   const char* pk_env = std::getenv("SMES_GEMM_PAIR_K");
   const bool pair_k = pk_env != nullptr && pk_env[0] == '1';
-  if (pair_enabled() && pair_k && a_period == 0 && I >= 2 * BM && J >= 256 && rows_cap >= 64L * 1024) {
+  if (pair_enabled() && pair_k && gather == nullptr && a_period == 0 && I >= 2 * BM && J >= 256 &&
+      rows_cap >= 64L * 1024) {
     auto kern = grouped_gemm_pair_k_kernel;
     static bool attr = false;
     if (!attr) {
@@ -1147,6 +1206,19 @@ int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void
   const int tiles256 = G * ((I + BM - 1) / BM) * ((J + 255) / 256);
   if (J >= 256 && (I > BM || tiles256 >= num_sms())) return launch<256, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
   return launch<128, MODE_RAGGED_K, true, true>(ta, tb, tc, args, st);
+}
+
+int smes_gemm_ragged_k_periodic(const void* P, long ldp, long p_rows, const void* Q, long ldq, long rows_cap, int G,
+                                int I, int J, const int* seg, float* C, float* db_out, int a_period, void* stream) {
+  return ragged_k_impl(P, ldp, p_rows, Q, ldq, rows_cap, G, I, J, seg, C, db_out, a_period, nullptr, 0, stream);
+}
+
+int smes_gemm_ragged_k_gather(const void* P, long ldp, const void* src, long ld_src, long n_src, const int32_t* gather,
+                              long rows_cap, int G, int I, int J, const int* seg, float* C, float* db_out,
+                              void* stream) {
+  if (gather == nullptr || n_src < 1) return set_error(SMES_ERR_SHAPE, "ragged_k_gather: empty source");
+  if (reinterpret_cast<uintptr_t>(gather) % 16) return set_error(SMES_ERR_SHAPE, "ragged_k_gather: row table must be 16-byte aligned");
+  return ragged_k_impl(P, ldp, rows_cap, src, ld_src, rows_cap, G, I, J, seg, C, db_out, 0, gather, n_src, stream);
 }
 
 long smes_gemm_ragged_k_split_work(int G, int I, int J, int splits, int with_db) {

@@ -72,6 +72,8 @@ struct FwdArgs {
   int bits_ld;
   float* P;                      // (rows, ldp) fp32 head projections
   int store_h;                   // write H through tmH
+  const int* gather;             // non-null: X row r is source row gather[r] (tmX maps the source,
+                                 // box {64, 1}); -1 (pad rows) reads zeros
 };
 
 struct DgradArgs {
@@ -112,6 +114,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 // S accumulators (128 TMEM columns each): three, so the S-MMA of chunk c+2 does not wait for the
 // epilogue to drain chunk c (a double buffer left a ~380-cycle bubble per chunk, tools/mma_probe)
 constexpr int kSB = 3;
+// lanes of warp 0 issuing the gathered X rows (TMA gather4) in mlp_fwd
+#ifndef SMES_GATHER_LANES
+#define SMES_GATHER_LANES 8
+#endif
+constexpr int kGatherLanes = SMES_GATHER_LANES;
 // H staging tiles in shared memory (the P-MMA operand and the TMA-store source).  Two tiles (the
 // epilogue writing chunk c + 1 while the P-MMA / store of chunk c read theirs, W1 ring 6 -> 4)
 // measured 123 us against 120 us for one at c2, so one it is (SMES_FWD_HB=2 builds the other)
@@ -132,7 +139,8 @@ struct FwdSmem {
   static constexpr int kOffG = kOffW + kWS * 16384;
   static constexpr int kOffH = kOffG + kGS * 4096;      // kHB x (2 x 16 KB atoms: 128 rows x 64 cols)
   static constexpr int kOffBias = kOffH + kHB * 32768;  // 64 fp32 per epilogue warp
-  static constexpr int kOffBar = kOffBias + kEpiWarps * 256;
+  static constexpr int kOffIdx = kOffBias + kEpiWarps * 256;   // gathered X: 2 x 128 source-row indices
+  static constexpr int kOffBar = kOffIdx + 2 * BM * 4;
   static constexpr int kOffSeg = kOffBar + 512;
   static constexpr int kBytes = kOffSeg + 257 * 4 + 1024;
   static_assert(kBytes <= 232448, "mlp_fwd smem");
@@ -196,7 +204,43 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
   if (warp == 0) {
-    if (lane == 1) {
+    if (lane >= 1 && lane <= kGatherLanes && a.gather != nullptr) {
+      // ================= X producer, gathered: the tile's rows straight from the source rows
+      // (TMA gather4, 4 rows per op); the packed X is never materialised.  kGatherLanes lanes issue
+      // the 32 ops of a k-block together (one issuing thread managed ~1 op / 75 cycles); each lane
+      // copies its own row indices of the next tile to shared memory (LDGSTS) a tile ahead.
+      constexpr unsigned kMask = ((1u << kGatherLanes) - 1u) << 1;
+      const int gl = lane - 1;
+      int* sIdx = reinterpret_cast<int*>(smem + S::kOffIdx);
+      auto fetch_idx = [&](int tile, int slot) {
+        if (tile < num_tiles) {
+#pragma unroll
+          for (int q = gl; q < BM / 4; q += kGatherLanes)
+            cp_async16(sIdx + slot * BM + 4 * q, a.gather + (long)tile * BM + 4 * q);
+        }
+        cp_async_commit();
+      };
+      fetch_idx(blockIdx.x, 0);
+      int xi = 0, ti = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ti) {
+        fetch_idx(tile + gridDim.x, (ti + 1) & 1);
+        cp_async_wait<1>();
+        const int4* ix = reinterpret_cast<const int4*>(sIdx + (ti & 1) * BM);
+        for (int kb = 0; kb < DK; ++kb, ++xi) {
+          const int s = slot_of(xi, S::kXS);
+          if (gl == 0) {
+            TW(0, mbar_wait(&xempty[s], par_of(xi, S::kXS) ^ 1));
+            mbar_expect_tx(&xfull[s], 16384);
+          }
+          __syncwarp(kMask);
+#pragma unroll
+          for (int q = gl; q < BM / 4; q += kGatherLanes) {
+            const int4 r = ix[q];
+            tma_gather4(sX + s * 16384 + q * 512, &tmX, &xfull[s], kb * 64, r.x, r.y, r.z, r.w);
+          }
+        }
+      }
+    } else if (lane == 1) {
       // ================= X producer (lane 1): its own thread, so the next tile's W1 k-blocks do
       // not queue behind X loads that wait for the current tile's last chunk
       int xi = 0;
@@ -1758,9 +1802,10 @@ using namespace smes;
 
 extern "C" {
 
-int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
-                 const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* bits, long bits_ld,
-                 void* H, long ldh, float* P, long ldp, void* stream) {
+static int mlp_fwd_impl(const void* X, long ldx, long rows_cap, const int* gather, long n_src, const void* W1,
+                        const float* b1, const void* G, const float* c, int ldg, int E, int d, int d_ff,
+                        const int* seg, uint32_t* bits, long bits_ld, void* H, long ldh, float* P, long ldp,
+                        void* stream) {
   if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_fwd: expert count %d outside [1, 256]", E);
   if (d % 64 || d < 64 || d > 512) return set_error(SMES_ERR_SHAPE, "mlp_fwd: d=%d must be a multiple of 64 in [64, 512]", d);
   if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_fwd: d_ff=%d must be a multiple of 128", d_ff);
@@ -1770,8 +1815,9 @@ int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const f
   CUtensorMap tx, tw, tg, th;
   int rc;
   {
-    uint64_t dims[2] = {(uint64_t)d, (uint64_t)rows_cap}, str[1] = {(uint64_t)ldx * 2};
-    uint32_t box[2] = {64, 128};
+    // gathered: X is the source ((n_src, ldx) rows), one row per box (4 per gather4 op)
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)(gather ? n_src : rows_cap)}, str[1] = {(uint64_t)ldx * 2};
+    uint32_t box[2] = {64, gather ? 1u : 128u};
     if ((rc = bf16_map(&tx, 2, X, dims, str, box))) return rc;
   }
   {
@@ -1793,7 +1839,7 @@ int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const f
     if (H == nullptr) dims[0] = (uint64_t)d;
     if ((rc = bf16_map(&th, 2, hp, dims, str, box))) return rc;
   }
-  mlp::FwdArgs args{seg, E, d, d_ff, (int)ldp, b1, c, ldg, bits, (int)bits_ld, P, H != nullptr ? 1 : 0};
+  mlp::FwdArgs args{seg, E, d, d_ff, (int)ldp, b1, c, ldg, bits, (int)bits_ld, P, H != nullptr ? 1 : 0, gather};
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e;
 #define SMES_FWD_CASE(DK)                                                                              \
@@ -1817,6 +1863,23 @@ int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const f
   e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd launch: %s", cudaGetErrorString(e));
   return SMES_OK;
+}
+
+int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
+                 const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* bits, long bits_ld,
+                 void* H, long ldh, float* P, long ldp, void* stream) {
+  return mlp_fwd_impl(X, ldx, rows_cap, nullptr, 0, W1, b1, G, c, ldg, E, d, d_ff, seg, bits, bits_ld, H, ldh, P,
+                      ldp, stream);
+}
+
+int smes_mlp_fwd_gather(const void* src, long ld_src, long n_src, const int32_t* gather, long rows_cap,
+                        const void* W1, const float* b1, const void* G, const float* c, int ldg, int E, int d,
+                        int d_ff, const int* seg, uint32_t* bits, long bits_ld, void* H, long ldh, float* P, long ldp,
+                        void* stream) {
+  if (gather == nullptr || n_src < 1) return set_error(SMES_ERR_SHAPE, "mlp_fwd_gather: empty source");
+  if (reinterpret_cast<uintptr_t>(gather) % 16) return set_error(SMES_ERR_SHAPE, "mlp_fwd_gather: row table must be 16-byte aligned");
+  return mlp_fwd_impl(src, ld_src, rows_cap, gather, n_src, W1, b1, G, c, ldg, E, d, d_ff, seg, bits, bits_ld, H,
+                      ldh, P, ldp, stream);
 }
 
 int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,

@@ -215,6 +215,14 @@ class SMESEngine:
         # fc1 wgrad with dH recomputed per row block (csrc/mlp.cu mlp_wgrad) instead of storing dH:
         # measured slower at c2 (one CTA per (expert, d_ff chunk) re-streams X), so off by default
         self.fuse_wgrad = bool(fuse_wgrad and self.fuse_mlp)
+        # SMES_GATHER_X=1: folded training steps read the layer input rows straight from h with
+        # TMA gather4 (mlp_fwd and the fc1 weight gradient), so the packed copy X (the reference's
+        # hidden[gather_instances], model.py:301) is never written.  Bit-identical, but measured
+        # slower at c2 (0.776 vs 0.524 ms: gather4 ran at ~1 op / 75 cycles per SM whatever the
+        # number of issuing lanes -- mlp_fwd 124 -> 181 us, fc1 wgrad 84 -> 351 us against the
+        # scatter's 38 -> 15 us, tools/ab_gather.sh), so the packed copy stays the default.
+        self.gather_x = os.environ.get("SMES_GATHER_X", "0") == "1"
+        self._x_gathered = False
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
         # fused router front (csrc/front.cu): router GEMM -> routing straight from TMEM, so the
@@ -514,8 +522,12 @@ class SMESEngine:
                     ptr(self.chunk_mass), ptr(self.chunk_dmass), ptr(self.chunk_base), ptr(self.loads),
                     ptr(self.stats_raw), ptr(self.seg_pad), ptr(self.seg_log), ptr(self.totals), ptr(self.ticket),
                     ptr(self.seg_half), s)
+        # X is gathered by its consumers in folded training steps: the scatter only places rows
+        self._x_gathered = bool(fold and self.fuse_mlp_fwd and self.gather_x and not self.fuse_wgrad)
+        xg = self._x_gathered
         _tagged("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
-             ptr(self.loads), ptr(self.h), self.ldh, ptr(self.X), self.ld_in[0], ptr(self.row_of), self.umax,
+             ptr(self.loads), None if xg else ptr(self.h), self.ldh, None if xg else ptr(self.X), self.ld_in[0],
+             ptr(self.row_of), self.umax,
              ptr(self.gather_inst),
              ptr(self.gather_exp), ptr(self.Cm), self.ldc, self.ldc, s)
         if fold and not self.can_fold:
@@ -588,6 +600,13 @@ class SMESEngine:
                 self._folded_in_reduce = False
             elif refold:   # training steps refold every step (the weights move between steps)
                 self._fold(s)
+            if self.fuse_mlp_fwd and self._x_gathered:
+                # the same, X rows gathered from h (TMA gather4)
+                _tagged("mlp_fwd", "smes_mlp_fwd_gather", ptr(self.h), self.ldh, self.B, ptr(self.gather_inst), R,
+                        ptr(self.w_bf[0]), ptr(self.b32[0]), ptr(self.G_fold), ptr(self.c_fold), self.ldg, self.E,
+                        self.d, di, ptr(self.seg_pad), ptr(self.bits[0]) if store_hidden else None, R,
+                        ptr(self.outs[0]) if store_hidden else None, self.ld_out[0], ptr(self.P), self.ldp, s)
+                return
             if self.fuse_mlp_fwd:
                 # fc1 (+ relu mask, H kept for the weight gradients) and P in one chained kernel
                 _tagged("mlp_fwd", "smes_mlp_fwd", ptr(self.X), self.ld_in[0], R, ptr(self.w_bf[0]),
@@ -721,6 +740,10 @@ class SMESEngine:
                         di, ptr(self.seg_pad), ptr(gw), None, s)
                 _tagged(f"fc{i + 1}_bias", "smes_bias_from_csum", E, T, do, ptr(self.csum), ptr(self.head_w), ptr(gb),
                         s)
+            elif i == 0 and self._x_gathered:
+                # wgrad + bias grad, the layer input rows gathered from h (TMA gather4)
+                _tagged("fc1_wgrad", "smes_gemm_ragged_k_gather", ptr(dout), do, ptr(self.h), self.ldh, B,
+                        ptr(self.gather_inst), R, E, do, di, ptr(self.seg_pad), ptr(gw), ptr(gb), s)
             else:
                 # wgrad + bias grad in one launch (ones column of the layer input, see _alloc)
                 _tagged(f"fc{i + 1}_wgrad", "smes_gemm_ragged_k", ptr(dout), do, ptr(inp), self.ld_in[i], R, E, do,
@@ -913,6 +936,13 @@ class SMESEngine:
                 w["mlp_dgrad"] = (2.0 * n_act * (T * dff + dff * d),
                                   n_act * (self.ldc * 2 + dff / 8 + d * 2 + (0 if self.fuse_wgrad else dff * 2)))
                 w["mlp_wgrad"] = (2.0 * n_act * (T * dff + dff * d), n_act * (self.ldc * 2 + dff / 8 + d * 2))
+            if self._x_gathered:
+                # X never written: the scatter places rows only; its consumers read h's B rows once
+                # from HBM (the U-fold re-reads hit L2)
+                dff = self.dims[1]
+                w["plan_scatter"] = (0.0, B * U * 4 + n_act * 8)
+                w["mlp_fwd"] = (w["mlp_fwd"][0], B * d * 2 + n_act * (dff * 2 + dff / 8 + self.ldp * 4))
+                w["fc1_wgrad"] = (w["fc1_wgrad"][0], B * d * 2 + n_act * dff * 2)
         return {k: (f, b, "tensor" if b > 0 and f / b > balance else ("tensor" if b == 0 else "hbm"))
                 for k, (f, b) in w.items()}
 

@@ -351,3 +351,44 @@ def test_part_reduce_split_k_partials(nparts, n):
     assert torch.allclose(out.double(), ref, rtol=1e-5, atol=1e-5 * nparts)
     if nparts == 1:
         assert torch.equal(out, part[0])
+
+
+@pytest.mark.parametrize("J,I", [(256, 512), (128, 256), (64, 64)])
+def test_ragged_k_gather_matches_packed(J, I):
+    """smes_gemm_ragged_k_gather (Q rows by TMA gather4 from their source rows, -1 = zero row)
+    equals the packed ragged-K GEMM bit for bit, bias sums included."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(J + I)
+    loads = [300, 0, 129, 1, 700, 64]
+    G = len(loads)
+    seg, Pm = _packed(loads, I, g, dev)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    R = Pm.shape[0]
+    Pb = Pm.to(torch.bfloat16)
+    n = sum(loads)
+    cg = torch.Generator(device="cpu").manual_seed(I)
+    perm = torch.randperm(n + 5, generator=cg)[:n]
+    src = torch.randn(n + 5, J + 64, generator=cg).to(torch.bfloat16).to(dev)
+    gather = torch.full((R,), -1, dtype=torch.int32)
+    k = 0
+    for e, m in enumerate(loads):
+        for i in range(m):
+            gather[seg[e] + i] = int(perm[k])
+            k += 1
+    gather = gather.to(dev)
+    Q = torch.zeros(R, J + 64, dtype=torch.bfloat16, device=dev)
+    real = gather >= 0
+    Q[real] = src[gather[real].long()]
+    st = torch.cuda.current_stream().cuda_stream
+    C0 = torch.full((G, I, J), float("nan"), device=dev)
+    C1 = torch.full((G, I, J), float("nan"), device=dev)
+    d0 = torch.full((G, I), float("nan"), device=dev)
+    d1 = torch.full((G, I), float("nan"), device=dev)
+    call("smes_gemm_ragged_k", ptr(Pb), I, ptr(Q), J + 64, R, G, I, J, ptr(seg_t), ptr(C0), ptr(d0), st)
+    call("smes_gemm_ragged_k_gather", ptr(Pb), I, ptr(src), J + 64, src.shape[0], ptr(gather), R, G, I, J,
+         ptr(seg_t), ptr(C1), ptr(d1), st)
+    torch.cuda.synchronize()
+    assert torch.equal(C0, C1)
+    assert torch.equal(d0, d1)
+    ref = torch.stack([Pb[seg[e]:seg[e + 1]].float().T @ Q[seg[e]:seg[e + 1], :J].float() for e in range(G)])
+    assert torch.allclose(C1, ref, rtol=1e-3, atol=1e-3)

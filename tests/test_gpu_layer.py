@@ -149,6 +149,24 @@ def test_graph_replay_is_deterministic():
         assert torch.equal(a, b)
 
 
+def test_gathered_layer_input_is_bit_identical():
+    """SMES_GATHER_X mode (mlp_fwd and the fc1 weight gradient read the layer input rows from h by
+    TMA gather4, no packed X): the training step's loss, gradients and d_hidden equal the
+    packed-X step bit for bit."""
+    p, h, y, lam, beta = make_case(11, 2048, 8, 32, 256, 256, 4, 2, d_ff=512)
+    outs = []
+    for gather in (False, True):
+        eng = SMESEngine(to_engine_params(p, lam, beta), 2048, 4, 2)
+        eng.gather_x = gather
+        eng.set_inputs(torch.tensor(h, device="cuda"), torch.tensor(y, device="cuda", dtype=torch.float32))
+        eng.step()
+        torch.cuda.synchronize()
+        assert eng._x_gathered == gather
+        outs.append([t.clone() for t in (eng.loss_out, eng.grad_flat, eng.d_hidden, eng.P)])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
 @pytest.mark.parametrize("name", ["c1_mlp", "c2_small_batch", "c3_shape_d512", "c1_single_relu"])
 def test_score_matches_oracle(name):
     """Inference scoring (SMESEngine.score, BASELINE c4): predictions and logits from the folded

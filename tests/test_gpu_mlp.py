@@ -127,3 +127,52 @@ def test_mlp_wgrad(E, d, d_ff, T, loads):
         ref_b = dh.sum(0)
         assert (dW[e] - ref_w).abs().max().item() <= 2e-3 * ref_w.abs().max().item()
         assert (db[e] - ref_b).abs().max().item() <= 2e-3 * ref_b.abs().max().item()
+
+
+def _gathered_source(X, seg, loads, d, seed):
+    """Scatter the packed rows back to a shuffled source (n_src rows, one extra column block) and
+    the row table: packed row r = source row gather[r], pad rows -1."""
+    dev = X.device
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    n = sum(loads)
+    perm = torch.randperm(n + 7, generator=g)[:n]          # sparse, shuffled source rows
+    src = torch.randn(n + 7, d + 64, generator=g).to(torch.bfloat16).to(dev)
+    gather = torch.full((X.shape[0],), -1, dtype=torch.int32)
+    k = 0
+    for e, m in enumerate(loads):
+        for i in range(m):
+            gather[seg[e] + i] = int(perm[k])
+            k += 1
+    gather = gather.to(dev)
+    real = gather >= 0
+    src[gather[real].long(), :d] = X[real, :d]
+    return src, gather
+
+
+@pytest.mark.parametrize("E,d,d_ff,T,loads", CASES)
+def test_mlp_fwd_gather_matches_packed(E, d, d_ff, T, loads):
+    """smes_mlp_fwd_gather (X rows by TMA gather4 from their source rows, -1 = zero row) gives the
+    packed-X kernel's H, relu mask and P bit for bit, pad rows included."""
+    dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, E + d + d_ff)
+    src, gather = _gathered_source(X, seg, loads, d, E + d)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    ldh = d_ff + 64
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    for mode in ("packed", "gather"):
+        H = torch.full((R, ldh), 3.0, device=dev).to(torch.bfloat16)
+        bits = torch.zeros(d_ff // 32, R, dtype=torch.int32, device=dev)
+        P = torch.full((R, ldg), float("nan"), device=dev)
+        if mode == "packed":
+            call("smes_mlp_fwd", ptr(X), ldx, R, ptr(W1), ptr(b1), ptr(G), ptr(c), ldg, E, d, d_ff, ptr(seg_t),
+                 ptr(bits), R, ptr(H), ldh, ptr(P), ldg, st)
+        else:
+            call("smes_mlp_fwd_gather", ptr(src), d + 64, src.shape[0], ptr(gather), R, ptr(W1), ptr(b1), ptr(G),
+                 ptr(c), ldg, E, d, d_ff, ptr(seg_t), ptr(bits), R, ptr(H), ldh, ptr(P), ldg, st)
+        torch.cuda.synchronize()
+        outs.append((H, bits, P))
+    (H0, b0, P0), (H1, b1_, P1) = outs
+    rows = seg[-1]
+    assert torch.equal(H0[:rows], H1[:rows])
+    assert torch.equal(b0[:, :rows], b1_[:, :rows])
+    assert torch.equal(P0[:rows], P1[:rows])
