@@ -17,6 +17,7 @@ sliced back to the logical shapes, so results equal those of the unpadded layer.
 """
 from __future__ import annotations
 
+import os
 import weakref
 from dataclasses import dataclass, field
 
@@ -445,8 +446,8 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
     if frozen is not None:
         eng.shared.copy_(frozen.routing.shared_i32)
         eng.adaptive.copy_(frozen.routing.adaptive_i32)
-    eng.forward_a(frozen=frozen is not None)
-    eng.forward_b(with_loss=False)
+    fz = frozen is not None
+    api_replay(eng, ("fwd", fz, eng.dense), lambda: (eng.forward_a(frozen=fz), eng.forward_b(with_loss=False)))
     eng.step_id += 1
     # the result owns its arrays (the reference returns fresh arrays): clone the engine's buffers so a
     # later forward through the same cached engine cannot rewrite this result's routing or plan
@@ -491,6 +492,26 @@ def forward_sparse(batch, model: MoeModel, counter: FlopCounter | None = None, f
                 state["rows"] = eng.outs[-1][plan.physical_rows, :d_out]
         eng._pending = [(weakref.ref(res), settle)]
     return res
+
+
+def api_replay(eng, key, launches) -> None:
+    """Run ``launches`` -- a fixed launch sequence on the engine's own buffers -- through a CUDA
+    graph captured on its second use (the first runs eagerly: it creates the engine's side stream
+    and sets kernel attributes).  The API step is host-bound (~50 launches through ctypes); a replay
+    is one launch.  SMES_API_GRAPHS=0 keeps every call eager."""
+    graphs = eng.__dict__.setdefault("_api_graphs", {})
+    g = graphs.get(key)
+    if g is None:
+        seen = eng.__dict__.setdefault("_api_seen", set())
+        if key not in seen or os.environ.get("SMES_API_GRAPHS", "1") == "0":
+            seen.add(key)
+            launches()
+            return
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            launches()
+        graphs[key] = g
+    g.replay()
 
 
 def _settle(eng) -> None:

@@ -15,7 +15,7 @@ import torch
 from ._lib import call, ptr
 from .balance import LoadStats, finalize_stats, load_stats
 from .errors import NumericsError, ShapeError, StateError
-from .model import ForwardResult, MoeModel, _gemm, _round
+from .model import ForwardResult, MoeModel, _gemm, _round, api_replay
 from .routing import _stream
 
 __all__ = ["CLAMP_LO", "CLAMP_HI", "task_loss", "total_loss", "backward", "BackwardResult"]
@@ -93,8 +93,8 @@ def backward(result: ForwardResult, model: MoeModel, labels, dense_probs_in_stat
     bad = ((y != 0) & (y != 1)).any()
     eng.labels.copy_(y)
     eng.dense = bool(dense_probs_in_stats)
-    eng.forward_b(with_loss=True, train=True)   # loss + LoadStats (training.py:140-142) + fused combine bwd
-    eng.backward()
+    # loss + LoadStats (training.py:140-142) + fused combine bwd, then the expert / router backward
+    api_replay(eng, ("bwd", eng.dense), lambda: (eng.forward_b(with_loss=True, train=True), eng.backward()))
     K = eng.K
     E, Ep = model.num_experts, eng.E
     raw = eng.stats_raw.view(3, Ep)[:, :E].reshape(-1).contiguous()
