@@ -230,6 +230,13 @@ int smes_unfold_grads(int E, int T, int ldg, int d_out, int d_in, const float* Q
 int smes_mlp_fwd(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,
                  const float* c, int ldg, int E, int d, int d_ff, const int* seg, uint32_t* relu_bits,
                  long bits_ld, void* H, long ldh, float* P, long ldp, void* stream);
+/* smes_mlp_fwd_pack: the same, its X rows copied by an in-kernel gather warp from src[gather[r]]
+ * (LDGSTS; -1 = a zero row) and also stored as the packed X (rows_cap, ldx) for the weight
+ * gradient: the plan scatter then only places rows (model.py:301 inside the expert kernel). */
+int smes_mlp_fwd_pack(const void* src, long ld_src, const int32_t* gather, void* X, long ldx, long rows_cap,
+                      const void* W1, const float* b1, const void* G, const float* c, int ldg, int E, int d, int d_ff,
+                      const int* seg, uint32_t* relu_bits, long bits_ld, void* H, long ldh, float* P, long ldp,
+                      void* stream);
 /* smes_mlp_fwd_gather: the same with X gathered from its source rows (X row r = src row gather[r],
  * -1 = zeros; TMA gather4), replacing the gather of model.py:301 -- no packed X in HBM. */
 int smes_mlp_fwd_gather(const void* src, long ld_src, long n_src, const int32_t* gather, long rows_cap,

@@ -69,6 +69,7 @@ SIGNATURES = {
     "smes_ipc_close": [P],
     "smes_mlp_fwd": [P, L, L, P, P, P, P, I, I, I, I, P, P, L, P, L, P, L, P],
     "smes_mlp_fwd_gather": [P, L, L, P, L, P, P, P, P, I, I, I, I, P, P, L, P, L, P, L, P],
+    "smes_mlp_fwd_pack": [P, L, P, P, L, L, P, P, P, P, I, I, I, I, P, P, L, P, L, P, L, P],
     "smes_mlp_fwd2": [P, L, L, P, P, P, P, I, I, I, I, P, P, L, P, L, P, L, P],
     "smes_mlp_dgrad": [P, L, L, P, I, P, I, I, I, P, P, L, P, L, P, L, P],
     "smes_mlp_dgrad2": [P, L, L, P, I, P, I, I, I, P, P, L, P, L, P, L, P],
@@ -116,7 +117,7 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_all
                     "smes_gemm_ragged_k": 1, "smes_combine_fwd": 1, "smes_combine_bwd": 1, "smes_stats_finalize": 1,
                     "smes_loss_finalize": 1, "smes_seg_colsum": 2, "smes_unpermute": 1, "smes_part_reduce": 1,
                     "smes_plan_counts": 1, "smes_combine_train": 1, "smes_bias_from_csum": 1, "smes_lb_grad": 1, "smes_bce_loss": 1,
-                    "smes_post_combine": 1, "smes_fold_heads": _fold_launches, "smes_unfold_grads": _unfold_launches, "smes_gemm_ragged_k_periodic": 1, "smes_gemm_ragged_k_gather": 1, "smes_mlp_fwd_gather": 1,
+                    "smes_post_combine": 1, "smes_fold_heads": _fold_launches, "smes_unfold_grads": _unfold_launches, "smes_gemm_ragged_k_periodic": 1, "smes_gemm_ragged_k_gather": 1, "smes_mlp_fwd_gather": 1, "smes_mlp_fwd_pack": 1,
                     "smes_mlp_fwd": 1, "smes_mlp_fwd2": 1, "smes_mlp_dgrad": 1, "smes_mlp_dgrad2": 1, "smes_mlp_wgrad": 1, "smes_ep_pack": 2, "smes_ep_segments": 1,
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,

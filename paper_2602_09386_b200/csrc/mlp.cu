@@ -31,6 +31,7 @@ namespace mlp {
 constexpr int BM = 128;          // rows per tile
 constexpr int CH = 128;          // d_ff columns per chunk
 constexpr int kThreads = 384;
+constexpr int kThreadsPack = kThreads + 32;   // mlp_fwd with its own X gather warp (warp 12)
 constexpr int kEpiWarps = 8;
 #ifndef SMES_FWD_XS         // ring depths of mlp_fwd (X / W1 k-block slots); 0 = the defaults below
 #define SMES_FWD_XS 0
@@ -74,6 +75,8 @@ struct FwdArgs {
   int store_h;                   // write H through tmH
   const int* gather;             // non-null: X row r is source row gather[r] (tmX maps the source,
                                  // box {64, 1}); -1 (pad rows) reads zeros
+  const __nv_bfloat16* src;      // pack mode (NT = kThreadsPack): the gather warp copies X rows from
+  long ld_src;                   // src[gather[r]] (LDGSTS) and stores the packed tile through tmX
 };
 
 struct DgradArgs {
@@ -146,8 +149,8 @@ struct FwdSmem {
   static_assert(kBytes <= 232448, "mlp_fwd smem");
 };
 
-template <int DK>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int DK, int NT>
+__global__ void __launch_bounds__(NT, 1)
     mlp_fwd_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                    const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmH,
                    const FwdArgs a) {
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
 
   if (warp == 0) {
-    if (lane >= 1 && lane <= kGatherLanes && a.gather != nullptr) {
+    if (NT == kThreads && lane >= 1 && lane <= kGatherLanes && a.gather != nullptr) {
       // ================= X producer, gathered: the tile's rows straight from the source rows
       // (TMA gather4, 4 rows per op); the packed X is never materialised.  kGatherLanes lanes issue
       // the 32 ops of a k-block together (one issuing thread managed ~1 op / 75 cycles); each lane
@@ -240,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (lane == 1) {
+    } else if (lane == 1 && NT == kThreads) {
       // ================= X producer (lane 1): its own thread, so the next tile's W1 k-blocks do
       // not queue behind X loads that wait for the current tile's last chunk
       int xi = 0;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_commit(&pfull[pb]);
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
     // ================= epilogue
     const int q = warp & 3;
     const int par = (warp - 4) >> 2;          // 64-column half of the chunk
@@ -492,6 +495,66 @@ __global__ void __launch_bounds__(kThreads, 1)
       p_e = e; p_row = row; p_it = it;
     }
     if (p_e >= 0) store_p();
+    if (lane == 0) bulk_wait<0>();
+  } else if (NT > kThreads && warp == 4 + kEpiWarps) {
+    // ================= X gather warp (pack mode): the tile's rows copied from their source rows
+    // src[gather[r]] by LDGSTS (16 B per lane, zero-filled for pad rows), swizzled like a TMA tile;
+    // once a k-block's copies land (up to LAG k-blocks later, the tile's last at once) it is fenced to the async proxy, handed to
+    // the S-MMA and stored to the packed X (the fc1 weight gradient reads it) -- the plan scatter
+    // then only places rows
+    constexpr int LAG = 2;
+    constexpr int kStoreLag = S::kXS - 1 - LAG > 0 ? S::kXS - 1 - LAG : 0;
+    int* sIdx = reinterpret_cast<int*>(smem + S::kOffIdx);
+    const int jc = lane & 7, rb = lane >> 3;
+    const int per_cta = (num_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int total = per_cta > 0 ? per_cta * DK : 0;
+    auto finish = [&](int k) {                   // k-block k of this CTA's sequence has landed
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        const int s = slot_of(k, S::kXS);
+        const int tile = (int)blockIdx.x + (k / DK) * (int)gridDim.x, kb = k % DK;
+        tma_store_2d(&tmX, sX + s * 16384, kb * 64, tile * BM);
+        bulk_commit();
+        mbar_arrive(&xfull[s]);
+      }
+    };
+    int done = 0;                                // k-blocks handed over so far
+    for (int k = 0; k < total; ++k) {
+      const int tile = (int)blockIdx.x + (k / DK) * (int)gridDim.x, kb = k % DK;
+      if (kb == 0) {
+        __syncwarp();
+        const int4 v = __ldg(reinterpret_cast<const int4*>(a.gather + (long)tile * BM) + lane);
+        reinterpret_cast<int4*>(sIdx)[lane] = v;
+        __syncwarp();
+      }
+      const int s = slot_of(k, S::kXS);
+      if (lane == 0) {
+        mbar_wait(&xempty[s], par_of(k, S::kXS) ^ 1);
+        bulk_wait_read<kStoreLag>();              // the store of this slot's previous k-block has read it
+      }
+      __syncwarp();
+      uint8_t* dst = sX + s * 16384;
+#pragma unroll 8
+      for (int i = 0; i < BM / 4; ++i) {
+        const int r = rb + 4 * i;
+        const int idx = sIdx[r];
+        const __nv_bfloat16* g = a.src + (idx >= 0 ? (long)idx * a.ld_src : 0L) + kb * 64 + jc * 8;
+        cp_async16_zfill(dst + r * 128 + ((jc ^ (r & 7)) << 4), g, idx >= 0 ? 16 : 0);
+      }
+      cp_async_commit();
+      if (kb == DK - 1) {
+        // a tile's k-blocks are all handed over before the next tile's are issued: its slots are
+        // released only after this tile's last S-MMA, which needs every k-block of this tile
+        cp_async_wait<0>();
+        while (done <= k) finish(done++);
+      } else if (k - done >= LAG) {
+        cp_async_wait<LAG>();
+        finish(done++);
+      }
+    }
+    cp_async_wait<0>();
+    while (done < total) finish(done++);
     if (lane == 0) bulk_wait<0>();
   }
 #ifdef SMES_TRACE
@@ -1805,7 +1868,10 @@ extern "C" {
 static int mlp_fwd_impl(const void* X, long ldx, long rows_cap, const int* gather, long n_src, const void* W1,
                         const float* b1, const void* G, const float* c, int ldg, int E, int d, int d_ff,
                         const int* seg, uint32_t* bits, long bits_ld, void* H, long ldh, float* P, long ldp,
-                        void* stream) {
+                        void* stream, const void* pack_src = nullptr, long pack_ld = 0) {
+  // pack mode: X is the packed output (written by the kernel); rows come from pack_src[gather[r]]
+  const bool pack = pack_src != nullptr;
+  const int* tma_gather = pack ? nullptr : gather;
   if (E < 1 || E > 256) return set_error(SMES_ERR_SHAPE, "mlp_fwd: expert count %d outside [1, 256]", E);
   if (d % 64 || d < 64 || d > 512) return set_error(SMES_ERR_SHAPE, "mlp_fwd: d=%d must be a multiple of 64 in [64, 512]", d);
   if (d_ff % 128 || d_ff < 128) return set_error(SMES_ERR_SHAPE, "mlp_fwd: d_ff=%d must be a multiple of 128", d_ff);
@@ -1816,8 +1882,8 @@ static int mlp_fwd_impl(const void* X, long ldx, long rows_cap, const int* gathe
   int rc;
   {
     // gathered: X is the source ((n_src, ldx) rows), one row per box (4 per gather4 op)
-    uint64_t dims[2] = {(uint64_t)d, (uint64_t)(gather ? n_src : rows_cap)}, str[1] = {(uint64_t)ldx * 2};
-    uint32_t box[2] = {64, gather ? 1u : 128u};
+    uint64_t dims[2] = {(uint64_t)d, (uint64_t)(tma_gather ? n_src : rows_cap)}, str[1] = {(uint64_t)ldx * 2};
+    uint32_t box[2] = {64, tma_gather ? 1u : 128u};
     if ((rc = bf16_map(&tx, 2, X, dims, str, box))) return rc;
   }
   {
@@ -1839,16 +1905,18 @@ static int mlp_fwd_impl(const void* X, long ldx, long rows_cap, const int* gathe
     if (H == nullptr) dims[0] = (uint64_t)d;
     if ((rc = bf16_map(&th, 2, hp, dims, str, box))) return rc;
   }
-  mlp::FwdArgs args{seg, E, d, d_ff, (int)ldp, b1, c, ldg, bits, (int)bits_ld, P, H != nullptr ? 1 : 0, gather};
+  mlp::FwdArgs args{seg, E, d, d_ff, (int)ldp, b1, c, ldg, bits, (int)bits_ld, P, H != nullptr ? 1 : 0, tma_gather,
+                    reinterpret_cast<const __nv_bfloat16*>(pack_src), pack_ld};
+  if (pack) args.gather = gather;   // read by the gather warp (tma_gather stays off: no gather4 ops)
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   cudaError_t e;
 #define SMES_FWD_CASE(DK)                                                                              \
   case DK: {                                                                                           \
-    auto k = mlp::mlp_fwd_kernel<DK>;                                                                  \
+    auto k = pack ? mlp::mlp_fwd_kernel<DK, mlp::kThreadsPack> : mlp::mlp_fwd_kernel<DK, mlp::kThreads>; \
     const int sm = mlp::FwdSmem<DK>::kBytes;                                                           \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd smem attribute: %s", cudaGetErrorString(e)); \
-    smes_launch(k, sm_count(), mlp::kThreads, sm, st, tx, tw, tg, th, args);                                    \
+    smes_launch(k, sm_count(), pack ? mlp::kThreadsPack : mlp::kThreads, sm, st, tx, tw, tg, th, args);          \
     break;                                                                                             \
   }
   switch (d / 64) {
@@ -1880,6 +1948,17 @@ int smes_mlp_fwd_gather(const void* src, long ld_src, long n_src, const int32_t*
   if (reinterpret_cast<uintptr_t>(gather) % 16) return set_error(SMES_ERR_SHAPE, "mlp_fwd_gather: row table must be 16-byte aligned");
   return mlp_fwd_impl(src, ld_src, rows_cap, gather, n_src, W1, b1, G, c, ldg, E, d, d_ff, seg, bits, bits_ld, H,
                       ldh, P, ldp, stream);
+}
+
+int smes_mlp_fwd_pack(const void* src, long ld_src, const int32_t* gather, void* X, long ldx, long rows_cap,
+                      const void* W1, const float* b1, const void* G, const float* c, int ldg, int E, int d, int d_ff,
+                      const int* seg, uint32_t* bits, long bits_ld, void* H, long ldh, float* P, long ldp,
+                      void* stream) {
+  if (src == nullptr || gather == nullptr || X == nullptr) return set_error(SMES_ERR_SHAPE, "mlp_fwd_pack: null operand");
+  if (reinterpret_cast<uintptr_t>(gather) % 16 || (ld_src * 2) % 16 || reinterpret_cast<uintptr_t>(src) % 16)
+    return set_error(SMES_ERR_SHAPE, "mlp_fwd_pack: row table and source rows must be 16-byte aligned");
+  return mlp_fwd_impl(X, ldx, rows_cap, gather, 0, W1, b1, G, c, ldg, E, d, d_ff, seg, bits, bits_ld, H, ldh, P, ldp,
+                      stream, src, ld_src);
 }
 
 int smes_mlp_fwd2(const void* X, long ldx, long rows_cap, const void* W1, const float* b1, const void* G,

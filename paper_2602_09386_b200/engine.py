@@ -222,7 +222,13 @@ class SMESEngine:
         # number of issuing lanes -- mlp_fwd 124 -> 181 us, fc1 wgrad 84 -> 351 us against the
         # scatter's 38 -> 15 us, tools/ab_gather.sh), so the packed copy stays the default.
         self.gather_x = os.environ.get("SMES_GATHER_X", "0") == "1"
+        # SMES_FWD_PACK=1: mlp_fwd's own gather warp copies the X rows from h (LDGSTS) and writes the
+        # packed X the weight gradient reads, so the plan scatter only places rows.  Bit-identical;
+        # measured slower at c2 (one gather warp: mlp_fwd 125 -> 192 us against the scatter's
+        # 37 -> 15 us, step 0.525 -> 0.562 ms, tools/ab_pack.sh), so off by default
+        self.fwd_pack = os.environ.get("SMES_FWD_PACK", "0") == "1"
         self._x_gathered = False
+        self._x_packed_by_fwd = False
         self.rpw = call("smes_route_rows_per_warp", B)
         self.C = call("smes_route_num_chunks", B, self.rpw)
         # fused router front (csrc/front.cu): router GEMM -> routing straight from TMEM, so the
@@ -524,7 +530,8 @@ class SMESEngine:
                     ptr(self.seg_half), s)
         # X is gathered by its consumers in folded training steps: the scatter only places rows
         self._x_gathered = bool(fold and self.fuse_mlp_fwd and self.gather_x and not self.fuse_wgrad)
-        xg = self._x_gathered
+        self._x_packed_by_fwd = bool(fold and self.fuse_mlp_fwd and self.fwd_pack and not self._x_gathered)
+        xg = self._x_gathered or self._x_packed_by_fwd
         _tagged("plan_scatter", "smes_plan_scatter", B, E, d, self.rpw, ptr(self.umask), ptr(self.chunk_base), ptr(self.seg_pad),
              ptr(self.loads), None if xg else ptr(self.h), self.ldh, None if xg else ptr(self.X), self.ld_in[0],
              ptr(self.row_of), self.umax,
@@ -600,6 +607,13 @@ class SMESEngine:
                 self._folded_in_reduce = False
             elif refold:   # training steps refold every step (the weights move between steps)
                 self._fold(s)
+            if self.fuse_mlp_fwd and self._x_packed_by_fwd:
+                # the same, X rows gathered from h by the kernel's own warp and stored packed
+                _tagged("mlp_fwd", "smes_mlp_fwd_pack", ptr(self.h), self.ldh, ptr(self.gather_inst), ptr(self.X),
+                        self.ld_in[0], R, ptr(self.w_bf[0]), ptr(self.b32[0]), ptr(self.G_fold), ptr(self.c_fold),
+                        self.ldg, self.E, self.d, di, ptr(self.seg_pad), ptr(self.bits[0]) if store_hidden else None,
+                        R, ptr(self.outs[0]) if store_hidden else None, self.ld_out[0], ptr(self.P), self.ldp, s)
+                return
             if self.fuse_mlp_fwd and self._x_gathered:
                 # the same, X rows gathered from h (TMA gather4)
                 _tagged("mlp_fwd", "smes_mlp_fwd_gather", ptr(self.h), self.ldh, self.B, ptr(self.gather_inst), R,

@@ -151,20 +151,22 @@ def test_graph_replay_is_deterministic():
 
 def test_gathered_layer_input_is_bit_identical():
     """SMES_GATHER_X mode (mlp_fwd and the fc1 weight gradient read the layer input rows from h by
-    TMA gather4, no packed X): the training step's loss, gradients and d_hidden equal the
-    packed-X step bit for bit."""
+    TMA gather4, no packed X) and SMES_FWD_PACK mode (mlp_fwd's gather warp copies the rows and
+    writes the packed X): the training step's loss, gradients and d_hidden equal the packed-X step
+    bit for bit."""
     p, h, y, lam, beta = make_case(11, 2048, 8, 32, 256, 256, 4, 2, d_ff=512)
     outs = []
-    for gather in (False, True):
+    for gather, pack in ((False, False), (True, False), (False, True)):
         eng = SMESEngine(to_engine_params(p, lam, beta), 2048, 4, 2)
-        eng.gather_x = gather
+        eng.gather_x, eng.fwd_pack = gather, pack
         eng.set_inputs(torch.tensor(h, device="cuda"), torch.tensor(y, device="cuda", dtype=torch.float32))
         eng.step()
         torch.cuda.synchronize()
-        assert eng._x_gathered == gather
+        assert eng._x_gathered == gather and eng._x_packed_by_fwd == pack
         outs.append([t.clone() for t in (eng.loss_out, eng.grad_flat, eng.d_hidden, eng.P)])
-    for a, b in zip(*outs):
-        assert torch.equal(a, b)
+    for other in outs[1:]:
+        for a, b in zip(outs[0], other):
+            assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("name", ["c1_mlp", "c2_small_batch", "c3_shape_d512", "c1_single_relu"])

@@ -176,3 +176,35 @@ def test_mlp_fwd_gather_matches_packed(E, d, d_ff, T, loads):
     assert torch.equal(H0[:rows], H1[:rows])
     assert torch.equal(b0[:, :rows], b1_[:, :rows])
     assert torch.equal(P0[:rows], P1[:rows])
+
+
+@pytest.mark.parametrize("E,d,d_ff,T,loads", CASES)
+def test_mlp_fwd_pack_matches_packed(E, d, d_ff, T, loads):
+    """smes_mlp_fwd_pack (the kernel's gather warp copies X rows from their source rows, -1 = zero
+    row, and stores the packed X) gives the packed-X kernel's H, relu mask and P bit for bit, and
+    writes exactly the packed X (pad rows zero)."""
+    dev, g, seg, R, ldx, X, W1, b1, ldg, G, c = _setup(E, d, d_ff, T, loads, E + d + d_ff + 1)
+    src, gather = _gathered_source(X, seg, loads, d, E + d + 1)
+    seg_t = torch.tensor(seg, dtype=torch.int32, device=dev)
+    ldh = d_ff + 64
+    st = torch.cuda.current_stream().cuda_stream
+    outs = []
+    Xw = torch.full_like(X, 7.0)
+    for mode in ("packed", "pack"):
+        H = torch.full((R, ldh), 3.0, device=dev).to(torch.bfloat16)
+        bits = torch.zeros(d_ff // 32, R, dtype=torch.int32, device=dev)
+        P = torch.full((R, ldg), float("nan"), device=dev)
+        if mode == "packed":
+            call("smes_mlp_fwd", ptr(X), ldx, R, ptr(W1), ptr(b1), ptr(G), ptr(c), ldg, E, d, d_ff, ptr(seg_t),
+                 ptr(bits), R, ptr(H), ldh, ptr(P), ldg, st)
+        else:
+            call("smes_mlp_fwd_pack", ptr(src), d + 64, ptr(gather), ptr(Xw), ldx, R, ptr(W1), ptr(b1), ptr(G),
+                 ptr(c), ldg, E, d, d_ff, ptr(seg_t), ptr(bits), R, ptr(H), ldh, ptr(P), ldg, st)
+        torch.cuda.synchronize()
+        outs.append((H, bits, P))
+    (H0, b0, P0), (H1, b1_, P1) = outs
+    rows = seg[-1]
+    assert torch.equal(H0[:rows], H1[:rows])
+    assert torch.equal(b0[:, :rows], b1_[:, :rows])
+    assert torch.equal(P0[:rows], P1[:rows])
+    assert torch.equal(Xw[:rows, :d], X[:rows, :d])
