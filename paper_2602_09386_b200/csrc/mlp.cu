@@ -31,7 +31,6 @@ namespace mlp {
 constexpr int BM = 128;          // rows per tile
 constexpr int CH = 128;          // d_ff columns per chunk
 constexpr int kThreads = 384;
-constexpr int kThreadsPack = kThreads + 32;   // mlp_fwd with its own X gather warp (warp 12)
 constexpr int kEpiWarps = 8;
 #ifndef SMES_FWD_XS         // ring depths of mlp_fwd (X / W1 k-block slots); 0 = the defaults below
 #define SMES_FWD_XS 0
@@ -75,7 +74,7 @@ struct FwdArgs {
   int store_h;                   // write H through tmH
   const int* gather;             // non-null: X row r is source row gather[r] (tmX maps the source,
                                  // box {64, 1}); -1 (pad rows) reads zeros
-  const __nv_bfloat16* src;      // pack mode (NT = kThreadsPack): the gather warp copies X rows from
+  const __nv_bfloat16* src;      // pack mode (PACK): warp 2 copies the X rows from
   long ld_src;                   // src[gather[r]] (LDGSTS) and stores the packed tile through tmX
 };
 
@@ -149,8 +148,8 @@ struct FwdSmem {
   static_assert(kBytes <= 232448, "mlp_fwd smem");
 };
 
-template <int DK, int NT>
-__global__ void __launch_bounds__(NT, 1)
+template <int DK, bool PACK>
+__global__ void __launch_bounds__(kThreads, 1)
     mlp_fwd_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                    const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmH,
                    const FwdArgs a) {
@@ -206,8 +205,23 @@ __global__ void __launch_bounds__(NT, 1)
   if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 10] = gtimer();
 #endif
 
+  // G producer: released by the P-MMA, kept off the W1 stream (warp 2 lane 0; warp 0 lane 1 when
+  // warp 2 copies X rows)
+  auto produce_g = [&]() {
+    int gi = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const int e = find_group(seg_s, a.E, tile * BM);
+      for (int c = 0; c < NC; ++c, ++gi) {
+        const int s = slot_of(gi, S::kGS);
+        TW(2, mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1));
+        mbar_expect_tx(&gfull[s], 4096);
+        tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);          // box {64 f, 16 t, 1}
+        tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
+      }
+    }
+  };
   if (warp == 0) {
-    if (NT == kThreads && lane >= 1 && lane <= kGatherLanes && a.gather != nullptr) {
+    if (!PACK && lane >= 1 && lane <= kGatherLanes && a.gather != nullptr) {
       // ================= X producer, gathered: the tile's rows straight from the source rows
       // (TMA gather4, 4 rows per op); the packed X is never materialised.  kGatherLanes lanes issue
       // the 32 ops of a k-block together (one issuing thread managed ~1 op / 75 cycles); each lane
@@ -243,7 +257,9 @@ __global__ void __launch_bounds__(NT, 1)
           }
         }
       }
-    } else if (lane == 1 && NT == kThreads) {
+    } else if (lane == 1 && PACK) {
+      produce_g();
+    } else if (lane == 1) {
       // ================= X producer (lane 1): its own thread, so the next tile's W1 k-blocks do
       // not queue behind X loads that wait for the current tile's last chunk
       int xi = 0;
@@ -275,19 +291,68 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
   } else if (warp == 2) {
-    if (lane == 0) {
-      // ================= G producer: released by the P-MMA, kept off the W1 stream
-      int gi = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int e = find_group(seg_s, a.E, tile * BM);
-        for (int c = 0; c < NC; ++c, ++gi) {
-          const int s = slot_of(gi, S::kGS);
-          TW(2, mbar_wait(&gempty[s], par_of(gi, S::kGS) ^ 1));
-          mbar_expect_tx(&gfull[s], 4096);
-          tma_load_3d(sG + s * 4096, &tmG, &gfull[s], c * CH, 0, e);          // box {64 f, 16 t, 1}
-          tma_load_3d(sG + s * 4096 + 2048, &tmG, &gfull[s], c * CH + 64, 0, e);
+    if (PACK) {
+      // ================= X copy warp (pack mode; the G producer moved to warp 0 lane 1): the tile's rows copied from their source rows
+      // src[gather[r]] by LDGSTS (16 B per lane, zero-filled for pad rows), swizzled like a TMA tile;
+      // once a k-block's copies land (up to LAG k-blocks later, the tile's last at once) it is fenced to the async proxy, handed to
+      // the S-MMA and stored to the packed X (the fc1 weight gradient reads it) -- the plan scatter
+      // then only places rows
+      constexpr int LAG = 2;
+      constexpr int kStoreLag = S::kXS - 1 - LAG > 0 ? S::kXS - 1 - LAG : 0;
+      int* sIdx = reinterpret_cast<int*>(smem + S::kOffIdx);
+      const int jc = lane & 7, rb = lane >> 3;
+      const int per_cta = (num_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+      const int total = per_cta > 0 ? per_cta * DK : 0;
+      auto finish = [&](int k) {                   // k-block k of this CTA's sequence has landed
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          const int s = slot_of(k, S::kXS);
+          const int tile = (int)blockIdx.x + (k / DK) * (int)gridDim.x, kb = k % DK;
+          tma_store_2d(&tmX, sX + s * 16384, kb * 64, tile * BM);
+          bulk_commit();
+          mbar_arrive(&xfull[s]);
+        }
+      };
+      int done = 0;                                // k-blocks handed over so far
+      for (int k = 0; k < total; ++k) {
+        const int tile = (int)blockIdx.x + (k / DK) * (int)gridDim.x, kb = k % DK;
+        if (kb == 0) {
+          __syncwarp();
+          const int4 v = __ldg(reinterpret_cast<const int4*>(a.gather + (long)tile * BM) + lane);
+          reinterpret_cast<int4*>(sIdx)[lane] = v;
+          __syncwarp();
+        }
+        const int s = slot_of(k, S::kXS);
+        if (lane == 0) {
+          mbar_wait(&xempty[s], par_of(k, S::kXS) ^ 1);
+          bulk_wait_read<kStoreLag>();              // the store of this slot's previous k-block has read it
+        }
+        __syncwarp();
+        uint8_t* dst = sX + s * 16384;
+#pragma unroll 8
+        for (int i = 0; i < BM / 4; ++i) {
+          const int r = rb + 4 * i;
+          const int idx = sIdx[r];
+          const __nv_bfloat16* g = a.src + (idx >= 0 ? (long)idx * a.ld_src : 0L) + kb * 64 + jc * 8;
+          cp_async16_zfill(dst + r * 128 + ((jc ^ (r & 7)) << 4), g, idx >= 0 ? 16 : 0);
+        }
+        cp_async_commit();
+        if (kb == DK - 1) {
+          // a tile's k-blocks are all handed over before the next tile's are issued: its slots are
+          // released only after this tile's last S-MMA, which needs every k-block of this tile
+          cp_async_wait<0>();
+          while (done <= k) finish(done++);
+        } else if (k - done >= LAG) {
+          cp_async_wait<LAG>();
+          finish(done++);
         }
       }
+      cp_async_wait<0>();
+      while (done < total) finish(done++);
+      if (lane == 0) bulk_wait<0>();
+    } else if (lane == 0) {
+      produce_g();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -352,7 +417,7 @@ __global__ void __launch_bounds__(NT, 1)
         tc_commit(&pfull[pb]);
       }
     }
-  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
+  } else if (warp >= 4) {
     // ================= epilogue
     const int q = warp & 3;
     const int par = (warp - 4) >> 2;          // 64-column half of the chunk
@@ -495,66 +560,6 @@ __global__ void __launch_bounds__(NT, 1)
       p_e = e; p_row = row; p_it = it;
     }
     if (p_e >= 0) store_p();
-    if (lane == 0) bulk_wait<0>();
-  } else if (NT > kThreads && warp == 4 + kEpiWarps) {
-    // ================= X gather warp (pack mode): the tile's rows copied from their source rows
-    // src[gather[r]] by LDGSTS (16 B per lane, zero-filled for pad rows), swizzled like a TMA tile;
-    // once a k-block's copies land (up to LAG k-blocks later, the tile's last at once) it is fenced to the async proxy, handed to
-    // the S-MMA and stored to the packed X (the fc1 weight gradient reads it) -- the plan scatter
-    // then only places rows
-    constexpr int LAG = 2;
-    constexpr int kStoreLag = S::kXS - 1 - LAG > 0 ? S::kXS - 1 - LAG : 0;
-    int* sIdx = reinterpret_cast<int*>(smem + S::kOffIdx);
-    const int jc = lane & 7, rb = lane >> 3;
-    const int per_cta = (num_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int total = per_cta > 0 ? per_cta * DK : 0;
-    auto finish = [&](int k) {                   // k-block k of this CTA's sequence has landed
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        const int s = slot_of(k, S::kXS);
-        const int tile = (int)blockIdx.x + (k / DK) * (int)gridDim.x, kb = k % DK;
-        tma_store_2d(&tmX, sX + s * 16384, kb * 64, tile * BM);
-        bulk_commit();
-        mbar_arrive(&xfull[s]);
-      }
-    };
-    int done = 0;                                // k-blocks handed over so far
-    for (int k = 0; k < total; ++k) {
-      const int tile = (int)blockIdx.x + (k / DK) * (int)gridDim.x, kb = k % DK;
-      if (kb == 0) {
-        __syncwarp();
-        const int4 v = __ldg(reinterpret_cast<const int4*>(a.gather + (long)tile * BM) + lane);
-        reinterpret_cast<int4*>(sIdx)[lane] = v;
-        __syncwarp();
-      }
-      const int s = slot_of(k, S::kXS);
-      if (lane == 0) {
-        mbar_wait(&xempty[s], par_of(k, S::kXS) ^ 1);
-        bulk_wait_read<kStoreLag>();              // the store of this slot's previous k-block has read it
-      }
-      __syncwarp();
-      uint8_t* dst = sX + s * 16384;
-#pragma unroll 8
-      for (int i = 0; i < BM / 4; ++i) {
-        const int r = rb + 4 * i;
-        const int idx = sIdx[r];
-        const __nv_bfloat16* g = a.src + (idx >= 0 ? (long)idx * a.ld_src : 0L) + kb * 64 + jc * 8;
-        cp_async16_zfill(dst + r * 128 + ((jc ^ (r & 7)) << 4), g, idx >= 0 ? 16 : 0);
-      }
-      cp_async_commit();
-      if (kb == DK - 1) {
-        // a tile's k-blocks are all handed over before the next tile's are issued: its slots are
-        // released only after this tile's last S-MMA, which needs every k-block of this tile
-        cp_async_wait<0>();
-        while (done <= k) finish(done++);
-      } else if (k - done >= LAG) {
-        cp_async_wait<LAG>();
-        finish(done++);
-      }
-    }
-    cp_async_wait<0>();
-    while (done < total) finish(done++);
     if (lane == 0) bulk_wait<0>();
   }
 #ifdef SMES_TRACE
@@ -1912,11 +1917,11 @@ static int mlp_fwd_impl(const void* X, long ldx, long rows_cap, const int* gathe
   cudaError_t e;
 #define SMES_FWD_CASE(DK)                                                                              \
   case DK: {                                                                                           \
-    auto k = pack ? mlp::mlp_fwd_kernel<DK, mlp::kThreadsPack> : mlp::mlp_fwd_kernel<DK, mlp::kThreads>; \
+    auto k = pack ? mlp::mlp_fwd_kernel<DK, true> : mlp::mlp_fwd_kernel<DK, false>;                  \
     const int sm = mlp::FwdSmem<DK>::kBytes;                                                           \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);                      \
     if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "mlp_fwd smem attribute: %s", cudaGetErrorString(e)); \
-    smes_launch(k, sm_count(), pack ? mlp::kThreadsPack : mlp::kThreads, sm, st, tx, tw, tg, th, args);          \
+    smes_launch(k, sm_count(), mlp::kThreads, sm, st, tx, tw, tg, th, args);                                    \
     break;                                                                                             \
   }
   switch (d / 64) {

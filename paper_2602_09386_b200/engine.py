@@ -224,8 +224,8 @@ class SMESEngine:
         self.gather_x = os.environ.get("SMES_GATHER_X", "0") == "1"
         # SMES_FWD_PACK=1: mlp_fwd's own gather warp copies the X rows from h (LDGSTS) and writes the
         # packed X the weight gradient reads, so the plan scatter only places rows.  Bit-identical;
-        # measured slower at c2 (one gather warp: mlp_fwd 125 -> 192 us against the scatter's
-        # 37 -> 15 us, step 0.525 -> 0.562 ms, tools/ab_pack.sh), so off by default
+        # measured slower at c2 (mlp_fwd 125 -> 187 us against the scatter's 37 -> 15 us, step
+        # 0.5225 -> 0.557 ms, tools/ab_pack.sh), so off by default
         self.fwd_pack = os.environ.get("SMES_FWD_PACK", "0") == "1"
         self._x_gathered = False
         self._x_packed_by_fwd = False
