@@ -348,6 +348,15 @@ int smes_combine_fwd_f32(int T, int B, int E, int K, int d_out, int umax, const 
                          const int32_t* row_of, const int32_t* active, const float* wsel, const float* O, long ldo,
                          const float* head_w, const float* head_b, float* reps, float* logits, float* preds,
                          const float* labels, const float* lam, double* loss_part, int grid, void* stream);
+/* the same with the loss finalize (smes_loss_finalize) done by the last CTA to finish: loss_out =
+ * [task, L_lb, task + beta L_lb] (training.py:60-94); ticket: one int32, zero before the first
+ * launch (the kernel resets it). */
+int smes_combine_fwd_f32_loss(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask,
+                              const int32_t* usize, const int32_t* row_of, const int32_t* active, const float* wsel,
+                              const float* O, long ldo, const float* head_w, const float* head_b, float* reps,
+                              float* logits, float* preds, const float* labels, const float* lam, double* loss_part,
+                              int grid, int32_t* ticket, double inv_b, double beta, const double* stats_value,
+                              double* loss_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -89,6 +89,7 @@ SIGNATURES = {
     "smes_split_bf16x3": [L, I, P, L, P, L, P, P],
     "smes_combine_fwd_f32_grid": [I],
     "smes_combine_fwd_f32": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, P, P, P, P, P, I, P],
+    "smes_combine_fwd_f32_loss": [I, I, I, I, I, I, P, P, P, P, P, P, L, P, P, P, P, P, P, P, P, I, P, D, D, P, P, P],
 }
 _RESTYPE = {"smes_last_error": C.c_char_p, "smes_gemm_ragged_k_split_work": C.c_long}
 # entry points that return a value rather than a status
@@ -122,7 +123,7 @@ KERNELS_PER_CALL = {"smes_route_batch": 1, "smes_route_front": 1, "smes_peer_all
                     "smes_ep_copy_rows": 1, "smes_ep_combine_dh": 1, "smes_ep_capacity_guard": 1,
                     "smes_ep_put_slots": 1, "smes_ep_signal_wait": 2, "smes_ep_pack_put": 2,
                     "smes_ep_copy_rows_put": 1, "smes_gemm_ragged_m_x3": 1, "smes_split_bf16x3": 1,
-                    "smes_combine_fwd_f32": 1, "smes_route_rt": 1,
+                    "smes_combine_fwd_f32": 1, "smes_combine_fwd_f32_loss": 1, "smes_route_rt": 1,
                     "smes_plan_reduce_stats_fold": 1,
                     "smes_gemm_ragged_k_split": lambda *a: 1 if a[11] <= 1 else 2}
 launch_count = 0

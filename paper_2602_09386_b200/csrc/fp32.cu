@@ -53,6 +53,14 @@ __device__ __forceinline__ int union_rank_f32(const uint32_t* um, int e) {
   return r + __popc(um[e >> 5] & ((1u << (e & 31)) - 1u));
 }
 
+// optional loss finalize by the last CTA (smes_combine_fwd_f32_loss)
+struct LossTail {
+  int* ticket;                   // zero before the launch; the last CTA resets it
+  double inv_b, beta;
+  const double* stats_value;     // L_lb (LoadStats value) or null
+  double* loss_out;              // [task, lb, total]
+};
+
 // One instance per CTA iteration (grid-stride).  Thread = columns col, col + 128, ...; the union's
 // packed rows are read from L2 once per task (d_out * U * 4 bytes, L1-resident across tasks).
 __global__ void __launch_bounds__(CF_THREADS)
@@ -62,7 +70,7 @@ __global__ void __launch_bounds__(CF_THREADS)
                            const float* __restrict__ O, long ldo, const float* __restrict__ head_w,
                            const float* __restrict__ head_b, float* __restrict__ reps, float* __restrict__ logits,
                            float* __restrict__ preds, const float* __restrict__ labels, const float* __restrict__ lam,
-                           double* __restrict__ loss_part) {
+                           double* __restrict__ loss_part, const LossTail tail) {
   pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   const int EW = (E + 31) >> 5;
@@ -128,6 +136,32 @@ __global__ void __launch_bounds__(CF_THREADS)
       for (int i = 0; i < CF_THREADS; ++i) s += s_loss[i];
       loss_part[blockIdx.x] = s;
     }
+    if (tail.ticket != nullptr) {
+      // loss finalize in the last CTA to finish (training.py:60-94): the partials in a fixed order
+      __shared__ int s_last;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(tail.ticket, 1) == (int)gridDim.x - 1;
+      }
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        double v = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += CF_THREADS) v += __ldcg(loss_part + i);
+        s_loss[threadIdx.x] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          double t = 0.0;
+          for (int i = 0; i < CF_THREADS; ++i) t += s_loss[i];
+          const double task = t * tail.inv_b;
+          const double lb = tail.stats_value ? *tail.stats_value : 0.0;
+          tail.loss_out[0] = task;
+          tail.loss_out[1] = lb;
+          tail.loss_out[2] = task + tail.beta * lb;
+          *tail.ticket = 0;                          // ready for the next launch (graph replays)
+        }
+      }
+    }
   }
 }
 
@@ -155,10 +189,11 @@ int smes_split_bf16x3(long rows, int cols, const float* src, long lds, void* dst
 
 int smes_combine_fwd_f32_grid(int B) { return B < 148 * 8 ? B : 148 * 8; }
 
-int smes_combine_fwd_f32(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
-                         const int32_t* row_of, const int32_t* active, const float* wsel, const float* O, long ldo,
-                         const float* head_w, const float* head_b, float* reps, float* logits, float* preds,
-                         const float* labels, const float* lam, double* loss_part, int grid, void* stream) {
+static int combine_f32_impl(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask,
+                            const int32_t* usize, const int32_t* row_of, const int32_t* active, const float* wsel,
+                            const float* O, long ldo, const float* head_w, const float* head_b, float* reps,
+                            float* logits, float* preds, const float* labels, const float* lam, double* loss_part,
+                            int grid, const LossTail& tail, void* stream) {
   if (T < 1 || B < 1 || E < 1 || K < 1 || d_out < 1 || umax < 1)
     return set_error(SMES_ERR_SHAPE, "combine_fwd_f32: empty shape");
   if (!O || !reps || !logits || !preds) return set_error(SMES_ERR_STATE, "combine_fwd_f32: missing buffer");
@@ -174,10 +209,32 @@ int smes_combine_fwd_f32(int T, int B, int E, int K, int d_out, int umax, const 
   }
   smes_launch(combine_fwd_f32_kernel, grid, CF_THREADS, smem, reinterpret_cast<cudaStream_t>(stream), 
       T, B, E, K, d_out, umax, umask, usize, row_of, active, wsel, O, ldo, head_w, head_b, reps, logits, preds, labels,
-      lam, loss_part);
+      lam, loss_part, tail);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "combine_fwd_f32 launch: %s", cudaGetErrorString(e));
   return SMES_OK;
+}
+
+int smes_combine_fwd_f32(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
+                         const int32_t* row_of, const int32_t* active, const float* wsel, const float* O, long ldo,
+                         const float* head_w, const float* head_b, float* reps, float* logits, float* preds,
+                         const float* labels, const float* lam, double* loss_part, int grid, void* stream) {
+  return combine_f32_impl(T, B, E, K, d_out, umax, umask, usize, row_of, active, wsel, O, ldo, head_w, head_b, reps,
+                          logits, preds, labels, lam, loss_part, grid, LossTail{nullptr, 0.0, 0.0, nullptr, nullptr},
+                          stream);
+}
+
+int smes_combine_fwd_f32_loss(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask,
+                              const int32_t* usize, const int32_t* row_of, const int32_t* active, const float* wsel,
+                              const float* O, long ldo, const float* head_w, const float* head_b, float* reps,
+                              float* logits, float* preds, const float* labels, const float* lam, double* loss_part,
+                              int grid, int32_t* ticket, double inv_b, double beta, const double* stats_value,
+                              double* loss_out, void* stream) {
+  if (labels == nullptr || loss_part == nullptr || ticket == nullptr || loss_out == nullptr)
+    return set_error(SMES_ERR_STATE, "combine_fwd_f32_loss: labels, partials, ticket and loss_out are required");
+  return combine_f32_impl(T, B, E, K, d_out, umax, umask, usize, row_of, active, wsel, O, ldo, head_w, head_b, reps,
+                          logits, preds, labels, lam, loss_part, grid,
+                          LossTail{ticket, inv_b, beta, stats_value, loss_out}, stream);
 }
 
 }  // extern "C"

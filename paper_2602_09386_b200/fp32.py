@@ -108,6 +108,7 @@ class SMESForwardF32:
         self.labels = z(T, B)
         self.loss_part = z(self.grid, dt=f64)
         self.loss_out = z(3, dt=f64)
+        self.ticket_loss = z(1, dt=i32)      # last-CTA ticket of the fused loss finalize
         self.stats_out = z(3 * E + 1, dt=f64)
         self.freq32 = z(E)
         self.seg_router = torch.tensor([0, self.B_pad], dtype=i32, device=dev)
@@ -192,14 +193,19 @@ class SMESForwardF32:
             if i < len(self.p.layers) - 1:
                 self._split(f"split_fc{i + 1}", self.outs[i], R, n, self.outs3[i], rows_dev=padded_rows, s=s)
                 inp, ld = self.outs3[i], 3 * n
-        _tagged("combine_fwd_f32", "smes_combine_fwd_f32", T, B, E, K, self.d_out, self.umax, ptr(self.umask),
-                ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
-                self.d_out, ptr(self.head_w), ptr(self.head_b), ptr(self.reps), ptr(self.logits),
-                ptr(self.preds), ptr(self.labels) if with_loss else None, ptr(self.lam),
-                ptr(self.loss_part) if with_loss else None, self.grid, s)
         if with_loss:
-            _tagged("loss_finalize", "smes_loss_finalize", self.grid, ptr(self.loss_part), 1.0 / B, self.beta,
-                    self.stats_out[3 * E:].data_ptr(), ptr(self.loss_out), s)
+            # combine + heads + BCE, the loss finalize in the last CTA (one launch fewer)
+            _tagged("combine_fwd_f32", "smes_combine_fwd_f32_loss", T, B, E, K, self.d_out, self.umax,
+                    ptr(self.umask), ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel),
+                    ptr(self.outs[-1]), self.d_out, ptr(self.head_w), ptr(self.head_b), ptr(self.reps),
+                    ptr(self.logits), ptr(self.preds), ptr(self.labels), ptr(self.lam), ptr(self.loss_part),
+                    self.grid, ptr(self.ticket_loss), 1.0 / B, self.beta, self.stats_out[3 * E:].data_ptr(),
+                    ptr(self.loss_out), s)
+        else:
+            _tagged("combine_fwd_f32", "smes_combine_fwd_f32", T, B, E, K, self.d_out, self.umax, ptr(self.umask),
+                    ptr(self.usize), ptr(self.row_of), ptr(self.active), ptr(self.wsel), ptr(self.outs[-1]),
+                    self.d_out, ptr(self.head_w), ptr(self.head_b), ptr(self.reps), ptr(self.logits),
+                    ptr(self.preds), None, ptr(self.lam), None, self.grid, s)
 
     def check_finite(self):
         """Raise NumericsError if the router saw a non-finite logit (read after a forward)."""
