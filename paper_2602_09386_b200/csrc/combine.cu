@@ -151,6 +151,41 @@ struct GroupLayout {
   }
 };
 
+// Scoring without task reps (P only, no labels): a warp per instance, TPL = 32 / next_pow2(T) lanes
+// per task, each lane summing w * P[row(e), t] over its share of the task's K active experts in k
+// order, then a fixed xor tree over the task's lanes (model.py:202-208 on the folded heads).  No
+// shared memory, no block barriers: the per-instance gathers are the whole cost.
+template <int TPL>
+__global__ void __launch_bounds__(256) combine_score_kernel(const CombineArgs a) {
+  pdl_wait();
+  const int lane = threadIdx.x & 31;
+  const int t = lane / TPL, sub = lane % TPL;
+  const int EW = (a.E + 31) >> 5, K = a.K;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  for (int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); b < a.B; b += nw) {
+    float acc = 0.f;
+    if (t < a.T) {
+      const uint32_t* um = a.umask + (long)b * EW;
+      const long o0 = ((long)t * a.B + b) * K;
+      for (int k = sub; k < K; k += TPL) {
+        const int e = __ldg(a.active + o0 + k);
+        const float w = __ldg(a.wsel + o0 + k);
+        const int row = __ldg(a.row_of + (long)b * a.umax + union_rank(um, e));
+        acc = fmaf(w, __ldg(a.P + (long)row * a.ldp + t), acc);
+      }
+    }
+#pragma unroll
+    for (int o = TPL / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (sub == 0 && t < a.T) {
+      const float lg = acc + a.head_b[t];
+      const float ez = expf(-fabsf(lg));               // stable sigmoid (linalg.py:108-113)
+      const float pos = 1.f / (1.f + ez);
+      a.logits[(long)t * a.B + b] = lg;
+      a.preds[(long)t * a.B + b] = lg >= 0.f ? pos : 1.f - pos;
+    }
+  }
+}
+
 template <int VPL, int MAXT>
 __global__ void __launch_bounds__(CB_THREADS) combine_fwd_kernel(const CombineArgs a) {
   pdl_wait();
@@ -780,6 +815,15 @@ int smes_combine_grid(int B, int T, int d_out) {
   return need < g ? need : g;
 }
 
+// SMES_SCORE_KERNEL=0 keeps scoring on the staged combine kernel (A/B)
+static bool score_kernel_enabled() {
+  static const int on = [] {
+    const char* v = std::getenv("SMES_SCORE_KERNEL");
+    return (v == nullptr || v[0] != '0') ? 1 : 0;
+  }();
+  return on != 0;
+}
+
 int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint32_t* umask, const int32_t* usize,
                      const int32_t* row_of, const int32_t* active, const float* wsel, const void* O, long ldo,
                      const float* head_w, const float* head_b, const float* P, long ldp, void* reps, float* logits, float* preds,
@@ -793,6 +837,25 @@ int smes_combine_fwd(int T, int B, int E, int K, int d_out, int umax, const uint
   a.lam = lam; a.loss_part = loss_part;
   if (!reps && O) return set_error(SMES_ERR_STATE, "combine_fwd: reps buffer is required with O");
   if (!O && !P) return set_error(SMES_ERR_STATE, "combine_fwd: scoring without O needs the head projections P");
+  if (!O && !labels && !loss_part && T <= 32 && score_kernel_enabled()) {
+    // scoring: warp per instance (combine_score_kernel)
+    const int tp = T <= 1 ? 1 : T <= 2 ? 2 : T <= 4 ? 4 : T <= 8 ? 8 : T <= 16 ? 16 : 32;
+    const int warps = 8;
+    long want = ((long)B + warps - 1) / warps;
+    const int g = (int)(want < 148L * 8 ? want : 148L * 8);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    switch (32 / tp) {
+      case 32: smes_launch(combine_score_kernel<32>, g, warps * 32, 0, st, a); break;
+      case 16: smes_launch(combine_score_kernel<16>, g, warps * 32, 0, st, a); break;
+      case 8: smes_launch(combine_score_kernel<8>, g, warps * 32, 0, st, a); break;
+      case 4: smes_launch(combine_score_kernel<4>, g, warps * 32, 0, st, a); break;
+      case 2: smes_launch(combine_score_kernel<2>, g, warps * 32, 0, st, a); break;
+      default: smes_launch(combine_score_kernel<1>, g, warps * 32, 0, st, a); break;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(SMES_ERR_CUDA, "combine_score launch: %s", cudaGetErrorString(e));
+    return SMES_OK;
+  }
   return combine_launch(false, a, grid, stream);
 }
 
